@@ -1,0 +1,196 @@
+/*
+ * nbzg.h -- C ABI of the B200 (sm_100a) nbz compression path.
+ *
+ * Drop-in boundary for the reference package `nbz` (pure Python + numba,
+ * /root/reference/pkg/src/nbz).  The reference's operator table is the flat
+ * module `nbz._kernels`; its whole-path entry points are
+ * `pipeline.compress` / `pipeline.decompress`.  Each function below cites
+ * the reference interface it replaces.  INTEGRATION.md shows the ctypes
+ * binding a maintainer adds on the reference side.
+ *
+ * Conventions (mirroring _kernels.py's calling convention):
+ *   - every pointer argument is a DEVICE pointer unless named h_*;
+ *   - the caller owns and pre-allocates every buffer (workspace sizes come
+ *     from the *_workspace_size queries);
+ *   - `stream` is a cudaStream_t passed as void*; every call is async on it
+ *     and keeps no mutable global state (reentrant across streams);
+ *   - the return value is a status (NBZG_OK = 0); device-side failures
+ *     (bound too small, invalid code, ...) are reported through the
+ *     `status` word of the nbzg_meta block written by the call.
+ */
+#ifndef NBZG_H_
+#define NBZG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  NBZG_OK = 0,
+  NBZG_BOUND_TOO_SMALL = 1, /* quantize.py:123-126 -> BoundTooSmallError */
+  NBZG_CODE_TOO_LONG = 2,   /* encode.py:215-216 -> EncodeError */
+  NBZG_INVALID_CODE = 3,    /* _kernels.py:348-374 status 1 -> DecodeError */
+  NBZG_TRUNCATED = 4,       /* status 2 / pipeline.py:213-214 -> DecodeError */
+  NBZG_BAD_ARG = 5,         /* -> ValidationError */
+  NBZG_CUDA_ERROR = 6,
+  NBZG_UNSUPPORTED = 7,     /* parameter outside the GPU path's range */
+  NBZG_BAD_STREAM = 8       /* malformed table / counts -> DecodeError */
+};
+
+/* Per-field resolved parameters and produced sizes. */
+typedef struct nbzg_field_meta {
+  double bound;        /* resolved absolute bound b (model.py:112-125); 0 if constant */
+  double twob;         /* 2b   (_kernels.py:154) */
+  double inv;          /* 1/(2b) (_kernels.py:155) */
+  float inv32;         /* (float)inv, FP32 fast-path scale */
+  float constant;      /* value of a constant field (pipeline.py:174-178) */
+  float lo, hi;        /* exact f32 min / max (model.py:104-109) */
+  uint32_t is_const;
+  uint32_t k;          /* Huffman symbols in the table */
+  uint32_t min_len, max_len;
+  uint64_t n_esc;      /* escapes (code 0) */
+  uint64_t total_bits; /* Huffman bitstream length */
+  uint64_t payload_off;/* offset of this field's payload in the arena */
+  uint64_t payload_len;
+  uint64_t index_off;  /* payload-relative offset of u32 chunk_bits[] */
+  uint64_t bits_off;   /* payload-relative offset of the bitstream (4-aligned) */
+  uint64_t esc_off;    /* payload-relative offset of f32 escapes (4-aligned) */
+} nbzg_field_meta;
+
+typedef struct nbzg_meta {
+  nbzg_field_meta f[6];
+  uint32_t mask;       /* constant-field mask (bit f) */
+  uint32_t status;     /* first device-side failure (NBZG_*), 0 if none */
+  uint64_t arena_used; /* total payload bytes (sum of payload_len) */
+  uint64_t nseg;       /* R-index segments (sorted mode) */
+  uint64_t pad;
+} nbzg_meta;
+
+/* Whole-snapshot compress of Mode.SZ_LV (sorted=0) / Mode.SZ_LV_PRX (sorted=1).
+ * Replaces pipeline.compress (pipeline.py:447-526) for these two modes.
+ * Output: payloads of the v2 SZ_DQ streams laid out back to back in `arena`
+ * (field order, constant fields skipped), `meta` (device), seg_bits[nseg]
+ * (u8, sorted mode) and perm[n] (u16 tile-local source index of every sorted
+ * position; the CompressResult.order sidecar, pipeline.py:146-149). */
+typedef struct nbzg_compress_args {
+  const float *fields[6]; /* device, n floats each */
+  int64_t n;
+  int32_t sorted;
+  int32_t bound_kind[6];  /* 0 = absolute, 1 = value-range relative (model.py:79-101) */
+  double bound_value[6];
+  int64_t interval_count; /* Settings.interval_count (pipeline.py:79) */
+  int64_t segment_size;   /* Settings.segment_size */
+  int32_t ignored_groups; /* Settings.ignored_groups */
+  int32_t pad0;
+  void *workspace;        /* nbzg_compress_workspace_size() bytes */
+  size_t workspace_bytes;
+  uint8_t *arena;         /* nbzg_compress_arena_bound() bytes */
+  size_t arena_bytes;
+  nbzg_meta *meta;        /* device */
+  uint8_t *seg_bits;      /* device, ceil(n/segment_size) bytes (sorted) */
+  uint16_t *perm;         /* device, n entries (sorted) */
+} nbzg_compress_args;
+
+size_t nbzg_compress_workspace_size(int64_t n, int32_t sorted, int64_t interval_count,
+                                    int64_t segment_size);
+size_t nbzg_compress_arena_bound(int64_t n, int64_t interval_count);
+int nbzg_compress(const nbzg_compress_args *args, void *stream);
+
+/* Decompress up to six field payloads (sorted order output, n floats each).
+ * Replaces pipeline._parse_sz_stream (pipeline.py:203-223) ->
+ * encode.huffman_decode (encode.py:242-261) -> K.huff_decode
+ * (_kernels.py:348-374) -> quantize.dequantize_field -> K.sz_dequantize
+ * (_kernels.py:126-147).  kind 3 = SZ_DQ (v2, chunk-parallel); kind 0 =
+ * SZ_FIELD (v1 reference streams, exact sequential chain, compat path).
+ * payload: device bytes, any alignment, readable for payload_len + 16 bytes.
+ * status: device u32, receives the first failure (NBZG_*). */
+typedef struct nbzg_decompress_args {
+  const uint8_t *payload[6];
+  int64_t payload_len[6];
+  int32_t kind[6];
+  double bound[6];        /* resolved bound of the field (archive header) */
+  float *out[6];
+  int32_t nfields;
+  int32_t pad0;
+  int64_t n;
+  int64_t interval_count;
+  void *workspace;        /* nbzg_decompress_workspace_size() bytes */
+  size_t workspace_bytes;
+  uint32_t *status;
+} nbzg_decompress_args;
+
+size_t nbzg_decompress_workspace_size(int64_t n, int64_t interval_count, int32_t nfields);
+int nbzg_decompress(const nbzg_decompress_args *args, void *stream);
+
+/* ---- stage-level parity hooks (mirror nbz._kernels, same semantics) ---- */
+
+/* model.field_range x6 (model.py:104-109): out[2f] = min, out[2f+1] = max */
+int nbzg_minmax6(const float *const *h_fields, int64_t n, float *out12, void *stream);
+
+/* quantize.integerize (quantize.py:117-128): ints = rint(f64(x)/(2b)).
+ * *status_dev (u32) receives NBZG_BOUND_TOO_SMALL if max|x/(2b)| > 2^62. */
+int nbzg_integerize(const float *x, int64_t n, double bound, int64_t *ints,
+                    uint32_t *status_dev, void *stream);
+
+/* rindex.build_r_indices (rindex.py:164-198) + K.interleave3: full u64 keys
+ * and per-segment bits from three coordinate fields (bounds[3], 0 = constant
+ * coordinate -> zero column). */
+int nbzg_rindex_keys(const float *x, const float *y, const float *z, int64_t n,
+                     const double *h_bounds3, int64_t segment_size, uint64_t *keys,
+                     uint8_t *seg_bits, uint32_t *status_dev, void *stream);
+
+/* rindex.prx_sort (rindex.py:201-229) -> K.prx_order (_kernels.py:887-927):
+ * stable per-segment order by key >> 3*min(k, bits), returned as global int64
+ * source indices (`order`, the CompressResult sidecar). */
+int nbzg_prx_order(const uint64_t *keys, int64_t n, int64_t segment_size,
+                   const uint8_t *seg_bits, int32_t ignored_groups, int64_t *order,
+                   void *stream);
+
+/* Expand the tile-local u16 permutation written by nbzg_compress into global
+ * int64 source indices (the CompressResult.order sidecar). */
+int nbzg_order_expand(const uint16_t *perm, int64_t n, int64_t segment_size, int64_t *order,
+                      void *stream);
+
+/* K.huffman_lengths (_kernels.py:204-238): two-queue code lengths of k
+ * ascending counts (leaf wins ties); single symbol -> length 1.  workspace:
+ * 16*k bytes (used when k > 16384). */
+int nbzg_huffman_lengths(const uint32_t *sorted_counts, int64_t k, uint8_t *lengths,
+                         void *workspace, size_t workspace_bytes, uint32_t *status_dev,
+                         void *stream);
+
+/* encode.huffman_build (encode.py:199-219) + HuffmanTable._build_tables
+ * (encode.py:123-152) from a bincount histogram of nbins u32: ascending
+ * symbols (u32), their lengths (u8, by rank), and the encode LUT
+ * lut[sym] = (len << 57) | word.  meta_out->f[0] receives k, min/max length,
+ * total bits and n_esc (= hist[0]); meta_out->status CODE_TOO_LONG.
+ * workspace: 20*nbins bytes. */
+int nbzg_huffman_codebook(const uint32_t *hist, int64_t nbins, uint32_t *symbols,
+                          uint8_t *lengths, uint64_t *lut, nbzg_meta *meta_out,
+                          void *workspace, size_t workspace_bytes, void *stream);
+
+/* K.huff_encode (_kernels.py:304-345): MSB-first concatenation of the code
+ * words of u16 symbols into `out` (ceil(total_bits/32)*4 bytes, written as
+ * big-endian words, zero padded -- byte-identical to the reference's bytes
+ * for the first ceil(total_bits/8)).  chunk_bits[ceil(n/16384)] receives
+ * the per-16384-symbol bit counts (the v2 index).  workspace: 16 *
+ * ceil(n/16384) + 64 bytes. */
+int nbzg_huff_encode(const uint16_t *syms, int64_t n, const uint64_t *lut, uint8_t *out,
+                     uint32_t *chunk_bits, void *workspace, size_t workspace_bytes,
+                     void *stream);
+
+/* CRC-64/XZ (_kernels.py:954-994) of a device buffer; result to *crc_dev. */
+int nbzg_crc64(const uint8_t *data, int64_t n, uint64_t *crc_dev, void *workspace,
+               size_t workspace_bytes, void *stream);
+size_t nbzg_crc64_workspace_size(int64_t n);
+
+/* library / device info */
+const char *nbzg_version(void);
+int nbzg_device_sm_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NBZG_H_ */

@@ -1,0 +1,150 @@
+// bounds.cu -- K1: exact per-field min/max (model.py:104-109) and bound
+// resolution (model.py:112-125, pipeline.py:157-181) on device.
+//
+// One streaming pass over the six SoA fields with 128-bit loads; per-block
+// reduction, then one atomicMin/Max per block on an order-preserving u32
+// encoding of the floats.  HBM-bound: 24 B/particle read.
+#include "nbzg_internal.cuh"
+#include "plan.h"
+
+namespace nbzg {
+
+struct Fields6 {
+  const float* p[6];
+};
+
+__global__ void minmax_init_kernel(uint32_t* mm) {
+  int i = threadIdx.x;
+  if (i < 12) mm[i] = (i & 1) ? 0u : 0xffffffffu;
+}
+
+__global__ void __launch_bounds__(512) minmax6_kernel(Fields6 F, int64_t n, uint32_t* mm) {
+  float lo[6], hi[6];
+#pragma unroll
+  for (int f = 0; f < 6; f++) {
+    lo[f] = __int_as_float(0x7f800000);
+    hi[f] = -__int_as_float(0x7f800000);
+  }
+  const int64_t nv = n >> 2;  // float4 count
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+#pragma unroll
+    for (int f = 0; f < 6; f++) {
+      float4 v = __ldcs(reinterpret_cast<const float4*>(F.p[f]) + i);
+      lo[f] = fminf(lo[f], fminf(fminf(v.x, v.y), fminf(v.z, v.w)));
+      hi[f] = fmaxf(hi[f], fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+    }
+  }
+  // tail (n % 4)
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    int64_t i = (nv << 2) + threadIdx.x;
+#pragma unroll
+    for (int f = 0; f < 6; f++) {
+      float v = F.p[f][i];
+      lo[f] = fminf(lo[f], v);
+      hi[f] = fmaxf(hi[f], v);
+    }
+  }
+  __shared__ uint32_t s_lo[6], s_hi[6];
+  if (threadIdx.x < 6) {
+    s_lo[threadIdx.x] = 0xffffffffu;
+    s_hi[threadIdx.x] = 0u;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int f = 0; f < 6; f++) {
+    float a = lo[f], b = hi[f];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&s_lo[f], f2ord(a));
+      atomicMax(&s_hi[f], f2ord(b));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    atomicMin(&mm[2 * threadIdx.x], s_lo[threadIdx.x]);
+    atomicMax(&mm[2 * threadIdx.x + 1], s_hi[threadIdx.x]);
+  }
+}
+
+int launch_minmax6(const float* const* f, int64_t n, uint32_t* mm, cudaStream_t st) {
+  Fields6 F;
+  for (int i = 0; i < 6; i++) F.p[i] = f[i];
+  minmax_init_kernel<<<1, 32, 0, st>>>(mm);
+  if (n > 0) {
+    int64_t nv = (n >> 2);
+    int blocks = (int)((nv + 511) / 512);
+    int cap = sm_count() * 4;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    minmax6_kernel<<<blocks, 512, 0, st>>>(F, n, mm);
+  }
+  return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
+}
+
+// resolve_field_bounds (pipeline.py:157-181): constant fields (zero range)
+// take the fast path regardless of bound kind; others get
+// b = value (absolute) or b = value * (float(hi) - float(lo)) in f64.
+struct ResolveArgs {
+  const float* f[6];
+  int kind[6];
+  double value[6];
+  int64_t n;
+  int64_t nseg;
+};
+
+__global__ void resolve_kernel(ResolveArgs a, const uint32_t* mm, nbzg_meta* meta) {
+  if (threadIdx.x != 0) return;
+  uint32_t mask = 0;
+  for (int f = 0; f < 6; f++) {
+    nbzg_field_meta& m = meta->f[f];
+    float lo = ord2f(mm[2 * f]), hi = ord2f(mm[2 * f + 1]);
+    m.lo = lo;
+    m.hi = hi;
+    m.k = 0;
+    m.min_len = m.max_len = 0;
+    m.n_esc = m.total_bits = 0;
+    m.payload_off = m.payload_len = 0;
+    m.index_off = m.bits_off = m.esc_off = 0;
+    m.constant = 0.0f;
+    m.is_const = 0;
+    double b = 0.0;
+    if (a.n > 0) {
+      double rng = (double)hi - (double)lo;
+      if (rng == 0.0) {
+        mask |= 1u << f;
+        m.is_const = 1;
+        m.constant = a.f[f][0];
+      } else {
+        b = a.kind[f] == 0 ? a.value[f] : a.value[f] * rng;
+      }
+    }
+    m.bound = b;
+    m.twob = 2.0 * b;
+    m.inv = b > 0.0 ? 1.0 / (2.0 * b) : 0.0;
+    m.inv32 = (float)m.inv;
+  }
+  meta->mask = mask;
+  meta->status = 0;
+  meta->arena_used = 0;
+  meta->nseg = (uint64_t)a.nseg;
+}
+
+int launch_resolve(const Plan& p, cudaStream_t st) {
+  ResolveArgs a;
+  for (int f = 0; f < 6; f++) {
+    a.f[f] = p.f[f];
+    a.kind[f] = p.bound_kind[f];
+    a.value[f] = p.bound_value[f];
+  }
+  a.n = p.n;
+  a.nseg = p.nseg;
+  resolve_kernel<<<1, 32, 0, st>>>(a, p.minmax, p.meta);
+  return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
+}
+
+}  // namespace nbzg

@@ -1,0 +1,293 @@
+// capi.cu -- the extern "C" boundary (include/nbzg.h): argument validation,
+// workspace carving and kernel sequencing.  No mutable global state beyond
+// one-time cudaFuncSetAttribute calls.
+#include <cstring>
+
+#include "nbzg_internal.cuh"
+#include "plan.h"
+
+namespace nbzg {
+
+int launch_rindex_keys(const float* x, const float* y, const float* z, int64_t n,
+                       const double* bounds3, int64_t S, uint64_t* keys, uint8_t* seg_bits,
+                       uint32_t* status, cudaStream_t st);
+int launch_prx_order(const uint64_t* keys, int64_t n, int64_t S, const uint8_t* seg_bits, int ig,
+                     int64_t* order, cudaStream_t st);
+int launch_order_expand(const uint16_t* perm, int64_t n, int64_t tile, int64_t* order,
+                        cudaStream_t st);
+int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uint8_t* len,
+                         uint64_t* lut, uint32_t* scratch, nbzg_meta* meta, int64_t n,
+                         int64_t nchunks, int single_field, cudaStream_t st);
+int launch_huffman_lengths(const uint32_t* counts, int64_t k, uint8_t* lengths, uint32_t* scr,
+                           uint32_t* status, cudaStream_t st);
+int launch_huff_encode_raw(const uint16_t* syms, int64_t n, const uint64_t* lut, uint8_t* out,
+                           uint32_t* chunk_bits, uint64_t* lb, uint32_t* tickets,
+                           cudaStream_t st);
+size_t crc_ws(int64_t n);
+int launch_crc64(const uint8_t* data, int64_t n, uint64_t* crc_out, void* ws, size_t ws_bytes,
+                 cudaStream_t st);
+
+size_t decompress_ws(int nf, int64_t n, int64_t nbins);
+
+int sm_count() {
+  static int c = 0;
+  if (!c) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    if (c <= 0) c = 148;
+  }
+  return c;
+}
+
+static inline size_t al256(size_t v) { return (v + 255) & ~size_t(255); }
+
+void plan_shape(Plan& p, int64_t n, int sorted, int64_t ic, int64_t S) {
+  p.n = n;
+  p.sorted = sorted;
+  p.S = S;
+  if (sorted) {
+    int64_t spt = S >= kTileMax ? 1 : kTileMax / S;
+    p.tile = spt * S;
+  } else {
+    p.tile = kTileMax;
+  }
+  p.ntiles = (n + p.tile - 1) / p.tile;
+  p.nseg = sorted ? (n + S - 1) / S : 0;
+  p.nchunks = (n + kChunk - 1) / kChunk;
+  p.nbins = ic;
+  p.half = (int)(ic / 2);
+}
+
+size_t plan_workspace(Plan& p, void* base) {
+  uint8_t* b = reinterpret_cast<uint8_t*>(base);
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> uint8_t* {
+    uint8_t* r = b ? b + off : nullptr;
+    off += al256(bytes);
+    return r;
+  };
+  const int64_t cs = (p.n + 7) & ~int64_t(7);
+  p.minmax = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 12));
+  p.codes = reinterpret_cast<uint16_t*>(take(sizeof(uint16_t) * 6 * cs));
+  p.hist = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 6 * p.nbins));
+  p.cb_sym = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 6 * p.nbins));
+  p.cb_len = reinterpret_cast<uint8_t*>(take(6 * p.nbins));
+  p.lut = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 6 * p.nbins));
+  p.cb_scratch = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 6 * 5 * p.nbins));
+  p.lb = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 12 * (p.nchunks + 1)));
+  p.counters = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 64));
+  p.tile_flags = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * (p.ntiles + 1)));
+  return off;
+}
+
+size_t decompress_ws(int nf, int64_t n, int64_t nbins);  // decode.cu
+
+}  // namespace nbzg
+
+using namespace nbzg;
+
+namespace nbzg {
+int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_count, void* ws,
+                      size_t ws_bytes, uint32_t* status, cudaStream_t st);
+__global__ void ord_decode_kernel(uint32_t* m) {
+  int i = threadIdx.x;
+  if (i < 12) m[i] = __float_as_uint(ord2f(m[i]));
+}
+}  // namespace nbzg
+
+static int cuda_status() { return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR; }
+
+extern "C" {
+
+const char* nbzg_version(void) { return "nbzg 0.1.0 sm_100a"; }
+
+int nbzg_device_sm_count(void) { return sm_count(); }
+
+size_t nbzg_compress_workspace_size(int64_t n, int32_t sorted, int64_t interval_count,
+                                    int64_t segment_size) {
+  Plan p;
+  plan_shape(p, n, sorted, interval_count, segment_size < 1 ? 1 : segment_size);
+  return plan_workspace(p, nullptr);
+}
+
+size_t nbzg_compress_arena_bound(int64_t n, int64_t interval_count) {
+  int lg = 1;
+  while ((int64_t(1) << lg) < interval_count) lg++;
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
+  const int64_t k = interval_count < n ? interval_count : n;
+  // Huffman average length < log2(k) + 1, so bits < n * (lg + 1); escapes <= n
+  size_t per = 8 + 5 * (size_t)k + 8 + 4 * (size_t)nchunks + 4 +
+               4 * (((size_t)n * (lg + 1) + 31) / 32) + 4 * (size_t)n + 16;
+  return 6 * per + 256;
+}
+
+int nbzg_compress(const nbzg_compress_args* a, void* stream) {
+  if (!a) return NBZG_BAD_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (a->n < 0 || a->n >= (int64_t(1) << 32) - 1) return NBZG_UNSUPPORTED;
+  if (a->interval_count < 2 || (a->interval_count & 1) || a->interval_count > 65536)
+    return NBZG_UNSUPPORTED;
+  if (a->segment_size < 1 || a->ignored_groups < 0) return NBZG_BAD_ARG;
+  if (a->sorted && a->segment_size > kTileMax) return NBZG_UNSUPPORTED;
+  for (int f = 0; f < 6; f++) {
+    if (a->n > 0 && (!a->fields[f] || (reinterpret_cast<uintptr_t>(a->fields[f]) & 15)))
+      return NBZG_BAD_ARG;
+    if (a->bound_kind[f] != 0 && a->bound_kind[f] != 1) return NBZG_BAD_ARG;
+    if (!(a->bound_value[f] > 0)) return NBZG_BAD_ARG;
+  }
+  Plan p;
+  plan_shape(p, a->n, a->sorted, a->interval_count, a->segment_size);
+  p.ig = a->ignored_groups;
+  for (int f = 0; f < 6; f++) {
+    p.f[f] = a->fields[f];
+    p.bound_kind[f] = a->bound_kind[f];
+    p.bound_value[f] = a->bound_value[f];
+  }
+  if (a->workspace_bytes < plan_workspace(p, nullptr)) return NBZG_BAD_ARG;
+  if (a->arena_bytes < nbzg_compress_arena_bound(a->n, a->interval_count)) return NBZG_BAD_ARG;
+  if (!a->meta || (a->sorted && a->n > 0 && (!a->perm || !a->seg_bits))) return NBZG_BAD_ARG;
+  plan_workspace(p, a->workspace);
+  p.meta = a->meta;
+  p.perm = a->perm;
+  p.seg_bits = a->seg_bits;
+  p.arena = a->arena;
+  p.arena_bytes = a->arena_bytes;
+  int rc;
+  if ((rc = launch_minmax6(p.f, p.n, p.minmax, st))) return rc;
+  if ((rc = launch_resolve(p, st))) return rc;
+  if (p.n == 0) return cuda_status();
+  if (p.sorted && (rc = launch_rindex_sort(p, st))) return rc;
+  if ((rc = launch_quantize(p, st))) return rc;
+  if ((rc = launch_codebook(p, st))) return rc;
+  if ((rc = launch_layout(p, st))) return rc;
+  if ((rc = launch_encode(p, st))) return rc;
+  return cuda_status();
+}
+
+size_t nbzg_decompress_workspace_size(int64_t n, int64_t interval_count, int32_t nfields) {
+  return decompress_ws(nfields, n, interval_count + 1);
+}
+
+int nbzg_decompress(const nbzg_decompress_args* a, void* stream) {
+  if (!a || a->nfields < 0 || a->nfields > 6 || a->n < 0) return NBZG_BAD_ARG;
+  if (a->nfields == 0 || a->n == 0) return NBZG_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  DField f[6];
+  for (int i = 0; i < a->nfields; i++) {
+    if (a->kind[i] != 0 && a->kind[i] != 3) return NBZG_BAD_ARG;
+    if (!(a->bound[i] > 0)) return NBZG_BAD_ARG;
+    f[i].payload = a->payload[i];
+    f[i].payload_len = a->payload_len[i];
+    f[i].kind = a->kind[i];
+    f[i].bound = a->bound[i];
+    f[i].twob = 2.0 * a->bound[i];
+    f[i].inv = 1.0 / f[i].twob;
+    f[i].inv32 = (float)f[i].inv;
+    f[i].out = a->out[i];
+  }
+  cudaMemsetAsync(a->status, 0, sizeof(uint32_t), st);
+  return launch_decompress(f, a->nfields, a->n, a->interval_count,
+                           a->workspace, a->workspace_bytes, a->status, st);
+}
+
+int nbzg_minmax6(const float* const* h_fields, int64_t n, float* out12, void* stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  for (int f = 0; f < 6; f++)
+    if (n > 0 && (reinterpret_cast<uintptr_t>(h_fields[f]) & 15)) return NBZG_BAD_ARG;
+  uint32_t* mm = reinterpret_cast<uint32_t*>(out12);
+  int rc = launch_minmax6(h_fields, n, mm, st);
+  if (rc) return rc;
+  ord_decode_kernel<<<1, 32, 0, st>>>(mm);  // decode the order-preserving encoding
+  return cuda_status();
+}
+
+}  // extern "C"
+
+namespace nbzg {
+__global__ void integerize_kernel(const float* x, int64_t n, double twob, double inv, float inv32,
+                                  int64_t* out, uint32_t* status) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool fast;
+  double k = lattice_index<true>(x[i], inv32, inv, twob, fast);
+  if (!fast && fabs(__ddiv_rn((double)x[i], twob)) > kIntLimit)
+    atomicCAS(status, 0u, (uint32_t)NBZG_BOUND_TOO_SMALL);
+  out[i] = (int64_t)k;
+}
+}  // namespace nbzg
+
+extern "C" {
+
+int nbzg_integerize(const float* x, int64_t n, double bound, int64_t* ints, uint32_t* status_dev,
+                    void* stream) {
+  if (!(bound > 0)) return NBZG_BAD_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  double twob = 2.0 * bound, inv = 1.0 / twob;
+  if (n > 0)
+    integerize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, n, twob, inv, (float)inv,
+                                                                   ints, status_dev);
+  return cuda_status();
+}
+
+int nbzg_rindex_keys(const float* x, const float* y, const float* z, int64_t n,
+                     const double* h_bounds3, int64_t segment_size, uint64_t* keys,
+                     uint8_t* seg_bits, uint32_t* status_dev, void* stream) {
+  if (segment_size < 1) return NBZG_BAD_ARG;
+  return launch_rindex_keys(x, y, z, n, h_bounds3, segment_size, keys, seg_bits, status_dev,
+                            reinterpret_cast<cudaStream_t>(stream));
+}
+
+int nbzg_prx_order(const uint64_t* keys, int64_t n, int64_t segment_size, const uint8_t* seg_bits,
+                   int32_t ignored_groups, int64_t* order, void* stream) {
+  if (segment_size < 1 || ignored_groups < 0) return NBZG_BAD_ARG;
+  return launch_prx_order(keys, n, segment_size, seg_bits, ignored_groups, order,
+                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+int nbzg_order_expand(const uint16_t* perm, int64_t n, int64_t segment_size, int64_t* order,
+                      void* stream) {
+  if (segment_size < 1) return NBZG_BAD_ARG;
+  Plan p;
+  plan_shape(p, n, 1, 65536, segment_size);
+  return launch_order_expand(perm, n, p.tile, order, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int nbzg_huffman_lengths(const uint32_t* sorted_counts, int64_t k, uint8_t* lengths,
+                         void* workspace, size_t workspace_bytes, uint32_t* status_dev,
+                         void* stream) {
+  if (k > 16384 && workspace_bytes < 16 * (size_t)k) return NBZG_BAD_ARG;
+  return launch_huffman_lengths(sorted_counts, k, lengths, reinterpret_cast<uint32_t*>(workspace),
+                                status_dev, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int nbzg_huffman_codebook(const uint32_t* hist, int64_t nbins, uint32_t* symbols, uint8_t* lengths,
+                          uint64_t* lut, nbzg_meta* meta_out, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+  if (nbins < 1 || nbins > 65536 || workspace_bytes < 20 * (size_t)nbins) return NBZG_BAD_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(meta_out, 0, sizeof(nbzg_meta), st);
+  return launch_codebook_impl(hist, nbins, symbols, lengths, lut,
+                              reinterpret_cast<uint32_t*>(workspace), meta_out, 1, 1, 0, st);
+}
+
+int nbzg_huff_encode(const uint16_t* syms, int64_t n, const uint64_t* lut, uint8_t* out,
+                     uint32_t* chunk_bits, void* workspace, size_t workspace_bytes, void* stream) {
+  int64_t nchunks = (n + kChunk - 1) / kChunk;
+  if (workspace_bytes < 16 * (size_t)nchunks + 64) return NBZG_BAD_ARG;
+  if (reinterpret_cast<uintptr_t>(out) & 3) return NBZG_BAD_ARG;
+  uint64_t* lb = reinterpret_cast<uint64_t*>(workspace);
+  uint32_t* tickets = reinterpret_cast<uint32_t*>(lb + 2 * nchunks);
+  return launch_huff_encode_raw(syms, n, lut, out, chunk_bits, lb, tickets,
+                                reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t nbzg_crc64_workspace_size(int64_t n) { return crc_ws(n); }
+
+int nbzg_crc64(const uint8_t* data, int64_t n, uint64_t* crc_dev, void* workspace,
+               size_t workspace_bytes, void* stream) {
+  return launch_crc64(data, n, crc_dev, workspace, workspace_bytes,
+                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

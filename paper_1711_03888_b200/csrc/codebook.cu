@@ -1,0 +1,338 @@
+// codebook.cu -- K4: on-device canonical Huffman codebook, bit-exact with
+// encode.huffman_build (encode.py:199-219) -> K.huffman_lengths
+// (_kernels.py:204-238) and HuffmanTable._build_tables (encode.py:123-152).
+//
+// One CTA per field:
+//   A. compact the non-zero bins of the code histogram (ascending symbol);
+//   B. order leaves by (count, symbol) -- identical to the reference's stable
+//      argsort by count -- with a bitonic sort of (count << 16 | rank) keys;
+//   C. the exact two-queue merge (leaf wins ties, _kernels.py:218,224) run by
+//      one thread over shared memory, parents stored in place;
+//   D. depths by parallel pointer jumping; lengths > 57 -> CODE_TOO_LONG;
+//   E. canonical code words in (length, symbol) order and the u64 encode LUT
+//      (len << 57) | word; payload sizes of the v2 stream.
+// Leaf arrays live in shared memory for k <= 16384 symbols and in global
+// scratch (L2-resident) above that.
+#include "nbzg_internal.cuh"
+#include "plan.h"
+
+namespace nbzg {
+
+constexpr int kCBThreads = 1024;
+constexpr int kCBSmemK = 16384;
+
+struct CBArgs {
+  const uint32_t* hist;
+  int64_t nbins;
+  uint32_t* sym;      // [6][nbins] ascending symbols
+  uint8_t* len;       // [6][nbins] lengths by rank
+  uint64_t* lut;      // [6][nbins] by symbol
+  uint32_t* scratch;  // [6][5*nbins]
+  nbzg_meta* meta;
+  int64_t n;
+  int64_t nchunks;
+  int single_field;   // >= 0: only this field (parity hook), meta->f[0] receives
+};
+
+NBZG_DEV void bitonic_sort_u64(uint64_t* a, int N) {
+  for (int size = 2; size <= N; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < N / 2; i += blockDim.x) {
+        int lo = 2 * i - (i & (stride - 1));
+        int hi = lo + stride;
+        bool asc = (lo & size) == 0;
+        uint64_t x = a[lo], y = a[hi];
+        if ((x > y) == asc) {
+          a[lo] = y;
+          a[hi] = x;
+        }
+      }
+      __syncthreads();
+    }
+}
+
+// Two-queue Huffman over ascending leaf weights L[0..k).  On return L[i]
+// holds the internal index of leaf i's parent and I[j] that of internal node
+// j's parent (root = k-2 holds 0xffffffff).  Exactly _kernels.py:213-232.
+NBZG_DEV void two_queue(uint32_t* L, uint32_t* I, int k) {
+  const uint32_t INF = 0xffffffffu;
+  int leaf = 0, node = 0;
+  uint32_t wl = L[0];
+  uint32_t wl_next = k > 1 ? L[1] : INF;
+  uint32_t wi = INF;
+  for (int nI = 0; nI < k - 1; nI++) {
+    uint32_t w2[2];
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+      if (wl <= wi) {  // leaf wins ties (weight[leaf] <= weight[node])
+        w2[r] = wl;
+        L[leaf] = (uint32_t)nI;
+        leaf++;
+        wl = wl_next;
+        wl_next = leaf + 1 < k ? L[leaf + 1] : INF;
+      } else {
+        w2[r] = wi;
+        I[node] = (uint32_t)nI;
+        node++;
+        wi = node < nI ? I[node] : INF;
+      }
+    }
+    uint32_t s = w2[0] + w2[1];
+    I[nI] = s;
+    if (node == nI) wi = s;
+  }
+  I[k - 2] = INF;
+}
+
+// Depth of every internal node (root = ni-1, parent index in I[j], parent >
+// child): level-synchronous passes until no node changes (<= 58 passes).
+NBZG_DEV void node_depths(const uint32_t* I, uint8_t* D, int ni) {
+  for (int j = threadIdx.x; j < ni; j += blockDim.x) D[j] = (j == ni - 1) ? 0 : 0xff;
+  __syncthreads();
+  while (true) {
+    int changed = 0;
+    for (int j = threadIdx.x; j < ni; j += blockDim.x) {
+      if (D[j] == 0xff) {
+        uint8_t dp = D[I[j]];
+        if (dp != 0xff) {
+          D[j] = (uint8_t)min(dp + 1, 254);
+          changed = 1;
+        }
+      }
+    }
+    if (!__syncthreads_or(changed)) break;
+  }
+}
+
+__global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t scan_u32[33];
+  __shared__ unsigned long long scan_u64[33];
+  __shared__ uint32_t s_cbl[64];
+  __shared__ uint64_t s_fc[64];
+  __shared__ uint32_t s_k, s_max, s_min;
+  const int field = a.single_field >= 0 ? a.single_field : (int)blockIdx.x;
+  const int mslot = a.single_field >= 0 ? 0 : field;
+  nbzg_field_meta& fm = a.meta->f[mslot];
+  if (a.single_field < 0 && (fm.is_const || a.n == 0)) return;
+  const uint32_t* hist = a.hist + (a.single_field >= 0 ? 0 : field * a.nbins);
+  uint32_t* sym = a.sym + field * a.nbins;
+  uint8_t* lenr = a.len + field * a.nbins;
+  uint64_t* lut = a.lut + field * a.nbins;
+  uint32_t* scr = a.scratch + field * 5 * a.nbins;
+  const int tid = threadIdx.x;
+  const int64_t nb = a.nbins;
+
+  // ---- A. compact non-zero bins, ascending symbol
+  const int R = (int)((nb + kCBThreads - 1) / kCBThreads);
+  uint32_t* cnt = scr;  // compact counts (global scratch, k entries)
+  uint32_t mine = 0;
+  for (int r = 0; r < R; r++) {
+    int64_t bin = (int64_t)tid * R + r;
+    if (bin < nb && hist[bin]) mine++;
+  }
+  uint32_t ktot;
+  uint32_t off = block_excl_scan<uint32_t>(mine, scan_u32, &ktot);
+  for (int r = 0; r < R; r++) {
+    int64_t bin = (int64_t)tid * R + r;
+    if (bin < nb) {
+      uint32_t c = hist[bin];
+      if (c) {
+        sym[off] = (uint32_t)bin;
+        cnt[off] = c;
+        off++;
+      }
+    }
+  }
+  const int k = (int)ktot;
+  if (tid == 0) {
+    fm.k = (uint32_t)k;
+    fm.n_esc = hist[0];
+  }
+  __syncthreads();
+  if (k == 0) return;
+
+  // memory for the merge: shared for k <= 16384, else global scratch.
+  // layout (N = pow2 >= k): keys u64[N] | L u32[N] | order u16[N]; after the
+  // split the keys region is reused for I u32[N] | D u8[N].
+  const bool small = k <= kCBSmemK;
+  uint8_t* base = small ? smem : reinterpret_cast<uint8_t*>(scr + a.nbins);  // after cnt
+  int N = 1;
+  while (N < k) N <<= 1;
+  uint64_t* keys = reinterpret_cast<uint64_t*>(base);
+  uint32_t* L = reinterpret_cast<uint32_t*>(base + 8 * (size_t)N);
+  uint16_t* order = reinterpret_cast<uint16_t*>(base + 12 * (size_t)N);
+  uint32_t* I = reinterpret_cast<uint32_t*>(base);
+  uint8_t* D = base + 4 * (size_t)N;
+
+  if (k == 1) {
+    if (tid == 0) lenr[0] = 1;  // _kernels.py:207-209
+  } else {
+    // ---- B. sort leaves by (count, rank)
+    for (int i = tid; i < N; i += kCBThreads)
+      keys[i] = i < k ? (((uint64_t)cnt[i] << 16) | (uint64_t)i) : ~0ull;
+    __syncthreads();
+    bitonic_sort_u64(keys, N);
+    for (int i = tid; i < k; i += kCBThreads) {
+      uint64_t kv = keys[i];
+      L[i] = (uint32_t)(kv >> 16);
+      order[i] = (uint16_t)(kv & 0xffff);
+    }
+    __syncthreads();
+    // ---- C. two-queue merge (sequential, exact)
+    if (tid == 0) two_queue(L, I, k);
+    __syncthreads();
+    // ---- D. depths
+    node_depths(I, D, k - 1);
+    // leaf depth = depth(parent) + 1, scattered to ascending-symbol rank
+    for (int i = tid; i < k; i += kCBThreads) {
+      uint32_t d = (uint32_t)D[L[i]] + 1;
+      lenr[order[i]] = (uint8_t)min(d, 255u);
+    }
+  }
+  __syncthreads();
+
+  // ---- E. canonical codes (encode.py:123-152)
+  if (tid < 64) s_cbl[tid] = 0;
+  if (tid == 0) {
+    s_max = 0;
+    s_min = 255;
+  }
+  __syncthreads();
+  for (int i = tid; i < k; i += kCBThreads) {
+    uint32_t l = lenr[i];
+    atomicAdd(&s_cbl[min(l, 63u)], 1u);
+    atomicMax(&s_max, l);
+    atomicMin(&s_min, l);
+  }
+  __syncthreads();
+  const int max_len = (int)s_max;
+  if (max_len > kMaxCodeLen) {
+    if (tid == 0) atomicCAS(&a.meta->status, 0u, (uint32_t)NBZG_CODE_TOO_LONG);
+    return;
+  }
+  if (tid == 0) {
+    uint64_t code = 0;
+    for (int l = 1; l <= max_len; l++) {
+      s_fc[l] = code;
+      code = (code + s_cbl[l]) << 1;
+    }
+    fm.min_len = s_min;
+    fm.max_len = s_max;
+  }
+  __syncthreads();
+  // rank within length class, ascending symbol: per present length, a block scan
+  const int RK = (k + kCBThreads - 1) / kCBThreads;
+  for (int l = 1; l <= max_len; l++) {
+    if (s_cbl[l] == 0) continue;  // uniform
+    uint32_t c = 0;
+    for (int r = 0; r < RK; r++) {
+      int i = tid * RK + r;
+      if (i < k && lenr[i] == l) c++;
+    }
+    uint32_t tot;
+    uint32_t ex = block_excl_scan<uint32_t>(c, scan_u32, &tot);
+    for (int r = 0; r < RK; r++) {
+      int i = tid * RK + r;
+      if (i < k && lenr[i] == l) {
+        lut[sym[i]] = ((uint64_t)l << 57) | (s_fc[l] + ex);
+        ex++;
+      }
+    }
+  }
+  // ---- sizes: total bits = sum count * len
+  unsigned long long tb = 0;
+  for (int i = tid; i < k; i += kCBThreads) tb += (unsigned long long)cnt[i] * lenr[i];
+  unsigned long long tbits;
+  block_excl_scan<unsigned long long>(tb, scan_u64, &tbits);
+  if (tid == 0) {
+    fm.total_bits = tbits;
+    uint64_t table_end = 8 + 5 * (uint64_t)k;
+    fm.index_off = table_end + 8;
+    fm.bits_off = (fm.index_off + 4 * (uint64_t)a.nchunks + 3) & ~3ull;
+    fm.esc_off = fm.bits_off + 4 * ((tbits + 31) / 32);
+    fm.payload_len = fm.esc_off + 4 * fm.n_esc;
+  }
+}
+
+int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uint8_t* len,
+                         uint64_t* lut, uint32_t* scratch, nbzg_meta* meta, int64_t n,
+                         int64_t nchunks, int single_field, cudaStream_t st) {
+  CBArgs a{hist, nbins, sym, len, lut, scratch, meta, n, nchunks, single_field};
+  size_t sm = 14 * (size_t)kCBSmemK;  // keys u64 | L u32 | order u16
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(codebook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  codebook_kernel<<<single_field >= 0 ? 1 : 6, kCBThreads, sm, st>>>(a);
+  return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
+}
+
+int launch_codebook(const Plan& p, cudaStream_t st) {
+  if (p.n == 0) return NBZG_OK;
+  return launch_codebook_impl(p.hist, p.nbins, p.cb_sym, p.cb_len, p.lut, p.cb_scratch, p.meta,
+                              p.n, p.nchunks, -1, st);
+}
+
+// ---- parity hook: K.huffman_lengths on sorted counts (one CTA)
+__global__ void __launch_bounds__(kCBThreads) huffman_lengths_kernel(const uint32_t* counts,
+                                                                     int k, uint8_t* lengths,
+                                                                     uint32_t* scr,
+                                                                     uint32_t* status) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const bool small = k <= kCBSmemK;
+  int N = 1;
+  while (N < k) N <<= 1;
+  uint8_t* base = small ? smem : reinterpret_cast<uint8_t*>(scr);
+  uint32_t* I = reinterpret_cast<uint32_t*>(base);
+  uint8_t* D = base + 4 * (size_t)N;
+  uint32_t* L = reinterpret_cast<uint32_t*>(base + 8 * (size_t)N);
+  const int tid = threadIdx.x;
+  if (k == 1) {
+    if (tid == 0) lengths[0] = 1;
+    return;
+  }
+  for (int i = tid; i < k; i += kCBThreads) L[i] = counts[i];
+  __syncthreads();
+  if (tid == 0) two_queue(L, I, k);
+  __syncthreads();
+  node_depths(I, D, k - 1);
+  for (int i = tid; i < k; i += kCBThreads) {
+    uint32_t d = (uint32_t)D[L[i]] + 1;
+    lengths[i] = (uint8_t)min(d, 255u);
+    if (d > kMaxCodeLen) atomicCAS(status, 0u, (uint32_t)NBZG_CODE_TOO_LONG);
+  }
+}
+
+int launch_huffman_lengths(const uint32_t* counts, int64_t k, uint8_t* lengths, uint32_t* scr,
+                           uint32_t* status, cudaStream_t st) {
+  if (k <= 0 || k > 65536) return NBZG_BAD_ARG;
+  size_t sm = 12 * (size_t)kCBSmemK;
+  cudaFuncSetAttribute(huffman_lengths_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  huffman_lengths_kernel<<<1, kCBThreads, sm, st>>>(counts, (int)k, lengths, scr, status);
+  return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
+}
+
+// ---- K5: payload layout (offsets of the non-constant fields, field order)
+__global__ void layout_kernel(nbzg_meta* meta, int64_t n) {
+  if (threadIdx.x != 0) return;
+  uint64_t off = 0;
+  for (int f = 0; f < 6; f++) {
+    nbzg_field_meta& m = meta->f[f];
+    m.payload_off = off;
+    if (m.is_const || n == 0) {
+      m.payload_len = 0;
+      continue;
+    }
+    off += m.payload_len;
+  }
+  meta->arena_used = off;
+}
+
+int launch_layout(const Plan& p, cudaStream_t st) {
+  layout_kernel<<<1, 32, 0, st>>>(p.meta, p.n);
+  return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
+}
+
+}  // namespace nbzg

@@ -1,0 +1,68 @@
+// plan.h -- host-side plan of one compress call: sizes and workspace carving.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/nbzg.h"
+
+namespace nbzg {
+
+struct Plan {
+  // problem
+  int64_t n = 0;
+  int sorted = 0;
+  int64_t S = 16384;    // segment size
+  int64_t tile = 0;     // particles per tile (whole segments, <= 16384)
+  int64_t ntiles = 0;
+  int64_t nseg = 0;
+  int64_t nchunks = 0;  // ceil(n / 16384)
+  int64_t nbins = 0;    // interval_count (codes 0 .. 2*half-1)
+  int half = 0;
+  int ig = 6;
+  const float* f[6] = {};
+  int bound_kind[6] = {};
+  double bound_value[6] = {};
+  // workspace
+  uint32_t* minmax = nullptr;   // 12 ordered u32
+  nbzg_meta* meta = nullptr;
+  uint16_t* perm = nullptr;
+  uint8_t* seg_bits = nullptr;
+  uint16_t* codes = nullptr;    // 6*n
+  uint32_t* hist = nullptr;     // 6*nbins
+  uint32_t* cb_sym = nullptr;   // 6*nbins ascending symbols
+  uint8_t* cb_len = nullptr;    // 6*nbins lengths by rank
+  uint64_t* lut = nullptr;      // 6*nbins
+  uint32_t* cb_scratch = nullptr;  // 6 * 4*nbins u32 (sort + queues, large-k path)
+  uint64_t* lb = nullptr;       // 6*nchunks*2 look-back words
+  uint32_t* counters = nullptr; // 64 u32 (tickets, flags)
+  uint32_t* tile_flags = nullptr;  // ntiles (u64-key fallback tiles)
+  uint8_t* arena = nullptr;
+  size_t arena_bytes = 0;
+};
+
+// one field of a decompress call (decode.cu)
+struct DField {
+  const uint8_t* payload;
+  int64_t payload_len;
+  int32_t kind;  // 3 = SZ_DQ (v2), 0 = SZ_FIELD (v1)
+  double bound, twob, inv;
+  float inv32;
+  float* out;
+};
+
+size_t plan_workspace(Plan& p, void* base);  // carve (base may be null: size only)
+void plan_shape(Plan& p, int64_t n, int sorted, int64_t interval_count, int64_t segment_size);
+
+// kernel launchers (each enqueues on `st`)
+int launch_minmax6(const float* const* f, int64_t n, uint32_t* minmax12, cudaStream_t st);
+int launch_resolve(const Plan& p, cudaStream_t st);
+int launch_rindex_sort(const Plan& p, cudaStream_t st);
+int launch_quantize(const Plan& p, cudaStream_t st);
+int launch_codebook(const Plan& p, cudaStream_t st);
+int launch_layout(const Plan& p, cudaStream_t st);
+int launch_encode(const Plan& p, cudaStream_t st);
+
+int sm_count();
+
+}  // namespace nbzg

@@ -1,0 +1,265 @@
+// quant.cu -- K3: permutation gather + dual-quant + code histogram.
+//
+// Replaces the gather (pipeline.py:466), quantize.quantize_field ->
+// K.sz_quantize (_kernels.py:150-184) and np.bincount (pipeline.py:191).
+// The reference's reconstruct-and-predict chain is sequential; this kernel
+// computes the parallel "pre-quantise then difference" restatement
+// (oracle/nbz_oracle.c orc_dq_quantize):
+//     k_i = rint(x_i / 2b) (lattice index), q_i = k_i - k_{i-1},
+//     code_i = q_i + half + 1 if q_i in [-half, half-2] and
+//              |x_i - f32(k_i * 2b)| <= b, else 0 (escape).
+//
+// Persistent CTAs, each owning ONE field and a contiguous range of tiles, so
+// a CTA keeps one shared-memory histogram window for its whole range and
+// flushes it once (out-of-window codes go straight to global atomics).
+// Tiles (field values + the tile-local permutation) are staged into shared
+// memory with TMA bulk copies (cp.async.bulk + mbarrier), double buffered,
+// so the next tile streams in while the current one is gathered.
+#include "nbzg_internal.cuh"
+#include "plan.h"
+
+namespace nbzg {
+
+constexpr int kQThreads = 1024;
+constexpr int kQPer = kTileMax / kQThreads;  // 16 positions per thread
+constexpr int kQWin = 4096;                  // histogram window (bins)
+
+struct QArgs {
+  const float* f[6];
+  int64_t n, tile, ntiles;
+  const uint16_t* perm;  // tile-local source index per sorted position (null: identity)
+  const nbzg_meta* meta;
+  int half;
+  uint16_t* codes;  // 6 x code_stride
+  int64_t code_stride;
+  uint32_t* hist;  // 6 x nbins
+  int64_t nbins;
+  int groups;
+  int use_tma;
+};
+
+NBZG_DEV uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+NBZG_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+NBZG_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+NBZG_DEV bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+NBZG_DEV void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+NBZG_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// dual-quant lattice index, clamped (orc_dq_quantize: dq_k)
+NBZG_DEV int64_t dq_index(float x, const nbzg_field_meta& m, bool& fast) {
+  double k = lattice_index<false>(x, m.inv32, m.inv, m.twob, fast);
+  if (!fast) k = fmin(fmax(k, -kDqKmax), kDqKmax);
+  return (int64_t)k;
+}
+
+template <bool SORTED>
+__global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  float* xbuf = reinterpret_cast<float*>(smem);                      // [2][16384]
+  uint16_t* pbuf = reinterpret_cast<uint16_t*>(xbuf + 2 * kTileMax);  // [2][16384]
+  uint32_t* hw = reinterpret_cast<uint32_t*>(pbuf + 2 * kTileMax);    // [kQWin]
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ int64_t s_klast[kQThreads / 32];
+  __shared__ int64_t s_carry;
+  __shared__ uint32_t s_esc;
+
+  const int field = blockIdx.x % 6;
+  const int g = blockIdx.x / 6;
+  const nbzg_field_meta& fm = a.meta->f[field];
+  if (fm.is_const || a.n == 0 || a.meta->status) return;  // e.g. BOUND_TOO_SMALL in K2
+  const int64_t tb = (a.ntiles * g) / a.groups, te = (a.ntiles * (g + 1)) / a.groups;
+  if (tb >= te) return;
+  const float* __restrict__ x = a.f[field];
+  uint16_t* __restrict__ codes = a.codes + field * a.code_stride;
+  uint32_t* __restrict__ hist = a.hist + field * a.nbins;
+  const int half = a.half;
+  const int wlo = half + 1 - kQWin / 2;
+  const double b = fm.bound, twob = fm.twob;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+  for (int i = tid; i < kQWin; i += kQThreads) hw[i] = 0;
+  if (tid == 0) {
+    s_esc = 0;
+    // k carried into the range: k of the last sorted element of tile tb-1
+    int64_t kc = 0;
+    if (tb > 0) {
+      int64_t p = tb * a.tile - 1;
+      int64_t src = SORTED ? (tb - 1) * a.tile + a.perm[p] : p;
+      bool fast;
+      kc = dq_index(x[src], fm, fast);
+    }
+    s_carry = kc;
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  auto issue = [&](int64_t t, int buf) {
+    const int64_t t0 = t * a.tile;
+    const int m = (int)min(a.tile, a.n - t0);
+    const int mb = m & ~7;  // bulk part (16-byte multiples for both arrays)
+    uint32_t bytes = (uint32_t)mb * (SORTED ? 6u : 4u);
+    mbar_expect_tx(&bar[buf], bytes);
+    if (mb) {
+      tma_load(xbuf + buf * kTileMax, x + t0, (uint32_t)mb * 4u, &bar[buf]);
+      if (SORTED) tma_load(pbuf + buf * kTileMax, a.perm + t0, (uint32_t)mb * 2u, &bar[buf]);
+    }
+  };
+
+  if (a.use_tma && tid == 0) {
+    issue(tb, 0);
+    if (tb + 1 < te) issue(tb + 1, 1);
+  }
+  uint32_t phase[2] = {0, 0};
+  for (int64_t t = tb; t < te; t++) {
+    const int buf = (int)((t - tb) & 1);
+    const int64_t t0 = t * a.tile;
+    const int m = (int)min(a.tile, a.n - t0);
+    float* xs = xbuf + buf * kTileMax;
+    uint16_t* ps = pbuf + buf * kTileMax;
+    if (a.use_tma) {
+      while (!mbar_try_wait(&bar[buf], phase[buf])) {
+      }
+      phase[buf] ^= 1;
+      const int mb = m & ~7;
+      if (tid < m - mb) {
+        xs[mb + tid] = x[t0 + mb + tid];
+        if (SORTED) ps[mb + tid] = a.perm[t0 + mb + tid];
+      }
+    } else {
+      for (int i = tid; i < m; i += kQThreads) {
+        xs[i] = x[t0 + i];
+        if (SORTED) ps[i] = a.perm[t0 + i];
+      }
+    }
+    __syncthreads();
+
+    // ---- per thread: positions p0 .. p0+15
+    const int p0 = tid * kQPer;
+    const int cnt = max(0, min(kQPer, m - p0));
+    // k of this thread's last element, exchanged to the right neighbour
+    int64_t klast = 0;
+    if (cnt > 0) {
+      int p = p0 + cnt - 1;
+      float xv = SORTED ? xs[min((int)ps[p], m - 1)] : xs[p];
+      bool fast;
+      klast = dq_index(xv, fm, fast);
+    }
+    int64_t kprev = __shfl_up_sync(0xffffffffu, klast, 1);
+    if (lane == 31) s_klast[wid] = klast;
+    __syncthreads();
+    if (lane == 0) kprev = wid == 0 ? s_carry : s_klast[wid - 1];
+    uint32_t packed[kQPer / 2];
+#pragma unroll
+    for (int j = 0; j < kQPer; j++) {
+      uint32_t code = 0;
+      if (j < cnt) {
+        int p = p0 + j;
+        float xv = SORTED ? xs[min((int)ps[p], m - 1)] : xs[p];
+        bool fast;
+        int64_t k = dq_index(xv, fm, fast);
+        int64_t q = k - kprev;
+        bool ok = q >= -half && q <= half - 2;
+        if (ok && !fast) {
+          float r = (float)__dmul_rn((double)k, twob);
+          ok = fabs((double)xv - (double)r) <= b;
+        }
+        code = ok ? (uint32_t)(q + half + 1) : 0u;
+        kprev = k;
+        if (code == 0) {
+          atomicAdd(&s_esc, 1u);
+        } else {
+          int wb = (int)code - wlo;
+          if ((unsigned)wb < (unsigned)kQWin) atomicAdd(&hw[wb], 1u);
+          else atomicAdd(&hist[code], 1u);
+        }
+      }
+      if (j & 1) packed[j >> 1] |= code << 16;
+      else packed[j >> 1] = code;
+    }
+    // ---- store codes (16 x u16 per thread)
+    uint16_t* dst = codes + t0 + p0;
+    if (cnt == kQPer && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+      uint4* d4 = reinterpret_cast<uint4*>(dst);
+      d4[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      d4[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+    } else {
+      for (int j = 0; j < cnt; j++) dst[j] = (uint16_t)(packed[j >> 1] >> ((j & 1) * 16));
+    }
+    // carry for the next tile = k of position m-1
+    if (cnt > 0 && p0 + cnt == m) s_carry = kprev;
+    __syncthreads();  // buffer `buf` fully consumed; s_carry visible
+    if (a.use_tma && tid == 0 && t + 2 < te) {
+      fence_proxy_async();
+      issue(t + 2, buf);
+    }
+  }
+  // ---- flush the histogram window
+  for (int i = tid; i < kQWin; i += kQThreads) {
+    uint32_t c = hw[i];
+    int code = wlo + i;
+    if (c && code >= 1 && code < (int)a.nbins) atomicAdd(&hist[code], c);
+  }
+  if (tid == 0 && s_esc) atomicAdd(&hist[0], s_esc);
+}
+
+int launch_quantize(const Plan& p, cudaStream_t st) {
+  if (p.n == 0) return NBZG_OK;
+  QArgs a;
+  for (int f = 0; f < 6; f++) a.f[f] = p.f[f];
+  a.n = p.n;
+  a.tile = p.tile;
+  a.ntiles = p.ntiles;
+  a.perm = p.sorted ? p.perm : nullptr;
+  a.meta = p.meta;
+  a.half = p.half;
+  a.codes = p.codes;
+  a.code_stride = (p.n + 7) & ~int64_t(7);
+  a.hist = p.hist;
+  a.nbins = p.nbins;
+  int per_field = max(1, sm_count() / 6);
+  if (per_field > p.ntiles) per_field = (int)p.ntiles;
+  a.groups = per_field;
+  bool aligned = true;
+  for (int f = 0; f < 6; f++) aligned &= (reinterpret_cast<uintptr_t>(p.f[f]) & 15) == 0;
+  a.use_tma = aligned && (p.tile % 8 == 0);
+  size_t sm = 2 * kTileMax * 4 + 2 * kTileMax * 2 + kQWin * 4;
+  cudaMemsetAsync(p.hist, 0, sizeof(uint32_t) * 6 * p.nbins, st);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(quantize_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(quantize_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    attr = true;
+  }
+  if (p.sorted) quantize_kernel<true><<<6 * per_field, kQThreads, sm, st>>>(a);
+  else quantize_kernel<false><<<6 * per_field, kQThreads, sm, st>>>(a);
+  return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
+}
+
+}  // namespace nbzg

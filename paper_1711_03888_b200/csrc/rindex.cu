@@ -1,0 +1,441 @@
+// rindex.cu -- K2: R-index keys + segment-local stable radix sort.
+//
+// Replaces rindex.build_r_indices (rindex.py:164-198), K.interleave3
+// (_kernels.py:778-786) and rindex.prx_sort -> K.prx_order
+// (_kernels.py:887-927) for the coordinate variant.
+//
+// One CTA per tile (whole segments, <= 16384 particles).  Per segment:
+//   1. exact f32 min/max of the three coordinates (block reduce); because
+//      rint(f64(x)/2b) is monotone in x, the integerised minima/maxima are the
+//      integerised min/max -- six exact FP64 divisions per segment give the
+//      per-segment minima, `need`, `bits` and the 21-bit clamp drop;
+//   2. per particle: exact integerise (FP32 fast path, FP64 fallback), shift,
+//      and interleave ONLY the bits the sort looks at: key >> 3*min(k,bits)
+//      == interleave(v_t >> (drop + min(k,bits))) with w = bits - min(k,bits)
+//      bits per field (3w <= 32 -> u32 keys);
+//   3. stable LSD radix sort of the tile-local indices by that key, 8-bit
+//      digits, warp-level __match_any_sync ranking + per-warp shared-memory
+//      digit histograms (digit-major/warp-minor scan keeps it stable).
+// Output: u16 tile-local source index per sorted position, u8 bits/segment.
+// Tiles whose masked keys need more than 32 bits are flagged and redone by
+// the u64-key instantiation.
+#include "nbzg_internal.cuh"
+#include "plan.h"
+
+namespace nbzg {
+
+constexpr int kSortThreads = 512;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kRadix = 256;
+
+struct RArgs {
+  const float* x[3];
+  int64_t n, S, tile, ntiles;
+  int ig;
+  const nbzg_meta* meta;
+  uint16_t* perm;
+  uint8_t* seg_bits;
+  uint32_t* tile_flags;
+  uint32_t* status;
+  int pass;  // 0 = u32 main pass, 1 = u64 pass over flagged tiles
+};
+
+NBZG_DEV void set_status(uint32_t* status, uint32_t code) { atomicCAS(status, 0u, code); }
+
+struct SegParams {
+  int64_t mn[3];
+  int shift;  // drop + eff
+  int w;      // key bits per field after masking
+  int bits;
+  int bad;
+};
+
+// exact integerize of one float (quantize.py:117-128 semantics)
+NBZG_DEV int64_t integerize1(float x, const nbzg_field_meta& m) {
+  bool fast;
+  double k = lattice_index<true>(x, m.inv32, m.inv, m.twob, fast);
+  return (int64_t)k;
+}
+
+template <typename KeyT>
+NBZG_DEV KeyT make_key(uint64_t u0, uint64_t u1, uint64_t u2);
+template <>
+NBZG_DEV uint32_t make_key<uint32_t>(uint64_t u0, uint64_t u1, uint64_t u2) {
+  return (spread3_32((uint32_t)u0) << 2) | (spread3_32((uint32_t)u1) << 1) |
+         spread3_32((uint32_t)u2);
+}
+template <>
+NBZG_DEV uint64_t make_key<uint64_t>(uint64_t u0, uint64_t u1, uint64_t u2) {
+  return (spread3_64(u0) << 2) | (spread3_64(u1) << 1) | spread3_64(u2);
+}
+
+// Stable LSD sort of perm[lo, lo+m) by keys[perm[.]] over sort_bits bits.
+template <typename KeyT>
+NBZG_DEV void block_sort_range(const KeyT* keys, uint16_t* perm, int lo, int m, int sort_bits,
+                               uint16_t* whist, uint32_t* scan_tmp) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int E = ((m + kSortWarps * 32 - 1) / (kSortWarps * 32)) * 32;  // per-warp span
+  const int J = E / 32;
+  const int base = w * E;
+  uint16_t* wh = whist + w * kRadix;
+  for (int sh = 0; sh < sort_bits; sh += 8) {
+    for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) whist[i] = 0;
+    __syncthreads();
+    uint32_t packed[32];
+#pragma unroll
+    for (int j = 0; j < 32; j++) {
+      if (j < J) {
+        int pos = base + j * 32 + lane;
+        bool valid = pos < m;
+        uint32_t idx = valid ? perm[lo + pos] : 0u;
+        uint32_t d = valid ? (uint32_t)((keys[idx] >> sh) & 0xff) : 0x100u;
+        uint32_t peers = __match_any_sync(0xffffffffu, d);
+        uint32_t lt = __popc(peers & lanemask_lt());
+        uint32_t cnt = valid ? wh[d] : 0u;
+        __syncwarp();
+        if (valid && lt == 0) wh[d] = (uint16_t)(cnt + __popc(peers));
+        __syncwarp();
+        packed[j] = idx | ((cnt + lt) << 14) | (d << 24);
+      }
+    }
+    __syncthreads();
+    // digit-major / warp-minor exclusive scan of the per-warp histograms
+    {
+      const int t = threadIdx.x;
+      const int d = t >> 1, w0 = (t & 1) * (kSortWarps / 2);
+      uint32_t c[kSortWarps / 2];
+      uint32_t s = 0;
+#pragma unroll
+      for (int q = 0; q < kSortWarps / 2; q++) {
+        c[q] = whist[(w0 + q) * kRadix + d];
+        s += c[q];
+      }
+      uint32_t tot;
+      uint32_t ex = block_excl_scan<uint32_t>(s, scan_tmp, &tot);
+#pragma unroll
+      for (int q = 0; q < kSortWarps / 2; q++) {
+        whist[(w0 + q) * kRadix + d] = (uint16_t)ex;
+        ex += c[q];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; j++) {
+      if (j < J && base + j * 32 + lane < m) {
+        uint32_t v = packed[j];
+        uint32_t idx = v & 0x3fff, r = (v >> 14) & 0x3ff, d = v >> 24;
+        perm[lo + wh[d] + r] = (uint16_t)idx;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <typename KeyT>
+__global__ void __launch_bounds__(kSortThreads) rindex_sort_kernel(RArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  KeyT* keys = reinterpret_cast<KeyT*>(smem);
+  uint16_t* perm = reinterpret_cast<uint16_t*>(keys + kTileMax);
+  uint16_t* whist = perm + kTileMax;
+  __shared__ uint32_t scan_tmp[33];
+  __shared__ float red[2][3][kSortWarps];
+  __shared__ SegParams sp;
+
+  const int64_t t = blockIdx.x;
+  if (a.pass == 1 && a.tile_flags[t] == 0) return;
+  const int64_t t0 = t * a.tile;
+  const int64_t t1 = min(a.n, t0 + a.tile);
+  const int mt = (int)(t1 - t0);
+  const nbzg_field_meta* fm = a.meta->f;
+
+  for (int i = threadIdx.x; i < mt; i += kSortThreads) perm[i] = (uint16_t)i;
+
+  for (int64_t s0 = t0; s0 < t1; s0 += a.S) {
+    const int lo = (int)(s0 - t0);
+    const int m = (int)(min(t1, s0 + a.S) - s0);
+    // ---- 1. per-segment min / max of the coordinates
+    float mn[3], mx[3];
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      mn[c] = __int_as_float(0x7f800000);
+      mx[c] = -__int_as_float(0x7f800000);
+    }
+    for (int i = threadIdx.x; i < m; i += kSortThreads) {
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        float v = a.x[c][s0 + i];
+        mn[c] = fminf(mn[c], v);
+        mx[c] = fmaxf(mx[c], v);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        mn[c] = fminf(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
+        mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+      }
+      if ((threadIdx.x & 31) == 0) {
+        red[0][c][threadIdx.x >> 5] = mn[c];
+        red[1][c][threadIdx.x >> 5] = mx[c];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int need = 0, bad = 0;
+      for (int c = 0; c < 3; c++) {
+        float a0 = red[0][c][0], b0 = red[1][c][0];
+        for (int q = 1; q < kSortWarps; q++) {
+          a0 = fminf(a0, red[0][c][q]);
+          b0 = fmaxf(b0, red[1][c][q]);
+        }
+        if (fm[c].is_const) {
+          sp.mn[c] = 0;
+          continue;
+        }
+        double qa = __ddiv_rn((double)a0, fm[c].twob), qb = __ddiv_rn((double)b0, fm[c].twob);
+        if (fabs(qa) > kIntLimit || fabs(qb) > kIntLimit) bad = 1;
+        int64_t ia = (int64_t)rint(qa), ib = (int64_t)rint(qb);
+        sp.mn[c] = ia;
+        int bl = bitlen64((uint64_t)(ib - ia));
+        need = max(need, bl);
+      }
+      int bits = min(need, 21);
+      int drop = need > 21 ? need - 21 : 0;  // allow_key_clamp=True for sz-lv-prx (pipeline.py:463)
+      int eff = min(a.ig, bits);
+      sp.bits = bits;
+      sp.shift = drop + eff;
+      sp.w = bits - eff;
+      sp.bad = bad;
+    }
+    __syncthreads();
+    if (sp.bad) {
+      if (threadIdx.x == 0) set_status(a.status, NBZG_BOUND_TOO_SMALL);
+      return;
+    }
+    const int w = sp.w;
+    if (sizeof(KeyT) == 4 && 3 * w > 32) {
+      if (threadIdx.x == 0) a.tile_flags[t] = 1;
+      return;  // redone by the u64 pass
+    }
+    if (threadIdx.x == 0) a.seg_bits[(s0) / a.S] = (uint8_t)sp.bits;  // staged below
+    if (w > 0) {
+      // ---- 2. masked keys
+      const int shift = sp.shift;
+      const int64_t m0 = sp.mn[0], m1 = sp.mn[1], m2 = sp.mn[2];
+      for (int i = threadIdx.x; i < m; i += kSortThreads) {
+        uint64_t u[3];
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+          int64_t iv = fm[c].is_const ? 0 : integerize1(a.x[c][s0 + i], fm[c]);
+          int64_t mm = c == 0 ? m0 : (c == 1 ? m1 : m2);
+          u[c] = (uint64_t)(iv - mm) >> shift;
+        }
+        keys[lo + i] = make_key<KeyT>(u[0], u[1], u[2]);
+      }
+      __syncthreads();
+      // ---- 3. stable radix sort over 3w bits
+      block_sort_range<KeyT>(keys, perm, lo, m, 3 * w, whist, scan_tmp);
+    }
+    __syncthreads();
+  }
+  // ---- write the tile's permutation (coalesced)
+  for (int i = threadIdx.x; i < mt; i += kSortThreads) a.perm[t0 + i] = perm[i];
+}
+
+int launch_rindex_sort(const Plan& p, cudaStream_t st) {
+  if (p.n == 0) return NBZG_OK;
+  RArgs a;
+  for (int c = 0; c < 3; c++) a.x[c] = p.f[c];
+  a.n = p.n;
+  a.S = p.S;
+  a.tile = p.tile;
+  a.ntiles = p.ntiles;
+  a.ig = p.ig;
+  a.meta = p.meta;
+  a.perm = p.perm;
+  a.seg_bits = p.seg_bits;
+  a.tile_flags = p.tile_flags;
+  a.status = &p.meta->status;
+  size_t sm32 = kTileMax * (4 + 2) + kSortWarps * kRadix * 2;
+  size_t sm64 = kTileMax * (8 + 2) + kSortWarps * kRadix * 2;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(rindex_sort_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm32);
+    cudaFuncSetAttribute(rindex_sort_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm64);
+    attr = true;
+  }
+  cudaMemsetAsync(p.tile_flags, 0, sizeof(uint32_t) * p.ntiles, st);
+  a.pass = 0;
+  rindex_sort_kernel<uint32_t><<<(unsigned)p.ntiles, kSortThreads, sm32, st>>>(a);
+  a.pass = 1;
+  rindex_sort_kernel<uint64_t><<<(unsigned)p.ntiles, kSortThreads, sm64, st>>>(a);
+  return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
+}
+
+// ---------------------------------------------------------------- parity hooks
+// Full 63-bit keys (rindex.py:164-198 + _kernels.py:778-786), one CTA per
+// segment; used by nbzg_rindex_keys for bit-exact key parity.
+struct KArgs {
+  const float* x[3];
+  int64_t n, S;
+  double twob[3];
+  double inv[3];
+  float inv32[3];
+  int is_const[3];
+  uint64_t* keys;
+  uint8_t* seg_bits;
+  uint32_t* status;
+};
+
+__global__ void __launch_bounds__(256) rindex_keys_kernel(KArgs a) {
+  const int64_t s0 = (int64_t)blockIdx.x * a.S;
+  const int64_t s1 = min(a.n, s0 + a.S);
+  __shared__ float red[2][3][8];
+  __shared__ int64_t smn[3];
+  __shared__ int sdrop, sbad;
+  float mn[3], mx[3];
+  for (int c = 0; c < 3; c++) {
+    mn[c] = __int_as_float(0x7f800000);
+    mx[c] = -__int_as_float(0x7f800000);
+  }
+  for (int64_t i = s0 + threadIdx.x; i < s1; i += blockDim.x)
+    for (int c = 0; c < 3; c++) {
+      float v = a.x[c][i];
+      mn[c] = fminf(mn[c], v);
+      mx[c] = fmaxf(mx[c], v);
+    }
+  for (int c = 0; c < 3; c++) {
+    for (int o = 16; o; o >>= 1) {
+      mn[c] = fminf(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
+      mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      red[0][c][threadIdx.x >> 5] = mn[c];
+      red[1][c][threadIdx.x >> 5] = mx[c];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int need = 0, bad = 0;
+    for (int c = 0; c < 3; c++) {
+      float a0 = red[0][c][0], b0 = red[1][c][0];
+      for (int q = 1; q < 8; q++) {
+        a0 = fminf(a0, red[0][c][q]);
+        b0 = fmaxf(b0, red[1][c][q]);
+      }
+      if (a.is_const[c]) {
+        smn[c] = 0;
+        continue;
+      }
+      double qa = __ddiv_rn((double)a0, a.twob[c]), qb = __ddiv_rn((double)b0, a.twob[c]);
+      if (fabs(qa) > kIntLimit || fabs(qb) > kIntLimit) bad = 1;
+      int64_t ia = (int64_t)rint(qa), ib = (int64_t)rint(qb);
+      smn[c] = ia;
+      need = max(need, bitlen64((uint64_t)(ib - ia)));
+    }
+    int bits = min(need, 21);
+    sdrop = need > 21 ? need - 21 : 0;
+    sbad = bad;
+    a.seg_bits[blockIdx.x] = (uint8_t)bits;
+  }
+  __syncthreads();
+  if (sbad) {
+    if (threadIdx.x == 0) set_status(a.status, NBZG_BOUND_TOO_SMALL);
+    return;
+  }
+  for (int64_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
+    uint64_t u[3];
+    for (int c = 0; c < 3; c++) {
+      int64_t iv = 0;
+      if (!a.is_const[c]) {
+        bool fast;
+        iv = (int64_t)lattice_index<true>(a.x[c][i], a.inv32[c], a.inv[c], a.twob[c], fast);
+      }
+      u[c] = (uint64_t)(iv - smn[c]) >> sdrop;
+    }
+    a.keys[i] = make_key<uint64_t>(u[0], u[1], u[2]);
+  }
+}
+
+int launch_rindex_keys(const float* x, const float* y, const float* z, int64_t n,
+                       const double* bounds3, int64_t S, uint64_t* keys, uint8_t* seg_bits,
+                       uint32_t* status, cudaStream_t st) {
+  KArgs a;
+  a.x[0] = x;
+  a.x[1] = y;
+  a.x[2] = z;
+  a.n = n;
+  a.S = S;
+  for (int c = 0; c < 3; c++) {
+    a.is_const[c] = bounds3[c] <= 0.0;
+    a.twob[c] = 2.0 * bounds3[c];
+    a.inv[c] = a.is_const[c] ? 0.0 : 1.0 / a.twob[c];
+    a.inv32[c] = (float)a.inv[c];
+  }
+  a.keys = keys;
+  a.seg_bits = seg_bits;
+  a.status = status;
+  int64_t nseg = (n + S - 1) / S;
+  if (nseg > 0) rindex_keys_kernel<<<(unsigned)nseg, 256, 0, st>>>(a);
+  return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
+}
+
+// prx_order parity hook on full keys (_kernels.py:887-927): one CTA per
+// segment, masked key = key >> 3*min(k,bits), up to 63 bits (u64 smem keys).
+struct OArgs {
+  const uint64_t* keys;
+  int64_t n, S;
+  const uint8_t* seg_bits;
+  int ig;
+  int64_t* order;
+};
+
+__global__ void __launch_bounds__(kSortThreads) prx_order_kernel(OArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
+  uint16_t* perm = reinterpret_cast<uint16_t*>(keys + kTileMax);
+  uint16_t* whist = perm + kTileMax;
+  __shared__ uint32_t scan_tmp[33];
+  const int64_t s0 = (int64_t)blockIdx.x * a.S;
+  const int m = (int)(min(a.n, s0 + a.S) - s0);
+  const int bits = a.seg_bits[blockIdx.x];
+  const int eff = min(a.ig, bits);
+  const int sort_bits = 3 * bits - 3 * eff;
+  for (int i = threadIdx.x; i < m; i += kSortThreads) {
+    perm[i] = (uint16_t)i;
+    keys[i] = a.keys[s0 + i] >> (3 * eff);
+  }
+  __syncthreads();
+  if (sort_bits > 0) block_sort_range<uint64_t>(keys, perm, 0, m, sort_bits, whist, scan_tmp);
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += kSortThreads) a.order[s0 + i] = s0 + perm[i];
+}
+
+int launch_prx_order(const uint64_t* keys, int64_t n, int64_t S, const uint8_t* seg_bits, int ig,
+                     int64_t* order, cudaStream_t st) {
+  if (S > kTileMax) return NBZG_UNSUPPORTED;
+  OArgs a{keys, n, S, seg_bits, ig, order};
+  size_t sm = kTileMax * (8 + 2) + kSortWarps * kRadix * 2;
+  cudaFuncSetAttribute(prx_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int64_t nseg = (n + S - 1) / S;
+  if (nseg > 0) prx_order_kernel<<<(unsigned)nseg, kSortThreads, sm, st>>>(a);
+  return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
+}
+
+// tile-local u16 permutation -> global int64 order (CompressResult.order)
+__global__ void order_expand_kernel(const uint16_t* perm, int64_t n, int64_t tile,
+                                    int64_t* order) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) order[i] = (i / tile) * tile + perm[i];
+}
+
+int launch_order_expand(const uint16_t* perm, int64_t n, int64_t tile, int64_t* order,
+                        cudaStream_t st) {
+  if (n > 0) order_expand_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(perm, n, tile, order);
+  return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
+}
+
+}  // namespace nbzg

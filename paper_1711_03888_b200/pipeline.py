@@ -1,0 +1,484 @@
+"""The reference's host API for the SZ-LV / SZ-LV-PRX path, backed by the
+B200 kernels (pkg/src/nbz/pipeline.py:43-149, 447-612).
+
+``compress`` / ``decompress`` / ``ratio`` keep the reference's names,
+signatures, defaults and exception types.  What changes underneath:
+
+* every stage runs on device through the C ABI (``libnbzg.so``): bounds,
+  R-index keys + segment sort, gather + dual-quant + histogram, Huffman
+  codebook, chunk-parallel encoding, and the fused decode + dequantise;
+* SZ streams are written as stream kind ``SZ_DQ`` (3) in a version-2
+  container: the reference's sequential reconstruct-and-predict chain
+  (_kernels.py:150-184) has no exact parallel form, so the B200 path uses
+  the pre-quantise-then-difference restatement plus a
+  16384-symbol chunk index.  Reference (v1, ``SZ_FIELD``) archives are
+  still decoded (exact sequential chain, compat path);
+* archives stay device-resident until their bytes are asked for
+  (``Archive.streams`` / ``serialized()``), and ``CompressResult.order``
+  is materialised from the device permutation on first access.
+
+Modes outside the north-star path (sz-lcf, sz-cpc2000, cpc2000) are not
+implemented by the B200 path and raise ``ValidationError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import enum
+import struct
+from dataclasses import dataclass, field
+from typing import List, Mapping, Optional, Sequence, Tuple, Union
+
+import numpy as np
+
+from . import _native as N
+from .errors import (BoundTooSmallError, DecodeError, EncodeError, NbzError,
+                     ValidationError)
+from .model import FIELD_NAMES, BoundKind, ErrorBoundSpec, ParticleSnapshot, _is_tensor
+from .rindex import RIndexVariant, Segment, segment_bounds
+
+DEFAULT_INTERVALS = 65536
+CHUNK_SYMBOLS = 16384
+
+
+class Mode(enum.Enum):
+    SZ_LCF = "sz-lcf"
+    SZ_LV = "sz-lv"
+    SZ_LV_PRX = "sz-lv-prx"
+    SZ_CPC2000 = "sz-cpc2000"
+    CPC2000 = "cpc2000"
+
+    @property
+    def uid(self) -> int:
+        return _MODE_UIDS[self]
+
+    @property
+    def is_sorted(self) -> bool:
+        return self in (Mode.SZ_LV_PRX, Mode.SZ_CPC2000, Mode.CPC2000)
+
+    @property
+    def stores_minima(self) -> bool:
+        return self in (Mode.SZ_CPC2000, Mode.CPC2000)
+
+    @classmethod
+    def from_uid(cls, uid: int) -> "Mode":
+        for m in cls:
+            if m.uid == uid:
+                return m
+        raise DecodeError(f"unknown mode id {uid}")
+
+
+_MODE_UIDS = {Mode.SZ_LCF: 0, Mode.SZ_LV: 1, Mode.SZ_LV_PRX: 2,
+              Mode.SZ_CPC2000: 3, Mode.CPC2000: 4}
+
+MODE_ALIASES = {"best-speed": Mode.SZ_LV, "best-tradeoff": Mode.SZ_LV_PRX,
+                "best-compression": Mode.SZ_CPC2000}
+
+GPU_MODES = (Mode.SZ_LV, Mode.SZ_LV_PRX)
+
+
+@dataclass(frozen=True)
+class Settings:
+    """pipeline.py:78-92, same defaults and validation."""
+
+    interval_count: int = DEFAULT_INTERVALS
+    segment_size: int = 16384
+    ignored_groups: int = 6
+    rindex_variant: RIndexVariant = RIndexVariant.COORDINATE
+
+    def __post_init__(self):
+        if self.segment_size < 1:
+            raise ValidationError("segment_size must be >= 1")
+        if self.ignored_groups < 0:
+            raise ValidationError("ignored_groups must be >= 0")
+        if (self.interval_count < 2 or self.interval_count % 2
+                or self.interval_count > (1 << 30)):
+            raise ValidationError("interval_count must be even and in [2, 2^30]")
+
+
+DEFAULT_SETTINGS = Settings()
+
+Bounds = Union[ErrorBoundSpec, Mapping[str, ErrorBoundSpec]]
+
+
+class StreamKind(enum.IntEnum):
+    SZ_FIELD = 0   # reference SZ stream (exact sequential chain), container v1
+    VLC_FIELD = 1
+    RINDEX = 2
+    SZ_DQ = 3      # B200 dual-quant SZ stream with chunk index, container v2
+
+
+NO_FIELD = 255
+
+
+@dataclass(frozen=True)
+class Stream:
+    kind: StreamKind
+    field: int
+    payload: bytes
+
+
+class _Device:
+    """Device-resident side of an archive: the payload arena and where each
+    field's payload sits in it (host copy of the nbzg_meta block)."""
+
+    def __init__(self, arena, offsets, lengths, kinds, keep=()):
+        self.arena = arena          # torch uint8 CUDA tensor
+        self.offsets = offsets      # per field (None for constant fields)
+        self.lengths = lengths
+        self.kinds = kinds
+        self.keep = keep            # tensors that must outlive the archive
+
+
+class Archive:
+    """Self-describing compressed container (in-memory form, pipeline.py:116-143).
+
+    Same attributes as the reference.  ``streams`` and ``serialized()`` pull
+    payload bytes off the device on first use.
+    """
+
+    def __init__(self, mode: Mode, n: int, interval_count: int, segment_size: int,
+                 ignored_groups: int, rindex_variant: Optional[RIndexVariant],
+                 bounds: Tuple[float, ...], constant_mask: int, constants: Tuple[float, ...],
+                 seg_bits=None, streams: Optional[Tuple[Stream, ...]] = None,
+                 device: Optional[_Device] = None, version: int = 2,
+                 device_output: bool = False):
+        self.mode = mode
+        self.n = int(n)
+        self.interval_count = int(interval_count)
+        self.segment_size = int(segment_size)
+        self.ignored_groups = int(ignored_groups)
+        self.rindex_variant = rindex_variant
+        self.bounds = tuple(float(b) for b in bounds)
+        self.constant_mask = int(constant_mask)
+        self.constants = tuple(float(c) for c in constants)
+        self._seg_bits = seg_bits          # numpy u8 or CUDA tensor or None
+        self._segments: Optional[Tuple[Segment, ...]] = None
+        self._streams = streams
+        self._dev = device
+        self.version = version
+        self.device_output = device_output
+        self._wire: Optional[bytes] = None
+
+    # -- reference attributes -------------------------------------------------
+    def is_constant(self, field_index: int) -> bool:
+        return bool(self.constant_mask & (1 << field_index))
+
+    @property
+    def seg_bits(self) -> np.ndarray:
+        sb = self._seg_bits
+        if sb is None:
+            return np.zeros(0, np.uint8)
+        if _is_tensor(sb):
+            sb = sb.cpu().numpy().astype(np.uint8)
+            self._seg_bits = sb
+        return sb
+
+    @property
+    def segments(self) -> Tuple[Segment, ...]:
+        if self._segments is None:
+            if not (self.mode.is_sorted and self.n > 0):
+                self._segments = ()
+            else:
+                edges = segment_bounds(self.n, self.segment_size)
+                bits = self.seg_bits
+                self._segments = tuple(Segment(int(edges[i]), int(edges[i + 1]), int(bits[i]), ())
+                                       for i in range(edges.shape[0] - 1))
+        return self._segments
+
+    @property
+    def streams(self) -> Tuple[Stream, ...]:
+        if self._streams is None:
+            d = self._dev
+            host = d.arena.cpu().numpy() if d is not None else None
+            out = []
+            for fi in range(6):
+                if d is None or d.offsets[fi] is None:
+                    continue
+                o, ln = d.offsets[fi], d.lengths[fi]
+                out.append(Stream(StreamKind(d.kinds[fi]), fi, host[o:o + ln].tobytes()))
+            self._streams = tuple(out)
+        return self._streams
+
+    def payload_lengths(self) -> List[int]:
+        if self._dev is not None:
+            return [ln for o, ln in zip(self._dev.offsets, self._dev.lengths) if o is not None]
+        return [len(s.payload) for s in self.streams]
+
+    def serialized(self) -> bytes:
+        if self._wire is None:
+            from . import io as nbz_io
+            self._wire = nbz_io.serialize_archive(self)
+        return self._wire
+
+    def total_bytes(self) -> int:
+        """Serialized size, computed from the layout (no D2H needed)."""
+        from . import io as nbz_io
+        return nbz_io.serialized_size(self)
+
+    def __repr__(self):
+        return (f"Archive(mode={self.mode.value}, n={self.n}, version={self.version}, "
+                f"mask={self.constant_mask}, payloads={self.payload_lengths()})")
+
+
+class CompressResult:
+    """pipeline.py:146-149: the archive plus the sorted-mode permutation
+    sidecar (``order[i]`` = original index of sorted position i)."""
+
+    def __init__(self, archive: Archive, perm=None, tile: int = 16384):
+        self.archive = archive
+        self._perm = perm
+        self._tile = tile
+        self._order = None
+
+    @property
+    def order(self) -> Optional[np.ndarray]:
+        if self._perm is None:
+            return None
+        if self._order is None:
+            self._order = self.order_device().cpu().numpy()
+        return self._order
+
+    def order_device(self):
+        import torch
+        if self._perm is None:
+            return None
+        n = self.archive.n
+        out = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
+        L = N.lib()
+        N.check(L.nbzg_order_expand(N.ptr(self._perm), n, self.archive.segment_size,
+                                    N.ptr(out), N.stream_handle()), "order_expand")
+        return out[:n]
+
+
+_STATUS_EXC = {N.NBZG_BOUND_TOO_SMALL: BoundTooSmallError,
+               N.NBZG_CODE_TOO_LONG: EncodeError,
+               N.NBZG_INVALID_CODE: DecodeError,
+               N.NBZG_TRUNCATED: DecodeError,
+               N.NBZG_BAD_STREAM: DecodeError}
+
+
+def _raise_status(status: int, what: str):
+    if status:
+        exc = _STATUS_EXC.get(status, NbzError)
+        raise exc(f"{what}: {N.STATUS_NAMES.get(status, status)}")
+
+
+def _as_mode(mode) -> Mode:
+    if isinstance(mode, Mode):
+        return mode
+    if isinstance(mode, str):
+        if mode in MODE_ALIASES:
+            return MODE_ALIASES[mode]
+        try:
+            return Mode(mode)
+        except ValueError:
+            pass
+    raise ValidationError(f"unknown mode {mode!r}")
+
+
+def _specs(bounds: Bounds) -> List[ErrorBoundSpec]:
+    if isinstance(bounds, Mapping):
+        try:
+            return [bounds[name] for name in FIELD_NAMES]
+        except KeyError as exc:
+            raise ValidationError(f"missing bound for field {exc}") from exc
+    if not isinstance(bounds, ErrorBoundSpec):
+        raise ValidationError("bounds must be an ErrorBoundSpec or a mapping of them")
+    return [bounds] * 6
+
+
+def _align_n(n: int) -> int:
+    return (n + 63) // 64 * 64
+
+
+def device_fields(snapshot: ParticleSnapshot):
+    """The six fields as 16-byte aligned CUDA float32 tensors (H2D for numpy)."""
+    import torch
+    n = snapshot.n
+    fs = list(snapshot.fields())
+    if all(_is_tensor(f) and f.is_cuda for f in fs):
+        out = []
+        for f in fs:
+            if f.data_ptr() % 16:
+                f = f.clone()
+            out.append(f)
+        return out, None
+    stride = _align_n(n)
+    buf = torch.empty(6 * max(stride, 1), dtype=torch.float32, device="cuda")
+    out = []
+    for i, f in enumerate(fs):
+        dst = buf[i * stride:i * stride + n]
+        if n:
+            src = f if _is_tensor(f) else torch.from_numpy(f)
+            dst.copy_(src, non_blocking=True)
+        out.append(dst)
+    return out, buf
+
+
+def compress(snapshot: ParticleSnapshot, mode, bounds: Bounds,
+             settings: Settings = DEFAULT_SETTINGS) -> CompressResult:
+    """pipeline.py:447-526 on the B200: SZ-LV (R-index off) and SZ-LV-PRX
+    (R-index on)."""
+    import torch
+    mode = _as_mode(mode)
+    if mode not in GPU_MODES:
+        raise ValidationError(f"mode {mode.value} is not implemented by the B200 path "
+                              f"(supported: sz-lv, sz-lv-prx)")
+    if mode.is_sorted and settings.rindex_variant is not RIndexVariant.COORDINATE:
+        raise ValidationError("the B200 path implements the coordinate r-index variant only")
+    specs = _specs(bounds)
+    n = snapshot.n
+    L = N.lib()
+    fields, _hold = device_fields(snapshot)
+    sorted_mode = 1 if (mode.is_sorted and n > 0) else 0
+    ic = settings.interval_count
+    if ic > 65536:
+        raise ValidationError("the B200 path supports interval_count <= 65536")
+    S = settings.segment_size
+    if sorted_mode and S > 16384:
+        raise ValidationError("the B200 path supports segment_size <= 16384")
+    ws_bytes = L.nbzg_compress_workspace_size(n, sorted_mode, ic, S)
+    ws = N.POOL.get("compress_ws", ws_bytes)
+    arena_bytes = L.nbzg_compress_arena_bound(n, ic)
+    arena = torch.empty(arena_bytes, dtype=torch.uint8, device="cuda")
+    meta_t = torch.empty(ctypes.sizeof(N.Meta), dtype=torch.uint8, device="cuda")
+    nseg = (n + S - 1) // S if sorted_mode else 0
+    seg_bits = torch.empty(max(nseg, 1), dtype=torch.uint8, device="cuda")
+    perm = torch.empty(max(n, 1), dtype=torch.int16, device="cuda") if sorted_mode else None
+    a = N.CompressArgs()
+    for i in range(6):
+        a.fields[i] = N.ptr(fields[i]) if n else None
+        a.bound_kind[i] = 0 if specs[i].kind is BoundKind.ABSOLUTE else 1
+        a.bound_value[i] = float(specs[i].value)
+    a.n = n
+    a.sorted = sorted_mode
+    a.interval_count = ic
+    a.segment_size = S
+    a.ignored_groups = settings.ignored_groups
+    a.workspace = N.ptr(ws)
+    a.workspace_bytes = ws.numel()
+    a.arena = N.ptr(arena)
+    a.arena_bytes = arena.numel()
+    a.meta = N.ptr(meta_t)
+    a.seg_bits = N.ptr(seg_bits)
+    a.perm = N.ptr(perm) if perm is not None else None
+    N.check(L.nbzg_compress(ctypes.byref(a), N.stream_handle()), "compress")
+    meta = N.Meta.from_buffer_copy(meta_t.cpu().numpy().tobytes())
+    _raise_status(meta.status, "compress")
+    offsets, lengths, kinds = [], [], []
+    for fi in range(6):
+        fm = meta.f[fi]
+        if n == 0 or fm.is_const:
+            offsets.append(None)
+            lengths.append(0)
+        else:
+            offsets.append(int(fm.payload_off))
+            lengths.append(int(fm.payload_len))
+        kinds.append(int(StreamKind.SZ_DQ))
+    dev = _Device(arena[:max(int(meta.arena_used), 1)], offsets, lengths, kinds,
+                  keep=(meta_t,))
+    archive = Archive(
+        mode=mode, n=n, interval_count=ic, segment_size=S,
+        ignored_groups=settings.ignored_groups,
+        rindex_variant=settings.rindex_variant if sorted_mode else None,
+        bounds=tuple(meta.f[i].bound for i in range(6)),
+        constant_mask=meta.mask,
+        constants=tuple(meta.f[i].constant for i in range(6)),
+        seg_bits=seg_bits[:nseg] if sorted_mode else None,
+        device=dev, version=2, device_output=snapshot.on_device)
+    tile = (max(1, 16384 // S) * S) if S < 16384 else S
+    return CompressResult(archive, perm=perm[:n] if perm is not None else None, tile=tile)
+
+
+_KIND_CODE = {StreamKind.SZ_DQ: 3, StreamKind.SZ_FIELD: 0}
+
+
+def decompress(archive: Archive, device: Optional[bool] = None) -> ParticleSnapshot:
+    """pipeline.py:542-604 (SZ branch) on the B200.  Output stays in the
+    compressed (sorted) order, as in the reference.  ``device=True`` returns
+    CUDA tensors (default: follow where the compressed snapshot lived)."""
+    import torch
+    n = archive.n
+    if device is None:
+        device = archive.device_output
+    if n == 0:
+        return ParticleSnapshot.empty()
+    if archive.mode not in GPU_MODES:
+        raise DecodeError(f"mode {archive.mode.value} is not implemented by the B200 path")
+    L = N.lib()
+    stride = _align_n(n)
+    out = torch.empty(6 * stride, dtype=torch.float32, device="cuda")
+    views = [out[i * stride:i * stride + n] for i in range(6)]
+    a = N.DecompressArgs()
+    nf = 0
+    d = archive._dev
+    if d is None:
+        # host payloads (deserialized archive): one H2D of all payloads
+        by_field = {s.field: s for s in archive.streams}
+        blob = bytearray()
+        offs = {}
+        for fi in range(6):
+            if archive.is_constant(fi):
+                continue
+            st = by_field.get(fi)
+            if st is None:
+                raise DecodeError(f"missing stream for field {FIELD_NAMES[fi]}")
+            if st.kind not in _KIND_CODE:
+                raise DecodeError(f"stream kind {int(st.kind)} is not decodable by the B200 path")
+            offs[fi] = (len(blob), len(st.payload), _KIND_CODE[st.kind])
+            blob += st.payload
+            blob += b"\0" * ((-len(blob)) % 16)
+        blob += b"\0" * 32
+        arena = torch.frombuffer(bytearray(blob), dtype=torch.uint8).cuda()
+        d = _Device(arena, [offs[f][0] if f in offs else None for f in range(6)],
+                    [offs[f][1] if f in offs else 0 for f in range(6)],
+                    [StreamKind.SZ_DQ if (f in offs and offs[f][2] == 3) else StreamKind.SZ_FIELD
+                     for f in range(6)])
+        archive._dev = d
+    base = N.ptr(d.arena)
+    for fi in range(6):
+        if archive.is_constant(fi):
+            views[fi].fill_(archive.constants[fi])
+            continue
+        if d.offsets[fi] is None:
+            raise DecodeError(f"missing stream for field {FIELD_NAMES[fi]}")
+        a.payload[nf] = base + d.offsets[fi]
+        a.payload_len[nf] = d.lengths[fi]
+        a.kind[nf] = _KIND_CODE.get(StreamKind(d.kinds[fi]), -1)
+        if a.kind[nf] < 0:
+            raise DecodeError("unsupported stream kind")
+        a.bound[nf] = archive.bounds[fi]
+        if not (archive.bounds[fi] > 0):
+            raise DecodeError(f"field {FIELD_NAMES[fi]}: invalid bound")
+        a.out[nf] = N.ptr(views[fi])
+        nf += 1
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    if nf:
+        ws_bytes = L.nbzg_decompress_workspace_size(n, archive.interval_count, nf)
+        ws = N.POOL.get("decompress_ws", ws_bytes)
+        a.nfields = nf
+        a.n = n
+        a.interval_count = archive.interval_count
+        a.workspace = N.ptr(ws)
+        a.workspace_bytes = ws.numel()
+        a.status = N.ptr(status)
+        rc = L.nbzg_decompress(ctypes.byref(a), N.stream_handle())
+        if rc in (N.NBZG_BAD_ARG, N.NBZG_UNSUPPORTED):
+            raise DecodeError(f"decompress: {N.STATUS_NAMES.get(rc, rc)}")
+        N.check(rc, "decompress")
+    st = int(status.item())
+    if st:
+        raise DecodeError(f"decompress: {N.STATUS_NAMES.get(st, st)}")
+    snap = ParticleSnapshot.__new__(ParticleSnapshot)
+    for i, name in enumerate(FIELD_NAMES):
+        object.__setattr__(snap, name, views[i])
+    return snap if device else snap.numpy()
+
+
+def ratio(archive: Archive, original_bytes: Optional[int] = None) -> Optional[float]:
+    """pipeline.py:607-612."""
+    ob = 24 * archive.n if original_bytes is None else original_bytes
+    if ob == 0:
+        return None
+    return ob / archive.total_bytes()

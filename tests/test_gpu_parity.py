@@ -1,0 +1,382 @@
+"""GPU parity: every CUDA stage and the whole path against the CPU oracle
+(which is itself pinned to the reference, tests/test_oracle_golden.py).
+
+Integer / byte / index work is compared bit-exactly; decoded floats are
+compared bit-exactly against the oracle's decoder AND checked against the
+point-wise error bound.  Run on a B200: pytest -m gpu."""
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_CASES, golden_inputs, load_golden, sha
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import gpu_hooks as H  # noqa: E402
+import paper_1711_03888_b200 as nbz  # noqa: E402
+from paper_1711_03888_b200 import datagen  # noqa: E402
+
+REL4 = nbz.ErrorBoundSpec.relative(1e-4)
+
+
+@pytest.fixture(scope="module")
+def O(oracle_lib):
+    return oracle_lib
+
+
+# ---------------------------------------------------------------- stages
+
+def test_minmax6(rng):
+    fields = [rng.normal(0, 100, 100003).astype(np.float32) for _ in range(6)]
+    fields[2][5] = -0.0
+    mm = H.minmax6(fields)
+    for f in range(6):
+        assert mm[2 * f] == fields[f].min() and mm[2 * f + 1] == fields[f].max()
+
+
+def test_integerize_matches_oracle(O, rng):
+    for b in (0.0256, 0.05, 1e-3, 0.125, 7.0):
+        x = rng.normal(0, 300, 200000).astype(np.float32)
+        # exact half-integer ties and near-ties of x / 2b
+        t = np.arange(-5000, 5000) + 0.5
+        x[:10000] = (t * 2 * b).astype(np.float32)
+        x[10000:20000] = np.nextafter(x[:10000], np.float32(np.inf))
+        got, st = H.integerize(x, b)
+        assert st == 0
+        assert np.array_equal(got, O.integerize(x, b)), b
+    got, st = H.integerize(np.array([1e30, 1.0], np.float32), 1e-12)
+    assert st == nbz_status("bound too small")
+
+
+def nbz_status(name):
+    from paper_1711_03888_b200 import _native as N
+    return {v: k for k, v in N.STATUS_NAMES.items()}[name]
+
+
+@pytest.mark.parametrize("case", ["hacc34", "amdf40k", "sweep_hacc20", "sweep_amdf8k", "tiny3",
+                                  "const2", "noise20k"])
+def test_rindex_keys_and_order(O, case):
+    g = load_golden(case)
+    fields = golden_inputs(g)
+    n = fields[0].size
+    for tag in g["tags"]:
+        t = str(tag)
+        if not t.startswith("sz-lv-prx"):
+            continue
+        bounds = g[f"{t}|bounds"]
+        mask = int(g[f"{t}|mask"])
+        b3 = [0.0 if mask & (1 << i) else bounds[i] for i in range(3)]
+        keys, bits, st = H.rindex_keys(fields[:3], b3)
+        assert st == 0
+        cols = [O.integerize(fields[i], bounds[i]) if not mask & (1 << i)
+                else np.zeros(n, np.int64) for i in range(3)]
+        okeys, obits, _ = O.build_rindex(cols, 16384)
+        assert np.array_equal(keys, okeys), t
+        assert np.array_equal(bits, obits), t
+        if f"{t}|keys_sha" in g:
+            assert sha(keys) == str(g[f"{t}|keys_sha"])
+        order = H.prx_order(keys, 16384, bits, 6)
+        assert np.array_equal(order, O.prx_order(okeys, 16384, obits, 6)), t
+        for k in (0, 2, 4, 8):
+            assert np.array_equal(H.prx_order(keys, 16384, bits, k),
+                                  O.prx_order(okeys, 16384, obits, k)), (t, k)
+
+
+def test_huffman_lengths_kats(O):
+    k = load_golden("kats")
+    for i in (1, 2, 3):
+        got, st = H.huffman_lengths(k[f"hl_c{i}"])
+        assert st == 0
+        assert np.array_equal(got.astype(np.int64), k[f"hl_l{i}"]), i
+
+
+def test_huffman_lengths_random(O, rng):
+    for kk in (2, 3, 17, 300, 5000, 16384, 20000, 65536):
+        c = np.sort(rng.integers(1, 10 ** 5, kk)).astype(np.int64)
+        got, st = H.huffman_lengths(c)
+        assert st == 0
+        assert np.array_equal(got.astype(np.int64), O.huffman_lengths(c)), kk
+    # heavy ties (leaf-wins-ties rule matters)
+    c = np.sort(np.repeat(np.arange(1, 40), 97)).astype(np.int64)
+    got, _ = H.huffman_lengths(c)
+    assert np.array_equal(got.astype(np.int64), O.huffman_lengths(c))
+
+
+def test_codebook_matches_oracle(O, rng):
+    for nsym, spread in ((200, 30.0), (5000, 900.0), (30000, 9000.0)):
+        codes = np.clip(np.rint(rng.normal(32769, spread, 400000)), 1, 65535).astype(np.int64)
+        codes[::997] = 0
+        hist = np.bincount(codes, minlength=65536)
+        sym, lens, lut, m = H.huffman_codebook(hist)
+        osym, olens = O.huffman_build(hist)
+        assert np.array_equal(sym, osym)
+        assert np.array_equal(lens, olens)
+        tabs = O.huffman_tables(osym, olens)
+        assert np.array_equal(lut[osym], tabs["enc_packed"][osym])
+        assert m.f[0].total_bits == int((hist[osym] * olens.astype(np.int64)).sum())
+        assert m.f[0].n_esc == hist[0]
+
+
+def test_huff_encode_bytes_match_reference_kat(O):
+    k = load_golden("kats")
+    syms = k["hb_syms_in"].astype(np.uint16)
+    tabs = O.huffman_tables(k["hb_symbols"], k["hb_lengths"])
+    lut = np.zeros(65536, np.uint64)
+    lut[:tabs["enc_packed"].size] = tabs["enc_packed"]
+    data, bits, _ = H.huff_encode(syms, lut)
+    assert bits == int(k["hb_bits"])
+    assert data == k["hb_bytes"].tobytes()
+
+
+def test_huff_encode_multichunk(O, rng):
+    for n in (16383, 16384, 16385, 100000, 333333):
+        codes = np.clip(np.rint(rng.normal(32769, 40, n)), 1, 65535).astype(np.int64)
+        codes[::61] = rng.integers(1, 65535, codes[::61].size)
+        hist = np.bincount(codes, minlength=65536)
+        osym, olens = O.huffman_build(hist)
+        tabs = O.huffman_tables(osym, olens)
+        lut = np.zeros(65536, np.uint64)
+        lut[:tabs["enc_packed"].size] = tabs["enc_packed"]
+        data, bits, cb = H.huff_encode(codes.astype(np.uint16), lut)
+        odata, obits = O.huff_encode(codes.astype(np.int32), tabs["enc_packed"])
+        assert bits == obits and data == odata, n
+        lens = (tabs["enc_packed"][codes] >> np.uint64(57)).astype(np.int64)
+        want = [int(lens[i:i + 16384].sum()) for i in range(0, n, 16384)]
+        assert list(cb) == want
+
+
+def test_crc64(O, rng):
+    assert H.crc64(b"123456789") == 0x995DC9BBDF1939FA
+    for n in (0, 1, 7, 1023, 1024, 1025, 100003, 3 << 20):
+        b = rng.integers(0, 256, n).astype(np.uint8).tobytes()
+        assert H.crc64(b) == O.crc64(b), n
+
+
+# ---------------------------------------------------------------- whole path
+
+@pytest.mark.parametrize("case", GOLDEN_CASES)
+def test_archive_byte_identical_to_oracle(O, case):
+    """The GPU v2 archive equals the oracle's v2 archive byte for byte:
+    bounds, seg bits, permutation, dual-quant codes, Huffman tables, chunk
+    index, bitstream, escapes, CRCs, header."""
+    g = load_golden(case)
+    fields = golden_inputs(g)
+    snap = nbz.ParticleSnapshot(*fields)
+    for tag in g["tags"]:
+        mode, eb = str(tag).split("|")
+        res = nbz.compress(snap, mode, nbz.ErrorBoundSpec.relative(float(eb)))
+        ref = O.compress(fields, mode, "rel", float(eb), fmt=2)
+        assert tuple(res.archive.bounds) == tuple(ref["bounds"]), tag
+        assert res.archive.constant_mask == ref["mask"]
+        if mode == "sz-lv-prx" and snap.n:
+            assert np.array_equal(res.archive.seg_bits, ref["seg_bits"]), tag
+            assert np.array_equal(res.order, ref["order"]), tag
+            if f"{tag}|order_sha" in g:
+                assert sha(res.order.astype(np.int64)) == str(g[f"{tag}|order_sha"])
+        for st in res.archive.streams:
+            assert st.payload == ref["payloads"][st.field], (tag, st.field)
+        wire = res.archive.serialized()
+        assert wire == ref["wire"], tag
+        assert res.archive.total_bytes() == len(wire)
+        # ratio within 0.5% of the REFERENCE's (golden) ratio
+        if snap.n >= 1000:
+            r = nbz.ratio(res.archive)
+            assert abs(r / float(g[f"{tag}|ratio"]) - 1) < 0.005, (tag, r)
+
+
+@pytest.mark.parametrize("case", GOLDEN_CASES)
+def test_decompress_matches_oracle_and_bound(O, case):
+    g = load_golden(case)
+    fields = golden_inputs(g)
+    snap = nbz.ParticleSnapshot(*fields)
+    for tag in g["tags"]:
+        mode, eb = str(tag).split("|")
+        res = nbz.compress(snap, mode, nbz.ErrorBoundSpec.relative(float(eb)))
+        recon = nbz.decompress(res.archive)
+        ref = O.compress(fields, mode, "rel", float(eb), fmt=2)
+        odec = O.decompress(ref["wire"])
+        work = fields if res.order is None else [f[res.order] for f in fields]
+        for fi in range(6):
+            got = np.asarray(recon.field(fi))
+            assert np.array_equal(got, odec[fi]), (tag, fi)
+            err = np.abs(work[fi].astype(np.float64) - got.astype(np.float64))
+            lim = res.archive.bounds[fi] if not res.archive.is_constant(fi) else 0.0
+            assert float(err.max(initial=0.0)) <= lim, (tag, fi)
+
+
+@pytest.mark.parametrize("case", ["hacc34", "amdf40k", "sweep_hacc20", "const2", "noise20k"])
+def test_reference_v1_archives_decode(O, case):
+    """Archives written by the reference (v1, exact chain) decode on the GPU
+    to exactly the reference's decompressed values (golden SHA-256)."""
+    from paper_1711_03888_b200 import io as nio
+    g = load_golden(case)
+    fields = golden_inputs(g)
+    for tag in g["tags"]:
+        mode, eb = str(tag).split("|")
+        wire = O.compress(fields, mode, "rel", float(eb), fmt=1)["wire"]
+        assert sha(wire) == str(g[f"{tag}|wire_sha"])  # this IS the reference's archive
+        ar = nio.deserialize_archive(wire)
+        assert ar.version == 1
+        recon = nbz.decompress(ar)
+        for fi in range(6):
+            key = f"{tag}|recon{fi}_sha"
+            if key in g:
+                assert sha(np.asarray(recon.field(fi))) == str(g[key]), (tag, fi)
+        assert nio.serialize_archive(ar) == wire
+
+
+def test_wire_round_trip_and_device_input(O):
+    from paper_1711_03888_b200 import io as nio
+    fields = datagen.small_amdf(70000)
+    snap = nbz.ParticleSnapshot(*fields)
+    res = nbz.compress(snap, "sz-lv-prx", REL4)
+    wire = res.archive.serialized()
+    again = nio.deserialize_archive(wire)
+    assert nio.serialize_archive(again) == wire
+    a = nbz.decompress(res.archive)
+    b = nbz.decompress(again)
+    for x, y in zip(a.fields(), b.fields()):
+        assert np.array_equal(np.asarray(x), np.asarray(y))
+    # in-situ: CUDA tensors in, CUDA tensors out, same bytes
+    dsnap = nbz.ParticleSnapshot(*[torch.from_numpy(f).cuda() for f in fields])
+    dres = nbz.compress(dsnap, "sz-lv-prx", REL4)
+    assert dres.archive.serialized() == wire
+    drec = nbz.decompress(dres.archive)
+    assert drec.on_device
+    assert np.array_equal(drec.xx.cpu().numpy(), np.asarray(a.xx))
+
+
+# ---------------------------------------------------------------- edge cases
+
+def test_empty_snapshot():
+    res = nbz.compress(nbz.ParticleSnapshot.empty(), "sz-lv-prx", REL4)
+    assert res.archive.n == 0 and res.archive.streams == ()
+    assert nbz.ratio(res.archive) is None
+    out = nbz.decompress(res.archive)
+    assert out.n == 0
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 8, 9, 100, 16383, 16385])
+def test_tiny_and_ragged(O, rng, n):
+    fields = [rng.uniform(0, 100, n).astype(np.float32) for _ in range(3)]
+    fields += [rng.normal(0, 300, n).astype(np.float32) for _ in range(3)]
+    snap = nbz.ParticleSnapshot(*fields)
+    for mode in ("sz-lv", "sz-lv-prx"):
+        res = nbz.compress(snap, mode, REL4)
+        ref = O.compress(fields, mode, "rel", 1e-4, fmt=2)
+        assert res.archive.serialized() == ref["wire"], (mode, n)
+        rec = nbz.decompress(res.archive)
+        odec = O.decompress(ref["wire"])
+        for fi in range(6):
+            assert np.array_equal(np.asarray(rec.field(fi)), odec[fi])
+
+
+def test_constant_fields_and_absolute_bounds(O, rng):
+    n = 40000
+    fields = [rng.uniform(0, 100, n).astype(np.float32) for _ in range(6)]
+    fields[0][:] = 3.25
+    fields[5][:] = -1.0
+    snap = nbz.ParticleSnapshot(*fields)
+    bounds = {name: nbz.ErrorBoundSpec.absolute(0.01) for name in nbz.FIELD_NAMES}
+    for mode in ("sz-lv", "sz-lv-prx"):
+        res = nbz.compress(snap, mode, bounds)
+        assert res.archive.constant_mask == 0b100001
+        ref = O.compress(fields, mode, "abs", 0.01, fmt=2)
+        assert res.archive.serialized() == ref["wire"]
+        rec = nbz.decompress(res.archive)
+        assert np.all(np.asarray(rec.xx) == np.float32(3.25))
+
+
+def test_escape_heavy_and_tight_bounds(O, rng):
+    n = 50000
+    fields = [(rng.standard_cauchy(n) * 50).astype(np.float32) for _ in range(6)]
+    snap = nbz.ParticleSnapshot(*fields)
+    for eb in (1e-4, 1e-6, 1e-7):
+        for mode in ("sz-lv", "sz-lv-prx"):
+            res = nbz.compress(snap, mode, nbz.ErrorBoundSpec.relative(eb))
+            ref = O.compress(fields, mode, "rel", eb, fmt=2)
+            assert res.archive.serialized() == ref["wire"], (eb, mode)
+            rec = nbz.decompress(res.archive)
+            work = fields if res.order is None else [f[res.order] for f in fields]
+            for fi in range(6):
+                err = np.abs(work[fi].astype(np.float64) - np.asarray(rec.field(fi), np.float64))
+                assert float(err.max()) <= res.archive.bounds[fi]
+
+
+def test_bound_too_small_raises():
+    x = np.array([1e30, -1e30, 5.0, 7.0], np.float32)
+    snap = nbz.ParticleSnapshot(x, x, x, x, x, x)
+    with pytest.raises(nbz.BoundTooSmallError):
+        nbz.compress(snap, "sz-lv-prx", nbz.ErrorBoundSpec.absolute(1e-30))
+
+
+def test_unsupported_modes_raise():
+    snap = nbz.ParticleSnapshot(*datagen.small_hacc(5))
+    for mode in ("sz-lcf", "cpc2000", "sz-cpc2000"):
+        with pytest.raises(nbz.ValidationError):
+            nbz.compress(snap, mode, REL4)
+
+
+def test_corrupt_archives_rejected():
+    from paper_1711_03888_b200 import io as nio
+    snap = nbz.ParticleSnapshot(*datagen.small_hacc(20))
+    wire = nbz.compress(snap, "sz-lv-prx", REL4).archive.serialized()
+    with pytest.raises(nbz.ArchiveError):
+        nio.deserialize_archive(wire[:-1])
+    with pytest.raises(nbz.ArchiveError):
+        nio.deserialize_archive(b"XXXX" + wire[4:])
+    rng = np.random.default_rng(5)
+    for pos in rng.integers(0, len(wire), 40):
+        bad = bytearray(wire)
+        bad[pos] ^= 0x5A
+        try:
+            ar = nio.deserialize_archive(bytes(bad))
+        except nbz.ArchiveError:
+            continue
+        nbz.decompress(ar)  # only reachable when the flip hit a CRC-neutral spot
+
+
+def test_corrupt_payloads_fail_cleanly():
+    """Bypass the CRC: hand-corrupted payloads must raise DecodeError (or
+    decode to something), never hang or fault."""
+    snap = nbz.ParticleSnapshot(*datagen.small_amdf(40000))
+    res = nbz.compress(snap, "sz-lv", REL4)
+    streams = res.archive.streams
+    rng = np.random.default_rng(11)
+    for trial in range(12):
+        st = streams[trial % len(streams)]
+        p = bytearray(st.payload)
+        for pos in rng.integers(0, len(p), 3):
+            p[pos] ^= int(rng.integers(1, 256))
+        ar = nbz.Archive(res.archive.mode, res.archive.n, res.archive.interval_count,
+                         res.archive.segment_size, res.archive.ignored_groups, None,
+                         res.archive.bounds, res.archive.constant_mask, res.archive.constants,
+                         streams=tuple(nbz.Stream(s.kind, s.field, bytes(p) if s is st else
+                                                  s.payload) for s in streams))
+        try:
+            nbz.decompress(ar)
+        except nbz.DecodeError:
+            pass
+    torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------- larger sizes
+
+@pytest.mark.parametrize("spec,mode", [("C1", "sz-lv"), ("C1", "sz-lv-prx"),
+                                       ("C0", "sz-lv-prx")])
+def test_config_scale_parity(O, spec, mode):
+    """BASELINE configs 0 and 1 at full size: byte-identical archives."""
+    fields = datagen.generate(spec)
+    snap = nbz.ParticleSnapshot(*fields)
+    res = nbz.compress(snap, mode, REL4)
+    ref = O.compress(fields, mode, "rel", 1e-4, fmt=2)
+    assert res.archive.serialized() == ref["wire"]
+    rec = nbz.decompress(res.archive, device=True)
+    work = fields if res.order is None else [f[res.order] for f in fields]
+    for fi in range(6):
+        err = (torch.from_numpy(work[fi]).cuda().double() - rec.field(fi).double()).abs().max()
+        assert float(err) <= res.archive.bounds[fi]

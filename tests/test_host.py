@@ -1,0 +1,98 @@
+"""CPU-only checks of the host side: the C-ABI library loads and exports
+every symbol include/nbzg.h declares (no compute calls without a GPU), the
+API objects validate like the reference's, and the generators match
+BASELINE.json's descriptions."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+import paper_1711_03888_b200 as nbz
+from paper_1711_03888_b200 import _native as N
+from paper_1711_03888_b200 import datagen
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "nbzg.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:const char \*\s*|size_t\s+|int\s+)(nbzg_\w+)\(", src, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = N.load_library(require_cuda=False)
+    names = header_functions()
+    assert len(names) >= 15
+    for name in names:
+        assert hasattr(L, name), name
+    assert set(N.EXPORTED) <= set(names)
+    assert L.nbzg_version().decode().startswith("nbzg")
+
+
+def test_size_queries_without_gpu():
+    L = N.load_library(require_cuda=False)
+    ws = L.nbzg_compress_workspace_size(1 << 20, 1, 65536, 16384)
+    assert ws > 6 * 2 * (1 << 20)
+    assert L.nbzg_compress_arena_bound(1 << 20, 65536) > 6 * 4 * (1 << 20)
+    assert L.nbzg_decompress_workspace_size(1 << 20, 65536, 6) > 0
+    assert L.nbzg_crc64_workspace_size(1 << 20) > 0
+
+
+def test_settings_validation_matches_reference():
+    with pytest.raises(nbz.ValidationError):
+        nbz.Settings(segment_size=0)
+    with pytest.raises(nbz.ValidationError):
+        nbz.Settings(ignored_groups=-1)
+    with pytest.raises(nbz.ValidationError):
+        nbz.Settings(interval_count=3)
+    s = nbz.Settings()
+    assert (s.interval_count, s.segment_size, s.ignored_groups) == (65536, 16384, 6)
+
+
+def test_modes_and_aliases():
+    assert nbz.Mode("sz-lv-prx").uid == 2 and nbz.Mode.SZ_LV.uid == 1
+    assert nbz.MODE_ALIASES["best-tradeoff"] is nbz.Mode.SZ_LV_PRX
+    assert nbz.Mode.from_uid(2) is nbz.Mode.SZ_LV_PRX
+    with pytest.raises(nbz.DecodeError):
+        nbz.Mode.from_uid(9)
+
+
+def test_snapshot_validation():
+    with pytest.raises(nbz.ValidationError):
+        nbz.ParticleSnapshot(*[np.zeros((2, 2))] * 6)
+    with pytest.raises(nbz.ValidationError):
+        x = np.zeros(3, np.float32)
+        nbz.ParticleSnapshot(x, x, x, x, x, np.array([1, np.nan, 2], np.float32))
+    with pytest.raises(nbz.ValidationError):
+        nbz.ParticleSnapshot(*([np.zeros(3)] * 5 + [np.zeros(4)]))
+    with pytest.raises(nbz.ValidationError):
+        nbz.ErrorBoundSpec.relative(0.0)
+    s = nbz.ParticleSnapshot(*[np.arange(4, dtype=np.float64)] * 6)
+    assert s.xx.dtype == np.float32 and s.n == 4
+
+
+def test_generators_follow_baseline_configs():
+    f = datagen.generate("C0")
+    assert f[0].size == 1_000_000 and all(a.dtype == np.float32 for a in f)
+    assert 0 <= f[0].min() and f[0].max() <= 256
+    lag = [datagen.lag1(a) for a in f]
+    assert lag[0] > 0.96 and lag[1] > 0.96 and lag[2] > 0.93     # lattice order
+    assert all(abs(v - 0.92) < 0.01 for v in lag[3:])            # AR(1) rho = 0.92
+    # any contiguous range is reproducible on its own (multi-GPU shards)
+    g = datagen.generate("C0", 300000, 700000)
+    assert all(np.array_equal(a[300000:700000], b) for a, b in zip(f, g))
+    a = datagen.generate(datagen.AmdfSpec(1 << 18))
+    assert all(0 <= x.min() and x.max() < 100 for x in a[:3])
+    assert all(abs(datagen.lag1(v)) < 0.02 for v in a[3:])
+
+
+def test_no_oracle_import_in_product():
+    pkg = os.path.join(ROOT, "paper_1711_03888_b200")
+    for dirpath, _dirs, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, fn)).read()
+                assert "import oracle" not in src and "from oracle" not in src, fn
+                assert "liboracle" not in src, fn
