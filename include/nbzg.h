@@ -156,7 +156,7 @@ int nbzg_order_expand(const uint16_t *perm, int64_t n, int64_t segment_size, int
 
 /* K.huffman_lengths (_kernels.py:204-238): two-queue code lengths of k
  * ascending counts (leaf wins ties); single symbol -> length 1.  workspace:
- * 16*k bytes (used when k > 16384). */
+ * 12 * next_pow2(k) bytes (used when k > 16384). */
 int nbzg_huffman_lengths(const uint32_t *sorted_counts, int64_t k, uint8_t *lengths,
                          void *workspace, size_t workspace_bytes, uint32_t *status_dev,
                          void *stream);

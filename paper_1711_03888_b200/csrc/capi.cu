@@ -256,7 +256,9 @@ int nbzg_order_expand(const uint16_t* perm, int64_t n, int64_t segment_size, int
 int nbzg_huffman_lengths(const uint32_t* sorted_counts, int64_t k, uint8_t* lengths,
                          void* workspace, size_t workspace_bytes, uint32_t* status_dev,
                          void* stream) {
-  if (k > 16384 && workspace_bytes < 16 * (size_t)k) return NBZG_BAD_ARG;
+  size_t np2 = 1;
+  while ((int64_t)np2 < k) np2 <<= 1;
+  if (k > 16384 && workspace_bytes < 12 * np2) return NBZG_BAD_ARG;
   return launch_huffman_lengths(sorted_counts, k, lengths, reinterpret_cast<uint32_t*>(workspace),
                                 status_dev, reinterpret_cast<cudaStream_t>(stream));
 }

@@ -72,7 +72,8 @@ def huffman_lengths(sorted_counts):
     c = _dev(np.asarray(sorted_counts, np.uint32).view(np.int32))
     k = c.numel()
     out = torch.zeros(k, dtype=torch.uint8, device="cuda")
-    ws = torch.zeros(16 * k + 64, dtype=torch.uint8, device="cuda")
+    np2 = 1 << max(0, (k - 1).bit_length())
+    ws = torch.zeros(12 * np2 + 64, dtype=torch.uint8, device="cuda")
     st = torch.zeros(1, dtype=torch.int32, device="cuda")
     N.check(L.nbzg_huffman_lengths(N.ptr(c), k, N.ptr(out), N.ptr(ws), ws.numel(), N.ptr(st),
                                    N.stream_handle()), "huffman_lengths")
