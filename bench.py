@@ -1,0 +1,449 @@
+#!/usr/bin/env python3
+"""bench.py -- BASELINE.json's metric on B200.
+
+Metric: compress/decompress GB/s per 6-field fp32 snapshot at eb_rel = 1e-4
+(input-referenced, 24 B/particle, 1 GB = 1e9 B, the reference's definition,
+pkg/src/nbz/metrics.py:100-110), plus ratio and %HBM roofline.
+
+One STEP = compress + decompress of the resident snapshot through the public
+API (nbz.compress -> nbz.decompress, device-resident input and output).
+``value`` is the round-trip rate 24*n_total / step time; the compress and
+decompress rates are reported beside it.
+
+Workload at N=1: BASELINE config 2, the 640^3 HACC-like snapshot
+(262,144,000 particles, 6.29 GB), mode sz-lv-prx (R-index on).  At N>1 each
+rank compresses its own 640^3 x-slab of a (640N) x 640 x 640 lattice
+(contiguous particle-range shards, weak scaling); global bounds come from an
+NCCL all-gather of per-shard min/max and the per-shard archive sizes are
+all-gathered after compress -- the only collectives.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "compress/decompress GB/s per 6-field fp32 snapshot, eb_rel=1e-4; ratio; %HBM peak"
+SIDE = 640  # C2: 640^3 per GPU
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md "clocks" line)
+# ----------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------
+# distributed plumbing
+# ----------------------------------------------------------------------
+def dist_init(n_gpus):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def allgather_f64(vals, world):
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return np.asarray(vals, np.float64).reshape(1, -1)
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return torch.stack(out).cpu().numpy()
+
+
+def reduce_max(v, world):
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return float(v)
+    t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+        torch.cuda.synchronize()
+
+
+# ----------------------------------------------------------------------
+# CPU oracle (reference algorithm, C port) -- baseline and reference arm
+# ----------------------------------------------------------------------
+def cpu_round_trip(fields, mode, eb, threads):
+    import oracle
+    t0 = time.perf_counter()
+    oracle.compress_shards(fields, mode, eb, nshards=threads, nthreads=threads, fmt=1,
+                           decompress_too=True)
+    return time.perf_counter() - t0
+
+
+def cpu_sample(spec, m):
+    from paper_1711_03888_b200 import datagen
+    return datagen.generate(spec, 0, m)
+
+
+def cpu_baseline(spec, mode, eb, budget_s=12.0):
+    """Reference algorithm (oracle C port, exact chain = the reference's
+    SZ_FIELD path) on the host's cores over a bounded prefix sample."""
+    import oracle
+    oracle.build()
+    threads = os.cpu_count() or 1
+    m = 1 << 21
+    fields = cpu_sample(spec, m)
+    cpu_round_trip(fields, mode, eb, threads)  # warm
+    t = cpu_round_trip(fields, mode, eb, threads)
+    target = int(m * budget_s / 2 / max(t, 1e-3))
+    m2 = int(min(max(m, target), 1 << 26, spec.n))
+    m2 = (m2 // 16384) * 16384 or m
+    if m2 != m:
+        fields = cpu_sample(spec, m2)
+        m = m2
+    t = min(cpu_round_trip(fields, mode, eb, threads) for _ in range(2))
+    return {"value": 24.0 * m / t / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": f"first {m} particles of the {spec.lattice[0]}x{spec.lattice[1]}x"
+                      f"{spec.lattice[2]} HACC-like workload, {mode} eb_rel {eb}, compress+"
+                      f"decompress round trip, {threads} threads x contiguous shards "
+                      f"(oracle/nbz_oracle.c, the reference's exact SZ-LV chain), best of 2"}
+
+
+def run_reference(args):
+    """--impl reference: the reference's algorithm on the host CPU cores
+    (oracle/ C port; the reference itself is a Python+numba package that
+    cannot travel to the GPU box)."""
+    import oracle
+    from paper_1711_03888_b200 import datagen
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    oracle.build()
+    spec = datagen.HaccSpec((SIDE * max(1, args.gpus), SIDE, SIDE), 2.5)
+    threads = os.cpu_count() or 1
+    m = 1 << 22
+    fields = cpu_sample(spec, m)
+    t = cpu_round_trip(fields, args.mode, args.eb, threads)
+    # size each step to ~3 s of CPU work so K+W steps finish in minutes
+    m2 = int(min(max(m, m * 3.0 / max(t, 1e-3)), 1 << 26))
+    m2 = (m2 // 16384) * 16384
+    if m2 > m:
+        fields = cpu_sample(spec, m2)
+        m = m2
+    for _ in range(args.warmup):
+        cpu_round_trip(fields, args.mode, args.eb, threads)
+    ts = [cpu_round_trip(fields, args.mode, args.eb, threads) for _ in range(args.steps)]
+    tot = sum(ts)
+    value = 24.0 * m * args.steps / tot / 1e9
+    sample = (f"first {m} particles of the C2 HACC-like workload per step, {args.mode} eb_rel "
+              f"{args.eb}, compress+decompress, {threads} threads")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded HACC-like generator)",
+            "config": {"workload": "C2 HACC-like 640^3 per GPU (bounded CPU sample per step)",
+                       "mode": args.mode, "eb_rel": args.eb},
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------
+# the B200 arm
+# ----------------------------------------------------------------------
+ALGO_BYTES = {  # algorithmic bytes per particle per launch
+    "minmax6": lambda n, S: 24 * n,
+    "rindex_sort": lambda n, S: 14 * n,
+    "quantize": lambda n, S: 38 * n,
+    "encode": lambda n, S: 12 * n + S,
+    "dq_decode": lambda n, S: S + 24 * n,
+}
+
+
+def run_b200(args):
+    import torch
+
+    import paper_1711_03888_b200 as nbz
+    from paper_1711_03888_b200 import _native as N
+    from paper_1711_03888_b200 import datagen
+
+    rank, world, local = dist_init(args.gpus)
+    N.lib()
+    n = SIDE ** 3 if args.n is None else args.n
+    spec = datagen.HaccSpec((SIDE * world, SIDE, SIDE), 2.5)
+    p0, p1 = rank * n, (rank + 1) * n
+    # pinned host snapshot (the e2e leg reads it from here)
+    host_t = [torch.empty(n, dtype=torch.float32, pin_memory=True) for _ in range(6)]
+    host = [t.numpy() for t in host_t]
+    tg = time.perf_counter()
+    datagen.generate(spec, p0, p1, out=host)
+    gen_s = time.perf_counter() - tg
+    dev = [t.cuda(non_blocking=True) for t in host_t]
+    torch.cuda.synchronize()
+    snap = nbz.ParticleSnapshot(*dev)
+
+    # global bounds: all-gather of per-shard min/max (collective 1)
+    mm = []
+    for f in dev:
+        lo, hi = torch.aminmax(f)
+        mm += [float(lo), float(hi)]
+    g = allgather_f64(mm, world)
+    if world == 1:
+        bounds = nbz.ErrorBoundSpec.relative(args.eb)
+    else:
+        bounds = {}
+        for i, name in enumerate(nbz.FIELD_NAMES):
+            rng = float(g[:, 2 * i + 1].max()) - float(g[:, 2 * i].min())
+            bounds[name] = nbz.ErrorBoundSpec.absolute(args.eb * rng if rng > 0 else 1.0)
+
+    def step(record=None):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = nbz.compress(snap, args.mode, bounds)
+        sizes = allgather_f64([float(res.archive.total_bytes())], world)  # collective 2
+        e1.record()
+        out = nbz.decompress(res.archive, device=True)
+        e2.record()
+        if record is not None:
+            record.append((e0, e1, e2, res, sizes))
+        return res, out
+
+    for _ in range(args.warmup):
+        step()
+    barrier(world)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    N.trace_enable(True)
+    lc0 = N.launch_count()
+    rec = []
+    barrier(world)
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record()
+    for _ in range(args.steps):
+        step(rec)
+    t_end.record()
+    barrier(world)
+    launches = N.launch_count() - lc0
+    trace = N.trace_read()
+    N.trace_enable(False)
+    clk = clocks.stop()
+    total_ms = reduce_max(t_start.elapsed_time(t_end), world)
+    tc = reduce_max(sum(r[0].elapsed_time(r[1]) for r in rec) / args.steps, world)
+    td = reduce_max(sum(r[1].elapsed_time(r[2]) for r in rec) / args.steps, world)
+    ms_step = total_ms / args.steps
+    last = rec[-1]
+    S_local = last[3].archive.total_bytes()
+    S_total = float(last[4].sum())
+    n_total = n * world
+    hbm, peak_kind = peaks()
+
+    # per-kernel averages from the live CUDA-event trace
+    kern = {}
+    for name, ms in trace:
+        kern.setdefault(name, []).append(ms)
+    kavg = {k: sum(v) / args.steps for k, v in kern.items()}
+    dominant = max((k for k in kavg if k in ALGO_BYTES), key=lambda k: kavg[k])
+    algo = ALGO_BYTES[dominant](n, S_local)
+    achieved = algo / (kavg[dominant] * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(dominant)
+        except Exception:
+            traffic = None
+    bc = 24 * n + S_local
+    roof_step = {"compress": {"achieved": bc / (tc * 1e-3) / 1e9, "frac": bc / (tc * 1e-3) / 1e9 / hbm},
+                 "decompress": {"achieved": bc / (td * 1e-3) / 1e9,
+                                "frac": bc / (td * 1e-3) / 1e9 / hbm},
+                 "unit": "GB/s", "bytes": "24n + S per direction (SURVEY.md 8d)",
+                 "peak": hbm}
+
+    # ---- e2e: host buffers through the public API, H2D/D2H inside the region
+    e2e = None
+    if args.e2e_steps > 0:
+        from paper_1711_03888_b200 import io as nio
+        hsnap = nbz.ParticleSnapshot(*host)
+
+        def e2e_step():
+            res = nbz.compress(hsnap, args.mode, bounds)
+            wire = res.archive.serialized()
+            ar = nio.deserialize_archive(wire)
+            out = nbz.decompress(ar, device=False)
+            return len(wire), out
+
+        e2e_step()
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            wl, _o = e2e_step()
+        torch.cuda.synchronize()
+        dt = reduce_max((time.perf_counter() - t0) / args.e2e_steps, world)
+        e2e = {"value": 24.0 * n_total / dt / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": 24 * n + wl, "d2h_bytes_per_step": wl + 24 * n,
+               "steps": args.e2e_steps,
+               "path": "numpy (pinned) -> compress -> serialized() -> deserialize_archive -> "
+                       "decompress -> numpy; wall clock, max over ranks"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(datagen.HaccSpec((SIDE, SIDE, SIDE), 2.5), args.mode, args.eb)
+        except Exception as exc:  # never fail the bench line on the baseline leg
+            cpu = {"value": None, "error": str(exc)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": 24.0 * n_total / (ms_step * 1e-3) / 1e9,
+            "unit": "GB/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (seeded HACC-like generator, BASELINE config 2)",
+            "config": {"workload": f"C2: HACC-like {SIDE}^3 = {n} particles per GPU "
+                                   f"(6.29 GB), box 1600, {args.mode}",
+                       "n_per_gpu": n, "mode": args.mode, "eb_rel": args.eb,
+                       "step": "compress + decompress, device-resident in/out",
+                       "l2": "inputs (6.3 GB/GPU) exceed the 126 MB L2; no flush needed",
+                       "parallelism": f"{world} contiguous shard(s), weak scaling"},
+            "compress_gbps": 24.0 * n_total / (tc * 1e-3) / 1e9,
+            "decompress_gbps": 24.0 * n_total / (td * 1e-3) / 1e9,
+            "compress_ms": tc, "decompress_ms": td,
+            "ratio": 24.0 * n_total / S_total,
+            "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": hbm,
+                         "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                         "algo_bytes_per_launch": algo, "launch_ms": kavg[dominant],
+                         "peak_kind": peak_kind},
+            "roofline_step": roof_step,
+            "kernels_ms": {k: round(v, 4) for k, v in sorted(kavg.items())},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+            "gen_s": round(gen_s, 1),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--mode", default="sz-lv-prx", choices=["sz-lv", "sz-lv-prx"])
+    ap.add_argument("--eb", type=float, default=1e-4)
+    ap.add_argument("--n", type=int, default=None, help="particles per GPU (default 640^3)")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

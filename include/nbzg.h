@@ -186,9 +186,15 @@ int nbzg_crc64(const uint8_t *data, int64_t n, uint64_t *crc_dev, void *workspac
                size_t workspace_bytes, void *stream);
 size_t nbzg_crc64_workspace_size(int64_t n);
 
-/* library / device info */
+/* library / device info and diagnostics */
 const char *nbzg_version(void);
 int nbzg_device_sm_count(void);
+/* number of kernels this library has launched (process lifetime) */
+unsigned long long nbzg_launch_count(void);
+/* per-stage CUDA-event trace of subsequent compress / decompress calls:
+ * enable (resets), then read (name, ms) intervals (synchronises). */
+int nbzg_trace_enable(int on);
+int nbzg_trace_read(char *names, int name_stride, float *ms, int max);
 
 #ifdef __cplusplus
 }

@@ -37,7 +37,8 @@ EXPORTED = (
     "nbzg_decompress", "nbzg_decompress_workspace_size", "nbzg_minmax6", "nbzg_integerize",
     "nbzg_rindex_keys", "nbzg_prx_order", "nbzg_order_expand", "nbzg_huffman_lengths",
     "nbzg_huffman_codebook", "nbzg_huff_encode", "nbzg_crc64", "nbzg_crc64_workspace_size",
-    "nbzg_version", "nbzg_device_sm_count",
+    "nbzg_version", "nbzg_device_sm_count", "nbzg_launch_count", "nbzg_trace_enable",
+    "nbzg_trace_read",
 )
 
 
@@ -101,6 +102,9 @@ _SIGS = {
     "nbzg_crc64_workspace_size": (c_sz, [c_i64]),
     "nbzg_version": (ctypes.c_char_p, []),
     "nbzg_device_sm_count": (ctypes.c_int, []),
+    "nbzg_launch_count": (ctypes.c_ulonglong, []),
+    "nbzg_trace_enable": (ctypes.c_int, [ctypes.c_int]),
+    "nbzg_trace_read": (ctypes.c_int, [c_p, ctypes.c_int, c_p, ctypes.c_int]),
 }
 
 _lib = None
@@ -149,6 +153,25 @@ def stream_handle():
 
 def ptr(t) -> int:
     return int(t.data_ptr())
+
+
+def launch_count() -> int:
+    return int(load_library().nbzg_launch_count())
+
+
+def trace_enable(on: bool = True) -> None:
+    load_library().nbzg_trace_enable(1 if on else 0)
+
+
+def trace_read(max_entries: int = 65536):
+    """[(stage name, ms)] recorded since trace_enable (synchronises)."""
+    stride = 32
+    names = ctypes.create_string_buffer(stride * max_entries)
+    ms = (ctypes.c_float * max_entries)()
+    cnt = load_library().nbzg_trace_read(names, stride, ms, max_entries)
+    raw = names.raw
+    return [(raw[i * stride:(i + 1) * stride].split(b"\0", 1)[0].decode(), float(ms[i]))
+            for i in range(cnt)]
 
 
 class _Pool:

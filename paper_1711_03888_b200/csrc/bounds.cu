@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(512) minmax6_kernel(Fields6 F, int64_t n, uint
 int launch_minmax6(const float* const* f, int64_t n, uint32_t* mm, cudaStream_t st) {
   Fields6 F;
   for (int i = 0; i < 6; i++) F.p[i] = f[i];
+  count_launch();
   minmax_init_kernel<<<1, 32, 0, st>>>(mm);
   if (n > 0) {
     int64_t nv = (n >> 2);
@@ -81,6 +82,7 @@ int launch_minmax6(const float* const* f, int64_t n, uint32_t* mm, cudaStream_t 
     int cap = sm_count() * 4;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
+    count_launch();
     minmax6_kernel<<<blocks, 512, 0, st>>>(F, n, mm);
   }
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
@@ -143,6 +145,7 @@ int launch_resolve(const Plan& p, cudaStream_t st) {
   }
   a.n = p.n;
   a.nseg = p.nseg;
+  count_launch();
   resolve_kernel<<<1, 32, 0, st>>>(a, p.minmax, p.meta);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }

@@ -1,7 +1,10 @@
 // capi.cu -- the extern "C" boundary (include/nbzg.h): argument validation,
 // workspace carving and kernel sequencing.  No mutable global state beyond
 // one-time cudaFuncSetAttribute calls.
+#include <atomic>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "nbzg_internal.cuh"
 #include "plan.h"
@@ -28,6 +31,33 @@ int launch_crc64(const uint8_t* data, int64_t n, uint64_t* crc_out, void* ws, si
                  cudaStream_t st);
 
 size_t decompress_ws(int nf, int64_t n, int64_t nbins);
+
+// ---- launch counter and event trace (diagnostics for bench.py; the trace is
+// off unless nbzg_trace_enable(1) is called)
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+struct TraceMark {
+  const char* name;
+  cudaEvent_t ev;
+};
+static std::mutex g_tmu;
+static bool g_trace_on = false;
+static std::vector<TraceMark> g_marks;
+static std::vector<cudaEvent_t> g_pool;
+
+void trace_mark(const char* name, cudaStream_t st) {
+  if (!g_trace_on) return;
+  std::lock_guard<std::mutex> lk(g_tmu);
+  if (g_marks.size() == g_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_pool.push_back(e);
+  }
+  cudaEvent_t e = g_pool[g_marks.size()];
+  cudaEventRecord(e, st);
+  g_marks.push_back({name, e});
+}
 
 int sm_count() {
   static int c = 0;
@@ -102,6 +132,32 @@ extern "C" {
 
 const char* nbzg_version(void) { return "nbzg 0.1.0 sm_100a"; }
 
+unsigned long long nbzg_launch_count(void) { return g_launches.load(); }
+
+int nbzg_trace_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_trace_on = on != 0;
+  g_marks.clear();
+  return NBZG_OK;
+}
+
+int nbzg_trace_read(char* names, int name_stride, float* ms, int max) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  if (g_marks.empty()) return 0;
+  cudaEventSynchronize(g_marks.back().ev);
+  int cnt = 0;
+  for (size_t i = 1; i < g_marks.size() && cnt < max; i++) {
+    if (!g_marks[i].name) continue;
+    float t = 0.f;
+    cudaEventElapsedTime(&t, g_marks[i - 1].ev, g_marks[i].ev);
+    std::strncpy(names + (size_t)cnt * name_stride, g_marks[i].name, name_stride - 1);
+    names[(size_t)cnt * name_stride + name_stride - 1] = 0;
+    ms[cnt] = t;
+    cnt++;
+  }
+  return cnt;
+}
+
 int nbzg_device_sm_count(void) { return sm_count(); }
 
 size_t nbzg_compress_workspace_size(int64_t n, int32_t sorted, int64_t interval_count,
@@ -154,14 +210,24 @@ int nbzg_compress(const nbzg_compress_args* a, void* stream) {
   p.arena = a->arena;
   p.arena_bytes = a->arena_bytes;
   int rc;
+  trace_mark(nullptr, st);
   if ((rc = launch_minmax6(p.f, p.n, p.minmax, st))) return rc;
+  trace_mark("minmax6", st);
   if ((rc = launch_resolve(p, st))) return rc;
+  trace_mark("resolve", st);
   if (p.n == 0) return cuda_status();
-  if (p.sorted && (rc = launch_rindex_sort(p, st))) return rc;
+  if (p.sorted) {
+    if ((rc = launch_rindex_sort(p, st))) return rc;
+    trace_mark("rindex_sort", st);
+  }
   if ((rc = launch_quantize(p, st))) return rc;
+  trace_mark("quantize", st);
   if ((rc = launch_codebook(p, st))) return rc;
+  trace_mark("codebook", st);
   if ((rc = launch_layout(p, st))) return rc;
+  trace_mark("layout", st);
   if ((rc = launch_encode(p, st))) return rc;
+  trace_mark("encode", st);
   return cuda_status();
 }
 
@@ -187,6 +253,7 @@ int nbzg_decompress(const nbzg_decompress_args* a, void* stream) {
     f[i].out = a->out[i];
   }
   cudaMemsetAsync(a->status, 0, sizeof(uint32_t), st);
+  trace_mark(nullptr, st);
   return launch_decompress(f, a->nfields, a->n, a->interval_count,
                            a->workspace, a->workspace_bytes, a->status, st);
 }
@@ -198,6 +265,7 @@ int nbzg_minmax6(const float* const* h_fields, int64_t n, float* out12, void* st
   uint32_t* mm = reinterpret_cast<uint32_t*>(out12);
   int rc = launch_minmax6(h_fields, n, mm, st);
   if (rc) return rc;
+  count_launch();
   ord_decode_kernel<<<1, 32, 0, st>>>(mm);  // decode the order-preserving encoding
   return cuda_status();
 }
@@ -225,6 +293,7 @@ int nbzg_integerize(const float* x, int64_t n, double bound, int64_t* ints, uint
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   double twob = 2.0 * bound, inv = 1.0 / twob;
   if (n > 0)
+    count_launch();
     integerize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, n, twob, inv, (float)inv,
                                                                    ints, status_dev);
   return cuda_status();

@@ -265,6 +265,7 @@ int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uin
     cudaFuncSetAttribute(codebook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
+  count_launch();
   codebook_kernel<<<single_field >= 0 ? 1 : 6, kCBThreads, sm, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
@@ -310,6 +311,7 @@ int launch_huffman_lengths(const uint32_t* counts, int64_t k, uint8_t* lengths, 
   if (k <= 0 || k > 65536) return NBZG_BAD_ARG;
   size_t sm = 12 * (size_t)kCBSmemK;
   cudaFuncSetAttribute(huffman_lengths_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  count_launch();
   huffman_lengths_kernel<<<1, kCBThreads, sm, st>>>(counts, (int)k, lengths, scr, status);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
@@ -331,6 +333,7 @@ __global__ void layout_kernel(nbzg_meta* meta, int64_t n) {
 }
 
 int launch_layout(const Plan& p, cudaStream_t st) {
+  count_launch();
   layout_kernel<<<1, 32, 0, st>>>(p.meta, p.n);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }

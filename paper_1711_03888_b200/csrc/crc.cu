@@ -104,9 +104,11 @@ int launch_crc64(const uint8_t* data, int64_t n, uint64_t* crc_out, void* ws, si
   int64_t np2 = 1;
   while (np2 < nb) np2 <<= 1;
   uint64_t* bufB = bufA + np2;
+  count_launch();
   crc_tables_kernel<<<1, 1024, 0, st>>>(tabs, base_tab);
   // front padding: leading (np2 - nb) zero blocks + `pad` zero bytes
   int64_t pad = (np2 << kCrcBlockLog) - n;
+  count_launch();
   crc_blocks_kernel<<<(unsigned)((np2 + 255) / 256), 256, 0, st>>>(data, n, pad, np2, base_tab,
                                                                    bufA);
   uint64_t* in = bufA;
@@ -114,12 +116,14 @@ int launch_crc64(const uint8_t* data, int64_t n, uint64_t* crc_out, void* ws, si
   int level = kCrcBlockLog;
   for (int64_t cnt = np2; cnt > 1; cnt >>= 1, level++) {
     int64_t npairs = cnt >> 1;
+    count_launch();
     crc_combine_kernel<<<(unsigned)((npairs + 255) / 256), 256, 0, st>>>(
         in, out, npairs, tabs + (size_t)level * 2048);
     uint64_t* t = in;
     in = out;
     out = t;
   }
+  count_launch();
   crc_final_kernel<<<1, 32, 0, st>>>(in, tabs, n, crc_out);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }

@@ -676,8 +676,12 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
   if (n == 0) return NBZG_OK;
   cudaMemsetAsync(a.lb, 0, sizeof(uint64_t) * nf * 2 * a.nchunks, st);
   cudaMemsetAsync(a.tickets, 0, sizeof(uint32_t) * 16, st);
+  count_launch();
   parse_kernel<<<nf, 1024, 0, st>>>(a);
+  trace_mark("dq_parse", st);
+  count_launch();
   chunk_offsets_kernel<<<nf, 1024, 0, st>>>(a);
+  trace_mark("dq_offsets", st);
   size_t sm = (kDBufWords + 4) * 4 + (kDBufWords + 1) * 4 + kChunk * 2 + (1 << kLutBits) * 4;
   static bool attr = false;
   if (!attr) {
@@ -689,8 +693,16 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
     any_v2 |= fields[i].kind == 3;
     any_v1 |= fields[i].kind == 0;
   }
-  if (any_v2) decode_kernel<<<dim3((unsigned)a.nchunks, nf), kDThreads, sm, st>>>(a);
-  if (any_v1) decode_v1_kernel<<<nf, 32, 0, st>>>(a);
+  if (any_v2) {
+    count_launch();
+    decode_kernel<<<dim3((unsigned)a.nchunks, nf), kDThreads, sm, st>>>(a);
+  }
+  if (any_v2) trace_mark("dq_decode", st);
+  if (any_v1) {
+    count_launch();
+    decode_v1_kernel<<<nf, 32, 0, st>>>(a);
+    trace_mark("dq_decode_v1", st);
+  }
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
 

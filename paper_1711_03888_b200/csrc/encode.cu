@@ -271,6 +271,7 @@ __global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
 int launch_encode(const Plan& p, cudaStream_t st) {
   if (p.n == 0) return NBZG_OK;
   TArgs t{p.meta, p.arena, p.cb_sym, p.cb_len, p.nbins, p.nchunks, p.n};
+  count_launch();
   table_writer_kernel<<<6, 256, 0, st>>>(t);
   EArgs a{};
   a.meta = p.meta;
@@ -289,6 +290,7 @@ int launch_encode(const Plan& p, cudaStream_t st) {
   cudaMemsetAsync(p.lb, 0, sizeof(uint64_t) * 12 * p.nchunks, st);
   cudaMemsetAsync(p.counters, 0, sizeof(uint32_t) * 8, st);
   dim3 grid((unsigned)p.nchunks, 6);
+  count_launch();
   encode_kernel<<<grid, kEThreads, 0, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
@@ -312,6 +314,7 @@ int launch_huff_encode_raw(const uint16_t* syms, int64_t n, const uint64_t* lut,
   cudaMemsetAsync(lb, 0, sizeof(uint64_t) * 2 * a.nchunks, st);
   cudaMemsetAsync(tickets, 0, sizeof(uint32_t), st);
   dim3 grid((unsigned)a.nchunks, 1);
+  count_launch();
   encode_kernel<<<grid, kEThreads, 0, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }

@@ -17,6 +17,10 @@
 
 namespace nbzg {
 
+// launch accounting + optional per-kernel CUDA-event tracing (capi.cu)
+void count_launch();
+void trace_mark(const char* name, cudaStream_t st);
+
 constexpr int kTileMax = 16384;        // particles per tile / codes per chunk
 constexpr int kChunk = 16384;          // v2 chunk index granularity (symbols)
 constexpr int kMaxCodeLen = 57;        // encode.py:21

@@ -257,6 +257,7 @@ int launch_quantize(const Plan& p, cudaStream_t st) {
                          (int)sm);
     attr = true;
   }
+  count_launch();
   if (p.sorted) quantize_kernel<true><<<6 * per_field, kQThreads, sm, st>>>(a);
   else quantize_kernel<false><<<6 * per_field, kQThreads, sm, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;

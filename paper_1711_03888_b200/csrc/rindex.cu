@@ -269,8 +269,10 @@ int launch_rindex_sort(const Plan& p, cudaStream_t st) {
   }
   cudaMemsetAsync(p.tile_flags, 0, sizeof(uint32_t) * p.ntiles, st);
   a.pass = 0;
+  count_launch();
   rindex_sort_kernel<uint32_t><<<(unsigned)p.ntiles, kSortThreads, sm32, st>>>(a);
   a.pass = 1;
+  count_launch();
   rindex_sort_kernel<uint64_t><<<(unsigned)p.ntiles, kSortThreads, sm64, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
@@ -379,7 +381,10 @@ int launch_rindex_keys(const float* x, const float* y, const float* z, int64_t n
   a.seg_bits = seg_bits;
   a.status = status;
   int64_t nseg = (n + S - 1) / S;
-  if (nseg > 0) rindex_keys_kernel<<<(unsigned)nseg, 256, 0, st>>>(a);
+  if (nseg > 0) {
+    count_launch();
+    rindex_keys_kernel<<<(unsigned)nseg, 256, 0, st>>>(a);
+  }
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
 
@@ -421,7 +426,10 @@ int launch_prx_order(const uint64_t* keys, int64_t n, int64_t S, const uint8_t* 
   size_t sm = kTileMax * (8 + 2) + kSortWarps * kRadix * 2;
   cudaFuncSetAttribute(prx_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   int64_t nseg = (n + S - 1) / S;
-  if (nseg > 0) prx_order_kernel<<<(unsigned)nseg, kSortThreads, sm, st>>>(a);
+  if (nseg > 0) {
+    count_launch();
+    prx_order_kernel<<<(unsigned)nseg, kSortThreads, sm, st>>>(a);
+  }
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
 
@@ -434,7 +442,10 @@ __global__ void order_expand_kernel(const uint16_t* perm, int64_t n, int64_t til
 
 int launch_order_expand(const uint16_t* perm, int64_t n, int64_t tile, int64_t* order,
                         cudaStream_t st) {
-  if (n > 0) order_expand_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(perm, n, tile, order);
+  if (n > 0) {
+    count_launch();
+    order_expand_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(perm, n, tile, order);
+  }
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
 
