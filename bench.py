@@ -294,7 +294,7 @@ def run_b200(args):
         out = nbz.decompress(res.archive, device=True)
         e2.record()
         if record is not None:
-            record.append((e0, e1, e2, res, sizes))
+            record.append((e0, e1, e2, res.archive.total_bytes(), sizes))
         return res, out
 
     for _ in range(args.warmup):
@@ -323,7 +323,7 @@ def run_b200(args):
     td = reduce_max(sum(r[1].elapsed_time(r[2]) for r in rec) / args.steps, world)
     ms_step = total_ms / args.steps
     last = rec[-1]
-    S_local = last[3].archive.total_bytes()
+    S_local = last[3]
     S_total = float(last[4].sum())
     n_total = n * world
     hbm, peak_kind = peaks()

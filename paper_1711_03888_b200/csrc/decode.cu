@@ -28,7 +28,8 @@ namespace nbzg {
 constexpr int kDThreads = 1024;
 constexpr int kDPer = kChunk / kDThreads;  // 16 symbols per thread (dequant)
 constexpr int kDBufWords = 8192;           // 262144 bits of stream per chunk in smem
-constexpr int kLutBits = 12;
+constexpr int kLutBits = 13;
+constexpr int kSmemSyms = 16384;  // sorted-symbol table staged in smem up to this k
 
 struct DParsed {
   uint64_t n_esc, k, total_bits;
@@ -223,10 +224,17 @@ __global__ void __launch_bounds__(1024) chunk_offsets_kernel(DArgs a) {
 }
 
 // ---------------------------------------------------------------- decode step
+// Shared-memory decode tables: a 2^13-entry primary LUT (sym | len << 16,
+// len 63 = longer code) and, for longer codes, the canonical left-justified
+// limits (encode.py:133-139 first_code recurrence): a codeword's length is
+// the smallest l with window < limit[l].
 struct DecTab {
-  const uint32_t* lut;       // smem copy
+  const uint32_t* lut;       // smem [1 << kLutBits]
+  const uint64_t* limit;     // smem [64] left-justified (<< (32 - l)) limits
+  const int32_t* base;       // smem [64] first_idx[l] - first_code[l]
+  const uint16_t* ss16;      // smem sorted symbols (k <= kSmemSyms) or null
+  const uint32_t* ss;        // global sorted symbols
   const DParsed* P;
-  const uint32_t* ss;
   int max_len;
 };
 
@@ -235,7 +243,7 @@ NBZG_DEV uint32_t peek32(const uint32_t* W, uint32_t p) {
   return __funnelshift_l(W[i + 1], W[i], s);
 }
 
-// decode one codeword at bit p; returns length (0 = invalid), sym via ref
+// decode one codeword at bit p; returns its length (0 = invalid)
 NBZG_DEV int decode_one(const uint32_t* W, uint32_t p, const DecTab& T, uint32_t& sym) {
   uint32_t v = peek32(W, p);
   uint32_t e = T.lut[v >> (32 - kLutBits)];
@@ -245,7 +253,17 @@ NBZG_DEV int decode_one(const uint32_t* W, uint32_t p, const DecTab& T, uint32_t
     return l;
   }
   if (l != 63) return 0;
-  // long code: canonical search over lengths > kLutBits (_kernels.py:361-372)
+  if (T.max_len <= 32) {
+    for (int len = kLutBits + 1; len <= T.max_len; len++) {
+      if ((uint64_t)v < T.limit[len]) {
+        uint32_t idx = (uint32_t)(T.base[len] + (int32_t)(v >> (32 - len)));
+        sym = T.ss16 ? T.ss16[idx] : T.ss[idx];
+        return len;
+      }
+    }
+    return 0;
+  }
+  // > 32-bit codes (pathological alphabets): canonical search, 64-bit window
   uint64_t v64 = ((uint64_t)v << 32) | peek32(W, p + 32);
   for (int len = kLutBits + 1; len <= T.max_len; len++) {
     uint32_t cnt = T.P->counts[len];
@@ -322,7 +340,10 @@ __global__ void __launch_bounds__(kDThreads) decode_kernel(DArgs a) {
   uint32_t* W = reinterpret_cast<uint32_t*>(smem);                 // [kDBufWords + 4]
   uint32_t* M = W + kDBufWords + 4;                                // [kDBufWords + 1] start marks
   uint16_t* S = reinterpret_cast<uint16_t*>(M + kDBufWords + 1);   // [16384]
-  uint32_t* LUT = reinterpret_cast<uint32_t*>(S + kChunk);         // [4096]
+  uint32_t* LUT = reinterpret_cast<uint32_t*>(S + kChunk);         // [1 << kLutBits]
+  uint16_t* SS = reinterpret_cast<uint16_t*>(LUT + (1 << kLutBits));  // [kSmemSyms]
+  __shared__ uint64_t s_limit[64];
+  __shared__ int32_t s_base[64];
   __shared__ uint32_t ends[kDThreads];
   __shared__ uint32_t scan_tmp[33];
   __shared__ KSeg kscan[33];
@@ -353,10 +374,26 @@ __global__ void __launch_bounds__(kDThreads) decode_kernel(DArgs a) {
 
   DecTab T;
   T.lut = LUT;
+  T.limit = s_limit;
+  T.base = s_base;
   T.P = &P;
   T.ss = ss;
+  T.ss16 = P.k <= (uint64_t)kSmemSyms ? SS : nullptr;
   T.max_len = (int)P.max_len;
   for (int i = tid; i < (1 << kLutBits); i += kDThreads) LUT[i] = a.lut[fi * (1 << kLutBits) + i];
+  if (T.ss16)
+    for (uint32_t i = tid; i < (uint32_t)P.k; i += kDThreads) SS[i] = (uint16_t)ss[i];
+  if (tid < 64) {
+    const int l = tid;
+    uint64_t lim = 0;
+    int32_t bs = 0;
+    if (l >= 1 && l <= 32) {
+      lim = (P.first_code[l] + P.counts[l]) << (32 - l);
+      bs = (int32_t)P.first_idx[l] - (int32_t)P.first_code[l];
+    }
+    s_limit[l] = l > (int)P.max_len ? ~0ull : lim;
+    s_base[l] = bs;
+  }
 
   const bool big = (uint64_t)Lb + 64 > (uint64_t)kDBufWords * 32;
   if (big) {
@@ -494,7 +531,10 @@ __global__ void __launch_bounds__(kDThreads) decode_kernel(DArgs a) {
   for (int j = 0; j < qn; j++) my_esc += S[q0 + j] == 0;
   uint32_t etot;
   uint32_t eo = block_excl_scan<uint32_t>(my_esc, scan_tmp, &etot);
-  if (tid == 0) s_eoff = lookback_sum(a.lb + (fi * 2 + 0) * a.nchunks, c, etot);
+  if (tid < 32) {
+    uint64_t eo2 = lookback_sum(a.lb + (fi * 2 + 0) * a.nchunks, c, etot);
+    if (tid == 0) s_eoff = eo2;
+  }
   __syncthreads();
   const uint8_t* escp = F.payload + P.esc_off;
   const uint64_t e_idx = s_eoff + eo;
@@ -551,10 +591,13 @@ __global__ void __launch_bounds__(kDThreads) decode_kernel(DArgs a) {
   exw.v = __shfl_up_sync(0xffffffffu, inc.v, 1);
   if (lane == 0) exw = KSeg{0, 0};
   KSeg before = kseg_op(kscan[wid], exw);
-  if (tid == 0) {
+  if (tid < 32) {
     KSeg ca = kscan[32];
-    s_carry = lookback_kcarry(a.lb + (fi * 2 + 1) * a.nchunks, c, ca.r != 0, ca.v);
-    if (s_err) fail(a.status, s_err);
+    long long cr = lookback_kcarry(a.lb + (fi * 2 + 1) * a.nchunks, c, ca.r != 0, ca.v);
+    if (tid == 0) {
+      s_carry = cr;
+      if (s_err) fail(a.status, s_err);
+    }
   }
   __syncthreads();
   long long k = before.r ? before.v : s_carry + before.v;
@@ -682,7 +725,8 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
   count_launch();
   chunk_offsets_kernel<<<nf, 1024, 0, st>>>(a);
   trace_mark("dq_offsets", st);
-  size_t sm = (kDBufWords + 4) * 4 + (kDBufWords + 1) * 4 + kChunk * 2 + (1 << kLutBits) * 4;
+  size_t sm = (kDBufWords + 4) * 4 + (kDBufWords + 1) * 4 + kChunk * 2 + (1 << kLutBits) * 4 +
+              kSmemSyms * 2;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -163,13 +163,17 @@ __global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
   uint32_t my_esc = block_excl_scan<uint32_t>(tesc, scan_tmp, &chunk_esc);
 
   // ---- decoupled look-back: global bit / escape offsets of this chunk
-  if (tid == 0) {
+  if (tid < 32) {
     uint64_t* lbb = a.lb + (field * 2 + 0) * a.nchunks;
     uint64_t* lbe = a.lb + (field * 2 + 1) * a.nchunks;
-    s_boff = lookback_sum(lbb, c, chunk_bits);
-    s_eoff = raw ? 0 : lookback_sum(lbe, c, chunk_esc);
-    if (raw) a.raw_chunk_bits[c] = chunk_bits;
-    else put_u32_bytes(payload + m.index_off + 4 * c, chunk_bits);
+    uint64_t bo = lookback_sum(lbb, c, chunk_bits);
+    uint64_t eo = raw ? 0 : lookback_sum(lbe, c, chunk_esc);
+    if (tid == 0) {
+      s_boff = bo;
+      s_eoff = eo;
+      if (raw) a.raw_chunk_bits[c] = chunk_bits;
+      else put_u32_bytes(payload + m.index_off + 4 * c, chunk_bits);
+    }
   }
   __syncthreads();
   const uint64_t B = s_boff;

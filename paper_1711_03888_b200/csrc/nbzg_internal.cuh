@@ -150,63 +150,82 @@ NBZG_DEV uint64_t lb_load(const uint64_t* p) {
   return v;
 }
 
-// Called by ONE thread of chunk `c` after it knows its local aggregate.
-// Returns the exclusive prefix and publishes the inclusive value.
+// Warp-parallel decoupled look-back, called by ALL 32 lanes of one warp of
+// chunk `c` after the chunk knows its local aggregate.  Lane l inspects
+// predecessor p - l, so each round covers 32 predecessors with one load per
+// lane.  Returns the exclusive prefix (in every lane) and publishes the
+// inclusive value.
+template <typename T>
+NBZG_DEV T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 NBZG_DEV uint64_t lookback_sum(uint64_t* status, int64_t c, uint64_t agg) {
+  const int lane = threadIdx.x & 31;
   if (c == 0) {
-    lb_store(&status[0], kFlagInc | (agg & kValMask));
+    if (lane == 0) lb_store(&status[0], kFlagInc | (agg & kValMask));
     return 0;
   }
-  lb_store(&status[c], kFlagAgg | (agg & kValMask));
+  if (lane == 0) lb_store(&status[c], kFlagAgg | (agg & kValMask));
   uint64_t excl = 0;
   int64_t p = c - 1;
   while (true) {
-    uint64_t s = lb_load(&status[p]);
+    const int64_t idx = p - lane;
+    uint64_t s = idx >= 0 ? lb_load(&status[idx]) : kFlagInc;
     uint64_t f = s & ~kValMask;
-    if (f == 0) continue;  // spin: predecessor has a lower ticket, it is running
-    excl += s & kValMask;
-    if (f == kFlagInc) break;
-    --p;
+    if (__any_sync(0xffffffffu, f == 0)) continue;  // predecessors hold lower tickets: running
+    uint32_t inc = __ballot_sync(0xffffffffu, f == kFlagInc);
+    if (inc) {
+      const int first = __ffs(inc) - 1;
+      excl += warp_sum<uint64_t>(lane <= first ? (s & kValMask) : 0ull);
+      break;
+    }
+    excl += warp_sum<uint64_t>(s & kValMask);
+    p -= 32;
   }
-  lb_store(&status[c], kFlagInc | ((excl + agg) & kValMask));
+  if (lane == 0) lb_store(&status[c], kFlagInc | ((excl + agg) & kValMask));
   return excl;
 }
 
 // Segmented "k-carry" look-back for the decoder: value = (reset:1 | k:61 as
-// two's complement).  Composition: later(reset) wins, else adds.
+// two's complement).  Composition: a later reset wins, otherwise values add.
 NBZG_DEV uint64_t kc_pack(bool reset, int64_t k) {
   return ((uint64_t)reset << 61) | ((uint64_t)k & ((1ull << 61) - 1));
 }
 NBZG_DEV int64_t kc_val(uint64_t s) {
-  int64_t v = (int64_t)(s << 3) >> 3;  // sign-extend 61 bits
-  return v;
+  return (int64_t)(s << 3) >> 3;  // sign-extend 61 bits
 }
 NBZG_DEV bool kc_reset(uint64_t s) { return (s >> 61) & 1; }
 
-// Returns the k carried INTO chunk c (k of the element before the chunk).
+// Warp-parallel; returns the k carried INTO chunk c (k of the element before
+// the chunk; 0 at the stream start) in every lane.
 NBZG_DEV int64_t lookback_kcarry(uint64_t* status, int64_t c, bool reset, int64_t kloc) {
+  const int lane = threadIdx.x & 31;
   if (c == 0) {
-    // stream start: k_{-1} = 0, so the inclusive value is (reset ? k : 0 + k)
-    lb_store(&status[0], kFlagInc | kc_pack(true, kloc));
+    if (lane == 0) lb_store(&status[0], kFlagInc | kc_pack(true, kloc));
     return 0;
   }
-  lb_store(&status[c], kFlagAgg | kc_pack(reset, kloc));
-  int64_t add = 0;
+  if (lane == 0) lb_store(&status[c], kFlagAgg | kc_pack(reset, kloc));
   int64_t carry = 0;
   int64_t p = c - 1;
   while (true) {
-    uint64_t s = lb_load(&status[p]);
+    const int64_t idx = p - lane;
+    uint64_t s = idx >= 0 ? lb_load(&status[idx]) : (kFlagInc | kc_pack(true, 0));
     uint64_t f = s & ~kValMask;
-    if (f == 0) continue;
-    if (f == kFlagInc || kc_reset(s)) {
-      carry = kc_val(s) + add;
+    if (__any_sync(0xffffffffu, f == 0)) continue;
+    uint32_t stop = __ballot_sync(0xffffffffu, f == kFlagInc || kc_reset(s));
+    if (stop) {
+      const int first = __ffs(stop) - 1;
+      carry += warp_sum<long long>(lane <= first ? (long long)kc_val(s) : 0ll);
       break;
     }
-    add += kc_val(s);
-    --p;
+    carry += warp_sum<long long>((long long)kc_val(s));
+    p -= 32;
   }
   int64_t inc = reset ? kloc : carry + kloc;
-  lb_store(&status[c], kFlagInc | kc_pack(true, inc));
+  if (lane == 0) lb_store(&status[c], kFlagInc | kc_pack(true, inc));
   return carry;
 }
 

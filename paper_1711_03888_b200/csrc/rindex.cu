@@ -132,7 +132,7 @@ NBZG_DEV void block_sort_range(const KeyT* keys, uint16_t* perm, int lo, int m, 
 }
 
 template <typename KeyT>
-__global__ void __launch_bounds__(kSortThreads) rindex_sort_kernel(RArgs a) {
+__global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   KeyT* keys = reinterpret_cast<KeyT*>(smem);
   uint16_t* perm = reinterpret_cast<uint16_t*>(keys + kTileMax);
