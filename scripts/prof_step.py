@@ -1,0 +1,35 @@
+#!/usr/bin/env python3
+"""One compress + decompress of a HACC-like slab on cuda:0 -- the short
+command profiled with ncu (profiles/*).  Usage:
+    python scripts/prof_step.py [--n N] [--mode sz-lv-prx] [--reps R]"""
+
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+
+import torch  # noqa: E402
+
+import paper_1711_03888_b200 as nbz  # noqa: E402
+from paper_1711_03888_b200 import datagen  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=1 << 24)
+    ap.add_argument("--mode", default="sz-lv-prx")
+    ap.add_argument("--reps", type=int, default=2)
+    args = ap.parse_args()
+    spec = datagen.HaccSpec((640, 640, 640), 2.5)
+    fields = datagen.generate(spec, 0, args.n)
+    snap = nbz.ParticleSnapshot(*[torch.from_numpy(f).cuda() for f in fields])
+    for _ in range(args.reps):
+        res = nbz.compress(snap, args.mode, nbz.ErrorBoundSpec.relative(1e-4))
+        out = nbz.decompress(res.archive, device=True)
+    torch.cuda.synchronize()
+    print("ratio", nbz.ratio(res.archive), "n", out.n)
+
+
+if __name__ == "__main__":
+    main()
