@@ -28,8 +28,9 @@ namespace nbzg {
 constexpr int kDThreads = 1024;
 constexpr int kDPer = kChunk / kDThreads;  // 16 symbols per thread (dequant)
 constexpr int kDBufWords = 8192;           // 262144 bits of stream per chunk in smem
-constexpr int kLutBits = 13;
+constexpr int kLutBits = 12;       // length LUT index bits
 constexpr int kSmemSyms = 16384;  // sorted-symbol table staged in smem up to this k
+constexpr int kSegBits = 192;      // minimum bits per decoding thread (limits sync cascades)
 
 struct DParsed {
   uint64_t n_esc, k, total_bits;
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
   const int fi = blockIdx.x;
   const DField& F = a.f[fi];
   DParsed& P = a.parsed[fi];
-  uint32_t* lut = a.lut + fi * (1 << kLutBits);
+  uint8_t* lut = reinterpret_cast<uint8_t*>(a.lut) + fi * (1 << kLutBits);
   uint32_t* ss = a.ssyms + fi * a.nbins;
   __shared__ uint32_t s_bad, s_cbl[64], s_max, s_min;
   __shared__ uint32_t scan_tmp[33];
@@ -154,14 +155,11 @@ __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
         uint32_t pos = s_fi[l] + ex;
         ss[pos] = sym;
         uint64_t word = s_fc[l] + ex;
-        if (l <= kLutBits && sym < 65536) {
+        if (l <= kLutBits) {
           uint32_t lo = (uint32_t)(word << (kLutBits - l)), cntl = 1u << (kLutBits - l);
-          for (uint32_t q = 0; q < cntl; q++) lut[lo + q] = sym | ((uint32_t)l << 16);
-        } else if (l > kLutBits) {
-          lut[(uint32_t)(word >> (l - kLutBits))] = 63u << 16;  // long-code prefix
+          for (uint32_t q = 0; q < cntl; q++) lut[lo + q] = (uint8_t)l;
         } else {
-          uint32_t lo = (uint32_t)(word << (kLutBits - l)), cntl = 1u << (kLutBits - l);
-          for (uint32_t q = 0; q < cntl; q++) lut[lo + q] = 63u << 16;  // sym >= 2^16: slow path
+          lut[(uint32_t)(word >> (l - kLutBits))] = 0xFE;  // prefix of a longer code
         }
         ex++;
       }
@@ -224,17 +222,16 @@ __global__ void __launch_bounds__(1024) chunk_offsets_kernel(DArgs a) {
 }
 
 // ---------------------------------------------------------------- decode step
-// Shared-memory decode tables: a 2^13-entry primary LUT (sym | len << 16,
-// len 63 = longer code) and, for longer codes, the canonical left-justified
-// limits (encode.py:133-139 first_code recurrence): a codeword's length is
-// the smallest l with window < limit[l].
+// Shared-memory tables: a 2^12-entry code-LENGTH table (0 = invalid prefix,
+// 0xFE = longer code) and the canonical left-justified limits
+// (encode.py:133-139): a codeword's length is the smallest l with
+// window < limit[l], its symbol ss[base[l] + (window >> (32 - l))].
 struct DecTab {
-  const uint32_t* lut;       // smem [1 << kLutBits]
-  const uint64_t* limit;     // smem [64] left-justified (<< (32 - l)) limits
+  const uint8_t* ll;         // smem [1 << kLutBits]
+  const uint64_t* limit;     // smem [64]
   const int32_t* base;       // smem [64] first_idx[l] - first_code[l]
   const uint16_t* ss16;      // smem sorted symbols (k <= kSmemSyms) or null
   const uint32_t* ss;        // global sorted symbols
-  const DParsed* P;
   int max_len;
 };
 
@@ -243,39 +240,19 @@ NBZG_DEV uint32_t peek32(const uint32_t* W, uint32_t p) {
   return __funnelshift_l(W[i + 1], W[i], s);
 }
 
-// decode one codeword at bit p; returns its length (0 = invalid)
-NBZG_DEV int decode_one(const uint32_t* W, uint32_t p, const DecTab& T, uint32_t& sym) {
-  uint32_t v = peek32(W, p);
-  uint32_t e = T.lut[v >> (32 - kLutBits)];
-  int l = (int)(e >> 16);
-  if (l >= 1 && l <= kLutBits) {
-    sym = e & 0xffff;
-    return l;
-  }
-  if (l != 63) return 0;
-  if (T.max_len <= 32) {
-    for (int len = kLutBits + 1; len <= T.max_len; len++) {
-      if ((uint64_t)v < T.limit[len]) {
-        uint32_t idx = (uint32_t)(T.base[len] + (int32_t)(v >> (32 - len)));
-        sym = T.ss16 ? T.ss16[idx] : T.ss[idx];
-        return len;
-      }
-    }
-    return 0;
-  }
-  // > 32-bit codes (pathological alphabets): canonical search, 64-bit window
-  uint64_t v64 = ((uint64_t)v << 32) | peek32(W, p + 32);
-  for (int len = kLutBits + 1; len <= T.max_len; len++) {
-    uint32_t cnt = T.P->counts[len];
-    if (!cnt) continue;
-    uint64_t code = v64 >> (64 - len);
-    uint64_t fc = T.P->first_code[len];
-    if (code >= fc && code - fc < cnt) {
-      sym = T.ss[T.P->first_idx[len] + (uint32_t)(code - fc)];
-      return len;
-    }
-  }
+// length of the codeword whose left-justified bits are v (0 = invalid)
+NBZG_DEV int code_len(uint32_t v, const DecTab& T) {
+  int l = T.ll[v >> (32 - kLutBits)];
+  if (l < 0xFE) return l;
+#pragma unroll 1
+  for (int len = kLutBits + 1; len <= T.max_len; len++)
+    if ((uint64_t)v < T.limit[len]) return len;
   return 0;
+}
+
+NBZG_DEV uint32_t code_sym(uint32_t v, int len, const DecTab& T) {
+  uint32_t idx = (uint32_t)(T.base[len] + (int32_t)(v >> (32 - len)));
+  return T.ss16 ? T.ss16[idx] : T.ss[idx];
 }
 
 NBZG_DEV bool mark_get(const uint32_t* M, uint32_t p) { return (M[p >> 5] >> (p & 31)) & 1u; }
@@ -340,8 +317,8 @@ __global__ void __launch_bounds__(kDThreads) decode_kernel(DArgs a) {
   uint32_t* W = reinterpret_cast<uint32_t*>(smem);                 // [kDBufWords + 4]
   uint32_t* M = W + kDBufWords + 4;                                // [kDBufWords + 1] start marks
   uint16_t* S = reinterpret_cast<uint16_t*>(M + kDBufWords + 1);   // [16384]
-  uint32_t* LUT = reinterpret_cast<uint32_t*>(S + kChunk);         // [1 << kLutBits]
-  uint16_t* SS = reinterpret_cast<uint16_t*>(LUT + (1 << kLutBits));  // [kSmemSyms]
+  uint16_t* SS = S + kChunk;                                       // [kSmemSyms]
+  uint8_t* LL = reinterpret_cast<uint8_t*>(SS + kSmemSyms);        // [1 << kLutBits]
   __shared__ uint64_t s_limit[64];
   __shared__ int32_t s_base[64];
   __shared__ uint32_t ends[kDThreads];
@@ -373,29 +350,32 @@ __global__ void __launch_bounds__(kDThreads) decode_kernel(DArgs a) {
   const uint32_t* ss = a.ssyms + fi * a.nbins;
 
   DecTab T;
-  T.lut = LUT;
+  T.ll = LL;
   T.limit = s_limit;
   T.base = s_base;
-  T.P = &P;
   T.ss = ss;
   T.ss16 = P.k <= (uint64_t)kSmemSyms ? SS : nullptr;
   T.max_len = (int)P.max_len;
-  for (int i = tid; i < (1 << kLutBits); i += kDThreads) LUT[i] = a.lut[fi * (1 << kLutBits) + i];
+  {
+    const uint32_t* gl = reinterpret_cast<const uint32_t*>(
+        reinterpret_cast<const uint8_t*>(a.lut) + fi * (1 << kLutBits));
+    uint32_t* sl = reinterpret_cast<uint32_t*>(LL);
+    for (int i = tid; i < (1 << kLutBits) / 4; i += kDThreads) sl[i] = gl[i];
+  }
   if (T.ss16)
     for (uint32_t i = tid; i < (uint32_t)P.k; i += kDThreads) SS[i] = (uint16_t)ss[i];
   if (tid < 64) {
     const int l = tid;
     uint64_t lim = 0;
     int32_t bs = 0;
-    if (l >= 1 && l <= 32) {
+    if (l >= 1 && l <= 32 && l <= (int)P.max_len) {
       lim = (P.first_code[l] + P.counts[l]) << (32 - l);
       bs = (int32_t)P.first_idx[l] - (int32_t)P.first_code[l];
     }
     s_limit[l] = l > (int)P.max_len ? ~0ull : lim;
     s_base[l] = bs;
   }
-
-  const bool big = (uint64_t)Lb + 64 > (uint64_t)kDBufWords * 32;
+  const bool big = (uint64_t)Lb + 64 > (uint64_t)kDBufWords * 32 || P.max_len > 32;
   if (big) {
     // rare: > 16 bits/symbol on average in this chunk -- sequential decode
     if (tid == 0) {
@@ -437,15 +417,16 @@ __global__ void __launch_bounds__(kDThreads) decode_kernel(DArgs a) {
     }
     __syncthreads();
 
-    // ---- 2. self-synchronising decode
-    const uint32_t seg0 = (uint32_t)(((uint64_t)Lb * tid) / kDThreads);
-    const uint32_t seg1 = (uint32_t)(((uint64_t)Lb * (tid + 1)) / kDThreads);
+    // ---- 2. self-synchronising decode over T_dec threads (>= kSegBits bits each)
+    int tdec = (int)min((uint32_t)kDThreads, max(32u, ((Lb / kSegBits) + 31u) & ~31u));
+    const bool active = tid < tdec;
+    const uint32_t seg0 = active ? (uint32_t)(((uint64_t)Lb * tid) / tdec) : Lb;
+    const uint32_t seg1 = active ? (uint32_t)(((uint64_t)Lb * (tid + 1)) / tdec) : Lb;
     uint32_t start = seg0;
-    {
+    if (active) {
       uint32_t p = seg0;
       while (p < seg1) {
-        uint32_t sym;
-        int l = decode_one(W, p, T, sym);
+        int l = code_len(peek32(W, p), T);
         if (l == 0) {  // garbage from a wrong start: step one bit
           p += 1;
           continue;
@@ -459,7 +440,7 @@ __global__ void __launch_bounds__(kDThreads) decode_kernel(DArgs a) {
     int invalid = 0;
     for (int iter = 0; iter <= kDThreads; iter++) {
       int changed = 0;
-      if (tid > 0) {
+      if (active && tid > 0) {
         uint32_t s = ends[tid - 1];
         if (s != start) {
           uint32_t p = s, sync = 0xffffffffu;
@@ -468,8 +449,7 @@ __global__ void __launch_bounds__(kDThreads) decode_kernel(DArgs a) {
               sync = p;
               break;
             }
-            uint32_t sym;
-            int l = decode_one(W, p, T, sym);
+            int l = code_len(peek32(W, p), T);
             if (l == 0) {
               invalid = 1;
               break;
@@ -480,8 +460,7 @@ __global__ void __launch_bounds__(kDThreads) decode_kernel(DArgs a) {
           mark_clear_range(M, seg0, max(stop, seg0));
           uint32_t q = s;
           while (q < stop) {
-            uint32_t sym;
-            int l = decode_one(W, q, T, sym);
+            int l = code_len(peek32(W, q), T);
             if (l == 0) break;
             mark_set(M, q);
             q += l;
@@ -497,23 +476,23 @@ __global__ void __launch_bounds__(kDThreads) decode_kernel(DArgs a) {
     }
     if (__syncthreads_or(invalid) && tid == 0) s_err = NBZG_INVALID_CODE;
     // ---- 3. counts and decode into shared memory
-    uint32_t cnt = mark_count(M, seg0, seg1);
+    uint32_t cnt = active ? mark_count(M, seg0, seg1) : 0u;
     uint32_t tot;
     uint32_t o = block_excl_scan<uint32_t>(cnt, scan_tmp, &tot);
-    if (tid == 0 && (tot != (uint32_t)mc || ends[kDThreads - 1] != Lb) && !s_err)
+    if (tid == 0 && (tot != (uint32_t)mc || ends[tdec - 1] != Lb) && !s_err)
       s_err = tot < (uint32_t)mc ? NBZG_TRUNCATED : NBZG_BAD_STREAM;
     __syncthreads();
-    if (!s_err) {
+    if (!s_err && active) {
       uint32_t p = tid == 0 ? 0 : ends[tid - 1];
       int bad = 0;
       for (uint32_t i = 0; i < cnt; i++) {
-        uint32_t sym = 0;
-        int l = decode_one(W, p, T, sym);
+        uint32_t v = peek32(W, p);
+        int l = code_len(v, T);
         if (l == 0) {
           bad = 1;
           break;
         }
-        if (o + i < (uint32_t)kChunk) S[o + i] = (uint16_t)sym;
+        if (o + i < (uint32_t)kChunk) S[o + i] = (uint16_t)code_sym(v, l, T);
         p += l;
       }
       if (bad) atomicCAS(&s_err, 0u, (uint32_t)NBZG_INVALID_CODE);
@@ -681,7 +660,7 @@ size_t decompress_ws(int nf, int64_t n, int64_t nbins) {
   size_t s = 0;
   auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
   s += al(sizeof(DParsed) * nf);
-  s += al(sizeof(uint32_t) * nf * (1 << kLutBits));
+  s += al((size_t)nf * (1 << kLutBits));
   s += al(sizeof(uint32_t) * nf * nbins);
   s += al(sizeof(uint64_t) * nf * (nchunks + 1));
   s += al(sizeof(uint64_t) * nf * 2 * (nchunks + 1));
@@ -707,7 +686,7 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
   a.parsed = reinterpret_cast<DParsed*>(p);
   p += al(sizeof(DParsed) * nf);
   a.lut = reinterpret_cast<uint32_t*>(p);
-  p += al(sizeof(uint32_t) * nf * (1 << kLutBits));
+  p += al((size_t)nf * (1 << kLutBits));
   a.ssyms = reinterpret_cast<uint32_t*>(p);
   p += al(sizeof(uint32_t) * nf * nbins);
   a.choff = reinterpret_cast<uint64_t*>(p);
@@ -725,8 +704,8 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
   count_launch();
   chunk_offsets_kernel<<<nf, 1024, 0, st>>>(a);
   trace_mark("dq_offsets", st);
-  size_t sm = (kDBufWords + 4) * 4 + (kDBufWords + 1) * 4 + kChunk * 2 + (1 << kLutBits) * 4 +
-              kSmemSyms * 2;
+  size_t sm = (kDBufWords + 4) * 4 + (kDBufWords + 1) * 4 + kChunk * 2 + kSmemSyms * 2 +
+              (1 << kLutBits);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

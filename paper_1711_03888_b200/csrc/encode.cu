@@ -22,8 +22,8 @@
 
 namespace nbzg {
 
-constexpr int kEThreads = 1024;
-constexpr int kEPer = kChunk / kEThreads;  // 16 codes per thread
+constexpr int kEThreads = 512;
+constexpr int kEPer = kChunk / kEThreads;  // 32 codes per thread
 constexpr int kEBufWords = 8192;           // 262144 bits per round
 
 NBZG_DEV void put_u32_bytes(uint8_t* p, uint32_t v) {
@@ -113,7 +113,7 @@ NBZG_DEV uint32_t lookahead_bits(const uint16_t* codes, int64_t c1, int64_t n, c
   return need >= 32 ? out : (out & ~(0xffffffffu >> need));
 }
 
-__global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
+__global__ void __launch_bounds__(kEThreads, 2) encode_kernel(EArgs a) {
   __shared__ uint32_t buf[kEBufWords + 2];
   __shared__ uint32_t scan_tmp[33];
   __shared__ unsigned long long s_boff, s_eoff;
@@ -136,36 +136,51 @@ __global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
   const int64_t c0 = c * kChunk;
   const int mc = (int)min((int64_t)kChunk, a.n - c0);
 
-  // ---- load 16 codes, lengths, escape flags
-  uint16_t cv[kEPer];
+  // ---- load 32 codes (packed pairs), lengths, escape flags
+  uint32_t cw[kEPer / 2];
   const int p0 = tid * kEPer;
   const int cnt = max(0, min(kEPer, mc - p0));
   if (cnt == kEPer && ((reinterpret_cast<uintptr_t>(codes + c0 + p0) & 15) == 0)) {
     const uint4* s4 = reinterpret_cast<const uint4*>(codes + c0 + p0);
-    uint4 u0 = s4[0], u1 = s4[1];
-    uint32_t w8[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
 #pragma unroll
-    for (int j = 0; j < kEPer; j++) cv[j] = (uint16_t)(w8[j >> 1] >> ((j & 1) * 16));
+    for (int q = 0; q < kEPer / 8; q++) {
+      uint4 u = s4[q];
+      cw[4 * q] = u.x;
+      cw[4 * q + 1] = u.y;
+      cw[4 * q + 2] = u.z;
+      cw[4 * q + 3] = u.w;
+    }
   } else {
 #pragma unroll
-    for (int j = 0; j < kEPer; j++) cv[j] = j < cnt ? codes[c0 + p0 + j] : 0;
+    for (int j = 0; j < kEPer / 2; j++) {
+      uint32_t lo = 2 * j < cnt ? codes[c0 + p0 + 2 * j] : 0u;
+      uint32_t hi = 2 * j + 1 < cnt ? codes[c0 + p0 + 2 * j + 1] : 0u;
+      cw[j] = lo | (hi << 16);
+    }
   }
+#define CODE_AT(j) ((cw[(j) >> 1] >> (((j) & 1) * 16)) & 0xffffu)
   uint32_t tbits = 0, tesc = 0;
 #pragma unroll
   for (int j = 0; j < kEPer; j++) {
     if (j < cnt) {
-      tbits += (uint32_t)(__ldg(&lut[cv[j]]) >> 57);
-      tesc += cv[j] == 0;
+      uint32_t cv = CODE_AT(j);
+      tbits += (uint32_t)(__ldg(&lut[cv]) >> 57);
+      tesc += cv == 0;
     }
   }
   uint32_t chunk_bits, chunk_esc;
   uint32_t my_off = block_excl_scan<uint32_t>(tbits, scan_tmp, &chunk_bits);
   uint32_t my_esc = block_excl_scan<uint32_t>(tesc, scan_tmp, &chunk_esc);
+  uint64_t* lbb = a.lb + (field * 2 + 0) * a.nchunks;
+  uint64_t* lbe = a.lb + (field * 2 + 1) * a.nchunks;
+  // publish the local aggregates at once so successors' look-backs never wait on our packing
+  if (tid == 0 && c > 0) {
+    lb_store(&lbb[c], kFlagAgg | chunk_bits);
+    if (!raw) lb_store(&lbe[c], kFlagAgg | chunk_esc);
+  }
 
   // ---- decoupled look-back: global bit / escape offsets of this chunk
   if (tid < 32) {
-    uint64_t* lbb = a.lb + (field * 2 + 0) * a.nchunks;
-    uint64_t* lbe = a.lb + (field * 2 + 1) * a.nchunks;
     uint64_t bo = lookback_sum(lbb, c, chunk_bits);
     uint64_t eo = raw ? 0 : lookback_sum(lbe, c, chunk_esc);
     if (tid == 0) {
@@ -183,9 +198,8 @@ __global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
   if (!raw && tesc) {
     float* esc = reinterpret_cast<float*>(payload + m.esc_off);
     uint64_t e = s_eoff + my_esc;
-#pragma unroll
-    for (int j = 0; j < kEPer; j++) {
-      if (j < cnt && cv[j] == 0) {
+    for (int j = 0; j < cnt; j++) {
+      if (CODE_AT(j) == 0) {
         int64_t pos = c0 + p0 + j;
         int64_t src = a.perm ? (pos / a.tile) * a.tile + a.perm[pos] : pos;
         esc[e++] = a.f[field][src];
@@ -223,7 +237,7 @@ __global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
 #pragma unroll
       for (int j = 0; j < kEPer; j++) {
         if (j < cnt) {
-          uint64_t e = __ldg(&lut[cv[j]]);
+          uint64_t e = __ldg(&lut[CODE_AT(j)]);
           int l = (int)(e >> 57);
           uint64_t w = e & ((1ull << 57) - 1);
           // write l bits of w starting at bit `pos` (MSB-first)
@@ -270,6 +284,7 @@ __global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
     }
   }
   (void)s_tail;
+#undef CODE_AT
 }
 
 int launch_encode(const Plan& p, cudaStream_t st) {
