@@ -10,11 +10,12 @@
 // index:
 //   1. stage the chunk's bits in shared memory, re-aligned so bit 0 is the
 //      MSB of word 0 (any payload alignment);
-//   2. self-synchronising parallel Huffman decode: every thread decodes from
-//      an arbitrary bit of its slice marking codeword starts in a bitmap,
-//      then re-decodes from its predecessor's true end until it lands on a
-//      start the first pass already visited (Huffman codes resynchronise
-//      within a few codewords); counts come from the bitmap;
+//   2. self-synchronising parallel Huffman decode: every thread decodes its
+//      slice (>= 192 bits) from an arbitrary bit, counting codewords and
+//      remembering its first 8 codeword starts in registers, then re-walks
+//      from its predecessor's true end until it lands on a remembered start
+//      (Huffman codes resynchronise within a few codewords) and corrects its
+//      count; a 2^16-entry code-length table in shared memory decodes;
 //   3. decode again from the true starts into shared memory;
 //   4. dequantise: escape offsets and the lattice index k carried into the
 //      chunk come from two decoupled look-backs; recon = f32(k * 2b) or the
@@ -28,7 +29,8 @@ namespace nbzg {
 constexpr int kDThreads = 1024;
 constexpr int kDPer = kChunk / kDThreads;  // 16 symbols per thread (dequant)
 constexpr int kDBufWords = 8192;           // 262144 bits of stream per chunk in smem
-constexpr int kLutBits = 12;       // length LUT index bits
+constexpr int kLutBits = 16;       // length LUT index bits (u8 entries, 64 KiB)
+constexpr int kRec = 8;            // phase-1 codeword starts remembered per thread
 constexpr int kSmemSyms = 16384;  // sorted-symbol table staged in smem up to this k
 constexpr int kSegBits = 192;      // minimum bits per decoding thread (limits sync cascades)
 
@@ -154,16 +156,27 @@ __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
         uint32_t sym = ld_u32_bytes(p + 8 + 5 * i);
         uint32_t pos = s_fi[l] + ex;
         ss[pos] = sym;
-        uint64_t word = s_fc[l] + ex;
-        if (l <= kLutBits) {
-          uint32_t lo = (uint32_t)(word << (kLutBits - l)), cntl = 1u << (kLutBits - l);
-          for (uint32_t q = 0; q < cntl; q++) lut[lo + q] = (uint8_t)l;
-        } else {
-          lut[(uint32_t)(word >> (l - kLutBits))] = 0xFE;  // prefix of a longer code
-        }
         ex++;
       }
     }
+  }
+  // length table: entry e (16-bit prefix) -> smallest l with e.. < limit[l]
+  // (canonical order), 0xFE when the code is longer than 16 bits, 0 = invalid
+  for (int e = tid; e < (1 << kLutBits); e += blockDim.x) {
+    uint8_t len = 0;
+    for (int l = 1; l <= max_len; l++) {
+      if (l <= kLutBits) {
+        uint64_t lim = (s_fc[l] + s_cbl[l]) << (kLutBits - l);  // limit in 16-bit units
+        if ((uint64_t)e < lim) {
+          len = (uint8_t)l;
+          break;
+        }
+      } else {
+        len = 0xFE;
+        break;
+      }
+    }
+    lut[e] = len;
   }
   if (tid == 0) {
     const uint64_t table_end = 8 + 5 * k;
@@ -255,29 +268,6 @@ NBZG_DEV uint32_t code_sym(uint32_t v, int len, const DecTab& T) {
   return T.ss16 ? T.ss16[idx] : T.ss[idx];
 }
 
-NBZG_DEV bool mark_get(const uint32_t* M, uint32_t p) { return (M[p >> 5] >> (p & 31)) & 1u; }
-NBZG_DEV void mark_set(uint32_t* M, uint32_t p) { atomicOr(&M[p >> 5], 1u << (p & 31)); }
-NBZG_DEV void mark_clear_range(uint32_t* M, uint32_t a, uint32_t b) {  // [a, b)
-  while (a < b) {
-    uint32_t wi = a >> 5, bo = a & 31;
-    uint32_t take = min(32 - bo, b - a);
-    uint32_t mask = (take == 32 ? 0xffffffffu : ((1u << take) - 1u)) << bo;
-    atomicAnd(&M[wi], ~mask);
-    a += take;
-  }
-}
-NBZG_DEV uint32_t mark_count(const uint32_t* M, uint32_t a, uint32_t b) {
-  uint32_t c = 0;
-  while (a < b) {
-    uint32_t wi = a >> 5, bo = a & 31;
-    uint32_t take = min(32 - bo, b - a);
-    uint32_t mask = (take == 32 ? 0xffffffffu : ((1u << take) - 1u)) << bo;
-    c += __popc(M[wi] & mask);
-    a += take;
-  }
-  return c;
-}
-
 // segmented (reset, k) scan element
 struct KSeg {
   int r;
@@ -315,8 +305,7 @@ NBZG_DEV int decode_serial(const uint8_t* bits, uint64_t& bp, uint64_t total, co
 __global__ void __launch_bounds__(kDThreads) decode_kernel(DArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint32_t* W = reinterpret_cast<uint32_t*>(smem);                 // [kDBufWords + 4]
-  uint32_t* M = W + kDBufWords + 4;                                // [kDBufWords + 1] start marks
-  uint16_t* S = reinterpret_cast<uint16_t*>(M + kDBufWords + 1);   // [16384]
+  uint16_t* S = reinterpret_cast<uint16_t*>(W + kDBufWords + 4);  // [16384]
   uint16_t* SS = S + kChunk;                                       // [kSmemSyms]
   uint8_t* LL = reinterpret_cast<uint8_t*>(SS + kSmemSyms);        // [1 << kLutBits]
   __shared__ uint64_t s_limit[64];
@@ -413,61 +402,88 @@ __global__ void __launch_bounds__(kDThreads) decode_kernel(DArgs a) {
         else if (endbit < 32) v &= ~(0xffffffffu >> endbit);
         W[j] = v;
       }
-      for (int j = tid; j < kDBufWords + 1; j += kDThreads) M[j] = 0;
     }
     __syncthreads();
 
-    // ---- 2. self-synchronising decode over T_dec threads (>= kSegBits bits each)
+    // ---- 2. self-synchronising decode over T_dec threads (>= kSegBits bits each).
+    // Phase 1: every thread decodes its slice from an arbitrary bit, counting
+    // codewords and remembering the first kRec codeword starts (registers).
     int tdec = (int)min((uint32_t)kDThreads, max(32u, ((Lb / kSegBits) + 31u) & ~31u));
     const bool active = tid < tdec;
     const uint32_t seg0 = active ? (uint32_t)(((uint64_t)Lb * tid) / tdec) : Lb;
     const uint32_t seg1 = active ? (uint32_t)(((uint64_t)Lb * (tid + 1)) / tdec) : Lb;
+    uint32_t rec[kRec];
+    int nrec = 0;
+    uint32_t cnt = 0;
     uint32_t start = seg0;
-    if (active) {
-      uint32_t p = seg0;
+    auto walk_full = [&](uint32_t s) -> uint32_t {  // decode [s, seg1): count + record
+      uint32_t p = s;
+      cnt = 0;
+      nrec = 0;
       while (p < seg1) {
         int l = code_len(peek32(W, p), T);
-        if (l == 0) {  // garbage from a wrong start: step one bit
+        if (l == 0) {  // garbage from a wrong start (incomplete codes only): step a bit
           p += 1;
           continue;
         }
-        mark_set(M, p);
+#pragma unroll
+        for (int r = 0; r < kRec; r++)
+          if (r == nrec) rec[r] = p;
+        nrec = min(nrec + 1, kRec);
+        cnt++;
         p += l;
       }
-      ends[tid] = p;
-    }
+      return p;
+    };
+    if (active) ends[tid] = walk_full(seg0);
     __syncthreads();
+    // Phase 2: thread t re-walks from its predecessor's true end until it lands
+    // on one of its remembered starts (resynchronised: later codewords agree).
     int invalid = 0;
     for (int iter = 0; iter <= kDThreads; iter++) {
       int changed = 0;
       if (active && tid > 0) {
         uint32_t s = ends[tid - 1];
         if (s != start) {
-          uint32_t p = s, sync = 0xffffffffu;
-          while (p < seg1) {  // walk the true path until it meets a marked start
-            if (mark_get(M, p)) {
-              sync = p;
+          uint32_t q = s;
+          int steps = 0, sync_j = -1;
+          while (q < seg1) {
+            int j = -1;
+#pragma unroll
+            for (int r = 0; r < kRec; r++)
+              if (r < nrec && rec[r] == q) j = r;
+            if (j >= 0) {
+              sync_j = j;
               break;
             }
-            int l = code_len(peek32(W, p), T);
+            if (nrec == kRec && q > rec[kRec - 1]) break;  // past the remembered window
+            int l = code_len(peek32(W, q), T);
             if (l == 0) {
               invalid = 1;
               break;
             }
-            p += l;
-          }
-          uint32_t stop = sync != 0xffffffffu ? sync : min(p, seg1);
-          mark_clear_range(M, seg0, max(stop, seg0));
-          uint32_t q = s;
-          while (q < stop) {
-            int l = code_len(peek32(W, q), T);
-            if (l == 0) break;
-            mark_set(M, q);
             q += l;
+            steps++;
           }
-          if (sync == 0xffffffffu) {
-            if (ends[tid] != p) changed = 1;
-            ends[tid] = p;
+          if (sync_j >= 0) {
+            cnt = cnt - (uint32_t)sync_j + (uint32_t)steps;
+            // refresh the remembered starts along the true path
+            uint32_t p = s;
+            int nr = 0;
+            for (int r = 0; r < kRec && p < seg1; r++) {
+              int l = code_len(peek32(W, p), T);
+              if (l == 0) break;
+#pragma unroll
+              for (int r2 = 0; r2 < kRec; r2++)
+                if (r2 == nr) rec[r2] = p;
+              nr++;
+              p += l;
+            }
+            nrec = nr;
+          } else if (!invalid) {
+            uint32_t e = walk_full(s);
+            if (ends[tid] != e) changed = 1;
+            ends[tid] = e;
           }
           start = s;
         }
@@ -475,10 +491,9 @@ __global__ void __launch_bounds__(kDThreads) decode_kernel(DArgs a) {
       if (!__syncthreads_or(changed)) break;
     }
     if (__syncthreads_or(invalid) && tid == 0) s_err = NBZG_INVALID_CODE;
-    // ---- 3. counts and decode into shared memory
-    uint32_t cnt = active ? mark_count(M, seg0, seg1) : 0u;
+    // ---- 3. output offsets and the final decode into shared memory
     uint32_t tot;
-    uint32_t o = block_excl_scan<uint32_t>(cnt, scan_tmp, &tot);
+    uint32_t o = block_excl_scan<uint32_t>(active ? cnt : 0u, scan_tmp, &tot);
     if (tid == 0 && (tot != (uint32_t)mc || ends[tdec - 1] != Lb) && !s_err)
       s_err = tot < (uint32_t)mc ? NBZG_TRUNCATED : NBZG_BAD_STREAM;
     __syncthreads();
@@ -704,8 +719,7 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
   count_launch();
   chunk_offsets_kernel<<<nf, 1024, 0, st>>>(a);
   trace_mark("dq_offsets", st);
-  size_t sm = (kDBufWords + 4) * 4 + (kDBufWords + 1) * 4 + kChunk * 2 + kSmemSyms * 2 +
-              (1 << kLutBits);
+  size_t sm = (kDBufWords + 4) * 4 + kChunk * 2 + kSmemSyms * 2 + (1 << kLutBits);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
