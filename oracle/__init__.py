@@ -14,7 +14,9 @@ Python layer:
 * ``resolve_field_bounds``   pipeline.py:157-181 / model.py:104-125
 * ``compress``               pipeline.py:447-526 (SZ-LV and SZ-LV-PRX only)
 * ``serialize``              io.py:105-125 (container v1; v2 = same layout,
-                             version 2, stream kind 3 = SZ_DQ)
+                             version 2, stream kind 3 = SZ_DQ: dual-quant
+                             codes, chain restart + chunk index every 16384
+                             symbols, escapes inline in the bitstream)
 * ``decompress``             pipeline.py:542-604 (SZ branch)
 
 Parity is PINNED: ``tests/test_oracle_golden.py`` checks this oracle
@@ -77,8 +79,8 @@ def lib():
             "orc_prx_order": (None, [P, I64, I64, P, I, I, P]),
             "orc_sz_quantize": (I64, [P, I64, D, I64, I, P, P, P]),
             "orc_sz_dequantize": (I64, [P, I64, P, I64, D, I64, I, P]),
-            "orc_dq_quantize": (I64, [P, I64, D, I64, I64, P, P, P]),
-            "orc_dq_dequantize": (I64, [P, I64, P, I64, D, I64, I64, P]),
+            "orc_dq_quantize": (I64, [P, I64, D, I64, I64, I64, P, P, P]),
+            "orc_dq_dequantize": (I64, [P, I64, P, I64, D, I64, I64, I64, P]),
             "orc_huffman_lengths": (None, [P, I64, P]),
             "orc_huffman_build": (I64, [P, I64, P, P]),
             "orc_huffman_tables": (None, [P, P, I64, P, P, P, P, P]),
@@ -209,23 +211,27 @@ def sz_dequantize(codes, esc, bound: float, half: int, use_lcf: bool = False):
     return out
 
 
-def dq_quantize(x: np.ndarray, bound: float, half: int, k_prev: int = 0):
-    """Dual-quant restatement (v2 stream kind SZ_DQ); returns codes, escapes, k_last."""
+def dq_quantize(x: np.ndarray, bound: float, half: int, k_prev: int = 0,
+                chunk: int = CHUNK_SYMBOLS):
+    """Dual-quant restatement (v2 stream kind SZ_DQ; chain restarts every
+    `chunk` symbols, 0 = never); returns codes, escapes, k_last."""
     x = _c(x, np.float32)
     codes = np.empty(x.size, np.int32)
     esc = np.empty(max(x.size, 1), np.float32)
     kl = np.zeros(1, np.int64)
-    ne = lib().orc_dq_quantize(_p(x), x.size, float(bound), half, int(k_prev), _p(codes),
-                               _p(esc), _p(kl))
+    ne = lib().orc_dq_quantize(_p(x), x.size, float(bound), half, int(k_prev), int(chunk),
+                               _p(codes), _p(esc), _p(kl))
     return codes, esc[:ne].copy(), int(kl[0])
 
 
-def dq_dequantize(codes, esc, bound: float, half: int, k_prev: int = 0):
+def dq_dequantize(codes, esc, bound: float, half: int, k_prev: int = 0,
+                  chunk: int = CHUNK_SYMBOLS):
     codes = _c(codes, np.int32)
     esc = _c(esc, np.float32)
     out = np.empty(codes.size, np.float32)
-    used = lib().orc_dq_dequantize(_p(codes), codes.size, _p(esc), esc.size, float(bound), half,
-                                   int(k_prev), _p(out))
+    escb = esc if esc.size else np.zeros(1, np.float32)
+    used = lib().orc_dq_dequantize(_p(codes), codes.size, _p(escb), esc.size, float(bound), half,
+                                   int(k_prev), int(chunk), _p(out))
     if used != esc.size:
         raise ValueError("escape count mismatch")
     return out

@@ -246,12 +246,13 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
   unsigned long long tbits;
   block_excl_scan<unsigned long long>(tb, scan_u64, &tbits);
   if (tid == 0) {
+    tbits += 32ull * fm.n_esc;  // v2: escape values ride inline in the bitstream
     fm.total_bits = tbits;
     uint64_t table_end = 8 + 5 * (uint64_t)k;
     fm.index_off = table_end + 8;
     fm.bits_off = (fm.index_off + 4 * (uint64_t)a.nchunks + 3) & ~3ull;
-    fm.esc_off = fm.bits_off + 4 * ((tbits + 31) / 32);
-    fm.payload_len = fm.esc_off + 4 * fm.n_esc;
+    fm.esc_off = fm.bits_off + 4 * ((tbits + 31) / 32);  // == payload end (no escape area)
+    fm.payload_len = fm.esc_off;
   }
 }
 

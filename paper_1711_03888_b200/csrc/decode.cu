@@ -6,40 +6,39 @@
 // (_kernels.py:348-374) and quantize.dequantize_field -> K.sz_dequantize
 // (_kernels.py:126-147).
 //
-// v2 (kind 3) decode, one CTA per 16384-symbol chunk located by the chunk
-// index:
-//   1. stage the chunk's bits in shared memory, re-aligned so bit 0 is the
-//      MSB of word 0 (any payload alignment);
-//   2. self-synchronising parallel Huffman decode: every thread decodes its
-//      slice (>= 192 bits) from an arbitrary bit, counting codewords and
-//      remembering its first 8 codeword starts in registers, then re-walks
-//      from its predecessor's true end until it lands on a remembered start
-//      (Huffman codes resynchronise within a few codewords) and corrects its
-//      count; a 2^16-entry code-length table in shared memory decodes;
-//   3. decode again from the true starts into shared memory;
-//   4. dequantise: escape offsets and the lattice index k carried into the
-//      chunk come from two decoupled look-backs; recon = f32(k * 2b) or the
-//      verbatim escape; 16 floats per thread written with 128-bit stores.
+// v2 (kind 3) decode: chunks are self-contained (the dual-quant chain
+// restarts at every 16384-symbol chunk and escape values sit inline in the
+// bitstream), so one WARP decodes one chunk with no cross-chunk traffic:
+//   1. persistent CTAs, one field each, stage a 2^16-entry code-length table
+//      and the canonical symbol table in shared memory once;
+//   2. each lane takes 1/32 of the chunk's bits and walks it from an
+//      arbitrary bit with a 64-bit register bit-reader (code lengths only):
+//      Huffman codes resynchronise within a few codewords, so the walk's end
+//      is the true codeword boundary after the slice;
+//   3. lane l decodes from lane l-1's end, counting codewords and summing
+//      the lattice deltas (reset at escapes); lanes whose start moved
+//      repeat until no end moves;
+//   4. warp scans give each lane its output offset and incoming lattice
+//      index; lanes decode their slice once more and write
+//      recon = f32(k * 2b) or the inline escape value.
 // Status words: INVALID_CODE / TRUNCATED / BAD_STREAM -> DecodeError.
 #include "nbzg_internal.cuh"
 #include "plan.h"
 
 namespace nbzg {
 
-constexpr int kDThreads = 1024;
-constexpr int kDPer = kChunk / kDThreads;  // 16 symbols per thread (dequant)
-constexpr int kDBufWords = 8192;           // 262144 bits of stream per chunk in smem
-constexpr int kLutBits = 16;       // length LUT index bits (u8 entries, 64 KiB)
-constexpr int kRec = 8;            // phase-1 codeword starts remembered per thread
-constexpr int kSmemSyms = 16384;  // sorted-symbol table staged in smem up to this k
-constexpr int kSegBits = 192;      // minimum bits per decoding thread (limits sync cascades)
+constexpr int kDWarps = 32;        // warps per CTA, each decodes one chunk at a time
+constexpr int kDThreads = kDWarps * 32;
+constexpr int kLutBits = 16;       // code-length table index bits (u8 entries, 64 KiB)
+constexpr int kSmemSyms = 16384;   // sorted-symbol table staged in smem up to this k
 
 struct DParsed {
   uint64_t n_esc, k, total_bits;
   uint64_t index_off, bits_off, esc_off;
   uint32_t min_len, max_len;
   uint32_t status;
-  uint32_t pad;
+  uint32_t esc_len;   // code length of symbol 0 (escape), 0 if absent
+  uint64_t esc_code;  // its canonical code word: first_code[esc_len] (rank 0)
   uint64_t first_code[64];
   uint32_t first_idx[64];
   uint32_t counts[64];
@@ -180,6 +179,9 @@ __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
   }
   if (tid == 0) {
     const uint64_t table_end = 8 + 5 * k;
+    const bool has_esc = ld_u32_bytes(p + 8) == 0;  // ascending symbols: 0 is first
+    P.esc_len = has_esc ? p[12] : 0;
+    P.esc_code = has_esc ? s_fc[p[12]] : 0;
     P.n_esc = n_esc;
     P.k = k;
     P.min_len = s_min;
@@ -188,11 +190,11 @@ __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
     if (table_end + 8 > (uint64_t)L) st = NBZG_TRUNCATED;
     else {
       P.total_bits = ld_u64_bytes(p + table_end);
-      if (F.kind == 3) {
+      if (F.kind == 3) {  // escapes inline: the bitstream ends the payload
         P.index_off = table_end + 8;
         P.bits_off = (P.index_off + 4 * (uint64_t)a.nchunks + 3) & ~3ull;
         P.esc_off = P.bits_off + 4 * ((P.total_bits + 31) / 32);
-        if (P.esc_off + 4 * n_esc != (uint64_t)L) st = NBZG_TRUNCATED;
+        if (P.esc_off != (uint64_t)L) st = NBZG_TRUNCATED;
       } else {
         P.index_off = 0;
         P.bits_off = table_end + 8;
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(1024) chunk_offsets_kernel(DArgs a) {
 }
 
 // ---------------------------------------------------------------- decode step
-// Shared-memory tables: a 2^12-entry code-LENGTH table (0 = invalid prefix,
+// Shared-memory tables: a 2^16-entry code-LENGTH table (0 = invalid prefix,
 // 0xFE = longer code) and the canonical left-justified limits
 // (encode.py:133-139): a codeword's length is the smallest l with
 // window < limit[l], its symbol ss[base[l] + (window >> (32 - l))].
@@ -247,11 +249,6 @@ struct DecTab {
   const uint32_t* ss;        // global sorted symbols
   int max_len;
 };
-
-NBZG_DEV uint32_t peek32(const uint32_t* W, uint32_t p) {
-  uint32_t i = p >> 5, s = p & 31;
-  return __funnelshift_l(W[i + 1], W[i], s);
-}
 
 // length of the codeword whose left-justified bits are v (0 = invalid)
 NBZG_DEV int code_len(uint32_t v, const DecTab& T) {
@@ -268,15 +265,62 @@ NBZG_DEV uint32_t code_sym(uint32_t v, int len, const DecTab& T) {
   return T.ss16 ? T.ss16[idx] : T.ss[idx];
 }
 
-// segmented (reset, k) scan element
+// MSB-first bit reader over a 4-byte-aligned-down view of the stream
+struct BitReader {
+  const uint32_t* g;  // aligned word base
+  uint64_t buf;       // next bits, MSB-aligned; >= 32 valid after refill
+  int nb;
+  uint64_t wi;        // next word to load
+};
+
+NBZG_DEV uint32_t bswap32(uint32_t w) { return __byte_perm(w, 0, 0x0123); }
+
+NBZG_DEV void br_init(BitReader& R, const uint32_t* g, uint32_t a0, uint64_t pos) {
+  uint64_t q = pos + a0;
+  uint64_t w = q >> 5;
+  int o = (int)(q & 31);
+  R.g = g;
+  R.buf = (((uint64_t)bswap32(__ldg(g + w)) << 32) | bswap32(__ldg(g + w + 1))) << o;
+  R.nb = 64 - o;
+  R.wi = w + 2;
+}
+NBZG_DEV uint32_t br_peek(const BitReader& R) { return (uint32_t)(R.buf >> 32); }
+NBZG_DEV void br_skip(BitReader& R, int l) {  // l <= 32
+  R.buf <<= l;
+  R.nb -= l;
+  if (R.nb < 32) {
+    R.buf |= (uint64_t)bswap32(__ldg(R.g + R.wi)) << (32 - R.nb);
+    R.wi++;
+    R.nb += 32;
+  }
+}
+
+// segmented (reset, k) scan element: a later reset wins, otherwise values add
 struct KSeg {
   int r;
   long long v;
 };
 NBZG_DEV KSeg kseg_op(KSeg a, KSeg b) { return b.r ? b : KSeg{a.r, a.v + b.v}; }
 
+NBZG_DEV long long esc_k(float v, const DField& F) {
+  bool fast;
+  double kd = lattice_index<false>(v, F.inv32, F.inv, F.twob, fast);
+  if (!fast) kd = fmin(fmax(kd, -kDqKmax), kDqKmax);
+  return (long long)kd;
+}
+
+// Decode symbols from `pos` until the position reaches `stop`: counts
+// codewords and accumulates the segmented lattice sum.  Returns the end
+// position (first codeword start >= stop), or ~0 on an invalid code.
+struct WalkOut {
+  uint64_t end;
+  uint32_t cnt;
+  KSeg agg;
+  uint64_t last_reset;  // position of the last escape codeword (or 0)
+};
+
 // bit-serial canonical decode of one symbol straight from global bytes
-// (fallback for chunks too large for the shared buffer, and the v1 path).
+// (v1 compat path and pathological > 32-bit codes).
 NBZG_DEV int decode_serial(const uint8_t* bits, uint64_t& bp, uint64_t total, const DParsed& P,
                            const uint32_t* ss, uint32_t& sym) {
   uint64_t code = 0;
@@ -299,59 +343,33 @@ NBZG_DEV int decode_serial(const uint8_t* bits, uint64_t& bp, uint64_t total, co
 }
 
 // ---------------------------------------------------------------- D2: decode
-// Error handling rule: once a CTA holds a chunk ticket it ALWAYS publishes
-// both look-back values (successors spin on them); failures only set the
-// status word.
-__global__ void __launch_bounds__(kDThreads) decode_kernel(DArgs a) {
+__global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  uint32_t* W = reinterpret_cast<uint32_t*>(smem);                 // [kDBufWords + 4]
-  uint16_t* S = reinterpret_cast<uint16_t*>(W + kDBufWords + 4);  // [16384]
-  uint16_t* SS = S + kChunk;                                       // [kSmemSyms]
-  uint8_t* LL = reinterpret_cast<uint8_t*>(SS + kSmemSyms);        // [1 << kLutBits]
+  uint8_t* LL = smem;                                               // [1 << kLutBits]
+  uint16_t* SS = reinterpret_cast<uint16_t*>(smem + (1 << kLutBits));  // [kSmemSyms]
   __shared__ uint64_t s_limit[64];
   __shared__ int32_t s_base[64];
-  __shared__ uint32_t ends[kDThreads];
-  __shared__ uint32_t scan_tmp[33];
-  __shared__ KSeg kscan[33];
-  __shared__ int64_t s_c;
-  __shared__ unsigned long long s_eoff;
-  __shared__ long long s_carry;
-  __shared__ uint32_t s_err;
+  __shared__ int s_next;
 
-  const int fi = blockIdx.y;
+  const int fi = blockIdx.x % a.nf;
+  const int grp = blockIdx.x / a.nf, ngrp = gridDim.x / a.nf;
   const DField& F = a.f[fi];
   const DParsed& P = a.parsed[fi];
   if (F.kind != 3 || P.status || *a.status) return;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid == 0) {
-    s_c = atomicAdd(&a.tickets[fi], 1u);
-    s_err = 0;
-  }
-  __syncthreads();
-  const int64_t c = s_c;
-  if (c >= a.nchunks) return;
-  const uint64_t* choff = a.choff + fi * (a.nchunks + 1);
-  const uint64_t B = choff[c];
-  const uint32_t Lb = (uint32_t)(choff[c + 1] - B);
-  const int64_t c0 = c * kChunk;
-  const int mc = (int)min((int64_t)kChunk, a.n - c0);
-  const int half = a.half;
+  const int64_t cb = (a.nchunks * grp) / ngrp, ce = (a.nchunks * (grp + 1)) / ngrp;
+  if (cb >= ce) return;
+  const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t* ss = a.ssyms + fi * a.nbins;
 
-  DecTab T;
-  T.ll = LL;
-  T.limit = s_limit;
-  T.base = s_base;
-  T.ss = ss;
-  T.ss16 = P.k <= (uint64_t)kSmemSyms ? SS : nullptr;
-  T.max_len = (int)P.max_len;
+  // ---- stage the decode tables once per CTA
   {
-    const uint32_t* gl = reinterpret_cast<const uint32_t*>(
-        reinterpret_cast<const uint8_t*>(a.lut) + fi * (1 << kLutBits));
-    uint32_t* sl = reinterpret_cast<uint32_t*>(LL);
-    for (int i = tid; i < (1 << kLutBits) / 4; i += kDThreads) sl[i] = gl[i];
+    const uint4* gl = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(a.lut) +
+                                                     (size_t)fi * (1 << kLutBits));
+    uint4* sl = reinterpret_cast<uint4*>(LL);
+    for (int i = tid; i < (1 << kLutBits) / 16; i += kDThreads) sl[i] = gl[i];
   }
-  if (T.ss16)
+  const bool small_k = P.k <= (uint64_t)kSmemSyms;
+  if (small_k)
     for (uint32_t i = tid; i < (uint32_t)P.k; i += kDThreads) SS[i] = (uint16_t)ss[i];
   if (tid < 64) {
     const int l = tid;
@@ -364,269 +382,204 @@ __global__ void __launch_bounds__(kDThreads) decode_kernel(DArgs a) {
     s_limit[l] = l > (int)P.max_len ? ~0ull : lim;
     s_base[l] = bs;
   }
-  const bool big = (uint64_t)Lb + 64 > (uint64_t)kDBufWords * 32 || P.max_len > 32;
-  if (big) {
-    // rare: > 16 bits/symbol on average in this chunk -- sequential decode
-    if (tid == 0) {
-      uint64_t bp = B, total = B + Lb;
-      for (int i = 0; i < mc; i++) {
-        uint32_t sym = 0;
-        int l = decode_serial(F.payload + P.bits_off, bp, total, P, ss, sym);
-        if (l < 0) {
-          s_err = (uint32_t)(-l);
-          sym = 1;
-        }
-        S[i] = (uint16_t)sym;
-      }
-      if (bp != total && !s_err) s_err = NBZG_BAD_STREAM;
-    }
-    __syncthreads();
-  } else {
-    // ---- 1. stage bits: W[j] = 32 stream bits starting at chunk bit 32j (MSB-first)
-    {
-      const uint8_t* bits = F.payload + P.bits_off;
-      const uint64_t byte0 = B >> 3;
-      const uintptr_t addr = reinterpret_cast<uintptr_t>(bits) + byte0;
-      const uint32_t* g = reinterpret_cast<const uint32_t*>(addr & ~uintptr_t(3));
-      const uint32_t sh = (uint32_t)((addr & 3) * 8 + (B & 7));
-      const int nw = (int)((Lb + 31) / 32) + 2;
-      const uint64_t avail_bytes =
-          (uint64_t)(reinterpret_cast<uintptr_t>(F.payload + F.payload_len + 16) -
-                     reinterpret_cast<uintptr_t>(g));
-      for (int j = tid; j < nw; j += kDThreads) {
-        uint32_t w0 = (4ull * j + 4 <= avail_bytes) ? __byte_perm(g[j], 0, 0x0123) : 0u;
-        uint32_t w1 = (4ull * j + 8 <= avail_bytes) ? __byte_perm(g[j + 1], 0, 0x0123) : 0u;
-        uint32_t v = sh ? __funnelshift_l(w1, w0, sh) : w0;
-        int64_t endbit = (int64_t)Lb - 32ll * j;  // zero bits past the chunk end
-        if (endbit <= 0) v = 0;
-        else if (endbit < 32) v &= ~(0xffffffffu >> endbit);
-        W[j] = v;
-      }
-    }
-    __syncthreads();
+  if (tid == 0) s_next = (int)cb;
+  __syncthreads();
+  DecTab T;
+  T.ll = LL;
+  T.limit = s_limit;
+  T.base = s_base;
+  T.ss = ss;
+  T.ss16 = small_k ? SS : nullptr;
+  T.max_len = (int)P.max_len;
 
-    // ---- 2. self-synchronising decode over T_dec threads (>= kSegBits bits each).
-    // Phase 1: every thread decodes its slice from an arbitrary bit, counting
-    // codewords and remembering the first kRec codeword starts (registers).
-    int tdec = (int)min((uint32_t)kDThreads, max(32u, ((Lb / kSegBits) + 31u) & ~31u));
-    const bool active = tid < tdec;
-    const uint32_t seg0 = active ? (uint32_t)(((uint64_t)Lb * tid) / tdec) : Lb;
-    const uint32_t seg1 = active ? (uint32_t)(((uint64_t)Lb * (tid + 1)) / tdec) : Lb;
-    uint32_t rec[kRec];
-    int nrec = 0;
-    uint32_t cnt = 0;
-    uint32_t start = seg0;
-    auto walk_full = [&](uint32_t s) -> uint32_t {  // decode [s, seg1): count + record
-      uint32_t p = s;
-      cnt = 0;
-      nrec = 0;
-      while (p < seg1) {
-        int l = code_len(peek32(W, p), T);
-        if (l == 0) {  // garbage from a wrong start (incomplete codes only): step a bit
-          p += 1;
+  const uintptr_t bits_addr = reinterpret_cast<uintptr_t>(F.payload + P.bits_off);
+  const uint32_t* G = reinterpret_cast<const uint32_t*>(bits_addr & ~uintptr_t(3));
+  const uint32_t a0 = (uint32_t)(bits_addr & 3) * 8;
+  const uint64_t* choff = a.choff + fi * (a.nchunks + 1);
+  const int half = a.half;
+  const int esc_len = (int)P.esc_len;
+  const uint32_t esc_code = (uint32_t)P.esc_code;
+
+  // one symbol step: decode at the reader, consume code (+ inline escape)
+  // and fold the lattice delta into `agg`; returns the code length (0 invalid)
+  auto step = [&](BitReader& R, KSeg& agg, bool& esc, float& ev) -> int {
+    uint32_t v = br_peek(R);
+    int l = code_len(v, T);
+    if (l == 0) return 0;
+    uint32_t sym = code_sym(v, l, T);
+    br_skip(R, l);
+    esc = sym == 0;
+    if (esc) {
+      ev = __uint_as_float(br_peek(R));
+      br_skip(R, 32);
+      agg = KSeg{1, esc_k(ev, F)};
+      return l + 32;
+    }
+    agg.v += (long long)((int)sym - half - 1);
+    return l;
+  };
+
+  while (true) {
+    int c32 = 0;
+    if (lane == 0) c32 = atomicAdd(&s_next, 1);
+    const int64_t c = __shfl_sync(0xffffffffu, c32, 0);
+    if (c >= ce) break;
+    const uint64_t B = choff[c];
+    const uint64_t Tb = choff[c + 1] - B;
+    const uint64_t E = B + Tb;
+    const int64_t c0 = c * kChunk;
+    const int mc = (int)min((int64_t)kChunk, a.n - c0);
+    const uint64_t seg0 = B + (Tb * lane) / 32, seg1 = B + (Tb * (lane + 1)) / 32;
+    int err = 0;
+
+    // ---- phase 1: code lengths only, from an arbitrary start -> slice end
+    uint64_t end = seg0;
+    {
+      BitReader R;
+      br_init(R, G, a0, seg0);
+      uint64_t pos = seg0;
+      while (pos < seg1) {
+        uint32_t v = br_peek(R);
+        int l = code_len(v, T);
+        if (l == 0) {  // garbage from a wrong start (incomplete codes): step a bit
+          pos += 1;
+          br_init(R, G, a0, pos);
           continue;
         }
-#pragma unroll
-        for (int r = 0; r < kRec; r++)
-          if (r == nrec) rec[r] = p;
-        nrec = min(nrec + 1, kRec);
-        cnt++;
-        p += l;
-      }
-      return p;
-    };
-    if (active) ends[tid] = walk_full(seg0);
-    __syncthreads();
-    // Phase 2: thread t re-walks from its predecessor's true end until it lands
-    // on one of its remembered starts (resynchronised: later codewords agree).
-    int invalid = 0;
-    for (int iter = 0; iter <= kDThreads; iter++) {
-      int changed = 0;
-      if (active && tid > 0) {
-        uint32_t s = ends[tid - 1];
-        if (s != start) {
-          uint32_t q = s;
-          int steps = 0, sync_j = -1;
-          while (q < seg1) {
-            int j = -1;
-#pragma unroll
-            for (int r = 0; r < kRec; r++)
-              if (r < nrec && rec[r] == q) j = r;
-            if (j >= 0) {
-              sync_j = j;
-              break;
-            }
-            if (nrec == kRec && q > rec[kRec - 1]) break;  // past the remembered window
-            int l = code_len(peek32(W, q), T);
-            if (l == 0) {
-              invalid = 1;
-              break;
-            }
-            q += l;
-            steps++;
-          }
-          if (sync_j >= 0) {
-            cnt = cnt - (uint32_t)sync_j + (uint32_t)steps;
-            // refresh the remembered starts along the true path
-            uint32_t p = s;
-            int nr = 0;
-            for (int r = 0; r < kRec && p < seg1; r++) {
-              int l = code_len(peek32(W, p), T);
-              if (l == 0) break;
-#pragma unroll
-              for (int r2 = 0; r2 < kRec; r2++)
-                if (r2 == nr) rec[r2] = p;
-              nr++;
-              p += l;
-            }
-            nrec = nr;
-          } else if (!invalid) {
-            uint32_t e = walk_full(s);
-            if (ends[tid] != e) changed = 1;
-            ends[tid] = e;
-          }
-          start = s;
+        br_skip(R, l);
+        pos += l;
+        if (l == esc_len && (v >> (32 - l)) == esc_code) {  // inline escape value
+          br_skip(R, 32);
+          pos += 32;
         }
       }
-      if (!__syncthreads_or(changed)) break;
+      end = pos;
     }
-    if (__syncthreads_or(invalid) && tid == 0) s_err = NBZG_INVALID_CODE;
-    // ---- 3. output offsets and the final decode into shared memory
-    uint32_t tot;
-    uint32_t o = block_excl_scan<uint32_t>(active ? cnt : 0u, scan_tmp, &tot);
-    if (tid == 0 && (tot != (uint32_t)mc || ends[tdec - 1] != Lb) && !s_err)
-      s_err = tot < (uint32_t)mc ? NBZG_TRUNCATED : NBZG_BAD_STREAM;
-    __syncthreads();
-    if (!s_err && active) {
-      uint32_t p = tid == 0 ? 0 : ends[tid - 1];
-      int bad = 0;
-      for (uint32_t i = 0; i < cnt; i++) {
-        uint32_t v = peek32(W, p);
-        int l = code_len(v, T);
-        if (l == 0) {
-          bad = 1;
-          break;
+    // ---- phase 2: decode from the predecessor's end (the true start once
+    // lane l-1 is synchronised, which Huffman self-synchronisation makes
+    // near-certain over a slice); recount and iterate while any end moves
+    uint32_t cnt = 0;
+    KSeg agg{0, 0};
+    uint64_t start = ~0ull;
+    for (int iter = 0; iter < 33; iter++) {
+      uint64_t s = __shfl_up_sync(0xffffffffu, end, 1);
+      if (lane == 0) s = B;
+      bool changed = false;
+      if (s != start && !err) {
+        BitReader R;
+        br_init(R, G, a0, s);
+        uint64_t p = s;
+        cnt = 0;
+        agg = KSeg{0, 0};
+        while (p < seg1) {
+          bool esc;
+          float ev;
+          int l = step(R, agg, esc, ev);
+          if (l == 0) {
+            err = NBZG_INVALID_CODE;
+            break;
+          }
+          p += l;
+          cnt++;
         }
-        if (o + i < (uint32_t)kChunk) S[o + i] = (uint16_t)code_sym(v, l, T);
-        p += l;
+        if (p != end) changed = true;
+        end = p;
+        start = s;
       }
-      if (bad) atomicCAS(&s_err, 0u, (uint32_t)NBZG_INVALID_CODE);
+      if (!__any_sync(0xffffffffu, changed)) break;
     }
-    __syncthreads();
-    if (s_err)
-      for (int i = tid; i < mc; i += kDThreads) S[i] = 1;  // keep going: publish look-backs
-    __syncthreads();
-  }
 
-  // ---- 4. dequantise (orc_dq_dequantize)
-  const int q0 = tid * kDPer;
-  const int qn = max(0, min(kDPer, mc - q0));
-  uint32_t my_esc = 0;
-  for (int j = 0; j < qn; j++) my_esc += S[q0 + j] == 0;
-  uint32_t etot;
-  uint32_t eo = block_excl_scan<uint32_t>(my_esc, scan_tmp, &etot);
-  if (tid < 32) {
-    uint64_t eo2 = lookback_sum(a.lb + (fi * 2 + 0) * a.nchunks, c, etot);
-    if (tid == 0) s_eoff = eo2;
-  }
-  __syncthreads();
-  const uint8_t* escp = F.payload + P.esc_off;
-  const uint64_t e_idx = s_eoff + eo;
-  const bool esc_ok = e_idx + my_esc <= P.n_esc;
-  if (!esc_ok) atomicCAS(&s_err, 0u, (uint32_t)NBZG_BAD_STREAM);
-  KSeg agg{0, 0};
-  {
-    uint64_t ei = e_idx;
-    for (int j = 0; j < qn; j++) {
-      uint32_t code = S[q0 + j];
-      if (code == 0) {
-        float v = esc_ok ? __uint_as_float(ld_u32_bytes(escp + 4 * ei)) : 0.0f;
-        ei++;
-        bool fast;
-        double kd = lattice_index<false>(v, F.inv32, F.inv, F.twob, fast);
-        if (!fast) kd = fmin(fmax(kd, -kDqKmax), kDqKmax);
-        agg = KSeg{1, (long long)kd};
-      } else {
-        agg.v += (long long)((int)code - half - 1);
-      }
-    }
-  }
-  // block-wide exclusive segmented scan of agg
-  KSeg inc = agg;
+    // ---- offsets, incoming lattice index, validation
+    uint32_t o = warp_incl_scan<uint32_t>(cnt) - cnt;
+    uint32_t tot = __shfl_sync(0xffffffffu, o + cnt, 31);
+    KSeg inc = agg;
 #pragma unroll
-  for (int o2 = 1; o2 < 32; o2 <<= 1) {
-    KSeg u;
-    u.r = __shfl_up_sync(0xffffffffu, inc.r, o2);
-    u.v = __shfl_up_sync(0xffffffffu, inc.v, o2);
-    if (lane >= o2) inc = kseg_op(u, inc);
-  }
-  if (lane == 31) kscan[wid] = inc;
-  __syncthreads();
-  if (wid == 0) {
-    KSeg wi = kscan[lane];
-#pragma unroll
-    for (int o2 = 1; o2 < 32; o2 <<= 1) {
+    for (int d = 1; d < 32; d <<= 1) {
       KSeg u;
-      u.r = __shfl_up_sync(0xffffffffu, wi.r, o2);
-      u.v = __shfl_up_sync(0xffffffffu, wi.v, o2);
-      if (lane >= o2) wi = kseg_op(u, wi);
+      u.r = __shfl_up_sync(0xffffffffu, inc.r, d);
+      u.v = __shfl_up_sync(0xffffffffu, inc.v, d);
+      if (lane >= d) inc = kseg_op(u, inc);
     }
     KSeg ex;
-    ex.r = __shfl_up_sync(0xffffffffu, wi.r, 1);
-    ex.v = __shfl_up_sync(0xffffffffu, wi.v, 1);
+    ex.r = __shfl_up_sync(0xffffffffu, inc.r, 1);
+    ex.v = __shfl_up_sync(0xffffffffu, inc.v, 1);
     if (lane == 0) ex = KSeg{0, 0};
-    __syncwarp();
-    kscan[lane] = ex;
-    if (lane == 31) kscan[32] = wi;  // chunk aggregate
-  }
-  __syncthreads();
-  KSeg exw;
-  exw.r = __shfl_up_sync(0xffffffffu, inc.r, 1);
-  exw.v = __shfl_up_sync(0xffffffffu, inc.v, 1);
-  if (lane == 0) exw = KSeg{0, 0};
-  KSeg before = kseg_op(kscan[wid], exw);
-  if (tid < 32) {
-    KSeg ca = kscan[32];
-    long long cr = lookback_kcarry(a.lb + (fi * 2 + 1) * a.nchunks, c, ca.r != 0, ca.v);
-    if (tid == 0) {
-      s_carry = cr;
-      if (s_err) fail(a.status, s_err);
+    long long k = ex.v;  // chunk start: k = 0, so the incoming index is the prefix value
+    uint64_t last_end = __shfl_sync(0xffffffffu, end, 31);
+    err = __reduce_max_sync(0xffffffffu, (unsigned)err);
+    if (!err && (tot != (uint32_t)mc || last_end != E))
+      err = tot < (uint32_t)mc ? NBZG_TRUNCATED : NBZG_BAD_STREAM;
+    if (err) {
+      if (lane == 0) fail(a.status, (uint32_t)err);
+      continue;
     }
-  }
-  __syncthreads();
-  long long k = before.r ? before.v : s_carry + before.v;
-  float outv[kDPer];
-  {
-    uint64_t ei = e_idx;
-#pragma unroll
-    for (int j = 0; j < kDPer; j++) {
-      outv[j] = 0.0f;
-      if (j < qn) {
-        uint32_t code = S[q0 + j];
-        if (code == 0) {
-          float v = esc_ok ? __uint_as_float(ld_u32_bytes(escp + 4 * ei)) : 0.0f;
-          ei++;
-          bool fast;
-          double kd = lattice_index<false>(v, F.inv32, F.inv, F.twob, fast);
-          if (!fast) kd = fmin(fmax(kd, -kDqKmax), kDqKmax);
-          k = (long long)kd;
-          outv[j] = v;
+
+    // ---- phase 3: decode from the true start and write
+    {
+      uint64_t s = __shfl_up_sync(0xffffffffu, end, 1);
+      if (lane == 0) s = B;
+      BitReader R;
+      br_init(R, G, a0, s);
+      float* dst = F.out + c0 + o;
+      for (uint32_t i = 0; i < cnt; i++) {
+        uint32_t v = br_peek(R);
+        int l = code_len(v, T);
+        uint32_t sym = code_sym(v, l, T);
+        br_skip(R, l);
+        float outv;
+        if (sym == 0) {
+          outv = __uint_as_float(br_peek(R));
+          br_skip(R, 32);
+          k = esc_k(outv, F);
         } else {
-          k += (long long)((int)code - half - 1);
-          outv[j] = (float)__dmul_rn((double)k, F.twob);
+          k += (long long)((int)sym - half - 1);
+          outv = (float)__dmul_rn((double)k, F.twob);
         }
+        dst[i] = outv;
       }
     }
   }
-  float* dst = F.out + c0 + q0;
-  if (qn == kDPer && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-    float4* d4 = reinterpret_cast<float4*>(dst);
-#pragma unroll
-    for (int q = 0; q < 4; q++)
-      d4[q] = make_float4(outv[4 * q], outv[4 * q + 1], outv[4 * q + 2], outv[4 * q + 3]);
-  } else {
-    for (int j = 0; j < qn; j++) dst[j] = outv[j];
+}
+
+// v2 streams with codes longer than 32 bits (pathological alphabets):
+// serial decode per chunk (one thread per chunk), same semantics.
+__global__ void decode_v2_serial_kernel(DArgs a) {
+  const int fi = blockIdx.y;
+  const DField& F = a.f[fi];
+  const DParsed& P = a.parsed[fi];
+  if (F.kind != 3 || P.status || P.max_len <= 32) return;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= a.nchunks) return;
+  const uint64_t* choff = a.choff + fi * (a.nchunks + 1);
+  const uint8_t* bits = F.payload + P.bits_off;
+  uint64_t bp = choff[c], endp = choff[c + 1];
+  const uint32_t* ss = a.ssyms + fi * a.nbins;
+  const int64_t c0 = c * kChunk, c1 = min(a.n, c0 + kChunk);
+  long long k = 0;
+  for (int64_t i = c0; i < c1; i++) {
+    uint32_t sym = 0;
+    int l = decode_serial(bits, bp, endp, P, ss, sym);
+    if (l < 0) {
+      fail(a.status, (uint32_t)(-l));
+      return;
+    }
+    float outv;
+    if (sym == 0) {
+      if (bp + 32 > endp) {
+        fail(a.status, NBZG_TRUNCATED);
+        return;
+      }
+      uint32_t u = 0;
+      for (int b = 0; b < 32; b++, bp++) u = (u << 1) | ((bits[bp >> 3] >> (7 - (bp & 7))) & 1u);
+      outv = __uint_as_float(u);
+      k = esc_k(outv, F);
+    } else {
+      k += (long long)((int)sym - a.half - 1);
+      outv = (float)__dmul_rn((double)k, F.twob);
+    }
+    F.out[i] = outv;
   }
+  if (bp != endp) fail(a.status, NBZG_BAD_STREAM);
 }
 
 // ---------------------------------------------------------------- v1 compat
@@ -719,7 +672,7 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
   count_launch();
   chunk_offsets_kernel<<<nf, 1024, 0, st>>>(a);
   trace_mark("dq_offsets", st);
-  size_t sm = (kDBufWords + 4) * 4 + kChunk * 2 + kSmemSyms * 2 + (1 << kLutBits);
+  size_t sm = (1 << kLutBits) + kSmemSyms * 2;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -731,10 +684,14 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
     any_v1 |= fields[i].kind == 0;
   }
   if (any_v2) {
+    int groups = max(1, sm_count() / nf);
+    if (groups > a.nchunks) groups = (int)a.nchunks;
     count_launch();
-    decode_kernel<<<dim3((unsigned)a.nchunks, nf), kDThreads, sm, st>>>(a);
+    decode_kernel<<<groups * nf, kDThreads, sm, st>>>(a);
+    count_launch();
+    decode_v2_serial_kernel<<<dim3((unsigned)((a.nchunks + 63) / 64), nf), 64, 0, st>>>(a);
+    trace_mark("dq_decode", st);
   }
-  if (any_v2) trace_mark("dq_decode", st);
   if (any_v1) {
     count_launch();
     decode_v1_kernel<<<nf, 32, 0, st>>>(a);

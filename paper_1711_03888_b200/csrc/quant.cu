@@ -5,7 +5,8 @@
 // The reference's reconstruct-and-predict chain is sequential; this kernel
 // computes the parallel "pre-quantise then difference" restatement
 // (oracle/nbz_oracle.c orc_dq_quantize):
-//     k_i = rint(x_i / 2b) (lattice index), q_i = k_i - k_{i-1},
+//     k_i = rint(x_i / 2b) (lattice index), q_i = k_i - k_{i-1} (k_{-1} = 0
+//     at every 16384-symbol chunk start, so v2 chunks decode independently),
 //     code_i = q_i + half + 1 if q_i in [-half, half-2] and
 //              |x_i - f32(k_i * 2b)| <= b, else 0 (escape).
 //
@@ -183,6 +184,7 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
         float xv = SORTED ? xs[min((int)ps[p], m - 1)] : xs[p];
         bool fast;
         int64_t k = dq_index(xv, fm, fast);
+        if (((t0 + p) & (kChunk - 1)) == 0) kprev = 0;  // chain restarts every v2 chunk
         int64_t q = k - kprev;
         bool ok = q >= -half && q <= half - 2;
         if (ok && !fast) {

@@ -18,7 +18,7 @@ from paper_1711_03888_b200 import datagen
 
 def header_functions():
     src = open(os.path.join(ROOT, "include", "nbzg.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:const char \*\s*|size_t\s+|int\s+)(nbzg_\w+)\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const char \*\s*|size_t\s+|int\s+|unsigned long long\s+)(nbzg_\w+)\(", src, re.M)))
 
 
 def test_library_exports_every_declared_symbol():

@@ -118,9 +118,14 @@ def test_dual_quant_bound_and_roundtrip(oracle_lib, rng):
         assert np.all(np.abs(x.astype(np.float64) - y.astype(np.float64)) <= b)
         assert (codes == 0).sum() == esc.size
         # chaining over a split point with the carried k gives identical codes
-        c1, e1, k1 = O.dq_quantize(x[:7000], b, 32768)
-        c2, e2, _ = O.dq_quantize(x[7000:], b, 32768, k_prev=k1)
-        assert np.array_equal(np.concatenate([c1, c2]), codes)
+        c0, _, _ = O.dq_quantize(x, b, 32768, chunk=0)
+        c1, e1, k1 = O.dq_quantize(x[:7000], b, 32768, chunk=0)
+        c2, e2, _ = O.dq_quantize(x[7000:], b, 32768, k_prev=k1, chunk=0)
+        assert np.array_equal(np.concatenate([c1, c2]), c0)
+        # with chunk restarts, each 16384-symbol chunk is independent
+        for lo in range(0, x.size, 16384):
+            cc, _, _ = O.dq_quantize(x[lo:lo + 16384], b, 32768, chunk=0)
+            assert np.array_equal(cc, codes[lo:lo + 16384])
 
 
 @pytest.mark.parametrize("case", ["hacc34", "amdf40k", "sweep_hacc20", "noise20k"])
