@@ -22,6 +22,8 @@
 //      index; lanes decode their slice once more and write
 //      recon = f32(k * 2b) or the inline escape value.
 // Status words: INVALID_CODE / TRUNCATED / BAD_STREAM -> DecodeError.
+#include <cstdio>
+
 #include "nbzg_internal.cuh"
 #include "plan.h"
 
@@ -250,14 +252,19 @@ struct DecTab {
   int max_len;
 };
 
-// length of the codeword whose left-justified bits are v (0 = invalid)
+// length of the codeword whose left-justified bits are v (0 = invalid).
+// Branch-light so a warp never splits for long codes: the long-code search
+// runs a field-uniform trip count without early exit.
 NBZG_DEV int code_len(uint32_t v, const DecTab& T) {
   int l = T.ll[v >> (32 - kLutBits)];
-  if (l < 0xFE) return l;
+  if (l >= 0xFE) {
+    int r = 0;
 #pragma unroll 1
-  for (int len = kLutBits + 1; len <= T.max_len; len++)
-    if ((uint64_t)v < T.limit[len]) return len;
-  return 0;
+    for (int len = T.max_len; len > kLutBits; len--)
+      r = ((uint64_t)v < T.limit[len]) ? len : r;
+    l = r;
+  }
+  return l;
 }
 
 NBZG_DEV uint32_t code_sym(uint32_t v, int len, const DecTab& T) {
@@ -405,18 +412,19 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
   auto step = [&](BitReader& R, KSeg& agg, bool& esc, float& ev) -> int {
     uint32_t v = br_peek(R);
     int l = code_len(v, T);
-    if (l == 0) return 0;
-    uint32_t sym = code_sym(v, l, T);
-    br_skip(R, l);
-    esc = sym == 0;
+    uint32_t sym = l ? code_sym(v, l, T) : 1u;
+    br_skip(R, l ? l : 1);
+    esc = l && sym == 0;
+    int used = l;
     if (esc) {
       ev = __uint_as_float(br_peek(R));
       br_skip(R, 32);
       agg = KSeg{1, esc_k(ev, F)};
-      return l + 32;
+      used = l + 32;
+    } else {
+      agg.v += (long long)((int)sym - half - 1);
     }
-    agg.v += (long long)((int)sym - half - 1);
-    return l;
+    return used;
   };
 
   while (true) {
@@ -438,19 +446,22 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
       BitReader R;
       br_init(R, G, a0, seg0);
       uint64_t pos = seg0;
-      while (pos < seg1) {
-        uint32_t v = br_peek(R);
-        int l = code_len(v, T);
-        if (l == 0) {  // garbage from a wrong start (incomplete codes): step a bit
-          pos += 1;
-          br_init(R, G, a0, pos);
-          continue;
-        }
-        br_skip(R, l);
-        pos += l;
-        if (l == esc_len && (v >> (32 - l)) == esc_code) {  // inline escape value
-          br_skip(R, 32);
-          pos += 32;
+      // warp-uniform loop with a predicated body (keeps the warp converged)
+      while (__any_sync(0xffffffffu, pos < seg1)) {
+        if (pos < seg1) {
+          uint32_t v = br_peek(R);
+          int l = code_len(v, T);
+          if (l == 0) {  // garbage from a wrong start (incomplete codes): step a bit
+            pos += 1;
+            br_init(R, G, a0, pos);
+          } else {
+            br_skip(R, l);
+            pos += l;
+            if (l == esc_len && (v >> (32 - l)) == esc_code) {  // inline escape value
+              br_skip(R, 32);
+              pos += 32;
+            }
+          }
         }
       }
       end = pos;
@@ -465,23 +476,29 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
       uint64_t s = __shfl_up_sync(0xffffffffu, end, 1);
       if (lane == 0) s = B;
       bool changed = false;
-      if (s != start && !err) {
-        BitReader R;
-        br_init(R, G, a0, s);
-        uint64_t p = s;
+      const bool redo = s != start && !err;
+      BitReader R;
+      br_init(R, G, a0, redo ? s : seg1);
+      uint64_t p = redo ? s : seg1;
+      if (redo) {
         cnt = 0;
         agg = KSeg{0, 0};
-        while (p < seg1) {
+      }
+      while (__any_sync(0xffffffffu, p < seg1)) {
+        if (p < seg1) {
           bool esc;
           float ev;
           int l = step(R, agg, esc, ev);
           if (l == 0) {
             err = NBZG_INVALID_CODE;
-            break;
+            p = seg1;  // stop this lane
+          } else {
+            p += l;
+            cnt++;
           }
-          p += l;
-          cnt++;
         }
+      }
+      if (redo) {
         if (p != end) changed = true;
         end = p;
         start = s;
@@ -521,7 +538,9 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
       BitReader R;
       br_init(R, G, a0, s);
       float* dst = F.out + c0 + o;
-      for (uint32_t i = 0; i < cnt; i++) {
+      const uint32_t maxcnt = __reduce_max_sync(0xffffffffu, cnt);
+      for (uint32_t i = 0; i < maxcnt; i++) {
+        if (i >= cnt) continue;
         uint32_t v = br_peek(R);
         int l = code_len(v, T);
         uint32_t sym = code_sym(v, l, T);
