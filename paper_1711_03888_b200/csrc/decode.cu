@@ -272,11 +272,13 @@ NBZG_DEV uint32_t code_sym(uint32_t v, int len, const DecTab& T) {
   return T.ss16 ? T.ss16[idx] : T.ss[idx];
 }
 
-// MSB-first bit reader over a 4-byte-aligned-down view of the stream
+// MSB-first bit reader over a 4-byte-aligned-down view of the stream, with
+// a two-word prefetch queue so a refill never waits on the load it uses.
 struct BitReader {
   const uint32_t* g;  // aligned word base
   uint64_t buf;       // next bits, MSB-aligned; >= 32 valid after refill
   int nb;
+  uint32_t q0, q1;    // the next two words (already byte-swapped)
   uint64_t wi;        // next word to load
 };
 
@@ -289,16 +291,20 @@ NBZG_DEV void br_init(BitReader& R, const uint32_t* g, uint32_t a0, uint64_t pos
   R.g = g;
   R.buf = (((uint64_t)bswap32(__ldg(g + w)) << 32) | bswap32(__ldg(g + w + 1))) << o;
   R.nb = 64 - o;
-  R.wi = w + 2;
+  R.q0 = bswap32(__ldg(g + w + 2));
+  R.q1 = bswap32(__ldg(g + w + 3));
+  R.wi = w + 4;
 }
 NBZG_DEV uint32_t br_peek(const BitReader& R) { return (uint32_t)(R.buf >> 32); }
 NBZG_DEV void br_skip(BitReader& R, int l) {  // l <= 32
   R.buf <<= l;
   R.nb -= l;
   if (R.nb < 32) {
-    R.buf |= (uint64_t)bswap32(__ldg(R.g + R.wi)) << (32 - R.nb);
-    R.wi++;
+    R.buf |= (uint64_t)R.q0 << (32 - R.nb);
     R.nb += 32;
+    R.q0 = R.q1;
+    R.q1 = bswap32(__ldg(R.g + R.wi));
+    R.wi++;
   }
 }
 
@@ -434,73 +440,120 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
     if (c >= ce) break;
     const uint64_t B = choff[c];
     const uint64_t Tb = choff[c + 1] - B;
-    const uint64_t E = B + Tb;
     const int64_t c0 = c * kChunk;
     const int mc = (int)min((int64_t)kChunk, a.n - c0);
-    const uint64_t seg0 = B + (Tb * lane) / 32, seg1 = B + (Tb * (lane + 1)) / 32;
+    // lane slice [rs0, rs1), chunk-relative bit positions (< 2^32)
+    const uint32_t rs0 = (uint32_t)((Tb * lane) / 32), rs1 = (uint32_t)((Tb * (lane + 1)) / 32);
     int err = 0;
 
-    // ---- phase 1: code lengths only, from an arbitrary start -> slice end
-    uint64_t end = seg0;
+    // ---- phase 1: full decode from an arbitrary start (count + lattice sum),
+    // remembering checkpoints after 16, 32, 48, 64 codewords
+    constexpr int kCp = 4;
+    uint32_t cp_pos[kCp], cp_cnt[kCp];
+    long long cp_v[kCp];
+    int ncp = 0;
+    uint32_t cnt = 0;
+    KSeg agg{0, 0};
+    uint32_t last_reset = 0;  // 1 + position of the last escape codeword (0: none)
+    uint32_t end;
     {
       BitReader R;
-      br_init(R, G, a0, seg0);
-      uint64_t pos = seg0;
-      // warp-uniform loop with a predicated body (keeps the warp converged)
-      while (__any_sync(0xffffffffu, pos < seg1)) {
-        if (pos < seg1) {
-          uint32_t v = br_peek(R);
-          int l = code_len(v, T);
+      br_init(R, G, a0, B + rs0);
+      uint32_t pos = rs0;
+      while (__any_sync(0xffffffffu, pos < rs1)) {
+        if (pos < rs1) {
+          if (cnt >= 16u * (ncp + 1) && ncp < kCp) {
+#pragma unroll
+            for (int j = 0; j < kCp; j++)
+              if (j == ncp) {
+                cp_pos[j] = pos;
+                cp_cnt[j] = cnt;
+                cp_v[j] = agg.v;
+              }
+            ncp++;
+          }
+          bool esc;
+          float ev;
+          int l = step(R, agg, esc, ev);
           if (l == 0) {  // garbage from a wrong start (incomplete codes): step a bit
             pos += 1;
-            br_init(R, G, a0, pos);
+            br_init(R, G, a0, B + pos);
           } else {
-            br_skip(R, l);
+            if (esc) last_reset = pos + 1;
             pos += l;
-            if (l == esc_len && (v >> (32 - l)) == esc_code) {  // inline escape value
-              br_skip(R, 32);
-              pos += 32;
-            }
+            cnt++;
           }
         }
       }
       end = pos;
     }
-    // ---- phase 2: decode from the predecessor's end (the true start once
-    // lane l-1 is synchronised, which Huffman self-synchronisation makes
-    // near-certain over a slice); recount and iterate while any end moves
-    uint32_t cnt = 0;
-    KSeg agg{0, 0};
-    uint64_t start = ~0ull;
+    // ---- phase 2: lane l re-walks from lane l-1's end (its true start once
+    // l-1 is synchronised) until it meets one of its checkpoints, then
+    // splices the phase-1 totals; lanes that never meet one redo the slice.
+    uint32_t start = rs0;
     for (int iter = 0; iter < 33; iter++) {
-      uint64_t s = __shfl_up_sync(0xffffffffu, end, 1);
-      if (lane == 0) s = B;
+      uint32_t s = __shfl_up_sync(0xffffffffu, end, 1);
+      if (lane == 0) s = 0;
+      bool active = (s != start) && !err;
       bool changed = false;
-      const bool redo = s != start && !err;
       BitReader R;
-      br_init(R, G, a0, redo ? s : seg1);
-      uint64_t p = redo ? s : seg1;
-      if (redo) {
-        cnt = 0;
-        agg = KSeg{0, 0};
-      }
-      while (__any_sync(0xffffffffu, p < seg1)) {
-        if (p < seg1) {
-          bool esc;
-          float ev;
-          int l = step(R, agg, esc, ev);
-          if (l == 0) {
-            err = NBZG_INVALID_CODE;
-            p = seg1;  // stop this lane
+      br_init(R, G, a0, B + (active ? s : rs1));
+      uint32_t q = active ? s : rs1;
+      uint32_t steps = 0;
+      KSeg wagg{0, 0};
+      uint32_t wlast = 0;
+      int hit = -1;
+      bool full = false;  // walking the whole slice (no checkpoint left)
+      while (__any_sync(0xffffffffu, active)) {
+        if (active) {
+          if (!full) {
+#pragma unroll
+            for (int j = 0; j < kCp; j++)
+              if (j < ncp && cp_pos[j] == q) hit = j;
+            if (hit < 0 && (ncp == 0 || q > cp_pos[ncp - 1])) full = true;
+          }
+          if (hit >= 0 || q >= rs1) {
+            active = false;
           } else {
-            p += l;
-            cnt++;
+            bool esc;
+            float ev;
+            int l = step(R, wagg, esc, ev);
+            if (l == 0) {
+              err = NBZG_INVALID_CODE;
+              active = false;
+            } else {
+              if (esc) wlast = q + 1;
+              q += l;
+              steps++;
+            }
           }
         }
       }
-      if (redo) {
-        if (p != end) changed = true;
-        end = p;
+      if (s != start && !err) {
+        if (hit >= 0) {
+          uint32_t hc = 0, hp = 0;
+          long long hv = 0;
+#pragma unroll
+          for (int j = 0; j < kCp; j++)
+            if (j == hit) {
+              hc = cp_cnt[j];
+              hp = cp_pos[j];
+              hv = cp_v[j];
+            }
+          // phase-1 suffix from the checkpoint: a reset after it wins
+          KSeg suf = (last_reset > hp) ? KSeg{1, agg.v} : KSeg{0, agg.v - hv};
+          cnt = steps + (cnt - hc);
+          agg = kseg_op(wagg, suf);
+          last_reset = (last_reset > hp) ? last_reset : wlast;
+          ncp = 0;  // checkpoints before the splice point are stale
+        } else {
+          cnt = steps;
+          agg = wagg;
+          last_reset = wlast;
+          ncp = 0;
+          if (q != end) changed = true;
+          end = q;
+        }
         start = s;
       }
       if (!__any_sync(0xffffffffu, changed)) break;
@@ -522,9 +575,9 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
     ex.v = __shfl_up_sync(0xffffffffu, inc.v, 1);
     if (lane == 0) ex = KSeg{0, 0};
     long long k = ex.v;  // chunk start: k = 0, so the incoming index is the prefix value
-    uint64_t last_end = __shfl_sync(0xffffffffu, end, 31);
+    uint32_t last_end = __shfl_sync(0xffffffffu, end, 31);
     err = __reduce_max_sync(0xffffffffu, (unsigned)err);
-    if (!err && (tot != (uint32_t)mc || last_end != E))
+    if (!err && (tot != (uint32_t)mc || (uint64_t)last_end != Tb))
       err = tot < (uint32_t)mc ? NBZG_TRUNCATED : NBZG_BAD_STREAM;
     if (err) {
       if (lane == 0) fail(a.status, (uint32_t)err);
@@ -533,10 +586,10 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
 
     // ---- phase 3: decode from the true start and write
     {
-      uint64_t s = __shfl_up_sync(0xffffffffu, end, 1);
-      if (lane == 0) s = B;
+      uint32_t s = __shfl_up_sync(0xffffffffu, end, 1);
+      if (lane == 0) s = 0;
       BitReader R;
-      br_init(R, G, a0, s);
+      br_init(R, G, a0, B + s);
       float* dst = F.out + c0 + o;
       const uint32_t maxcnt = __reduce_max_sync(0xffffffffu, cnt);
       for (uint32_t i = 0; i < maxcnt; i++) {
