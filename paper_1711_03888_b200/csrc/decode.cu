@@ -278,7 +278,7 @@ struct BitReader {
   const uint32_t* g;  // aligned word base
   uint64_t buf;       // next bits, MSB-aligned; >= 32 valid after refill
   int nb;
-  uint32_t q0, q1;    // the next two words (already byte-swapped)
+  uint32_t q0, q1;    // the next two words (raw, big-endian byte order)
   uint64_t wi;        // next word to load
 };
 
@@ -291,8 +291,8 @@ NBZG_DEV void br_init(BitReader& R, const uint32_t* g, uint32_t a0, uint64_t pos
   R.g = g;
   R.buf = (((uint64_t)bswap32(__ldg(g + w)) << 32) | bswap32(__ldg(g + w + 1))) << o;
   R.nb = 64 - o;
-  R.q0 = bswap32(__ldg(g + w + 2));
-  R.q1 = bswap32(__ldg(g + w + 3));
+  R.q0 = __ldg(g + w + 2);  // raw words: the byte swap happens at use, so
+  R.q1 = __ldg(g + w + 3);  // nothing waits on a load until its refill
   R.wi = w + 4;
 }
 NBZG_DEV uint32_t br_peek(const BitReader& R) { return (uint32_t)(R.buf >> 32); }
@@ -300,10 +300,10 @@ NBZG_DEV void br_skip(BitReader& R, int l) {  // l <= 32
   R.buf <<= l;
   R.nb -= l;
   if (R.nb < 32) {
-    R.buf |= (uint64_t)R.q0 << (32 - R.nb);
+    R.buf |= (uint64_t)bswap32(R.q0) << (32 - R.nb);
     R.nb += 32;
     R.q0 = R.q1;
-    R.q1 = bswap32(__ldg(R.g + R.wi));
+    R.q1 = __ldg(R.g + R.wi);
     R.wi++;
   }
 }
