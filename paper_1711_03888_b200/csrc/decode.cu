@@ -239,71 +239,36 @@ __global__ void __launch_bounds__(1024) chunk_offsets_kernel(DArgs a) {
 }
 
 // ---------------------------------------------------------------- decode step
-// Shared-memory tables: a 2^16-entry code-LENGTH table (0 = invalid prefix,
-// 0xFE = longer code) and the canonical left-justified limits
-// (encode.py:133-139): a codeword's length is the smallest l with
-// window < limit[l], its symbol ss[base[l] + (window >> (32 - l))].
-struct DecTab {
-  const uint8_t* ll;         // smem [1 << kLutBits]
-  const uint64_t* limit;     // smem [64]
-  const int32_t* base;       // smem [64] first_idx[l] - first_code[l]
-  const uint16_t* ss16;      // smem sorted symbols (k <= kSmemSyms) or null
-  const uint32_t* ss;        // global sorted symbols
-  int max_len;
-};
-
-// length of the codeword whose left-justified bits are v (0 = invalid).
-// Branch-light so a warp never splits for long codes: the long-code search
-// runs a field-uniform trip count without early exit.
-NBZG_DEV int code_len(uint32_t v, const DecTab& T) {
-  int l = T.ll[v >> (32 - kLutBits)];
-  if (l >= 0xFE) {
-    int r = 0;
-#pragma unroll 1
-    for (int len = T.max_len; len > kLutBits; len--)
-      r = ((uint64_t)v < T.limit[len]) ? len : r;
-    l = r;
-  }
-  return l;
-}
-
-NBZG_DEV uint32_t code_sym(uint32_t v, int len, const DecTab& T) {
-  uint32_t idx = (uint32_t)(T.base[len] + (int32_t)(v >> (32 - len)));
-  return T.ss16 ? T.ss16[idx] : T.ss[idx];
-}
-
-// MSB-first bit reader over a 4-byte-aligned-down view of the stream, with
-// a two-word prefetch queue so a refill never waits on the load it uses.
+// MSB-first bit reader: two current words + one prefetched raw word; a
+// 32-bit window is one funnel shift, a refill never waits on its own load.
 struct BitReader {
   const uint32_t* g;  // aligned word base
-  uint64_t buf;       // next bits, MSB-aligned; >= 32 valid after refill
-  int nb;
-  uint32_t q0, q1;    // the next two words (raw, big-endian byte order)
-  uint64_t wi;        // next word to load
+  uint32_t w0, w1;    // current words (byte-swapped)
+  uint32_t q;         // prefetched next word (raw)
+  uint32_t off;       // bit offset into w0 (0..31)
+  uint32_t wi;        // next word index to load
 };
 
 NBZG_DEV uint32_t bswap32(uint32_t w) { return __byte_perm(w, 0, 0x0123); }
 
 NBZG_DEV void br_init(BitReader& R, const uint32_t* g, uint32_t a0, uint64_t pos) {
   uint64_t q = pos + a0;
-  uint64_t w = q >> 5;
-  int o = (int)(q & 31);
+  uint32_t w = (uint32_t)(q >> 5);
   R.g = g;
-  R.buf = (((uint64_t)bswap32(__ldg(g + w)) << 32) | bswap32(__ldg(g + w + 1))) << o;
-  R.nb = 64 - o;
-  R.q0 = __ldg(g + w + 2);  // raw words: the byte swap happens at use, so
-  R.q1 = __ldg(g + w + 3);  // nothing waits on a load until its refill
-  R.wi = w + 4;
+  R.off = (uint32_t)(q & 31);
+  R.w0 = bswap32(__ldg(g + w));
+  R.w1 = bswap32(__ldg(g + w + 1));
+  R.q = __ldg(g + w + 2);
+  R.wi = w + 3;
 }
-NBZG_DEV uint32_t br_peek(const BitReader& R) { return (uint32_t)(R.buf >> 32); }
-NBZG_DEV void br_skip(BitReader& R, int l) {  // l <= 32
-  R.buf <<= l;
-  R.nb -= l;
-  if (R.nb < 32) {
-    R.buf |= (uint64_t)bswap32(R.q0) << (32 - R.nb);
-    R.nb += 32;
-    R.q0 = R.q1;
-    R.q1 = __ldg(R.g + R.wi);
+NBZG_DEV uint32_t br_peek(const BitReader& R) { return __funnelshift_l(R.w1, R.w0, R.off); }
+NBZG_DEV void br_skip(BitReader& R, uint32_t l) {  // l <= 32
+  R.off += l;
+  if (R.off >= 32) {
+    R.off -= 32;
+    R.w0 = R.w1;
+    R.w1 = bswap32(R.q);
+    R.q = __ldg(R.g + R.wi);
     R.wi++;
   }
 }
@@ -356,9 +321,45 @@ NBZG_DEV int decode_serial(const uint8_t* bits, uint64_t& bp, uint64_t total, co
 }
 
 // ---------------------------------------------------------------- D2: decode
+template <bool SMALL_K>
+NBZG_DEV uint32_t sym_of(uint32_t v, int l, const int32_t* base, const uint16_t* SS,
+                         const uint32_t* ss) {
+  uint32_t idx = (uint32_t)(base[l] + (int32_t)(v >> (32 - l)));
+  return SMALL_K ? (uint32_t)SS[idx] : __ldg(ss + idx);
+}
+
+// one decode step shared by all phases: returns bits consumed (0 = invalid);
+// escapes (symbol 0) consume their inline 32-bit value and reset the sum
+template <bool SMALL_K>
+NBZG_DEV uint32_t dstep(BitReader& R, const uint8_t* LL, const uint64_t* limit,
+                        const int32_t* base, const uint16_t* SS, const uint32_t* ss,
+                        int max_len, int bias, const DField& F, KSeg& agg, uint32_t& sym,
+                        float& ev) {
+  uint32_t v = br_peek(R);
+  int l = LL[v >> (32 - kLutBits)];
+  if (l >= 0xFE) {
+    int r = 0;
+#pragma unroll 1
+    for (int len = max_len; len > kLutBits; len--) r = ((uint64_t)v < limit[len]) ? len : r;
+    l = r;
+    if (l == 0) return 0;
+  }
+  sym = sym_of<SMALL_K>(v, l, base, SS, ss);
+  br_skip(R, (uint32_t)l);
+  if (sym == 0) {
+    ev = __uint_as_float(br_peek(R));
+    br_skip(R, 32);
+    agg = KSeg{1, esc_k(ev, F)};
+    return (uint32_t)l + 32;
+  }
+  agg.v += (long long)((int)sym - bias);
+  return (uint32_t)l;
+}
+
+template <bool SMALL_K>
 __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  uint8_t* LL = smem;                                               // [1 << kLutBits]
+  uint8_t* LL = smem;                                                  // [1 << kLutBits]
   uint16_t* SS = reinterpret_cast<uint16_t*>(smem + (1 << kLutBits));  // [kSmemSyms]
   __shared__ uint64_t s_limit[64];
   __shared__ int32_t s_base[64];
@@ -368,7 +369,8 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
   const int grp = blockIdx.x / a.nf, ngrp = gridDim.x / a.nf;
   const DField& F = a.f[fi];
   const DParsed& P = a.parsed[fi];
-  if (F.kind != 3 || P.status || *a.status) return;
+  if (F.kind != 3 || P.status || *a.status || P.max_len > 32) return;
+  if (SMALL_K != (P.k <= (uint64_t)kSmemSyms)) return;
   const int64_t cb = (a.nchunks * grp) / ngrp, ce = (a.nchunks * (grp + 1)) / ngrp;
   if (cb >= ce) return;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -381,8 +383,7 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
     uint4* sl = reinterpret_cast<uint4*>(LL);
     for (int i = tid; i < (1 << kLutBits) / 16; i += kDThreads) sl[i] = gl[i];
   }
-  const bool small_k = P.k <= (uint64_t)kSmemSyms;
-  if (small_k)
+  if (SMALL_K)
     for (uint32_t i = tid; i < (uint32_t)P.k; i += kDThreads) SS[i] = (uint16_t)ss[i];
   if (tid < 64) {
     const int l = tid;
@@ -397,41 +398,16 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
   }
   if (tid == 0) s_next = (int)cb;
   __syncthreads();
-  DecTab T;
-  T.ll = LL;
-  T.limit = s_limit;
-  T.base = s_base;
-  T.ss = ss;
-  T.ss16 = small_k ? SS : nullptr;
-  T.max_len = (int)P.max_len;
 
   const uintptr_t bits_addr = reinterpret_cast<uintptr_t>(F.payload + P.bits_off);
   const uint32_t* G = reinterpret_cast<const uint32_t*>(bits_addr & ~uintptr_t(3));
   const uint32_t a0 = (uint32_t)(bits_addr & 3) * 8;
   const uint64_t* choff = a.choff + fi * (a.nchunks + 1);
-  const int half = a.half;
-  const int esc_len = (int)P.esc_len;
-  const uint32_t esc_code = (uint32_t)P.esc_code;
+  const int bias = a.half + 1;
+  const int max_len = (int)P.max_len;
 
-  // one symbol step: decode at the reader, consume code (+ inline escape)
-  // and fold the lattice delta into `agg`; returns the code length (0 invalid)
-  auto step = [&](BitReader& R, KSeg& agg, bool& esc, float& ev) -> int {
-    uint32_t v = br_peek(R);
-    int l = code_len(v, T);
-    uint32_t sym = l ? code_sym(v, l, T) : 1u;
-    br_skip(R, l ? l : 1);
-    esc = l && sym == 0;
-    int used = l;
-    if (esc) {
-      ev = __uint_as_float(br_peek(R));
-      br_skip(R, 32);
-      agg = KSeg{1, esc_k(ev, F)};
-      used = l + 32;
-    } else {
-      agg.v += (long long)((int)sym - half - 1);
-    }
-    return used;
-  };
+#define DSTEP(R, agg, sym, ev) \
+  dstep<SMALL_K>(R, LL, s_limit, s_base, SS, ss, max_len, bias, F, agg, sym, ev)
 
   while (true) {
     int c32 = 0;
@@ -439,11 +415,12 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
     const int64_t c = __shfl_sync(0xffffffffu, c32, 0);
     if (c >= ce) break;
     const uint64_t B = choff[c];
-    const uint64_t Tb = choff[c + 1] - B;
+    const uint32_t Tb = (uint32_t)(choff[c + 1] - B);
     const int64_t c0 = c * kChunk;
     const int mc = (int)min((int64_t)kChunk, a.n - c0);
     // lane slice [rs0, rs1), chunk-relative bit positions (< 2^32)
-    const uint32_t rs0 = (uint32_t)((Tb * lane) / 32), rs1 = (uint32_t)((Tb * (lane + 1)) / 32);
+    const uint32_t rs0 = (uint32_t)(((uint64_t)Tb * lane) / 32);
+    const uint32_t rs1 = (uint32_t)(((uint64_t)Tb * (lane + 1)) / 32);
     int err = 0;
 
     // ---- phase 1: full decode from an arbitrary start (count + lattice sum),
@@ -452,7 +429,7 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
     uint32_t cp_pos[kCp], cp_cnt[kCp];
     long long cp_v[kCp];
     int ncp = 0;
-    uint32_t cnt = 0;
+    uint32_t cnt = 0, next_cp = 16;
     KSeg agg{0, 0};
     uint32_t last_reset = 0;  // 1 + position of the last escape codeword (0: none)
     uint32_t end;
@@ -462,24 +439,27 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
       uint32_t pos = rs0;
       while (__any_sync(0xffffffffu, pos < rs1)) {
         if (pos < rs1) {
-          if (cnt >= 16u * (ncp + 1) && ncp < kCp) {
+          if (cnt >= next_cp) {
+            if (ncp < kCp) {
 #pragma unroll
-            for (int j = 0; j < kCp; j++)
-              if (j == ncp) {
-                cp_pos[j] = pos;
-                cp_cnt[j] = cnt;
-                cp_v[j] = agg.v;
-              }
-            ncp++;
+              for (int j = 0; j < kCp; j++)
+                if (j == ncp) {
+                  cp_pos[j] = pos;
+                  cp_cnt[j] = cnt;
+                  cp_v[j] = agg.v;
+                }
+              ncp++;
+            }
+            next_cp += 16;
           }
-          bool esc;
+          uint32_t sym;
           float ev;
-          int l = step(R, agg, esc, ev);
+          uint32_t l = DSTEP(R, agg, sym, ev);
           if (l == 0) {  // garbage from a wrong start (incomplete codes): step a bit
             pos += 1;
             br_init(R, G, a0, B + pos);
           } else {
-            if (esc) last_reset = pos + 1;
+            if (sym == 0) last_reset = pos + 1;
             pos += l;
             cnt++;
           }
@@ -494,16 +474,17 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
     for (int iter = 0; iter < 33; iter++) {
       uint32_t s = __shfl_up_sync(0xffffffffu, end, 1);
       if (lane == 0) s = 0;
-      bool active = (s != start) && !err;
+      const bool redo = (s != start) && !err;
+      bool active = redo;
       bool changed = false;
       BitReader R;
-      br_init(R, G, a0, B + (active ? s : rs1));
-      uint32_t q = active ? s : rs1;
+      br_init(R, G, a0, B + (active ? s : rs0));
+      uint32_t q = s;
       uint32_t steps = 0;
       KSeg wagg{0, 0};
       uint32_t wlast = 0;
       int hit = -1;
-      bool full = false;  // walking the whole slice (no checkpoint left)
+      bool full = false;  // past the last checkpoint: walking the whole slice
       while (__any_sync(0xffffffffu, active)) {
         if (active) {
           if (!full) {
@@ -515,21 +496,21 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
           if (hit >= 0 || q >= rs1) {
             active = false;
           } else {
-            bool esc;
+            uint32_t sym;
             float ev;
-            int l = step(R, wagg, esc, ev);
+            uint32_t l = DSTEP(R, wagg, sym, ev);
             if (l == 0) {
               err = NBZG_INVALID_CODE;
               active = false;
             } else {
-              if (esc) wlast = q + 1;
+              if (sym == 0) wlast = q + 1;
               q += l;
               steps++;
             }
           }
         }
       }
-      if (s != start && !err) {
+      if (redo) {
         if (hit >= 0) {
           uint32_t hc = 0, hp = 0;
           long long hv = 0;
@@ -545,15 +526,14 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
           cnt = steps + (cnt - hc);
           agg = kseg_op(wagg, suf);
           last_reset = (last_reset > hp) ? last_reset : wlast;
-          ncp = 0;  // checkpoints before the splice point are stale
-        } else {
+        } else if (!err) {
           cnt = steps;
           agg = wagg;
           last_reset = wlast;
-          ncp = 0;
           if (q != end) changed = true;
           end = q;
         }
+        ncp = 0;  // checkpoints before the splice point are stale
         start = s;
       }
       if (!__any_sync(0xffffffffu, changed)) break;
@@ -564,20 +544,17 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
     uint32_t tot = __shfl_sync(0xffffffffu, o + cnt, 31);
     KSeg inc = agg;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
+    for (int dd = 1; dd < 32; dd <<= 1) {
       KSeg u;
-      u.r = __shfl_up_sync(0xffffffffu, inc.r, d);
-      u.v = __shfl_up_sync(0xffffffffu, inc.v, d);
-      if (lane >= d) inc = kseg_op(u, inc);
+      u.r = __shfl_up_sync(0xffffffffu, inc.r, dd);
+      u.v = __shfl_up_sync(0xffffffffu, inc.v, dd);
+      if (lane >= dd) inc = kseg_op(u, inc);
     }
-    KSeg ex;
-    ex.r = __shfl_up_sync(0xffffffffu, inc.r, 1);
-    ex.v = __shfl_up_sync(0xffffffffu, inc.v, 1);
-    if (lane == 0) ex = KSeg{0, 0};
-    long long k = ex.v;  // chunk start: k = 0, so the incoming index is the prefix value
+    long long k = __shfl_up_sync(0xffffffffu, inc.v, 1);
+    if (lane == 0) k = 0;  // chunk start: k_{-1} = 0, so the prefix value is the index
     uint32_t last_end = __shfl_sync(0xffffffffu, end, 31);
-    err = __reduce_max_sync(0xffffffffu, (unsigned)err);
-    if (!err && (tot != (uint32_t)mc || (uint64_t)last_end != Tb))
+    err = (int)__reduce_max_sync(0xffffffffu, (unsigned)err);
+    if (!err && (tot != (uint32_t)mc || last_end != Tb))
       err = tot < (uint32_t)mc ? NBZG_TRUNCATED : NBZG_BAD_STREAM;
     if (err) {
       if (lane == 0) fail(a.status, (uint32_t)err);
@@ -591,26 +568,36 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
       BitReader R;
       br_init(R, G, a0, B + s);
       float* dst = F.out + c0 + o;
+      const double twob = F.twob;
       const uint32_t maxcnt = __reduce_max_sync(0xffffffffu, cnt);
       for (uint32_t i = 0; i < maxcnt; i++) {
-        if (i >= cnt) continue;
-        uint32_t v = br_peek(R);
-        int l = code_len(v, T);
-        uint32_t sym = code_sym(v, l, T);
-        br_skip(R, l);
-        float outv;
-        if (sym == 0) {
-          outv = __uint_as_float(br_peek(R));
-          br_skip(R, 32);
-          k = esc_k(outv, F);
-        } else {
-          k += (long long)((int)sym - half - 1);
-          outv = (float)__dmul_rn((double)k, F.twob);
+        if (i < cnt) {
+          uint32_t v = br_peek(R);
+          int l = LL[v >> (32 - kLutBits)];
+          if (l >= 0xFE) {
+            int r = 0;
+#pragma unroll 1
+            for (int len = max_len; len > kLutBits; len--)
+              r = ((uint64_t)v < s_limit[len]) ? len : r;
+            l = r;
+          }
+          uint32_t sym = sym_of<SMALL_K>(v, l, s_base, SS, ss);
+          br_skip(R, (uint32_t)l);
+          float outv;
+          if (sym == 0) {
+            outv = __uint_as_float(br_peek(R));
+            br_skip(R, 32);
+            k = esc_k(outv, F);
+          } else {
+            k += (long long)((int)sym - bias);
+            outv = (float)__dmul_rn((double)k, twob);
+          }
+          dst[i] = outv;
         }
-        dst[i] = outv;
       }
     }
   }
+#undef DSTEP
 }
 
 // v2 streams with codes longer than 32 bits (pathological alphabets):
@@ -747,7 +734,9 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
   size_t sm = (1 << kLutBits) + kSmemSyms * 2;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
     attr = true;
   }
   bool any_v2 = false, any_v1 = false;
@@ -759,7 +748,9 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
     int groups = max(1, sm_count() / nf);
     if (groups > a.nchunks) groups = (int)a.nchunks;
     count_launch();
-    decode_kernel<<<groups * nf, kDThreads, sm, st>>>(a);
+    decode_kernel<true><<<groups * nf, kDThreads, sm, st>>>(a);
+    count_launch();
+    decode_kernel<false><<<groups * nf, kDThreads, sm, st>>>(a);
     count_launch();
     decode_v2_serial_kernel<<<dim3((unsigned)((a.nchunks + 63) / 64), nf), 64, 0, st>>>(a);
     trace_mark("dq_decode", st);
