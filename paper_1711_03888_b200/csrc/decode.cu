@@ -29,7 +29,7 @@
 
 namespace nbzg {
 
-constexpr int kDWarps = 32;        // warps per CTA, each decodes one chunk at a time
+constexpr int kDWarps = 24;        // warps per CTA, each decodes one chunk at a time
 constexpr int kDThreads = kDWarps * 32;
 constexpr int kLutBits = 16;       // code-length table index bits (u8 entries, 64 KiB)
 constexpr int kSmemSyms = 16384;   // sorted-symbol table staged in smem up to this k
@@ -242,11 +242,11 @@ __global__ void __launch_bounds__(1024) chunk_offsets_kernel(DArgs a) {
 // MSB-first bit reader: two current words + one prefetched raw word; a
 // 32-bit window is one funnel shift, a refill never waits on its own load.
 struct BitReader {
-  const uint32_t* g;  // aligned word base
-  uint32_t w0, w1;    // current words (byte-swapped)
-  uint32_t q;         // prefetched next word (raw)
-  uint32_t off;       // bit offset into w0 (0..31)
-  uint32_t wi;        // next word index to load
+  const uint32_t* g;       // aligned word base
+  uint32_t w0, w1;         // current words (byte-swapped)
+  uint32_t q0, q1, q2, q3; // next four words (raw): loads run 4 refills ahead
+  uint32_t off;            // bit offset into w0 (0..31)
+  uint32_t wi;             // next word index to load
 };
 
 NBZG_DEV uint32_t bswap32(uint32_t w) { return __byte_perm(w, 0, 0x0123); }
@@ -258,8 +258,11 @@ NBZG_DEV void br_init(BitReader& R, const uint32_t* g, uint32_t a0, uint64_t pos
   R.off = (uint32_t)(q & 31);
   R.w0 = bswap32(__ldg(g + w));
   R.w1 = bswap32(__ldg(g + w + 1));
-  R.q = __ldg(g + w + 2);
-  R.wi = w + 3;
+  R.q0 = __ldg(g + w + 2);
+  R.q1 = __ldg(g + w + 3);
+  R.q2 = __ldg(g + w + 4);
+  R.q3 = __ldg(g + w + 5);
+  R.wi = w + 6;
 }
 NBZG_DEV uint32_t br_peek(const BitReader& R) { return __funnelshift_l(R.w1, R.w0, R.off); }
 NBZG_DEV void br_skip(BitReader& R, uint32_t l) {  // l <= 32
@@ -267,8 +270,11 @@ NBZG_DEV void br_skip(BitReader& R, uint32_t l) {  // l <= 32
   if (R.off >= 32) {
     R.off -= 32;
     R.w0 = R.w1;
-    R.w1 = bswap32(R.q);
-    R.q = __ldg(R.g + R.wi);
+    R.w1 = bswap32(R.q0);
+    R.q0 = R.q1;
+    R.q1 = R.q2;
+    R.q2 = R.q3;
+    R.q3 = __ldg(R.g + R.wi);
     R.wi++;
   }
 }
