@@ -105,7 +105,7 @@ int nbzg_compress(const nbzg_compress_args *args, void *stream);
  * (_kernels.py:348-374) -> quantize.dequantize_field -> K.sz_dequantize
  * (_kernels.py:126-147).  kind 3 = SZ_DQ (v2, chunk-parallel); kind 0 =
  * SZ_FIELD (v1 reference streams, exact sequential chain, compat path).
- * payload: device bytes, any alignment, readable for payload_len + 32 bytes.
+ * payload: device bytes, any alignment, readable for payload_len + 64 bytes.
  * status: device u32, receives the first failure (NBZG_*). */
 typedef struct nbzg_decompress_args {
   const uint8_t *payload[6];

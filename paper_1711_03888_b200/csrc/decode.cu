@@ -242,27 +242,34 @@ __global__ void __launch_bounds__(1024) chunk_offsets_kernel(DArgs a) {
 // MSB-first bit reader: two current words + one prefetched raw word; a
 // 32-bit window is one funnel shift, a refill never waits on its own load.
 struct BitReader {
-  const uint32_t* g;       // aligned word base
-  uint32_t w0, w1;         // current words (byte-swapped)
-  uint32_t q0, q1, q2, q3; // next four words (raw): loads run 4 refills ahead
-  uint32_t off;            // bit offset into w0 (0..31)
-  uint32_t wi;             // next word index to load
+  const uint4* g4;   // 16-byte aligned view of the stream
+  uint32_t w0, w1;   // current words (byte-swapped)
+  uint4 qa;          // next raw words, consumed from .x; nq of them valid
+  uint4 qb;          // the next aligned uint4, already in flight
+  uint32_t nq;
+  uint32_t off;      // bit offset into w0 (0..31)
+  uint32_t vi;       // next uint4 index to load
 };
 
 NBZG_DEV uint32_t bswap32(uint32_t w) { return __byte_perm(w, 0, 0x0123); }
 
-NBZG_DEV void br_init(BitReader& R, const uint32_t* g, uint32_t a0, uint64_t pos) {
-  uint64_t q = pos + a0;
-  uint32_t w = (uint32_t)(q >> 5);
-  R.g = g;
-  R.off = (uint32_t)(q & 31);
+// pos: bit position relative to the 16-byte aligned base
+NBZG_DEV void br_init(BitReader& R, const uint4* g4, uint64_t pos) {
+  const uint32_t w = (uint32_t)(pos >> 5);  // word index
+  const uint32_t* g = reinterpret_cast<const uint32_t*>(g4);
+  R.g4 = g4;
+  R.off = (uint32_t)(pos & 31);
   R.w0 = bswap32(__ldg(g + w));
   R.w1 = bswap32(__ldg(g + w + 1));
-  R.q0 = __ldg(g + w + 2);
-  R.q1 = __ldg(g + w + 3);
-  R.q2 = __ldg(g + w + 4);
-  R.q3 = __ldg(g + w + 5);
-  R.wi = w + 6;
+  const uint32_t n = w + 2, v = n >> 2, s = n & 3;
+  uint4 A = __ldg(g4 + v);
+  if (s == 1) A = make_uint4(A.y, A.z, A.w, 0u);
+  else if (s == 2) A = make_uint4(A.z, A.w, 0u, 0u);
+  else if (s == 3) A = make_uint4(A.w, 0u, 0u, 0u);
+  R.qa = A;
+  R.nq = 4 - s;
+  R.qb = __ldg(g4 + v + 1);
+  R.vi = v + 2;
 }
 NBZG_DEV uint32_t br_peek(const BitReader& R) { return __funnelshift_l(R.w1, R.w0, R.off); }
 NBZG_DEV void br_skip(BitReader& R, uint32_t l) {  // l <= 32
@@ -270,12 +277,16 @@ NBZG_DEV void br_skip(BitReader& R, uint32_t l) {  // l <= 32
   if (R.off >= 32) {
     R.off -= 32;
     R.w0 = R.w1;
-    R.w1 = bswap32(R.q0);
-    R.q0 = R.q1;
-    R.q1 = R.q2;
-    R.q2 = R.q3;
-    R.q3 = __ldg(R.g + R.wi);
-    R.wi++;
+    R.w1 = bswap32(R.qa.x);
+    R.qa.x = R.qa.y;
+    R.qa.y = R.qa.z;
+    R.qa.z = R.qa.w;
+    if (--R.nq == 0) {
+      R.qa = R.qb;
+      R.nq = 4;
+      R.qb = __ldg(R.g4 + R.vi);
+      R.vi++;
+    }
   }
 }
 
@@ -406,8 +417,8 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
   __syncthreads();
 
   const uintptr_t bits_addr = reinterpret_cast<uintptr_t>(F.payload + P.bits_off);
-  const uint32_t* G = reinterpret_cast<const uint32_t*>(bits_addr & ~uintptr_t(3));
-  const uint32_t a0 = (uint32_t)(bits_addr & 3) * 8;
+  const uint4* G = reinterpret_cast<const uint4*>(bits_addr & ~uintptr_t(15));
+  const uint32_t a0 = (uint32_t)(bits_addr & 15) * 8;
   const uint64_t* choff = a.choff + fi * (a.nchunks + 1);
   const int bias = a.half + 1;
   const int max_len = (int)P.max_len;
@@ -441,7 +452,7 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
     uint32_t end;
     {
       BitReader R;
-      br_init(R, G, a0, B + rs0);
+      br_init(R, G, a0 + B + rs0);
       uint32_t pos = rs0;
       while (__any_sync(0xffffffffu, pos < rs1)) {
         if (pos < rs1) {
@@ -463,7 +474,7 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
           uint32_t l = DSTEP(R, agg, sym, ev);
           if (l == 0) {  // garbage from a wrong start (incomplete codes): step a bit
             pos += 1;
-            br_init(R, G, a0, B + pos);
+            br_init(R, G, a0 + B + pos);
           } else {
             if (sym == 0) last_reset = pos + 1;
             pos += l;
@@ -484,7 +495,7 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
       bool active = redo;
       bool changed = false;
       BitReader R;
-      br_init(R, G, a0, B + (active ? s : rs0));
+      br_init(R, G, a0 + B + (active ? s : rs0));
       uint32_t q = s;
       uint32_t steps = 0;
       KSeg wagg{0, 0};
@@ -572,7 +583,7 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
       uint32_t s = __shfl_up_sync(0xffffffffu, end, 1);
       if (lane == 0) s = 0;
       BitReader R;
-      br_init(R, G, a0, B + s);
+      br_init(R, G, a0 + B + s);
       float* dst = F.out + c0 + o;
       const double twob = F.twob;
       const uint32_t maxcnt = __reduce_max_sync(0xffffffffu, cnt);

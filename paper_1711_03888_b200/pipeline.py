@@ -429,7 +429,7 @@ def decompress(archive: Archive, device: Optional[bool] = None) -> ParticleSnaps
             offs[fi] = (len(blob), len(st.payload), _KIND_CODE[st.kind])
             blob += st.payload
             blob += b"\0" * ((-len(blob)) % 16)
-        blob += b"\0" * 32
+        blob += b"\0" * 64
         arena = torch.frombuffer(bytearray(blob), dtype=torch.uint8).cuda()
         d = _Device(arena, [offs[f][0] if f in offs else None for f in range(6)],
                     [offs[f][1] if f in offs else 0 for f in range(6)],
