@@ -23,6 +23,7 @@
 //      recon = f32(k * 2b) or the inline escape value.
 // Status words: INVALID_CODE / TRUNCATED / BAD_STREAM -> DecodeError.
 #include <cstdio>
+#include <cstdlib>
 
 #include "nbzg_internal.cuh"
 #include "plan.h"
@@ -33,6 +34,9 @@ constexpr int kDWarps = 24;        // warps per CTA, each decodes one chunk at a
 constexpr int kDThreads = kDWarps * 32;
 constexpr int kLutBits = 16;       // code-length table index bits (u8 entries, 64 KiB)
 constexpr int kSmemSyms = 16384;   // sorted-symbol table staged in smem up to this k
+constexpr int kTpcBits = 15;       // thread-per-chunk fused table index bits (i32, 128 KiB)
+constexpr int kTpc2Cap = 12288;    // secondary (long-code) table entries (48 KiB)
+constexpr int kTpcTab = (1 << kTpcBits) + kTpc2Cap;
 
 struct DParsed {
   uint64_t n_esc, k, total_bits;
@@ -41,6 +45,8 @@ struct DParsed {
   uint32_t status;
   uint32_t esc_len;   // code length of symbol 0 (escape), 0 if absent
   uint64_t esc_code;  // its canonical code word: first_code[esc_len] (rank 0)
+  uint64_t t2_r0;     // thread-per-chunk secondary table: window start,
+  uint32_t t2_w, t2_n;  // resolution bits and entry count (0 = none)
   uint64_t first_code[64];
   uint32_t first_idx[64];
   uint32_t counts[64];
@@ -52,7 +58,8 @@ struct DArgs {
   int64_t n, nchunks, nbins;
   int half;
   DParsed* parsed;     // [nf]
-  uint32_t* lut;       // [nf][4096]
+  uint32_t* lut;       // [nf][2^16] u8 code lengths
+  int32_t* lut2;       // [nf][2^15] fused (delta, length) entries, 0 = slow path
   uint32_t* ssyms;     // [nf][nbins] sorted (len, sym) symbols
   uint64_t* choff;     // [nf][nchunks+1] chunk bit offsets
   uint64_t* lb;        // [nf][2][nchunks]
@@ -179,6 +186,51 @@ __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
     }
     lut[e] = len;
   }
+  __syncthreads();  // ss (global) complete for the fused table
+  // fused tables for the thread-per-chunk decoder.  Entry: bits 0-5 code
+  // length (0 = unresolved), bit 6 escape, bits 7-31 lattice delta
+  // sym - bias.  Primary: 15-bit prefix, codes <= 15 bits.  Secondary: the
+  // canonical tail (32-bit window value >= R0, i.e. codes > 15 bits) at W-bit
+  // resolution, W <= 24 chosen so the tail fits kTpc2Cap entries.
+  if (F.kind == 3) {
+    int32_t* lut2 = a.lut2 + (size_t)fi * kTpcTab;
+    const int bias = a.half + 1;
+    auto entry = [&](int l, uint64_t u) -> int32_t {  // u: 32-bit window value
+      const uint32_t idx = s_fi[l] + (uint32_t)((u >> (32 - l)) - s_fc[l]);
+      const int sym = (int)ss[idx];
+      return sym == 0 ? (int32_t)(l | 64) : (int32_t)(((uint32_t)(sym - bias) << 7) | (uint32_t)l);
+    };
+    for (int e = tid; e < (1 << kTpcBits); e += blockDim.x) {
+      const int l = lut[e << (kLutBits - kTpcBits)];
+      lut2[e] = (l >= 1 && l <= kTpcBits) ? entry(l, (uint64_t)e << (32 - kTpcBits)) : 0;
+    }
+    uint64_t R0 = 1ull << 32;
+    int W = 0;
+    uint32_t n2 = 0;
+    if (max_len > kTpcBits && max_len <= 32) {
+      R0 = (s_fc[kTpcBits] + s_cbl[kTpcBits]) << (32 - kTpcBits);
+      for (int w = min(max_len, 24); w > kTpcBits; w--) {
+        const uint64_t cnt = ((1ull << 32) - R0 + (1ull << (32 - w)) - 1) >> (32 - w);
+        if (cnt <= (uint64_t)kTpc2Cap) {
+          W = w;
+          n2 = (uint32_t)cnt;
+          break;
+        }
+      }
+    }
+    for (uint32_t j = tid; j < n2; j += blockDim.x) {
+      const uint64_t u = R0 + ((uint64_t)j << (32 - W));
+      int l = 0;
+      for (int m = max_len; m > kTpcBits; m--)
+        if (u < ((s_fc[m] + s_cbl[m]) << (32 - m))) l = m;
+      lut2[(1 << kTpcBits) + j] = (l > 0 && l <= W) ? entry(l, u) : 0;
+    }
+    if (tid == 0) {
+      P.t2_r0 = R0;
+      P.t2_w = (uint32_t)W;
+      P.t2_n = n2;
+    }
+  }
   if (tid == 0) {
     const uint64_t table_end = 8 + 5 * k;
     const bool has_esc = ld_u32_bytes(p + 8) == 0;  // ascending symbols: 0 is first
@@ -272,22 +324,35 @@ NBZG_DEV void br_init(BitReader& R, const uint4* g4, uint64_t pos) {
   R.vi = v + 2;
 }
 NBZG_DEV uint32_t br_peek(const BitReader& R) { return __funnelshift_l(R.w1, R.w0, R.off); }
+// predicated in-place 16-byte load: the destination registers ARE the
+// queue slot, so no register copy waits on the load (a plain conditional
+// load makes the compiler merge the result with a move right after it).
+NBZG_DEV void ldg_v4_if(uint4& q, const uint4* p, bool pred) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.u32 p, %4, 0;\n"
+      " @p ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%5];\n}\n"
+      : "+r"(q.x), "+r"(q.y), "+r"(q.z), "+r"(q.w)
+      : "r"((uint32_t)pred), "l"(p));
+}
 NBZG_DEV void br_skip(BitReader& R, uint32_t l) {  // l <= 32
   R.off += l;
-  if (R.off >= 32) {
+  const bool adv = R.off >= 32;
+  bool refill = false;
+  if (adv) {
     R.off -= 32;
     R.w0 = R.w1;
     R.w1 = bswap32(R.qa.x);
     R.qa.x = R.qa.y;
     R.qa.y = R.qa.z;
     R.qa.z = R.qa.w;
-    if (--R.nq == 0) {
+    refill = --R.nq == 0;
+    if (refill) {
       R.qa = R.qb;
       R.nq = 4;
-      R.qb = __ldg(R.g4 + R.vi);
-      R.vi++;
     }
   }
+  ldg_v4_if(R.qb, R.g4 + R.vi, refill);
+  R.vi += refill ? 1u : 0u;
 }
 
 // segmented (reset, k) scan element: a later reset wins, otherwise values add
@@ -617,6 +682,152 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
 #undef DSTEP
 }
 
+// ---------------------------------------------------------------- D2': thread per chunk
+// When a field has many chunks (>= kTpcMinChunks) every THREAD decodes one
+// whole chunk serially: no resynchronisation and one pass over the bits
+// instead of the warp decoder's two and a half.  The fused 2^15-entry table
+// (128 KiB of shared memory) turns a common step into one LDS: peek 32 bits,
+// look up (delta, length), add the delta to the lattice index, write
+// f32(k * 2b).  Outputs are buffered 8 at a time and written as two 16-byte
+// stores (one full sector per lane).  Escapes and codes longer than 15 bits
+// take the canonical slow path (limits + symbol table, also in smem).
+constexpr int kTpcMinChunks = 256;
+
+NBZG_DEV void br_skip_c(BitReader& R, uint32_t l, uint32_t vmax) {  // clamped refills
+  R.off += l;
+  bool refill = false;
+  if (R.off >= 32) {
+    R.off -= 32;
+    R.w0 = R.w1;
+    R.w1 = bswap32(R.qa.x);
+    R.qa.x = R.qa.y;
+    R.qa.y = R.qa.z;
+    R.qa.z = R.qa.w;
+    refill = --R.nq == 0;
+    if (refill) {
+      R.qa = R.qb;
+      R.nq = 4;
+    }
+  }
+  ldg_v4_if(R.qb, R.g4 + min(R.vi, vmax), refill);
+  R.vi += refill ? 1u : 0u;
+}
+
+__global__ void __launch_bounds__(1024, 1) decode_tpc_kernel(DArgs a, int ctas_per_field) {
+  extern __shared__ __align__(16) uint8_t dsm2[];
+  int32_t* LT = reinterpret_cast<int32_t*>(dsm2);  // [2^15 + t2_n]
+  __shared__ uint64_t s_limit[64];
+  __shared__ int32_t s_base[64];
+  const int fi = blockIdx.y;
+  const DField& F = a.f[fi];
+  const DParsed& P = a.parsed[fi];
+  if (F.kind != 3 || P.status || *a.status || P.max_len > 32) return;
+  const int64_t cb = (a.nchunks * blockIdx.x) / ctas_per_field;
+  const int64_t ce = (a.nchunks * (blockIdx.x + 1)) / ctas_per_field;
+  if (cb >= ce) return;
+  const int tid = threadIdx.x;
+  const uint32_t* ss = a.ssyms + fi * a.nbins;
+  const uint32_t n2 = P.t2_n;
+  {
+    const int32_t* gl = a.lut2 + (size_t)fi * kTpcTab;
+    const uint32_t nv = ((1u << kTpcBits) + n2 + 3) / 4;
+    for (uint32_t i = tid; i < nv; i += blockDim.x)
+      reinterpret_cast<uint4*>(LT)[i] = __ldg(reinterpret_cast<const uint4*>(gl) + i);
+  }
+  if (tid < 64) {
+    const int l = tid;
+    uint64_t lim = 0;
+    int32_t bs = 0;
+    if (l >= 1 && l <= 32 && l <= (int)P.max_len) {
+      lim = (P.first_code[l] + P.counts[l]) << (32 - l);
+      bs = (int32_t)P.first_idx[l] - (int32_t)P.first_code[l];
+    }
+    s_limit[l] = l > (int)P.max_len ? ~0ull : lim;
+    s_base[l] = bs;
+  }
+  __syncthreads();
+
+  const uintptr_t bits_addr = reinterpret_cast<uintptr_t>(F.payload + P.bits_off);
+  const uint4* G = reinterpret_cast<const uint4*>(bits_addr & ~uintptr_t(15));
+  const uint32_t a0 = (uint32_t)(bits_addr & 15) * 8;
+  // last 16-byte block the stream may touch (payload + 64-byte read slack)
+  const uint32_t vmax = (uint32_t)((a0 / 8 + 4 * ((P.total_bits + 31) / 32) + 16) / 16);
+  const uint64_t* choff = a.choff + fi * (a.nchunks + 1);
+  const int bias = a.half + 1;
+  const int max_len = (int)P.max_len;
+  const double twob = F.twob;
+  const bool vec = (reinterpret_cast<uintptr_t>(F.out) & 15) == 0;
+  const uint32_t r0 = (uint32_t)min(P.t2_r0, (uint64_t)0xFFFFFFFFu);
+  const uint32_t sh2 = 32u - P.t2_w;
+  int32_t* LT2 = LT + (1 << kTpcBits);
+
+  for (int64_t c = cb + tid; c < ce; c += blockDim.x) {
+    const uint64_t b0 = choff[c];
+    const uint32_t Tb = (uint32_t)(choff[c + 1] - b0);
+    const int64_t i0 = c * kChunk;
+    const int mc = (int)min((int64_t)kChunk, a.n - i0);
+    BitReader R;
+    br_init(R, G, a0 + b0);
+    uint32_t pos = 0;
+    double kd = 0.0;
+    int err = 0;
+    float* dst = F.out + i0;
+    // one symbol: returns the value, advances the reader
+    auto step = [&](float& o) {
+      const uint32_t v = br_peek(R);
+      int32_t e = LT[v >> (32 - kTpcBits)];
+      if ((e & 63) == 0) {
+        const uint32_t j = (v - r0) >> sh2;  // long code: secondary table
+        e = (v >= r0 && j < n2) ? LT2[j] : 0;
+        if ((e & 63) == 0) {  // longer than W bits, or invalid: canonical search
+          int r = 0;
+#pragma unroll 1
+          for (int len = max_len; len >= 1; len--) r = ((uint64_t)v < s_limit[len]) ? len : r;
+          if (r == 0) {
+            err = NBZG_INVALID_CODE;
+            e = 1;
+          } else {
+            const uint32_t sym = __ldg(ss + (uint32_t)(s_base[r] + (int32_t)(v >> (32 - r))));
+            e = sym == 0 ? (r | 64) : (int32_t)(((uint32_t)((int)sym - bias) << 7) | (uint32_t)r);
+          }
+        }
+      }
+      uint32_t l = (uint32_t)e & 63u;
+      if (e & 64) {  // escape: the raw float follows the codeword
+        br_skip_c(R, l, vmax);
+        pos += l;
+        o = __uint_as_float(br_peek(R));
+        l = 32;
+        kd = (double)esc_k(o, F);
+      } else {
+        kd += (double)(e >> 7);
+        o = (float)__dmul_rn(kd, twob);
+      }
+      br_skip_c(R, l, vmax);
+      pos += l;
+    };
+    int i = 0;
+    if (vec) {
+      for (; i + 8 <= mc; i += 8) {
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) step(o[j]);
+        float4* d4 = reinterpret_cast<float4*>(dst + i);
+        __stcs(d4, make_float4(o[0], o[1], o[2], o[3]));
+        __stcs(d4 + 1, make_float4(o[4], o[5], o[6], o[7]));
+        if (pos > Tb) break;  // corrupt: stop early, reported below
+      }
+    }
+    for (; i < mc && pos <= Tb; i++) {
+      float o;
+      step(o);
+      dst[i] = o;
+    }
+    if (!err && pos != Tb) err = pos > Tb ? NBZG_TRUNCATED : NBZG_BAD_STREAM;
+    if (err) fail(a.status, (uint32_t)err);
+  }
+}
+
 // v2 streams with codes longer than 32 bits (pathological alphabets):
 // serial decode per chunk (one thread per chunk), same semantics.
 __global__ void decode_v2_serial_kernel(DArgs a) {
@@ -699,12 +910,21 @@ __global__ void decode_v1_kernel(DArgs a) {
 }
 
 // ---------------------------------------------------------------- launcher
+// NBZG_DECODE=warp|thread forces one v2 decoder (tests cover both).
+static bool use_tpc(int64_t nchunks) {
+  const char* e = getenv("NBZG_DECODE");
+  if (e && e[0] == 't') return true;
+  if (e && e[0] == 'w') return false;
+  return nchunks >= kTpcMinChunks;
+}
+
 size_t decompress_ws(int nf, int64_t n, int64_t nbins) {
   int64_t nchunks = (n + kChunk - 1) / kChunk;
   size_t s = 0;
   auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
   s += al(sizeof(DParsed) * nf);
   s += al((size_t)nf * (1 << kLutBits));
+  s += al((size_t)nf * 4 * kTpcTab);
   s += al(sizeof(uint32_t) * nf * nbins);
   s += al(sizeof(uint64_t) * nf * (nchunks + 1));
   s += al(sizeof(uint64_t) * nf * 2 * (nchunks + 1));
@@ -731,6 +951,8 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
   p += al(sizeof(DParsed) * nf);
   a.lut = reinterpret_cast<uint32_t*>(p);
   p += al((size_t)nf * (1 << kLutBits));
+  a.lut2 = reinterpret_cast<int32_t*>(p);
+  p += al((size_t)nf * 4 * kTpcTab);
   a.ssyms = reinterpret_cast<uint32_t*>(p);
   p += al(sizeof(uint32_t) * nf * nbins);
   a.choff = reinterpret_cast<uint64_t*>(p);
@@ -764,10 +986,24 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
   if (any_v2) {
     int groups = max(1, sm_count() / nf);
     if (groups > a.nchunks) groups = (int)a.nchunks;
-    count_launch();
-    decode_kernel<true><<<groups * nf, kDThreads, sm, st>>>(a);
-    count_launch();
-    decode_kernel<false><<<groups * nf, kDThreads, sm, st>>>(a);
+    if (use_tpc(a.nchunks)) {
+      const int per = (int)((a.nchunks + groups - 1) / groups);
+      const int thr = min(1024, (per + 31) / 32 * 32);
+      const size_t sm2 = 4 * kTpcTab;
+      static bool attr2 = false;
+      if (!attr2) {
+        cudaFuncSetAttribute(decode_tpc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm2);
+        attr2 = true;
+      }
+      count_launch();
+      decode_tpc_kernel<<<dim3(groups, nf), thr, sm2, st>>>(a, groups);
+    } else {
+      count_launch();
+      decode_kernel<true><<<groups * nf, kDThreads, sm, st>>>(a);
+      count_launch();
+      decode_kernel<false><<<groups * nf, kDThreads, sm, st>>>(a);
+    }
     count_launch();
     decode_v2_serial_kernel<<<dim3((unsigned)((a.nchunks + 63) / 64), nf), 64, 0, st>>>(a);
     trace_mark("dq_decode", st);

@@ -28,6 +28,14 @@ def O(oracle_lib):
     return oracle_lib
 
 
+@pytest.fixture(params=["warp", "thread"])
+def decoder(request, monkeypatch):
+    """Both v2 decoders (warp-per-chunk with resync, thread-per-chunk);
+    csrc/decode.cu picks by chunk count unless NBZG_DECODE forces one."""
+    monkeypatch.setenv("NBZG_DECODE", request.param)
+    return request.param
+
+
 # ---------------------------------------------------------------- stages
 
 def test_minmax6(rng):
@@ -189,7 +197,7 @@ def test_archive_byte_identical_to_oracle(O, case):
 
 
 @pytest.mark.parametrize("case", GOLDEN_CASES)
-def test_decompress_matches_oracle_and_bound(O, case):
+def test_decompress_matches_oracle_and_bound(O, case, decoder):
     g = load_golden(case)
     fields = golden_inputs(g)
     snap = nbz.ParticleSnapshot(*fields)
@@ -291,7 +299,7 @@ def test_constant_fields_and_absolute_bounds(O, rng):
         assert np.all(np.asarray(rec.xx) == np.float32(3.25))
 
 
-def test_escape_heavy_and_tight_bounds(O, rng):
+def test_escape_heavy_and_tight_bounds(O, rng, decoder):
     n = 50000
     fields = [(rng.standard_cauchy(n) * 50).astype(np.float32) for _ in range(6)]
     snap = nbz.ParticleSnapshot(*fields)
@@ -301,9 +309,12 @@ def test_escape_heavy_and_tight_bounds(O, rng):
             ref = O.compress(fields, mode, "rel", eb, fmt=2)
             assert res.archive.serialized() == ref["wire"], (eb, mode)
             rec = nbz.decompress(res.archive)
+            odec = O.decompress(ref["wire"])
             work = fields if res.order is None else [f[res.order] for f in fields]
             for fi in range(6):
-                err = np.abs(work[fi].astype(np.float64) - np.asarray(rec.field(fi), np.float64))
+                got = np.asarray(rec.field(fi))
+                assert np.array_equal(got, odec[fi]), (eb, mode, fi)
+                err = np.abs(work[fi].astype(np.float64) - got.astype(np.float64))
                 assert float(err.max()) <= res.archive.bounds[fi]
 
 
@@ -340,7 +351,7 @@ def test_corrupt_archives_rejected():
         nbz.decompress(ar)  # only reachable when the flip hit a CRC-neutral spot
 
 
-def test_corrupt_payloads_fail_cleanly():
+def test_corrupt_payloads_fail_cleanly(decoder):
     """Bypass the CRC: hand-corrupted payloads must raise DecodeError (or
     decode to something), never hang or fault."""
     snap = nbz.ParticleSnapshot(*datagen.small_amdf(40000))
@@ -368,7 +379,7 @@ def test_corrupt_payloads_fail_cleanly():
 
 @pytest.mark.parametrize("spec,mode", [("C1", "sz-lv"), ("C1", "sz-lv-prx"),
                                        ("C0", "sz-lv-prx")])
-def test_config_scale_parity(O, spec, mode):
+def test_config_scale_parity(O, spec, mode, decoder):
     """BASELINE configs 0 and 1 at full size: byte-identical archives."""
     fields = datagen.generate(spec)
     snap = nbz.ParticleSnapshot(*fields)
@@ -376,7 +387,10 @@ def test_config_scale_parity(O, spec, mode):
     ref = O.compress(fields, mode, "rel", 1e-4, fmt=2)
     assert res.archive.serialized() == ref["wire"]
     rec = nbz.decompress(res.archive, device=True)
+    odec = O.decompress(ref["wire"])
     work = fields if res.order is None else [f[res.order] for f in fields]
     for fi in range(6):
-        err = (torch.from_numpy(work[fi]).cuda().double() - rec.field(fi).double()).abs().max()
+        got = rec.field(fi)
+        assert torch.equal(got.cpu(), torch.from_numpy(odec[fi])), fi
+        err = (torch.from_numpy(work[fi]).cuda().double() - got.double()).abs().max()
         assert float(err) <= res.archive.bounds[fi]
