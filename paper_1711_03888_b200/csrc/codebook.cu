@@ -32,6 +32,9 @@ struct CBArgs {
   int64_t n;
   int64_t nchunks;
   int single_field;   // >= 0: only this field (parity hook), meta->f[0] receives
+  uint8_t* tlen;      // [6][nbins] length by symbol (encoder tables; may be null)
+  uint16_t* trank;    // [6][nbins] rank within the length class
+  uint64_t* tfc;      // [6][64] first canonical code per length
 };
 
 NBZG_DEV void bitonic_sort_u64(uint64_t* a, int N) {
@@ -221,6 +224,7 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
     fm.max_len = s_max;
   }
   __syncthreads();
+  if (a.tfc && tid < 64) a.tfc[field * 64 + tid] = (tid >= 1 && tid <= max_len) ? s_fc[tid] : 0;
   // rank within length class, ascending symbol: per present length, a block scan
   const int RK = (k + kCBThreads - 1) / kCBThreads;
   for (int l = 1; l <= max_len; l++) {
@@ -236,6 +240,10 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
       int i = tid * RK + r;
       if (i < k && lenr[i] == l) {
         lut[sym[i]] = ((uint64_t)l << 57) | (s_fc[l] + ex);
+        if (a.tlen) {
+          a.tlen[field * a.nbins + sym[i]] = (uint8_t)l;
+          a.trank[field * a.nbins + sym[i]] = (uint16_t)ex;
+        }
         ex++;
       }
     }
@@ -258,8 +266,9 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
 
 int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uint8_t* len,
                          uint64_t* lut, uint32_t* scratch, nbzg_meta* meta, int64_t n,
-                         int64_t nchunks, int single_field, cudaStream_t st) {
-  CBArgs a{hist, nbins, sym, len, lut, scratch, meta, n, nchunks, single_field};
+                         int64_t nchunks, int single_field, cudaStream_t st,
+                         uint8_t* tlen, uint16_t* trank, uint64_t* tfc) {
+  CBArgs a{hist, nbins, sym, len, lut, scratch, meta, n, nchunks, single_field, tlen, trank, tfc};
   size_t sm = 14 * (size_t)kCBSmemK;  // keys u64 | L u32 | order u16
   static bool attr = false;
   if (!attr) {
@@ -274,7 +283,7 @@ int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uin
 int launch_codebook(const Plan& p, cudaStream_t st) {
   if (p.n == 0) return NBZG_OK;
   return launch_codebook_impl(p.hist, p.nbins, p.cb_sym, p.cb_len, p.lut, p.cb_scratch, p.meta,
-                              p.n, p.nchunks, -1, st);
+                              p.n, p.nchunks, -1, st, p.enc_len, p.enc_rank, p.enc_fc);
 }
 
 // ---- parity hook: K.huffman_lengths on sorted counts (one CTA)

@@ -23,6 +23,8 @@
 //      bit; a chunk ending mid-word appends the first bits of the next chunk
 //      (encoded on the spot), so every word is written exactly once -- no
 //      zero fill, no global atomics.
+#include <cstdio>
+
 #include "nbzg_internal.cuh"
 #include "plan.h"
 
@@ -81,6 +83,9 @@ struct EArgs {
   const uint16_t* codes;  // [6][code_stride]
   int64_t code_stride;
   const uint64_t* lut;    // [6][nbins]
+  const uint8_t* tlen;    // [6][nbins] (FAST path: staged in smem)
+  const uint16_t* trank;  // [6][nbins]
+  const uint64_t* tfc;    // [6][64]
   int64_t nbins;
   int64_t n, nchunks;
   const float* f[6];
@@ -121,17 +126,41 @@ NBZG_DEV void acc_put(Acc& A, uint64_t v, int nb, Emit&& emit) {
   }
 }
 
+// code-word lookup: global u64 LUT (hook path) or the smem (length, rank)
+// tables plus first canonical codes (payload path)
+struct CodeTab {
+  const uint64_t* lut;
+  const uint8_t* len;
+  const uint16_t* rank;
+  const uint64_t* fc;
+};
+template <bool FAST>
+NBZG_DEV uint32_t code_len(const CodeTab& T, uint32_t code) {
+  return FAST ? (uint32_t)T.len[code] : (uint32_t)(__ldg(&T.lut[code]) >> 57);
+}
+template <bool FAST>
+NBZG_DEV uint64_t code_word(const CodeTab& T, uint32_t code, uint32_t& l) {
+  if (FAST) {
+    l = T.len[code];
+    return T.fc[l] + T.rank[code];
+  }
+  const uint64_t e = __ldg(&T.lut[code]);
+  l = (uint32_t)(e >> 57);
+  return e & ((1ull << 57) - 1);
+}
+
 // first `need` (1..31) bits of chunk c1's stream, MSB-aligned (serial, one lane)
+template <bool FAST>
 NBZG_DEV uint32_t chunk_head_bits(const EArgs& a, int field, const uint16_t* codes,
-                                  const uint64_t* lut, int64_t c1, int need) {
+                                  const CodeTab& T, int64_t c1, int need) {
   const int64_t s0 = c1 * kChunk, s1 = min(a.n, s0 + kChunk);
   uint64_t acc = 0;
   int nacc = 0;
   for (int64_t i = s0; i < s1 && nacc < need; i++) {
     uint32_t code = codes[i];
-    uint64_t e = __ldg(&lut[code]);
-    int l = (int)(e >> 57);
-    uint64_t w = e & ((1ull << 57) - 1);
+    uint32_t lu;
+    uint64_t w = code_word<FAST>(T, code, lu);
+    int l = (int)lu;
     if (l > 32) {  // only the leading bits can still land in the window
       w >>= (l - 32);
       l = 32;
@@ -147,20 +176,14 @@ NBZG_DEV uint32_t chunk_head_bits(const EArgs& a, int field, const uint16_t* cod
   return top & ~(0xffffffffu >> need);
 }
 
-__global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
-  __shared__ long long s_idx[kEWarps][64];
-  __shared__ uint32_t s_bits[kEWarps][64];
-  const int field = blockIdx.y;
+// one chunk, one warp (see the file comment)
+template <bool FAST>
+NBZG_DEV void encode_chunk(const EArgs& a, int field, int64_t c, const CodeTab& T,
+                           long long* s_idx, uint32_t* s_bits) {
+  const int lane = threadIdx.x & 31;
   const bool raw = a.raw_out != nullptr;
   const nbzg_field_meta* mp = raw ? nullptr : &a.meta->f[field];
-  if (!raw && (mp->is_const || a.n == 0 || a.meta->status)) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int64_t c = 0;
-  if (lane == 0) c = atomicAdd(&a.tickets[field], 1u);
-  c = __shfl_sync(0xffffffffu, c, 0);
-  if (c >= a.nchunks) return;
   const uint16_t* codes = a.codes + field * a.code_stride;
-  const uint64_t* lut = a.lut + field * a.nbins;
   uint8_t* payload = raw ? nullptr : a.arena + mp->payload_off;
   uint32_t* outw = raw ? reinterpret_cast<uint32_t*>(a.raw_out)
                        : reinterpret_cast<uint32_t*>(payload + mp->bits_off);
@@ -176,7 +199,7 @@ __global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
   for (int j = 0; j < cnt; j += 8) {
     uint16_t cv[8];
     if (vec && j + 8 <= cnt) {
-      uint4 u = *reinterpret_cast<const uint4*>(cp + j);
+      uint4 u = __ldg(reinterpret_cast<const uint4*>(cp + j));
       uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
       for (int q = 0; q < 8; q++) cv[q] = (uint16_t)(w4[q >> 1] >> ((q & 1) * 16));
@@ -187,22 +210,22 @@ __global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
 #pragma unroll
     for (int q = 0; q < 8; q++) {
       if (j + q < cnt) {
-        bits += (uint32_t)(__ldg(&lut[cv[q]]) >> 57);
+        bits += code_len<FAST>(T, cv[q]);
         if (cv[q] == 0 && a.inline_esc) bits += 32;
       }
     }
   }
   const uint32_t incl = warp_incl_scan<uint32_t>(bits);
   const uint32_t off = incl - bits;
-  const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
+  const uint32_t Tt = __shfl_sync(0xffffffffu, incl, 31);
 
   // ---- 2. publish, look back for the chunk's global bit offset
   uint64_t* lbb = a.lb + field * a.nchunks;
-  if (lane == 0 && c > 0) lb_store(&lbb[c], kFlagAgg | T);
-  const uint64_t B = lookback_sum(lbb, c, T);
+  if (lane == 0 && c > 0) lb_store(&lbb[c], kFlagAgg | Tt);
+  const uint64_t B = lookback_sum(lbb, c, Tt);
   if (lane == 0) {
-    if (raw) a.raw_chunk_bits[c] = T;
-    else put_u32_bytes(payload + mp->index_off + 4 * c, T);
+    if (raw) a.raw_chunk_bits[c] = Tt;
+    else put_u32_bytes(payload + mp->index_off + 4 * c, Tt);
   }
 
   // ---- 3. pack
@@ -218,6 +241,12 @@ __global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
       head_bits = w;
       head_pending = false;
     } else {
+#ifdef NBZG_BOUNDS
+      if (!raw && widx * 4 + mp->bits_off + 4 > mp->payload_len) {
+        printf("OOB emit field %d chunk %lld lane %d widx %llu B %llu off %u bits %u T %u plen %llu boff %llu\n", field, (long long)c, lane, (unsigned long long)widx, (unsigned long long)B, off, bits, Tt, (unsigned long long)mp->payload_len, (unsigned long long)mp->bits_off);
+        __trap();
+      }
+#endif
       outw[widx] = __byte_perm(w, 0, 0x0123);
     }
     widx++;
@@ -225,7 +254,7 @@ __global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
   for (int j = 0; j < cnt; j += 8) {
     uint16_t cv[8];
     if (vec && j + 8 <= cnt) {
-      uint4 u = *reinterpret_cast<const uint4*>(cp + j);
+      uint4 u = __ldg(reinterpret_cast<const uint4*>(cp + j));
       uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
       for (int q = 0; q < 8; q++) cv[q] = (uint16_t)(w4[q >> 1] >> ((q & 1) * 16));
@@ -234,12 +263,16 @@ __global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
       for (int q = 0; q < 8; q++) cv[q] = j + q < cnt ? cp[j + q] : (uint16_t)0xffff;
     }
     uint64_t e[8];
+    uint32_t el[8];
 #pragma unroll
-    for (int q = 0; q < 8; q++) e[q] = j + q < cnt ? __ldg(&lut[cv[q]]) : 0ull;
+    for (int q = 0; q < 8; q++) {
+      el[q] = 0;
+      e[q] = j + q < cnt ? code_word<FAST>(T, cv[q], el[q]) : 0ull;
+    }
 #pragma unroll
     for (int q = 0; q < 8; q++) {
       if (j + q < cnt) {
-        acc_put(A, e[q] & ((1ull << 57) - 1), (int)(e[q] >> 57), emit);
+        acc_put(A, e[q], (int)el[q], emit);
         if (cv[q] == 0 && a.inline_esc)
           acc_put(A, esc_value_bits(a, field, c0 + lo + j + q), 32, emit);
       }
@@ -250,15 +283,16 @@ __global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
     tail_idx = (long long)widx;
     tail_bits = (uint32_t)(A.acc >> 32);
   }
-  s_idx[warp][2 * lane] = head_idx;
-  s_bits[warp][2 * lane] = head_bits;
-  s_idx[warp][2 * lane + 1] = tail_idx;
-  s_bits[warp][2 * lane + 1] = tail_bits;
+  __syncwarp();
+  s_idx[2 * lane] = head_idx;
+  s_bits[2 * lane] = head_bits;
+  s_idx[2 * lane + 1] = tail_idx;
+  s_bits[2 * lane + 1] = tail_bits;
   __syncwarp();
 
   // ---- 4. merge boundary words (lane 0): OR the parts of each word
-  if (lane == 0 && T > 0) {
-    const uint64_t Bend = B + T;
+  if (lane == 0 && Tt > 0) {
+    const uint64_t Bend = B + Tt;
     const long long first_owned = (long long)((B + 31) >> 5);
     const long long last_word = (long long)((Bend - 1) >> 5);
     long long cur = -1;
@@ -267,22 +301,78 @@ __global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
       if (idx < first_owned) return;  // belongs to the previous chunk
       if (idx == last_word && (Bend & 31) && c + 1 < a.nchunks) {
         int need = 32 - (int)(Bend & 31);
-        w |= chunk_head_bits(a, field, codes, lut, c + 1, need) >> (Bend & 31);
+        w |= chunk_head_bits<FAST>(a, field, codes, T, c + 1, need) >> (Bend & 31);
       }
+#ifdef NBZG_BOUNDS
+      if (!raw && idx * 4 + mp->bits_off + 4 > mp->payload_len) {
+        printf("OOB merge field %d chunk %lld idx %lld B %llu T %u\n", field, (long long)c, idx, (unsigned long long)B, Tt);
+        __trap();
+      }
+#endif
       outw[idx] = __byte_perm(w, 0, 0x0123);
     };
     for (int s = 0; s < 64; s++) {
-      long long idx = s_idx[warp][s];
+      long long idx = s_idx[s];
       if (idx < 0) continue;
       if (idx == cur) {
-        acc |= s_bits[warp][s];
+        acc |= s_bits[s];
       } else {
         if (cur >= 0) flush(cur, acc);
         cur = idx;
-        acc = s_bits[warp][s];
+        acc = s_bits[s];
       }
     }
     if (cur >= 0) flush(cur, acc);
+  }
+}
+
+// hook path: one warp per ticketed chunk, global LUT
+__global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
+  __shared__ long long s_idx[kEWarps][64];
+  __shared__ uint32_t s_bits[kEWarps][64];
+  const int field = blockIdx.y;
+  const bool raw = a.raw_out != nullptr;
+  if (!raw && (a.meta->f[field].is_const || a.n == 0 || a.meta->status)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t c = 0;
+  if (lane == 0) c = atomicAdd(&a.tickets[field], 1u);
+  c = __shfl_sync(0xffffffffu, c, 0);
+  if (c >= a.nchunks) return;
+  CodeTab T{a.lut + field * a.nbins, nullptr, nullptr, nullptr};
+  encode_chunk<false>(a, field, c, T, s_idx[warp], s_bits[warp]);
+}
+
+// payload path: persistent CTAs (one field each, one per SM) stage the
+// (length, rank) tables of their field in shared memory (192 KiB), then
+// each warp encodes ticketed chunks until the field is done
+constexpr int kEFWarps = 24;
+constexpr int kEncSyms = 65536;
+__global__ void __launch_bounds__(kEFWarps * 32, 1) encode_fast_kernel(EArgs a) {
+  extern __shared__ __align__(16) uint8_t esm[];
+  uint16_t* s_rank = reinterpret_cast<uint16_t*>(esm);                 // [65536]
+  uint8_t* s_len = esm + 2 * kEncSyms;                                 // [65536]
+  uint64_t* s_fc = reinterpret_cast<uint64_t*>(esm + 3 * kEncSyms);    // [64]
+  long long* s_idx = reinterpret_cast<long long*>(s_fc + 64);          // [warps][64]
+  uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_idx + kEFWarps * 64);
+  const int field = blockIdx.y;
+  if (a.meta->f[field].is_const || a.n == 0 || a.meta->status) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  {
+    const uint4* gr = reinterpret_cast<const uint4*>(a.trank + (size_t)field * a.nbins);
+    const uint4* gl = reinterpret_cast<const uint4*>(a.tlen + (size_t)field * a.nbins);
+    const int nr = (int)(a.nbins * 2 / 16), nl = (int)(a.nbins / 16);
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) reinterpret_cast<uint4*>(s_rank)[i] = __ldg(gr + i);
+    for (int i = threadIdx.x; i < nl; i += blockDim.x) reinterpret_cast<uint4*>(s_len)[i] = __ldg(gl + i);
+    if (threadIdx.x < 64) s_fc[threadIdx.x] = a.tfc[field * 64 + threadIdx.x];
+  }
+  __syncthreads();
+  CodeTab T{nullptr, s_len, s_rank, s_fc};
+  while (true) {
+    int64_t c = 0;
+    if (lane == 0) c = atomicAdd(&a.tickets[field], 1u);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= a.nchunks) return;
+    encode_chunk<true>(a, field, c, T, s_idx + warp * 64, s_bits + warp * 64);
   }
 }
 
@@ -306,11 +396,29 @@ int launch_encode(const Plan& p, cudaStream_t st) {
   a.lb = p.lb;
   a.tickets = p.counters;
   a.inline_esc = 1;
+  a.tlen = p.enc_len;
+  a.trank = p.enc_rank;
+  a.tfc = p.enc_fc;
   cudaMemsetAsync(p.lb, 0, sizeof(uint64_t) * 6 * p.nchunks, st);
   cudaMemsetAsync(p.counters, 0, sizeof(uint32_t) * 8, st);
-  dim3 grid((unsigned)((p.nchunks + kEWarps - 1) / kEWarps), 6);
-  count_launch();
-  encode_kernel<<<grid, kEThreads, 0, st>>>(a);
+  if (p.nbins == kEncSyms) {
+    const size_t sm = 3 * kEncSyms + 64 * 8 + kEFWarps * 64 * 12;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(encode_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sm);
+      attr = true;
+    }
+    int groups = max(1, sm_count() / 6);
+    const int64_t need = (p.nchunks + kEFWarps - 1) / kEFWarps;
+    if (groups > need) groups = (int)need;
+    count_launch();
+    encode_fast_kernel<<<dim3(groups, 6), kEFWarps * 32, sm, st>>>(a);
+  } else {
+    dim3 grid((unsigned)((p.nchunks + kEWarps - 1) / kEWarps), 6);
+    count_launch();
+    encode_kernel<<<grid, kEThreads, 0, st>>>(a);
+  }
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
 
