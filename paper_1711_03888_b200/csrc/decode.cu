@@ -693,24 +693,77 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
 // take the canonical slow path (limits + symbol table, also in smem).
 constexpr int kTpcMinChunks = 256;
 
-NBZG_DEV void br_skip_c(BitReader& R, uint32_t l, uint32_t vmax) {  // clamped refills
+// Per-lane bit reader of the thread-per-chunk decoder.  The window (w0, w1)
+// lives in registers; the words after it come from an 8-word ring per lane
+// in shared memory (word-major, so lanes never conflict).  Refills happen
+// only at 8-symbol group boundaries: the 16-byte block loaded at the
+// previous boundary is stored into the ring and the next block's load is
+// issued.  A register that is the target of an in-flight load is therefore
+// read once per group, 8 symbols after its load was issued -- never inside
+// the decode step (the register scoreboard is per warp: a per-step refill
+// by any lane would stall every lane).  A lane that outruns its ring reads
+// the word straight from global memory (rare: > 4 words in 8 symbols).
+struct TpcReader {
+  uint32_t w0, w1, off;  // window: bits [off, off+32) of w0:w1
+  uint32_t wi;           // stream word index of w1
+  uint32_t wr;           // first stream word not in the ring (multiple of 4)
+  uint4 qs;              // block wr/4, loaded at the last boundary
+};
+
+NBZG_DEV void tpc_init(TpcReader& R, const uint4* G, uint32_t* ring, int nthr, uint64_t bitpos,
+                       uint32_t vmax) {
+  const uint32_t gw0 = (uint32_t)(bitpos >> 5);
+  const uint32_t blk = gw0 >> 2;
+  const uint4 A = __ldg(G + min(blk, vmax)), B = __ldg(G + min(blk + 1, vmax));
+  const uint32_t s0 = (4 * blk) & 7, s1 = s0 ^ 4;  // word 4 blk + i -> slot (4 blk + i) & 7
+  ring[(s0 + 0) * nthr] = A.x;
+  ring[(s0 + 1) * nthr] = A.y;
+  ring[(s0 + 2) * nthr] = A.z;
+  ring[(s0 + 3) * nthr] = A.w;
+  ring[(s1 + 0) * nthr] = B.x;
+  ring[(s1 + 1) * nthr] = B.y;
+  ring[(s1 + 2) * nthr] = B.z;
+  ring[(s1 + 3) * nthr] = B.w;
+  R.off = (uint32_t)(bitpos & 31);
+  R.w0 = bswap32(ring[(gw0 & 7) * nthr]);
+  R.w1 = bswap32(ring[((gw0 + 1) & 7) * nthr]);
+  R.wi = gw0 + 1;
+  R.wr = 4 * (blk + 2);
+  R.qs = make_uint4(0, 0, 0, 0);
+  ldg_v4_if(R.qs, G + min(blk + 2, vmax), true);
+}
+
+// consume l <= 32 bits.  The next ring word is read unconditionally (its
+// address depends only on wi, so the load overlaps the table lookup) and the
+// window advances through selects; only a lane that outran its ring takes
+// the branch to global memory.
+NBZG_DEV void tpc_skip(TpcReader& R, uint32_t l, const uint32_t* ring, int nthr,
+                       const uint32_t* G32, uint32_t wmax, uint32_t nw) {
   R.off += l;
-  bool refill = false;
-  if (R.off >= 32) {
-    R.off -= 32;
-    R.w0 = R.w1;
-    R.w1 = bswap32(R.qa.x);
-    R.qa.x = R.qa.y;
-    R.qa.y = R.qa.z;
-    R.qa.z = R.qa.w;
-    refill = --R.nq == 0;
-    if (refill) {
-      R.qa = R.qb;
-      R.nq = 4;
-    }
+  const bool cross = R.off >= 32;
+  if (cross && (int32_t)(R.wr - (R.wi + 1)) <= 0) {  // outran the ring (rare)
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(nw) : "l"(G32 + min(R.wi + 1, wmax)));
   }
-  ldg_v4_if(R.qb, R.g4 + min(R.vi, vmax), refill);
-  R.vi += refill ? 1u : 0u;
+  R.w0 = cross ? R.w1 : R.w0;
+  R.w1 = cross ? bswap32(nw) : R.w1;
+  R.wi += cross ? 1u : 0u;
+  R.off -= cross ? 32u : 0u;
+}
+NBZG_DEV uint32_t tpc_next(const TpcReader& R, const uint32_t* ring, int nthr) {
+  return ring[((R.wi + 1) & 7) * nthr];
+}
+
+NBZG_DEV void tpc_refill(TpcReader& R, uint32_t* ring, int nthr, const uint4* G, uint32_t vmax) {
+  const bool room = (int32_t)(R.wr - R.wi) <= 5;
+  if (room) {
+    const uint32_t s = R.wr & 7;  // 0 or 4
+    ring[(s + 0) * nthr] = R.qs.x;
+    ring[(s + 1) * nthr] = R.qs.y;
+    ring[(s + 2) * nthr] = R.qs.z;
+    ring[(s + 3) * nthr] = R.qs.w;
+    R.wr += 4;
+  }
+  ldg_v4_if(R.qs, G + min(R.wr >> 2, vmax), room);
 }
 
 __global__ void __launch_bounds__(1024, 1) decode_tpc_kernel(DArgs a, int ctas_per_field) {
@@ -725,13 +778,14 @@ __global__ void __launch_bounds__(1024, 1) decode_tpc_kernel(DArgs a, int ctas_p
   const int64_t cb = (a.nchunks * blockIdx.x) / ctas_per_field;
   const int64_t ce = (a.nchunks * (blockIdx.x + 1)) / ctas_per_field;
   if (cb >= ce) return;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  uint32_t* ring = reinterpret_cast<uint32_t*>(dsm2 + 4 * kTpcTab) + tid;  // [8][nthr]
   const uint32_t* ss = a.ssyms + fi * a.nbins;
   const uint32_t n2 = P.t2_n;
   {
     const int32_t* gl = a.lut2 + (size_t)fi * kTpcTab;
     const uint32_t nv = ((1u << kTpcBits) + n2 + 3) / 4;
-    for (uint32_t i = tid; i < nv; i += blockDim.x)
+    for (uint32_t i = tid; i < nv; i += nthr)
       reinterpret_cast<uint4*>(LT)[i] = __ldg(reinterpret_cast<const uint4*>(gl) + i);
   }
   if (tid < 64) {
@@ -749,9 +803,11 @@ __global__ void __launch_bounds__(1024, 1) decode_tpc_kernel(DArgs a, int ctas_p
 
   const uintptr_t bits_addr = reinterpret_cast<uintptr_t>(F.payload + P.bits_off);
   const uint4* G = reinterpret_cast<const uint4*>(bits_addr & ~uintptr_t(15));
+  const uint32_t* G32 = reinterpret_cast<const uint32_t*>(G);
   const uint32_t a0 = (uint32_t)(bits_addr & 15) * 8;
-  // last 16-byte block the stream may touch (payload + 64-byte read slack)
+  // last 16-byte block / word the stream may touch (payload + 64-byte slack)
   const uint32_t vmax = (uint32_t)((a0 / 8 + 4 * ((P.total_bits + 31) / 32) + 16) / 16);
+  const uint32_t wmax = 4 * vmax + 3;
   const uint64_t* choff = a.choff + fi * (a.nchunks + 1);
   const int bias = a.half + 1;
   const int max_len = (int)P.max_len;
@@ -759,27 +815,30 @@ __global__ void __launch_bounds__(1024, 1) decode_tpc_kernel(DArgs a, int ctas_p
   const bool vec = (reinterpret_cast<uintptr_t>(F.out) & 15) == 0;
   const uint32_t r0 = (uint32_t)min(P.t2_r0, (uint64_t)0xFFFFFFFFu);
   const uint32_t sh2 = 32u - P.t2_w;
-  int32_t* LT2 = LT + (1 << kTpcBits);
+  const int32_t* LT2 = LT + (1 << kTpcBits);
+  const uint32_t n2m1 = n2 ? n2 - 1 : 0;
 
-  for (int64_t c = cb + tid; c < ce; c += blockDim.x) {
+  for (int64_t c = cb + tid; c < ce; c += nthr) {
     const uint64_t b0 = choff[c];
-    const uint32_t Tb = (uint32_t)(choff[c + 1] - b0);
+    const uint64_t Tb = choff[c + 1] - b0;
     const int64_t i0 = c * kChunk;
     const int mc = (int)min((int64_t)kChunk, a.n - i0);
-    BitReader R;
-    br_init(R, G, a0 + b0);
-    uint32_t pos = 0;
+    const uint64_t B = a0 + b0;
+    TpcReader R;
+    tpc_init(R, G, ring, nthr, B, vmax);
     double kd = 0.0;
     int err = 0;
     float* dst = F.out + i0;
-    // one symbol: returns the value, advances the reader
-    auto step = [&](float& o) {
-      const uint32_t v = br_peek(R);
+    // bits consumed so far
+    auto consumed = [&]() -> uint64_t { return ((uint64_t)(R.wi - 1) << 5) + R.off - B; };
+    // canonical decode of the symbol at the window (any length <= 32):
+    // returns the fused entry (length | escape flag | delta)
+    auto resolve = [&](uint32_t v) -> int32_t {
       int32_t e = LT[v >> (32 - kTpcBits)];
       if ((e & 63) == 0) {
-        const uint32_t j = (v - r0) >> sh2;  // long code: secondary table
+        const uint32_t j = (v - r0) >> sh2;
         e = (v >= r0 && j < n2) ? LT2[j] : 0;
-        if ((e & 63) == 0) {  // longer than W bits, or invalid: canonical search
+        if ((e & 63) == 0) {
           int r = 0;
 #pragma unroll 1
           for (int len = max_len; len >= 1; len--) r = ((uint64_t)v < s_limit[len]) ? len : r;
@@ -792,37 +851,98 @@ __global__ void __launch_bounds__(1024, 1) decode_tpc_kernel(DArgs a, int ctas_p
           }
         }
       }
-      uint32_t l = (uint32_t)e & 63u;
-      if (e & 64) {  // escape: the raw float follows the codeword
-        br_skip_c(R, l, vmax);
-        pos += l;
-        o = __uint_as_float(br_peek(R));
-        l = 32;
+      return e;
+    };
+    // exact step (ring or global words): escapes, slow codes, replays, tails
+    auto safe_step = [&](float& o) {
+      const int32_t e = resolve(__funnelshift_l(R.w1, R.w0, R.off));
+      const uint32_t l = (uint32_t)e & 63u;
+      if (e & 64) {
+        tpc_skip(R, l, ring, nthr, G32, wmax, tpc_next(R, ring, nthr));
+        o = __uint_as_float(__funnelshift_l(R.w1, R.w0, R.off));
         kd = (double)esc_k(o, F);
+        tpc_skip(R, 32, ring, nthr, G32, wmax, tpc_next(R, ring, nthr));
       } else {
         kd += (double)(e >> 7);
         o = (float)__dmul_rn(kd, twob);
+        tpc_skip(R, l, ring, nthr, G32, wmax, tpc_next(R, ring, nthr));
       }
-      br_skip_c(R, l, vmax);
-      pos += l;
+    };
+    // common step: table hit (primary or secondary), no escape; the window
+    // advances from the ring speculatively and `under` records a lane that
+    // needed a word the ring did not hold yet (the group is then replayed)
+    bool under = false;
+    auto fast_step = [&](float& o) {
+      const uint32_t v = __funnelshift_l(R.w1, R.w0, R.off);
+      const uint32_t nw = tpc_next(R, ring, nthr);
+      int32_t e = LT[v >> (32 - kTpcBits)];
+      const uint32_t j = min((v - r0) >> sh2, n2m1);
+      const int32_t e2 = LT2[j];
+      if ((e & 63) == 0) e = (v >= r0 && ((v - r0) >> sh2) < n2) ? e2 : 0;
+      if ((e & 63) == 0 || (e & 64)) {
+        safe_step(o);
+        return;
+      }
+      kd += (double)(e >> 7);
+      o = (float)__dmul_rn(kd, twob);
+      R.off += (uint32_t)e & 63u;
+      const bool cross = R.off >= 32;
+      under |= cross && (int32_t)(R.wr - R.wi) <= 1;
+      R.w0 = cross ? R.w1 : R.w0;
+      R.w1 = cross ? bswap32(nw) : R.w1;
+      R.wi += cross ? 1u : 0u;
+      R.off -= cross ? 32u : 0u;
+    };
+    // 8 symbols; replayed exactly if any window word came from past the ring
+    auto group = [&](float (&o)[8]) {
+      const TpcReader S = R;
+      const double kd0 = kd;
+      under = false;
+#pragma unroll
+      for (int q = 0; q < 8; q++) fast_step(o[q]);
+      if (under) {
+        R = S;
+        kd = kd0;
+#pragma unroll 1
+        for (int q = 0; q < 8; q++) {
+          float t;
+          safe_step(t);
+#pragma unroll
+          for (int u = 0; u < 8; u++) o[u] = (u == q) ? t : o[u];
+        }
+      }
+      tpc_refill(R, ring, nthr, G, vmax);
     };
     int i = 0;
     if (vec) {
-      for (; i + 8 <= mc; i += 8) {
-        float o[8];
+      // two register sets: a set's 16-byte stores are issued one group
+      // before the set is rewritten (pinned live meanwhile), so the decode
+      // never waits for the store queue to read its source registers
+      float oa[8], ob[8];
 #pragma unroll
-        for (int j = 0; j < 8; j++) step(o[j]);
+      for (int u = 0; u < 8; u++) ob[u] = 0.0f;
+      for (; i + 16 <= mc; i += 16) {
+        group(oa);
+        asm volatile("" ::"f"(ob[0]), "f"(ob[1]), "f"(ob[2]), "f"(ob[3]), "f"(ob[4]),
+                     "f"(ob[5]), "f"(ob[6]), "f"(ob[7]));
         float4* d4 = reinterpret_cast<float4*>(dst + i);
-        __stcs(d4, make_float4(o[0], o[1], o[2], o[3]));
-        __stcs(d4 + 1, make_float4(o[4], o[5], o[6], o[7]));
-        if (pos > Tb) break;  // corrupt: stop early, reported below
+        __stcs(d4, make_float4(oa[0], oa[1], oa[2], oa[3]));
+        __stcs(d4 + 1, make_float4(oa[4], oa[5], oa[6], oa[7]));
+        group(ob);
+        asm volatile("" ::"f"(oa[0]), "f"(oa[1]), "f"(oa[2]), "f"(oa[3]), "f"(oa[4]),
+                     "f"(oa[5]), "f"(oa[6]), "f"(oa[7]));
+        __stcs(d4 + 2, make_float4(ob[0], ob[1], ob[2], ob[3]));
+        __stcs(d4 + 3, make_float4(ob[4], ob[5], ob[6], ob[7]));
+        if (consumed() > Tb) break;  // corrupt: stop early, reported below
       }
     }
-    for (; i < mc && pos <= Tb; i++) {
+    for (; i < mc && consumed() <= Tb; i++) {
       float o;
-      step(o);
+      safe_step(o);
+      if ((i & 7) == 7) tpc_refill(R, ring, nthr, G, vmax);
       dst[i] = o;
     }
+    const uint64_t pos = consumed();
     if (!err && pos != Tb) err = pos > Tb ? NBZG_TRUNCATED : NBZG_BAD_STREAM;
     if (err) fail(a.status, (uint32_t)err);
   }
@@ -989,7 +1109,7 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
     if (use_tpc(a.nchunks)) {
       const int per = (int)((a.nchunks + groups - 1) / groups);
       const int thr = min(1024, (per + 31) / 32 * 32);
-      const size_t sm2 = 4 * kTpcTab;
+      const size_t sm2 = 4 * kTpcTab + 32 * (size_t)thr;
       static bool attr2 = false;
       if (!attr2) {
         cudaFuncSetAttribute(decode_tpc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
