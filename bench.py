@@ -252,7 +252,7 @@ def run_b200(args):
 
     import paper_1711_03888_b200 as nbz
     from paper_1711_03888_b200 import _native as N
-    from paper_1711_03888_b200 import datagen
+    from paper_1711_03888_b200 import datagen, shard
 
     rank, world, local = dist_init(args.gpus)
     N.lib()
@@ -269,33 +269,23 @@ def run_b200(args):
     torch.cuda.synchronize()
     snap = nbz.ParticleSnapshot(*dev)
 
-    # global bounds: all-gather of per-shard min/max (collective 1)
-    mm = []
-    for f in dev:
-        lo, hi = torch.aminmax(f)
-        mm += [float(lo), float(hi)]
-    g = allgather_f64(mm, world)
-    if world == 1:
-        bounds = nbz.ErrorBoundSpec.relative(args.eb)
-    else:
-        bounds = {}
-        for i, name in enumerate(nbz.FIELD_NAMES):
-            rng = float(g[:, 2 * i + 1].max()) - float(g[:, 2 * i].min())
-            bounds[name] = nbz.ErrorBoundSpec.absolute(args.eb * rng if rng > 0 else 1.0)
+    bounds = nbz.ErrorBoundSpec.relative(args.eb)
+    shard_bounds = [None]
 
     def step(record=None):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e2 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        res = nbz.compress(snap, args.mode, bounds)
-        sizes = allgather_f64([float(res.archive.total_bytes())], world)  # collective 2
+        # global bounds (collective 1), shard compress, archive sizes (collective 2)
+        sr = shard.compress_shard(snap, args.mode, bounds, device="cuda")
         e1.record()
-        out = nbz.decompress(res.archive, device=True)
+        out = nbz.decompress(sr.result.archive, device=True)
         e2.record()
         if record is not None:
-            record.append((e0, e1, e2, res.archive.total_bytes(), sizes))
-        return res, out
+            record.append((e0, e1, e2, sr.result.archive.total_bytes(), sr.total_bytes))
+        shard_bounds[0] = sr.bounds
+        return sr, out
 
     for _ in range(args.warmup):
         step()
@@ -324,7 +314,7 @@ def run_b200(args):
     ms_step = total_ms / args.steps
     last = rec[-1]
     S_local = last[3]
-    S_total = float(last[4].sum())
+    S_total = float(last[4])
     n_total = n * world
     hbm, peak_kind = peaks()
 
@@ -355,9 +345,11 @@ def run_b200(args):
     if args.e2e_steps > 0:
         from paper_1711_03888_b200 import io as nio
         hsnap = nbz.ParticleSnapshot(*host)
+        # the globally resolved bounds of the device step (identical at N=1)
+        e2e_bounds = dict(zip(nbz.FIELD_NAMES, shard_bounds[0]))
 
         def e2e_step():
-            res = nbz.compress(hsnap, args.mode, bounds)
+            res = nbz.compress(hsnap, args.mode, e2e_bounds)
             wire = res.archive.serialized()
             ar = nio.deserialize_archive(wire)
             out = nbz.decompress(ar, device=False)
