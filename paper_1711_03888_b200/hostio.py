@@ -1,0 +1,151 @@
+"""Host <-> device transfers for the public API's host-buffer paths.
+
+PCIe moves pinned memory at ~50 GB/s but pageable memory far slower, and
+the reference's API hands out plain ``bytes`` / numpy arrays.  Every large
+transfer therefore goes through two grow-only pinned staging buffers: the
+DMA of chunk k+1 overlaps the (multi-threaded) CPU copy of chunk k between
+the staging buffer and the caller's pageable memory.  Already-pinned host
+tensors are copied directly.
+"""
+
+from __future__ import annotations
+
+from typing import Dict, Tuple
+
+import numpy as np
+
+CHUNK = 64 << 20  # bytes per staging chunk
+
+_pinned: Dict[Tuple[str, int], object] = {}
+
+
+def pinned(role: str, nbytes: int):
+    """Grow-only pinned uint8 host buffer keyed by role."""
+    import torch
+    key = (role, 0)
+    b = _pinned.get(key)
+    if b is None or b.numel() < nbytes:
+        b = torch.empty(max(int(nbytes), 4096), dtype=torch.uint8, pin_memory=True)
+        _pinned[key] = b
+    return b
+
+
+def _host_u8(buf):
+    """A uint8 CPU tensor viewing `buf` (bytes / bytearray / memoryview /
+    numpy / CPU tensor) without copying."""
+    import torch
+    if isinstance(buf, torch.Tensor):
+        return buf.reshape(-1).view(torch.uint8)
+    if isinstance(buf, np.ndarray):
+        return torch.from_numpy(np.ascontiguousarray(buf).reshape(-1).view(np.uint8))
+    mv = memoryview(buf).cast("B")
+    if mv.readonly:  # torch wants a writable buffer; numpy gives a read-only view
+        import warnings
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            return torch.frombuffer(mv, dtype=torch.uint8)
+    return torch.frombuffer(mv, dtype=torch.uint8)
+
+
+def to_device(src, dst) -> None:
+    """Copy host bytes `src` into the CUDA uint8 tensor `dst` (same length)."""
+    import torch
+    h = _host_u8(src)
+    n = h.numel()
+    if n == 0:
+        return
+    if h.is_pinned():
+        dst[:n].copy_(h, non_blocking=True)
+        return
+    stage = [pinned("h2d0", CHUNK), pinned("h2d1", CHUNK)]
+    ev = [None, None]
+    stream = torch.cuda.current_stream()
+    for k, off in enumerate(range(0, n, CHUNK)):
+        m = min(CHUNK, n - off)
+        s = k & 1
+        if ev[s] is not None:
+            ev[s].synchronize()  # the DMA that last read this buffer is done
+        stage[s][:m].copy_(h[off:off + m])
+        dst[off:off + m].copy_(stage[s][:m], non_blocking=True)
+        ev[s] = torch.cuda.Event()
+        ev[s].record(stream)
+
+
+def to_host(src, dst) -> None:
+    """Copy the CUDA uint8 tensor `src` into host memory `dst` (a writable
+    buffer / numpy array / CPU tensor of the same byte length)."""
+    import torch
+    h = _host_u8(dst)
+    n = h.numel()
+    if n == 0:
+        return
+    if h.is_pinned():
+        h.copy_(src[:n], non_blocking=False)
+        return
+    stage = [pinned("d2h0", CHUNK), pinned("d2h1", CHUNK)]
+    stream = torch.cuda.current_stream()
+    chunks = list(range(0, n, CHUNK))
+    ev = [None, None]
+
+    def issue(k):
+        off = chunks[k]
+        m = min(CHUNK, n - off)
+        stage[k & 1][:m].copy_(src[off:off + m], non_blocking=True)
+        e = torch.cuda.Event()
+        e.record(stream)
+        ev[k & 1] = e
+
+    issue(0)
+    for k, off in enumerate(chunks):
+        if k + 1 < len(chunks):
+            issue(k + 1)
+        ev[k & 1].synchronize()
+        m = min(CHUNK, n - off)
+        h[off:off + m].copy_(stage[k & 1][:m])
+
+
+def bytes_from(src_u8, n: int) -> bytes:
+    """A new ``bytes`` object holding the first n bytes of the CPU uint8
+    tensor `src_u8` (typically pinned), filled by torch's multi-threaded
+    copy instead of a single-threaded memcpy: the object is created
+    uninitialised (PyBytes_FromStringAndSize(NULL, n), the CPython idiom
+    for building a bytes object in place) and written before anyone else
+    can see it."""
+    import ctypes
+
+    import torch
+    if n == 0:
+        return b""
+    api = ctypes.pythonapi
+    api.PyBytes_FromStringAndSize.restype = ctypes.py_object
+    api.PyBytes_FromStringAndSize.argtypes = [ctypes.c_void_p, ctypes.c_ssize_t]
+    api.PyBytes_AsString.restype = ctypes.c_void_p
+    api.PyBytes_AsString.argtypes = [ctypes.py_object]
+    b = api.PyBytes_FromStringAndSize(None, n)
+    addr = api.PyBytes_AsString(b)
+    dst = torch.from_numpy(np.ctypeslib.as_array((ctypes.c_uint8 * n).from_address(addr)))
+    dst.copy_(src_u8[:n])
+    return b
+
+
+def empty_host(numel: int, dtype=None):
+    """Fresh pageable CPU tensor advised to transparent huge pages, so the
+    first-touch page faults of a multi-GB output cost ~1/512 as many
+    faults (no-op where THP is disabled)."""
+    import ctypes
+
+    import torch
+    dtype = dtype or torch.float32
+    t = torch.empty(numel, dtype=dtype)
+    nbytes = t.numel() * t.element_size()
+    if nbytes >= (4 << 20):
+        try:
+            libc = ctypes.CDLL(None, use_errno=True)
+            addr = t.data_ptr()
+            a0 = (addr + (2 << 20) - 1) & ~((2 << 20) - 1)
+            ln = (addr + nbytes - a0) & ~((2 << 20) - 1)
+            if ln > 0:
+                libc.madvise(ctypes.c_void_p(a0), ctypes.c_size_t(ln), 14)  # MADV_HUGEPAGE
+        except Exception:
+            pass
+    return t

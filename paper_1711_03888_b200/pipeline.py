@@ -159,6 +159,7 @@ class Archive:
         self.version = version
         self.device_output = device_output
         self._wire: Optional[bytes] = None
+        self._host_dir = None  # deserialized: [(kind, field, wire offset, length)]
 
     # -- reference attributes -------------------------------------------------
     def is_constant(self, field_index: int) -> bool:
@@ -188,6 +189,10 @@ class Archive:
 
     @property
     def streams(self) -> Tuple[Stream, ...]:
+        if self._streams is None and self._host_dir is not None:
+            w = self._wire  # deserialized archive: slices of the wire, in directory order
+            self._streams = tuple(Stream(StreamKind(k), f, bytes(w[a:a + ln]))
+                                  for k, f, a, ln in self._host_dir)
         if self._streams is None:
             d = self._dev
             host = d.arena.cpu().numpy() if d is not None else None
@@ -471,9 +476,16 @@ def decompress(archive: Archive, device: Optional[bool] = None) -> ParticleSnaps
     if st:
         raise DecodeError(f"decompress: {N.STATUS_NAMES.get(st, st)}")
     snap = ParticleSnapshot.__new__(ParticleSnapshot)
+    if not device:
+        # one staged D2H of all six fields into fresh host memory
+        from . import hostio
+        host = hostio.empty_host(6 * stride, torch.float32)
+        hostio.to_host(out.view(torch.uint8), host.view(torch.uint8))
+        hn = host.numpy()
+        views = [hn[i * stride:i * stride + n] for i in range(6)]
     for i, name in enumerate(FIELD_NAMES):
         object.__setattr__(snap, name, views[i])
-    return snap if device else snap.numpy()
+    return snap
 
 
 def ratio(archive: Archive, original_bytes: Optional[int] = None) -> Optional[float]:
