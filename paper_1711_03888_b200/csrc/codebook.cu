@@ -32,9 +32,8 @@ struct CBArgs {
   int64_t n;
   int64_t nchunks;
   int single_field;   // >= 0: only this field (parity hook), meta->f[0] receives
-  uint8_t* tlen;      // [6][nbins] length by symbol (encoder tables; may be null)
-  uint16_t* trank;    // [6][nbins] rank within the length class
-  uint64_t* tfc;      // [6][64] first canonical code per length
+  uint32_t* twin;     // [6][kEncWin] encoder window table (may be null): code
+                      // half+1-kEncWin/2+i -> word << 6 | len (len <= 26, else 0)
 };
 
 NBZG_DEV void bitonic_sort_u64(uint64_t* a, int N) {
@@ -224,7 +223,6 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
     fm.max_len = s_max;
   }
   __syncthreads();
-  if (a.tfc && tid < 64) a.tfc[field * 64 + tid] = (tid >= 1 && tid <= max_len) ? s_fc[tid] : 0;
   // rank within length class, ascending symbol: per present length, a block scan
   const int RK = (k + kCBThreads - 1) / kCBThreads;
   for (int l = 1; l <= max_len; l++) {
@@ -240,9 +238,10 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
       int i = tid * RK + r;
       if (i < k && lenr[i] == l) {
         lut[sym[i]] = ((uint64_t)l << 57) | (s_fc[l] + ex);
-        if (a.tlen) {
-          a.tlen[field * a.nbins + sym[i]] = (uint8_t)l;
-          a.trank[field * a.nbins + sym[i]] = (uint16_t)ex;
+        if (a.twin) {
+          const uint32_t wi = sym[i] - (uint32_t)(a.nbins / 2 + 1 - kEncWin / 2);
+          if (wi < (uint32_t)kEncWin)
+            a.twin[field * kEncWin + wi] = l <= 26 ? (uint32_t)((s_fc[l] + ex) << 6) | l : 0u;
         }
         ex++;
       }
@@ -267,8 +266,8 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
 int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uint8_t* len,
                          uint64_t* lut, uint32_t* scratch, nbzg_meta* meta, int64_t n,
                          int64_t nchunks, int single_field, cudaStream_t st,
-                         uint8_t* tlen, uint16_t* trank, uint64_t* tfc) {
-  CBArgs a{hist, nbins, sym, len, lut, scratch, meta, n, nchunks, single_field, tlen, trank, tfc};
+                         uint32_t* twin) {
+  CBArgs a{hist, nbins, sym, len, lut, scratch, meta, n, nchunks, single_field, twin};
   size_t sm = 14 * (size_t)kCBSmemK;  // keys u64 | L u32 | order u16
   static bool attr = false;
   if (!attr) {
@@ -283,7 +282,7 @@ int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uin
 int launch_codebook(const Plan& p, cudaStream_t st) {
   if (p.n == 0) return NBZG_OK;
   return launch_codebook_impl(p.hist, p.nbins, p.cb_sym, p.cb_len, p.lut, p.cb_scratch, p.meta,
-                              p.n, p.nchunks, -1, st, p.enc_len, p.enc_rank, p.enc_fc);
+                              p.n, p.nchunks, -1, st, p.enc_win);
 }
 
 // ---- parity hook: K.huffman_lengths on sorted counts (one CTA)

@@ -83,9 +83,7 @@ struct EArgs {
   const uint16_t* codes;  // [6][code_stride]
   int64_t code_stride;
   const uint64_t* lut;    // [6][nbins]
-  const uint8_t* tlen;    // [6][nbins] (FAST path: staged in smem)
-  const uint16_t* trank;  // [6][nbins]
-  const uint64_t* tfc;    // [6][64]
+  const uint32_t* twin;   // [6][kEncWin] (payload path: staged in smem)
   int64_t nbins;
   int64_t n, nchunks;
   const float* f[6];
@@ -126,24 +124,17 @@ NBZG_DEV void acc_put(Acc& A, uint64_t v, int nb, Emit&& emit) {
   }
 }
 
-// code-word lookup: global u64 LUT (hook path) or the smem (length, rank)
-// tables plus first canonical codes (payload path)
+// code-word lookup through the global u64 LUT (hook path; slow path of the
+// payload encoder)
 struct CodeTab {
   const uint64_t* lut;
-  const uint8_t* len;
-  const uint16_t* rank;
-  const uint64_t* fc;
 };
 template <bool FAST>
 NBZG_DEV uint32_t code_len(const CodeTab& T, uint32_t code) {
-  return FAST ? (uint32_t)T.len[code] : (uint32_t)(__ldg(&T.lut[code]) >> 57);
+  return (uint32_t)(__ldg(&T.lut[code]) >> 57);
 }
 template <bool FAST>
 NBZG_DEV uint64_t code_word(const CodeTab& T, uint32_t code, uint32_t& l) {
-  if (FAST) {
-    l = T.len[code];
-    return T.fc[l] + T.rank[code];
-  }
   const uint64_t e = __ldg(&T.lut[code]);
   l = (uint32_t)(e >> 57);
   return e & ((1ull << 57) - 1);
@@ -338,41 +329,232 @@ __global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
   if (lane == 0) c = atomicAdd(&a.tickets[field], 1u);
   c = __shfl_sync(0xffffffffu, c, 0);
   if (c >= a.nchunks) return;
-  CodeTab T{a.lut + field * a.nbins, nullptr, nullptr, nullptr};
+  CodeTab T{a.lut + field * a.nbins};
   encode_chunk<false>(a, field, c, T, s_idx[warp], s_bits[warp]);
 }
 
-// payload path: persistent CTAs (one field each, one per SM) stage the
-// (length, rank) tables of their field in shared memory (192 KiB), then
-// each warp encodes ticketed chunks until the field is done
-constexpr int kEFWarps = 24;
-constexpr int kEncSyms = 65536;
-__global__ void __launch_bounds__(kEFWarps * 32, 1) encode_fast_kernel(EArgs a) {
+// ---- payload path.  Code words of the codes nearest the centre (deltas in
+// [-8192, 8191], length <= 26: all but a few per mille of the codes) come
+// from a 64 KiB shared-memory window table, one LDS per code; the rest from
+// the global LUT.  Code loads are software-pipelined one 8-code group ahead.
+struct WinTab {
+  const uint32_t* win;  // smem [kEncWin]
+  uint32_t wlo;         // code of win[0]
+  const uint64_t* lut;  // global fallback
+};
+NBZG_DEV uint32_t win_len(const WinTab& T, uint32_t code) {
+  const uint32_t wi = code - T.wlo;
+  const uint32_t e = wi < (uint32_t)kEncWin ? T.win[wi] : 0u;
+  return e ? (e & 63u) : (uint32_t)(__ldg(&T.lut[code]) >> 57);
+}
+// (word, len); returns false when the word came from the global LUT
+NBZG_DEV bool win_word(const WinTab& T, uint32_t code, uint64_t& w, uint32_t& l) {
+  const uint32_t wi = code - T.wlo;
+  const uint32_t e = wi < (uint32_t)kEncWin ? T.win[wi] : 0u;
+  if (e) {
+    w = e >> 6;
+    l = e & 63u;
+    return true;
+  }
+  const uint64_t g = __ldg(&T.lut[code]);
+  l = (uint32_t)(g >> 57);
+  w = g & ((1ull << 57) - 1);
+  return false;
+}
+
+NBZG_DEV uint32_t chunk_head_bits_w(const EArgs& a, int field, const uint16_t* codes,
+                                    const WinTab& T, int64_t c1, int need) {
+  const int64_t s0 = c1 * kChunk, s1 = min(a.n, s0 + kChunk);
+  uint64_t acc = 0;
+  int nacc = 0;
+  for (int64_t i = s0; i < s1 && nacc < need; i++) {
+    const uint32_t code = codes[i];
+    uint64_t w;
+    uint32_t lu;
+    win_word(T, code, w, lu);
+    int l = (int)lu;
+    if (l > 32) {
+      w >>= (l - 32);
+      l = 32;
+    }
+    acc |= (w << (64 - l)) >> nacc;
+    nacc += l;
+    if (code == 0 && nacc < need) {
+      acc |= ((uint64_t)esc_value_bits(a, field, i) << 32) >> nacc;
+      nacc += 32;
+    }
+  }
+  return (uint32_t)(acc >> 32) & ~(0xffffffffu >> need);
+}
+
+NBZG_DEV void unpack8(uint4 u, uint32_t (&cv)[8]) {
+  cv[0] = u.x & 0xffffu; cv[1] = u.x >> 16;
+  cv[2] = u.y & 0xffffu; cv[3] = u.y >> 16;
+  cv[4] = u.z & 0xffffu; cv[5] = u.z >> 16;
+  cv[6] = u.w & 0xffffu; cv[7] = u.w >> 16;
+}
+
+NBZG_DEV void encode_chunk_fast(const EArgs& a, int field, int64_t c, const WinTab& T,
+                                long long* s_idx, uint32_t* s_bits) {
+  const int lane = threadIdx.x & 31;
+  const nbzg_field_meta* mp = &a.meta->f[field];
+  const uint16_t* codes = a.codes + field * a.code_stride;
+  uint8_t* payload = a.arena + mp->payload_off;
+  uint32_t* outw = reinterpret_cast<uint32_t*>(payload + mp->bits_off);
+  const int64_t c0 = c * kChunk;
+  const int mc = (int)min((int64_t)kChunk, a.n - c0);
+  const int lo = lane * kELane;
+  const int cnt = max(0, min(kELane, mc - lo));
+  const int cnt8 = cnt & ~7;  // full 8-code groups (codes are 16-byte aligned)
+  const uint16_t* cp = codes + c0 + lo;
+  const uint4* cp4 = reinterpret_cast<const uint4*>(cp);
+
+  // ---- 1. bits of this lane's codes
+  uint32_t bits = 0;
+  {
+    uint4 nxt = cnt8 ? __ldg(cp4) : make_uint4(0, 0, 0, 0);
+    for (int j = 0; j < cnt8; j += 8) {
+      const uint4 cur = nxt;
+      if (j + 8 < cnt8) nxt = __ldg(cp4 + (j >> 3) + 1);
+      uint32_t cv[8];
+      unpack8(cur, cv);
+#pragma unroll
+      for (int q = 0; q < 8; q++) bits += win_len(T, cv[q]) + (cv[q] == 0 ? 32u : 0u);
+    }
+    for (int j = cnt8; j < cnt; j++) {
+      const uint32_t code = cp[j];
+      bits += win_len(T, code) + (code == 0 ? 32u : 0u);
+    }
+  }
+  const uint32_t incl = warp_incl_scan<uint32_t>(bits);
+  const uint32_t off = incl - bits;
+  const uint32_t Tt = __shfl_sync(0xffffffffu, incl, 31);
+
+  // ---- 2. publish, look back for the chunk's global bit offset
+  uint64_t* lbb = a.lb + field * a.nchunks;
+  if (lane == 0 && c > 0) lb_store(&lbb[c], kFlagAgg | Tt);
+  const uint64_t B = lookback_sum(lbb, c, Tt);
+  if (lane == 0) put_u32_bytes(payload + mp->index_off + 4 * c, Tt);
+
+  // ---- 3. pack: 64-bit MSB-aligned accumulator, nacc < 32 between codes
+  const uint64_t g0 = B + off;
+  uint64_t widx = g0 >> 5;
+  uint64_t acc = 0;
+  uint32_t nacc = (uint32_t)(g0 & 31);
+  bool head_pending = nacc != 0;
+  long long head_idx = -1, tail_idx = -1;
+  uint32_t head_bits = 0, tail_bits = 0;
+  auto emit = [&](uint32_t w) {
+    if (head_pending) {
+      head_idx = (long long)widx;
+      head_bits = w;
+      head_pending = false;
+    } else {
+      outw[widx] = __byte_perm(w, 0, 0x0123);
+    }
+    widx++;
+  };
+  // slow append of up to 57 bits (long codes, escapes)
+  auto put_slow = [&](uint64_t v, uint32_t nb) {
+    Acc A{acc, (int)nacc};
+    acc_put(A, v, (int)nb, emit);
+    acc = A.acc;
+    nacc = (uint32_t)A.nacc;
+  };
+  auto put_code = [&](uint32_t code, int64_t pos) {
+    uint64_t w;
+    uint32_t l;
+    if (win_word(T, code, w, l)) {
+      acc |= w << (64 - nacc - l);
+      nacc += l;
+      if (nacc >= 32) {
+        emit((uint32_t)(acc >> 32));
+        acc <<= 32;
+        nacc -= 32;
+      }
+    } else {
+      put_slow(w, l);
+      if (code == 0) put_slow(esc_value_bits(a, field, pos), 32);
+    }
+  };
+  {
+    uint4 nxt = cnt8 ? __ldg(cp4) : make_uint4(0, 0, 0, 0);
+    for (int j = 0; j < cnt8; j += 8) {
+      const uint4 cur = nxt;
+      if (j + 8 < cnt8) nxt = __ldg(cp4 + (j >> 3) + 1);
+      uint32_t cv[8];
+      unpack8(cur, cv);
+#pragma unroll
+      for (int q = 0; q < 8; q++) put_code(cv[q], c0 + lo + j + q);
+    }
+    for (int j = cnt8; j < cnt; j++) put_code(cp[j], c0 + lo + j);
+  }
+  if (bits > 0 && nacc > 0) {
+    tail_idx = (long long)widx;
+    tail_bits = (uint32_t)(acc >> 32);
+  }
+  __syncwarp();
+  s_idx[2 * lane] = head_idx;
+  s_bits[2 * lane] = head_bits;
+  s_idx[2 * lane + 1] = tail_idx;
+  s_bits[2 * lane + 1] = tail_bits;
+  __syncwarp();
+
+  // ---- 4. merge boundary words (lane 0)
+  if (lane == 0 && Tt > 0) {
+    const uint64_t Bend = B + Tt;
+    const long long first_owned = (long long)((B + 31) >> 5);
+    const long long last_word = (long long)((Bend - 1) >> 5);
+    long long cur = -1;
+    uint32_t accw = 0;
+    auto flush = [&](long long idx, uint32_t w) {
+      if (idx < first_owned) return;  // belongs to the previous chunk
+      if (idx == last_word && (Bend & 31) && c + 1 < a.nchunks) {
+        const int need = 32 - (int)(Bend & 31);
+        w |= chunk_head_bits_w(a, field, codes, T, c + 1, need) >> (Bend & 31);
+      }
+      outw[idx] = __byte_perm(w, 0, 0x0123);
+    };
+    for (int s = 0; s < 64; s++) {
+      const long long idx = s_idx[s];
+      if (idx < 0) continue;
+      if (idx == cur) {
+        accw |= s_bits[s];
+      } else {
+        if (cur >= 0) flush(cur, accw);
+        cur = idx;
+        accw = s_bits[s];
+      }
+    }
+    if (cur >= 0) flush(cur, accw);
+  }
+}
+
+// payload path: persistent CTAs (one field each) stage the field's window
+// table in shared memory, then each warp encodes ticketed chunks until the
+// field is done
+constexpr int kEFWarps = 16;
+__global__ void __launch_bounds__(kEFWarps * 32, 2) encode_fast_kernel(EArgs a) {
   extern __shared__ __align__(16) uint8_t esm[];
-  uint16_t* s_rank = reinterpret_cast<uint16_t*>(esm);                 // [65536]
-  uint8_t* s_len = esm + 2 * kEncSyms;                                 // [65536]
-  uint64_t* s_fc = reinterpret_cast<uint64_t*>(esm + 3 * kEncSyms);    // [64]
-  long long* s_idx = reinterpret_cast<long long*>(s_fc + 64);          // [warps][64]
+  uint32_t* s_win = reinterpret_cast<uint32_t*>(esm);                 // [kEncWin]
+  long long* s_idx = reinterpret_cast<long long*>(s_win + kEncWin);  // [warps][64]
   uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_idx + kEFWarps * 64);
   const int field = blockIdx.y;
   if (a.meta->f[field].is_const || a.n == 0 || a.meta->status) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   {
-    const uint4* gr = reinterpret_cast<const uint4*>(a.trank + (size_t)field * a.nbins);
-    const uint4* gl = reinterpret_cast<const uint4*>(a.tlen + (size_t)field * a.nbins);
-    const int nr = (int)(a.nbins * 2 / 16), nl = (int)(a.nbins / 16);
-    for (int i = threadIdx.x; i < nr; i += blockDim.x) reinterpret_cast<uint4*>(s_rank)[i] = __ldg(gr + i);
-    for (int i = threadIdx.x; i < nl; i += blockDim.x) reinterpret_cast<uint4*>(s_len)[i] = __ldg(gl + i);
-    if (threadIdx.x < 64) s_fc[threadIdx.x] = a.tfc[field * 64 + threadIdx.x];
+    const uint4* g = reinterpret_cast<const uint4*>(a.twin + (size_t)field * kEncWin);
+    for (int i = threadIdx.x; i < kEncWin / 4; i += blockDim.x)
+      reinterpret_cast<uint4*>(s_win)[i] = __ldg(g + i);
   }
   __syncthreads();
-  CodeTab T{nullptr, s_len, s_rank, s_fc};
+  const WinTab T{s_win, (uint32_t)(a.nbins / 2 + 1 - kEncWin / 2), a.lut + field * a.nbins};
   while (true) {
     int64_t c = 0;
     if (lane == 0) c = atomicAdd(&a.tickets[field], 1u);
     c = __shfl_sync(0xffffffffu, c, 0);
     if (c >= a.nchunks) return;
-    encode_chunk<true>(a, field, c, T, s_idx + warp * 64, s_bits + warp * 64);
+    encode_chunk_fast(a, field, c, T, s_idx + warp * 64, s_bits + warp * 64);
   }
 }
 
@@ -396,20 +578,18 @@ int launch_encode(const Plan& p, cudaStream_t st) {
   a.lb = p.lb;
   a.tickets = p.counters;
   a.inline_esc = 1;
-  a.tlen = p.enc_len;
-  a.trank = p.enc_rank;
-  a.tfc = p.enc_fc;
+  a.twin = p.enc_win;
   cudaMemsetAsync(p.lb, 0, sizeof(uint64_t) * 6 * p.nchunks, st);
   cudaMemsetAsync(p.counters, 0, sizeof(uint32_t) * 8, st);
-  if (p.nbins == kEncSyms) {
-    const size_t sm = 3 * kEncSyms + 64 * 8 + kEFWarps * 64 * 12;
+  if (p.nbins == 65536) {
+    const size_t sm = 4 * kEncWin + kEFWarps * 64 * 12;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(encode_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sm);
       attr = true;
     }
-    int groups = max(1, sm_count() / 6);
+    int groups = max(1, 2 * sm_count() / 6);
     const int64_t need = (p.nchunks + kEFWarps - 1) / kEFWarps;
     if (groups > need) groups = (int)need;
     count_launch();

@@ -23,6 +23,7 @@ void trace_mark(const char* name, cudaStream_t st);
 
 constexpr int kTileMax = 16384;        // particles per tile / codes per chunk
 constexpr int kChunk = 16384;          // v2 chunk index granularity (symbols)
+constexpr int kEncWin = 16384;         // encoder smem code table: deltas in [-8192, 8191]
 constexpr int kMaxCodeLen = 57;        // encode.py:21
 constexpr int kHistWindow = 8192;      // smem histogram window (bins) in quantise
 constexpr double kIntLimit = 4611686018427387904.0;  // 2^62, quantize.py:29

@@ -33,9 +33,7 @@ struct Plan {
   uint32_t* cb_sym = nullptr;   // 6*nbins ascending symbols
   uint8_t* cb_len = nullptr;    // 6*nbins lengths by rank
   uint64_t* lut = nullptr;      // 6*nbins
-  uint8_t* enc_len = nullptr;   // 6*nbins code lengths (encoder smem table)
-  uint16_t* enc_rank = nullptr; // 6*nbins rank within the length class
-  uint64_t* enc_fc = nullptr;   // 6*64 first canonical code per length
+  uint32_t* enc_win = nullptr;  // 6*kEncWin (word << 6 | len) of codes near the centre
   uint32_t* cb_scratch = nullptr;  // 6 * 4*nbins u32 (sort + queues, large-k path)
   uint64_t* lb = nullptr;       // 6*nchunks*2 look-back words
   uint32_t* counters = nullptr; // 64 u32 (tickets, flags)

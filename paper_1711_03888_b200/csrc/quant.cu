@@ -77,6 +77,23 @@ NBZG_DEV int64_t dq_index(float x, const nbzg_field_meta& m, bool& fast) {
   return (int64_t)k;
 }
 
+// Same result as dq_index, FP32/int32 on the fast path: adding 1.5*2^23
+// rounds t to the nearest integer (ties to even, = rintf) for |t| < 2^22 and
+// leaves it in the low mantissa bits, so no conversion instructions are
+// needed; the FP64 slow path is taken only when the fast test fails.
+NBZG_DEV int64_t dq_index_fast(float x, float inv32, const nbzg_field_meta& m, bool& fast) {
+  const float t = x * inv32;
+  const float r = t + 12582912.0f;
+  const float kf = r - 12582912.0f;
+  const float d = fabsf(t - kf);
+  const float thr = fabsf(t) * 9.5367431640625e-07f + 9.5367431640625e-07f;
+  fast = (0.5f - d) > thr && fabsf(t) < 4194304.0f;
+  if (fast) return (int64_t)(__float_as_int(r) - 0x4B400000);
+  double k = rint(__dmul_rn((double)x, m.inv));
+  k = fmin(fmax(k, -kDqKmax), kDqKmax);
+  return (int64_t)k;
+}
+
 template <bool SORTED>
 __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -84,8 +101,7 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
   uint16_t* pbuf = reinterpret_cast<uint16_t*>(xbuf + 2 * kTileMax);  // [2][16384]
   uint32_t* hw = reinterpret_cast<uint32_t*>(pbuf + 2 * kTileMax);    // [kQWin]
   __shared__ __align__(8) uint64_t bar[2];
-  __shared__ int64_t s_klast[kQThreads / 32];
-  __shared__ int64_t s_carry;
+  __shared__ int64_t s_carry2[2];
   __shared__ uint32_t s_esc;
 
   const int field = blockIdx.x % 6;
@@ -100,6 +116,7 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
   const int half = a.half;
   const int wlo = half + 1 - kQWin / 2;
   const double b = fm.bound, twob = fm.twob;
+  const float inv32 = fm.inv32;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
   for (int i = tid; i < kQWin; i += kQThreads) hw[i] = 0;
@@ -113,7 +130,7 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
       bool fast;
       kc = dq_index(x[src], fm, fast);
     }
-    s_carry = kc;
+    s_carry2[0] = kc;
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -160,39 +177,46 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
     }
     __syncthreads();
 
-    // ---- per thread: positions p0 .. p0+15
-    const int p0 = tid * kQPer;
-    const int cnt = max(0, min(kQPer, m - p0));
-    // k of this thread's last element, exchanged to the right neighbour
-    int64_t klast = 0;
-    if (cnt > 0) {
-      int p = p0 + cnt - 1;
-      float xv = SORTED ? xs[min((int)ps[p], m - 1)] : xs[p];
-      bool fast;
-      klast = dq_index(xv, fm, fast);
-    }
-    int64_t kprev = __shfl_up_sync(0xffffffffu, klast, 1);
-    if (lane == 31) s_klast[wid] = klast;
-    __syncthreads();
-    if (lane == 0) kprev = wid == 0 ? s_carry : s_klast[wid - 1];
-    uint32_t packed[kQPer / 2];
-#pragma unroll
-    for (int j = 0; j < kQPer; j++) {
-      uint32_t code = 0;
-      if (j < cnt) {
-        int p = p0 + j;
-        float xv = SORTED ? xs[min((int)ps[p], m - 1)] : xs[p];
+    // ---- warp w owns positions [512 w, 512 w + 512); at step j lane l takes
+    // position 512 w + 32 j + l, so shared-memory reads and code stores are
+    // consecutive across the warp.  The predecessor's lattice index comes
+    // from lane l-1 (one rotate shuffle); lane 0 takes lane 31's from the
+    // previous step, and at j = 0 the last index of warp w-1 (recomputed) or
+    // of the previous tile (s_carry).
+    const int wbase = wid * (kQPer * 32);
+    const int cur = (int)((t - tb) & 1);
+    int64_t rot_prev = 0;
+    if (lane == 0) {
+      if (wbase == 0) {
+        rot_prev = s_carry2[cur];
+      } else if (wbase - 1 < m) {
+        const int p = wbase - 1;
+        const float xv = SORTED ? xs[min((int)ps[p], m - 1)] : xs[p];
         bool fast;
-        int64_t k = dq_index(xv, fm, fast);
-        if (((t0 + p) & (kChunk - 1)) == 0) kprev = 0;  // chain restarts every v2 chunk
-        int64_t q = k - kprev;
-        bool ok = q >= -half && q <= half - 2;
+        rot_prev = dq_index_fast(xv, inv32, fm, fast);
+      }
+    }
+    uint16_t* cdst = codes + t0;
+#pragma unroll 4
+    for (int j = 0; j < kQPer; j++) {
+      const int p = wbase + j * 32 + lane;
+      const bool valid = p < m;
+      float xv = 0.0f;
+      if (valid) xv = SORTED ? xs[min((int)ps[p], m - 1)] : xs[p];
+      bool fast;
+      const int64_t k = dq_index_fast(xv, inv32, fm, fast);
+      const int64_t kr = __shfl_sync(0xffffffffu, k, (lane + 31) & 31);
+      int64_t kp = lane == 0 ? rot_prev : kr;
+      rot_prev = kr;
+      if (((t0 + p) & (kChunk - 1)) == 0) kp = 0;  // chain restarts every v2 chunk
+      if (valid) {
+        const int64_t q = k - kp;
+        bool ok = (uint64_t)(q + half) <= (uint64_t)(2 * half - 2);
         if (ok && !fast) {
           float r = (float)__dmul_rn((double)k, twob);
           ok = fabs((double)xv - (double)r) <= b;
         }
-        code = ok ? (uint32_t)(q + half + 1) : 0u;
-        kprev = k;
+        const uint32_t code = ok ? (uint32_t)(q + half + 1) : 0u;
         if (code == 0) {
           atomicAdd(&s_esc, 1u);
         } else {
@@ -200,21 +224,10 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
           if ((unsigned)wb < (unsigned)kQWin) atomicAdd(&hw[wb], 1u);
           else atomicAdd(&hist[code], 1u);
         }
+        cdst[p] = (uint16_t)code;
+        if (p == m - 1) s_carry2[cur ^ 1] = k;  // carry for the next tile
       }
-      if (j & 1) packed[j >> 1] |= code << 16;
-      else packed[j >> 1] = code;
     }
-    // ---- store codes (16 x u16 per thread)
-    uint16_t* dst = codes + t0 + p0;
-    if (cnt == kQPer && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-      uint4* d4 = reinterpret_cast<uint4*>(dst);
-      d4[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-      d4[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
-    } else {
-      for (int j = 0; j < cnt; j++) dst[j] = (uint16_t)(packed[j >> 1] >> ((j & 1) * 16));
-    }
-    // carry for the next tile = k of position m-1
-    if (cnt > 0 && p0 + cnt == m) s_carry = kprev;
     __syncthreads();  // buffer `buf` fully consumed; s_carry visible
     if (a.use_tma && tid == 0 && t + 2 < te) {
       fence_proxy_async();
