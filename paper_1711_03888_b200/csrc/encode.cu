@@ -409,17 +409,31 @@ NBZG_DEV void encode_chunk_fast(const EArgs& a, int field, int64_t c, const WinT
   const uint16_t* cp = codes + c0 + lo;
   const uint4* cp4 = reinterpret_cast<const uint4*>(cp);
 
-  // ---- 1. bits of this lane's codes
+  // ---- 1. bits of this lane's codes (per 8-code group: window lookups,
+  // and the global LUT only for a group holding a miss)
   uint32_t bits = 0;
   {
     uint4 nxt = cnt8 ? __ldg(cp4) : make_uint4(0, 0, 0, 0);
     for (int j = 0; j < cnt8; j += 8) {
       const uint4 cur = nxt;
       if (j + 8 < cnt8) nxt = __ldg(cp4 + (j >> 3) + 1);
-      uint32_t cv[8];
+      uint32_t cv[8], e[8];
       unpack8(cur, cv);
+      bool hit = true;
+      uint32_t gb = 0;
 #pragma unroll
-      for (int q = 0; q < 8; q++) bits += win_len(T, cv[q]) + (cv[q] == 0 ? 32u : 0u);
+      for (int q = 0; q < 8; q++) {
+        const uint32_t wi = cv[q] - T.wlo;
+        e[q] = wi < (uint32_t)kEncWin ? T.win[wi] : 0u;
+        hit &= e[q] != 0;
+        gb += e[q] & 63u;
+      }
+      if (!hit) {
+        gb = 0;
+#pragma unroll
+        for (int q = 0; q < 8; q++) gb += win_len(T, cv[q]) + (cv[q] == 0 ? 32u : 0u);
+      }
+      bits += gb;
     }
     for (int j = cnt8; j < cnt; j++) {
       const uint32_t code = cp[j];
@@ -436,23 +450,35 @@ NBZG_DEV void encode_chunk_fast(const EArgs& a, int field, int64_t c, const WinT
   const uint64_t B = lookback_sum(lbb, c, Tt);
   if (lane == 0) put_u32_bytes(payload + mp->index_off + 4 * c, Tt);
 
-  // ---- 3. pack: 64-bit MSB-aligned accumulator, nacc < 32 between codes
+  // ---- 3. pack: 64-bit MSB-aligned accumulator, nacc < 32 between codes.
+  // The lane's first word is partial when it starts mid-word: it goes to
+  // the warp's merge slots instead of memory (predicated, no branch).
   const uint64_t g0 = B + off;
   uint64_t widx = g0 >> 5;
+  const uint64_t widx0 = widx;
   uint64_t acc = 0;
   uint32_t nacc = (uint32_t)(g0 & 31);
-  bool head_pending = nacc != 0;
+  const bool head_partial = nacc != 0;
   long long head_idx = -1, tail_idx = -1;
   uint32_t head_bits = 0, tail_bits = 0;
   auto emit = [&](uint32_t w) {
-    if (head_pending) {
+    const bool head = head_partial && widx == widx0;
+    if (head) {
       head_idx = (long long)widx;
       head_bits = w;
-      head_pending = false;
     } else {
       outw[widx] = __byte_perm(w, 0, 0x0123);
     }
     widx++;
+  };
+  auto append = [&](uint32_t w, uint32_t l) {  // l <= 26
+    acc |= (uint64_t)w << (64 - nacc - l);
+    nacc += l;
+    if (nacc >= 32) {
+      emit((uint32_t)(acc >> 32));
+      acc <<= 32;
+      nacc -= 32;
+    }
   };
   // slow append of up to 57 bits (long codes, escapes)
   auto put_slow = [&](uint64_t v, uint32_t nb) {
@@ -464,28 +490,31 @@ NBZG_DEV void encode_chunk_fast(const EArgs& a, int field, int64_t c, const WinT
   auto put_code = [&](uint32_t code, int64_t pos) {
     uint64_t w;
     uint32_t l;
-    if (win_word(T, code, w, l)) {
-      acc |= w << (64 - nacc - l);
-      nacc += l;
-      if (nacc >= 32) {
-        emit((uint32_t)(acc >> 32));
-        acc <<= 32;
-        nacc -= 32;
-      }
-    } else {
-      put_slow(w, l);
-      if (code == 0) put_slow(esc_value_bits(a, field, pos), 32);
-    }
+    win_word(T, code, w, l);
+    put_slow(w, l);
+    if (code == 0) put_slow(esc_value_bits(a, field, pos), 32);
   };
   {
     uint4 nxt = cnt8 ? __ldg(cp4) : make_uint4(0, 0, 0, 0);
     for (int j = 0; j < cnt8; j += 8) {
       const uint4 cur = nxt;
       if (j + 8 < cnt8) nxt = __ldg(cp4 + (j >> 3) + 1);
-      uint32_t cv[8];
+      uint32_t cv[8], e[8];
       unpack8(cur, cv);
+      bool hit = true;
 #pragma unroll
-      for (int q = 0; q < 8; q++) put_code(cv[q], c0 + lo + j + q);
+      for (int q = 0; q < 8; q++) {
+        const uint32_t wi = cv[q] - T.wlo;
+        e[q] = wi < (uint32_t)kEncWin ? T.win[wi] : 0u;
+        hit &= e[q] != 0;
+      }
+      if (hit) {
+#pragma unroll
+        for (int q = 0; q < 8; q++) append(e[q] >> 6, e[q] & 63u);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; q++) put_code(cv[q], c0 + lo + j + q);
+      }
     }
     for (int j = cnt8; j < cnt; j++) put_code(cp[j], c0 + lo + j);
   }
