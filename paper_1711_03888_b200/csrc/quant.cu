@@ -197,35 +197,56 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
       }
     }
     uint16_t* cdst = codes + t0;
+    const int pr = (int)((-t0) & (kChunk - 1));  // position of a chunk start in this tile
 #pragma unroll 4
     for (int j = 0; j < kQPer; j++) {
       const int p = wbase + j * 32 + lane;
       const bool valid = p < m;
       float xv = 0.0f;
       if (valid) xv = SORTED ? xs[min((int)ps[p], m - 1)] : xs[p];
-      bool fast;
-      const int64_t k = dq_index_fast(xv, inv32, fm, fast);
-      const int64_t kr = __shfl_sync(0xffffffffu, k, (lane + 31) & 31);
-      int64_t kp = lane == 0 ? rot_prev : kr;
-      rot_prev = kr;
-      if (((t0 + p) & (kChunk - 1)) == 0) kp = 0;  // chain restarts every v2 chunk
-      if (valid) {
+      // FP32 fast lattice index (see dq_index_fast)
+      const float tq = xv * inv32;
+      const float rq = tq + 12582912.0f;
+      const float kf = rq - 12582912.0f;
+      const float thr = fabsf(tq) * 9.5367431640625e-07f + 9.5367431640625e-07f;
+      const bool fast = (0.5f - fabsf(tq - kf)) > thr && fabsf(tq) < 4194304.0f;
+      uint32_t code;
+      if (__all_sync(0xffffffffu, fast)) {
+        // common case: every |k| < 2^22, 32-bit chain
+        const int32_t k = __float_as_int(rq) - 0x4B400000;
+        const int32_t kr = __shfl_sync(0xffffffffu, k, (lane + 31) & 31);
+        // lane 0's predecessor may be a clamped 64-bit index: 64-bit difference
+        int64_t kp = lane == 0 ? rot_prev : (int64_t)kr;
+        rot_prev = kr;
+        if (p == pr) kp = 0;  // chain restarts every v2 chunk
+        const int64_t q = (int64_t)k - kp;
+        code = (uint64_t)(q + half) <= (uint64_t)(2 * half - 2) ? (uint32_t)(q + half + 1) : 0u;
+        if (valid && p == m - 1) s_carry2[cur ^ 1] = k;  // carry for the next tile
+      } else {
+        bool fast2;
+        const int64_t k = dq_index_fast(xv, inv32, fm, fast2);
+        const int64_t kr = __shfl_sync(0xffffffffu, k, (lane + 31) & 31);
+        int64_t kp = lane == 0 ? rot_prev : kr;
+        rot_prev = kr;
+        if (p == pr) kp = 0;
         const int64_t q = k - kp;
         bool ok = (uint64_t)(q + half) <= (uint64_t)(2 * half - 2);
-        if (ok && !fast) {
+        if (ok && !fast2) {
           float r = (float)__dmul_rn((double)k, twob);
           ok = fabs((double)xv - (double)r) <= b;
         }
-        const uint32_t code = ok ? (uint32_t)(q + half + 1) : 0u;
+        code = ok ? (uint32_t)(q + half + 1) : 0u;
+        if (valid && p == m - 1) s_carry2[cur ^ 1] = k;
+      }
+      if (valid) {
         if (code == 0) {
           atomicAdd(&s_esc, 1u);
         } else {
-          int wb = (int)code - wlo;
+          const int wb = (int)code - wlo;
           if ((unsigned)wb < (unsigned)kQWin) atomicAdd(&hw[wb], 1u);
           else atomicAdd(&hist[code], 1u);
         }
         cdst[p] = (uint16_t)code;
-        if (p == m - 1) s_carry2[cur ^ 1] = k;  // carry for the next tile
       }
     }
     __syncthreads();  // buffer `buf` fully consumed; s_carry visible
