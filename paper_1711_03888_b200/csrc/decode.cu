@@ -716,17 +716,17 @@ NBZG_DEV void tpc_init(TpcReader& R, const uint4* G, uint32_t* ring, int nthr, u
   const uint32_t blk = gw0 >> 2;
   const uint4 A = __ldg(G + min(blk, vmax)), B = __ldg(G + min(blk + 1, vmax));
   const uint32_t s0 = (4 * blk) & 7, s1 = s0 ^ 4;  // word 4 blk + i -> slot (4 blk + i) & 7
-  ring[(s0 + 0) * nthr] = A.x;
-  ring[(s0 + 1) * nthr] = A.y;
-  ring[(s0 + 2) * nthr] = A.z;
-  ring[(s0 + 3) * nthr] = A.w;
-  ring[(s1 + 0) * nthr] = B.x;
-  ring[(s1 + 1) * nthr] = B.y;
-  ring[(s1 + 2) * nthr] = B.z;
-  ring[(s1 + 3) * nthr] = B.w;
+  ring[(s0 + 0) * nthr] = bswap32(A.x);  // words stored byte-swapped
+  ring[(s0 + 1) * nthr] = bswap32(A.y);
+  ring[(s0 + 2) * nthr] = bswap32(A.z);
+  ring[(s0 + 3) * nthr] = bswap32(A.w);
+  ring[(s1 + 0) * nthr] = bswap32(B.x);
+  ring[(s1 + 1) * nthr] = bswap32(B.y);
+  ring[(s1 + 2) * nthr] = bswap32(B.z);
+  ring[(s1 + 3) * nthr] = bswap32(B.w);
   R.off = (uint32_t)(bitpos & 31);
-  R.w0 = bswap32(ring[(gw0 & 7) * nthr]);
-  R.w1 = bswap32(ring[((gw0 + 1) & 7) * nthr]);
+  R.w0 = ring[(gw0 & 7) * nthr];
+  R.w1 = ring[((gw0 + 1) & 7) * nthr];
   R.wi = gw0 + 1;
   R.wr = 4 * (blk + 2);
   R.qs = make_uint4(0, 0, 0, 0);
@@ -743,9 +743,10 @@ NBZG_DEV void tpc_skip(TpcReader& R, uint32_t l, const uint32_t* ring, int nthr,
   const bool cross = R.off >= 32;
   if (cross && (int32_t)(R.wr - (R.wi + 1)) <= 0) {  // outran the ring (rare)
     asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(nw) : "l"(G32 + min(R.wi + 1, wmax)));
+    nw = bswap32(nw);
   }
   R.w0 = cross ? R.w1 : R.w0;
-  R.w1 = cross ? bswap32(nw) : R.w1;
+  R.w1 = cross ? nw : R.w1;
   R.wi += cross ? 1u : 0u;
   R.off -= cross ? 32u : 0u;
 }
@@ -757,10 +758,10 @@ NBZG_DEV void tpc_refill(TpcReader& R, uint32_t* ring, int nthr, const uint4* G,
   const bool room = (int32_t)(R.wr - R.wi) <= 5;
   if (room) {
     const uint32_t s = R.wr & 7;  // 0 or 4
-    ring[(s + 0) * nthr] = R.qs.x;
-    ring[(s + 1) * nthr] = R.qs.y;
-    ring[(s + 2) * nthr] = R.qs.z;
-    ring[(s + 3) * nthr] = R.qs.w;
+    ring[(s + 0) * nthr] = bswap32(R.qs.x);
+    ring[(s + 1) * nthr] = bswap32(R.qs.y);
+    ring[(s + 2) * nthr] = bswap32(R.qs.z);
+    ring[(s + 3) * nthr] = bswap32(R.qs.w);
     R.wr += 4;
   }
   ldg_v4_if(R.qs, G + min(R.wr >> 2, vmax), room);
@@ -871,7 +872,6 @@ __global__ void __launch_bounds__(1024, 1) decode_tpc_kernel(DArgs a, int ctas_p
     // common step: table hit (primary or secondary), no escape; the window
     // advances from the ring speculatively and `under` records a lane that
     // needed a word the ring did not hold yet (the group is then replayed)
-    bool under = false;
     auto fast_step = [&](float& o) {
       const uint32_t v = __funnelshift_l(R.w1, R.w0, R.off);
       const uint32_t nw = tpc_next(R, ring, nthr);
@@ -887,9 +887,8 @@ __global__ void __launch_bounds__(1024, 1) decode_tpc_kernel(DArgs a, int ctas_p
       o = (float)__dmul_rn(kd, twob);
       R.off += (uint32_t)e & 63u;
       const bool cross = R.off >= 32;
-      under |= cross && (int32_t)(R.wr - R.wi) <= 1;
       R.w0 = cross ? R.w1 : R.w0;
-      R.w1 = cross ? bswap32(nw) : R.w1;
+      R.w1 = cross ? nw : R.w1;
       R.wi += cross ? 1u : 0u;
       R.off -= cross ? 32u : 0u;
     };
@@ -897,10 +896,10 @@ __global__ void __launch_bounds__(1024, 1) decode_tpc_kernel(DArgs a, int ctas_p
     auto group = [&](float (&o)[8]) {
       const TpcReader S = R;
       const double kd0 = kd;
-      under = false;
 #pragma unroll
       for (int q = 0; q < 8; q++) fast_step(o[q]);
-      if (under) {
+      // the largest word index read in the group is the final wi
+      if ((int32_t)(R.wr - R.wi) <= 0) {
         R = S;
         kd = kd0;
 #pragma unroll 1

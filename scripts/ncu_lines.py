@@ -6,6 +6,8 @@ from the in-tree libnbzg.so (must be the build that was profiled).
 import collections, csv, glob, io, os, re, subprocess, sys, tempfile
 
 rep, kern = sys.argv[1], sys.argv[2]
+# "NCU_REGEX@MANGLED_SUBSTR" when the demangled and mangled names differ
+ncu_k, kern = (kern.split("@", 1) if "@" in kern else (kern, kern))
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
 lib = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1711_03888_b200",
                    "libnbzg.so")
@@ -29,12 +31,18 @@ for cub in glob.glob(os.path.join(tmp, "*.cubin")):
         m = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s+(.*?);", l)
         if m and fn:
             sass[fn].append((cur, m.group(2)))
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", "regex:" + kern, "-c",
-                      "1"], capture_output=True, text=True).stdout
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name-base",
+                      "mangled", "-k", "regex:" + ncu_k, "-c", "1"],
+                     capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
 ix = {h: i for i, h in enumerate(hdr)}
-data = [r for r in rows[2:] if len(r) == len(hdr)]
+data = []
+for r in rows[2:]:
+    if r and r[0] == "Kernel Name":
+        break  # next profiled kernel
+    if len(r) == len(hdr):
+        data.append(r)
 cands = [f for f in sass if kern in f and len(sass[f]) == len(data)]
 if not cands:
     sys.exit(f"no SASS function matching {kern} with {len(data)} instructions: " +
