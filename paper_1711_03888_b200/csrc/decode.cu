@@ -35,7 +35,8 @@ constexpr int kDThreads = kDWarps * 32;
 constexpr int kLutBits = 16;       // code-length table index bits (u8 entries, 64 KiB)
 constexpr int kSmemSyms = 16384;   // sorted-symbol table staged in smem up to this k
 constexpr int kTpcBits = 15;       // thread-per-chunk fused table index bits (i32, 128 KiB)
-constexpr int kTpc2Cap = 12288;    // secondary (long-code) table entries (48 KiB)
+constexpr int kTpc2Cap = 19456;    // secondary (long-code) table entries (76 KiB)
+constexpr int kTpcMaxThreads = 704;  // smem: 128 KiB + 76 KiB tables + 32 B ring per thread
 constexpr int kTpcTab = (1 << kTpcBits) + kTpc2Cap;
 
 struct DParsed {
@@ -767,7 +768,7 @@ NBZG_DEV void tpc_refill(TpcReader& R, uint32_t* ring, int nthr, const uint4* G,
   ldg_v4_if(R.qs, G + min(R.wr >> 2, vmax), room);
 }
 
-__global__ void __launch_bounds__(1024, 1) decode_tpc_kernel(DArgs a, int ctas_per_field) {
+__global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, int ctas_per_field) {
   extern __shared__ __align__(16) uint8_t dsm2[];
   int32_t* LT = reinterpret_cast<int32_t*>(dsm2);  // [2^15 + t2_n]
   __shared__ uint64_t s_limit[64];
@@ -1107,7 +1108,7 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
     if (groups > a.nchunks) groups = (int)a.nchunks;
     if (use_tpc(a.nchunks)) {
       const int per = (int)((a.nchunks + groups - 1) / groups);
-      const int thr = min(1024, (per + 31) / 32 * 32);
+      const int thr = min(kTpcMaxThreads, (per + 31) / 32 * 32);
       const size_t sm2 = 4 * kTpcTab + 32 * (size_t)thr;
       static bool attr2 = false;
       if (!attr2) {
