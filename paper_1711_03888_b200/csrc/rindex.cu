@@ -160,12 +160,28 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
       mn[c] = __int_as_float(0x7f800000);
       mx[c] = -__int_as_float(0x7f800000);
     }
-    for (int i = threadIdx.x; i < m; i += kSortThreads) {
+    {
+      // float4 loads, 4 x 3 in flight per thread (segments start 16-byte aligned)
+      const int m4 = (s0 & 3) ? 0 : m >> 2;  // float4 path needs 16-byte aligned segments
+      const float4* x4[3] = {reinterpret_cast<const float4*>(a.x[0] + s0),
+                             reinterpret_cast<const float4*>(a.x[1] + s0),
+                             reinterpret_cast<const float4*>(a.x[2] + s0)};
+#pragma unroll 4
+      for (int v = threadIdx.x; v < m4; v += kSortThreads) {
 #pragma unroll
-      for (int c = 0; c < 3; c++) {
-        float v = a.x[c][s0 + i];
-        mn[c] = fminf(mn[c], v);
-        mx[c] = fmaxf(mx[c], v);
+        for (int c = 0; c < 3; c++) {
+          const float4 q = __ldg(x4[c] + v);
+          mn[c] = fminf(mn[c], fminf(fminf(q.x, q.y), fminf(q.z, q.w)));
+          mx[c] = fmaxf(mx[c], fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
+        }
+      }
+      for (int i = 4 * m4 + threadIdx.x; i < m; i += kSortThreads) {
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+          const float v = a.x[c][s0 + i];
+          mn[c] = fminf(mn[c], v);
+          mx[c] = fmaxf(mx[c], v);
+        }
       }
     }
 #pragma unroll
@@ -223,16 +239,32 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
       // ---- 2. masked keys
       const int shift = sp.shift;
       const int64_t m0 = sp.mn[0], m1 = sp.mn[1], m2 = sp.mn[2];
-      for (int i = threadIdx.x; i < m; i += kSortThreads) {
+      auto key_of = [&](float x0, float x1, float x2) -> KeyT {
+        const float xv[3] = {x0, x1, x2};
         uint64_t u[3];
 #pragma unroll
         for (int c = 0; c < 3; c++) {
-          int64_t iv = fm[c].is_const ? 0 : integerize1(a.x[c][s0 + i], fm[c]);
+          int64_t iv = fm[c].is_const ? 0 : integerize1(xv[c], fm[c]);
           int64_t mm = c == 0 ? m0 : (c == 1 ? m1 : m2);
           u[c] = (uint64_t)(iv - mm) >> shift;
         }
-        keys[lo + i] = make_key<KeyT>(u[0], u[1], u[2]);
+        return make_key<KeyT>(u[0], u[1], u[2]);
+      };
+      const int m4 = (s0 & 3) ? 0 : m >> 2;  // float4 path needs 16-byte aligned segments
+      const float4* x4[3] = {reinterpret_cast<const float4*>(a.x[0] + s0),
+                             reinterpret_cast<const float4*>(a.x[1] + s0),
+                             reinterpret_cast<const float4*>(a.x[2] + s0)};
+#pragma unroll 2
+      for (int v = threadIdx.x; v < m4; v += kSortThreads) {
+        const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
+        KeyT* kd = keys + lo + 4 * v;
+        kd[0] = key_of(q0.x, q1.x, q2.x);
+        kd[1] = key_of(q0.y, q1.y, q2.y);
+        kd[2] = key_of(q0.z, q1.z, q2.z);
+        kd[3] = key_of(q0.w, q1.w, q2.w);
       }
+      for (int i = 4 * m4 + threadIdx.x; i < m; i += kSortThreads)
+        keys[lo + i] = key_of(a.x[0][s0 + i], a.x[1][s0 + i], a.x[2][s0 + i]);
       __syncthreads();
       // ---- 3. stable radix sort over 3w bits
       block_sort_range<KeyT>(keys, perm, lo, m, 3 * w, whist, scan_tmp);
