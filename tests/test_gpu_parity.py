@@ -394,3 +394,31 @@ def test_config_scale_parity(O, spec, mode, decoder):
         assert torch.equal(got.cpu(), torch.from_numpy(odec[fi])), fi
         err = (torch.from_numpy(work[fi]).cuda().double() - got.double()).abs().max()
         assert float(err) <= res.archive.bounds[fi]
+
+
+# ---------------------------------------------------------------- settings
+
+@pytest.mark.parametrize("seg,ig,ic", [(1000, 6, 65536), (4099, 2, 65536), (16384, 0, 65536),
+                                       (16384, 6, 1024), (777, 3, 4096), (16384, 6, 2)])
+def test_settings_variants_byte_identical(O, seg, ig, ic, decoder):
+    """Non-default Settings (segment size not a multiple of 4, ignored
+    groups, small interval counts -> generic encoder path, heavy escapes):
+    archives byte-identical to the oracle, decode exact and within bound."""
+    fields = datagen.small_hacc(30)
+    snap = nbz.ParticleSnapshot(*fields)
+    settings = nbz.Settings(interval_count=ic, segment_size=seg, ignored_groups=ig)
+    for mode in ("sz-lv", "sz-lv-prx"):
+        res = nbz.compress(snap, mode, REL4, settings)
+        ref = O.compress(fields, mode, "rel", 1e-4, interval_count=ic, segment_size=seg,
+                         ignored_groups=ig, fmt=2)
+        assert res.archive.serialized() == ref["wire"], (mode, seg, ig, ic)
+        if res.order is not None:
+            assert np.array_equal(res.order, ref["order"])
+        rec = nbz.decompress(res.archive)
+        odec = O.decompress(ref["wire"])
+        work = fields if res.order is None else [f[res.order] for f in fields]
+        for fi in range(6):
+            got = np.asarray(rec.field(fi))
+            assert np.array_equal(got, odec[fi]), (mode, fi)
+            err = np.abs(work[fi].astype(np.float64) - got.astype(np.float64))
+            assert float(err.max()) <= res.archive.bounds[fi]
