@@ -321,11 +321,31 @@ def device_fields(snapshot: ParticleSnapshot):
     return out, buf
 
 
+AUTO = "auto"
+
+
 def compress(snapshot: ParticleSnapshot, mode, bounds: Bounds,
              settings: Settings = DEFAULT_SETTINGS) -> CompressResult:
     """pipeline.py:447-526 on the B200: SZ-LV (R-index off) and SZ-LV-PRX
-    (R-index on)."""
+    (R-index on).
+
+    ``mode="auto"`` (not in the reference, which has no
+    selector): compress with both modes and keep the smaller archive.  The
+    result is an ordinary mode-1 or mode-2 archive, decodable by any reader;
+    the choice is snapshot-level because all six fields share one
+    permutation (a per-field choice would need the permutation stored)."""
     import torch
+    if isinstance(mode, str) and mode == AUTO:
+        fields, hold = device_fields(snapshot)  # one H2D for both attempts
+        dsnap = ParticleSnapshot.__new__(ParticleSnapshot)
+        for name, f in zip(FIELD_NAMES, fields):
+            object.__setattr__(dsnap, name, f)
+        a = compress(dsnap, Mode.SZ_LV, bounds, settings)
+        b = compress(dsnap, Mode.SZ_LV_PRX, bounds, settings)
+        best = b if b.archive.total_bytes() < a.archive.total_bytes() else a
+        best.archive.device_output = bool(snapshot.on_device)
+        del hold
+        return best
     mode = _as_mode(mode)
     if mode not in GPU_MODES:
         raise ValidationError(f"mode {mode.value} is not implemented by the B200 path "

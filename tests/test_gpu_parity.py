@@ -422,3 +422,19 @@ def test_settings_variants_byte_identical(O, seg, ig, ic, decoder):
             assert np.array_equal(got, odec[fi]), (mode, fi)
             err = np.abs(work[fi].astype(np.float64) - got.astype(np.float64))
             assert float(err.max()) <= res.archive.bounds[fi]
+
+
+@pytest.mark.parametrize("gen", ["hacc", "amdf"])
+def test_auto_mode_keeps_smaller_archive(O, gen):
+    """a13: snapshot-level auto policy = the smaller of sz-lv / sz-lv-prx."""
+    fields = datagen.small_hacc(32) if gen == "hacc" else datagen.small_amdf(40000)
+    snap = nbz.ParticleSnapshot(*fields)
+    a = nbz.compress(snap, "sz-lv", REL4).archive.serialized()
+    b = nbz.compress(snap, "sz-lv-prx", REL4).archive.serialized()
+    res = nbz.compress(snap, "auto", REL4)
+    wire = res.archive.serialized()
+    assert wire == (b if len(b) < len(a) else a)
+    assert res.archive.mode.value in ("sz-lv", "sz-lv-prx")
+    assert (res.order is not None) == (res.archive.mode.value == "sz-lv-prx")
+    rec = nbz.decompress(res.archive)
+    assert np.array_equal(np.asarray(rec.xx), O.decompress(wire)[0])
