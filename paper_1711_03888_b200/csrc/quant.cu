@@ -102,7 +102,6 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
   uint32_t* hw = reinterpret_cast<uint32_t*>(pbuf + 2 * kTileMax);    // [kQWin]
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ int64_t s_carry2[2];
-  __shared__ uint32_t s_esc;
 
   const int field = blockIdx.x % 6;
   const int g = blockIdx.x / 6;
@@ -121,7 +120,6 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
 
   for (int i = tid; i < kQWin; i += kQThreads) hw[i] = 0;
   if (tid == 0) {
-    s_esc = 0;
     // k carried into the range: k of the last sorted element of tile tb-1
     int64_t kc = 0;
     if (tb > 0) {
@@ -196,10 +194,10 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
         rot_prev = dq_index_fast(xv, inv32, fm, fast);
       }
     }
-    uint16_t* cdst = codes + t0;
     const int pr = (int)((-t0) & (kChunk - 1));  // position of a chunk start in this tile
+    uint16_t* cdst = codes + t0 + wbase + lane;   // advances 32 codes per step
 #pragma unroll 4
-    for (int j = 0; j < kQPer; j++) {
+    for (int j = 0; j < kQPer; j++, cdst += 32) {
       const int p = wbase + j * 32 + lane;
       const bool valid = p < m;
       float xv = 0.0f;
@@ -208,19 +206,21 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
       const float tq = xv * inv32;
       const float rq = tq + 12582912.0f;
       const float kf = rq - 12582912.0f;
-      const float thr = fabsf(tq) * 9.5367431640625e-07f + 9.5367431640625e-07f;
+      const float thr = __fmaf_rn(fabsf(tq), 9.5367431640625e-07f, 9.5367431640625e-07f);
       const bool fast = (0.5f - fabsf(tq - kf)) > thr && fabsf(tq) < 4194304.0f;
       uint32_t code;
       if (__all_sync(0xffffffffu, fast)) {
-        // common case: every |k| < 2^22, 32-bit chain
+        // common case: every |k| < 2^22.  32-bit chain: lane 0's predecessor
+        // is clamped to +-2^30, which keeps any out-of-range q out of range
+        // (|q| > half either way), so the escape decision is unchanged
         const int32_t k = __float_as_int(rq) - 0x4B400000;
         const int32_t kr = __shfl_sync(0xffffffffu, k, (lane + 31) & 31);
-        // lane 0's predecessor may be a clamped 64-bit index: 64-bit difference
-        int64_t kp = lane == 0 ? rot_prev : (int64_t)kr;
+        const int32_t kc = (int32_t)max(min(rot_prev, (int64_t)(1 << 30)), -(int64_t)(1 << 30));
+        int32_t kp = lane == 0 ? kc : kr;
         rot_prev = kr;
         if (p == pr) kp = 0;  // chain restarts every v2 chunk
-        const int64_t q = (int64_t)k - kp;
-        code = (uint64_t)(q + half) <= (uint64_t)(2 * half - 2) ? (uint32_t)(q + half + 1) : 0u;
+        const int32_t q = k - kp;
+        code = (uint32_t)(q + half) <= (uint32_t)(2 * half - 2) ? (uint32_t)(q + half + 1) : 0u;
         if (valid && p == m - 1) s_carry2[cur ^ 1] = k;  // carry for the next tile
       } else {
         bool fast2;
@@ -239,14 +239,12 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
         if (valid && p == m - 1) s_carry2[cur ^ 1] = k;
       }
       if (valid) {
-        if (code == 0) {
-          atomicAdd(&s_esc, 1u);
-        } else {
-          const int wb = (int)code - wlo;
-          if ((unsigned)wb < (unsigned)kQWin) atomicAdd(&hw[wb], 1u);
-          else atomicAdd(&hist[code], 1u);
-        }
-        cdst[p] = (uint16_t)code;
+        // histogram: smem window around the centre; escapes (code 0) and
+        // far codes go straight to global memory
+        const uint32_t wb = code - (uint32_t)wlo;
+        if (wb < (uint32_t)kQWin) atomicAdd(&hw[wb], 1u);
+        else atomicAdd(&hist[code], 1u);
+        *cdst = (uint16_t)code;
       }
     }
     __syncthreads();  // buffer `buf` fully consumed; s_carry visible
@@ -259,9 +257,8 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
   for (int i = tid; i < kQWin; i += kQThreads) {
     uint32_t c = hw[i];
     int code = wlo + i;
-    if (c && code >= 1 && code < (int)a.nbins) atomicAdd(&hist[code], c);
+    if (c && code >= 0 && code < (int)a.nbins) atomicAdd(&hist[code], c);
   }
-  if (tid == 0 && s_esc) atomicAdd(&hist[0], s_esc);
 }
 
 int launch_quantize(const Plan& p, cudaStream_t st) {
