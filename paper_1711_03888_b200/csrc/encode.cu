@@ -395,7 +395,7 @@ NBZG_DEV void unpack8(uint4 u, uint32_t (&cv)[8]) {
 }
 
 NBZG_DEV void encode_chunk_fast(const EArgs& a, int field, int64_t c, const WinTab& T,
-                                long long* s_idx, uint32_t* s_bits) {
+                                long long* s_idx, uint32_t* s_bits, uint32_t* s_headw) {
   const int lane = threadIdx.x & 31;
   const nbzg_field_meta* mp = &a.meta->f[field];
   const uint16_t* codes = a.codes + field * a.code_stride;
@@ -412,11 +412,16 @@ NBZG_DEV void encode_chunk_fast(const EArgs& a, int field, int64_t c, const WinT
   // ---- 1. bits of this lane's codes (per 8-code group: window lookups,
   // and the global LUT only for a group holding a miss)
   uint32_t bits = 0;
+  const int ng = cnt8 >> 3;  // 8-code groups; loads run 3 groups ahead
   {
-    uint4 nxt = cnt8 ? __ldg(cp4) : make_uint4(0, 0, 0, 0);
+    uint4 n0 = ng > 0 ? __ldg(cp4) : make_uint4(0, 0, 0, 0);
+    uint4 n1 = ng > 1 ? __ldg(cp4 + 1) : make_uint4(0, 0, 0, 0);
+    uint4 n2 = ng > 2 ? __ldg(cp4 + 2) : make_uint4(0, 0, 0, 0);
     for (int j = 0; j < cnt8; j += 8) {
-      const uint4 cur = nxt;
-      if (j + 8 < cnt8) nxt = __ldg(cp4 + (j >> 3) + 1);
+      const uint4 cur = n0;
+      n0 = n1;
+      n1 = n2;
+      if ((j >> 3) + 3 < ng) n2 = __ldg(cp4 + (j >> 3) + 3);
       uint32_t cv[8], e[8];
       unpack8(cur, cv);
       bool hit = true;
@@ -451,25 +456,22 @@ NBZG_DEV void encode_chunk_fast(const EArgs& a, int field, int64_t c, const WinT
   if (lane == 0) put_u32_bytes(payload + mp->index_off + 4 * c, Tt);
 
   // ---- 3. pack: 64-bit MSB-aligned accumulator, nacc < 32 between codes.
-  // The lane's first word is partial when it starts mid-word: it goes to
-  // the warp's merge slots instead of memory (predicated, no branch).
+  // Completed words go to consecutive addresses through a running pointer;
+  // a lane starting mid-word sends its first (partial) word to a shared
+  // slot instead (it is OR-merged with the neighbour's bits in step 4).
   const uint64_t g0 = B + off;
-  uint64_t widx = g0 >> 5;
-  const uint64_t widx0 = widx;
+  const uint64_t widx0 = g0 >> 5;
   uint64_t acc = 0;
   uint32_t nacc = (uint32_t)(g0 & 31);
   const bool head_partial = nacc != 0;
-  long long head_idx = -1, tail_idx = -1;
-  uint32_t head_bits = 0, tail_bits = 0;
+  uint32_t* wp = head_partial ? s_headw + lane : outw + widx0;  // generic pointer
+  uint32_t* wn = outw + widx0 + 1;
+  uint32_t nemit = 0;
   auto emit = [&](uint32_t w) {
-    const bool head = head_partial && widx == widx0;
-    if (head) {
-      head_idx = (long long)widx;
-      head_bits = w;
-    } else {
-      outw[widx] = __byte_perm(w, 0, 0x0123);
-    }
-    widx++;
+    *wp = __byte_perm(w, 0, 0x0123);
+    wp = wn;
+    wn++;
+    nemit++;
   };
   auto append = [&](uint32_t w, uint32_t l) {  // l <= 26
     acc |= (uint64_t)w << (64 - nacc - l);
@@ -495,10 +497,14 @@ NBZG_DEV void encode_chunk_fast(const EArgs& a, int field, int64_t c, const WinT
     if (code == 0) put_slow(esc_value_bits(a, field, pos), 32);
   };
   {
-    uint4 nxt = cnt8 ? __ldg(cp4) : make_uint4(0, 0, 0, 0);
+    uint4 n0 = ng > 0 ? __ldg(cp4) : make_uint4(0, 0, 0, 0);
+    uint4 n1 = ng > 1 ? __ldg(cp4 + 1) : make_uint4(0, 0, 0, 0);
+    uint4 n2 = ng > 2 ? __ldg(cp4 + 2) : make_uint4(0, 0, 0, 0);
     for (int j = 0; j < cnt8; j += 8) {
-      const uint4 cur = nxt;
-      if (j + 8 < cnt8) nxt = __ldg(cp4 + (j >> 3) + 1);
+      const uint4 cur = n0;
+      n0 = n1;
+      n1 = n2;
+      if ((j >> 3) + 3 < ng) n2 = __ldg(cp4 + (j >> 3) + 3);
       uint32_t cv[8], e[8];
       unpack8(cur, cv);
       bool hit = true;
@@ -518,8 +524,16 @@ NBZG_DEV void encode_chunk_fast(const EArgs& a, int field, int64_t c, const WinT
     }
     for (int j = cnt8; j < cnt; j++) put_code(cp[j], c0 + lo + j);
   }
+  long long head_idx = -1, tail_idx = -1;
+  uint32_t head_bits = 0, tail_bits = 0;
+  __syncwarp();
+  if (head_partial && nemit > 0) {
+    head_idx = (long long)widx0;
+    head_bits = __byte_perm(s_headw[lane], 0, 0x0123);
+  }
   if (bits > 0 && nacc > 0) {
-    tail_idx = (long long)widx;
+    // final partial word (also the first word when the lane never filled one)
+    tail_idx = (long long)(widx0 + nemit);
     tail_bits = (uint32_t)(acc >> 32);
   }
   __syncwarp();
@@ -568,6 +582,7 @@ __global__ void __launch_bounds__(kEFWarps * 32, 2) encode_fast_kernel(EArgs a) 
   uint32_t* s_win = reinterpret_cast<uint32_t*>(esm);                 // [kEncWin]
   long long* s_idx = reinterpret_cast<long long*>(s_win + kEncWin);  // [warps][64]
   uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_idx + kEFWarps * 64);
+  uint32_t* s_headw = s_bits + kEFWarps * 64;                         // [warps][32]
   const int field = blockIdx.y;
   if (a.meta->f[field].is_const || a.n == 0 || a.meta->status) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -583,7 +598,7 @@ __global__ void __launch_bounds__(kEFWarps * 32, 2) encode_fast_kernel(EArgs a) 
     if (lane == 0) c = atomicAdd(&a.tickets[field], 1u);
     c = __shfl_sync(0xffffffffu, c, 0);
     if (c >= a.nchunks) return;
-    encode_chunk_fast(a, field, c, T, s_idx + warp * 64, s_bits + warp * 64);
+    encode_chunk_fast(a, field, c, T, s_idx + warp * 64, s_bits + warp * 64, s_headw + warp * 32);
   }
 }
 
@@ -611,7 +626,7 @@ int launch_encode(const Plan& p, cudaStream_t st) {
   cudaMemsetAsync(p.lb, 0, sizeof(uint64_t) * 6 * p.nchunks, st);
   cudaMemsetAsync(p.counters, 0, sizeof(uint32_t) * 8, st);
   if (p.nbins == 65536) {
-    const size_t sm = 4 * kEncWin + kEFWarps * 64 * 12;
+    const size_t sm = 4 * kEncWin + kEFWarps * 64 * 12 + kEFWarps * 32 * 4;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(encode_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
