@@ -23,7 +23,7 @@ int launch_order_expand(const uint16_t* perm, int64_t n, int64_t tile, int64_t* 
 int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uint8_t* len,
                          uint64_t* lut, uint32_t* scratch, nbzg_meta* meta, int64_t n,
                          int64_t nchunks, int single_field, cudaStream_t st,
-                         uint32_t* twin = nullptr);
+                         uint32_t* twin = nullptr, uint8_t* tlen8 = nullptr);
 int launch_huffman_lengths(const uint32_t* counts, int64_t k, uint8_t* lengths, uint32_t* scr,
                            uint32_t* status, cudaStream_t st);
 int launch_huff_encode_raw(const uint16_t* syms, int64_t n, const uint64_t* lut, uint8_t* out,
@@ -114,6 +114,7 @@ size_t plan_workspace(Plan& p, void* base) {
   p.cb_len = reinterpret_cast<uint8_t*>(take(6 * p.nbins));
   p.lut = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 6 * p.nbins));
   p.enc_win = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 6 * kEncWin));
+  p.enc_len8 = reinterpret_cast<uint8_t*>(take(6 * (size_t)p.nbins));
   p.cb_scratch = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 6 * 5 * p.nbins));
   p.lb = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 12 * (p.nchunks + 1)));
   p.counters = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 64));

@@ -34,6 +34,7 @@ struct CBArgs {
   int single_field;   // >= 0: only this field (parity hook), meta->f[0] receives
   uint32_t* twin;     // [6][kEncWin] encoder window table (may be null): code
                       // half+1-kEncWin/2+i -> word << 6 | len (len <= 26, else 0)
+  uint8_t* tlen8;     // [6][nbins] code length by symbol (may be null)
 };
 
 NBZG_DEV void bitonic_sort_u64(uint64_t* a, int N) {
@@ -238,6 +239,7 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
       int i = tid * RK + r;
       if (i < k && lenr[i] == l) {
         lut[sym[i]] = ((uint64_t)l << 57) | (s_fc[l] + ex);
+        if (a.tlen8) a.tlen8[field * a.nbins + sym[i]] = (uint8_t)l;
         if (a.twin) {
           const uint32_t wi = sym[i] - (uint32_t)(a.nbins / 2 + 1 - kEncWin / 2);
           if (wi < (uint32_t)kEncWin)
@@ -266,8 +268,8 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
 int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uint8_t* len,
                          uint64_t* lut, uint32_t* scratch, nbzg_meta* meta, int64_t n,
                          int64_t nchunks, int single_field, cudaStream_t st,
-                         uint32_t* twin) {
-  CBArgs a{hist, nbins, sym, len, lut, scratch, meta, n, nchunks, single_field, twin};
+                         uint32_t* twin, uint8_t* tlen8) {
+  CBArgs a{hist, nbins, sym, len, lut, scratch, meta, n, nchunks, single_field, twin, tlen8};
   size_t sm = 14 * (size_t)kCBSmemK;  // keys u64 | L u32 | order u16
   static bool attr = false;
   if (!attr) {
@@ -282,7 +284,7 @@ int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uin
 int launch_codebook(const Plan& p, cudaStream_t st) {
   if (p.n == 0) return NBZG_OK;
   return launch_codebook_impl(p.hist, p.nbins, p.cb_sym, p.cb_len, p.lut, p.cb_scratch, p.meta,
-                              p.n, p.nchunks, -1, st, p.enc_win);
+                              p.n, p.nchunks, -1, st, p.enc_win, p.enc_len8);
 }
 
 // ---- parity hook: K.huffman_lengths on sorted counts (one CTA)

@@ -24,6 +24,7 @@
 //      (encoded on the spot), so every word is written exactly once -- no
 //      zero fill, no global atomics.
 #include <cstdio>
+#include <cstdlib>
 
 #include "nbzg_internal.cuh"
 #include "plan.h"
@@ -84,6 +85,7 @@ struct EArgs {
   int64_t code_stride;
   const uint64_t* lut;    // [6][nbins]
   const uint32_t* twin;   // [6][kEncWin] (payload path: staged in smem)
+  const uint8_t* tlen8;   // [6][nbins] code lengths (chunk bit counts)
   int64_t nbins;
   int64_t n, nchunks;
   const float* f[6];
@@ -387,6 +389,13 @@ NBZG_DEV uint32_t chunk_head_bits_w(const EArgs& a, int field, const uint16_t* c
   return (uint32_t)(acc >> 32) & ~(0xffffffffu >> need);
 }
 
+NBZG_DEV void st_pred_u32(uint32_t* p, uint32_t v, bool pred) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.global.u32 [%0], %1;\n}\n" ::"l"(p),
+      "r"(v), "r"((uint32_t)pred)
+      : "memory");
+}
+
 NBZG_DEV void unpack8(uint4 u, uint32_t (&cv)[8]) {
   cv[0] = u.x & 0xffffu; cv[1] = u.x >> 16;
   cv[2] = u.y & 0xffffu; cv[3] = u.y >> 16;
@@ -602,6 +611,180 @@ __global__ void __launch_bounds__(kEFWarps * 32, 2) encode_fast_kernel(EArgs a) 
   }
 }
 
+// ---- thread-per-chunk payload encoder (>= kTpcEncMinChunks chunks/field).
+// E1 counts every chunk's bits (one warp per chunk, coalesced code loads,
+// a 64 KiB shared-memory length table); E2 scans them per field into chunk
+// bit offsets (and writes the v2 chunk index); E3 packs each chunk with ONE
+// thread: no look-back, no lane merges.  A chunk writes the words whose
+// first bit it holds; its last, partial word is completed with the leading
+// bits of the next chunk (a few codes of lookahead).
+constexpr int kTpcEncMinChunks = 256;
+constexpr int kE1Warps = 16;
+
+__global__ void __launch_bounds__(kE1Warps * 32, 2) chunk_bits_kernel(EArgs a, uint32_t* cbits,
+                                                                      int ctas_per_field) {
+  extern __shared__ __align__(16) uint8_t e1sm[];
+  uint8_t* s_len = e1sm;  // [nbins]
+  const int field = blockIdx.y;
+  if (a.meta->f[field].is_const || a.n == 0 || a.meta->status) return;
+  {
+    const uint4* g = reinterpret_cast<const uint4*>(a.tlen8 + (size_t)field * a.nbins);
+    for (int i = threadIdx.x; i < (int)(a.nbins / 16); i += blockDim.x)
+      reinterpret_cast<uint4*>(s_len)[i] = __ldg(g + i);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t wg = (int64_t)blockIdx.x * kE1Warps + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)ctas_per_field * kE1Warps;
+  const uint16_t* codes = a.codes + field * a.code_stride;
+  for (int64_t c = wg; c < a.nchunks; c += nw) {
+    const int64_t c0 = c * kChunk;
+    const int mc = (int)min((int64_t)kChunk, a.n - c0);
+    const uint4* cp4 = reinterpret_cast<const uint4*>(codes + c0);
+    uint32_t bits = 0;
+    const int n8 = mc >> 3;
+#pragma unroll 4
+    for (int i = lane; i < n8; i += 32) {
+      uint32_t cv[8];
+      unpack8(__ldg(cp4 + i), cv);
+#pragma unroll
+      for (int q = 0; q < 8; q++) bits += s_len[cv[q]] + (cv[q] == 0 ? 32u : 0u);
+    }
+    for (int i = 8 * n8 + lane; i < mc; i += 32) {
+      const uint32_t code = codes[c0 + i];
+      bits += s_len[code] + (code == 0 ? 32u : 0u);
+    }
+    bits = warp_sum(bits);
+    if (lane == 0) cbits[field * a.nchunks + c] = bits;
+  }
+}
+
+// E2: per field exclusive scan of chunk bits -> chunk bit offsets; v2 index
+__global__ void __launch_bounds__(1024) chunk_scan_kernel(EArgs a, const uint32_t* cbits,
+                                                          uint64_t* coff) {
+  const int field = blockIdx.x;
+  const nbzg_field_meta& m = a.meta->f[field];
+  if (m.is_const || a.n == 0 || a.meta->status) return;
+  __shared__ unsigned long long scan_tmp[33];
+  const uint32_t* cb = cbits + field * a.nchunks;
+  uint64_t* off = coff + field * (a.nchunks + 1);
+  uint8_t* idx = a.arena + m.payload_off + m.index_off;
+  const int R = (int)((a.nchunks + blockDim.x - 1) / blockDim.x);
+  unsigned long long s = 0;
+  for (int r = 0; r < R; r++) {
+    const int64_t c = (int64_t)threadIdx.x * R + r;
+    if (c < a.nchunks) s += cb[c];
+  }
+  unsigned long long tot;
+  unsigned long long ex = block_excl_scan<unsigned long long>(s, scan_tmp, &tot);
+  for (int r = 0; r < R; r++) {
+    const int64_t c = (int64_t)threadIdx.x * R + r;
+    if (c < a.nchunks) {
+      off[c] = ex;
+      put_u32_bytes(idx + 4 * c, cb[c]);
+      ex += cb[c];
+    }
+  }
+  if (threadIdx.x == 0) {
+    off[a.nchunks] = tot;
+    if (tot != m.total_bits) atomicCAS(&a.meta->status, 0u, (uint32_t)NBZG_BAD_STREAM);
+  }
+}
+
+// E3: one thread packs one chunk
+constexpr int kE3Threads = 512;
+__global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, const uint64_t* coff,
+                                                                   int ctas_per_field) {
+  extern __shared__ __align__(16) uint8_t e3sm[];
+  uint32_t* s_win = reinterpret_cast<uint32_t*>(e3sm);  // [kEncWin]
+  const int field = blockIdx.y;
+  const nbzg_field_meta* mp = &a.meta->f[field];
+  if (mp->is_const || a.n == 0 || a.meta->status) return;
+  {
+    const uint4* g = reinterpret_cast<const uint4*>(a.twin + (size_t)field * kEncWin);
+    for (int i = threadIdx.x; i < kEncWin / 4; i += blockDim.x)
+      reinterpret_cast<uint4*>(s_win)[i] = __ldg(g + i);
+  }
+  __syncthreads();
+  const WinTab T{s_win, (uint32_t)(a.nbins / 2 + 1 - kEncWin / 2), a.lut + field * a.nbins};
+  const int64_t cb = (a.nchunks * blockIdx.x) / ctas_per_field;
+  const int64_t ce = (a.nchunks * (blockIdx.x + 1)) / ctas_per_field;
+  const uint16_t* codes = a.codes + field * a.code_stride;
+  uint32_t* outw = reinterpret_cast<uint32_t*>(a.arena + mp->payload_off + mp->bits_off);
+  const uint64_t* off = coff + field * (a.nchunks + 1);
+  for (int64_t c = cb + threadIdx.x; c < ce; c += blockDim.x) {
+    const uint64_t B = off[c], Bend = off[c + 1];
+    const int64_t c0 = c * kChunk;
+    const int mc = (int)min((int64_t)kChunk, a.n - c0);
+    const uint4* cp4 = reinterpret_cast<const uint4*>(codes + c0);
+    uint64_t acc = 0;
+    uint32_t nacc = (uint32_t)(B & 31);
+    uint32_t* wp = outw + (B >> 5);
+    bool skip = nacc != 0;  // the first, partial word belongs to chunk c-1
+    auto emit = [&](uint32_t w) {
+      st_pred_u32(wp, __byte_perm(w, 0, 0x0123), !skip);
+      skip = false;
+      wp++;
+    };
+    auto append = [&](uint32_t w, uint32_t l) {  // l <= 26
+      acc |= (uint64_t)w << (64 - nacc - l);
+      nacc += l;
+      if (nacc >= 32) {
+        emit((uint32_t)(acc >> 32));
+        acc <<= 32;
+        nacc -= 32;
+      }
+    };
+    auto put_slow = [&](uint64_t v, uint32_t nb) {
+      Acc A{acc, (int)nacc};
+      acc_put(A, v, (int)nb, emit);
+      acc = A.acc;
+      nacc = (uint32_t)A.nacc;
+    };
+    auto put_code = [&](uint32_t code, int64_t pos) {
+      uint64_t w;
+      uint32_t l;
+      win_word(T, code, w, l);
+      put_slow(w, l);
+      if (code == 0) put_slow(esc_value_bits(a, field, pos), 32);
+    };
+    const int ng = mc >> 3;
+    uint4 n0 = ng > 0 ? __ldg(cp4) : make_uint4(0, 0, 0, 0);
+    uint4 n1 = ng > 1 ? __ldg(cp4 + 1) : make_uint4(0, 0, 0, 0);
+    uint4 n2 = ng > 2 ? __ldg(cp4 + 2) : make_uint4(0, 0, 0, 0);
+    for (int g = 0; g < ng; g++) {
+      const uint4 cur = n0;
+      n0 = n1;
+      n1 = n2;
+      if (g + 3 < ng) n2 = __ldg(cp4 + g + 3);
+      uint32_t cv[8], e[8];
+      unpack8(cur, cv);
+      bool hit = true;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        const uint32_t wi = cv[q] - T.wlo;
+        e[q] = wi < (uint32_t)kEncWin ? T.win[wi] : 0u;
+        hit &= e[q] != 0;
+      }
+      if (hit) {
+#pragma unroll
+        for (int q = 0; q < 8; q++) append(e[q] >> 6, e[q] & 63u);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; q++) put_code(cv[q], c0 + 8 * g + q);
+      }
+    }
+    for (int j = 8 * ng; j < mc; j++) put_code(codes[c0 + j], c0 + j);
+    // final partial word: completed with the next chunk's leading bits
+    if (nacc > 0 && (Bend >> 5) >= ((B + 31) >> 5)) {
+      uint32_t w = (uint32_t)(acc >> 32);
+      if (c + 1 < a.nchunks)
+        w |= chunk_head_bits_w(a, field, codes, T, c + 1, 32 - (int)nacc) >> nacc;
+      *wp = __byte_perm(w, 0, 0x0123);
+    }
+  }
+}
+
 int launch_encode(const Plan& p, cudaStream_t st) {
   if (p.n == 0) return NBZG_OK;
   TArgs t{p.meta, p.arena, p.cb_sym, p.cb_len, p.nbins, p.nchunks, p.n};
@@ -623,9 +806,33 @@ int launch_encode(const Plan& p, cudaStream_t st) {
   a.tickets = p.counters;
   a.inline_esc = 1;
   a.twin = p.enc_win;
+  a.tlen8 = p.enc_len8;
   cudaMemsetAsync(p.lb, 0, sizeof(uint64_t) * 6 * p.nchunks, st);
   cudaMemsetAsync(p.counters, 0, sizeof(uint32_t) * 8, st);
-  if (p.nbins == 65536) {
+  const char* ev = getenv("NBZG_ENCODE");
+  const bool tpc = ev ? ev[0] == 't' : p.nchunks >= kTpcEncMinChunks;
+  if (p.nbins == 65536 && tpc) {
+    // E1 -> E2 -> E3; chunk bits in lb[6*(nchunks+1) ..], offsets in lb[0 ..]
+    uint64_t* coff = p.lb;
+    uint32_t* cbits = reinterpret_cast<uint32_t*>(p.lb + 6 * (p.nchunks + 1));
+    static bool attr3 = false;
+    if (!attr3) {
+      cudaFuncSetAttribute(chunk_bits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+      cudaFuncSetAttribute(encode_tpc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           4 * kEncWin);
+      attr3 = true;
+    }
+    int g1 = max(1, 2 * sm_count() / 6);
+    if (g1 > (p.nchunks + kE1Warps - 1) / kE1Warps) g1 = (int)((p.nchunks + kE1Warps - 1) / kE1Warps);
+    count_launch();
+    chunk_bits_kernel<<<dim3(g1, 6), kE1Warps * 32, (size_t)p.nbins, st>>>(a, cbits, g1);
+    count_launch();
+    chunk_scan_kernel<<<6, 1024, 0, st>>>(a, cbits, coff);
+    int g3 = max(1, 2 * sm_count() / 6);
+    if (g3 > p.nchunks) g3 = (int)p.nchunks;
+    count_launch();
+    encode_tpc_kernel<<<dim3(g3, 6), kE3Threads, 4 * kEncWin, st>>>(a, coff, g3);
+  } else if (p.nbins == 65536) {
     const size_t sm = 4 * kEncWin + kEFWarps * 64 * 12 + kEFWarps * 32 * 4;
     static bool attr = false;
     if (!attr) {

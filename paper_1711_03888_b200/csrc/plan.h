@@ -34,6 +34,7 @@ struct Plan {
   uint8_t* cb_len = nullptr;    // 6*nbins lengths by rank
   uint64_t* lut = nullptr;      // 6*nbins
   uint32_t* enc_win = nullptr;  // 6*kEncWin (word << 6 | len) of codes near the centre
+  uint8_t* enc_len8 = nullptr;  // 6*nbins code length by symbol (chunk bit counts)
   uint32_t* cb_scratch = nullptr;  // 6 * 4*nbins u32 (sort + queues, large-k path)
   uint64_t* lb = nullptr;       // 6*nchunks*2 look-back words
   uint32_t* counters = nullptr; // 64 u32 (tickets, flags)

@@ -29,6 +29,15 @@ def O(oracle_lib):
 
 
 @pytest.fixture(params=["warp", "thread"])
+def encoder(request, monkeypatch):
+    """Both v2 payload encoders (warp-per-chunk with look-back,
+    thread-per-chunk after a chunk-bit scan); csrc/encode.cu picks by chunk
+    count unless NBZG_ENCODE forces one."""
+    monkeypatch.setenv("NBZG_ENCODE", request.param)
+    return request.param
+
+
+@pytest.fixture(params=["warp", "thread"])
 def decoder(request, monkeypatch):
     """Both v2 decoders (warp-per-chunk with resync, thread-per-chunk);
     csrc/decode.cu picks by chunk count unless NBZG_DECODE forces one."""
@@ -167,7 +176,7 @@ def test_crc64(O, rng):
 # ---------------------------------------------------------------- whole path
 
 @pytest.mark.parametrize("case", GOLDEN_CASES)
-def test_archive_byte_identical_to_oracle(O, case):
+def test_archive_byte_identical_to_oracle(O, case, encoder):
     """The GPU v2 archive equals the oracle's v2 archive byte for byte:
     bounds, seg bits, permutation, dual-quant codes, Huffman tables, chunk
     index, bitstream, escapes, CRCs, header."""
@@ -299,7 +308,7 @@ def test_constant_fields_and_absolute_bounds(O, rng):
         assert np.all(np.asarray(rec.xx) == np.float32(3.25))
 
 
-def test_escape_heavy_and_tight_bounds(O, rng, decoder):
+def test_escape_heavy_and_tight_bounds(O, rng, decoder, encoder):
     n = 50000
     fields = [(rng.standard_cauchy(n) * 50).astype(np.float32) for _ in range(6)]
     snap = nbz.ParticleSnapshot(*fields)
@@ -379,7 +388,7 @@ def test_corrupt_payloads_fail_cleanly(decoder):
 
 @pytest.mark.parametrize("spec,mode", [("C1", "sz-lv"), ("C1", "sz-lv-prx"),
                                        ("C0", "sz-lv-prx")])
-def test_config_scale_parity(O, spec, mode, decoder):
+def test_config_scale_parity(O, spec, mode, decoder, encoder):
     """BASELINE configs 0 and 1 at full size: byte-identical archives."""
     fields = datagen.generate(spec)
     snap = nbz.ParticleSnapshot(*fields)
@@ -400,7 +409,7 @@ def test_config_scale_parity(O, spec, mode, decoder):
 
 @pytest.mark.parametrize("seg,ig,ic", [(1000, 6, 65536), (4099, 2, 65536), (16384, 0, 65536),
                                        (16384, 6, 1024), (777, 3, 4096), (16384, 6, 2)])
-def test_settings_variants_byte_identical(O, seg, ig, ic, decoder):
+def test_settings_variants_byte_identical(O, seg, ig, ic, decoder, encoder):
     """Non-default Settings (segment size not a multiple of 4, ignored
     groups, small interval counts -> generic encoder path, heavy escapes):
     archives byte-identical to the oracle, decode exact and within bound."""
