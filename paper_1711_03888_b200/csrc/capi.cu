@@ -115,6 +115,9 @@ size_t plan_workspace(Plan& p, void* base) {
   p.lut = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 6 * p.nbins));
   p.enc_win = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 6 * kEncWin));
   p.enc_len8 = reinterpret_cast<uint8_t*>(take(6 * (size_t)p.nbins));
+  p.enc_boff = reinterpret_cast<uint64_t*>(
+      take(sizeof(uint64_t) * 6 * ((size_t)p.nchunks + 1) +
+           sizeof(uint32_t) * 6 * (33 * (size_t)p.nchunks)));
   p.cb_scratch = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 6 * 5 * p.nbins));
   p.lb = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 12 * (p.nchunks + 1)));
   p.counters = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 64));

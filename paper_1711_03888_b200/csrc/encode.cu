@@ -396,6 +396,14 @@ NBZG_DEV void st_pred_u32(uint32_t* p, uint32_t v, bool pred) {
       : "memory");
 }
 
+NBZG_DEV void st_pred_v4(uint32_t* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d, bool pred) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.u32 p, %5, 0;\n"
+      " @p st.global.v4.u32 [%0], {%1, %2, %3, %4};\n}\n" ::"l"(p),
+      "r"(a), "r"(b), "r"(c), "r"(d), "r"((uint32_t)pred)
+      : "memory");
+}
+
 NBZG_DEV void unpack8(uint4 u, uint32_t (&cv)[8]) {
   cv[0] = u.x & 0xffffu; cv[1] = u.x >> 16;
   cv[2] = u.y & 0xffffu; cv[3] = u.y >> 16;
@@ -611,17 +619,46 @@ __global__ void __launch_bounds__(kEFWarps * 32, 2) encode_fast_kernel(EArgs a) 
   }
 }
 
-// ---- thread-per-chunk payload encoder (>= kTpcEncMinChunks chunks/field).
-// E1 counts every chunk's bits (one warp per chunk, coalesced code loads,
-// a 64 KiB shared-memory length table); E2 scans them per field into chunk
-// bit offsets (and writes the v2 chunk index); E3 packs each chunk with ONE
-// thread: no look-back, no lane merges.  A chunk writes the words whose
-// first bit it holds; its last, partial word is completed with the leading
-// bits of the next chunk (a few codes of lookahead).
+// ---- block-parallel payload encoder (>= kTpcEncMinChunks chunks/field).
+// A chunk's 16384 codes are 32 blocks of 512.  E1 counts every block's bits
+// (one warp per chunk, coalesced code loads, 64 KiB smem length table); E2
+// scans them per field into block bit offsets (and writes the v2 chunk
+// index); E3 packs each block with ONE thread at its known offset: no
+// look-back, no merges.  A block writes the words whose first bit it holds;
+// its last, partial word is completed with the leading bits of the stream
+// after it (a few codes of lookahead).
 constexpr int kTpcEncMinChunks = 256;
+constexpr int kBlk = 512;                  // codes per block (= warp encoder's lane share)
+constexpr int kBlkPerChunk = kChunk / kBlk;
 constexpr int kE1Warps = 16;
 
-__global__ void __launch_bounds__(kE1Warps * 32, 2) chunk_bits_kernel(EArgs a, uint32_t* cbits,
+// leading `need` (1..31) bits of the stream from code s0 on, MSB-aligned
+NBZG_DEV uint32_t head_bits_from(const EArgs& a, int field, const uint16_t* codes,
+                                 const WinTab& T, int64_t s0, int need) {
+  uint64_t acc = 0;
+  int nacc = 0;
+  for (int64_t i = s0; i < a.n && nacc < need; i++) {
+    const uint32_t code = codes[i];
+    uint64_t w;
+    uint32_t lu;
+    win_word(T, code, w, lu);
+    int l = (int)lu;
+    if (l > 32) {
+      w >>= (l - 32);
+      l = 32;
+    }
+    acc |= (w << (64 - l)) >> nacc;
+    nacc += l;
+    if (code == 0 && nacc < need) {
+      acc |= ((uint64_t)esc_value_bits(a, field, i) << 32) >> nacc;
+      nacc += 32;
+    }
+  }
+  return (uint32_t)(acc >> 32) & ~(0xffffffffu >> need);
+}
+
+__global__ void __launch_bounds__(kE1Warps * 32, 2) chunk_bits_kernel(EArgs a, uint32_t* bbits,
+                                                                      uint32_t* ctot,
                                                                       int ctas_per_field) {
   extern __shared__ __align__(16) uint8_t e1sm[];
   uint8_t* s_len = e1sm;  // [nbins]
@@ -637,52 +674,63 @@ __global__ void __launch_bounds__(kE1Warps * 32, 2) chunk_bits_kernel(EArgs a, u
   const int64_t wg = (int64_t)blockIdx.x * kE1Warps + (threadIdx.x >> 5);
   const int64_t nw = (int64_t)ctas_per_field * kE1Warps;
   const uint16_t* codes = a.codes + field * a.code_stride;
+  uint32_t* bb = bbits + (size_t)field * a.nchunks * kBlkPerChunk;
   for (int64_t c = wg; c < a.nchunks; c += nw) {
     const int64_t c0 = c * kChunk;
     const int mc = (int)min((int64_t)kChunk, a.n - c0);
     const uint4* cp4 = reinterpret_cast<const uint4*>(codes + c0);
-    uint32_t bits = 0;
-    const int n8 = mc >> 3;
-#pragma unroll 4
-    for (int i = lane; i < n8; i += 32) {
-      uint32_t cv[8];
-      unpack8(__ldg(cp4 + i), cv);
+    uint32_t mine = 0;  // lane b keeps block b's count
+#pragma unroll 2
+    for (int b = 0; b < kBlkPerChunk; b++) {
+      const int lo = b * kBlk;
+      uint32_t bits = 0;
+      if (lo + kBlk <= mc) {  // full block: 64 uint4, two per lane
+        uint32_t cv[8];
+        unpack8(__ldg(cp4 + lo / 8 + lane), cv);
 #pragma unroll
-      for (int q = 0; q < 8; q++) bits += s_len[cv[q]] + (cv[q] == 0 ? 32u : 0u);
+        for (int q = 0; q < 8; q++) bits += s_len[cv[q]] + (cv[q] == 0 ? 32u : 0u);
+        unpack8(__ldg(cp4 + lo / 8 + 32 + lane), cv);
+#pragma unroll
+        for (int q = 0; q < 8; q++) bits += s_len[cv[q]] + (cv[q] == 0 ? 32u : 0u);
+      } else {
+        for (int i = lo + lane; i < min(mc, lo + kBlk); i += 32) {
+          const uint32_t code = codes[c0 + i];
+          bits += s_len[code] + (code == 0 ? 32u : 0u);
+        }
+      }
+      bits = warp_sum(bits);
+      mine = lane == b ? bits : mine;
     }
-    for (int i = 8 * n8 + lane; i < mc; i += 32) {
-      const uint32_t code = codes[c0 + i];
-      bits += s_len[code] + (code == 0 ? 32u : 0u);
-    }
-    bits = warp_sum(bits);
-    if (lane == 0) cbits[field * a.nchunks + c] = bits;
+    const uint32_t incl = warp_incl_scan<uint32_t>(mine);
+    bb[c * kBlkPerChunk + lane] = incl - mine;  // in-chunk exclusive prefix
+    if (lane == 31) ctot[field * a.nchunks + c] = incl;
   }
 }
 
 // E2: per field exclusive scan of chunk bits -> chunk bit offsets; v2 index
-__global__ void __launch_bounds__(1024) chunk_scan_kernel(EArgs a, const uint32_t* cbits,
+__global__ void __launch_bounds__(1024) chunk_scan_kernel(EArgs a, const uint32_t* ctot,
                                                           uint64_t* coff) {
   const int field = blockIdx.x;
   const nbzg_field_meta& m = a.meta->f[field];
   if (m.is_const || a.n == 0 || a.meta->status) return;
   __shared__ unsigned long long scan_tmp[33];
-  const uint32_t* cb = cbits + field * a.nchunks;
-  uint64_t* off = coff + field * (a.nchunks + 1);
+  const uint32_t* ct = ctot + (size_t)field * a.nchunks;
+  uint64_t* off = coff + (size_t)field * (a.nchunks + 1);
   uint8_t* idx = a.arena + m.payload_off + m.index_off;
-  const int R = (int)((a.nchunks + blockDim.x - 1) / blockDim.x);
+  const int64_t R = (a.nchunks + blockDim.x - 1) / blockDim.x;
   unsigned long long s = 0;
-  for (int r = 0; r < R; r++) {
+  for (int64_t r = 0; r < R; r++) {
     const int64_t c = (int64_t)threadIdx.x * R + r;
-    if (c < a.nchunks) s += cb[c];
+    if (c < a.nchunks) s += ct[c];
   }
   unsigned long long tot;
   unsigned long long ex = block_excl_scan<unsigned long long>(s, scan_tmp, &tot);
-  for (int r = 0; r < R; r++) {
+  for (int64_t r = 0; r < R; r++) {
     const int64_t c = (int64_t)threadIdx.x * R + r;
     if (c < a.nchunks) {
       off[c] = ex;
-      put_u32_bytes(idx + 4 * c, cb[c]);
-      ex += cb[c];
+      put_u32_bytes(idx + 4 * c, ct[c]);
+      ex += ct[c];
     }
   }
   if (threadIdx.x == 0) {
@@ -691,9 +739,10 @@ __global__ void __launch_bounds__(1024) chunk_scan_kernel(EArgs a, const uint32_
   }
 }
 
-// E3: one thread packs one chunk
+// E3: one thread packs one 512-code block
 constexpr int kE3Threads = 512;
 __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, const uint64_t* coff,
+                                                                   const uint32_t* bpre,
                                                                    int ctas_per_field) {
   extern __shared__ __align__(16) uint8_t e3sm[];
   uint32_t* s_win = reinterpret_cast<uint32_t*>(e3sm);  // [kEncWin]
@@ -707,24 +756,42 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
   }
   __syncthreads();
   const WinTab T{s_win, (uint32_t)(a.nbins / 2 + 1 - kEncWin / 2), a.lut + field * a.nbins};
-  const int64_t cb = (a.nchunks * blockIdx.x) / ctas_per_field;
-  const int64_t ce = (a.nchunks * (blockIdx.x + 1)) / ctas_per_field;
+  const int64_t nb = a.nchunks * kBlkPerChunk;
   const uint16_t* codes = a.codes + field * a.code_stride;
   uint32_t* outw = reinterpret_cast<uint32_t*>(a.arena + mp->payload_off + mp->bits_off);
-  const uint64_t* off = coff + field * (a.nchunks + 1);
-  for (int64_t c = cb + threadIdx.x; c < ce; c += blockDim.x) {
-    const uint64_t B = off[c], Bend = off[c + 1];
-    const int64_t c0 = c * kChunk;
-    const int mc = (int)min((int64_t)kChunk, a.n - c0);
-    const uint4* cp4 = reinterpret_cast<const uint4*>(codes + c0);
+  const uint64_t* off = coff + (size_t)field * (a.nchunks + 1);
+  const uint32_t* bp = bpre + (size_t)field * nb;
+  const uint64_t ow = (reinterpret_cast<uintptr_t>(outw) >> 2) & 3;  // word phase of outw
+  const int64_t stride = (int64_t)ctas_per_field * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nb; k += stride) {
+    const int64_t s0 = k * kBlk;
+    if (s0 >= a.n) continue;  // empty tail blocks of the last chunk
+    const int mc = (int)min((int64_t)kBlk, a.n - s0);
+    const int64_t c = k / kBlkPerChunk;
+    const uint64_t B = off[c] + bp[k];
+    const uint64_t Bend = (k + 1) % kBlkPerChunk ? off[c] + bp[k + 1] : off[c + 1];
+    const uint4* cp4 = reinterpret_cast<const uint4*>(codes + s0);
     uint64_t acc = 0;
     uint32_t nacc = (uint32_t)(B & 31);
-    uint32_t* wp = outw + (B >> 5);
-    bool skip = nacc != 0;  // the first, partial word belongs to chunk c-1
+    // completed words: scalar stores up to the first 16-byte boundary at or
+    // after the first owned word (the first partial word belongs to the
+    // block before), then buffered 16-byte stores of aligned word quads
+    uint64_t widx = B >> 5;
+    const uint64_t fo = (B + 31) >> 5;
+    const uint64_t va = ((fo + ow + 3) & ~3ull) - ow;  // first 16-byte aligned owned word
+    uint32_t q0 = 0, q1 = 0, q2 = 0;
     auto emit = [&](uint32_t w) {
-      st_pred_u32(wp, __byte_perm(w, 0, 0x0123), !skip);
-      skip = false;
-      wp++;
+      w = __byte_perm(w, 0, 0x0123);
+      if (widx < va) {
+        st_pred_u32(outw + widx, w, widx >= fo);
+      } else {
+        const uint32_t sl = (uint32_t)(widx + ow) & 3u;
+        q0 = sl == 0 ? w : q0;
+        q1 = sl == 1 ? w : q1;
+        q2 = sl == 2 ? w : q2;
+        st_pred_v4(outw + widx - 3, q0, q1, q2, w, sl == 3);
+      }
+      widx++;
     };
     auto append = [&](uint32_t w, uint32_t l) {  // l <= 26
       acc |= (uint64_t)w << (64 - nacc - l);
@@ -735,9 +802,9 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
         nacc -= 32;
       }
     };
-    auto put_slow = [&](uint64_t v, uint32_t nb) {
+    auto put_slow = [&](uint64_t v, uint32_t nb2) {
       Acc A{acc, (int)nacc};
-      acc_put(A, v, (int)nb, emit);
+      acc_put(A, v, (int)nb2, emit);
       acc = A.acc;
       nacc = (uint32_t)A.nacc;
     };
@@ -771,16 +838,22 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
         for (int q = 0; q < 8; q++) append(e[q] >> 6, e[q] & 63u);
       } else {
 #pragma unroll
-        for (int q = 0; q < 8; q++) put_code(cv[q], c0 + 8 * g + q);
+        for (int q = 0; q < 8; q++) put_code(cv[q], s0 + 8 * g + q);
       }
     }
-    for (int j = 8 * ng; j < mc; j++) put_code(codes[c0 + j], c0 + j);
-    // final partial word: completed with the next chunk's leading bits
-    if (nacc > 0 && (Bend >> 5) >= ((B + 31) >> 5)) {
+    for (int j = 8 * ng; j < mc; j++) put_code(codes[s0 + j], s0 + j);
+    // flush buffered words of the last (incomplete) aligned quad
+    if (widx > va) {
+      const uint32_t nq = (uint32_t)(widx + ow) & 3u;  // words [widx - nq, widx) pending
+      if (nq > 0) outw[widx - nq] = q0;
+      if (nq > 1) outw[widx - nq + 1] = q1;
+      if (nq > 2) outw[widx - nq + 2] = q2;
+    }
+    // final partial word: completed with the leading bits that follow
+    if (nacc > 0 && (Bend >> 5) >= fo) {
       uint32_t w = (uint32_t)(acc >> 32);
-      if (c + 1 < a.nchunks)
-        w |= chunk_head_bits_w(a, field, codes, T, c + 1, 32 - (int)nacc) >> nacc;
-      *wp = __byte_perm(w, 0, 0x0123);
+      if (s0 + mc < a.n) w |= head_bits_from(a, field, codes, T, s0 + mc, 32 - (int)nacc) >> nacc;
+      outw[widx] = __byte_perm(w, 0, 0x0123);
     }
   }
 }
@@ -812,9 +885,11 @@ int launch_encode(const Plan& p, cudaStream_t st) {
   const char* ev = getenv("NBZG_ENCODE");
   const bool tpc = ev ? ev[0] == 't' : p.nchunks >= kTpcEncMinChunks;
   if (p.nbins == 65536 && tpc) {
-    // E1 -> E2 -> E3; chunk bits in lb[6*(nchunks+1) ..], offsets in lb[0 ..]
-    uint64_t* coff = p.lb;
-    uint32_t* cbits = reinterpret_cast<uint32_t*>(p.lb + 6 * (p.nchunks + 1));
+    // E1 -> E2 -> E3: chunk offsets, then in-chunk block prefixes, chunk totals
+    const int64_t nb = p.nchunks * kBlkPerChunk;
+    uint64_t* coff = p.enc_boff;
+    uint32_t* bpre = reinterpret_cast<uint32_t*>(p.enc_boff + 6 * (p.nchunks + 1));
+    uint32_t* ctot = bpre + 6 * nb;
     static bool attr3 = false;
     if (!attr3) {
       cudaFuncSetAttribute(chunk_bits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
@@ -825,13 +900,13 @@ int launch_encode(const Plan& p, cudaStream_t st) {
     int g1 = max(1, 2 * sm_count() / 6);
     if (g1 > (p.nchunks + kE1Warps - 1) / kE1Warps) g1 = (int)((p.nchunks + kE1Warps - 1) / kE1Warps);
     count_launch();
-    chunk_bits_kernel<<<dim3(g1, 6), kE1Warps * 32, (size_t)p.nbins, st>>>(a, cbits, g1);
+    chunk_bits_kernel<<<dim3(g1, 6), kE1Warps * 32, (size_t)p.nbins, st>>>(a, bpre, ctot, g1);
     count_launch();
-    chunk_scan_kernel<<<6, 1024, 0, st>>>(a, cbits, coff);
+    chunk_scan_kernel<<<6, 1024, 0, st>>>(a, ctot, coff);
     int g3 = max(1, 2 * sm_count() / 6);
-    if (g3 > p.nchunks) g3 = (int)p.nchunks;
+    if (g3 > (nb + kE3Threads - 1) / kE3Threads) g3 = (int)((nb + kE3Threads - 1) / kE3Threads);
     count_launch();
-    encode_tpc_kernel<<<dim3(g3, 6), kE3Threads, 4 * kEncWin, st>>>(a, coff, g3);
+    encode_tpc_kernel<<<dim3(g3, 6), kE3Threads, 4 * kEncWin, st>>>(a, coff, bpre, g3);
   } else if (p.nbins == 65536) {
     const size_t sm = 4 * kEncWin + kEFWarps * 64 * 12 + kEFWarps * 32 * 4;
     static bool attr = false;

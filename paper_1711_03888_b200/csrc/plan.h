@@ -35,6 +35,7 @@ struct Plan {
   uint64_t* lut = nullptr;      // 6*nbins
   uint32_t* enc_win = nullptr;  // 6*kEncWin (word << 6 | len) of codes near the centre
   uint8_t* enc_len8 = nullptr;  // 6*nbins code length by symbol (chunk bit counts)
+  uint64_t* enc_boff = nullptr; // 6*(32*nchunks+1) block bit offsets, then u32 block bits
   uint32_t* cb_scratch = nullptr;  // 6 * 4*nbins u32 (sort + queues, large-k path)
   uint64_t* lb = nullptr;       // 6*nchunks*2 look-back words
   uint32_t* counters = nullptr; // 64 u32 (tickets, flags)
