@@ -68,6 +68,19 @@ NBZG_DEV void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+NBZG_DEV uint32_t ld_shared_u16(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+NBZG_DEV float ld_shared_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+NBZG_DEV void red_shared_add1(uint32_t addr) {
+  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+}
 NBZG_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // dual-quant lattice index, clamped (orc_dq_quantize: dq_k)
@@ -196,12 +209,19 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
     }
     const int pr = (int)((-t0) & (kChunk - 1));  // position of a chunk start in this tile
     uint16_t* cdst = codes + t0 + wbase + lane;   // advances 32 codes per step
-#pragma unroll 4
-    for (int j = 0; j < kQPer; j++, cdst += 32) {
+    // 32-bit shared-window addresses, computed once (no per-access
+    // generic-to-shared conversion)
+    const uint32_t xs_s = smem_u32(xs), ps_s = smem_u32(ps), hw_s = smem_u32(hw);
+    int32_t rp32 = (int32_t)max(min(rot_prev, (int64_t)(1 << 30)), -(int64_t)(1 << 30));
+    auto step = [&](int j, bool full) {
       const int p = wbase + j * 32 + lane;
-      const bool valid = p < m;
+      const bool valid = full || p < m;
       float xv = 0.0f;
-      if (valid) xv = SORTED ? xs[min((int)ps[p], m - 1)] : xs[p];
+      if (valid) {
+        uint32_t src = (uint32_t)p;
+        if (SORTED) src = min(ld_shared_u16(ps_s + 2u * (uint32_t)p), (uint32_t)(m - 1));
+        xv = ld_shared_f32(xs_s + 4u * src);
+      }
       // FP32 fast lattice index (see dq_index_fast)
       const float tq = xv * inv32;
       const float rq = tq + 12582912.0f;
@@ -211,12 +231,12 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
       uint32_t code;
       if (__all_sync(0xffffffffu, fast)) {
         // common case: every |k| < 2^22.  32-bit chain: lane 0's predecessor
-        // is clamped to +-2^30, which keeps any out-of-range q out of range
-        // (|q| > half either way), so the escape decision is unchanged
+        // is clamped to +-2^30 (rp32), which keeps any out-of-range q out of
+        // range (|q| > half either way), so the escape decision is unchanged
         const int32_t k = __float_as_int(rq) - 0x4B400000;
         const int32_t kr = __shfl_sync(0xffffffffu, k, (lane + 31) & 31);
-        const int32_t kc = (int32_t)max(min(rot_prev, (int64_t)(1 << 30)), -(int64_t)(1 << 30));
-        int32_t kp = lane == 0 ? kc : kr;
+        int32_t kp = lane == 0 ? rp32 : kr;
+        rp32 = kr;
         rot_prev = kr;
         if (p == pr) kp = 0;  // chain restarts every v2 chunk
         const int32_t q = k - kp;
@@ -228,6 +248,7 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
         const int64_t kr = __shfl_sync(0xffffffffu, k, (lane + 31) & 31);
         int64_t kp = lane == 0 ? rot_prev : kr;
         rot_prev = kr;
+        rp32 = (int32_t)max(min(kr, (int64_t)(1 << 30)), -(int64_t)(1 << 30));
         if (p == pr) kp = 0;
         const int64_t q = k - kp;
         bool ok = (uint64_t)(q + half) <= (uint64_t)(2 * half - 2);
@@ -242,10 +263,17 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
         // histogram: smem window around the centre; escapes (code 0) and
         // far codes go straight to global memory
         const uint32_t wb = code - (uint32_t)wlo;
-        if (wb < (uint32_t)kQWin) atomicAdd(&hw[wb], 1u);
+        if (wb < (uint32_t)kQWin) red_shared_add1(hw_s + 4u * wb);
         else atomicAdd(&hist[code], 1u);
-        *cdst = (uint16_t)code;
+        cdst[32 * j] = (uint16_t)code;
       }
+    };
+    if (m == kQThreads * kQPer) {  // full tile: no bounds checks
+#pragma unroll 4
+      for (int j = 0; j < kQPer; j++) step(j, true);
+    } else {
+#pragma unroll 1
+      for (int j = 0; j < kQPer; j++) step(j, false);
     }
     __syncthreads();  // buffer `buf` fully consumed; s_carry visible
     if (a.use_tma && tid == 0 && t + 2 < te) {
