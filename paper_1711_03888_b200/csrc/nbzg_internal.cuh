@@ -87,6 +87,42 @@ NBZG_DEV uint64_t spread3_64(uint64_t v) {
   return v;
 }
 
+// ---------------------------------------------------------------- shared memory
+// 32-bit shared-window addresses: computed once per kernel, they spare the
+// per-access generic-to-shared conversion the compiler otherwise re-derives
+// inside hot loops for pointers into dynamic shared memory.
+NBZG_DEV uint32_t sh_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+NBZG_DEV uint32_t lds_u16(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+NBZG_DEV uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+NBZG_DEV uint64_t lds_u64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+NBZG_DEV void sts_u16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((uint16_t)v) : "memory");
+}
+NBZG_DEV void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+NBZG_DEV void sts_u64(uint32_t a, uint64_t v) {
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+template <typename T>
+NBZG_DEV T lds_key(uint32_t a);
+template <>
+NBZG_DEV uint32_t lds_key<uint32_t>(uint32_t a) { return lds_u32(a); }
+template <>
+NBZG_DEV uint64_t lds_key<uint64_t>(uint32_t a) { return lds_u64(a); }
+
 NBZG_DEV uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

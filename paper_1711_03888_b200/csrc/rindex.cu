@@ -70,6 +70,7 @@ NBZG_DEV uint64_t make_key<uint64_t>(uint64_t u0, uint64_t u1, uint64_t u2) {
 }
 
 // Stable LSD sort of perm[lo, lo+m) by keys[perm[.]] over sort_bits bits.
+// All shared accesses use 32-bit shared-window addresses.
 template <typename KeyT>
 NBZG_DEV void block_sort_range(const KeyT* keys, uint16_t* perm, int lo, int m, int sort_bits,
                                uint16_t* whist, uint32_t* scan_tmp) {
@@ -77,9 +78,11 @@ NBZG_DEV void block_sort_range(const KeyT* keys, uint16_t* perm, int lo, int m, 
   const int E = ((m + kSortWarps * 32 - 1) / (kSortWarps * 32)) * 32;  // per-warp span
   const int J = E / 32;
   const int base = w * E;
-  uint16_t* wh = whist + w * kRadix;
+  const uint32_t keys_s = sh_addr(keys), perm_s = sh_addr(perm) + 2u * (uint32_t)lo;
+  const uint32_t whist_s = sh_addr(whist), wh_s = whist_s + 2u * (uint32_t)(w * kRadix);
   for (int sh = 0; sh < sort_bits; sh += 8) {
-    for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) whist[i] = 0;
+    for (int i = threadIdx.x; i < kSortWarps * kRadix / 2; i += kSortThreads)
+      sts_u32(whist_s + 4u * (uint32_t)i, 0u);
     __syncthreads();
     uint32_t packed[32];
 #pragma unroll
@@ -87,13 +90,14 @@ NBZG_DEV void block_sort_range(const KeyT* keys, uint16_t* perm, int lo, int m, 
       if (j < J) {
         int pos = base + j * 32 + lane;
         bool valid = pos < m;
-        uint32_t idx = valid ? perm[lo + pos] : 0u;
-        uint32_t d = valid ? (uint32_t)((keys[idx] >> sh) & 0xff) : 0x100u;
+        uint32_t idx = valid ? lds_u16(perm_s + 2u * (uint32_t)pos) : 0u;
+        uint32_t d = valid ? (uint32_t)((lds_key<KeyT>(keys_s + (uint32_t)sizeof(KeyT) * idx) >> sh) & 0xff)
+                           : 0x100u;
         uint32_t peers = __match_any_sync(0xffffffffu, d);
         uint32_t lt = __popc(peers & lanemask_lt());
-        uint32_t cnt = valid ? wh[d] : 0u;
+        uint32_t cnt = valid ? lds_u16(wh_s + 2u * d) : 0u;
         __syncwarp();
-        if (valid && lt == 0) wh[d] = (uint16_t)(cnt + __popc(peers));
+        if (valid && lt == 0) sts_u16(wh_s + 2u * d, cnt + __popc(peers));
         __syncwarp();
         packed[j] = idx | ((cnt + lt) << 14) | (d << 24);
       }
@@ -124,7 +128,7 @@ NBZG_DEV void block_sort_range(const KeyT* keys, uint16_t* perm, int lo, int m, 
       if (j < J && base + j * 32 + lane < m) {
         uint32_t v = packed[j];
         uint32_t idx = v & 0x3fff, r = (v >> 14) & 0x3ff, d = v >> 24;
-        perm[lo + wh[d] + r] = (uint16_t)idx;
+        sts_u16(perm_s + 2u * (lds_u16(wh_s + 2u * d) + r), idx);
       }
     }
     __syncthreads();
