@@ -57,34 +57,54 @@ NBZG_DEV void bitonic_sort_u64(uint64_t* a, int N) {
 // Two-queue Huffman over ascending leaf weights L[0..k).  On return L[i]
 // holds the internal index of leaf i's parent and I[j] that of internal node
 // j's parent (root = k-2 holds 0xffffffff).  Exactly _kernels.py:213-232.
-NBZG_DEV void two_queue(uint32_t* L, uint32_t* I, int k) {
+template <bool SH>
+NBZG_DEV uint32_t tq_ld(uint32_t* base, uint32_t sbase, int i) {
+  return SH ? lds_u32(sbase + 4u * (uint32_t)i) : base[i];
+}
+template <bool SH>
+NBZG_DEV void tq_st(uint32_t* base, uint32_t sbase, int i, uint32_t v) {
+  if (SH) sts_u32(sbase + 4u * (uint32_t)i, v);
+  else base[i] = v;
+}
+// The merge is sequential; both queue heads and the element behind each
+// head are kept in registers, so the load of the next element overlaps the
+// following picks instead of sitting on the compare chain.
+template <bool SH>
+NBZG_DEV void two_queue_impl(uint32_t* L, uint32_t* I, int k) {
   const uint32_t INF = 0xffffffffu;
+  const uint32_t Ls = SH ? sh_addr(L) : 0u, Is = SH ? sh_addr(I) : 0u;
   int leaf = 0, node = 0;
-  uint32_t wl = L[0];
-  uint32_t wl_next = k > 1 ? L[1] : INF;
-  uint32_t wi = INF;
+  uint32_t wl = tq_ld<SH>(L, Ls, 0);
+  uint32_t wl_n = k > 1 ? tq_ld<SH>(L, Ls, 1) : INF;
+  uint32_t wi = INF, wi_n = INF;  // node queue I[node .. nI) empty
   for (int nI = 0; nI < k - 1; nI++) {
     uint32_t w2[2];
 #pragma unroll
     for (int r = 0; r < 2; r++) {
       if (wl <= wi) {  // leaf wins ties (weight[leaf] <= weight[node])
         w2[r] = wl;
-        L[leaf] = (uint32_t)nI;
+        tq_st<SH>(L, Ls, leaf, (uint32_t)nI);
         leaf++;
-        wl = wl_next;
-        wl_next = leaf + 1 < k ? L[leaf + 1] : INF;
+        wl = wl_n;
+        wl_n = leaf + 1 < k ? tq_ld<SH>(L, Ls, leaf + 1) : INF;
       } else {
         w2[r] = wi;
-        I[node] = (uint32_t)nI;
+        tq_st<SH>(I, Is, node, (uint32_t)nI);
         node++;
-        wi = node < nI ? I[node] : INF;
+        wi = wi_n;
+        wi_n = node + 1 < nI ? tq_ld<SH>(I, Is, node + 1) : INF;
       }
     }
-    uint32_t s = w2[0] + w2[1];
-    I[nI] = s;
-    if (node == nI) wi = s;
+    const uint32_t s = w2[0] + w2[1];
+    tq_st<SH>(I, Is, nI, s);
+    if (node == nI) wi = s;            // the queue was empty
+    else if (node + 1 == nI) wi_n = s;  // s sits right behind the head
   }
-  I[k - 2] = INF;
+  tq_st<SH>(I, Is, k - 2, INF);
+}
+NBZG_DEV void two_queue(uint32_t* L, uint32_t* I, int k, bool in_smem) {
+  if (in_smem) two_queue_impl<true>(L, I, k);
+  else two_queue_impl<false>(L, I, k);
 }
 
 // Depth of every internal node (root = ni-1, parent index in I[j], parent >
@@ -183,7 +203,7 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
     }
     __syncthreads();
     // ---- C. two-queue merge (sequential, exact)
-    if (tid == 0) two_queue(L, I, k);
+    if (tid == 0) two_queue(L, I, k, small);
     __syncthreads();
     // ---- D. depths
     node_depths(I, D, k - 1);
@@ -307,7 +327,7 @@ __global__ void __launch_bounds__(kCBThreads) huffman_lengths_kernel(const uint3
   }
   for (int i = tid; i < k; i += kCBThreads) L[i] = counts[i];
   __syncthreads();
-  if (tid == 0) two_queue(L, I, k);
+  if (tid == 0) two_queue(L, I, k, small);
   __syncthreads();
   node_depths(I, D, k - 1);
   for (int i = tid; i < k; i += kCBThreads) {
