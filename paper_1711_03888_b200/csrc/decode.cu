@@ -711,6 +711,13 @@ struct TpcReader {
   uint4 qs;              // block wr/4, loaded at the last boundary
 };
 
+// one 32-byte streaming store (sm_100 256-bit STG): a whole sector per lane
+NBZG_DEV void st_v8_cs(float* p, const float (&o)[8]) {
+  asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(o[0]),
+               "f"(o[1]), "f"(o[2]), "f"(o[3]), "f"(o[4]), "f"(o[5]), "f"(o[6]), "f"(o[7])
+               : "memory");
+}
+
 NBZG_DEV void tpc_init(TpcReader& R, const uint4* G, uint32_t* ring, int nthr, uint64_t bitpos,
                        uint32_t vmax) {
   const uint32_t gw0 = (uint32_t)(bitpos >> 5);
@@ -814,7 +821,7 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, 
   const int bias = a.half + 1;
   const int max_len = (int)P.max_len;
   const double twob = F.twob;
-  const bool vec = (reinterpret_cast<uintptr_t>(F.out) & 15) == 0;
+  const bool vec = (reinterpret_cast<uintptr_t>(F.out) & 31) == 0;  // 32-byte stores
   const uint32_t r0 = (uint32_t)min(P.t2_r0, (uint64_t)0xFFFFFFFFu);
   const uint32_t sh2 = 32u - P.t2_w;
   const int32_t* LT2 = LT + (1 << kTpcBits);
@@ -925,14 +932,11 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, 
         group(oa);
         asm volatile("" ::"f"(ob[0]), "f"(ob[1]), "f"(ob[2]), "f"(ob[3]), "f"(ob[4]),
                      "f"(ob[5]), "f"(ob[6]), "f"(ob[7]));
-        float4* d4 = reinterpret_cast<float4*>(dst + i);
-        __stcs(d4, make_float4(oa[0], oa[1], oa[2], oa[3]));
-        __stcs(d4 + 1, make_float4(oa[4], oa[5], oa[6], oa[7]));
+        st_v8_cs(dst + i, oa);
         group(ob);
         asm volatile("" ::"f"(oa[0]), "f"(oa[1]), "f"(oa[2]), "f"(oa[3]), "f"(oa[4]),
                      "f"(oa[5]), "f"(oa[6]), "f"(oa[7]));
-        __stcs(d4 + 2, make_float4(ob[0], ob[1], ob[2], ob[3]));
-        __stcs(d4 + 3, make_float4(ob[4], ob[5], ob[6], ob[7]));
+        st_v8_cs(dst + i + 8, ob);
         if (consumed() > Tb) break;  // corrupt: stop early, reported below
       }
     }
