@@ -404,6 +404,15 @@ NBZG_DEV void st_pred_v4(uint32_t* p, uint32_t a, uint32_t b, uint32_t c, uint32
       : "memory");
 }
 
+NBZG_DEV void st_pred_v8(uint32_t* p, const uint32_t (&q)[7], uint32_t w, bool pred) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.u32 p, %9, 0;\n"
+      " @p st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n}\n" ::"l"(p),
+      "r"(q[0]), "r"(q[1]), "r"(q[2]), "r"(q[3]), "r"(q[4]), "r"(q[5]), "r"(q[6]), "r"(w),
+      "r"((uint32_t)pred)
+      : "memory");
+}
+
 NBZG_DEV void unpack8(uint4 u, uint32_t (&cv)[8]) {
   cv[0] = u.x & 0xffffu; cv[1] = u.x >> 16;
   cv[2] = u.y & 0xffffu; cv[3] = u.y >> 16;
@@ -740,7 +749,7 @@ __global__ void __launch_bounds__(1024) chunk_scan_kernel(EArgs a, const uint32_
 }
 
 // E3: one thread packs one 512-code block
-constexpr int kE3Threads = 512;
+constexpr int kE3Threads = 384;
 __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, const uint64_t* coff,
                                                                    const uint32_t* bpre,
                                                                    int ctas_per_field) {
@@ -761,7 +770,7 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
   uint32_t* outw = reinterpret_cast<uint32_t*>(a.arena + mp->payload_off + mp->bits_off);
   const uint64_t* off = coff + (size_t)field * (a.nchunks + 1);
   const uint32_t* bp = bpre + (size_t)field * nb;
-  const uint64_t ow = (reinterpret_cast<uintptr_t>(outw) >> 2) & 3;  // word phase of outw
+  const uint64_t ow = (reinterpret_cast<uintptr_t>(outw) >> 2) & 7;  // word phase of outw
   const int64_t stride = (int64_t)ctas_per_field * blockDim.x;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nb; k += stride) {
     const int64_t s0 = k * kBlk;
@@ -778,18 +787,18 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
     // block before), then buffered 16-byte stores of aligned word quads
     uint64_t widx = B >> 5;
     const uint64_t fo = (B + 31) >> 5;
-    const uint64_t va = ((fo + ow + 3) & ~3ull) - ow;  // first 16-byte aligned owned word
-    uint32_t q0 = 0, q1 = 0, q2 = 0;
+    const uint64_t va = ((fo + ow + 7) & ~7ull) - ow;  // first 32-byte aligned owned word
+    uint32_t q[7] = {0, 0, 0, 0, 0, 0, 0};  // shift register of the pending words
     auto emit = [&](uint32_t w) {
       w = __byte_perm(w, 0, 0x0123);
       if (widx < va) {
         st_pred_u32(outw + widx, w, widx >= fo);
       } else {
-        const uint32_t sl = (uint32_t)(widx + ow) & 3u;
-        q0 = sl == 0 ? w : q0;
-        q1 = sl == 1 ? w : q1;
-        q2 = sl == 2 ? w : q2;
-        st_pred_v4(outw + widx - 3, q0, q1, q2, w, sl == 3);
+        // one 256-bit store per aligned 8-word sector group
+        st_pred_v8(outw + widx - 7, q, w, ((uint32_t)(widx + ow) & 7u) == 7u);
+#pragma unroll
+        for (int u = 0; u < 6; u++) q[u] = q[u + 1];
+        q[6] = w;
       }
       widx++;
     };
@@ -844,10 +853,10 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
     for (int j = 8 * ng; j < mc; j++) put_code(codes[s0 + j], s0 + j);
     // flush buffered words of the last (incomplete) aligned quad
     if (widx > va) {
-      const uint32_t nq = (uint32_t)(widx + ow) & 3u;  // words [widx - nq, widx) pending
-      if (nq > 0) outw[widx - nq] = q0;
-      if (nq > 1) outw[widx - nq + 1] = q1;
-      if (nq > 2) outw[widx - nq + 2] = q2;
+      const uint32_t nq = (uint32_t)(widx + ow) & 7u;  // words [widx - nq, widx) pending
+#pragma unroll
+      for (uint32_t u = 0; u < 7; u++)  // the last nq shift-register slots
+        if (u >= 7 - nq) outw[widx - 7 + u] = q[u];
     }
     // final partial word: completed with the leading bits that follow
     if (nacc > 0 && (Bend >> 5) >= fo) {
