@@ -91,6 +91,8 @@ def lib():
             "orc_sz_decode": (I, [P, I64, I64, D, I64, I, P]),
             "orc_free": (None, [P]),
             "orc_compress": (I, [P, I64, I, P, ctypes.c_uint32, I64, I64, I, I, P, P, P, P]),
+            "orc_compress_v": (I, [P, I64, I, I, P, ctypes.c_uint32, I64, I64, I, I, P, P, P, P]),
+            "orc_build_rindex_n": (I, [P, I, I64, I64, I, P, P, P]),
             "orc_compress_shards": (I64, [P, I64, I, P, ctypes.c_uint32, I64, I64, I, I, I,
                                           I, I, P]),
             "orc_num_threads": (I, []),
@@ -332,10 +334,11 @@ _FIXED = struct.Struct("<4sHBBQIIBBH")
 
 
 def serialize(mode: str, n: int, interval_count: int, segment_size: int, ignored_groups: int,
-              bounds, mask: int, constants, seg_bits, payloads, fmt: int) -> bytes:
+              bounds, mask: int, constants, seg_bits, payloads, fmt: int,
+              variant: int = 0) -> bytes:
     """Container restatement of io.py:105-125; fmt 2 writes version 2 and kind 3."""
     sorted_mode = mode == "sz-lv-prx"
-    variant_uid = 0 if (sorted_mode and n > 0) else 255
+    variant_uid = variant if (sorted_mode and n > 0) else 255
     head = bytearray()
     head += _FIXED.pack(b"NBZ1", fmt, MODE_UIDS[mode], variant_uid, n, interval_count,
                         segment_size, ignored_groups, mask, 0)
@@ -352,8 +355,28 @@ def serialize(mode: str, n: int, interval_count: int, segment_size: int, ignored
     return bytes(head) + b"".join(p for _, p in streams)
 
 
+VARIANTS = {"coord": 0, "vel": 1, "coordvel": 2}
+
+
+def build_rindex_n(cols: Sequence[np.ndarray], segment_size: int, allow_clamp: bool = True):
+    """rindex.build_r_indices for 3 or 6 interleaved fields."""
+    c = [_c(a, np.int64) for a in cols]
+    f, n = len(c), c[0].size
+    nseg = (n + segment_size - 1) // segment_size
+    keys = np.empty(n, np.uint64)
+    bits = np.zeros(max(nseg, 1), np.uint8)
+    minima = np.zeros(f * max(nseg, 1), np.int64)
+    ptrs = (ctypes.c_void_p * f)(*[a.ctypes.data for a in c])
+    st = lib().orc_build_rindex_n(ptrs, f, n, segment_size, int(allow_clamp), _p(keys),
+                                  _p(bits), _p(minima))
+    if st:
+        raise OverflowError("segment needs more index bits than the key budget")
+    return keys, bits[:nseg], minima[:f * nseg].reshape(nseg, f)
+
+
 def compress(fields: Sequence[np.ndarray], mode: str, kinds, values, interval_count: int = 65536,
-             segment_size: int = 16384, ignored_groups: int = 6, fmt: int = 1) -> dict:
+             segment_size: int = 16384, ignored_groups: int = 6, fmt: int = 1,
+             variant: str = "coord") -> dict:
     """Whole-snapshot oracle compress.  fmt 1 reproduces the reference's v1
     archive byte-for-byte; fmt 2 is the dual-quant v2 archive the GPU emits."""
     f32 = [_c(a, np.float32) for a in fields]
@@ -371,9 +394,9 @@ def compress(fields: Sequence[np.ndarray], mode: str, kinds, values, interval_co
     ptrs = (ctypes.c_void_p * 6)(*[a.ctypes.data for a in f32])
     outs = (ctypes.c_void_p * 6)()
     lens = np.zeros(6, np.int64)
-    st = lib().orc_compress(ptrs, n, int(sorted_mode), _p(bounds), mask, interval_count,
-                            segment_size, ignored_groups, fmt, outs, _p(lens), _p(seg_bits),
-                            _p(order) if order is not None else None)
+    st = lib().orc_compress_v(ptrs, n, int(sorted_mode), VARIANTS[variant], _p(bounds), mask,
+                              interval_count, segment_size, ignored_groups, fmt, outs,
+                              _p(lens), _p(seg_bits), _p(order) if order is not None else None)
     payloads: List[Optional[bytes]] = []
     for f in range(6):
         if outs[f]:
@@ -386,7 +409,7 @@ def compress(fields: Sequence[np.ndarray], mode: str, kinds, values, interval_co
     if n == 0:
         payloads = [None] * 6
     wire = serialize(mode, n, interval_count, segment_size, ignored_groups, bounds, mask,
-                     constants, seg_bits[:nseg], payloads, fmt)
+                     constants, seg_bits[:nseg], payloads, fmt, variant=VARIANTS[variant])
     return dict(wire=wire, payloads=payloads, bounds=bounds, constants=constants, mask=mask,
                 seg_bits=seg_bits[:nseg].copy(), order=None if order is None else order[:n],
                 ratio=(24.0 * n / len(wire)) if n else None)

@@ -96,6 +96,42 @@ def dump_case(name: str, fields, modes, ebs, settings=Settings()):
     print(name, len(meta), "tags")
 
 
+def dump_variant_case(name: str, fields, ebs, segment_size: int = 16384, ig: int = 6):
+    """R-index variants (rindex.py:24-44): velocity keys, and six-field
+    coord+velocity keys (group width 6, 10-bit cap), sz-lv-prx."""
+    from nbz.rindex import RIndexVariant
+    snap = ParticleSnapshot(*fields)
+    rec = {f"in_{i}": np.asarray(f, np.float32) for i, f in enumerate(fields)}
+    meta = []
+    for variant in (RIndexVariant.VELOCITY, RIndexVariant.COORD_VELOCITY):
+        settings = Settings(segment_size=segment_size, ignored_groups=ig, rindex_variant=variant)
+        for eb in ebs:
+            tag = f"{variant.value}|{eb:g}"
+            res = compress(snap, Mode.SZ_LV_PRX, ErrorBoundSpec.relative(eb), settings)
+            ar = res.archive
+            wire = ar.serialized()
+            rec[f"{tag}|wire_sha"] = np.array(h(wire))
+            rec[f"{tag}|wire_len"] = np.array(len(wire))
+            rec[f"{tag}|ratio"] = np.array(ratio(ar))
+            rec[f"{tag}|bounds"] = np.array(ar.bounds, np.float64)
+            rec[f"{tag}|mask"] = np.array(ar.constant_mask)
+            rec[f"{tag}|seg_bits"] = np.array([sg.bits for sg in ar.segments], np.uint8)
+            rec[f"{tag}|order_sha"] = np.array(h(res.order.astype(np.int64)))
+            cols = [integerize(snap.field(i), ar.bounds[i]).ints if not ar.is_constant(i)
+                    else np.zeros(ar.n, np.int64) for i in variant.field_indices]
+            keys, segs = build_r_indices(cols, segment_size)
+            rec[f"{tag}|keys_sha"] = np.array(h(keys))
+            out = decompress(ar)
+            for fi in range(6):
+                rec[f"{tag}|recon{fi}_sha"] = np.array(h(out.field(fi)))
+            meta.append(tag)
+    rec["tags"] = np.array(meta)
+    rec["segment_size"] = np.array(segment_size)
+    rec["ignored_groups"] = np.array(ig)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **rec)
+    print(name, len(meta), "tags")
+
+
 def dump_kats():
     rec = {}
     # interleave field-order KATs (test_rindex.py:23-29 style) and a random sweep
@@ -155,6 +191,10 @@ def dump_kats():
 def main():
     os.makedirs(OUT, exist_ok=True)
     K.warmup()
+    if "--variants" in sys.argv:  # only the R-index variant fixtures
+        dump_variant_case("variants_hacc24", D.small_hacc(24), [1e-3, 1e-4])
+        dump_variant_case("variants_amdf20k", D.small_amdf(20000), [1e-4], segment_size=4096, ig=2)
+        return
     dump_kats()
     both = [Mode.SZ_LV, Mode.SZ_LV_PRX]
     dump_case("hacc34", D.small_hacc(34), both, [1e-4])

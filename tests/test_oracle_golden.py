@@ -146,3 +146,31 @@ def test_dual_quant_ratio_within_tolerance(oracle_lib, case):
         for fi in range(6):
             err = np.abs(work[fi].astype(np.float64) - dec[fi].astype(np.float64))
             assert float(err.max()) <= r2["bounds"][fi] or r2["mask"] & (1 << fi)
+
+
+@pytest.mark.parametrize("case", ["variants_hacc24", "variants_amdf20k"])
+def test_oracle_rindex_variants_match_reference(oracle_lib, case):
+    """Velocity and six-field coord+velocity R-index variants (rindex.py:24-44,
+    interleave_any _kernels.py:801-810): keys, seg bits, order and the whole
+    v1 archive byte-identical to the reference's."""
+    O = oracle_lib
+    g = load_golden(case)
+    fields = golden_inputs(g)
+    S, ig = int(g["segment_size"]), int(g["ignored_groups"])
+    fi_of = {"vel": (3, 4, 5), "coordvel": (0, 1, 2, 3, 4, 5)}
+    for tag in g["tags"]:
+        t = str(tag)
+        variant, eb = t.split("|")
+        res = O.compress(fields, "sz-lv-prx", "rel", float(eb), fmt=1, variant=variant,
+                         segment_size=S, ignored_groups=ig)
+        assert np.array_equal(res["seg_bits"], g[f"{t}|seg_bits"]), t
+        assert sha(res["order"].astype(np.int64)) == str(g[f"{t}|order_sha"]), t
+        assert sha(res["wire"]) == str(g[f"{t}|wire_sha"]), t
+        b, mask = g[f"{t}|bounds"], int(g[f"{t}|mask"])
+        cols = [O.integerize(fields[i], b[i]) if not mask & (1 << i)
+                else np.zeros(fields[0].size, np.int64) for i in fi_of[variant]]
+        keys, bits, _ = O.build_rindex_n(cols, S)
+        assert sha(keys) == str(g[f"{t}|keys_sha"]), t
+        dec = O.decompress(res["wire"])
+        for fi in range(6):
+            assert sha(dec[fi]) == str(g[f"{t}|recon{fi}_sha"]), (t, fi)
