@@ -84,7 +84,9 @@ typedef struct nbzg_compress_args {
   int64_t interval_count; /* Settings.interval_count (pipeline.py:79) */
   int64_t segment_size;   /* Settings.segment_size */
   int32_t ignored_groups; /* Settings.ignored_groups */
-  int32_t pad0;
+  int32_t rindex_variant; /* RIndexVariant (rindex.py:24-39): 0 coordinate keys (fields 0-2),
+                             1 velocity keys (3-5), 2 coord+velocity keys (all six,
+                             group width 6, 10-bit cap) */
   void *workspace;        /* nbzg_compress_workspace_size() bytes */
   size_t workspace_bytes;
   uint8_t *arena;         /* nbzg_compress_arena_bound() bytes */

@@ -72,7 +72,7 @@ class Meta(ctypes.Structure):
 class CompressArgs(ctypes.Structure):
     _fields_ = [("fields", c_p * 6), ("n", c_i64), ("sorted", c_i32), ("bound_kind", c_i32 * 6),
                 ("bound_value", c_d * 6), ("interval_count", c_i64), ("segment_size", c_i64),
-                ("ignored_groups", c_i32), ("pad0", c_i32), ("workspace", c_p),
+                ("ignored_groups", c_i32), ("rindex_variant", c_i32), ("workspace", c_p),
                 ("workspace_bytes", c_sz), ("arena", c_p), ("arena_bytes", c_sz),
                 ("meta", c_p), ("seg_bits", c_p), ("perm", c_p)]
 

@@ -209,6 +209,8 @@ int nbzg_compress(const nbzg_compress_args* a, void* stream) {
   Plan p;
   plan_shape(p, a->n, a->sorted, a->interval_count, a->segment_size);
   p.ig = a->ignored_groups;
+  if (a->rindex_variant < 0 || a->rindex_variant > 2) return NBZG_BAD_ARG;
+  p.variant = a->rindex_variant;
   for (int f = 0; f < 6; f++) {
     p.f[f] = a->fields[f];
     p.bound_kind[f] = a->bound_kind[f];

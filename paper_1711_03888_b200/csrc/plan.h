@@ -20,6 +20,7 @@ struct Plan {
   int64_t nbins = 0;    // interval_count (codes 0 .. 2*half-1)
   int half = 0;
   int ig = 6;
+  int variant = 0;      // RIndexVariant: 0 coord, 1 vel, 2 coord+vel
   const float* f[6] = {};
   int bound_kind[6] = {};
   double bound_value[6] = {};

@@ -29,7 +29,8 @@ constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kRadix = 256;
 
 struct RArgs {
-  const float* x[3];
+  const float* x[6];      // key fields (coord / vel: 3, coord+vel: 6)
+  int fbase;              // meta index of x[0] (0, or 3 for the velocity variant)
   int64_t n, S, tile, ntiles;
   int ig;
   const nbzg_meta* meta;
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
   const int64_t t0 = t * a.tile;
   const int64_t t1 = min(a.n, t0 + a.tile);
   const int mt = (int)(t1 - t0);
-  const nbzg_field_meta* fm = a.meta->f;
+  const nbzg_field_meta* fm = a.meta->f + a.fbase;
 
   for (int i = threadIdx.x; i < mt; i += kSortThreads) perm[i] = (uint16_t)i;
 
@@ -279,10 +280,121 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
   for (int i = threadIdx.x; i < mt; i += kSortThreads) a.perm[t0 + i] = perm[i];
 }
 
+// Six-field coord+velocity keys (RIndexVariant.COORD_VELOCITY): group
+// width 6, at most 10 bits per field (max_bits_per_field, rindex.py:42-44),
+// bit j of field t at key bit 6j + 5 - t (interleave_any, _kernels.py:801).
+// Scalar loads and a bit loop: a rarely used variant, kept simple.
+template <typename KeyT>
+__global__ void __launch_bounds__(kSortThreads, 2) rindex_sort6_kernel(RArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  KeyT* keys = reinterpret_cast<KeyT*>(smem);
+  uint16_t* perm = reinterpret_cast<uint16_t*>(keys + kTileMax);
+  uint16_t* whist = perm + kTileMax;
+  __shared__ uint32_t scan_tmp[33];
+  __shared__ float red[2][6][kSortWarps];
+  __shared__ int64_t s_mn[6];
+  __shared__ int s_shift, s_w, s_bits, s_bad;
+
+  const int64_t t = blockIdx.x;
+  if (a.pass == 1 && a.tile_flags[t] == 0) return;
+  const int64_t t0 = t * a.tile;
+  const int64_t t1 = min(a.n, t0 + a.tile);
+  const int mt = (int)(t1 - t0);
+  const nbzg_field_meta* fm = a.meta->f;
+  for (int i = threadIdx.x; i < mt; i += kSortThreads) perm[i] = (uint16_t)i;
+  for (int64_t s0 = t0; s0 < t1; s0 += a.S) {
+    const int lo = (int)(s0 - t0);
+    const int m = (int)(min(t1, s0 + a.S) - s0);
+    float mn[6], mx[6];
+#pragma unroll
+    for (int c = 0; c < 6; c++) {
+      mn[c] = __int_as_float(0x7f800000);
+      mx[c] = -__int_as_float(0x7f800000);
+    }
+    for (int i = threadIdx.x; i < m; i += kSortThreads)
+#pragma unroll
+      for (int c = 0; c < 6; c++) {
+        const float v = a.x[c][s0 + i];
+        mn[c] = fminf(mn[c], v);
+        mx[c] = fmaxf(mx[c], v);
+      }
+#pragma unroll
+    for (int c = 0; c < 6; c++) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        mn[c] = fminf(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
+        mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+      }
+      if ((threadIdx.x & 31) == 0) {
+        red[0][c][threadIdx.x >> 5] = mn[c];
+        red[1][c][threadIdx.x >> 5] = mx[c];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int need = 0, bad = 0;
+      for (int c = 0; c < 6; c++) {
+        float a0 = red[0][c][0], b0 = red[1][c][0];
+        for (int q = 1; q < kSortWarps; q++) {
+          a0 = fminf(a0, red[0][c][q]);
+          b0 = fmaxf(b0, red[1][c][q]);
+        }
+        if (fm[c].is_const) {
+          s_mn[c] = 0;
+          continue;
+        }
+        double qa = __ddiv_rn((double)a0, fm[c].twob), qb = __ddiv_rn((double)b0, fm[c].twob);
+        if (fabs(qa) > kIntLimit || fabs(qb) > kIntLimit) bad = 1;
+        int64_t ia = (int64_t)rint(qa), ib = (int64_t)rint(qb);
+        s_mn[c] = ia;
+        need = max(need, bitlen64((uint64_t)(ib - ia)));
+      }
+      const int cap = 10;
+      const int bits = min(need, cap);
+      const int drop = need > cap ? need - cap : 0;
+      const int eff = min(a.ig, bits);
+      s_bits = bits;
+      s_shift = drop + eff;
+      s_w = bits - eff;
+      s_bad = bad;
+    }
+    __syncthreads();
+    if (s_bad) {
+      if (threadIdx.x == 0) set_status(a.status, NBZG_BOUND_TOO_SMALL);
+      return;
+    }
+    const int w = s_w;
+    if (sizeof(KeyT) == 4 && 6 * w > 32) {
+      if (threadIdx.x == 0) a.tile_flags[t] = 1;
+      return;  // redone by the u64 pass
+    }
+    if (threadIdx.x == 0) a.seg_bits[s0 / a.S] = (uint8_t)s_bits;
+    if (w > 0) {
+      const int shift = s_shift;
+      for (int i = threadIdx.x; i < m; i += kSortThreads) {
+        KeyT key = 0;
+#pragma unroll
+        for (int c = 0; c < 6; c++) {
+          const int64_t iv = fm[c].is_const ? 0 : integerize1(a.x[c][s0 + i], fm[c]);
+          const uint64_t u = (uint64_t)(iv - s_mn[c]) >> shift;
+          for (int j = 0; j < w; j++) key |= (KeyT)((u >> j) & 1u) << (6 * j + 5 - c);
+        }
+        keys[lo + i] = key;
+      }
+      __syncthreads();
+      block_sort_range<KeyT>(keys, perm, lo, m, 6 * w, whist, scan_tmp);
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < mt; i += kSortThreads) a.perm[t0 + i] = perm[i];
+}
+
 int launch_rindex_sort(const Plan& p, cudaStream_t st) {
   if (p.n == 0) return NBZG_OK;
   RArgs a;
-  for (int c = 0; c < 3; c++) a.x[c] = p.f[c];
+  const int nk = p.variant == 2 ? 6 : 3;
+  a.fbase = p.variant == 1 ? 3 : 0;
+  for (int c = 0; c < 6; c++) a.x[c] = c < nk ? p.f[a.fbase + c] : nullptr;
   a.n = p.n;
   a.S = p.S;
   a.tile = p.tile;
@@ -301,15 +413,21 @@ int launch_rindex_sort(const Plan& p, cudaStream_t st) {
                          (int)sm32);
     cudaFuncSetAttribute(rindex_sort_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm64);
+    cudaFuncSetAttribute(rindex_sort6_kernel<uint32_t>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm32);
+    cudaFuncSetAttribute(rindex_sort6_kernel<uint64_t>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm64);
     attr = true;
   }
   cudaMemsetAsync(p.tile_flags, 0, sizeof(uint32_t) * p.ntiles, st);
   a.pass = 0;
   count_launch();
-  rindex_sort_kernel<uint32_t><<<(unsigned)p.ntiles, kSortThreads, sm32, st>>>(a);
+  if (nk == 6) rindex_sort6_kernel<uint32_t><<<(unsigned)p.ntiles, kSortThreads, sm32, st>>>(a);
+  else rindex_sort_kernel<uint32_t><<<(unsigned)p.ntiles, kSortThreads, sm32, st>>>(a);
   a.pass = 1;
   count_launch();
-  rindex_sort_kernel<uint64_t><<<(unsigned)p.ntiles, kSortThreads, sm64, st>>>(a);
+  if (nk == 6) rindex_sort6_kernel<uint64_t><<<(unsigned)p.ntiles, kSortThreads, sm64, st>>>(a);
+  else rindex_sort_kernel<uint64_t><<<(unsigned)p.ntiles, kSortThreads, sm64, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
 

@@ -322,6 +322,8 @@ def device_fields(snapshot: ParticleSnapshot):
 
 
 AUTO = "auto"
+_VARIANT_CODE = {RIndexVariant.COORDINATE: 0, RIndexVariant.VELOCITY: 1,
+                 RIndexVariant.COORD_VELOCITY: 2}
 
 
 def compress(snapshot: ParticleSnapshot, mode, bounds: Bounds,
@@ -350,8 +352,6 @@ def compress(snapshot: ParticleSnapshot, mode, bounds: Bounds,
     if mode not in GPU_MODES:
         raise ValidationError(f"mode {mode.value} is not implemented by the B200 path "
                               f"(supported: sz-lv, sz-lv-prx)")
-    if mode.is_sorted and settings.rindex_variant is not RIndexVariant.COORDINATE:
-        raise ValidationError("the B200 path implements the coordinate r-index variant only")
     specs = _specs(bounds)
     n = snapshot.n
     L = N.lib()
@@ -381,6 +381,7 @@ def compress(snapshot: ParticleSnapshot, mode, bounds: Bounds,
     a.interval_count = ic
     a.segment_size = S
     a.ignored_groups = settings.ignored_groups
+    a.rindex_variant = _VARIANT_CODE[settings.rindex_variant]
     a.workspace = N.ptr(ws)
     a.workspace_bytes = ws.numel()
     a.arena = N.ptr(arena)
