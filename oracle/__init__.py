@@ -38,7 +38,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "_ref", "liboracle.so")
 
-MODE_UIDS = {"sz-lv": 1, "sz-lv-prx": 2}
+MODE_UIDS = {"sz-lcf": 0, "sz-lv": 1, "sz-lv-prx": 2}
 KIND_SZ_FIELD = 0
 KIND_SZ_DQ = 3
 CHUNK_SYMBOLS = 16384
@@ -91,7 +91,10 @@ def lib():
             "orc_sz_decode": (I, [P, I64, I64, D, I64, I, P]),
             "orc_free": (None, [P]),
             "orc_compress": (I, [P, I64, I, P, ctypes.c_uint32, I64, I64, I, I, P, P, P, P]),
-            "orc_compress_v": (I, [P, I64, I, I, P, ctypes.c_uint32, I64, I64, I, I, P, P, P, P]),
+            "orc_compress_v": (I, [P, I64, I, I, I, P, ctypes.c_uint32, I64, I64, I, I, P, P, P, P]),
+            "orc_sz_decode_p": (I, [P, I64, I64, D, I64, I, I, P]),
+            "orc_dq_quantize_p": (I64, [P, I64, D, I64, I64, I, P, P]),
+            "orc_dq_dequantize_p": (I64, [P, I64, P, I64, D, I64, I64, I, P]),
             "orc_build_rindex_n": (I, [P, I, I64, I64, I, P, P, P]),
             "orc_compress_shards": (I64, [P, I64, I, P, ctypes.c_uint32, I64, I64, I, I, I,
                                           I, I, P]),
@@ -316,11 +319,12 @@ def sz_payload(codes: np.ndarray, esc: np.ndarray, interval_count: int, fmt: int
     return data
 
 
-def sz_decode(payload: bytes, n: int, bound: float, interval_count: int, fmt: int) -> np.ndarray:
+def sz_decode(payload: bytes, n: int, bound: float, interval_count: int, fmt: int,
+              lcf: bool = False) -> np.ndarray:
     buf = np.frombuffer(bytes(payload) + b"\0" * 8, np.uint8)
     out = np.zeros(max(n, 1), np.float32)
-    st = lib().orc_sz_decode(_p(buf), len(payload), n, float(bound), interval_count, fmt,
-                             _p(out))
+    st = lib().orc_sz_decode_p(_p(buf), len(payload), n, float(bound), interval_count, fmt,
+                               int(lcf), _p(out))
     if st:
         raise ValueError(ORC_STATUS.get(st, str(st)))
     return out[:n]
@@ -394,7 +398,8 @@ def compress(fields: Sequence[np.ndarray], mode: str, kinds, values, interval_co
     ptrs = (ctypes.c_void_p * 6)(*[a.ctypes.data for a in f32])
     outs = (ctypes.c_void_p * 6)()
     lens = np.zeros(6, np.int64)
-    st = lib().orc_compress_v(ptrs, n, int(sorted_mode), VARIANTS[variant], _p(bounds), mask,
+    st = lib().orc_compress_v(ptrs, n, int(sorted_mode), VARIANTS[variant],
+                              int(mode == "sz-lcf"), _p(bounds), mask,
                               interval_count, segment_size, ignored_groups, fmt, outs,
                               _p(lens), _p(seg_bits), _p(order) if order is not None else None)
     payloads: List[Optional[bytes]] = []
@@ -449,7 +454,8 @@ def decompress(wire: bytes) -> List[np.ndarray]:
             out.append(np.zeros(0, np.float32))
         else:
             fmt = 1 if a["kinds"][f] == KIND_SZ_FIELD else 2
-            out.append(sz_decode(a["payloads"][f], n, a["bounds"][f], a["interval_count"], fmt))
+            out.append(sz_decode(a["payloads"][f], n, a["bounds"][f], a["interval_count"], fmt,
+                                 lcf=a["mode_uid"] == 0))
     return out
 
 

@@ -132,6 +132,33 @@ def dump_variant_case(name: str, fields, ebs, segment_size: int = 16384, ig: int
     print(name, len(meta), "tags")
 
 
+def dump_lcf_case(name: str, fields, ebs):
+    """sz-lcf (mode uid 0): the LCF predictor pred = 2*prev - prev2
+    (_kernels.py:162-165), no R-index."""
+    snap = ParticleSnapshot(*fields)
+    rec = {f"in_{i}": np.asarray(f, np.float32) for i, f in enumerate(fields)}
+    meta = []
+    for eb in ebs:
+        tag = f"sz-lcf|{eb:g}"
+        res = compress(snap, Mode.SZ_LCF, ErrorBoundSpec.relative(eb))
+        ar = res.archive
+        wire = ar.serialized()
+        rec[f"{tag}|wire_sha"] = np.array(h(wire))
+        rec[f"{tag}|wire_len"] = np.array(len(wire))
+        rec[f"{tag}|ratio"] = np.array(ratio(ar))
+        rec[f"{tag}|bounds"] = np.array(ar.bounds, np.float64)
+        rec[f"{tag}|mask"] = np.array(ar.constant_mask)
+        for st in ar.streams:
+            rec[f"{tag}|payload{st.field}_sha"] = np.array(h(st.payload))
+        out = decompress(ar)
+        for fi in range(6):
+            rec[f"{tag}|recon{fi}_sha"] = np.array(h(out.field(fi)))
+        meta.append(tag)
+    rec["tags"] = np.array(meta)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **rec)
+    print(name, len(meta), "tags")
+
+
 def dump_kats():
     rec = {}
     # interleave field-order KATs (test_rindex.py:23-29 style) and a random sweep
@@ -191,6 +218,13 @@ def dump_kats():
 def main():
     os.makedirs(OUT, exist_ok=True)
     K.warmup()
+    if "--lcf" in sys.argv:  # only the sz-lcf fixtures
+        dump_lcf_case("lcf_hacc24", D.small_hacc(24), [1e-3, 1e-4])
+        rng = np.random.default_rng(11)
+        noise = [rng.uniform(0, 100, 20000).astype(np.float32) for _ in range(3)]
+        noise += [(rng.standard_cauchy(20000) * 10).astype(np.float32) for _ in range(3)]
+        dump_lcf_case("lcf_noise20k", noise, [1e-4, 1e-6])
+        return
     if "--variants" in sys.argv:  # only the R-index variant fixtures
         dump_variant_case("variants_hacc24", D.small_hacc(24), [1e-3, 1e-4])
         dump_variant_case("variants_amdf20k", D.small_amdf(20000), [1e-4], segment_size=4096, ig=2)

@@ -174,3 +174,34 @@ def test_oracle_rindex_variants_match_reference(oracle_lib, case):
         dec = O.decompress(res["wire"])
         for fi in range(6):
             assert sha(dec[fi]) == str(g[f"{t}|recon{fi}_sha"]), (t, fi)
+
+
+@pytest.mark.parametrize("case", ["lcf_hacc24", "lcf_noise20k"])
+def test_oracle_lcf_matches_reference(oracle_lib, case):
+    """sz-lcf (LCF predictor pred = 2*prev - prev2, _kernels.py:162-165):
+    v1 archives and decoded values byte-identical to the reference; the v2
+    dual-quant restatement within bound and within 0.5% of its ratio."""
+    O = oracle_lib
+    g = load_golden(case)
+    fields = golden_inputs(g)
+    for tag in g["tags"]:
+        t = str(tag)
+        eb = float(t.split("|")[1])
+        res = O.compress(fields, "sz-lcf", "rel", eb, fmt=1)
+        assert np.array_equal(res["bounds"], g[f"{t}|bounds"]), t
+        for fi in range(6):
+            key = f"{t}|payload{fi}_sha"
+            if key in g:
+                assert sha(res["payloads"][fi]) == str(g[key]), (t, fi)
+        assert sha(res["wire"]) == str(g[f"{t}|wire_sha"]), t
+        dec = O.decompress(res["wire"])
+        for fi in range(6):
+            assert sha(dec[fi]) == str(g[f"{t}|recon{fi}_sha"]), (t, fi)
+        r2 = O.compress(fields, "sz-lcf", "rel", eb, fmt=2)
+        # compressed size never more than 0.5% above the reference's (on
+        # escape-heavy noise the dual-quant LCF chain is smaller)
+        assert r2["ratio"] >= float(g[f"{t}|ratio"]) * (1 - 0.005), (t, r2["ratio"])
+        d2 = O.decompress(r2["wire"])
+        for fi in range(6):
+            err = np.abs(fields[fi].astype(np.float64) - d2[fi].astype(np.float64))
+            assert float(err.max()) <= r2["bounds"][fi] or r2["mask"] & (1 << fi)
