@@ -28,6 +28,8 @@
 extern "C" {
 #endif
 
+enum { NBZG_KIND_LCF = 16 };
+
 enum {
   NBZG_OK = 0,
   NBZG_BOUND_TOO_SMALL = 1, /* quantize.py:123-126 -> BoundTooSmallError */
@@ -94,6 +96,9 @@ typedef struct nbzg_compress_args {
   nbzg_meta *meta;        /* device */
   uint8_t *seg_bits;      /* device, ceil(n/segment_size) bytes (sorted) */
   uint16_t *perm;         /* device, n entries (sorted) */
+  int32_t predictor;      /* 0 = last value (sz-lv, sz-lv-prx), 1 = LCF 2*prev - prev2
+                             (Mode.SZ_LCF, _kernels.py:162-165; unsorted only) */
+  int32_t pad1;
 } nbzg_compress_args;
 
 size_t nbzg_compress_workspace_size(int64_t n, int32_t sorted, int64_t interval_count,
@@ -105,8 +110,9 @@ int nbzg_compress(const nbzg_compress_args *args, void *stream);
  * Replaces pipeline._parse_sz_stream (pipeline.py:203-223) ->
  * encode.huffman_decode (encode.py:242-261) -> K.huff_decode
  * (_kernels.py:348-374) -> quantize.dequantize_field -> K.sz_dequantize
- * (_kernels.py:126-147).  kind 3 = SZ_DQ (v2, chunk-parallel); kind 0 =
- * SZ_FIELD (v1 reference streams, exact sequential chain, compat path).
+ * (_kernels.py:126-147).  kind: 3 = SZ_DQ (v2, chunk-parallel), 0 = SZ_FIELD
+ * (v1 reference streams, exact sequential chain); + NBZG_KIND_LCF (16) when the
+ * archive's mode is sz-lcf (LCF predictor instead of last value).
  * payload: device bytes, any alignment, readable for payload_len + 64 bytes.
  * status: device u32, receives the first failure (NBZG_*). */
 typedef struct nbzg_decompress_args {

@@ -74,7 +74,8 @@ class CompressArgs(ctypes.Structure):
                 ("bound_value", c_d * 6), ("interval_count", c_i64), ("segment_size", c_i64),
                 ("ignored_groups", c_i32), ("rindex_variant", c_i32), ("workspace", c_p),
                 ("workspace_bytes", c_sz), ("arena", c_p), ("arena_bytes", c_sz),
-                ("meta", c_p), ("seg_bits", c_p), ("perm", c_p)]
+                ("meta", c_p), ("seg_bits", c_p), ("perm", c_p), ("predictor", c_i32),
+                ("pad1", c_i32)]
 
 
 class DecompressArgs(ctypes.Structure):

@@ -211,6 +211,9 @@ int nbzg_compress(const nbzg_compress_args* a, void* stream) {
   p.ig = a->ignored_groups;
   if (a->rindex_variant < 0 || a->rindex_variant > 2) return NBZG_BAD_ARG;
   p.variant = a->rindex_variant;
+  if (a->predictor < 0 || a->predictor > 1 || (a->predictor == 1 && a->sorted))
+    return NBZG_UNSUPPORTED;
+  p.predictor = a->predictor;
   for (int f = 0; f < 6; f++) {
     p.f[f] = a->fields[f];
     p.bound_kind[f] = a->bound_kind[f];
@@ -257,7 +260,8 @@ int nbzg_decompress(const nbzg_decompress_args* a, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   DField f[6];
   for (int i = 0; i < a->nfields; i++) {
-    if (a->kind[i] != 0 && a->kind[i] != 3) return NBZG_BAD_ARG;
+    const int kb = a->kind[i] & ~NBZG_KIND_LCF;
+    if ((kb != 0 && kb != 3) || (a->kind[i] & ~(NBZG_KIND_LCF | 15))) return NBZG_BAD_ARG;
     if (!(a->bound[i] > 0)) return NBZG_BAD_ARG;
     f[i].payload = a->payload[i];
     f[i].payload_len = a->payload_len[i];

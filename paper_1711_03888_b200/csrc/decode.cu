@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
     const uint8_t* e = p + 8 + 5 * i;
     uint32_t s = ld_u32_bytes(e), l = e[4];
     // v1 codes span [0, interval_count]; v2 codes [0, interval_count-1]
-    bool bad = l < 1 || l > kMaxCodeLen || s >= (uint64_t)a.nbins - (F.kind == 3 ? 1 : 0);
+    bool bad = l < 1 || l > kMaxCodeLen || s >= (uint64_t)a.nbins - ((F.kind & 15) == 3 ? 1 : 0);
     if (i > 0 && ld_u32_bytes(e - 5) >= s) bad = true;
     if (bad) atomicOr(&s_bad, 1u);
     else {
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
   // sym - bias.  Primary: 15-bit prefix, codes <= 15 bits.  Secondary: the
   // canonical tail (32-bit window value >= R0, i.e. codes > 15 bits) at W-bit
   // resolution, W <= 24 chosen so the tail fits kTpc2Cap entries.
-  if (F.kind == 3) {
+  if ((F.kind & 15) == 3) {
     int32_t* lut2 = a.lut2 + (size_t)fi * kTpcTab;
     const int bias = a.half + 1;
     auto entry = [&](int l, uint64_t u) -> int32_t {  // u: 32-bit window value
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
     if (table_end + 8 > (uint64_t)L) st = NBZG_TRUNCATED;
     else {
       P.total_bits = ld_u64_bytes(p + table_end);
-      if (F.kind == 3) {  // escapes inline: the bitstream ends the payload
+      if ((F.kind & 15) == 3) {  // escapes inline: the bitstream ends the payload
         P.index_off = table_end + 8;
         P.bits_off = (P.index_off + 4 * (uint64_t)a.nchunks + 3) & ~3ull;
         P.esc_off = P.bits_off + 4 * ((P.total_bits + 31) / 32);
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
 __global__ void __launch_bounds__(1024) chunk_offsets_kernel(DArgs a) {
   const int fi = blockIdx.x;
   const DParsed& P = a.parsed[fi];
-  if (P.status || a.f[fi].kind != 3) return;
+  if (P.status || (a.f[fi].kind & 15) != 3) return;
   __shared__ unsigned long long scan_tmp[33];
   const uint8_t* idx = a.f[fi].payload + P.index_off;
   uint64_t* off = a.choff + fi * (a.nchunks + 1);
@@ -775,6 +775,38 @@ NBZG_DEV void tpc_refill(TpcReader& R, uint32_t* ring, int nthr, const uint4* G,
   ldg_v4_if(R.qs, G + min(R.wr >> 2, vmax), room);
 }
 
+// Lattice-index state of one chunk.  LV: k_i = k_{i-1} + q_i, kept in FP64
+// (exact: |k| <= 2^52).  LCF (sz-lcf): k_i = q_i + 2 k_{i-1} - k_{i-2} with
+// pred_1 = k_0 (both history slots hold k_0 after the first symbol), int64.
+template <bool LCF>
+struct KState;
+template <>
+struct KState<false> {
+  double kd = 0.0;
+  NBZG_DEV float apply(int32_t q, double twob) {
+    kd += (double)q;
+    return (float)__dmul_rn(kd, twob);
+  }
+  NBZG_DEV void escape(long long k) { kd = (double)k; }
+};
+template <>
+struct KState<true> {
+  long long k1 = 0, k2 = 0;
+  bool first = true;
+  NBZG_DEV void push(long long k) {
+    k2 = first ? k : k1;
+    k1 = k;
+    first = false;
+  }
+  NBZG_DEV float apply(int32_t q, double twob) {
+    const long long k = (long long)q + 2 * k1 - k2;
+    push(k);
+    return (float)__dmul_rn((double)k, twob);
+  }
+  NBZG_DEV void escape(long long k) { push(k); }
+};
+
+template <bool LCF>
 __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, int ctas_per_field) {
   extern __shared__ __align__(16) uint8_t dsm2[];
   int32_t* LT = reinterpret_cast<int32_t*>(dsm2);  // [2^15 + t2_n]
@@ -783,7 +815,7 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, 
   const int fi = blockIdx.y;
   const DField& F = a.f[fi];
   const DParsed& P = a.parsed[fi];
-  if (F.kind != 3 || P.status || *a.status || P.max_len > 32) return;
+  if (F.kind != (LCF ? 3 + NBZG_KIND_LCF : 3) || P.status || *a.status || P.max_len > 32) return;
   const int64_t cb = (a.nchunks * blockIdx.x) / ctas_per_field;
   const int64_t ce = (a.nchunks * (blockIdx.x + 1)) / ctas_per_field;
   if (cb >= ce) return;
@@ -835,7 +867,7 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, 
     const uint64_t B = a0 + b0;
     TpcReader R;
     tpc_init(R, G, ring, nthr, B, vmax);
-    double kd = 0.0;
+    KState<LCF> ks;
     int err = 0;
     float* dst = F.out + i0;
     // bits consumed so far
@@ -869,11 +901,10 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, 
       if (e & 64) {
         tpc_skip(R, l, ring, nthr, G32, wmax, tpc_next(R, ring, nthr));
         o = __uint_as_float(__funnelshift_l(R.w1, R.w0, R.off));
-        kd = (double)esc_k(o, F);
+        ks.escape(esc_k(o, F));
         tpc_skip(R, 32, ring, nthr, G32, wmax, tpc_next(R, ring, nthr));
       } else {
-        kd += (double)(e >> 7);
-        o = (float)__dmul_rn(kd, twob);
+        o = ks.apply(e >> 7, twob);
         tpc_skip(R, l, ring, nthr, G32, wmax, tpc_next(R, ring, nthr));
       }
     };
@@ -891,8 +922,7 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, 
         safe_step(o);
         return;
       }
-      kd += (double)(e >> 7);
-      o = (float)__dmul_rn(kd, twob);
+      o = ks.apply(e >> 7, twob);
       R.off += (uint32_t)e & 63u;
       const bool cross = R.off >= 32;
       R.w0 = cross ? R.w1 : R.w0;
@@ -903,13 +933,13 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, 
     // 8 symbols; replayed exactly if any window word came from past the ring
     auto group = [&](float (&o)[8]) {
       const TpcReader S = R;
-      const double kd0 = kd;
+      const KState<LCF> ks0 = ks;
 #pragma unroll
       for (int q = 0; q < 8; q++) fast_step(o[q]);
       // the largest word index read in the group is the final wi
       if ((int32_t)(R.wr - R.wi) <= 0) {
         R = S;
-        kd = kd0;
+        ks = ks0;
 #pragma unroll 1
         for (int q = 0; q < 8; q++) {
           float t;
@@ -954,11 +984,18 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, 
 
 // v2 streams with codes longer than 32 bits (pathological alphabets):
 // serial decode per chunk (one thread per chunk), same semantics.
+template <bool LCF>
+__device__ void decode_v2_serial_body(const DArgs& a, const DField& F, const DParsed& P, int fi);
 __global__ void decode_v2_serial_kernel(DArgs a) {
   const int fi = blockIdx.y;
   const DField& F = a.f[fi];
   const DParsed& P = a.parsed[fi];
-  if (F.kind != 3 || P.status || P.max_len <= 32) return;
+  if ((F.kind & 15) != 3 || P.status || P.max_len <= 32) return;
+  if (F.kind & NBZG_KIND_LCF) decode_v2_serial_body<true>(a, F, P, fi);
+  else decode_v2_serial_body<false>(a, F, P, fi);
+}
+template <bool LCF>
+__device__ void decode_v2_serial_body(const DArgs& a, const DField& F, const DParsed& P, int fi) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= a.nchunks) return;
   const uint64_t* choff = a.choff + fi * (a.nchunks + 1);
@@ -966,7 +1003,7 @@ __global__ void decode_v2_serial_kernel(DArgs a) {
   uint64_t bp = choff[c], endp = choff[c + 1];
   const uint32_t* ss = a.ssyms + fi * a.nbins;
   const int64_t c0 = c * kChunk, c1 = min(a.n, c0 + kChunk);
-  long long k = 0;
+  KState<LCF> ks;
   for (int64_t i = c0; i < c1; i++) {
     uint32_t sym = 0;
     int l = decode_serial(bits, bp, endp, P, ss, sym);
@@ -983,10 +1020,9 @@ __global__ void decode_v2_serial_kernel(DArgs a) {
       uint32_t u = 0;
       for (int b = 0; b < 32; b++, bp++) u = (u << 1) | ((bits[bp >> 3] >> (7 - (bp & 7))) & 1u);
       outv = __uint_as_float(u);
-      k = esc_k(outv, F);
+      ks.escape(esc_k(outv, F));
     } else {
-      k += (long long)((int)sym - a.half - 1);
-      outv = (float)__dmul_rn((double)k, F.twob);
+      outv = ks.apply((int)sym - a.half - 1, F.twob);
     }
     F.out[i] = outv;
   }
@@ -1000,13 +1036,14 @@ __global__ void decode_v1_kernel(DArgs a) {
   const int fi = blockIdx.x;
   const DField& F = a.f[fi];
   const DParsed& P = a.parsed[fi];
-  if (F.kind != 0 || P.status || threadIdx.x != 0) return;
+  if ((F.kind & 15) != 0 || P.status || threadIdx.x != 0) return;
+  const bool lcf = F.kind & NBZG_KIND_LCF;  // sz-lcf: pred = 2*h1 - h2 from i = 2
   const uint8_t* bits = F.payload + P.bits_off;
   const uint8_t* escp = F.payload + P.esc_off;
   const uint32_t* ss = a.ssyms + fi * a.nbins;
   const int half = a.half;
   uint64_t bp = 0, ei = 0;
-  double h1 = 0.0;
+  double h1 = 0.0, h2 = 0.0;
   for (int64_t i = 0; i < a.n; i++) {
     uint32_t sym = 0;
     int l = decode_serial(bits, bp, P.total_bits, P, ss, sym);
@@ -1023,11 +1060,12 @@ __global__ void decode_v1_kernel(DArgs a) {
       r = __uint_as_float(ld_u32_bytes(escp + 4 * ei));
       ei++;
     } else {
-      double pred = i == 0 ? 0.0 : h1;
+      double pred = i == 0 ? 0.0 : (lcf && i >= 2 ? __dsub_rn(2.0 * h1, h2) : h1);
       double q = (double)((int)sym - half - 1);
       r = (float)__dadd_rn(pred, __dmul_rn(q, F.twob));
     }
     F.out[i] = r;
+    h2 = h1;
     h1 = (double)r;
   }
   if (ei != P.n_esc) fail(a.status, NBZG_BAD_STREAM);
@@ -1102,26 +1140,34 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
                          (int)sm);
     attr = true;
   }
-  bool any_v2 = false, any_v1 = false;
+  bool any_v2 = false, any_v2_lcf = false, any_v1 = false;
   for (int i = 0; i < nf; i++) {
-    any_v2 |= fields[i].kind == 3;
-    any_v1 |= fields[i].kind == 0;
+    any_v2 |= (fields[i].kind & 15) == 3;
+    any_v2_lcf |= fields[i].kind == 3 + NBZG_KIND_LCF;
+    any_v1 |= (fields[i].kind & 15) == 0;
   }
   if (any_v2) {
     int groups = max(1, sm_count() / nf);
     if (groups > a.nchunks) groups = (int)a.nchunks;
-    if (use_tpc(a.nchunks)) {
-      const int per = (int)((a.nchunks + groups - 1) / groups);
-      const int thr = min(kTpcMaxThreads, (per + 31) / 32 * 32);
-      const size_t sm2 = 4 * kTpcTab + 32 * (size_t)thr;
-      static bool attr2 = false;
-      if (!attr2) {
-        cudaFuncSetAttribute(decode_tpc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sm2);
-        attr2 = true;
-      }
+    const int per = (int)((a.nchunks + groups - 1) / groups);
+    const int thr = min(kTpcMaxThreads, (per + 31) / 32 * 32);
+    const size_t sm2 = 4 * kTpcTab + 32 * (size_t)thr;
+    static bool attr2 = false;
+    if (!attr2) {  // sized for the largest launch
+      const int smax = 4 * kTpcTab + 32 * kTpcMaxThreads;
+      cudaFuncSetAttribute(decode_tpc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           smax);
+      cudaFuncSetAttribute(decode_tpc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           smax);
+      attr2 = true;
+    }
+    if (any_v2_lcf) {  // sz-lcf streams: thread-per-chunk decoder only
       count_launch();
-      decode_tpc_kernel<<<dim3(groups, nf), thr, sm2, st>>>(a, groups);
+      decode_tpc_kernel<true><<<dim3(groups, nf), thr, sm2, st>>>(a, groups);
+    }
+    if (use_tpc(a.nchunks)) {
+      count_launch();
+      decode_tpc_kernel<false><<<dim3(groups, nf), thr, sm2, st>>>(a, groups);
     } else {
       count_launch();
       decode_kernel<true><<<groups * nf, kDThreads, sm, st>>>(a);

@@ -21,6 +21,7 @@ struct Plan {
   int half = 0;
   int ig = 6;
   int variant = 0;      // RIndexVariant: 0 coord, 1 vel, 2 coord+vel
+  int predictor = 0;    // 0 last value, 1 LCF (sz-lcf)
   const float* f[6] = {};
   int bound_kind[6] = {};
   double bound_value[6] = {};

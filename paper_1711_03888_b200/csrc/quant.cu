@@ -289,6 +289,75 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
   }
 }
 
+// ---- sz-lcf (Mode.SZ_LCF, unsorted): LCF predictor on lattice indices,
+// pred_0 = 0, pred_1 = k_0, pred_i = 2 k_{i-1} - k_{i-2} (chunk-relative i;
+// _kernels.py:162-165 restated for dual quantisation).  Each thread takes
+// 16 consecutive positions and recomputes the two lattice indices before
+// them, so threads are independent.  (Not on the benchmarked path: kept
+// simple, no TMA staging.)
+constexpr int kQLThreads = 512;
+__global__ void __launch_bounds__(kQLThreads) quantize_lcf_kernel(QArgs a) {
+  __shared__ uint32_t hw[kQWin];
+  const int field = blockIdx.y;
+  const nbzg_field_meta& fm = a.meta->f[field];
+  if (fm.is_const || a.n == 0 || a.meta->status) return;
+  const float* __restrict__ x = a.f[field];
+  uint16_t* __restrict__ codes = a.codes + field * a.code_stride;
+  uint32_t* __restrict__ hist = a.hist + field * a.nbins;
+  const int half = a.half;
+  const int wlo = half + 1 - kQWin / 2;
+  const double b = fm.bound, twob = fm.twob;
+  const float inv32 = fm.inv32;
+  for (int i = threadIdx.x; i < kQWin; i += kQLThreads) hw[i] = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * kQLThreads * 16;
+  for (int64_t base = ((int64_t)blockIdx.x * kQLThreads + threadIdx.x) * 16; base < a.n;
+       base += stride) {
+    const int ic0 = (int)(base & (kChunk - 1));
+    int64_t k1 = 0, k2 = 0;
+    bool f;
+    if (ic0 >= 1) k1 = dq_index_fast(x[base - 1], inv32, fm, f);
+    if (ic0 >= 2) k2 = dq_index_fast(x[base - 2], inv32, fm, f);
+    if (ic0 == 1) k2 = k1;  // pred_1 = k_0 = 2 k_0 - k_0
+    const int cnt = (int)min((int64_t)16, a.n - base);
+    uint32_t packed[8];
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      uint32_t code = 0;
+      if (j < cnt) {
+        const float xv = x[base + j];
+        bool fast;
+        const int64_t k = dq_index_fast(xv, inv32, fm, fast);
+        const int64_t q = k - (2 * k1 - k2);
+        bool ok = (uint64_t)(q + half) <= (uint64_t)(2 * half - 2);
+        if (ok && !fast) ok = fabs((double)xv - (double)(float)__dmul_rn((double)k, twob)) <= b;
+        code = ok ? (uint32_t)(q + half + 1) : 0u;
+        k2 = (ic0 + j == 0) ? k : k1;  // after position 0 both hold k_0
+        k1 = k;
+        const uint32_t wb = code - (uint32_t)wlo;
+        if (wb < (uint32_t)kQWin) atomicAdd(&hw[wb], 1u);
+        else atomicAdd(&hist[code], 1u);
+      }
+      if (j & 1) packed[j >> 1] |= code << 16;
+      else packed[j >> 1] = code;
+    }
+    uint16_t* dst = codes + base;
+    if (cnt == 16) {
+      uint4* d4 = reinterpret_cast<uint4*>(dst);
+      d4[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      d4[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+    } else {
+      for (int j = 0; j < cnt; j++) dst[j] = (uint16_t)(packed[j >> 1] >> ((j & 1) * 16));
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kQWin; i += kQLThreads) {
+    const uint32_t c = hw[i];
+    const int code = wlo + i;
+    if (c && code >= 0 && code < (int)a.nbins) atomicAdd(&hist[code], c);
+  }
+}
+
 int launch_quantize(const Plan& p, cudaStream_t st) {
   if (p.n == 0) return NBZG_OK;
   QArgs a;
@@ -319,8 +388,15 @@ int launch_quantize(const Plan& p, cudaStream_t st) {
     attr = true;
   }
   count_launch();
-  if (p.sorted) quantize_kernel<true><<<6 * per_field, kQThreads, sm, st>>>(a);
-  else quantize_kernel<false><<<6 * per_field, kQThreads, sm, st>>>(a);
+  if (p.predictor == 1) {
+    const int64_t per_cta = (int64_t)kQLThreads * 16;
+    int blocks = (int)min((p.n + per_cta - 1) / per_cta, (int64_t)(4 * sm_count() / 6 + 1));
+    quantize_lcf_kernel<<<dim3(blocks, 6), kQLThreads, 0, st>>>(a);
+  } else if (p.sorted) {
+    quantize_kernel<true><<<6 * per_field, kQThreads, sm, st>>>(a);
+  } else {
+    quantize_kernel<false><<<6 * per_field, kQThreads, sm, st>>>(a);
+  }
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
 

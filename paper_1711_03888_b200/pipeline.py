@@ -74,7 +74,8 @@ _MODE_UIDS = {Mode.SZ_LCF: 0, Mode.SZ_LV: 1, Mode.SZ_LV_PRX: 2,
 MODE_ALIASES = {"best-speed": Mode.SZ_LV, "best-tradeoff": Mode.SZ_LV_PRX,
                 "best-compression": Mode.SZ_CPC2000}
 
-GPU_MODES = (Mode.SZ_LV, Mode.SZ_LV_PRX)
+GPU_MODES = (Mode.SZ_LCF, Mode.SZ_LV, Mode.SZ_LV_PRX)
+_KIND_LCF = 16  # NBZG_KIND_LCF: the stream's field uses the LCF predictor (mode sz-lcf)
 
 
 @dataclass(frozen=True)
@@ -351,7 +352,7 @@ def compress(snapshot: ParticleSnapshot, mode, bounds: Bounds,
     mode = _as_mode(mode)
     if mode not in GPU_MODES:
         raise ValidationError(f"mode {mode.value} is not implemented by the B200 path "
-                              f"(supported: sz-lv, sz-lv-prx)")
+                              f"(supported: sz-lcf, sz-lv, sz-lv-prx)")
     specs = _specs(bounds)
     n = snapshot.n
     L = N.lib()
@@ -382,6 +383,7 @@ def compress(snapshot: ParticleSnapshot, mode, bounds: Bounds,
     a.segment_size = S
     a.ignored_groups = settings.ignored_groups
     a.rindex_variant = _VARIANT_CODE[settings.rindex_variant]
+    a.predictor = 1 if mode is Mode.SZ_LCF else 0
     a.workspace = N.ptr(ws)
     a.workspace_bytes = ws.numel()
     a.arena = N.ptr(arena)
@@ -472,6 +474,8 @@ def decompress(archive: Archive, device: Optional[bool] = None) -> ParticleSnaps
         a.payload[nf] = base + d.offsets[fi]
         a.payload_len[nf] = d.lengths[fi]
         a.kind[nf] = _KIND_CODE.get(StreamKind(d.kinds[fi]), -1)
+        if a.kind[nf] >= 0 and archive.mode is Mode.SZ_LCF:
+            a.kind[nf] += _KIND_LCF
         if a.kind[nf] < 0:
             raise DecodeError("unsupported stream kind")
         a.bound[nf] = archive.bounds[fi]

@@ -336,7 +336,7 @@ def test_bound_too_small_raises():
 
 def test_unsupported_modes_raise():
     snap = nbz.ParticleSnapshot(*datagen.small_hacc(5))
-    for mode in ("sz-lcf", "cpc2000", "sz-cpc2000"):
+    for mode in ("cpc2000", "sz-cpc2000"):
         with pytest.raises(nbz.ValidationError):
             nbz.compress(snap, mode, REL4)
 
@@ -501,3 +501,48 @@ def test_rindex_variants_byte_identical(O, case):
         # and the archive round-trips through the container
         from paper_1711_03888_b200 import io as nio
         assert nio.deserialize_archive(ref["wire"]).rindex_variant is names[variant]
+
+
+
+@pytest.mark.parametrize("case", ["hacc34", "amdf40k", "noise20k", "lcf_hacc24", "lcf_noise20k"])
+def test_sz_lcf_byte_identical_and_reference_v1_decode(O, case):
+    """sz-lcf (LCF predictor, f4): GPU v2 archives byte-identical to the
+    oracle's; the reference's own v1 sz-lcf archives (reproduced byte for
+    byte by the pinned oracle) decode on the GPU to the reference's values."""
+    g = load_golden(case)
+    fields = golden_inputs(g)
+    snap = nbz.ParticleSnapshot(*fields)
+    for eb in (1e-4, 1e-6):
+        res = nbz.compress(snap, "sz-lcf", nbz.ErrorBoundSpec.relative(eb))
+        ref = O.compress(fields, "sz-lcf", "rel", eb, fmt=2)
+        assert res.archive.serialized() == ref["wire"], (case, eb)
+        rec = nbz.decompress(res.archive)
+        odec = O.decompress(ref["wire"])
+        for fi in range(6):
+            got = np.asarray(rec.field(fi))
+            assert np.array_equal(got, odec[fi]), (case, eb, fi)
+            err = np.abs(fields[fi].astype(np.float64) - got.astype(np.float64))
+            lim = res.archive.bounds[fi] if not res.archive.is_constant(fi) else 0.0
+            assert float(err.max(initial=0.0)) <= lim
+    if case.startswith("lcf_"):
+        from paper_1711_03888_b200 import io as nio
+        for tag in g["tags"]:
+            t = str(tag)
+            v1 = O.compress(fields, "sz-lcf", "rel", float(t.split("|")[1]), fmt=1)["wire"]
+            assert sha(v1) == str(g[f"{t}|wire_sha"])
+            out = nbz.decompress(nio.deserialize_archive(v1))
+            for fi in range(6):
+                assert sha(np.asarray(out.field(fi))) == str(g[f"{t}|recon{fi}_sha"]), (t, fi)
+
+
+def test_sz_lcf_multichunk(O):
+    """sz-lcf over many chunks (chain restart at every 16384 symbols)."""
+    fields = datagen.generate("C1")
+    snap = nbz.ParticleSnapshot(*fields)
+    res = nbz.compress(snap, "sz-lcf", REL4)
+    ref = O.compress(fields, "sz-lcf", "rel", 1e-4, fmt=2)
+    assert res.archive.serialized() == ref["wire"]
+    rec = nbz.decompress(res.archive, device=True)
+    for fi in range(6):
+        err = (torch.from_numpy(fields[fi]).cuda().double() - rec.field(fi).double()).abs().max()
+        assert float(err) <= res.archive.bounds[fi]
