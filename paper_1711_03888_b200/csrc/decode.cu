@@ -35,8 +35,9 @@ constexpr int kDThreads = kDWarps * 32;
 constexpr int kLutBits = 16;       // code-length table index bits (u8 entries, 64 KiB)
 constexpr int kSmemSyms = 16384;   // sorted-symbol table staged in smem up to this k
 constexpr int kTpcBits = 15;       // thread-per-chunk fused table index bits (i32, 128 KiB)
-constexpr int kTpc2Cap = 19456;    // secondary (long-code) table entries (76 KiB)
-constexpr int kTpcMaxThreads = 704;  // smem: 128 KiB + 76 KiB tables + 32 B ring per thread
+constexpr int kTpc2Cap = 16384;    // secondary (long-code) table entries (64 KiB)
+constexpr int kTpcMaxThreads = 704;
+constexpr int kRingStride = 1024;  // words between ring slots (power of two, >= threads)
 constexpr int kTpcTab = (1 << kTpcBits) + kTpc2Cap;
 
 struct DParsed {
@@ -820,7 +821,7 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, 
   const int64_t ce = (a.nchunks * (blockIdx.x + 1)) / ctas_per_field;
   if (cb >= ce) return;
   const int tid = threadIdx.x, nthr = blockDim.x;
-  uint32_t* ring = reinterpret_cast<uint32_t*>(dsm2 + 4 * kTpcTab) + tid;  // [8][nthr]
+  uint32_t* ring = reinterpret_cast<uint32_t*>(dsm2 + 4 * kTpcTab) + tid;  // [8][kRingStride]
   const uint32_t* ss = a.ssyms + fi * a.nbins;
   const uint32_t n2 = P.t2_n;
   {
@@ -866,7 +867,7 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, 
     const int mc = (int)min((int64_t)kChunk, a.n - i0);
     const uint64_t B = a0 + b0;
     TpcReader R;
-    tpc_init(R, G, ring, nthr, B, vmax);
+    tpc_init(R, G, ring, kRingStride, B, vmax);
     KState<LCF> ks;
     int err = 0;
     float* dst = F.out + i0;
@@ -899,13 +900,13 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, 
       const int32_t e = resolve(__funnelshift_l(R.w1, R.w0, R.off));
       const uint32_t l = (uint32_t)e & 63u;
       if (e & 64) {
-        tpc_skip(R, l, ring, nthr, G32, wmax, tpc_next(R, ring, nthr));
+        tpc_skip(R, l, ring, kRingStride, G32, wmax, tpc_next(R, ring, kRingStride));
         o = __uint_as_float(__funnelshift_l(R.w1, R.w0, R.off));
         ks.escape(esc_k(o, F));
-        tpc_skip(R, 32, ring, nthr, G32, wmax, tpc_next(R, ring, nthr));
+        tpc_skip(R, 32, ring, kRingStride, G32, wmax, tpc_next(R, ring, kRingStride));
       } else {
         o = ks.apply(e >> 7, twob);
-        tpc_skip(R, l, ring, nthr, G32, wmax, tpc_next(R, ring, nthr));
+        tpc_skip(R, l, ring, kRingStride, G32, wmax, tpc_next(R, ring, kRingStride));
       }
     };
     // common step: table hit (primary or secondary), no escape; the window
@@ -913,12 +914,12 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, 
     // needed a word the ring did not hold yet (the group is then replayed)
     auto fast_step = [&](float& o) {
       const uint32_t v = __funnelshift_l(R.w1, R.w0, R.off);
-      const uint32_t nw = tpc_next(R, ring, nthr);
+      const uint32_t nw = tpc_next(R, ring, kRingStride);
       int32_t e = LT[v >> (32 - kTpcBits)];
       const uint32_t j = min((v - r0) >> sh2, n2m1);
       const int32_t e2 = LT2[j];
       if ((e & 63) == 0) e = (v >= r0 && ((v - r0) >> sh2) < n2) ? e2 : 0;
-      if ((e & 63) == 0 || (e & 64)) {
+      if ((uint32_t)((e & 127) - 1) >= 63u) {  // unresolved (length 0) or escape
         safe_step(o);
         return;
       }
@@ -948,7 +949,7 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, 
           for (int u = 0; u < 8; u++) o[u] = (u == q) ? t : o[u];
         }
       }
-      tpc_refill(R, ring, nthr, G, vmax);
+      tpc_refill(R, ring, kRingStride, G, vmax);
     };
     int i = 0;
     if (vec) {
@@ -973,7 +974,7 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, 
     for (; i < mc && consumed() <= Tb; i++) {
       float o;
       safe_step(o);
-      if ((i & 7) == 7) tpc_refill(R, ring, nthr, G, vmax);
+      if ((i & 7) == 7) tpc_refill(R, ring, kRingStride, G, vmax);
       dst[i] = o;
     }
     const uint64_t pos = consumed();
@@ -1151,10 +1152,10 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
     if (groups > a.nchunks) groups = (int)a.nchunks;
     const int per = (int)((a.nchunks + groups - 1) / groups);
     const int thr = min(kTpcMaxThreads, (per + 31) / 32 * 32);
-    const size_t sm2 = 4 * kTpcTab + 32 * (size_t)thr;
+    const size_t sm2 = 4 * kTpcTab + 32 * (size_t)kRingStride;
     static bool attr2 = false;
     if (!attr2) {  // sized for the largest launch
-      const int smax = 4 * kTpcTab + 32 * kTpcMaxThreads;
+      const int smax = 4 * kTpcTab + 32 * kRingStride;
       cudaFuncSetAttribute(decode_tpc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            smax);
       cudaFuncSetAttribute(decode_tpc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -104,18 +104,33 @@ def to_host(src, dst) -> None:
         h[off:off + m].copy_(stage[k & 1][:m])
 
 
-def bytes_from(src_u8, n: int) -> bytes:
-    """A new ``bytes`` object holding the first n bytes of the CPU uint8
-    tensor `src_u8` (typically pinned), filled by torch's multi-threaded
-    copy instead of a single-threaded memcpy: the object is created
-    uninitialised (PyBytes_FromStringAndSize(NULL, n), the CPython idiom
-    for building a bytes object in place) and written before anyone else
-    can see it."""
+def _advise_huge(addr: int, nbytes: int) -> None:
+    """madvise(MADV_HUGEPAGE) on the 2 MiB-aligned interior of a fresh
+    mapping, so first-touch faults cost ~1/512 as many traps (no-op where
+    THP is disabled)."""
+    import ctypes
+    if nbytes < (4 << 20):
+        return
+    try:
+        libc = ctypes.CDLL(None, use_errno=True)
+        a0 = (addr + (2 << 20) - 1) & ~((2 << 20) - 1)
+        ln = (addr + nbytes - a0) & ~((2 << 20) - 1)
+        if ln > 0:
+            libc.madvise(ctypes.c_void_p(a0), ctypes.c_size_t(ln), 14)  # MADV_HUGEPAGE
+    except Exception:
+        pass
+
+
+def new_bytes(n: int):
+    """A new uninitialised ``bytes`` object of length n and a writable uint8
+    CPU tensor over its buffer.  PyBytes_FromStringAndSize(NULL, n) is the
+    CPython idiom for building a bytes object in place; the caller fills the
+    whole buffer before the object escapes."""
     import ctypes
 
     import torch
     if n == 0:
-        return b""
+        return b"", torch.empty(0, dtype=torch.uint8)
     api = ctypes.pythonapi
     api.PyBytes_FromStringAndSize.restype = ctypes.py_object
     api.PyBytes_FromStringAndSize.argtypes = [ctypes.c_void_p, ctypes.c_ssize_t]
@@ -123,29 +138,91 @@ def bytes_from(src_u8, n: int) -> bytes:
     api.PyBytes_AsString.argtypes = [ctypes.py_object]
     b = api.PyBytes_FromStringAndSize(None, n)
     addr = api.PyBytes_AsString(b)
-    dst = torch.from_numpy(np.ctypeslib.as_array((ctypes.c_uint8 * n).from_address(addr)))
-    dst.copy_(src_u8[:n])
+    _advise_huge(addr, n)
+    view = torch.from_numpy(np.ctypeslib.as_array((ctypes.c_uint8 * n).from_address(addr)))
+    return b, view
+
+
+def bytes_from(src_u8, n: int) -> bytes:
+    """A new ``bytes`` object holding the first n bytes of the CPU uint8
+    tensor `src_u8`, filled by torch's multi-threaded copy."""
+    b, view = new_bytes(n)
+    if n:
+        view.copy_(src_u8[:n])
     return b
 
 
 def empty_host(numel: int, dtype=None):
-    """Fresh pageable CPU tensor advised to transparent huge pages, so the
-    first-touch page faults of a multi-GB output cost ~1/512 as many
-    faults (no-op where THP is disabled)."""
-    import ctypes
-
+    """Fresh pageable CPU tensor advised to transparent huge pages."""
     import torch
     dtype = dtype or torch.float32
     t = torch.empty(numel, dtype=dtype)
-    nbytes = t.numel() * t.element_size()
-    if nbytes >= (4 << 20):
-        try:
-            libc = ctypes.CDLL(None, use_errno=True)
-            addr = t.data_ptr()
-            a0 = (addr + (2 << 20) - 1) & ~((2 << 20) - 1)
-            ln = (addr + nbytes - a0) & ~((2 << 20) - 1)
-            if ln > 0:
-                libc.madvise(ctypes.c_void_p(a0), ctypes.c_size_t(ln), 14)  # MADV_HUGEPAGE
-        except Exception:
-            pass
+    _advise_huge(t.data_ptr(), t.numel() * t.element_size())
     return t
+
+
+class PinnedPool:
+    """Page-locked host blocks for repeated multi-GB outputs.
+
+    A D2H into page-locked memory runs at the full PCIe rate (~50 GB/s)
+    while a transfer into fresh pageable memory is staged and runs at about
+    half that; but locking a fresh block costs ~0.5 s per GB, far more than
+    one transfer saves.  The pool therefore only pays for a block once a
+    size has been asked for repeatedly: the first request of a size class
+    returns None (the caller stages into pageable memory), later ones get a
+    pooled block.  Blocks are handed out as numpy arrays; every view the
+    caller derives keeps that array as its ``base`` (numpy collapses view
+    chains onto it), so a block is reused only once the pool holds the last
+    reference.  At most `per_size` blocks per size class and `cap_bytes` in
+    total are kept."""
+
+    def __init__(self, per_size: int = 2, cap_bytes: int = 48 << 30):
+        self.per_size = per_size
+        self.cap_bytes = cap_bytes
+        self.blocks = {}  # nbytes -> [np.ndarray over a pinned tensor]
+        self.misses = {}  # nbytes -> count
+
+    def take(self, nbytes: int):
+        import sys
+        lst = self.blocks.setdefault(nbytes, [])
+        for i in range(len(lst)):
+            # references: the list slot + getrefcount's argument
+            if sys.getrefcount(lst[i]) <= 2:
+                return lst[i]
+        self.misses[nbytes] = self.misses.get(nbytes, 0) + 1
+        total = sum(k * len(v) for k, v in self.blocks.items())
+        if self.misses[nbytes] < 2 or len(lst) >= self.per_size or total + nbytes > self.cap_bytes:
+            return None
+        a = self._alloc(nbytes)
+        if a is not None:
+            lst.append(a)
+        return a
+
+    @staticmethod
+    def _alloc(nbytes: int):
+        import torch
+        try:
+            return torch.empty(nbytes, dtype=torch.uint8, pin_memory=True).numpy()
+        except RuntimeError:
+            return None
+
+    def clear(self) -> None:
+        self.blocks.clear()
+        self.misses.clear()
+
+
+POOL = PinnedPool()
+
+
+def host_output(nbytes: int, src) -> np.ndarray:
+    """Copy the first nbytes of the CUDA uint8 tensor `src` into host
+    memory the caller owns: a pooled page-locked block (direct D2H) or
+    fresh pageable memory (staged D2H).  Returns a uint8 numpy array."""
+    import torch
+    a = POOL.take(nbytes)
+    if a is not None:
+        torch.from_numpy(a).copy_(src[:nbytes])
+        return a
+    h = empty_host(nbytes, torch.uint8)
+    to_host(src[:nbytes], h)
+    return h.numpy()

@@ -502,11 +502,10 @@ def decompress(archive: Archive, device: Optional[bool] = None) -> ParticleSnaps
         raise DecodeError(f"decompress: {N.STATUS_NAMES.get(st, st)}")
     snap = ParticleSnapshot.__new__(ParticleSnapshot)
     if not device:
-        # one staged D2H of all six fields into fresh host memory
+        # one D2H of all six fields (pooled page-locked block when the
+        # size repeats, else staged into fresh pageable memory)
         from . import hostio
-        host = hostio.empty_host(6 * stride, torch.float32)
-        hostio.to_host(out.view(torch.uint8), host.view(torch.uint8))
-        hn = host.numpy()
+        hn = hostio.host_output(6 * stride * 4, out.view(torch.uint8)).view(np.float32)
         views = [hn[i * stride:i * stride + n] for i in range(6)]
     for i, name in enumerate(FIELD_NAMES):
         object.__setattr__(snap, name, views[i])

@@ -11,7 +11,7 @@ host_t = [torch.empty(n, dtype=torch.float32, pin_memory=True) for _ in range(6)
 host = [t.numpy() for t in host_t]
 datagen.generate(datagen.HaccSpec((640, 640, 640), 2.5), 0, n, out=host)
 snap = nbz.ParticleSnapshot(*host)
-for rep in range(3):
+for rep in range(int(os.environ.get("REPS", "3"))):
     torch.cuda.synchronize()
     t = [time.perf_counter()]
     res = nbz.compress(snap, "sz-lv-prx", nbz.ErrorBoundSpec.relative(1e-4)); torch.cuda.synchronize(); t.append(time.perf_counter())

@@ -168,9 +168,26 @@ def test_huff_encode_multichunk(O, rng):
 
 def test_crc64(O, rng):
     assert H.crc64(b"123456789") == 0x995DC9BBDF1939FA
-    for n in (0, 1, 7, 1023, 1024, 1025, 100003, 3 << 20):
+    for n in (0, 1, 7, 1023, 1024, 1025, 2047, 2048, 2049, 100003, 3 << 20, (512 << 10) * 3 + 5):
         b = rng.integers(0, 256, n).astype(np.uint8).tobytes()
         assert H.crc64(b) == O.crc64(b), n
+
+
+def test_crc64_unaligned_and_batched(O, rng):
+    """Device ranges at every 16-byte misalignment, several queued with one
+    readback (crc64_device_many), and one range long enough (> 1024 spans of
+    512 KiB) for the fold kernel's sequential runs."""
+    import torch
+    from paper_1711_03888_b200 import io as nio
+    big = rng.integers(0, 256, (1 << 29) + (3 << 19) + 77).astype(np.uint8)
+    d = torch.from_numpy(big).cuda()
+    parts, want = [], []
+    for off in range(16):
+        ln = 70001 + 13 * off
+        parts.append((d[off:off + ln], ln))
+        want.append(O.crc64(big[off:off + ln].tobytes()))
+    assert nio.crc64_device_many(parts) == want
+    assert nio.crc64_device(d[5:], big.size - 5) == O.crc64(big[5:].tobytes())
 
 
 # ---------------------------------------------------------------- whole path
