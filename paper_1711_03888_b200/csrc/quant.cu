@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   float* xbuf = reinterpret_cast<float*>(smem);                      // [2][16384]
   uint16_t* pbuf = reinterpret_cast<uint16_t*>(xbuf + 2 * kTileMax);  // [2][16384]
-  uint32_t* hw = reinterpret_cast<uint32_t*>(pbuf + 2 * kTileMax);    // [kQWin]
+  uint32_t* hw = reinterpret_cast<uint32_t*>(pbuf + 2 * kTileMax);    // [kQWin + 1]: window + escapes
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ int64_t s_carry2[2];
 
@@ -130,8 +130,19 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
   const double b = fm.bound, twob = fm.twob;
   const float inv32 = fm.inv32;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // Field-wide FP32 margin.  t32 = fl(x * fl(inv)) is within |t| 2^-23 (1 +
+  // 2^-23) of the FP64 product x * inv, and |t| <= tmax for every value, so
+  // |t32 - rint(t32)| < cmargin = 0.5 - (tmax 2^-22 + 2^-20) puts the FP64
+  // product on the same side of every half-integer: rint agrees, and the
+  // remaining distance to the cell edge (> |x| 2^-22) exceeds the f32
+  // rounding of k * 2b (<= |x| 2^-24), so the reconstruction check holds.
+  // `small` = every |t| < 2^22 (the 32-bit chain applies).
+  const float tmax = fmaxf(fabsf(fm.lo), fabsf(fm.hi)) * inv32;
+  const bool small = tmax < 4194304.0f;
+  const float cmargin = 0.5f - __fmaf_ru(tmax, 2.384185791015625e-07f, 9.5367431640625e-07f);
+  const double inv = fm.inv;
 
-  for (int i = tid; i < kQWin; i += kQThreads) hw[i] = 0;
+  for (int i = tid; i <= kQWin; i += kQThreads) hw[i] = 0;
   if (tid == 0) {
     // k carried into the range: k of the last sorted element of tile tb-1
     int64_t kc = 0;
@@ -164,7 +175,7 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
     issue(tb, 0);
     if (tb + 1 < te) issue(tb + 1, 1);
   }
-  uint32_t phase[2] = {0, 0};
+  uint32_t phases = 0;  // bit b: parity of buffer b's barrier
   for (int64_t t = tb; t < te; t++) {
     const int buf = (int)((t - tb) & 1);
     const int64_t t0 = t * a.tile;
@@ -172,9 +183,9 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
     float* xs = xbuf + buf * kTileMax;
     uint16_t* ps = pbuf + buf * kTileMax;
     if (a.use_tma) {
-      while (!mbar_try_wait(&bar[buf], phase[buf])) {
+      while (!mbar_try_wait(&bar[buf], (phases >> buf) & 1u)) {
       }
-      phase[buf] ^= 1;
+      phases ^= 1u << buf;
       const int mb = m & ~7;
       if (tid < m - mb) {
         xs[mb + tid] = x[t0 + mb + tid];
@@ -212,6 +223,8 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
     // 32-bit shared-window addresses, computed once (no per-access
     // generic-to-shared conversion)
     const uint32_t xs_s = smem_u32(xs), ps_s = smem_u32(ps), hw_s = smem_u32(hw);
+    uint32_t hwin;  // opaque copy: keeps the compiler from re-deriving the window base per access
+    asm volatile("mov.u32 %0, %1;" : "=r"(hwin) : "r"(hw_s));
     int32_t rp32 = (int32_t)max(min(rot_prev, (int64_t)(1 << 30)), -(int64_t)(1 << 30));
     auto step = [&](int j, bool full) {
       const int p = wbase + j * 32 + lane;
@@ -268,9 +281,101 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
         cdst[32 * j] = (uint16_t)code;
       }
     };
-    if (m == kQThreads * kQPer) {  // full tile: no bounds checks
-#pragma unroll 4
-      for (int j = 0; j < kQPer; j++) step(j, true);
+    if (m == kQThreads * kQPer && small) {
+      // ---- full tile (tile = one 16384-symbol chunk, so the chain restarts at
+      // position 0: warp 0 lane 0 starts from k = 0), every |k| < 2^22.  Four
+      // consecutive positions per lane per step: at step j lane l takes
+      // 512 w + 128 j + 4 l + {0..3}; one 8-byte perm load, one rotate
+      // shuffle and one 8-byte code store per four values.  A value is on the
+      // FP32 path when its rounding is provably exact against the field-wide
+      // error margin (|t - rint(t)| < c); the others take the exact FP64
+      // index and reconstruction check (divergent, ~1%).  Escapes count in
+      // window bin kQWin; codes outside the window go to global atomics only
+      // when some lane holds one.
+      uint2* cd = reinterpret_cast<uint2*>(codes + t0 + wbase) + lane;
+      int32_t kp0 = wbase == 0 ? 0 : rp32;
+      const bool last_lane = (wbase + 4 * lane + 3 == m - 1 - 3 * 128);
+#pragma unroll 1
+      for (int j = 0; j < kQPer / 4; j++) {
+        const uint32_t p0 = (uint32_t)(wbase + j * 128 + 4 * lane);
+        float xv[4];
+        if (SORTED) {
+          uint32_t lo, hi;
+          asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(ps_s + 2u * p0));
+          xv[0] = ld_shared_f32(xs_s + ((lo << 2) & 0xfffcu));
+          xv[1] = ld_shared_f32(xs_s + ((lo >> 14) & 0xfffcu));
+          xv[2] = ld_shared_f32(xs_s + ((hi << 2) & 0xfffcu));
+          xv[3] = ld_shared_f32(xs_s + ((hi >> 14) & 0xfffcu));
+        } else {
+          float4 v;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                       : "r"(xs_s + 4u * p0));
+          xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
+        }
+        int32_t k[4];
+        bool slow = false;
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const float tq = xv[e] * inv32;
+          const float rq = tq + 12582912.0f;
+          const float dq = tq - (rq - 12582912.0f);
+          slow |= !(fabsf(dq) < cmargin);
+          k[e] = __float_as_int(rq) - 0x4B400000;
+        }
+        uint32_t bad = 0;
+        if (slow) {
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            const float tq = xv[e] * inv32;
+            const float dq = tq - ((tq + 12582912.0f) - 12582912.0f);
+            if (!(fabsf(dq) < cmargin)) {
+              const double kd = rint(__dmul_rn((double)xv[e], inv));
+              k[e] = (int32_t)kd;
+              const float r = (float)__dmul_rn(kd, twob);
+              bad |= (fabs((double)xv[e] - (double)r) <= b ? 0u : 1u) << e;
+            }
+          }
+        }
+        const int32_t kr = __shfl_sync(0xffffffffu, k[3], (lane + 31) & 31);
+        int32_t kp = lane == 0 ? kp0 : kr;
+        kp0 = kr;
+        uint32_t code[4];
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const uint32_t u = (uint32_t)(k[e] - kp + half);
+          code[e] = u <= (uint32_t)(2 * half - 2) ? u + 1u : 0u;
+          kp = k[e];
+        }
+        if (bad) {
+#pragma unroll
+          for (int e = 0; e < 4; e++)
+            if (bad & (1u << e)) code[e] = 0u;
+        }
+        if (j == kQPer / 4 - 1 && last_lane) s_carry2[cur ^ 1] = k[3];
+        // histogram
+        uint32_t wb[4], wf[4];  // window bin; far test value (escapes: 0)
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const uint32_t wv = code[e] - (uint32_t)wlo;
+          wb[e] = code[e] == 0u ? (uint32_t)kQWin : wv;
+          wf[e] = code[e] == 0u ? 0u : wv;
+        }
+        const uint32_t wmax = max(max(wf[0], wf[1]), max(wf[2], wf[3]));
+        if (__any_sync(0xffffffffu, wmax >= (uint32_t)kQWin)) {
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            if (wb[e] <= (uint32_t)kQWin && (code[e] == 0u || wb[e] < (uint32_t)kQWin))
+              red_shared_add1(hwin + 4u * wb[e]);
+            else atomicAdd(&hist[code[e]], 1u);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; e++) red_shared_add1(hwin + 4u * wb[e]);
+        }
+        cd[32 * j] = make_uint2(code[0] | (code[1] << 16), code[2] | (code[3] << 16));
+      }
+      rp32 = kp0;
     } else {
 #pragma unroll 1
       for (int j = 0; j < kQPer; j++) step(j, false);
@@ -281,10 +386,10 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
       issue(t + 2, buf);
     }
   }
-  // ---- flush the histogram window
-  for (int i = tid; i < kQWin; i += kQThreads) {
+  // ---- flush the histogram window (bin kQWin holds escapes, code 0)
+  for (int i = tid; i <= kQWin; i += kQThreads) {
     uint32_t c = hw[i];
-    int code = wlo + i;
+    int code = i == kQWin ? 0 : wlo + i;
     if (c && code >= 0 && code < (int)a.nbins) atomicAdd(&hist[code], c);
   }
 }
@@ -378,7 +483,7 @@ int launch_quantize(const Plan& p, cudaStream_t st) {
   bool aligned = true;
   for (int f = 0; f < 6; f++) aligned &= (reinterpret_cast<uintptr_t>(p.f[f]) & 15) == 0;
   a.use_tma = aligned && (p.tile % 8 == 0);
-  size_t sm = 2 * kTileMax * 4 + 2 * kTileMax * 2 + kQWin * 4;
+  size_t sm = 2 * kTileMax * 4 + 2 * kTileMax * 2 + (kQWin + 4) * 4;
   cudaMemsetAsync(p.hist, 0, sizeof(uint32_t) * 6 * p.nbins, st);
   static bool attr = false;
   if (!attr) {
