@@ -45,6 +45,7 @@ NBZG_DEV void set_status(uint32_t* status, uint32_t code) { atomicCAS(status, 0u
 
 struct SegParams {
   int64_t mn[3];
+  float amax[3];  // max |x| over the segment, per coordinate
   int shift;  // drop + eff
   int w;      // key bits per field after masking
   int bits;
@@ -72,11 +73,13 @@ NBZG_DEV uint64_t make_key<uint64_t>(uint64_t u0, uint64_t u1, uint64_t u2) {
 
 // Stable LSD sort of perm[lo, lo+m) by keys[perm[.]] over sort_bits bits.
 // All shared accesses use 32-bit shared-window addresses.
-template <typename KeyT>
-NBZG_DEV void block_sort_range(const KeyT* keys, uint16_t* perm, int lo, int m, int sort_bits,
-                               uint16_t* whist, uint32_t* scan_tmp) {
+template <typename KeyT, bool FULL>
+NBZG_DEV void block_sort_range_t(const KeyT* keys, uint16_t* perm, int lo, int m, int sort_bits,
+                                 uint16_t* whist, uint32_t* scan_tmp) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int E = ((m + kSortWarps * 32 - 1) / (kSortWarps * 32)) * 32;  // per-warp span
+  // FULL: m == kTileMax, every warp owns exactly 32 full rows (no bounds checks)
+  const int E = FULL ? kTileMax / kSortWarps
+                     : ((m + kSortWarps * 32 - 1) / (kSortWarps * 32)) * 32;  // per-warp span
   const int J = E / 32;
   const int base = w * E;
   const uint32_t keys_s = sh_addr(keys), perm_s = sh_addr(perm) + 2u * (uint32_t)lo;
@@ -90,7 +93,7 @@ NBZG_DEV void block_sort_range(const KeyT* keys, uint16_t* perm, int lo, int m, 
     for (int j = 0; j < 32; j++) {
       if (j < J) {
         int pos = base + j * 32 + lane;
-        bool valid = pos < m;
+        bool valid = FULL || pos < m;
         uint32_t idx = valid ? lds_u16(perm_s + 2u * (uint32_t)pos) : 0u;
         uint32_t d = valid ? (uint32_t)((lds_key<KeyT>(keys_s + (uint32_t)sizeof(KeyT) * idx) >> sh) & 0xff)
                            : 0x100u;
@@ -126,7 +129,7 @@ NBZG_DEV void block_sort_range(const KeyT* keys, uint16_t* perm, int lo, int m, 
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 32; j++) {
-      if (j < J && base + j * 32 + lane < m) {
+      if (j < J && (FULL || base + j * 32 + lane < m)) {
         uint32_t v = packed[j];
         uint32_t idx = v & 0x3fff, r = (v >> 14) & 0x3ff, d = v >> 24;
         sts_u16(perm_s + 2u * (lds_u16(wh_s + 2u * d) + r), idx);
@@ -134,6 +137,13 @@ NBZG_DEV void block_sort_range(const KeyT* keys, uint16_t* perm, int lo, int m, 
     }
     __syncthreads();
   }
+}
+
+template <typename KeyT>
+NBZG_DEV void block_sort_range(const KeyT* keys, uint16_t* perm, int lo, int m, int sort_bits,
+                               uint16_t* whist, uint32_t* scan_tmp) {
+  if (m == kTileMax) block_sort_range_t<KeyT, true>(keys, perm, lo, m, sort_bits, whist, scan_tmp);
+  else block_sort_range_t<KeyT, false>(keys, perm, lo, m, sort_bits, whist, scan_tmp);
 }
 
 template <typename KeyT>
@@ -210,6 +220,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
           a0 = fminf(a0, red[0][c][q]);
           b0 = fmaxf(b0, red[1][c][q]);
         }
+        sp.amax[c] = fmaxf(fabsf(a0), fabsf(b0));
         if (fm[c].is_const) {
           sp.mn[c] = 0;
           continue;
@@ -244,6 +255,35 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
       // ---- 2. masked keys
       const int shift = sp.shift;
       const int64_t m0 = sp.mn[0], m1 = sp.mn[1], m2 = sp.mn[2];
+      // Segment-wide FP32 path (same margin argument as quantize_kernel):
+      // with tmax = max |x| * inv32 over the segment, |t - rint(t)| < c_c
+      // proves rint(fl(x * inv32)) == rint(f64(x) / 2b); otherwise the exact
+      // FP64 division.  Needs every |t| < 2^22 (32-bit indices).
+      float cm[3];
+      bool small = true;
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        const float tmax = sp.amax[c] * fm[c].inv32;
+        small &= tmax < 4194304.0f;
+        cm[c] = 0.5f - __fmaf_ru(tmax, 2.384185791015625e-07f, 9.5367431640625e-07f);
+      }
+      const float i0 = fm[0].inv32, i1 = fm[1].inv32, i2 = fm[2].inv32;
+      auto key_fast = [&](float x0, float x1, float x2) -> KeyT {
+        const float xv[3] = {x0, x1, x2};
+        const float iv[3] = {i0, i1, i2};
+        uint32_t u[3];
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+          const float t = xv[c] * iv[c];
+          const float r = t + 12582912.0f;
+          const float d = t - (r - 12582912.0f);
+          int32_t k = __float_as_int(r) - 0x4B400000;
+          if (!(fabsf(d) < cm[c])) k = (int32_t)rint(__ddiv_rn((double)xv[c], fm[c].twob));
+          const int32_t mm = (int32_t)(c == 0 ? m0 : (c == 1 ? m1 : m2));
+          u[c] = (uint32_t)(k - mm) >> shift;
+        }
+        return make_key<KeyT>(u[0], u[1], u[2]);
+      };
       auto key_of = [&](float x0, float x1, float x2) -> KeyT {
         const float xv[3] = {x0, x1, x2};
         uint64_t u[3];
@@ -259,14 +299,26 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
       const float4* x4[3] = {reinterpret_cast<const float4*>(a.x[0] + s0),
                              reinterpret_cast<const float4*>(a.x[1] + s0),
                              reinterpret_cast<const float4*>(a.x[2] + s0)};
+      if (small && sizeof(KeyT) == 4) {
 #pragma unroll 2
-      for (int v = threadIdx.x; v < m4; v += kSortThreads) {
-        const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
-        KeyT* kd = keys + lo + 4 * v;
-        kd[0] = key_of(q0.x, q1.x, q2.x);
-        kd[1] = key_of(q0.y, q1.y, q2.y);
-        kd[2] = key_of(q0.z, q1.z, q2.z);
-        kd[3] = key_of(q0.w, q1.w, q2.w);
+        for (int v = threadIdx.x; v < m4; v += kSortThreads) {
+          const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
+          KeyT* kd = keys + lo + 4 * v;
+          kd[0] = key_fast(q0.x, q1.x, q2.x);
+          kd[1] = key_fast(q0.y, q1.y, q2.y);
+          kd[2] = key_fast(q0.z, q1.z, q2.z);
+          kd[3] = key_fast(q0.w, q1.w, q2.w);
+        }
+      } else {
+#pragma unroll 2
+        for (int v = threadIdx.x; v < m4; v += kSortThreads) {
+          const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
+          KeyT* kd = keys + lo + 4 * v;
+          kd[0] = key_of(q0.x, q1.x, q2.x);
+          kd[1] = key_of(q0.y, q1.y, q2.y);
+          kd[2] = key_of(q0.z, q1.z, q2.z);
+          kd[3] = key_of(q0.w, q1.w, q2.w);
+        }
       }
       for (int i = 4 * m4 + threadIdx.x; i < m; i += kSortThreads)
         keys[lo + i] = key_of(a.x[0][s0 + i], a.x[1][s0 + i], a.x[2][s0 + i]);
