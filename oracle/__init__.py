@@ -38,9 +38,13 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "_ref", "liboracle.so")
 
-MODE_UIDS = {"sz-lcf": 0, "sz-lv": 1, "sz-lv-prx": 2}
+MODE_UIDS = {"sz-lcf": 0, "sz-lv": 1, "sz-lv-prx": 2, "sz-cpc2000": 3, "cpc2000": 4}
+CPC_MODES = ("sz-cpc2000", "cpc2000")
 KIND_SZ_FIELD = 0
+KIND_VLC_FIELD = 1
+KIND_RINDEX = 2
 KIND_SZ_DQ = 3
+NO_FIELD = 255
 CHUNK_SYMBOLS = 16384
 
 ORC_STATUS = {0: "ok", 1: "bound too small", 2: "code too long", 3: "invalid code",
@@ -99,6 +103,10 @@ def lib():
             "orc_compress_shards": (I64, [P, I64, I, P, ctypes.c_uint32, I64, I64, I, I, I,
                                           I, I, P]),
             "orc_num_threads": (I, []),
+            "orc_cpc_coord_stream": (I64, [P, I64, I64, P, P, P, P, I, P]),
+            "orc_vlc_vel_stream": (I64, [P, P, I64, I64, D, I, P]),
+            "orc_cpc_coord_decode": (I, [P, I64, I64, I64, P, P, P, P]),
+            "orc_vlc_vel_decode": (I, [P, I64, I64, I64, D, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -456,6 +464,202 @@ def decompress(wire: bytes) -> List[np.ndarray]:
             fmt = 1 if a["kinds"][f] == KIND_SZ_FIELD else 2
             out.append(sz_decode(a["payloads"][f], n, a["bounds"][f], a["interval_count"], fmt,
                                  lcf=a["mode_uid"] == 0))
+    return out
+
+
+# ----------------------------------------------------------------------
+# CPC2000 family (pipeline.py:447-526 stores_minima branch, 316-428)
+# ----------------------------------------------------------------------
+
+_SEG_MIN = struct.Struct("<B3q")
+
+
+def _take(ptr, ln) -> bytes:
+    data = ctypes.string_at(ptr, int(ln))
+    lib().orc_free(ptr)
+    return data
+
+
+def cpc_coord_stream(keys_sorted, segment_size: int, seg_bits, xs_sorted, ints_sorted, bounds,
+                     fmt: int) -> bytes:
+    """_build_coord_stream (pipeline.py:316-337); ints_sorted[c] None for a
+    constant coordinate (no correction records)."""
+    k = _c(keys_sorted, np.uint64)
+    n = k.size
+    sb = _c(seg_bits, np.uint8)
+    xs = [_c(a, np.float32) for a in xs_sorted]
+    ints = [None if a is None else _c(a, np.int64) for a in ints_sorted]
+    xp = (ctypes.c_void_p * 3)(*[a.ctypes.data for a in xs])
+    ip = (ctypes.c_void_p * 3)(*[None if a is None else a.ctypes.data for a in ints])
+    b = _c(bounds, np.float64)
+    out = ctypes.c_void_p()
+    ln = lib().orc_cpc_coord_stream(_p(k), n, segment_size, _p(sb), xp, ip, _p(b), fmt,
+                                    ctypes.byref(out))
+    if ln < 0:
+        raise ValueError(ORC_STATUS.get(-ln, str(ln)))
+    return _take(out, ln)
+
+
+def vlc_vel_stream(ints_sorted, x_sorted, segment_size: int, bound: float, fmt: int) -> bytes:
+    """_build_vel_stream (pipeline.py:378-395)."""
+    i = _c(ints_sorted, np.int64)
+    x = _c(x_sorted, np.float32)
+    out = ctypes.c_void_p()
+    ln = lib().orc_vlc_vel_stream(_p(i), _p(x), i.size, segment_size, float(bound), fmt,
+                                  ctypes.byref(out))
+    if ln < 0:
+        raise ValueError(ORC_STATUS.get(-ln, str(ln)))
+    return _take(out, ln)
+
+
+def cpc_coord_decode(payload: bytes, n: int, segment_size: int, seg_bits, minima, bounds,
+                     mask: int) -> List[Optional[np.ndarray]]:
+    buf = np.frombuffer(bytes(payload) + b"\0" * 8, np.uint8)
+    sb = _c(seg_bits, np.uint8)
+    mn = _c(minima, np.int64).reshape(-1)
+    b = _c(bounds, np.float64)
+    outs = [None if mask & (1 << c) else np.zeros(max(n, 1), np.float32) for c in range(3)]
+    op = (ctypes.c_void_p * 3)(*[None if o is None else o.ctypes.data for o in outs])
+    st = lib().orc_cpc_coord_decode(_p(buf), len(payload), n, segment_size, _p(sb), _p(mn),
+                                    _p(b), op)
+    if st:
+        raise ValueError(ORC_STATUS.get(st, str(st)))
+    return [None if o is None else o[:n] for o in outs]
+
+
+def vlc_vel_decode(payload: bytes, n: int, segment_size: int, bound: float) -> np.ndarray:
+    buf = np.frombuffer(bytes(payload) + b"\0" * 8, np.uint8)
+    out = np.zeros(max(n, 1), np.float32)
+    st = lib().orc_vlc_vel_decode(_p(buf), len(payload), n, segment_size, float(bound), _p(out))
+    if st:
+        raise ValueError(ORC_STATUS.get(st, str(st)))
+    return out[:n]
+
+
+def serialize_cpc(mode: str, n: int, interval_count: int, segment_size: int,
+                  ignored_groups: int, bounds, mask: int, constants, seg_bits, minima,
+                  streams, fmt: int) -> bytes:
+    """io.py:105-125 for the stores_minima modes: segments carry (bits,
+    minima[3]); streams = [(kind, field, payload)], RINDEX first."""
+    head = bytearray()
+    head += _FIXED.pack(b"NBZ1", fmt, MODE_UIDS[mode], 0 if n > 0 else 255, n, interval_count,
+                        segment_size, ignored_groups, mask, 0)
+    head += struct.pack("<6d", *bounds)
+    head += struct.pack("<6f", *constants)
+    nseg = len(seg_bits) if n > 0 else 0
+    head += struct.pack("<II", nseg, len(streams))
+    for s in range(nseg):
+        head += _SEG_MIN.pack(int(seg_bits[s]), *[int(v) for v in minima[s]])
+    for kind, f, p in streams:
+        head += struct.pack("<BBHQQ", kind, f, 0, len(p), crc64(p))
+    head += struct.pack("<Q", crc64(bytes(head)))
+    return bytes(head) + b"".join(p for _, _, p in streams)
+
+
+def compress_cpc(fields: Sequence[np.ndarray], mode: str, kinds, values,
+                 interval_count: int = 65536, segment_size: int = 16384,
+                 ignored_groups: int = 6, fmt: int = 1) -> dict:
+    """pipeline.compress for sz-cpc2000 / cpc2000 (pipeline.py:447-526):
+    full-key R-index sort (k = 0, no key clamp: BoundTooSmallError past 21
+    bits), the coordinate stream (raw first key + unsigned VLC deltas per
+    segment + float32 corrections), velocities as SZ streams (sz-cpc2000;
+    v1 sequential chain for fmt 1, dual-quant v2 for fmt 2) or signed VLC
+    streams (cpc2000).  fmt 1 reproduces the reference archive byte for byte;
+    fmt 2 (the GPU's) adds u32 per-segment bit lengths after each VLC-family
+    payload and writes container version 2."""
+    f32 = [_c(a, np.float32) for a in fields]
+    n = int(f32[0].size)
+    if isinstance(kinds, str):
+        kinds = [kinds] * 6
+    if np.isscalar(values):
+        values = [values] * 6
+    resolved, constants, mask = resolve_field_bounds(f32, kinds, values)
+    bounds = np.array([b if b is not None else 0.0 for b in resolved], np.float64)
+    streams = []
+    order = None
+    seg_bits = np.zeros(0, np.uint8)
+    minima = np.zeros((0, 3), np.int64)
+    if n > 0:
+        ints = [np.zeros(n, np.int64) if resolved[i] is None else integerize(f32[i], resolved[i])
+                for i in range(3)]
+        keys, seg_bits, minima = build_rindex(ints, segment_size, allow_clamp=False)
+        order = prx_order(keys, segment_size, seg_bits, 0, 3)
+        work = [f[order] for f in f32]
+        if (mask & 0b111) != 0b111:
+            ks = keys[order]
+            isort = [None if mask & (1 << c) else ints[c][order] for c in range(3)]
+            streams.append((KIND_RINDEX, NO_FIELD,
+                            cpc_coord_stream(ks, segment_size, seg_bits, work[:3], isort,
+                                             bounds[:3], fmt)))
+        half = interval_count // 2
+        for fi in (3, 4, 5):
+            if mask & (1 << fi):
+                continue
+            if mode == "cpc2000":
+                iv = integerize(work[fi], resolved[fi])
+                streams.append((KIND_VLC_FIELD, fi,
+                                vlc_vel_stream(iv, work[fi], segment_size, resolved[fi], fmt)))
+            elif fmt == 1:
+                codes, esc, _r = sz_quantize(work[fi], resolved[fi], half)
+                streams.append((KIND_SZ_FIELD, fi, sz_payload(codes, esc, interval_count, 1)))
+            else:
+                codes, esc, _k = dq_quantize(work[fi], resolved[fi], half)
+                streams.append((KIND_SZ_DQ, fi, sz_payload(codes, esc, interval_count, 2)))
+    wire = serialize_cpc(mode, n, interval_count, segment_size, ignored_groups, bounds, mask,
+                         constants, seg_bits, minima, streams, fmt)
+    return dict(wire=wire, streams=streams, bounds=bounds, constants=constants, mask=mask,
+                seg_bits=seg_bits, minima=minima, order=order,
+                ratio=(24.0 * n / len(wire)) if n else None)
+
+
+def parse_cpc(wire: bytes) -> dict:
+    (magic, version, mode_uid, variant_uid, n, ic, ss, ig, mask, _pad) = _FIXED.unpack_from(wire, 0)
+    off = _FIXED.size
+    bounds = struct.unpack_from("<6d", wire, off); off += 48
+    consts = struct.unpack_from("<6f", wire, off); off += 24
+    nseg, nst = struct.unpack_from("<II", wire, off); off += 8
+    seg_bits = np.zeros(nseg, np.uint8)
+    minima = np.zeros((nseg, 3), np.int64)
+    for s in range(nseg):
+        b, m0, m1, m2 = _SEG_MIN.unpack_from(wire, off); off += _SEG_MIN.size
+        seg_bits[s] = b
+        minima[s] = (m0, m1, m2)
+    dirs = []
+    for _ in range(nst):
+        dirs.append(struct.unpack_from("<BBHQQ", wire, off)); off += 20
+    off += 8
+    streams = []
+    for kind, fid, _p2, ln, _crc in dirs:
+        streams.append((kind, fid, wire[off:off + ln]))
+        off += ln
+    return dict(version=version, mode_uid=mode_uid, n=n, interval_count=ic, segment_size=ss,
+                ignored_groups=ig, mask=mask, bounds=bounds, constants=consts,
+                seg_bits=seg_bits, minima=minima, streams=streams)
+
+
+def decompress_cpc(wire: bytes) -> List[np.ndarray]:
+    """pipeline.decompress stores_minima branch (pipeline.py:559-590); the
+    output stays in sorted order, as in the reference."""
+    a = parse_cpc(wire)
+    n, mask = a["n"], a["mask"]
+    out: List[Optional[np.ndarray]] = [None] * 6
+    for f in range(6):
+        if mask & (1 << f):
+            out[f] = np.full(n, np.float32(a["constants"][f]), np.float32)
+    if n == 0:
+        return [np.zeros(0, np.float32)] * 6
+    for kind, fid, p in a["streams"]:
+        if kind == KIND_RINDEX:
+            rec = cpc_coord_decode(p, n, a["segment_size"], a["seg_bits"], a["minima"],
+                                   a["bounds"][:3], mask)
+            for c in range(3):
+                if out[c] is None:
+                    out[c] = rec[c]
+        elif kind == KIND_VLC_FIELD:
+            out[fid] = vlc_vel_decode(p, n, a["segment_size"], a["bounds"][fid])
+        else:
+            out[fid] = sz_decode(p, n, a["bounds"][fid], a["interval_count"],
+                                 1 if kind == KIND_SZ_FIELD else 2)
     return out
 
 

@@ -159,6 +159,42 @@ def dump_lcf_case(name: str, fields, ebs):
     print(name, len(meta), "tags")
 
 
+def dump_cpc_case(name: str, fields, ebs, segment_size: int = 16384):
+    """CPC2000 family (mode uids 3, 4): the full-key R-index coordinate codec
+    (raw first key + unsigned VLC key deltas per segment, float32
+    corrections; pipeline.py:316-375, 460-500) with SZ (sz-cpc2000) or
+    signed-VLC (cpc2000) velocities.  Whole wires are stored verbatim."""
+    snap = ParticleSnapshot(*fields)
+    rec = {f"in_{i}": np.asarray(f, np.float32) for i, f in enumerate(fields)}
+    meta = []
+    settings = Settings(segment_size=segment_size)
+    for mode in (Mode.SZ_CPC2000, Mode.CPC2000):
+        for eb in ebs:
+            tag = f"{mode.value}|{eb:g}"
+            try:
+                res = compress(snap, mode, ErrorBoundSpec.relative(eb), settings)
+            except Exception as exc:  # e.g. BoundTooSmallError (no key clamp)
+                rec[f"{tag}|error"] = np.array(type(exc).__name__)
+                meta.append(tag)
+                continue
+            ar = res.archive
+            wire = ar.serialized()
+            rec[f"{tag}|wire"] = np.frombuffer(wire, np.uint8)
+            rec[f"{tag}|ratio"] = np.array(ratio(ar) if ar.n else -1.0)
+            rec[f"{tag}|bounds"] = np.array(ar.bounds, np.float64)
+            if res.order is not None:
+                rec[f"{tag}|order"] = res.order.astype(np.int64)
+            if ar.n:
+                out = decompress(ar)
+                for fi in range(6):
+                    rec[f"{tag}|recon{fi}"] = out.field(fi)
+            meta.append(tag)
+    rec["tags"] = np.array(meta)
+    rec["segment_size"] = np.array(segment_size)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **rec)
+    print(name, len(meta), "tags")
+
+
 def dump_kats():
     rec = {}
     # interleave field-order KATs (test_rindex.py:23-29 style) and a random sweep
@@ -224,6 +260,20 @@ def main():
         noise = [rng.uniform(0, 100, 20000).astype(np.float32) for _ in range(3)]
         noise += [(rng.standard_cauchy(20000) * 10).astype(np.float32) for _ in range(3)]
         dump_lcf_case("lcf_noise20k", noise, [1e-4, 1e-6])
+        return
+    if "--cpc" in sys.argv:  # only the CPC2000-family fixtures
+        dump_cpc_case("cpc_hacc24", D.small_hacc(24), [1e-3, 1e-4])
+        dump_cpc_case("cpc_amdf20k", D.small_amdf(20000), [1e-4, 1e-5], segment_size=4096)
+        rng = np.random.default_rng(31)
+        cst = [rng.uniform(0, 100, 5000).astype(np.float32) for _ in range(6)]
+        cst[1] = np.full(5000, 7.25, np.float32)
+        cst[4] = np.full(5000, -3.5, np.float32)
+        dump_cpc_case("cpc_const2", cst, [1e-4], segment_size=1000)
+        noise = [rng.uniform(0, 100, 9000).astype(np.float32) for _ in range(3)]
+        noise += [(rng.standard_cauchy(9000) * 10).astype(np.float32) for _ in range(3)]
+        dump_cpc_case("cpc_noise9k", noise, [1e-4, 1e-6], segment_size=2048)
+        dump_cpc_case("cpc_tiny", [rng.uniform(0, 10, 3).astype(np.float32) for _ in range(6)],
+                      [1e-4])
         return
     if "--variants" in sys.argv:  # only the R-index variant fixtures
         dump_variant_case("variants_hacc24", D.small_hacc(24), [1e-3, 1e-4])

@@ -32,6 +32,9 @@ GOLDEN_CASES = ["hacc34", "amdf40k", "sweep_hacc20", "sweep_amdf8k", "tiny1", "t
                 "const2", "noise20k"]
 
 
+CPC_CASES = ["cpc_hacc24", "cpc_amdf20k", "cpc_const2", "cpc_noise9k", "cpc_tiny"]
+
+
 def golden_inputs(g: dict):
     return [g[f"in_{i}"] for i in range(6)]
 

@@ -5,7 +5,7 @@ CPU-only; no GPU needed."""
 import numpy as np
 import pytest
 
-from conftest import GOLDEN_CASES, golden_inputs, load_golden, sha
+from conftest import CPC_CASES, GOLDEN_CASES, golden_inputs, load_golden, sha
 
 MODES = {"sz-lv": "sz-lv", "sz-lv-prx": "sz-lv-prx"}
 
@@ -205,3 +205,62 @@ def test_oracle_lcf_matches_reference(oracle_lib, case):
         for fi in range(6):
             err = np.abs(fields[fi].astype(np.float64) - d2[fi].astype(np.float64))
             assert float(err.max()) <= r2["bounds"][fi] or r2["mask"] & (1 << fi)
+
+
+# ---------------------------------------------------------------- CPC2000 family
+
+@pytest.mark.parametrize("case", CPC_CASES)
+def test_oracle_cpc_matches_reference(oracle_lib, case):
+    """sz-cpc2000 / cpc2000: the oracle's fmt-1 archive is the reference's
+    byte for byte (full-key sort, raw first key + unsigned VLC deltas per
+    segment, per-segment scheme choice, float32 corrections, SZ or signed-VLC
+    velocities, segment minima in the container), and decoding the
+    reference's archive reproduces the reference's reconstruction exactly."""
+    O = oracle_lib
+    g = load_golden(case)
+    fields = golden_inputs(g)
+    ss = int(g["segment_size"])
+    for tag in g["tags"]:
+        t = str(tag)
+        mode, eb = t.split("|")
+        if f"{t}|error" in g:
+            with pytest.raises(OverflowError):
+                O.compress_cpc(fields, mode, "rel", float(eb), segment_size=ss, fmt=1)
+            continue
+        res = O.compress_cpc(fields, mode, "rel", float(eb), segment_size=ss, fmt=1)
+        ref = bytes(g[f"{t}|wire"])
+        assert res["wire"] == ref, tag
+        assert np.array_equal(res["order"], g[f"{t}|order"]), tag
+        out = O.decompress_cpc(ref)
+        for fi in range(6):
+            assert np.array_equal(out[fi].view(np.uint32), g[f"{t}|recon{fi}"].view(np.uint32)), (tag, fi)
+
+
+@pytest.mark.parametrize("case", CPC_CASES)
+def test_oracle_cpc_v2_roundtrip_and_ratio(oracle_lib, case):
+    """fmt 2 (what the GPU writes: per-segment bit lengths appended to every
+    VLC-family payload, dual-quant SZ velocities) decodes to the same
+    coordinates and VLC velocities as fmt 1, every value within its bound,
+    ratio within 0.5% of the reference's (inputs of >= 1000 particles)."""
+    O = oracle_lib
+    g = load_golden(case)
+    fields = golden_inputs(g)
+    ss = int(g["segment_size"])
+    for tag in g["tags"]:
+        t = str(tag)
+        if f"{t}|error" in g:
+            continue
+        mode, eb = t.split("|")
+        r2 = O.compress_cpc(fields, mode, "rel", float(eb), segment_size=ss, fmt=2)
+        out = O.decompress_cpc(r2["wire"])
+        ref = O.decompress_cpc(bytes(g[f"{t}|wire"]))
+        order = r2["order"]
+        for fi in range(6):
+            if fi < 3 or mode == "cpc2000":
+                assert np.array_equal(out[fi].view(np.uint32), ref[fi].view(np.uint32)), (tag, fi)
+            if r2["mask"] & (1 << fi):
+                continue
+            err = np.abs(fields[fi][order].astype(np.float64) - out[fi].astype(np.float64))
+            assert float(err.max()) <= r2["bounds"][fi], (tag, fi)
+        if fields[0].size >= 1000:
+            assert abs(r2["ratio"] / float(g[f"{t}|ratio"]) - 1) < 0.005, (tag, r2["ratio"])
