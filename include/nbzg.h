@@ -98,7 +98,10 @@ typedef struct nbzg_compress_args {
   uint16_t *perm;         /* device, n entries (sorted) */
   int32_t predictor;      /* 0 = last value (sz-lv, sz-lv-prx), 1 = LCF 2*prev - prev2
                              (Mode.SZ_LCF, _kernels.py:162-165; unsorted only) */
-  int32_t pad1;
+  int32_t cpc;            /* 0; 1 = sz-cpc2000, 2 = cpc2000 (full keys, no clamp, minima) */
+  int64_t *seg_minima;    /* device, 3 x nseg (cpc) */
+  uint32_t sz_skip;       /* bit f: no SZ stream for field f (cpc modes) */
+  uint32_t pad2;
 } nbzg_compress_args;
 
 size_t nbzg_compress_workspace_size(int64_t n, int32_t sorted, int64_t interval_count,
@@ -132,6 +135,80 @@ typedef struct nbzg_decompress_args {
 
 size_t nbzg_decompress_workspace_size(int64_t n, int64_t interval_count, int32_t nfields);
 int nbzg_decompress(const nbzg_decompress_args *args, void *stream);
+
+/* ---- CPC2000 family (Mode.SZ_CPC2000, Mode.CPC2000) ----
+ * nbzg_compress with `cpc` = 1 / 2 sorts on full keys (ignored groups 0, no
+ * key clamp: NBZG_BOUND_TOO_SMALL past 21 bits, rindex.py:185-190), writes
+ * the segment minima (`seg_minima`, 3 x i64 per segment, io.py:115-117) and
+ * builds SZ streams only for the fields outside `sz_skip`.  The VLC-family
+ * streams then come from two calls on the same stream:
+ *   nbzg_cpc_plan  -- per-segment VLC costs under both candidate schemes,
+ *                     scheme choice, correction counts, per-stream scans
+ *                     (pipeline.py:275-300, 230-237); fills `cmeta`;
+ *   nbzg_cpc_pack  -- after the host read `cmeta` and placed each payload at
+ *                     cmeta->off[s] of a ZEROED arena (bit region
+ *                     off + nseg + 8 16-byte aligned, 64 bytes of slack):
+ *                     payload bytes (pipeline.py:316-337 / 378-395 ->
+ *                     K.cpc_encode_keys _kernels.py:623-645 /
+ *                     K.vlc_encode_segmented _kernels.py:648-660), plus the
+ *                     u32 per-segment bit lengths this path appends (v2).
+ * Stream s: 0 = coordinates (StreamKind.RINDEX), 1..3 = VLC velocity fields
+ * 3..5 (StreamKind.VLC_FIELD, cpc2000 only). */
+typedef struct nbzg_cpc_meta {
+  uint64_t off[4];        /* payload offset in the arena (host-filled before pack) */
+  uint64_t len[4];        /* payload bytes */
+  uint64_t total_bits[4]; /* bitstream length */
+  uint64_t corr[4][3];    /* correction records per list */
+  uint32_t status;        /* NBZG_BOUND_TOO_SMALL / NBZG_CODE_TOO_LONG, 0 if none */
+  uint32_t pad;
+} nbzg_cpc_meta;
+
+typedef struct nbzg_cpc_args {
+  const float *fields[6];    /* device, original (unsorted) order */
+  int64_t n;
+  int64_t segment_size;
+  int32_t mode;              /* 1 sz-cpc2000 (coordinate stream), 2 cpc2000 (+ velocities) */
+  int32_t pad0;
+  const uint16_t *perm;      /* from nbzg_compress (tile-local sorted -> source) */
+  const uint8_t *seg_bits;   /* from nbzg_compress */
+  const int64_t *seg_minima; /* from nbzg_compress */
+  const nbzg_meta *meta;     /* from nbzg_compress (bounds, ranges, constant mask) */
+  void *workspace;           /* nbzg_cpc_workspace_size() bytes */
+  size_t workspace_bytes;
+  uint8_t *arena;            /* pack only */
+  nbzg_cpc_meta *cmeta;      /* device */
+} nbzg_cpc_args;
+
+size_t nbzg_cpc_workspace_size(int64_t n, int64_t segment_size);
+int nbzg_cpc_plan(const nbzg_cpc_args *args, void *stream);
+int nbzg_cpc_pack(const nbzg_cpc_args *args, void *stream);
+
+/* Decode one VLC-family stream (pipeline.py:340-375 / 398-428 ->
+ * K.cpc_decode_keys _kernels.py:566-601 + deinterleave3 789-798 /
+ * K.vlc_decode_segmented).  indexed = 1: the payload ends with u32
+ * per-segment bit lengths (this path's v2 archives: one thread per segment);
+ * 0: a reference (v1) stream, segment offsets found by one sequential walk.
+ * Coordinates: out[c] = f32((deinterleaved key + minimum) * 2 bound[c]),
+ * null for constant coordinates; velocities: out[0]. */
+typedef struct nbzg_cpc_decode_args {
+  const uint8_t *payload;    /* device, 64 bytes of readable slack */
+  int64_t payload_len;
+  int32_t kind;              /* 2 = RINDEX (coordinates), 1 = VLC_FIELD */
+  int32_t indexed;
+  int64_t n;
+  int64_t segment_size;
+  uint64_t total_bits;       /* from the payload header (host-parsed) */
+  const uint8_t *seg_bits;   /* device (coordinates) */
+  const int64_t *seg_minima; /* device (coordinates) */
+  double bound[3];
+  float *out[3];
+  void *workspace;           /* nbzg_cpc_decode_workspace_size() bytes */
+  size_t workspace_bytes;
+  uint32_t *status;          /* device */
+} nbzg_cpc_decode_args;
+
+size_t nbzg_cpc_decode_workspace_size(int64_t n, int64_t segment_size);
+int nbzg_cpc_decode(const nbzg_cpc_decode_args *args, void *stream);
 
 /* ---- stage-level parity hooks (mirror nbz._kernels, same semantics) ---- */
 

@@ -38,7 +38,8 @@ EXPORTED = (
     "nbzg_rindex_keys", "nbzg_prx_order", "nbzg_order_expand", "nbzg_huffman_lengths",
     "nbzg_huffman_codebook", "nbzg_huff_encode", "nbzg_crc64", "nbzg_crc64_workspace_size",
     "nbzg_version", "nbzg_device_sm_count", "nbzg_launch_count", "nbzg_trace_enable",
-    "nbzg_trace_read",
+    "nbzg_trace_read", "nbzg_cpc_workspace_size", "nbzg_cpc_plan", "nbzg_cpc_pack",
+    "nbzg_cpc_decode", "nbzg_cpc_decode_workspace_size",
 )
 
 
@@ -75,7 +76,26 @@ class CompressArgs(ctypes.Structure):
                 ("ignored_groups", c_i32), ("rindex_variant", c_i32), ("workspace", c_p),
                 ("workspace_bytes", c_sz), ("arena", c_p), ("arena_bytes", c_sz),
                 ("meta", c_p), ("seg_bits", c_p), ("perm", c_p), ("predictor", c_i32),
-                ("pad1", c_i32)]
+                ("cpc", c_i32), ("seg_minima", c_p), ("sz_skip", c_u32), ("pad2", c_u32)]
+
+
+class CpcMeta(ctypes.Structure):
+    _fields_ = [("off", c_u64 * 4), ("len", c_u64 * 4), ("total_bits", c_u64 * 4),
+                ("corr", (c_u64 * 3) * 4), ("status", c_u32), ("pad", c_u32)]
+
+
+class CpcArgs(ctypes.Structure):
+    _fields_ = [("fields", c_p * 6), ("n", c_i64), ("segment_size", c_i64), ("mode", c_i32),
+                ("pad0", c_i32), ("perm", c_p), ("seg_bits", c_p), ("seg_minima", c_p),
+                ("meta", c_p), ("workspace", c_p), ("workspace_bytes", c_sz), ("arena", c_p),
+                ("cmeta", c_p)]
+
+
+class CpcDecodeArgs(ctypes.Structure):
+    _fields_ = [("payload", c_p), ("payload_len", c_i64), ("kind", c_i32), ("indexed", c_i32),
+                ("n", c_i64), ("segment_size", c_i64), ("total_bits", c_u64),
+                ("seg_bits", c_p), ("seg_minima", c_p), ("bound", c_d * 3), ("out", c_p * 3),
+                ("workspace", c_p), ("workspace_bytes", c_sz), ("status", c_p)]
 
 
 class DecompressArgs(ctypes.Structure):
@@ -106,6 +126,11 @@ _SIGS = {
     "nbzg_launch_count": (ctypes.c_ulonglong, []),
     "nbzg_trace_enable": (ctypes.c_int, [ctypes.c_int]),
     "nbzg_trace_read": (ctypes.c_int, [c_p, ctypes.c_int, c_p, ctypes.c_int]),
+    "nbzg_cpc_workspace_size": (c_sz, [c_i64, c_i64]),
+    "nbzg_cpc_plan": (ctypes.c_int, [c_p, c_p]),
+    "nbzg_cpc_pack": (ctypes.c_int, [c_p, c_p]),
+    "nbzg_cpc_decode_workspace_size": (c_sz, [c_i64, c_i64]),
+    "nbzg_cpc_decode": (ctypes.c_int, [c_p, c_p]),
 }
 
 _lib = None

@@ -150,4 +150,18 @@ int launch_resolve(const Plan& p, cudaStream_t st) {
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
 
+// CPC modes: fields without an SZ stream are marked constant for the SZ
+// stages (quantize / codebook / layout / encode skip them); meta->mask keeps
+// the true constant mask for the archive and the CPC kernels.
+__global__ void sz_skip_kernel(nbzg_meta* meta, uint32_t skip) {
+  const int f = threadIdx.x;
+  if (f < 6 && ((skip >> f) & 1u)) meta->f[f].is_const = 1;
+}
+
+int launch_sz_skip(const Plan& p, cudaStream_t st) {
+  count_launch();
+  sz_skip_kernel<<<1, 32, 0, st>>>(p.meta, p.sz_skip);
+  return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
+}
+
 }  // namespace nbzg

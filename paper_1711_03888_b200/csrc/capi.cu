@@ -214,6 +214,15 @@ int nbzg_compress(const nbzg_compress_args* a, void* stream) {
   if (a->predictor < 0 || a->predictor > 1 || (a->predictor == 1 && a->sorted))
     return NBZG_UNSUPPORTED;
   p.predictor = a->predictor;
+  if (a->cpc < 0 || a->cpc > 2 || (a->cpc && (!a->sorted || a->rindex_variant != 0)))
+    return NBZG_BAD_ARG;
+  p.cpc = a->cpc;
+  if (p.cpc) {
+    p.ig = 0;  // full-key sort (pipeline.py:464: k = 0 when the mode stores minima)
+    p.minima = a->seg_minima;
+    p.sz_skip = a->sz_skip & 63u;
+    if (a->n > 0 && !p.minima) return NBZG_BAD_ARG;
+  }
   for (int f = 0; f < 6; f++) {
     p.f[f] = a->fields[f];
     p.bound_kind[f] = a->bound_kind[f];
@@ -239,6 +248,7 @@ int nbzg_compress(const nbzg_compress_args* a, void* stream) {
     if ((rc = launch_rindex_sort(p, st))) return rc;
     trace_mark("rindex_sort", st);
   }
+  if (p.sz_skip && (rc = launch_sz_skip(p, st))) return rc;
   if ((rc = launch_quantize(p, st))) return rc;
   trace_mark("quantize", st);
   if ((rc = launch_codebook(p, st))) return rc;

@@ -22,6 +22,9 @@ struct Plan {
   int ig = 6;
   int variant = 0;      // RIndexVariant: 0 coord, 1 vel, 2 coord+vel
   int predictor = 0;    // 0 last value, 1 LCF (sz-lcf)
+  int cpc = 0;          // 0; 1 sz-cpc2000; 2 cpc2000 (full keys, no clamp, minima)
+  uint32_t sz_skip = 0; // fields without an SZ stream (CPC modes)
+  int64_t* minima = nullptr;  // 3 per segment (CPC)
   const float* f[6] = {};
   int bound_kind[6] = {};
   double bound_value[6] = {};
@@ -67,6 +70,7 @@ int launch_quantize(const Plan& p, cudaStream_t st);
 int launch_codebook(const Plan& p, cudaStream_t st);
 int launch_layout(const Plan& p, cudaStream_t st);
 int launch_encode(const Plan& p, cudaStream_t st);
+int launch_sz_skip(const Plan& p, cudaStream_t st);
 
 int sm_count();
 

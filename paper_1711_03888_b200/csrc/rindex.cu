@@ -39,6 +39,8 @@ struct RArgs {
   uint32_t* tile_flags;
   uint32_t* status;
   int pass;  // 0 = u32 main pass, 1 = u64 pass over flagged tiles
+  int no_clamp;     // CPC modes: allow_key_clamp=False (rindex.py:185-190)
+  int64_t* minima;  // CPC modes: 3 segment minima per segment (io.py:115-117), else null
 };
 
 NBZG_DEV void set_status(uint32_t* status, uint32_t code) { atomicCAS(status, 0u, code); }
@@ -234,6 +236,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
       }
       int bits = min(need, 21);
       int drop = need > 21 ? need - 21 : 0;  // allow_key_clamp=True for sz-lv-prx (pipeline.py:463)
+      if (a.no_clamp && need > 21) bad = 1;   // CPC: BoundTooSmallError (rindex.py:185-190)
       int eff = min(a.ig, bits);
       sp.bits = bits;
       sp.shift = drop + eff;
@@ -250,7 +253,11 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
       if (threadIdx.x == 0) a.tile_flags[t] = 1;
       return;  // redone by the u64 pass
     }
-    if (threadIdx.x == 0) a.seg_bits[(s0) / a.S] = (uint8_t)sp.bits;  // staged below
+    if (threadIdx.x == 0) {
+      a.seg_bits[(s0) / a.S] = (uint8_t)sp.bits;
+      if (a.minima)
+        for (int c = 0; c < 3; c++) a.minima[3 * (s0 / a.S) + c] = sp.mn[c];
+    }
     if (w > 0) {
       // ---- 2. masked keys
       const int shift = sp.shift;
@@ -457,6 +464,8 @@ int launch_rindex_sort(const Plan& p, cudaStream_t st) {
   a.seg_bits = p.seg_bits;
   a.tile_flags = p.tile_flags;
   a.status = &p.meta->status;
+  a.no_clamp = p.cpc ? 1 : 0;
+  a.minima = p.cpc ? p.minima : nullptr;
   size_t sm32 = kTileMax * (4 + 2) + kSortWarps * kRadix * 2;
   size_t sm64 = kTileMax * (8 + 2) + kSortWarps * kRadix * 2;
   static bool attr = false;

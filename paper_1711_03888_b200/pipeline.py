@@ -74,7 +74,8 @@ _MODE_UIDS = {Mode.SZ_LCF: 0, Mode.SZ_LV: 1, Mode.SZ_LV_PRX: 2,
 MODE_ALIASES = {"best-speed": Mode.SZ_LV, "best-tradeoff": Mode.SZ_LV_PRX,
                 "best-compression": Mode.SZ_CPC2000}
 
-GPU_MODES = (Mode.SZ_LCF, Mode.SZ_LV, Mode.SZ_LV_PRX)
+GPU_MODES = (Mode.SZ_LCF, Mode.SZ_LV, Mode.SZ_LV_PRX, Mode.SZ_CPC2000, Mode.CPC2000)
+COORD_SLOT = 6  # payload slot of the coordinate (RINDEX, field NO_FIELD) stream
 _KIND_LCF = 16  # NBZG_KIND_LCF: the stream's field uses the LCF predictor (mode sz-lcf)
 
 
@@ -121,14 +122,34 @@ class Stream:
 
 class _Device:
     """Device-resident side of an archive: the payload arena and where each
-    field's payload sits in it (host copy of the nbzg_meta block)."""
+    payload sits in it (host copy of the nbzg_meta block).  Slots 0-5 are the
+    per-field streams, slot 6 (COORD_SLOT) the CPC coordinate stream; a slot
+    listed in ``bufs`` lives in that tensor instead of ``arena``."""
 
-    def __init__(self, arena, offsets, lengths, kinds, keep=()):
+    def __init__(self, arena, offsets, lengths, kinds, keep=(), bufs=None):
         self.arena = arena          # torch uint8 CUDA tensor
-        self.offsets = offsets      # per field (None for constant fields)
-        self.lengths = lengths
-        self.kinds = kinds
+        self.offsets = list(offsets) + [None] * (7 - len(offsets))  # None: no stream
+        self.lengths = list(lengths) + [0] * (7 - len(lengths))
+        self.kinds = list(kinds) + [int(StreamKind.RINDEX)] * (7 - len(kinds))
         self.keep = keep            # tensors that must outlive the archive
+        self.bufs = bufs or {}
+
+    def buf(self, slot: int):
+        return self.bufs.get(slot, self.arena)
+
+    def payload(self, slot: int):
+        o = self.offsets[slot]
+        return self.buf(slot)[o:o + self.lengths[slot]]
+
+
+def slot_order(mode: "Mode"):
+    """Payload slots in stream (directory) order: the coordinate stream
+    first for the CPC modes (pipeline.py:482-500), then fields 0-5."""
+    return [COORD_SLOT, 0, 1, 2, 3, 4, 5] if mode.stores_minima else [0, 1, 2, 3, 4, 5]
+
+
+def slot_field(slot: int) -> int:
+    return NO_FIELD if slot == COORD_SLOT else slot
 
 
 class Archive:
@@ -143,7 +164,7 @@ class Archive:
                  bounds: Tuple[float, ...], constant_mask: int, constants: Tuple[float, ...],
                  seg_bits=None, streams: Optional[Tuple[Stream, ...]] = None,
                  device: Optional[_Device] = None, version: int = 2,
-                 device_output: bool = False):
+                 device_output: bool = False, seg_minima=None):
         self.mode = mode
         self.n = int(n)
         self.interval_count = int(interval_count)
@@ -154,6 +175,7 @@ class Archive:
         self.constant_mask = int(constant_mask)
         self.constants = tuple(float(c) for c in constants)
         self._seg_bits = seg_bits          # numpy u8 or CUDA tensor or None
+        self._seg_minima = seg_minima      # (nseg, 3) int64 numpy or CUDA tensor (CPC modes)
         self._segments: Optional[Tuple[Segment, ...]] = None
         self._streams = streams
         self._dev = device
@@ -177,6 +199,17 @@ class Archive:
         return sb
 
     @property
+    def seg_minima(self) -> np.ndarray:
+        """(nseg, 3) int64 segment minima (CPC modes, io.py:115-117)."""
+        mn = self._seg_minima
+        if mn is None:
+            return np.zeros((0, 3), np.int64)
+        if _is_tensor(mn):
+            mn = mn.cpu().numpy().astype(np.int64).reshape(-1, 3)
+            self._seg_minima = mn
+        return mn
+
+    @property
     def segments(self) -> Tuple[Segment, ...]:
         if self._segments is None:
             if not (self.mode.is_sorted and self.n > 0):
@@ -184,8 +217,11 @@ class Archive:
             else:
                 edges = segment_bounds(self.n, self.segment_size)
                 bits = self.seg_bits
-                self._segments = tuple(Segment(int(edges[i]), int(edges[i + 1]), int(bits[i]), ())
-                                       for i in range(edges.shape[0] - 1))
+                mins = self.seg_minima if self.mode.stores_minima else None
+                self._segments = tuple(
+                    Segment(int(edges[i]), int(edges[i + 1]), int(bits[i]),
+                            tuple(int(v) for v in mins[i]) if mins is not None else ())
+                    for i in range(edges.shape[0] - 1))
         return self._segments
 
     @property
@@ -196,19 +232,19 @@ class Archive:
                                   for k, f, a, ln in self._host_dir)
         if self._streams is None:
             d = self._dev
-            host = d.arena.cpu().numpy() if d is not None else None
             out = []
-            for fi in range(6):
-                if d is None or d.offsets[fi] is None:
+            for sl in slot_order(self.mode):
+                if d is None or d.offsets[sl] is None:
                     continue
-                o, ln = d.offsets[fi], d.lengths[fi]
-                out.append(Stream(StreamKind(d.kinds[fi]), fi, host[o:o + ln].tobytes()))
+                out.append(Stream(StreamKind(d.kinds[sl]), slot_field(sl),
+                                  d.payload(sl).cpu().numpy().tobytes()))
             self._streams = tuple(out)
         return self._streams
 
     def payload_lengths(self) -> List[int]:
         if self._dev is not None:
-            return [ln for o, ln in zip(self._dev.offsets, self._dev.lengths) if o is not None]
+            d = self._dev
+            return [d.lengths[sl] for sl in slot_order(self.mode) if d.offsets[sl] is not None]
         return [len(s.payload) for s in self.streams]
 
     def serialized(self) -> bytes:
@@ -351,8 +387,7 @@ def compress(snapshot: ParticleSnapshot, mode, bounds: Bounds,
         return best
     mode = _as_mode(mode)
     if mode not in GPU_MODES:
-        raise ValidationError(f"mode {mode.value} is not implemented by the B200 path "
-                              f"(supported: sz-lcf, sz-lv, sz-lv-prx)")
+        raise ValidationError(f"mode {mode.value} is not implemented by the B200 path")
     specs = _specs(bounds)
     n = snapshot.n
     L = N.lib()
@@ -372,6 +407,8 @@ def compress(snapshot: ParticleSnapshot, mode, bounds: Bounds,
     nseg = (n + S - 1) // S if sorted_mode else 0
     seg_bits = torch.empty(max(nseg, 1), dtype=torch.uint8, device="cuda")
     perm = torch.empty(max(n, 1), dtype=torch.int16, device="cuda") if sorted_mode else None
+    cpc = (1 if mode is Mode.SZ_CPC2000 else 2 if mode is Mode.CPC2000 else 0) if sorted_mode else 0
+    minima = torch.empty(3 * max(nseg, 1), dtype=torch.int64, device="cuda") if cpc else None
     a = N.CompressArgs()
     for i in range(6):
         a.fields[i] = N.ptr(fields[i]) if n else None
@@ -382,7 +419,11 @@ def compress(snapshot: ParticleSnapshot, mode, bounds: Bounds,
     a.interval_count = ic
     a.segment_size = S
     a.ignored_groups = settings.ignored_groups
-    a.rindex_variant = _VARIANT_CODE[settings.rindex_variant]
+    a.rindex_variant = 0 if mode.stores_minima else _VARIANT_CODE[settings.rindex_variant]
+    a.cpc = cpc
+    if cpc:
+        a.seg_minima = N.ptr(minima)
+        a.sz_skip = 0b000111 if cpc == 1 else 0b111111
     a.predictor = 1 if mode is Mode.SZ_LCF else 0
     a.workspace = N.ptr(ws)
     a.workspace_bytes = ws.numel()
@@ -406,17 +447,138 @@ def compress(snapshot: ParticleSnapshot, mode, bounds: Bounds,
         kinds.append(int(StreamKind.SZ_DQ))
     dev = _Device(arena[:max(int(meta.arena_used), 1)], offsets, lengths, kinds,
                   keep=(meta_t,))
+    if cpc:
+        _cpc_streams(dev, cpc, fields, n, S, perm, seg_bits, minima, meta, meta_t)
+    variant = None
+    if sorted_mode:
+        variant = RIndexVariant.COORDINATE if mode.stores_minima else settings.rindex_variant
     archive = Archive(
         mode=mode, n=n, interval_count=ic, segment_size=S,
         ignored_groups=settings.ignored_groups,
-        rindex_variant=settings.rindex_variant if sorted_mode else None,
+        rindex_variant=variant,
         bounds=tuple(meta.f[i].bound for i in range(6)),
         constant_mask=meta.mask,
         constants=tuple(meta.f[i].constant for i in range(6)),
         seg_bits=seg_bits[:nseg] if sorted_mode else None,
-        device=dev, version=2, device_output=snapshot.on_device)
+        device=dev, version=2, device_output=snapshot.on_device,
+        seg_minima=minima[:3 * nseg].view(nseg, 3) if cpc else None)
     tile = (max(1, 16384 // S) * S) if S < 16384 else S
     return CompressResult(archive, perm=perm[:n] if perm is not None else None, tile=tile)
+
+
+def _cpc_streams(dev: _Device, cpc: int, fields, n: int, S: int, perm, seg_bits, minima, meta,
+                 meta_t) -> None:
+    """The VLC-family streams of the CPC modes (pipeline.py:480-500):
+    nbzg_cpc_plan (segment costs, scheme choice, scans), one small D2H of
+    the per-stream sizes, an exact zeroed arena, nbzg_cpc_pack."""
+    import torch
+    L = N.lib()
+    nseg = (n + S - 1) // S
+    ws = N.POOL.get("cpc_ws", L.nbzg_cpc_workspace_size(n, S))
+    cm_t = torch.zeros(ctypes.sizeof(N.CpcMeta), dtype=torch.uint8, device="cuda")
+    ca = N.CpcArgs()
+    for i in range(6):
+        ca.fields[i] = N.ptr(fields[i])
+    ca.n = n
+    ca.segment_size = S
+    ca.mode = cpc
+    ca.perm = N.ptr(perm)
+    ca.seg_bits = N.ptr(seg_bits)
+    ca.seg_minima = N.ptr(minima)
+    ca.meta = N.ptr(meta_t)
+    ca.workspace = N.ptr(ws)
+    ca.workspace_bytes = ws.numel()
+    ca.arena = None
+    ca.cmeta = N.ptr(cm_t)
+    N.check(L.nbzg_cpc_plan(ctypes.byref(ca), N.stream_handle()), "cpc plan")
+    cm = N.CpcMeta.from_buffer_copy(cm_t.cpu().numpy().tobytes())
+    _raise_status(cm.status, "compress")
+    present = []
+    if (meta.mask & 0b111) != 0b111:
+        present.append((0, COORD_SLOT))
+    if cpc == 2:
+        present += [(s, 2 + s) for s in (1, 2, 3) if not (meta.mask >> (2 + s)) & 1]
+    off = 0
+    for s, _slot in present:
+        off += (-(off + nseg + 8)) % 16  # 16-byte aligned bit region
+        cm.off[s] = off
+        off += int(cm.len[s])
+    buf = torch.zeros(off + 64, dtype=torch.uint8, device="cuda")
+    cm_t.copy_(torch.frombuffer(bytearray(bytes(cm)), dtype=torch.uint8))
+    ca.arena = N.ptr(buf)
+    N.check(L.nbzg_cpc_pack(ctypes.byref(ca), N.stream_handle()), "cpc pack")
+    for s, slot in present:
+        dev.offsets[slot] = int(cm.off[s])
+        dev.lengths[slot] = int(cm.len[s])
+        dev.kinds[slot] = int(StreamKind.RINDEX if s == 0 else StreamKind.VLC_FIELD)
+        dev.bufs[slot] = buf
+    dev.keep = tuple(dev.keep) + (cm_t, buf)
+
+
+def _cpc_total_bits(archive: "Archive", slot: int, nseg: int) -> int:
+    d = archive._dev
+    if archive._host_dir is not None and archive._wire is not None:
+        for kind, fid, a, ln in archive._host_dir:
+            if slot_field(slot) == fid:
+                if ln < nseg + 8:
+                    raise DecodeError("truncated VLC-family payload")
+                return struct.unpack_from("<Q", archive._wire, a + nseg)[0]
+    if d.lengths[slot] < nseg + 8:
+        raise DecodeError("truncated VLC-family payload")
+    o = d.offsets[slot] + nseg
+    return int(np.frombuffer(d.buf(slot)[o:o + 8].cpu().numpy().tobytes(), np.uint64)[0])
+
+
+def _cpc_decode(archive: "Archive", views, status) -> None:
+    """Coordinate (RINDEX) and VLC velocity streams of a CPC archive."""
+    import torch
+    L = N.lib()
+    n, S = archive.n, archive.segment_size
+    nseg = (n + S - 1) // S
+    d = archive._dev
+    sb = archive._seg_bits
+    sb = sb if _is_tensor(sb) else torch.from_numpy(np.ascontiguousarray(sb, np.uint8)).cuda()
+    mn = archive._seg_minima
+    mn = (mn.contiguous() if _is_tensor(mn)
+          else torch.from_numpy(np.ascontiguousarray(mn, np.int64).reshape(-1)).cuda())
+    if int(archive.seg_bits.max(initial=0)) > 21:
+        raise DecodeError("segment bits above the 21-bit key budget")
+    ws = N.POOL.get("cpc_dec_ws", L.nbzg_cpc_decode_workspace_size(n, S))
+    jobs = []
+    if (archive.constant_mask & 0b111) != 0b111:
+        if d.offsets[COORD_SLOT] is None:
+            raise DecodeError("missing coordinate stream")
+        jobs.append((COORD_SLOT, 2, [0, 1, 2]))
+    if archive.mode is Mode.CPC2000:
+        for fi in (3, 4, 5):
+            if not archive.is_constant(fi):
+                if d.offsets[fi] is None or d.kinds[fi] != int(StreamKind.VLC_FIELD):
+                    raise DecodeError(f"missing stream for field {FIELD_NAMES[fi]}")
+                jobs.append((fi, 1, [fi]))
+    for slot, kind, fis in jobs:
+        a = N.CpcDecodeArgs()
+        a.payload = N.ptr(d.buf(slot)) + d.offsets[slot]
+        a.payload_len = d.lengths[slot]
+        a.kind = kind
+        a.indexed = 1 if archive.version >= 2 else 0
+        a.n = n
+        a.segment_size = S
+        a.total_bits = _cpc_total_bits(archive, slot, nseg)
+        a.seg_bits = N.ptr(sb)
+        a.seg_minima = N.ptr(mn)
+        for c, fi in enumerate(fis):
+            a.bound[c] = archive.bounds[fi]
+            if not archive.is_constant(fi):
+                if not (archive.bounds[fi] > 0):
+                    raise DecodeError(f"field {FIELD_NAMES[fi]}: invalid bound")
+                a.out[c] = N.ptr(views[fi])
+        a.workspace = N.ptr(ws)
+        a.workspace_bytes = ws.numel()
+        a.status = N.ptr(status)
+        rc = L.nbzg_cpc_decode(ctypes.byref(a), N.stream_handle())
+        if rc in (N.NBZG_BAD_ARG, N.NBZG_UNSUPPORTED, N.NBZG_TRUNCATED):
+            raise DecodeError(f"decompress: {N.STATUS_NAMES.get(rc, rc)}")
+        N.check(rc, "decompress")
 
 
 _KIND_CODE = {StreamKind.SZ_DQ: 3, StreamKind.SZ_FIELD: 0}
@@ -442,36 +604,32 @@ def decompress(archive: Archive, device: Optional[bool] = None) -> ParticleSnaps
     nf = 0
     d = archive._dev
     if d is None:
-        # host payloads (deserialized archive): one H2D of all payloads
-        by_field = {s.field: s for s in archive.streams}
+        # host payloads (in-memory archive): one H2D of all payloads
         blob = bytearray()
-        offs = {}
-        for fi in range(6):
-            if archive.is_constant(fi):
-                continue
-            st = by_field.get(fi)
-            if st is None:
-                raise DecodeError(f"missing stream for field {FIELD_NAMES[fi]}")
-            if st.kind not in _KIND_CODE:
-                raise DecodeError(f"stream kind {int(st.kind)} is not decodable by the B200 path")
-            offs[fi] = (len(blob), len(st.payload), _KIND_CODE[st.kind])
+        offs, lens, kinds = [None] * 7, [0] * 7, [int(StreamKind.SZ_DQ)] * 7
+        for st in archive.streams:
+            slot = COORD_SLOT if st.field == NO_FIELD else st.field
+            offs[slot], lens[slot], kinds[slot] = len(blob), len(st.payload), int(st.kind)
             blob += st.payload
             blob += b"\0" * ((-len(blob)) % 16)
         blob += b"\0" * 64
         arena = torch.frombuffer(bytearray(blob), dtype=torch.uint8).cuda()
-        d = _Device(arena, [offs[f][0] if f in offs else None for f in range(6)],
-                    [offs[f][1] if f in offs else 0 for f in range(6)],
-                    [StreamKind.SZ_DQ if (f in offs and offs[f][2] == 3) else StreamKind.SZ_FIELD
-                     for f in range(6)])
+        d = _Device(arena, offs, lens, kinds)
         archive._dev = d
-    base = N.ptr(d.arena)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    if archive.mode.stores_minima:
+        _cpc_decode(archive, views, status)
     for fi in range(6):
         if archive.is_constant(fi):
             views[fi].fill_(archive.constants[fi])
             continue
+        if archive.mode.stores_minima and (fi < 3 or archive.mode is Mode.CPC2000):
+            continue  # decoded by _cpc_decode
         if d.offsets[fi] is None:
             raise DecodeError(f"missing stream for field {FIELD_NAMES[fi]}")
-        a.payload[nf] = base + d.offsets[fi]
+        if StreamKind(d.kinds[fi]) not in _KIND_CODE:
+            raise DecodeError(f"stream kind {d.kinds[fi]} is not decodable by the B200 path")
+        a.payload[nf] = N.ptr(d.buf(fi)) + d.offsets[fi]
         a.payload_len[nf] = d.lengths[fi]
         a.kind[nf] = _KIND_CODE.get(StreamKind(d.kinds[fi]), -1)
         if a.kind[nf] >= 0 and archive.mode is Mode.SZ_LCF:
@@ -483,7 +641,6 @@ def decompress(archive: Archive, device: Optional[bool] = None) -> ParticleSnaps
             raise DecodeError(f"field {FIELD_NAMES[fi]}: invalid bound")
         a.out[nf] = N.ptr(views[fi])
         nf += 1
-    status = torch.zeros(1, dtype=torch.int32, device="cuda")
     if nf:
         ws_bytes = L.nbzg_decompress_workspace_size(n, archive.interval_count, nf)
         ws = N.POOL.get("decompress_ws", ws_bytes)

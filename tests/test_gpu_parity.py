@@ -8,7 +8,7 @@ point-wise error bound.  Run on a B200: pytest -m gpu."""
 import numpy as np
 import pytest
 
-from conftest import GOLDEN_CASES, golden_inputs, load_golden, sha
+from conftest import CPC_CASES, GOLDEN_CASES, golden_inputs, load_golden, sha
 
 pytestmark = pytest.mark.gpu
 
@@ -351,11 +351,60 @@ def test_bound_too_small_raises():
         nbz.compress(snap, "sz-lv-prx", nbz.ErrorBoundSpec.absolute(1e-30))
 
 
-def test_unsupported_modes_raise():
-    snap = nbz.ParticleSnapshot(*datagen.small_hacc(5))
+# ---------------------------------------------------------------- CPC2000 family
+
+@pytest.mark.parametrize("case", CPC_CASES)
+def test_cpc_archive_byte_identical_to_oracle(O, case):
+    """sz-cpc2000 / cpc2000 on the GPU: full-key sort (k = 0, no clamp),
+    segment minima, coordinate stream (raw first key + unsigned VLC deltas,
+    per-segment scheme, corrections), SZ or signed-VLC velocities; the v2
+    archive equals the oracle's byte for byte, and decoding it (and the
+    REFERENCE's own v1 archive) gives the oracle's / reference's values."""
+    g = load_golden(case)
+    fields = golden_inputs(g)
+    ss = int(g["segment_size"])
+    settings = nbz.Settings(segment_size=ss)
+    snap = nbz.ParticleSnapshot(*fields)
+    for tag in g["tags"]:
+        t = str(tag)
+        mode, eb = t.split("|")
+        res = nbz.compress(snap, mode, nbz.ErrorBoundSpec.relative(float(eb)), settings)
+        ref = O.compress_cpc(fields, mode, "rel", float(eb), segment_size=ss, fmt=2)
+        assert np.array_equal(res.order, ref["order"]), tag
+        wire = res.archive.serialized()
+        assert wire == ref["wire"], tag
+        assert res.archive.total_bytes() == len(wire)
+        out = nbz.decompress(res.archive)
+        odec = O.decompress_cpc(ref["wire"])
+        for fi in range(6):
+            assert np.array_equal(np.asarray(out.field(fi)).view(np.uint32),
+                                  odec[fi].view(np.uint32)), (tag, fi)
+            if not res.archive.is_constant(fi):
+                err = np.abs(fields[fi][ref["order"]].astype(np.float64)
+                             - np.asarray(out.field(fi)).astype(np.float64))
+                assert float(err.max()) <= res.archive.bounds[fi], (tag, fi)
+        # the reference's own (v1) archive decodes on the GPU to its values
+        from paper_1711_03888_b200 import io as nio
+        ar1 = nio.deserialize_archive(bytes(g[f"{t}|wire"]))
+        out1 = nbz.decompress(ar1)
+        for fi in range(6):
+            assert np.array_equal(np.asarray(out1.field(fi)).view(np.uint32),
+                                  g[f"{t}|recon{fi}"].view(np.uint32)), (tag, fi, "v1")
+        # v2 round trip through the wire
+        out2 = nbz.decompress(nio.deserialize_archive(wire))
+        for fi in range(6):
+            assert np.array_equal(np.asarray(out2.field(fi)), np.asarray(out.field(fi))), (tag, fi)
+
+
+def test_cpc_bound_too_small_raises():
+    """No key clamp in the CPC modes: > 21 index bits per field raises
+    BoundTooSmallError (rindex.py:185-190)."""
+    rng = np.random.default_rng(3)
+    f = [rng.uniform(0, 100, 5000).astype(np.float32) for _ in range(6)]
+    snap = nbz.ParticleSnapshot(*f)
     for mode in ("cpc2000", "sz-cpc2000"):
-        with pytest.raises(nbz.ValidationError):
-            nbz.compress(snap, mode, REL4)
+        with pytest.raises(nbz.BoundTooSmallError):
+            nbz.compress(snap, mode, nbz.ErrorBoundSpec.relative(1e-8))
 
 
 def test_corrupt_archives_rejected():
