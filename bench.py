@@ -432,7 +432,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--mode", default="sz-lv-prx", choices=["sz-lv", "sz-lv-prx"])
+    ap.add_argument("--mode", default="sz-lv-prx",
+                    choices=["sz-lv", "sz-lv-prx", "sz-cpc2000", "cpc2000"])
     ap.add_argument("--eb", type=float, default=1e-4)
     ap.add_argument("--n", type=int, default=None, help="particles per GPU (default 640^3)")
     ap.add_argument("--e2e-steps", type=int, default=2)

@@ -221,3 +221,16 @@ class _Pool:
 
 
 POOL = _Pool()
+
+_SIDE: Dict[int, list] = {}
+
+
+def side_streams(k: int):
+    """k persistent side CUDA streams of the current device (overlapping
+    independent per-stream decodes)."""
+    import torch
+    dev = torch.cuda.current_device()
+    lst = _SIDE.setdefault(dev, [])
+    while len(lst) < k:
+        lst.append(torch.cuda.Stream())
+    return lst[:k]

@@ -30,6 +30,8 @@
 
 namespace nbzg {
 
+void trace_mark(const char* name, cudaStream_t st);  // capi.cu (bench stage trace)
+
 constexpr int kCThreads = 512;
 
 __constant__ uint8_t c_vlcw[4][8] = {{2, 4, 6, 8, 12, 16, 24, 33},
@@ -802,6 +804,7 @@ int nbzg_cpc_plan(const nbzg_cpc_args* g, void* stream) {
   cpc_plan_kernel<<<dim3((unsigned)a.nseg, a.nstreams), kCThreads, 0, st>>>(a);
   count_launch();
   cpc_scan_kernel<<<a.nstreams, 1024, 0, st>>>(a);
+  trace_mark("cpc_plan", st);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
 
@@ -812,12 +815,14 @@ int nbzg_cpc_pack(const nbzg_cpc_args* g, void* stream) {
   if (!a.arena) return NBZG_BAD_ARG;
   if (a.n == 0) return NBZG_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  trace_mark(nullptr, st);
   count_launch();
   cpc_pack_kernel<<<dim3((unsigned)a.nseg, a.nstreams), kCThreads, 0, st>>>(a);
   count_launch();
   cpc_frame_kernel<<<a.nstreams, 256, 0, st>>>(a);
   count_launch();
   cpc_corr_kernel<<<dim3((unsigned)a.nseg, a.nstreams), kCThreads, 0, st>>>(a);
+  trace_mark("cpc_pack", st);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
 
@@ -854,6 +859,7 @@ int nbzg_cpc_decode(const nbzg_cpc_decode_args* g, void* stream) {
   const int64_t need = a.nseg + 8 + (int64_t)((a.total + 7) / 8) + (g->indexed ? 4 * a.nseg : 0);
   if (need > a.len) return NBZG_TRUNCATED;
   const uint8_t* ids = a.pay;
+  trace_mark(nullptr, st);
   if (!g->indexed) {
     a.len += 4 * a.nseg;  // no trailer: corrections run to the end
     count_launch();
@@ -866,6 +872,7 @@ int nbzg_cpc_decode(const nbzg_cpc_decode_args* g, void* stream) {
   cpc_dec_kernel<<<(unsigned)((a.nseg + 127) / 128), 128, 0, st>>>(a, ids);
   count_launch();
   cpc_dec_corr_kernel<<<a.kind == 2 ? 3 : 1, 256, 0, st>>>(a);
+  trace_mark("cpc_decode", st);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
 

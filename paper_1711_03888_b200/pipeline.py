@@ -543,7 +543,6 @@ def _cpc_decode(archive: "Archive", views, status) -> None:
           else torch.from_numpy(np.ascontiguousarray(mn, np.int64).reshape(-1)).cuda())
     if int(archive.seg_bits.max(initial=0)) > 21:
         raise DecodeError("segment bits above the 21-bit key budget")
-    ws = N.POOL.get("cpc_dec_ws", L.nbzg_cpc_decode_workspace_size(n, S))
     jobs = []
     if (archive.constant_mask & 0b111) != 0b111:
         if d.offsets[COORD_SLOT] is None:
@@ -555,7 +554,17 @@ def _cpc_decode(archive: "Archive", views, status) -> None:
                 if d.offsets[fi] is None or d.kinds[fi] != int(StreamKind.VLC_FIELD):
                     raise DecodeError(f"missing stream for field {FIELD_NAMES[fi]}")
                 jobs.append((fi, 1, [fi]))
-    for slot, kind, fis in jobs:
+    # one side stream per job: a decode launch holds one thread per segment,
+    # so independent streams overlap (e.g. the coordinate and three velocity
+    # streams of cpc2000)
+    totals = [_cpc_total_bits(archive, slot, nseg) for slot, _k, _f in jobs]  # before any launch
+    main = torch.cuda.current_stream()
+    ready = torch.cuda.Event()
+    ready.record(main)
+    side = N.side_streams(len(jobs))
+    for j, (slot, kind, fis) in enumerate(jobs):
+        sj = side[j]
+        sj.wait_event(ready)
         a = N.CpcDecodeArgs()
         a.payload = N.ptr(d.buf(slot)) + d.offsets[slot]
         a.payload_len = d.lengths[slot]
@@ -563,7 +572,7 @@ def _cpc_decode(archive: "Archive", views, status) -> None:
         a.indexed = 1 if archive.version >= 2 else 0
         a.n = n
         a.segment_size = S
-        a.total_bits = _cpc_total_bits(archive, slot, nseg)
+        a.total_bits = totals[j]
         a.seg_bits = N.ptr(sb)
         a.seg_minima = N.ptr(mn)
         for c, fi in enumerate(fis):
@@ -572,13 +581,17 @@ def _cpc_decode(archive: "Archive", views, status) -> None:
                 if not (archive.bounds[fi] > 0):
                     raise DecodeError(f"field {FIELD_NAMES[fi]}: invalid bound")
                 a.out[c] = N.ptr(views[fi])
-        a.workspace = N.ptr(ws)
-        a.workspace_bytes = ws.numel()
+        wsj = N.POOL.get(f"cpc_dec_ws{j}", L.nbzg_cpc_decode_workspace_size(n, S))
+        a.workspace = N.ptr(wsj)
+        a.workspace_bytes = wsj.numel()
         a.status = N.ptr(status)
-        rc = L.nbzg_cpc_decode(ctypes.byref(a), N.stream_handle())
+        rc = L.nbzg_cpc_decode(ctypes.byref(a), ctypes.c_void_p(sj.cuda_stream))
         if rc in (N.NBZG_BAD_ARG, N.NBZG_UNSUPPORTED, N.NBZG_TRUNCATED):
             raise DecodeError(f"decompress: {N.STATUS_NAMES.get(rc, rc)}")
         N.check(rc, "decompress")
+        done = torch.cuda.Event()
+        done.record(sj)
+        main.wait_event(done)
 
 
 _KIND_CODE = {StreamKind.SZ_DQ: 3, StreamKind.SZ_FIELD: 0}
