@@ -748,8 +748,23 @@ __global__ void __launch_bounds__(1024) chunk_scan_kernel(EArgs a, const uint32_
   }
 }
 
-// E3: one thread packs one 512-code block
+// E3: one thread packs one 512-code block at its known bit offset.  Completed
+// words go to a per-thread 16-word ring in shared memory (word-major, so the
+// lanes of a warp never conflict) with one predicated STS per code step --
+// no divergent register shuffling -- and every 8 codes the thread flushes the
+// 32-byte aligned 8-word groups it has completed with one 256-bit store.  The
+// words before the block's first aligned group go out as scalar stores; the
+// block's first partial word belongs to the block before (which completes it
+// with this block's leading bits).
 constexpr int kE3Threads = 384;
+constexpr int kE3Ring = 16;  // words per thread
+
+NBZG_DEV void st_v8_u32(uint32_t* p, const uint32_t (&v)[8]) {
+  asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+
 __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, const uint64_t* coff,
                                                                    const uint32_t* bpre,
                                                                    int ctas_per_field) {
@@ -764,6 +779,9 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
       reinterpret_cast<uint4*>(s_win)[i] = __ldg(g + i);
   }
   __syncthreads();
+  // ring word j of this thread at ring_s + 4 * j * blockDim.x
+  const uint32_t ring_s = sh_addr(s_win + kEncWin) + 4u * threadIdx.x;
+  const uint32_t rstride = 4u * blockDim.x;
   const WinTab T{s_win, (uint32_t)(a.nbins / 2 + 1 - kEncWin / 2), a.lut + field * a.nbins};
   const int64_t nb = a.nchunks * kBlkPerChunk;
   const uint16_t* codes = a.codes + field * a.code_stride;
@@ -780,61 +798,72 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
     const uint64_t B = off[c] + bp[k];
     const uint64_t Bend = (k + 1) % kBlkPerChunk ? off[c] + bp[k + 1] : off[c + 1];
     const uint4* cp4 = reinterpret_cast<const uint4*>(codes + s0);
-    uint64_t acc = 0;
+    // 32-bit MSB-aligned pending word `cur` holding `nacc` < 32 bits; every
+    // completed word goes to the ring with one predicated STS (no branch)
+    uint32_t cur = 0;
     uint32_t nacc = (uint32_t)(B & 31);
-    // completed words: scalar stores up to the first 16-byte boundary at or
-    // after the first owned word (the first partial word belongs to the
-    // block before), then buffered 16-byte stores of aligned word quads
     uint64_t widx = B >> 5;
-    const uint64_t fo = (B + 31) >> 5;
+    const uint64_t fo = (B + 31) >> 5;                  // first owned word
     const uint64_t va = ((fo + ow + 7) & ~7ull) - ow;  // first 32-byte aligned owned word
-    uint32_t q[7] = {0, 0, 0, 0, 0, 0, 0};  // shift register of the pending words
-    auto emit = [&](uint32_t w) {
-      w = __byte_perm(w, 0, 0x0123);
-      if (widx < va) {
-        st_pred_u32(outw + widx, w, widx >= fo);
-      } else {
-        // one 256-bit store per aligned 8-word sector group
-        st_pred_v8(outw + widx - 7, q, w, ((uint32_t)(widx + ow) & 7u) == 7u);
+    uint64_t fl = widx;                                 // next ring word to flush
+    // l in [1, 32]: append the low l bits of v
+    auto put32 = [&](uint32_t v, uint32_t l) {
+      const uint32_t wl = v << (32 - l);                 // MSB-aligned
+      cur |= wl >> nacc;
+      const uint32_t spill = __funnelshift_lc(0u, wl, 32 - nacc);  // wl << (32 - nacc), 0 at 32
+      const uint32_t t = nacc + l;
+      const bool full = t >= 32;
+      const uint32_t slot = ring_s + rstride * (uint32_t)(widx & (kE3Ring - 1));
+      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.shared.u32 [%0], %1;\n}\n" ::"r"(slot),
+                   "r"(__byte_perm(cur, 0, 0x0123)), "r"((uint32_t)full)
+                   : "memory");
+      widx += full ? 1 : 0;
+      cur = full ? spill : cur;
+      nacc = full ? t - 32 : t;
+    };
+    auto put64 = [&](uint64_t v, uint32_t l) {  // l <= 64
+      if (l > 32) {
+        put32((uint32_t)(v >> 32), l - 32);
+        put32((uint32_t)v, 32);
+      } else if (l) {
+        put32((uint32_t)v, l);
+      }
+    };
+    auto flush = [&]() {  // head words one by one, then complete aligned 8-word groups
+      while (fl < widx) {
+        if (fl < va) {
+          if (fl >= fo) outw[fl] = lds_u32(ring_s + rstride * (uint32_t)(fl & (kE3Ring - 1)));
+          fl++;
+        } else if (fl + 8 <= widx) {
+          uint32_t v[8];
 #pragma unroll
-        for (int u = 0; u < 6; u++) q[u] = q[u + 1];
-        q[6] = w;
+          for (int u = 0; u < 8; u++)
+            v[u] = lds_u32(ring_s + rstride * (uint32_t)((fl + u) & (kE3Ring - 1)));
+          st_v8_u32(outw + fl, v);
+          fl += 8;
+        } else {
+          break;
+        }
       }
-      widx++;
-    };
-    auto append = [&](uint32_t w, uint32_t l) {  // l <= 26
-      acc |= (uint64_t)w << (64 - nacc - l);
-      nacc += l;
-      if (nacc >= 32) {
-        emit((uint32_t)(acc >> 32));
-        acc <<= 32;
-        nacc -= 32;
-      }
-    };
-    auto put_slow = [&](uint64_t v, uint32_t nb2) {
-      Acc A{acc, (int)nacc};
-      acc_put(A, v, (int)nb2, emit);
-      acc = A.acc;
-      nacc = (uint32_t)A.nacc;
     };
     auto put_code = [&](uint32_t code, int64_t pos) {
       uint64_t w;
       uint32_t l;
       win_word(T, code, w, l);
-      put_slow(w, l);
-      if (code == 0) put_slow(esc_value_bits(a, field, pos), 32);
+      put64(w, l);
+      if (code == 0) put32(esc_value_bits(a, field, pos), 32);
     };
     const int ng = mc >> 3;
     uint4 n0 = ng > 0 ? __ldg(cp4) : make_uint4(0, 0, 0, 0);
     uint4 n1 = ng > 1 ? __ldg(cp4 + 1) : make_uint4(0, 0, 0, 0);
     uint4 n2 = ng > 2 ? __ldg(cp4 + 2) : make_uint4(0, 0, 0, 0);
     for (int g = 0; g < ng; g++) {
-      const uint4 cur = n0;
+      const uint4 cu = n0;
       n0 = n1;
       n1 = n2;
       if (g + 3 < ng) n2 = __ldg(cp4 + g + 3);
       uint32_t cv[8], e[8];
-      unpack8(cur, cv);
+      unpack8(cu, cv);
       bool hit = true;
 #pragma unroll
       for (int q = 0; q < 8; q++) {
@@ -843,24 +872,28 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
         hit &= e[q] != 0;
       }
       if (hit) {
+        // <= 8 x 26 bits: at most 7 new words; the ring (16) holds < 8 after a flush
 #pragma unroll
-        for (int q = 0; q < 8; q++) append(e[q] >> 6, e[q] & 63u);
+        for (int q = 0; q < 8; q++) put32(e[q] >> 6, e[q] & 63u);
       } else {
-#pragma unroll
-        for (int q = 0; q < 8; q++) put_code(cv[q], s0 + 8 * g + q);
+#pragma unroll 1
+        for (int q = 0; q < 8; q++) {
+          put_code(cv[q], s0 + 8 * g + q);
+          flush();  // long codes and escapes: up to 3 words per code
+        }
       }
+      flush();
     }
-    for (int j = 8 * ng; j < mc; j++) put_code(codes[s0 + j], s0 + j);
-    // flush buffered words of the last (incomplete) aligned quad
-    if (widx > va) {
-      const uint32_t nq = (uint32_t)(widx + ow) & 7u;  // words [widx - nq, widx) pending
-#pragma unroll
-      for (uint32_t u = 0; u < 7; u++)  // the last nq shift-register slots
-        if (u >= 7 - nq) outw[widx - 7 + u] = q[u];
+    for (int j = 8 * ng; j < mc; j++) {
+      put_code(codes[s0 + j], s0 + j);
+      flush();
     }
+    // ring words of the last (incomplete) aligned group
+    for (uint64_t u = fl; u < widx; u++)
+      if (u >= fo) outw[u] = lds_u32(ring_s + rstride * (uint32_t)(u & (kE3Ring - 1)));
     // final partial word: completed with the leading bits that follow
     if (nacc > 0 && (Bend >> 5) >= fo) {
-      uint32_t w = (uint32_t)(acc >> 32);
+      uint32_t w = cur;
       if (s0 + mc < a.n) w |= head_bits_from(a, field, codes, T, s0 + mc, 32 - (int)nacc) >> nacc;
       outw[widx] = __byte_perm(w, 0, 0x0123);
     }
@@ -903,7 +936,7 @@ int launch_encode(const Plan& p, cudaStream_t st) {
     if (!attr3) {
       cudaFuncSetAttribute(chunk_bits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
       cudaFuncSetAttribute(encode_tpc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           4 * kEncWin);
+                           4 * kEncWin + 4 * kE3Ring * kE3Threads);
       attr3 = true;
     }
     int g1 = max(1, 2 * sm_count() / 6);
@@ -915,7 +948,8 @@ int launch_encode(const Plan& p, cudaStream_t st) {
     int g3 = max(1, 2 * sm_count() / 6);
     if (g3 > (nb + kE3Threads - 1) / kE3Threads) g3 = (int)((nb + kE3Threads - 1) / kE3Threads);
     count_launch();
-    encode_tpc_kernel<<<dim3(g3, 6), kE3Threads, 4 * kEncWin, st>>>(a, coff, bpre, g3);
+    encode_tpc_kernel<<<dim3(g3, 6), kE3Threads, 4 * kEncWin + 4 * kE3Ring * kE3Threads, st>>>(
+        a, coff, bpre, g3);
   } else if (p.nbins == 65536) {
     const size_t sm = 4 * kEncWin + kEFWarps * 64 * 12 + kEFWarps * 32 * 4;
     static bool attr = false;
