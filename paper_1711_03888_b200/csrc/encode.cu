@@ -781,6 +781,8 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
   __syncthreads();
   // ring word j of this thread at ring_s + 4 * j * blockDim.x
   const uint32_t ring_s = sh_addr(s_win + kEncWin) + 4u * threadIdx.x;
+  uint32_t win_s;  // opaque copy: no per-lookup generic-to-shared conversion
+  asm volatile("mov.u32 %0, %1;" : "=r"(win_s) : "r"(sh_addr(s_win)));
   const uint32_t rstride = 4u * blockDim.x;
   const WinTab T{s_win, (uint32_t)(a.nbins / 2 + 1 - kEncWin / 2), a.lut + field * a.nbins};
   const int64_t nb = a.nchunks * kBlkPerChunk;
@@ -806,6 +808,9 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
     const uint64_t fo = (B + 31) >> 5;                  // first owned word
     const uint64_t va = ((fo + ow + 7) & ~7ull) - ow;  // first 32-byte aligned owned word
     uint64_t fl = widx;                                 // next ring word to flush
+    // ring slot of stream word u: (u + ow) & 15, so 32-byte aligned groups
+    // occupy slots 0-7 or 8-15; `rs` = slot counter of the next word
+    uint32_t rs = (uint32_t)(widx + ow);
     // l in [1, 32]: append the low l bits of v
     auto put32 = [&](uint32_t v, uint32_t l) {
       const uint32_t wl = v << (32 - l);                 // MSB-aligned
@@ -813,13 +818,13 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
       const uint32_t spill = __funnelshift_lc(0u, wl, 32 - nacc);  // wl << (32 - nacc), 0 at 32
       const uint32_t t = nacc + l;
       const bool full = t >= 32;
-      const uint32_t slot = ring_s + rstride * (uint32_t)(widx & (kE3Ring - 1));
+      const uint32_t slot = ring_s + rstride * (rs & (kE3Ring - 1));
       asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.shared.u32 [%0], %1;\n}\n" ::"r"(slot),
                    "r"(__byte_perm(cur, 0, 0x0123)), "r"((uint32_t)full)
                    : "memory");
-      widx += full ? 1 : 0;
+      rs += full ? 1u : 0u;
       cur = full ? spill : cur;
-      nacc = full ? t - 32 : t;
+      nacc = t & 31u;
     };
     auto put64 = [&](uint64_t v, uint32_t l) {  // l <= 64
       if (l > 32) {
@@ -829,16 +834,20 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
         put32((uint32_t)v, l);
       }
     };
+    auto ring_at = [&](uint64_t u) {
+      return lds_u32(ring_s + rstride * ((uint32_t)(u + ow) & (kE3Ring - 1)));
+    };
     auto flush = [&]() {  // head words one by one, then complete aligned 8-word groups
+      widx = (B >> 5) + (uint32_t)(rs - (uint32_t)((B >> 5) + ow));
       while (fl < widx) {
         if (fl < va) {
-          if (fl >= fo) outw[fl] = lds_u32(ring_s + rstride * (uint32_t)(fl & (kE3Ring - 1)));
+          if (fl >= fo) outw[fl] = ring_at(fl);
           fl++;
         } else if (fl + 8 <= widx) {
+          const uint32_t base = ring_s + rstride * ((uint32_t)(fl + ow) & 8u);
           uint32_t v[8];
 #pragma unroll
-          for (int u = 0; u < 8; u++)
-            v[u] = lds_u32(ring_s + rstride * (uint32_t)((fl + u) & (kE3Ring - 1)));
+          for (int u = 0; u < 8; u++) v[u] = lds_u32(base + rstride * u);
           st_v8_u32(outw + fl, v);
           fl += 8;
         } else {
@@ -868,17 +877,23 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
 #pragma unroll
       for (int q = 0; q < 8; q++) {
         const uint32_t wi = cv[q] - T.wlo;
-        e[q] = wi < (uint32_t)kEncWin ? T.win[wi] : 0u;
-        hit &= e[q] != 0;
+        uint32_t v = 0;
+        if (wi < (uint32_t)kEncWin)
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(win_s + 4u * wi));
+        e[q] = v;
+        hit &= v != 0;
       }
       if (hit) {
         // <= 8 x 26 bits: at most 7 new words; the ring (16) holds < 8 after a flush
 #pragma unroll
         for (int q = 0; q < 8; q++) put32(e[q] >> 6, e[q] & 63u);
       } else {
+        // codes re-extracted from the packed group (no dynamically indexed array)
+        const uint64_t lo = ((uint64_t)cu.y << 32) | cu.x, hi = ((uint64_t)cu.w << 32) | cu.z;
 #pragma unroll 1
         for (int q = 0; q < 8; q++) {
-          put_code(cv[q], s0 + 8 * g + q);
+          const uint32_t code = (uint32_t)(((q < 4 ? lo : hi) >> (16 * (q & 3))) & 0xffffu);
+          put_code(code, s0 + 8 * g + q);
           flush();  // long codes and escapes: up to 3 words per code
         }
       }
@@ -889,8 +904,9 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
       flush();
     }
     // ring words of the last (incomplete) aligned group
+    widx = (B >> 5) + (uint32_t)(rs - (uint32_t)((B >> 5) + ow));
     for (uint64_t u = fl; u < widx; u++)
-      if (u >= fo) outw[u] = lds_u32(ring_s + rstride * (uint32_t)(u & (kE3Ring - 1)));
+      if (u >= fo) outw[u] = ring_at(u);
     // final partial word: completed with the leading bits that follow
     if (nacc > 0 && (Bend >> 5) >= fo) {
       uint32_t w = cur;
