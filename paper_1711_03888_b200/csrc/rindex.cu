@@ -249,10 +249,12 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
       return;
     }
     const int w = sp.w;
-    if (sizeof(KeyT) == 4 && 3 * w > 32) {
-      if (threadIdx.x == 0) a.tile_flags[t] = 1;
-      return;  // redone by the u64 pass
-    }
+    // u32 keys hold 3w <= 32 bits; wider keys (the CPC modes' full keys,
+    // ignored groups 0) are sorted in two LSD phases over the same u32
+    // array: the low 32 key bits first, then the key's high bits
+    // (recomputed from the coordinates) -- stable passes, so the result is
+    // the full-key order and the tile keeps 2 CTAs per SM.
+    const bool split = sizeof(KeyT) == 4 && 3 * w > 32;
     if (threadIdx.x == 0) {
       a.seg_bits[(s0) / a.S] = (uint8_t)sp.bits;
       if (a.minima)
@@ -275,6 +277,13 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
         cm[c] = 0.5f - __fmaf_ru(tmax, 2.384185791015625e-07f, 9.5367431640625e-07f);
       }
       const float i0 = fm[0].inv32, i1 = fm[1].inv32, i2 = fm[2].inv32;
+      int part = 0;  // split keys: 0 = low 32 bits, 1 = high bits
+      auto mk = [&](uint64_t u0, uint64_t u1, uint64_t u2) -> KeyT {
+        if (sizeof(KeyT) == 8) return (KeyT)make_key<uint64_t>(u0, u1, u2);
+        if (!split) return (KeyT)make_key<uint32_t>(u0, u1, u2);
+        const uint64_t k = make_key<uint64_t>(u0, u1, u2);
+        return (KeyT)(part ? (k >> 32) : k);
+      };
       auto key_fast = [&](float x0, float x1, float x2) -> KeyT {
         const float xv[3] = {x0, x1, x2};
         const float iv[3] = {i0, i1, i2};
@@ -289,7 +298,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
           const int32_t mm = (int32_t)(c == 0 ? m0 : (c == 1 ? m1 : m2));
           u[c] = (uint32_t)(k - mm) >> shift;
         }
-        return make_key<KeyT>(u[0], u[1], u[2]);
+        return mk(u[0], u[1], u[2]);
       };
       auto key_of = [&](float x0, float x1, float x2) -> KeyT {
         const float xv[3] = {x0, x1, x2};
@@ -300,38 +309,45 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
           int64_t mm = c == 0 ? m0 : (c == 1 ? m1 : m2);
           u[c] = (uint64_t)(iv - mm) >> shift;
         }
-        return make_key<KeyT>(u[0], u[1], u[2]);
+        return mk(u[0], u[1], u[2]);
       };
       const int m4 = (s0 & 3) ? 0 : m >> 2;  // float4 path needs 16-byte aligned segments
       const float4* x4[3] = {reinterpret_cast<const float4*>(a.x[0] + s0),
                              reinterpret_cast<const float4*>(a.x[1] + s0),
                              reinterpret_cast<const float4*>(a.x[2] + s0)};
-      if (small && sizeof(KeyT) == 4) {
+      auto fill = [&]() {
+        if (small && sizeof(KeyT) == 4) {
 #pragma unroll 2
-        for (int v = threadIdx.x; v < m4; v += kSortThreads) {
-          const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
-          KeyT* kd = keys + lo + 4 * v;
-          kd[0] = key_fast(q0.x, q1.x, q2.x);
-          kd[1] = key_fast(q0.y, q1.y, q2.y);
-          kd[2] = key_fast(q0.z, q1.z, q2.z);
-          kd[3] = key_fast(q0.w, q1.w, q2.w);
-        }
-      } else {
+          for (int v = threadIdx.x; v < m4; v += kSortThreads) {
+            const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
+            KeyT* kd = keys + lo + 4 * v;
+            kd[0] = key_fast(q0.x, q1.x, q2.x);
+            kd[1] = key_fast(q0.y, q1.y, q2.y);
+            kd[2] = key_fast(q0.z, q1.z, q2.z);
+            kd[3] = key_fast(q0.w, q1.w, q2.w);
+          }
+        } else {
 #pragma unroll 2
-        for (int v = threadIdx.x; v < m4; v += kSortThreads) {
-          const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
-          KeyT* kd = keys + lo + 4 * v;
-          kd[0] = key_of(q0.x, q1.x, q2.x);
-          kd[1] = key_of(q0.y, q1.y, q2.y);
-          kd[2] = key_of(q0.z, q1.z, q2.z);
-          kd[3] = key_of(q0.w, q1.w, q2.w);
+          for (int v = threadIdx.x; v < m4; v += kSortThreads) {
+            const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
+            KeyT* kd = keys + lo + 4 * v;
+            kd[0] = key_of(q0.x, q1.x, q2.x);
+            kd[1] = key_of(q0.y, q1.y, q2.y);
+            kd[2] = key_of(q0.z, q1.z, q2.z);
+            kd[3] = key_of(q0.w, q1.w, q2.w);
+          }
         }
+        for (int i = 4 * m4 + threadIdx.x; i < m; i += kSortThreads)
+          keys[lo + i] = key_of(a.x[0][s0 + i], a.x[1][s0 + i], a.x[2][s0 + i]);
+        __syncthreads();
+      };
+      // ---- 3. stable radix sort over 3w bits (one call site: one inlined copy)
+      for (int ph = 0; ph < (split ? 2 : 1); ph++) {
+        part = ph;
+        fill();
+        const int nbits = split ? (ph == 0 ? 32 : 3 * w - 32) : 3 * w;
+        block_sort_range<KeyT>(keys, perm, lo, m, nbits, whist, scan_tmp);
       }
-      for (int i = 4 * m4 + threadIdx.x; i < m; i += kSortThreads)
-        keys[lo + i] = key_of(a.x[0][s0 + i], a.x[1][s0 + i], a.x[2][s0 + i]);
-      __syncthreads();
-      // ---- 3. stable radix sort over 3w bits
-      block_sort_range<KeyT>(keys, perm, lo, m, 3 * w, whist, scan_tmp);
     }
     __syncthreads();
   }
