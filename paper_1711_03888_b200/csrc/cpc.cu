@@ -60,6 +60,36 @@ NBZG_DEV uint64_t compact3_64(uint64_t v) {
 }
 NBZG_DEV int vlc_len(int b, int sid) { return (b < 7 ? b + 1 : 7) + c_vlcw[sid][b]; }
 
+// Shared-memory tables of a CPC CTA: VLC bucket and code length by the
+// magnitude's bit length (m < 2^w  <=>  bitlen(m) <= w), bucket widths, and
+// the 11-bit 3-way bit spread for key interleaving (interleave3,
+// _kernels.py:757-786: bit j of a field -> key bit 3j).
+struct CTabs {
+  uint8_t bkt[4][65];   // bucket, 8 = no bucket
+  uint8_t len[4][65];   // prefix + payload bits, 0 = no bucket
+  uint8_t w[4][8];
+  uint32_t sp11[2048];
+};
+NBZG_DEV void ctabs_init(CTabs& T) {
+  for (int i = threadIdx.x; i < 4 * 65; i += blockDim.x) {
+    const int sid = i / 65, bl = i % 65;
+    int b = 8;
+    for (int bb = 0; bb < 8; bb++)
+      if (c_vlcw[sid][bb] >= 64 || bl <= c_vlcw[sid][bb]) {
+        b = bb;
+        break;
+      }
+    T.bkt[sid][bl] = (uint8_t)b;
+    T.len[sid][bl] = (uint8_t)(b < 8 ? vlc_len(b, sid) : 0);
+  }
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) T.w[i >> 3][i & 7] = c_vlcw[i >> 3][i & 7];
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) T.sp11[i] = spread3_32((uint32_t)i);
+}
+NBZG_DEV int bitlen_u64(uint64_t m) { return 64 - __clzll((long long)m); }
+NBZG_DEV uint64_t spread21(const CTabs& T, uint64_t v) {
+  return (uint64_t)T.sp11[v & 0x7ffu] | ((uint64_t)T.sp11[(v >> 11) & 0x3ffu] << 33);
+}
+
 struct CStream {
   // per stream (0 coordinates, 1..3 velocity fields 3..5)
   uint64_t* seg_cost;  // [nseg] bits of the segment (raw key included)
@@ -130,7 +160,9 @@ template <>
 struct Eval<0> {
   float cm[3];
   uint32_t cmask;  // constant coordinates
-  NBZG_DEV void init(const CArgs& a) {
+  const CTabs* tabs;
+  NBZG_DEV void init(const CArgs& a, const CTabs* t) {
+    tabs = t;
     cmask = a.meta->mask & 7u;
     for (int c = 0; c < 3; c++) cm[c] = field_margin(a.meta->f[c]);
   }
@@ -144,7 +176,7 @@ struct Eval<0> {
       const nbzg_field_meta& fm = a.meta->f[c];
       const float x = a.f[c][src];
       const int64_t iv = integerize_m(x, fm, cm[c], big);
-      k |= spread3_64((uint64_t)(iv - a.minima[3 * p.s + c])) << (2 - c);
+      k |= spread21(*tabs, (uint64_t)(iv - a.minima[3 * p.s + c])) << (2 - c);
       if (needs_corr(x, iv, fm)) corr |= 1u << c;
     }
     return k;
@@ -169,6 +201,9 @@ NBZG_DEV uint64_t vel_mag(const CArgs& a, const SegPos& p, int64_t i, float cm, 
 __global__ void __launch_bounds__(kCThreads) cpc_plan_kernel(CArgs a) {
   const int sidx = blockIdx.y;
   if (stream_absent(a, sidx)) return;
+  __shared__ CTabs tabs;
+  ctabs_init(tabs);
+  __syncthreads();
   const SegPos p = seg_pos(a, blockIdx.x);
   const int64_t m = p.hi - p.lo;
   const int64_t cpt = (m + kCThreads - 1) / kCThreads;
@@ -180,7 +215,7 @@ __global__ void __launch_bounds__(kCThreads) cpc_plan_kernel(CArgs a) {
   if (i0 < i1) {
     if (sidx == 0) {
       Eval<0> E;
-      E.init(a);
+      E.init(a, &tabs);
       uint32_t cr;
       uint64_t prev = i0 > p.lo ? E.key(a, p, i0 - 1, cr, big) : 0;
       for (int64_t i = i0; i < i1; i++) {
@@ -188,10 +223,12 @@ __global__ void __launch_bounds__(kCThreads) cpc_plan_kernel(CArgs a) {
 #pragma unroll
         for (int c = 0; c < 3; c++) nc[c] += (cr >> c) & 1u;
         if (i > p.lo) {
-          const uint64_t d = k - prev;
-          const int b0 = vlc_bucket(d, c0), b1 = vlc_bucket(d, c0 + 1);
-          if (b0 == 8) bad0 = 1; else cost0 += vlc_len(b0, c0);
-          if (b1 == 8) bad1 = 1; else cost1 += vlc_len(b1, c0 + 1);
+          const int bl = bitlen_u64(k - prev);
+          const uint32_t l0 = tabs.len[c0][bl], l1 = tabs.len[c0 + 1][bl];
+          bad0 |= l0 == 0;
+          bad1 |= l1 == 0;
+          cost0 += l0;
+          cost1 += l1;
         }
         prev = k;
       }
@@ -206,9 +243,12 @@ __global__ void __launch_bounds__(kCThreads) cpc_plan_kernel(CArgs a) {
                             : sidx == 2 ? vel_mag<2>(a, p, i, cm, cr, big)
                                         : vel_mag<3>(a, p, i, cm, cr, big);
         nc[0] += cr;
-        const int b0 = vlc_bucket(ms, c0), b1 = vlc_bucket(ms, c0 + 1);
-        if (b0 == 8) bad0 = 1; else cost0 += vlc_len(b0, c0);
-        if (b1 == 8) bad1 = 1; else cost1 += vlc_len(b1, c0 + 1);
+        const int bl = bitlen_u64(ms);
+        const uint32_t l0 = tabs.len[c0][bl], l1 = tabs.len[c0 + 1][bl];
+        bad0 |= l0 == 0;
+        bad1 |= l1 == 0;
+        cost0 += l0;
+        cost1 += l1;
       }
     }
   }
@@ -352,17 +392,20 @@ struct BitSink {
   }
 };
 
-NBZG_DEV void vlc_emit(BitSink& B, uint64_t m, int sid) {
-  const int b = vlc_bucket(m, sid);
+NBZG_DEV void vlc_emit(BitSink& B, uint64_t m, int sid, const CTabs& T) {
+  const int b = T.bkt[sid][bitlen_u64(m)];
   if (b < 7) B.put((1u << (b + 1)) - 2, b + 1);
   else B.put(127, 7);
-  B.put64(m, c_vlcw[sid][b]);
+  B.put64(m, T.w[sid][b]);
 }
 
 // grid (nseg, nstreams): the bitstream of every segment
 __global__ void __launch_bounds__(kCThreads) cpc_pack_kernel(CArgs a) {
   const int sidx = blockIdx.y;
   if (stream_absent(a, sidx)) return;
+  __shared__ CTabs tabs;
+  ctabs_init(tabs);
+  __syncthreads();
   const SegPos p = seg_pos(a, blockIdx.x);
   const CStream& S = a.st[sidx];
   const int sid = S.seg_id[p.s];
@@ -373,7 +416,7 @@ __global__ void __launch_bounds__(kCThreads) cpc_pack_kernel(CArgs a) {
   bool big = false;
   Eval<0> E;
   float cm = 0.0f;
-  if (sidx == 0) E.init(a);
+  if (sidx == 0) E.init(a, &tabs);
   else if (sidx == 1) vel_init<1>(a, cm);
   else if (sidx == 2) vel_init<2>(a, cm);
   else vel_init<3>(a, cm);
@@ -392,11 +435,11 @@ __global__ void __launch_bounds__(kCThreads) cpc_pack_kernel(CArgs a) {
       uint64_t pv = prev;
       for (int64_t i = i0; i < i1; i++) {
         const uint64_t k = E.key(a, p, i, cr, big);
-        L += i == p.lo ? (uint64_t)kb : (uint64_t)vlc_len(vlc_bucket(k - pv, sid), sid);
+        L += i == p.lo ? (uint64_t)kb : (uint64_t)tabs.len[sid][bitlen_u64(k - pv)];
         pv = k;
       }
     } else {
-      for (int64_t i = i0; i < i1; i++) L += vlc_len(vlc_bucket(value(i, cr), sid), sid);
+      for (int64_t i = i0; i < i1; i++) L += tabs.len[sid][bitlen_u64(value(i, cr))];
     }
   }
   __shared__ unsigned long long tmp[33];
@@ -411,11 +454,11 @@ __global__ void __launch_bounds__(kCThreads) cpc_pack_kernel(CArgs a) {
       for (int64_t i = i0; i < i1; i++) {
         const uint64_t k = E.key(a, p, i, cr, big);
         if (i == p.lo) B.put64(k, kb);
-        else vlc_emit(B, k - pv, sid);
+        else vlc_emit(B, k - pv, sid, tabs);
         pv = k;
       }
     } else {
-      for (int64_t i = i0; i < i1; i++) vlc_emit(B, value(i, cr), sid);
+      for (int64_t i = i0; i < i1; i++) vlc_emit(B, value(i, cr), sid, tabs);
     }
     B.finish();
   }
@@ -435,19 +478,22 @@ NBZG_DEV void put_rec(uint8_t* d, uint64_t pos, float v) {
 __global__ void __launch_bounds__(kCThreads) cpc_corr_kernel(CArgs a) {
   const int sidx = blockIdx.y;
   if (stream_absent(a, sidx)) return;
+  __shared__ CTabs tabs;
   const SegPos p = seg_pos(a, blockIdx.x);
   const CStream& S = a.st[sidx];
   const int nl = sidx == 0 ? 3 : 1;
   bool any = false;
   for (int c = 0; c < nl; c++) any |= S.corr_cnt[(size_t)c * a.nseg + p.s] != 0;
   if (!any) return;  // block-uniform
+  ctabs_init(tabs);
+  __syncthreads();
   const int64_t m = p.hi - p.lo;
   const int64_t cpt = (m + kCThreads - 1) / kCThreads;
   const int64_t i0 = p.lo + threadIdx.x * cpt, i1 = min(p.hi, i0 + cpt);
   bool big = false;
   Eval<0> E;
   float cm = 0.0f;
-  if (sidx == 0) E.init(a);
+  if (sidx == 0) E.init(a, &tabs);
   else if (sidx == 1) vel_init<1>(a, cm);
   else if (sidx == 2) vel_init<2>(a, cm);
   else vel_init<3>(a, cm);
@@ -649,6 +695,9 @@ __global__ void cpc_dec_walk_kernel(KArgsD a, const uint8_t* ids) {
 // one thread per segment: raw first key + VLC deltas (coordinates) or VLC
 // magnitudes (velocities); writes the reconstructed floats
 __global__ void __launch_bounds__(128) cpc_dec_kernel(KArgsD a, const uint8_t* ids) {
+  __shared__ uint8_t sw[4][8];  // bucket widths (per-thread scheme: no divergent constant loads)
+  if (threadIdx.x < 32) sw[threadIdx.x >> 3][threadIdx.x & 7] = c_vlcw[threadIdx.x >> 3][threadIdx.x & 7];
+  __syncthreads();
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= a.nseg) return;
   const int64_t lo = s * a.S, hi = min(a.n, lo + a.S);
@@ -675,7 +724,7 @@ __global__ void __launch_bounds__(128) cpc_dec_kernel(KArgsD a, const uint8_t* i
         const int o = B.ones7();
         const int pl = o < 7 ? o + 1 : 7;
         B.get(pl);
-        const int w = c_vlcw[sid][o];
+        const int w = sw[sid][o];
         key += B.get64(w);
         pos += pl + w;
       }
@@ -688,7 +737,7 @@ __global__ void __launch_bounds__(128) cpc_dec_kernel(KArgsD a, const uint8_t* i
       const int o = B.ones7();
       const int pl = o < 7 ? o + 1 : 7;
       B.get(pl);
-      const int w = c_vlcw[sid][o];
+      const int w = sw[sid][o];
       const uint64_t mm = B.get64(w);
       pos += pl + w;
       const int64_t h = (int64_t)(mm >> 1);
