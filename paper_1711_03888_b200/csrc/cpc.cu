@@ -97,6 +97,7 @@ struct CStream {
   uint64_t* seg_off;   // [nseg + 1] exclusive bit offsets
   uint32_t* corr_cnt;  // [3][nseg] correction records per list
   uint32_t* corr_off;  // [3][nseg + 1]
+  uint32_t* run_bits;  // [2][nseg][kCThreads] bits of each thread's run per candidate
 };
 
 struct CArgs {
@@ -166,6 +167,7 @@ struct Eval<0> {
     cmask = a.meta->mask & 7u;
     for (int c = 0; c < 3; c++) cm[c] = field_margin(a.meta->f[c]);
   }
+  template <bool CORR = true>
   NBZG_DEV uint64_t key(const CArgs& a, const SegPos& p, int64_t i, uint32_t& corr, bool& big) {
     const int64_t src = src_of(a, p, i);
     uint64_t k = 0;
@@ -177,7 +179,7 @@ struct Eval<0> {
       const float x = a.f[c][src];
       const int64_t iv = integerize_m(x, fm, cm[c], big);
       k |= spread21(*tabs, (uint64_t)(iv - a.minima[3 * p.s + c])) << (2 - c);
-      if (needs_corr(x, iv, fm)) corr |= 1u << c;
+      if (CORR && needs_corr(x, iv, fm)) corr |= 1u << c;
     }
     return k;
   }
@@ -185,14 +187,14 @@ struct Eval<0> {
 
 template <int ST>
 NBZG_DEV void vel_init(const CArgs& a, float& cm) { cm = field_margin(a.meta->f[2 + ST]); }
-template <int ST>
+template <int ST, bool CORR = true>
 NBZG_DEV uint64_t vel_mag(const CArgs& a, const SegPos& p, int64_t i, float cm, uint32_t& corr,
                           bool& big) {
   const int fi = 2 + ST;
   const nbzg_field_meta& fm = a.meta->f[fi];
   const float x = a.f[fi][src_of(a, p, i)];
   const int64_t iv = integerize_m(x, fm, cm, big);
-  corr = needs_corr(x, iv, fm) ? 1u : 0u;
+  corr = CORR && needs_corr(x, iv, fm) ? 1u : 0u;
   return ((uint64_t)iv << 1) ^ (uint64_t)(iv >> 63);  // zigzag, encode.py:309-312
 }
 
@@ -251,6 +253,13 @@ __global__ void __launch_bounds__(kCThreads) cpc_plan_kernel(CArgs a) {
         cost1 += l1;
       }
     }
+  }
+  {
+    // per-thread run bits under both candidates (pack needs no length pass)
+    const uint32_t raw = (i0 < i1 && i0 == p.lo && sidx == 0) ? 3u * a.seg_bits[p.s] : 0u;
+    uint32_t* rb = a.st[sidx].run_bits + (size_t)p.s * kCThreads + threadIdx.x;
+    rb[0] = (uint32_t)cost0 + raw;
+    rb[(size_t)a.nseg * kCThreads] = (uint32_t)cost1 + raw;
   }
   __shared__ uint64_t r64[2][kCThreads / 32];
   __shared__ uint32_t r32[5][kCThreads / 32];
@@ -421,27 +430,16 @@ __global__ void __launch_bounds__(kCThreads) cpc_pack_kernel(CArgs a) {
   else if (sidx == 2) vel_init<2>(a, cm);
   else vel_init<3>(a, cm);
   auto value = [&](int64_t i, uint32_t& cr) -> uint64_t {
-    return sidx == 1 ? vel_mag<1>(a, p, i, cm, cr, big)
-           : sidx == 2 ? vel_mag<2>(a, p, i, cm, cr, big)
-                       : vel_mag<3>(a, p, i, cm, cr, big);
+    return sidx == 1 ? vel_mag<1, false>(a, p, i, cm, cr, big)
+           : sidx == 2 ? vel_mag<2, false>(a, p, i, cm, cr, big)
+                       : vel_mag<3, false>(a, p, i, cm, cr, big);
   };
-  // pass 1: bits of this thread's run
-  uint64_t L = 0;
+  // bits of this thread's run under the chosen scheme (from the plan)
+  const int cand = sid - (sidx == 0 ? 2 : 0);
+  const uint64_t L = S.run_bits[((size_t)cand * a.nseg + p.s) * kCThreads + threadIdx.x];
   uint64_t prev = 0;
   uint32_t cr;
-  if (i0 < i1) {
-    if (sidx == 0) {
-      prev = i0 > p.lo ? E.key(a, p, i0 - 1, cr, big) : 0;
-      uint64_t pv = prev;
-      for (int64_t i = i0; i < i1; i++) {
-        const uint64_t k = E.key(a, p, i, cr, big);
-        L += i == p.lo ? (uint64_t)kb : (uint64_t)tabs.len[sid][bitlen_u64(k - pv)];
-        pv = k;
-      }
-    } else {
-      for (int64_t i = i0; i < i1; i++) L += tabs.len[sid][bitlen_u64(value(i, cr))];
-    }
-  }
+  if (i0 < i1 && sidx == 0) prev = i0 > p.lo ? E.key<false>(a, p, i0 - 1, cr, big) : 0;
   __shared__ unsigned long long tmp[33];
   unsigned long long tot;
   const uint64_t o = S.seg_off[p.s] + block_excl_scan<unsigned long long>(L, tmp, &tot);
@@ -452,7 +450,7 @@ __global__ void __launch_bounds__(kCThreads) cpc_pack_kernel(CArgs a) {
     if (sidx == 0) {
       uint64_t pv = prev;
       for (int64_t i = i0; i < i1; i++) {
-        const uint64_t k = E.key(a, p, i, cr, big);
+        const uint64_t k = E.key<false>(a, p, i, cr, big);
         if (i == p.lo) B.put64(k, kb);
         else vlc_emit(B, k - pv, sid, tabs);
         pv = k;
@@ -788,7 +786,7 @@ size_t cpc_ws(int64_t nseg) {
   // per stream (carved in this order, 256-byte aligned): seg_cost u64,
   // seg_off u64 (+1), ids u8, corr cnt 3 x u32, corr off 3 x u32 (+1)
   const size_t per = r256(8 * nseg) + r256(8 * (nseg + 1)) + r256(nseg) + r256(12 * nseg) +
-                     r256(12 * (nseg + 1));
+                     r256(12 * (nseg + 1)) + r256(8 * (size_t)kCThreads * nseg);
   return 4 * per + 256;
 }
 
@@ -805,6 +803,7 @@ static void carve(CArgs& a, void* ws, int64_t nseg) {
     a.st[s].seg_id = take(nseg);
     a.st[s].corr_cnt = reinterpret_cast<uint32_t*>(take(12 * nseg));
     a.st[s].corr_off = reinterpret_cast<uint32_t*>(take(12 * (nseg + 1)));
+    a.st[s].run_bits = reinterpret_cast<uint32_t*>(take(8 * (size_t)kCThreads * nseg));
   }
 }
 
