@@ -580,16 +580,43 @@ struct KArgsD {
 
 // sequential bit reader over the MSB-first bytes (4-byte aligned loads)
 struct BitSrc {
-  const uint32_t* w;  // aligned base
-  uint64_t pos;       // absolute bit position from w
+  // 16-byte blocks, one prefetched ahead: the refill of the 64-bit window
+  // takes words from the current block and a block's load is issued four
+  // words before it is needed, so the decode chain rarely waits on memory
+  const uint4* g;     // 16-byte aligned base
   uint64_t cur;       // MSB-aligned window
-  int nv;
-  uint64_t nxt;       // next word index to load
+  int nv;             // valid bits in cur
+  uint32_t q0, q1, q2, q3;  // current block (byte-swapped), qn words left (from q0)
+  int qn;
+  uint4 nq;           // next block (raw), loaded ahead
+  uint64_t nb;        // index of the block after nq
+  NBZG_DEV void take_block() {
+    q0 = __byte_perm(nq.x, 0, 0x0123);
+    q1 = __byte_perm(nq.y, 0, 0x0123);
+    q2 = __byte_perm(nq.z, 0, 0x0123);
+    q3 = __byte_perm(nq.w, 0, 0x0123);
+    qn = 4;
+    nq = __ldg(g + nb);
+    nb++;
+  }
+  NBZG_DEV uint32_t take_word() {
+    if (qn == 0) take_block();
+    const uint32_t v = q0;
+    q0 = q1;
+    q1 = q2;
+    q2 = q3;
+    qn--;
+    return v;
+  }
   NBZG_DEV void init(const uint8_t* p, uint64_t bitpos) {
-    const uintptr_t base = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3);
-    w = reinterpret_cast<const uint32_t*>(base);
-    pos = bitpos + 8 * (reinterpret_cast<uintptr_t>(p) & 3);
-    nxt = pos >> 5;
+    const uintptr_t base = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+    g = reinterpret_cast<const uint4*>(base);
+    const uint64_t pos = bitpos + 8 * (reinterpret_cast<uintptr_t>(p) & 15);
+    const uint64_t blk = pos >> 7;
+    nq = __ldg(g + blk);
+    nb = blk + 1;
+    take_block();
+    for (int k = (int)((pos >> 5) & 3); k > 0; k--) take_word();
     cur = 0;
     nv = 0;
     fill();
@@ -600,26 +627,24 @@ struct BitSrc {
   }
   NBZG_DEV void fill() {
     while (nv <= 32) {
-      const uint32_t v = __byte_perm(__ldg(w + nxt), 0, 0x0123);
-      cur |= (uint64_t)v << (32 - nv);
+      cur |= (uint64_t)take_word() << (32 - nv);
       nv += 32;
-      nxt++;
     }
   }
-  NBZG_DEV uint64_t get(int nb) {  // nb <= 32
-    if (nb <= 0) return 0;
-    const uint64_t v = cur >> (64 - nb);
-    cur <<= nb;
-    nv -= nb;
+  NBZG_DEV uint64_t get(int nb2) {  // nb2 <= 32
+    if (nb2 <= 0) return 0;
+    const uint64_t v = cur >> (64 - nb2);
+    cur <<= nb2;
+    nv -= nb2;
     fill();
     return v;
   }
-  NBZG_DEV uint64_t get64(int nb) {
-    if (nb > 32) {
-      const uint64_t hi = get(nb - 32);
+  NBZG_DEV uint64_t get64(int nb2) {
+    if (nb2 > 32) {
+      const uint64_t hi = get(nb2 - 32);
       return (hi << 32) | get(32);
     }
-    return get(nb);
+    return get(nb2);
   }
   NBZG_DEV int ones7() {  // leading ones of the window, capped at 7
     const int o = __clz(~(uint32_t)(cur >> 32));
