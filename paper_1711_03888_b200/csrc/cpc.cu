@@ -33,6 +33,8 @@ namespace nbzg {
 void trace_mark(const char* name, cudaStream_t st);  // capi.cu (bench stage trace)
 
 constexpr int kCThreads = 512;
+constexpr int kCSub = 1024;  // values per decode sub-block (v2 segment index)
+__host__ __device__ inline int64_t cpc_subs(int64_t S) { return (S + kCSub - 1) / kCSub; }
 
 __constant__ uint8_t c_vlcw[4][8] = {{2, 4, 6, 8, 12, 16, 24, 33},
                                      {4, 8, 16, 24, 32, 40, 48, 64},
@@ -347,7 +349,8 @@ __global__ void __launch_bounds__(1024) cpc_scan_kernel(CArgs a) {
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    uint64_t len = (uint64_t)a.nseg + 8 + (a.cm->total_bits[sidx] + 7) / 8 + 4ull * a.nseg;
+    uint64_t len = (uint64_t)a.nseg + 8 + (a.cm->total_bits[sidx] + 7) / 8 +
+                   4ull * a.nseg * (uint64_t)cpc_subs(a.S);
     for (int c = 0; c < nl; c++) len += 4 + 12 * a.cm->corr[sidx][c];
     a.cm->len[sidx] = len;
   }
@@ -444,19 +447,38 @@ __global__ void __launch_bounds__(kCThreads) cpc_pack_kernel(CArgs a) {
   unsigned long long tot;
   const uint64_t o = S.seg_off[p.s] + block_excl_scan<unsigned long long>(L, tmp, &tot);
   if (i0 < i1) {
-    uint32_t* words = reinterpret_cast<uint32_t*>(a.arena + a.cm->off[sidx] + a.nseg + 8);
+    uint8_t* pay = a.arena + a.cm->off[sidx];
+    uint32_t* words = reinterpret_cast<uint32_t*>(pay + a.nseg + 8);
+    // v2 sub-block index: bit offset (from the segment start) of every
+    // kCSub-th value, after the u32 segment lengths
+    const int64_t subs = cpc_subs(a.S);
+    uint8_t* sub = pay + a.cm->len[sidx] - 4 * (uint64_t)a.nseg * subs + 4 * a.nseg +
+                   4 * (uint64_t)p.s * (subs - 1);
+    const uint64_t seg0 = S.seg_off[p.s];
+    auto mark = [&](int64_t i, const BitSink& B) {
+      const int64_t r = i - p.lo;
+      if (r > 0 && (r & (kCSub - 1)) == 0) {
+        const uint32_t v = (uint32_t)(B.wi * 32 + B.nacc - seg0);
+        uint8_t* d = sub + 4 * (r / kCSub - 1);
+        for (int b = 0; b < 4; b++) d[b] = (uint8_t)(v >> (8 * b));
+      }
+    };
     BitSink B;
     B.init(words, o);
     if (sidx == 0) {
       uint64_t pv = prev;
       for (int64_t i = i0; i < i1; i++) {
         const uint64_t k = E.key<false>(a, p, i, cr, big);
+        mark(i, B);
         if (i == p.lo) B.put64(k, kb);
         else vlc_emit(B, k - pv, sid, tabs);
         pv = k;
       }
     } else {
-      for (int64_t i = i0; i < i1; i++) vlc_emit(B, value(i, cr), sid, tabs);
+      for (int64_t i = i0; i < i1; i++) {
+        mark(i, B);
+        vlc_emit(B, value(i, cr), sid, tabs);
+      }
     }
     B.finish();
   }
@@ -556,10 +578,17 @@ __global__ void cpc_frame_kernel(CArgs a) {
   if (threadIdx.x != 0) {
     for (int c = 0; c < nl; c++) base += 4 + 12 * a.cm->corr[sidx][c];
   }
+  const int64_t subs = cpc_subs(a.S);
   for (int64_t s = threadIdx.x; s < a.nseg; s += blockDim.x) {
     const uint32_t v = (uint32_t)S.seg_cost[s];
     uint8_t* d = pay + base + 4 * s;
     for (int b = 0; b < 4; b++) d[b] = (uint8_t)(v >> (8 * b));
+    // sub-blocks past a short segment's end repeat its length
+    const int64_t m = min(a.S, a.n - s * a.S);
+    for (int64_t k = (m + kCSub - 1) / kCSub; k < subs; k++) {
+      uint8_t* e = pay + base + 4 * a.nseg + 4 * (s * (subs - 1) + k - 1);
+      for (int b = 0; b < 4; b++) e[b] = (uint8_t)(v >> (8 * b));
+    }
   }
 }
 
@@ -576,7 +605,13 @@ struct KArgsD {
   uint32_t* status;
   uint64_t total;
   int64_t bits_at;  // payload offset of the bit region
+  int64_t tr_bytes; // v2 segment index bytes at the payload end (0 for v1)
+  int64_t subs;     // sub-blocks per segment
 };
+
+NBZG_DEV uint32_t ld_u32_le(const uint8_t* d) {
+  return (uint32_t)d[0] | ((uint32_t)d[1] << 8) | ((uint32_t)d[2] << 16) | ((uint32_t)d[3] << 24);
+}
 
 // sequential bit reader over the MSB-first bytes (4-byte aligned loads)
 struct BitSrc {
@@ -656,7 +691,7 @@ struct BitSrc {
 __global__ void __launch_bounds__(1024) cpc_dec_offsets_kernel(KArgsD a) {
   __shared__ unsigned long long tmp[33];
   const int64_t R = (a.nseg + blockDim.x - 1) / blockDim.x;
-  const uint8_t* tr = a.pay + a.len - 4 * a.nseg;
+  const uint8_t* tr = a.pay + a.len - a.tr_bytes;
   unsigned long long s = 0;
   auto rd = [&](int64_t i) -> uint32_t {
     const uint8_t* d = tr + 4 * i;
@@ -771,12 +806,131 @@ __global__ void __launch_bounds__(128) cpc_dec_kernel(KArgsD a, const uint8_t* i
   if (pos != b1) atomicCAS(a.status, 0u, (uint32_t)(pos > b1 ? NBZG_TRUNCATED : NBZG_BAD_STREAM));
 }
 
+// v2 streams: one thread per sub-block (kCSub values) from the segment
+// index.  Coordinates take two passes: PHASE 0 sums each sub-block's key
+// deltas (sub-block 0 also records the raw first key), PHASE 1 starts each
+// sub-block from the raw key plus the sums before it and writes the floats.
+// Velocities have no carried state: PHASE 1 only.  Every sub-block must end
+// exactly where the next one starts.
+template <int PHASE>
+__global__ void __launch_bounds__(128) cpc_dec_sub_kernel(KArgsD a, const uint8_t* ids,
+                                                          uint64_t* sums, uint64_t* k0) {
+  __shared__ uint8_t sw[4][8];
+  if (threadIdx.x < 32) sw[threadIdx.x >> 3][threadIdx.x & 7] = c_vlcw[threadIdx.x >> 3][threadIdx.x & 7];
+  __syncthreads();
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gt >= a.nseg * a.subs) return;
+  const int64_t s = gt / a.subs, k = gt % a.subs;
+  const int64_t seg_lo = s * a.S, seg_hi = min(a.n, seg_lo + a.S);
+  const int64_t lo = seg_lo + k * kCSub;
+  if (lo >= seg_hi) return;
+  const int64_t hi = min(seg_hi, lo + kCSub);
+  const int sid = ids[s];
+  if (sid > 3) {
+    atomicCAS(a.status, 0u, (uint32_t)NBZG_BAD_STREAM);
+    return;
+  }
+  const uint8_t* subtab = a.pay + a.len - a.tr_bytes + 4 * a.nseg + 4 * s * (a.subs - 1);
+  const uint64_t s0 = a.seg_off[s], s1 = a.seg_off[s + 1];
+  const uint64_t b0 = s0 + (k == 0 ? 0 : ld_u32_le(subtab + 4 * (k - 1)));
+  const uint64_t b1 = hi == seg_hi ? s1 : s0 + ld_u32_le(subtab + 4 * k);
+  if (b1 > a.total || b0 > b1 || s1 > a.total) {
+    atomicCAS(a.status, 0u, (uint32_t)NBZG_TRUNCATED);
+    return;
+  }
+  BitSrc B;
+  B.init(a.pay + a.bits_at, b0);
+  uint64_t pos = b0;
+  auto vlc = [&]() -> uint64_t {
+    const int o = B.ones7();
+    const int pl = o < 7 ? o + 1 : 7;
+    B.get(pl);
+    const int w = sw[sid][o];
+    pos += pl + w;
+    return B.get64(w);
+  };
+  const bool vec = (a.S & 3) == 0;  // sub-blocks start 16-byte aligned
+  if (a.kind == 2) {
+    const int kb = 3 * a.seg_bits[s];
+    uint64_t key = 0;
+    int64_t i = lo;
+    if (k == 0) {
+      key = B.get64(kb);
+      pos += kb;
+      i++;
+    }
+    if (PHASE == 0) {
+      uint64_t sum = 0;
+      for (; i < hi; i++) sum += vlc();
+      sums[s * a.subs + k] = sum;
+      if (k == 0) k0[s] = key;
+    } else {
+      if (k > 0) {
+        key = k0[s];
+        for (int64_t j = 0; j < k; j++) key += sums[s * a.subs + j];
+      }
+      const int64_t m0 = a.minima[3 * s], m1 = a.minima[3 * s + 1], m2 = a.minima[3 * s + 2];
+      float ob[3][4];
+      int nb = 0;
+      auto out = [&](int64_t at) {
+        const float v0 = (float)__dmul_rn((double)((int64_t)compact3_64(key >> 2) + m0), a.twob[0]);
+        const float v1 = (float)__dmul_rn((double)((int64_t)compact3_64(key >> 1) + m1), a.twob[1]);
+        const float v2 = (float)__dmul_rn((double)((int64_t)compact3_64(key) + m2), a.twob[2]);
+        if (!vec) {
+          if (a.out[0]) a.out[0][at] = v0;
+          if (a.out[1]) a.out[1][at] = v1;
+          if (a.out[2]) a.out[2][at] = v2;
+          return;
+        }
+        ob[0][nb] = v0;
+        ob[1][nb] = v1;
+        ob[2][nb] = v2;
+        if (++nb == 4) {
+          for (int c = 0; c < 3; c++)
+            if (a.out[c])
+              *reinterpret_cast<float4*>(a.out[c] + at - 3) =
+                  make_float4(ob[c][0], ob[c][1], ob[c][2], ob[c][3]);
+          nb = 0;
+        }
+      };
+      if (k == 0) out(lo);
+      for (; i < hi; i++) {
+        key += vlc();
+        out(i);
+      }
+      for (int q = 0; q < nb; q++)
+        for (int c = 0; c < 3; c++)
+          if (a.out[c]) a.out[c][hi - nb + q] = ob[c][q];
+    }
+  } else {
+    float ob[4];
+    int nb = 0;
+    for (int64_t i = lo; i < hi; i++) {
+      const uint64_t mm = vlc();
+      const int64_t h = (int64_t)(mm >> 1);
+      const int64_t v = (mm & 1) ? -h - 1 : h;
+      const float f = (float)__dmul_rn((double)v, a.twob[0]);
+      if (!vec) {
+        a.out[0][i] = f;
+        continue;
+      }
+      ob[nb] = f;
+      if (++nb == 4) {
+        *reinterpret_cast<float4*>(a.out[0] + i - 3) = make_float4(ob[0], ob[1], ob[2], ob[3]);
+        nb = 0;
+      }
+    }
+    for (int q = 0; q < nb; q++) a.out[0][hi - nb + q] = ob[q];
+  }
+  if (pos != b1) atomicCAS(a.status, 0u, (uint32_t)(pos > b1 ? NBZG_TRUNCATED : NBZG_BAD_STREAM));
+}
+
 // correction lists (pipeline.py:240-260): one CTA per list, records applied
 // in parallel after a serial walk of the list headers
 __global__ void cpc_dec_corr_kernel(KArgsD a) {
   const int nl = a.kind == 2 ? 3 : 1;
   int64_t off = a.bits_at + (int64_t)((a.total + 7) / 8);
-  const int64_t end = a.len - 4 * a.nseg;  // trailer (indexed) or a.len
+  const int64_t end = a.len - a.tr_bytes;  // the segment index follows the corrections
   for (int c = 0; c < nl; c++) {
     if (off + 4 > end) {
       if (threadIdx.x == 0) atomicCAS(a.status, 0u, (uint32_t)NBZG_TRUNCATED);
@@ -901,7 +1055,8 @@ int nbzg_cpc_pack(const nbzg_cpc_args* g, void* stream) {
 
 size_t nbzg_cpc_decode_workspace_size(int64_t n, int64_t segment_size) {
   if (segment_size < 1) return 0;
-  return 8 * (size_t)((n + segment_size - 1) / segment_size + 1) + 256;
+  const size_t nseg = (size_t)((n + segment_size - 1) / segment_size);
+  return 8 * (nseg + 1) + 8 * nseg * (size_t)cpc_subs(segment_size) + 8 * nseg + 256;
 }
 
 int nbzg_cpc_decode(const nbzg_cpc_decode_args* g, void* stream) {
@@ -929,20 +1084,31 @@ int nbzg_cpc_decode(const nbzg_cpc_decode_args* g, void* stream) {
   a.bits_at = a.nseg + 8;
   // header fields the host already validated: ids, total bits (host passes)
   a.total = g->total_bits;
-  const int64_t need = a.nseg + 8 + (int64_t)((a.total + 7) / 8) + (g->indexed ? 4 * a.nseg : 0);
+  a.subs = cpc_subs(a.S);
+  a.tr_bytes = g->indexed ? 4 * a.nseg * a.subs : 0;
+  const int64_t need = a.nseg + 8 + (int64_t)((a.total + 7) / 8) + a.tr_bytes;
   if (need > a.len) return NBZG_TRUNCATED;
   const uint8_t* ids = a.pay;
   trace_mark(nullptr, st);
   if (!g->indexed) {
-    a.len += 4 * a.nseg;  // no trailer: corrections run to the end
     count_launch();
     cpc_dec_walk_kernel<<<1, 32, 0, st>>>(a, ids);
+    count_launch();
+    cpc_dec_kernel<<<(unsigned)((a.nseg + 127) / 128), 128, 0, st>>>(a, ids);
   } else {
+    uint64_t* sums = a.seg_off + (a.nseg + 1);       // [nseg][subs]
+    uint64_t* k0 = sums + a.nseg * a.subs;            // [nseg]
+    const int64_t nt = a.nseg * a.subs;
+    const unsigned grid = (unsigned)((nt + 127) / 128);
     count_launch();
     cpc_dec_offsets_kernel<<<1, 1024, 0, st>>>(a);
+    if (a.kind == 2) {
+      count_launch();
+      cpc_dec_sub_kernel<0><<<grid, 128, 0, st>>>(a, ids, sums, k0);
+    }
+    count_launch();
+    cpc_dec_sub_kernel<1><<<grid, 128, 0, st>>>(a, ids, sums, k0);
   }
-  count_launch();
-  cpc_dec_kernel<<<(unsigned)((a.nseg + 127) / 128), 128, 0, st>>>(a, ids);
   count_launch();
   cpc_dec_corr_kernel<<<a.kind == 2 ? 3 : 1, 256, 0, st>>>(a);
   trace_mark("cpc_decode", st);
