@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
   __shared__ unsigned long long scan_u64[33];
   __shared__ uint32_t s_cbl[64];
   __shared__ uint64_t s_fc[64];
-  __shared__ uint32_t s_k, s_max, s_min;
+  __shared__ uint32_t s_max, s_min;
   const int field = a.single_field >= 0 ? a.single_field : (int)blockIdx.x;
   const int mslot = a.single_field >= 0 ? 0 : field;
   nbzg_field_meta& fm = a.meta->f[mslot];
