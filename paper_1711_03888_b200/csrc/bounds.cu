@@ -88,6 +88,114 @@ int launch_minmax6(const float* const* f, int64_t n, uint32_t* mm, cudaStream_t 
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
 
+// Sorted mode: the same exact min/max of all six fields, one CTA per
+// R-index segment at a time, also writing the segment's min/max of the
+// three key fields (fields kf0..kf0+2) for K2's per-segment bits/minima.
+__global__ void __launch_bounds__(512) minmax_seg_kernel(Fields6 F, int64_t n, int64_t S,
+                                                         int64_t nseg, int kf0, uint32_t* mm,
+                                                         float* seg_mm) {
+  float lo[6], hi[6];
+#pragma unroll
+  for (int f = 0; f < 6; f++) {
+    lo[f] = __int_as_float(0x7f800000);
+    hi[f] = -__int_as_float(0x7f800000);
+  }
+  __shared__ float red[2][3][16];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t s = blockIdx.x; s < nseg; s += gridDim.x) {
+    const int64_t s0 = s * S;
+    const int m = (int)min(S, n - s0);
+    const int m4 = m >> 2;  // S % 4 == 0: segments start 16-byte aligned
+    float sl[6], sh[6];
+#pragma unroll
+    for (int f = 0; f < 6; f++) {
+      sl[f] = __int_as_float(0x7f800000);
+      sh[f] = -__int_as_float(0x7f800000);
+    }
+#pragma unroll 2
+    for (int v = threadIdx.x; v < m4; v += blockDim.x) {
+#pragma unroll
+      for (int f = 0; f < 6; f++) {
+        const float4 q = __ldcs(reinterpret_cast<const float4*>(F.p[f] + s0) + v);
+        sl[f] = fminf(sl[f], fminf(fminf(q.x, q.y), fminf(q.z, q.w)));
+        sh[f] = fmaxf(sh[f], fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
+      }
+    }
+    for (int i = 4 * m4 + threadIdx.x; i < m; i += blockDim.x)
+#pragma unroll
+      for (int f = 0; f < 6; f++) {
+        const float v = F.p[f][s0 + i];
+        sl[f] = fminf(sl[f], v);
+        sh[f] = fmaxf(sh[f], v);
+      }
+#pragma unroll
+    for (int f = 0; f < 6; f++) {
+      lo[f] = fminf(lo[f], sl[f]);
+      hi[f] = fmaxf(hi[f], sh[f]);
+    }
+    // segment reduction of the key fields
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      float a = sl[kf0 + c], b = sh[kf0 + c];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
+        b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+      }
+      if (lane == 0) {
+        red[0][c][wid] = a;
+        red[1][c][wid] = b;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+      const int c = threadIdx.x >> 1, hiw = threadIdx.x & 1;
+      float r = red[hiw][c][0];
+      for (int q = 1; q < (int)(blockDim.x >> 5); q++)
+        r = hiw ? fmaxf(r, red[1][c][q]) : fminf(r, red[0][c][q]);
+      seg_mm[6 * s + threadIdx.x] = r;  // [c][min, max]
+    }
+    __syncthreads();
+  }
+  __shared__ uint32_t s_lo[6], s_hi[6];
+  if (threadIdx.x < 6) {
+    s_lo[threadIdx.x] = 0xffffffffu;
+    s_hi[threadIdx.x] = 0u;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int f = 0; f < 6; f++) {
+    float a = lo[f], b = hi[f];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    if (lane == 0) {
+      atomicMin(&s_lo[f], f2ord(a));
+      atomicMax(&s_hi[f], f2ord(b));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    atomicMin(&mm[2 * threadIdx.x], s_lo[threadIdx.x]);
+    atomicMax(&mm[2 * threadIdx.x + 1], s_hi[threadIdx.x]);
+  }
+}
+
+int launch_minmax_seg(const Plan& p, cudaStream_t st) {
+  Fields6 F;
+  for (int i = 0; i < 6; i++) F.p[i] = p.f[i];
+  count_launch();
+  minmax_init_kernel<<<1, 32, 0, st>>>(p.minmax);
+  int blocks = (int)min(p.nseg, (int64_t)sm_count() * 4);
+  if (blocks < 1) blocks = 1;
+  count_launch();
+  minmax_seg_kernel<<<blocks, 512, 0, st>>>(F, p.n, p.S, p.nseg, p.variant == 1 ? 3 : 0,
+                                            p.minmax, p.seg_mm);
+  return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
+}
+
 // resolve_field_bounds (pipeline.py:157-181): constant fields (zero range)
 // take the fast path regardless of bound kind; others get
 // b = value (absolute) or b = value * (float(hi) - float(lo)) in f64.

@@ -122,6 +122,7 @@ size_t plan_workspace(Plan& p, void* base) {
   p.lb = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 12 * (p.nchunks + 1)));
   p.counters = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 64));
   p.tile_flags = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * (p.ntiles + 1)));
+  p.seg_mm = reinterpret_cast<float*>(take(sizeof(float) * 6 * ((size_t)p.nseg + 1)));
   return off;
 }
 
@@ -239,7 +240,11 @@ int nbzg_compress(const nbzg_compress_args* a, void* stream) {
   p.arena_bytes = a->arena_bytes;
   int rc;
   trace_mark(nullptr, st);
-  if ((rc = launch_minmax6(p.f, p.n, p.minmax, st))) return rc;
+  // sorted mode with 3-field keys: K1 walks whole segments and also leaves
+  // each segment's key-field min/max, so K2 reads the coordinates once
+  const bool segmm = p.sorted && p.variant != 2 && p.n > 0 && p.S % 4 == 0;
+  if ((rc = segmm ? launch_minmax_seg(p, st) : launch_minmax6(p.f, p.n, p.minmax, st))) return rc;
+  if (!segmm) p.seg_mm = nullptr;
   trace_mark("minmax6", st);
   if ((rc = launch_resolve(p, st))) return rc;
   trace_mark("resolve", st);

@@ -30,6 +30,7 @@ struct Plan {
   double bound_value[6] = {};
   // workspace
   uint32_t* minmax = nullptr;   // 12 ordered u32
+  float* seg_mm = nullptr;      // [nseg][3][2] per-segment min/max of the key fields (from K1)
   nbzg_meta* meta = nullptr;
   uint16_t* perm = nullptr;
   uint8_t* seg_bits = nullptr;
@@ -64,6 +65,7 @@ void plan_shape(Plan& p, int64_t n, int sorted, int64_t interval_count, int64_t 
 
 // kernel launchers (each enqueues on `st`)
 int launch_minmax6(const float* const* f, int64_t n, uint32_t* minmax12, cudaStream_t st);
+int launch_minmax_seg(const Plan& p, cudaStream_t st);
 int launch_resolve(const Plan& p, cudaStream_t st);
 int launch_rindex_sort(const Plan& p, cudaStream_t st);
 int launch_quantize(const Plan& p, cudaStream_t st);

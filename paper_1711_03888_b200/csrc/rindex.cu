@@ -41,6 +41,7 @@ struct RArgs {
   int pass;  // 0 = u32 main pass, 1 = u64 pass over flagged tiles
   int no_clamp;     // CPC modes: allow_key_clamp=False (rindex.py:185-190)
   int64_t* minima;  // CPC modes: 3 segment minima per segment (io.py:115-117), else null
+  const float* seg_mm;  // [nseg][3][2] key-field min/max per segment from K1, or null
 };
 
 NBZG_DEV void set_status(uint32_t* status, uint32_t code) { atomicCAS(status, 0u, code); }
@@ -177,7 +178,16 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
       mn[c] = __int_as_float(0x7f800000);
       mx[c] = -__int_as_float(0x7f800000);
     }
-    {
+    if (a.seg_mm) {
+      // K1 already reduced this segment: every thread takes the values, so
+      // the block reduction below returns them unchanged
+      const float* sm = a.seg_mm + 6 * (s0 / a.S);
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        mn[c] = sm[2 * c];
+        mx[c] = sm[2 * c + 1];
+      }
+    } else {
       // float4 loads, 4 x 3 in flight per thread (segments start 16-byte aligned)
       const int m4 = (s0 & 3) ? 0 : m >> 2;  // float4 path needs 16-byte aligned segments
       const float4* x4[3] = {reinterpret_cast<const float4*>(a.x[0] + s0),
@@ -482,6 +492,7 @@ int launch_rindex_sort(const Plan& p, cudaStream_t st) {
   a.status = &p.meta->status;
   a.no_clamp = p.cpc ? 1 : 0;
   a.minima = p.cpc ? p.minima : nullptr;
+  a.seg_mm = p.seg_mm;
   size_t sm32 = kTileMax * (4 + 2) + kSortWarps * kRadix * 2;
   size_t sm64 = kTileMax * (8 + 2) + kSortWarps * kRadix * 2;
   static bool attr = false;
