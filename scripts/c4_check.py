@@ -3,7 +3,8 @@
 particles (25.8 GB), sz-lv-prx eb_rel 1e-4.  Generated on the host in
 slabs straight into device memory; compress, decompress, then the error
 bound is checked at every point on the device (no oracle at this size:
-the per-stage bit-exactness is covered by the C0-C3 tests)."""
+the per-stage bit-exactness is covered by the C0-C3 tests).
+    python scripts/c4_check.py [side] [mode]"""
 import os, sys, time
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 import numpy as np
@@ -12,6 +13,7 @@ import paper_1711_03888_b200 as nbz
 from paper_1711_03888_b200 import datagen
 
 side = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+mode = sys.argv[2] if len(sys.argv) > 2 else "sz-lv-prx"
 spec = datagen.HaccSpec((side, side, side), 2.5)
 n = spec.n
 dev = [torch.empty(n, dtype=torch.float32, device="cuda") for _ in range(6)]
@@ -30,7 +32,7 @@ snap = nbz.ParticleSnapshot(*dev)
 for rep in range(2):
     e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
     e0.record()
-    res = nbz.compress(snap, "sz-lv-prx", nbz.ErrorBoundSpec.relative(1e-4))
+    res = nbz.compress(snap, mode, nbz.ErrorBoundSpec.relative(1e-4))
     e1.record()
     rec = nbz.decompress(res.archive, device=True)
     e2.record()
@@ -46,4 +48,11 @@ for fi in range(6):
     b = res.archive.bounds[fi]
     worst = max(worst, err / b)
     assert err <= b, (fi, err, b)
-print(f"bound holds at every point (max err/bound {worst:.4f})")
+print(f"{mode}: bound holds at every point (max err/bound {worst:.4f})")
+if mode in ("sz-cpc2000", "cpc2000"):
+    # the serialized archive decodes to the same values (v2 index path)
+    from paper_1711_03888_b200 import io as nio
+    rec2 = nbz.decompress(nio.deserialize_archive(res.archive.serialized()), device=True)
+    for fi in range(6):
+        assert torch.equal(rec2.field(fi), rec.field(fi)), fi
+    print(f"{mode}: wire round trip identical")
