@@ -212,6 +212,21 @@ int nbzg_cpc_decode(const nbzg_cpc_decode_args *args, void *stream);
 
 /* ---- stage-level parity hooks (mirror nbz._kernels, same semantics) ---- */
 
+/* K.huff_decode (_kernels.py:348-374): n symbols from a raw MSB-first
+ * bitstream with canonical tables (host arrays of 64: first code, count and
+ * first sorted index per length; device sorted symbols).  *status_dev: 0 ok,
+ * NBZG_INVALID_CODE, NBZG_TRUNCATED (the reference's 1 / 2).  One thread:
+ * a parity hook, not a fast path. */
+int nbzg_huff_decode(const uint8_t *data, uint64_t total_bits, int64_t n, int32_t min_len,
+                     int32_t max_len, const uint64_t *h_first_code, const uint32_t *h_counts,
+                     const uint32_t *h_first_idx, const uint32_t *sorted_syms, uint32_t *out,
+                     uint32_t *status_dev, void *stream);
+
+/* K.deinterleave3 (_kernels.py:789-798): the three 21-bit fields of each
+ * interleaved key (CPC2000 coordinate decode). */
+int nbzg_deinterleave3(const uint64_t *keys, int64_t n, int64_t *x, int64_t *y, int64_t *z,
+                       void *stream);
+
 /* model.field_range x6 (model.py:104-109): out[2f] = min, out[2f+1] = max */
 int nbzg_minmax6(const float *const *h_fields, int64_t n, float *out12, void *stream);
 

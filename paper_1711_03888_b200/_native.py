@@ -39,7 +39,8 @@ EXPORTED = (
     "nbzg_huffman_codebook", "nbzg_huff_encode", "nbzg_crc64", "nbzg_crc64_workspace_size",
     "nbzg_version", "nbzg_device_sm_count", "nbzg_launch_count", "nbzg_trace_enable",
     "nbzg_trace_read", "nbzg_cpc_workspace_size", "nbzg_cpc_plan", "nbzg_cpc_pack",
-    "nbzg_cpc_decode", "nbzg_cpc_decode_workspace_size",
+    "nbzg_cpc_decode", "nbzg_cpc_decode_workspace_size", "nbzg_huff_decode",
+    "nbzg_deinterleave3",
 )
 
 
@@ -131,6 +132,9 @@ _SIGS = {
     "nbzg_cpc_pack": (ctypes.c_int, [c_p, c_p]),
     "nbzg_cpc_decode_workspace_size": (c_sz, [c_i64, c_i64]),
     "nbzg_cpc_decode": (ctypes.c_int, [c_p, c_p]),
+    "nbzg_huff_decode": (ctypes.c_int, [c_p, c_u64, c_i64, c_i32, c_i32, c_p, c_p, c_p, c_p, c_p,
+                                        c_p, c_p]),
+    "nbzg_deinterleave3": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_p]),
 }
 
 _lib = None

@@ -34,6 +34,12 @@ int launch_crc64(const uint8_t* data, int64_t n, uint64_t* crc_out, void* ws, si
                  cudaStream_t st);
 
 size_t decompress_ws(int nf, int64_t n, int64_t nbins);
+int launch_huff_decode_hook(const uint8_t* bits, uint64_t total, int64_t n, int min_len,
+                            int max_len, const uint64_t* first_code, const uint32_t* counts,
+                            const uint32_t* first_idx, const uint32_t* ss, uint32_t* out,
+                            uint32_t* status, cudaStream_t st);
+int launch_deinterleave3(const uint64_t* keys, int64_t n, int64_t* x, int64_t* y, int64_t* z,
+                         cudaStream_t st);
 
 // ---- launch counter and event trace (diagnostics for bench.py; the trace is
 // off unless nbzg_trace_enable(1) is called)
@@ -386,6 +392,22 @@ int nbzg_huff_encode(const uint16_t* syms, int64_t n, const uint64_t* lut, uint8
   uint32_t* tickets = reinterpret_cast<uint32_t*>(lb + 2 * nchunks);
   return launch_huff_encode_raw(syms, n, lut, out, chunk_bits, lb, tickets,
                                 reinterpret_cast<cudaStream_t>(stream));
+}
+
+int nbzg_huff_decode(const uint8_t* data, uint64_t total_bits, int64_t n, int32_t min_len,
+                     int32_t max_len, const uint64_t* h_first_code, const uint32_t* h_counts,
+                     const uint32_t* h_first_idx, const uint32_t* sorted_syms, uint32_t* out,
+                     uint32_t* status_dev, void* stream) {
+  if (n < 0 || !h_first_code || !h_counts || !h_first_idx) return NBZG_BAD_ARG;
+  return launch_huff_decode_hook(data, total_bits, n, min_len, max_len, h_first_code, h_counts,
+                                 h_first_idx, sorted_syms, out, status_dev,
+                                 reinterpret_cast<cudaStream_t>(stream));
+}
+
+int nbzg_deinterleave3(const uint64_t* keys, int64_t n, int64_t* x, int64_t* y, int64_t* z,
+                       void* stream) {
+  if (n < 0) return NBZG_BAD_ARG;
+  return launch_deinterleave3(keys, n, x, y, z, reinterpret_cast<cudaStream_t>(stream));
 }
 
 size_t nbzg_crc64_workspace_size(int64_t n) { return crc_ws(n); }

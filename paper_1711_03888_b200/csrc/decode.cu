@@ -1072,6 +1072,73 @@ __global__ void decode_v1_kernel(DArgs a) {
   if (ei != P.n_esc) fail(a.status, NBZG_BAD_STREAM);
 }
 
+// ---------------------------------------------------------------- parity hook
+// K.huff_decode (_kernels.py:348-374): canonical decode of n symbols from a
+// raw MSB-first bitstream, one thread, the reference's exact walk and
+// statuses (0 ok, NBZG_INVALID_CODE, NBZG_TRUNCATED).
+__global__ void huff_decode_hook_kernel(const uint8_t* bits, uint64_t total, int64_t n,
+                                        DParsed P, const uint32_t* ss, uint32_t* out,
+                                        uint32_t* status) {
+  if (threadIdx.x || blockIdx.x) return;
+  uint64_t bp = 0;
+  for (int64_t i = 0; i < n; i++) {
+    uint32_t sym = 0;
+    const int l = decode_serial(bits, bp, total, P, ss, sym);
+    if (l < 0) {
+      *status = (uint32_t)(-l);
+      return;
+    }
+    out[i] = sym;
+  }
+  *status = 0;
+}
+
+int launch_huff_decode_hook(const uint8_t* bits, uint64_t total, int64_t n, int min_len,
+                            int max_len, const uint64_t* first_code, const uint32_t* counts,
+                            const uint32_t* first_idx, const uint32_t* ss, uint32_t* out,
+                            uint32_t* status, cudaStream_t st) {
+  if (min_len < 1 || max_len > 63 || min_len > max_len) return NBZG_BAD_ARG;
+  DParsed P{};
+  P.min_len = (uint32_t)min_len;
+  P.max_len = (uint32_t)max_len;
+  for (int l = 0; l < 64; l++) {
+    P.first_code[l] = first_code[l];
+    P.counts[l] = counts[l];
+    P.first_idx[l] = first_idx[l];
+  }
+  count_launch();
+  huff_decode_hook_kernel<<<1, 32, 0, st>>>(bits, total, n, P, ss, out, status);
+  return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
+}
+
+// deinterleave3 (_kernels.py:789-798): key bit 3j+2 -> x bit j, 3j+1 -> y, 3j -> z
+NBZG_DEV uint64_t compact3_hook(uint64_t v) {
+  v &= 0x1249249249249249ull;
+  v = (v | (v >> 2)) & 0x10C30C30C30C30C3ull;
+  v = (v | (v >> 4)) & 0x100F00F00F00F00Full;
+  v = (v | (v >> 8)) & 0x1F0000FF0000FFull;
+  v = (v | (v >> 16)) & 0x1F00000000FFFFull;
+  v = (v | (v >> 32)) & 0x1FFFFFull;
+  return v;
+}
+__global__ void deinterleave3_kernel(const uint64_t* keys, int64_t n, int64_t* x, int64_t* y,
+                                     int64_t* z) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t k = keys[i];
+  x[i] = (int64_t)compact3_hook(k >> 2);
+  y[i] = (int64_t)compact3_hook(k >> 1);
+  z[i] = (int64_t)compact3_hook(k);
+}
+int launch_deinterleave3(const uint64_t* keys, int64_t n, int64_t* x, int64_t* y, int64_t* z,
+                         cudaStream_t st) {
+  if (n > 0) {
+    count_launch();
+    deinterleave3_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(keys, n, x, y, z);
+  }
+  return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
+}
+
 // ---------------------------------------------------------------- launcher
 // NBZG_DECODE=warp|thread forces one v2 decoder (tests cover both).
 static bool use_tpc(int64_t nchunks) {

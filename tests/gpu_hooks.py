@@ -116,3 +116,31 @@ def huff_encode(codes_u16, lut_u64):
 def crc64(data: bytes):
     from paper_1711_03888_b200 import io as nio
     return nio.crc64(data)
+
+
+def huff_decode(data: bytes, total_bits: int, n: int, tables: dict):
+    """K.huff_decode hook: tables as returned by oracle.huffman_tables."""
+    import ctypes as C
+    L = N.lib()
+    buf = _dev(np.frombuffer(bytearray(bytes(data) + b"\0" * 16), np.uint8))
+    ss = _dev(np.asarray(tables["sorted_syms"], np.int32))
+    out = torch.zeros(max(n, 1), dtype=torch.int32, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    fc = np.ascontiguousarray(tables["first_code"], np.uint64)
+    cb = np.ascontiguousarray(tables["counts_by_len"], np.uint32)
+    fi = np.ascontiguousarray(tables["first_idx"], np.uint32)
+    N.check(L.nbzg_huff_decode(N.ptr(buf), total_bits, n, tables["min_len"], tables["max_len"],
+                               fc.ctypes.data_as(C.c_void_p), cb.ctypes.data_as(C.c_void_p),
+                               fi.ctypes.data_as(C.c_void_p), N.ptr(ss), N.ptr(out), N.ptr(st),
+                               N.stream_handle()), "huff_decode")
+    return out[:n].cpu().numpy(), int(st.item())
+
+
+def deinterleave3(keys):
+    L = N.lib()
+    k = _dev(np.asarray(keys, np.uint64).view(np.int64))
+    n = k.numel()
+    outs = [torch.zeros(max(n, 1), dtype=torch.int64, device="cuda") for _ in range(3)]
+    N.check(L.nbzg_deinterleave3(N.ptr(k), n, *[N.ptr(o) for o in outs], N.stream_handle()),
+            "deinterleave3")
+    return [o[:n].cpu().numpy() for o in outs]

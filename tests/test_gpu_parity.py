@@ -149,6 +149,34 @@ def test_huff_encode_bytes_match_reference_kat(O):
     assert data == k["hb_bytes"].tobytes()
 
 
+def test_huff_decode_hook_matches_reference_kat(O, rng):
+    """K.huff_decode parity hook: the reference's KAT bitstream decodes to
+    its symbols; truncated and invalid streams give the reference's
+    statuses (2 / 1 -> NBZG_TRUNCATED / NBZG_INVALID_CODE)."""
+    k = load_golden("kats")
+    syms, lens = k["hb_symbols"], k["hb_lengths"]
+    t = O.huffman_tables(syms, lens)
+    data = k["hb_bytes"].tobytes()
+    n = k["hb_syms_in"].size
+    out, st = H.huff_decode(data, int(k["hb_bits"]), n, t)
+    assert st == 0
+    assert np.array_equal(out, k["hb_syms_in"])
+    _o, st = H.huff_decode(data, int(k["hb_bits"]) - 3, n, t)
+    assert st == 4  # NBZG_TRUNCATED
+    # an incomplete code: one length-2 symbol only leaves "1..." invalid
+    t2 = O.huffman_tables(np.array([5], np.int32), np.array([2], np.uint8))
+    _o, st = H.huff_decode(b"\xff\xff", 16, 4, t2)
+    assert st == 3  # NBZG_INVALID_CODE
+
+
+def test_deinterleave3_hook(O):
+    """K.deinterleave3 hook inverts the reference's interleave3 KAT."""
+    k = load_golden("kats")
+    x, y, z = H.deinterleave3(k["il_keys"])
+    assert np.array_equal(x, k["il_x"]) and np.array_equal(y, k["il_y"])
+    assert np.array_equal(z, k["il_z"])
+
+
 def test_huff_encode_multichunk(O, rng):
     for n in (16383, 16384, 16385, 100000, 333333):
         codes = np.clip(np.rint(rng.normal(32769, 40, n)), 1, 65535).astype(np.int64)
