@@ -23,7 +23,8 @@ int launch_order_expand(const uint16_t* perm, int64_t n, int64_t tile, int64_t* 
 int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uint8_t* len,
                          uint64_t* lut, uint32_t* scratch, nbzg_meta* meta, int64_t n,
                          int64_t nchunks, int single_field, cudaStream_t st,
-                         uint32_t* twin = nullptr, uint8_t* tlen8 = nullptr);
+                         uint32_t* twin = nullptr, uint8_t* tlen8 = nullptr, int f0 = 0,
+                         int nf = 6);
 int launch_huffman_lengths(const uint32_t* counts, int64_t k, uint8_t* lengths, uint32_t* scr,
                            uint32_t* status, cudaStream_t st);
 int launch_huff_encode_raw(const uint16_t* syms, int64_t n, const uint64_t* lut, uint8_t* out,
@@ -149,6 +150,48 @@ __global__ void ord_decode_kernel(uint32_t* m) {
 
 static int cuda_status() { return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR; }
 
+// The SZ stages in two field groups (coordinates, velocities) so the
+// codebook -- six single-CTA Huffman builds that leave the rest of the GPU
+// idle -- overlaps real work: group A's codebook runs beside group B's
+// quantisation, group B's codebook beside group A's encoding.
+//   st: Q(A) -> Q(B) -> CB(B) -> [wait layout A] layout(B) -> E(B) -> [wait E(A)]
+//   sd:   [wait Q(A)] CB(A) -> layout(A) -> E(A)
+// A side stream and three events per call (no shared mutable state).
+static int sz_stages_split(Plan& p, cudaStream_t st) {
+  cudaStream_t sd;
+  cudaEvent_t eqa, ela, eea;
+  if (cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking) != cudaSuccess) return NBZG_CUDA_ERROR;
+  cudaEventCreateWithFlags(&eqa, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ela, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&eea, cudaEventDisableTiming);
+  int rc = NBZG_OK;
+  do {
+    if ((rc = launch_quantize(p, st, 0, 3))) break;
+    cudaEventRecord(eqa, st);
+    if ((rc = launch_quantize(p, st, 3, 3))) break;
+    trace_mark("quantize", st);
+    cudaStreamWaitEvent(sd, eqa, 0);
+    if ((rc = launch_codebook(p, sd, 0, 3))) break;
+    if ((rc = launch_layout(p, sd, 0, 3))) break;
+    cudaEventRecord(ela, sd);
+    if ((rc = launch_encode(p, sd, 0, 3))) break;
+    cudaEventRecord(eea, sd);
+    if ((rc = launch_codebook(p, st, 3, 3))) break;
+    trace_mark("codebook", st);
+    cudaStreamWaitEvent(st, ela, 0);
+    if ((rc = launch_layout(p, st, 3, 3))) break;
+    trace_mark("layout", st);
+    if ((rc = launch_encode(p, st, 3, 3))) break;
+    cudaStreamWaitEvent(st, eea, 0);
+    trace_mark("encode", st);
+  } while (0);
+  cudaEventDestroy(eqa);
+  cudaEventDestroy(ela);
+  cudaEventDestroy(eea);
+  cudaStreamDestroy(sd);
+  return rc ? rc : cuda_status();
+}
+
 extern "C" {
 
 const char* nbzg_version(void) { return "nbzg 0.1.0 sm_100a"; }
@@ -260,6 +303,7 @@ int nbzg_compress(const nbzg_compress_args* a, void* stream) {
     trace_mark("rindex_sort", st);
   }
   if (p.sz_skip && (rc = launch_sz_skip(p, st))) return rc;
+  if (p.predictor == 0 && encode_uses_tpc(p)) return sz_stages_split(p, st);
   if ((rc = launch_quantize(p, st))) return rc;
   trace_mark("quantize", st);
   if ((rc = launch_codebook(p, st))) return rc;

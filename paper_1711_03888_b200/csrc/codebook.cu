@@ -35,6 +35,7 @@ struct CBArgs {
   uint32_t* twin;     // [6][kEncWin] encoder window table (may be null): code
                       // half+1-kEncWin/2+i -> word << 6 | len (len <= 26, else 0)
   uint8_t* tlen8;     // [6][nbins] code length by symbol (may be null)
+  int f0;             // first field of this launch (CTA b -> field f0 + b)
 };
 
 NBZG_DEV void bitonic_sort_u64(uint64_t* a, int N) {
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
   __shared__ uint32_t s_cbl[64];
   __shared__ uint64_t s_fc[64];
   __shared__ uint32_t s_max, s_min;
-  const int field = a.single_field >= 0 ? a.single_field : (int)blockIdx.x;
+  const int field = a.single_field >= 0 ? a.single_field : a.f0 + (int)blockIdx.x;
   const int mslot = a.single_field >= 0 ? 0 : field;
   nbzg_field_meta& fm = a.meta->f[mslot];
   if (a.single_field < 0 && (fm.is_const || a.n == 0)) return;
@@ -288,8 +289,8 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
 int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uint8_t* len,
                          uint64_t* lut, uint32_t* scratch, nbzg_meta* meta, int64_t n,
                          int64_t nchunks, int single_field, cudaStream_t st,
-                         uint32_t* twin, uint8_t* tlen8) {
-  CBArgs a{hist, nbins, sym, len, lut, scratch, meta, n, nchunks, single_field, twin, tlen8};
+                         uint32_t* twin, uint8_t* tlen8, int f0, int nf) {
+  CBArgs a{hist, nbins, sym, len, lut, scratch, meta, n, nchunks, single_field, twin, tlen8, f0};
   size_t sm = 14 * (size_t)kCBSmemK;  // keys u64 | L u32 | order u16
   static bool attr = false;
   if (!attr) {
@@ -297,14 +298,14 @@ int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uin
     attr = true;
   }
   count_launch();
-  codebook_kernel<<<single_field >= 0 ? 1 : 6, kCBThreads, sm, st>>>(a);
+  codebook_kernel<<<single_field >= 0 ? 1 : nf, kCBThreads, sm, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
 
-int launch_codebook(const Plan& p, cudaStream_t st) {
+int launch_codebook(const Plan& p, cudaStream_t st, int f0, int nf) {
   if (p.n == 0) return NBZG_OK;
   return launch_codebook_impl(p.hist, p.nbins, p.cb_sym, p.cb_len, p.lut, p.cb_scratch, p.meta,
-                              p.n, p.nchunks, -1, st, p.enc_win, p.enc_len8);
+                              p.n, p.nchunks, -1, st, p.enc_win, p.enc_len8, f0, nf);
 }
 
 // ---- parity hook: K.huffman_lengths on sorted counts (one CTA)
@@ -348,10 +349,11 @@ int launch_huffman_lengths(const uint32_t* counts, int64_t k, uint8_t* lengths, 
 }
 
 // ---- K5: payload layout (offsets of the non-constant fields, field order)
-__global__ void layout_kernel(nbzg_meta* meta, int64_t n) {
+// fields f0 .. f1-1, placed after the fields before f0 (whose layout ran first)
+__global__ void layout_kernel(nbzg_meta* meta, int64_t n, int f0, int f1) {
   if (threadIdx.x != 0) return;
-  uint64_t off = 0;
-  for (int f = 0; f < 6; f++) {
+  uint64_t off = f0 == 0 ? 0 : meta->arena_used;
+  for (int f = f0; f < f1; f++) {
     nbzg_field_meta& m = meta->f[f];
     m.payload_off = off;
     if (m.is_const || n == 0) {
@@ -363,9 +365,9 @@ __global__ void layout_kernel(nbzg_meta* meta, int64_t n) {
   meta->arena_used = off;
 }
 
-int launch_layout(const Plan& p, cudaStream_t st) {
+int launch_layout(const Plan& p, cudaStream_t st, int f0, int nf) {
   count_launch();
-  layout_kernel<<<1, 32, 0, st>>>(p.meta, p.n);
+  layout_kernel<<<1, 32, 0, st>>>(p.meta, p.n, f0, f0 + nf);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
 

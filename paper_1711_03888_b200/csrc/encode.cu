@@ -55,10 +55,11 @@ struct TArgs {
   int64_t nbins;
   int64_t nchunks;
   int64_t n;
+  int f0;               // CTA b -> field f0 + b
 };
 
 __global__ void table_writer_kernel(TArgs a) {
-  const int field = blockIdx.x;
+  const int field = a.f0 + (int)blockIdx.x;
   const nbzg_field_meta& m = a.meta->f[field];
   if (m.is_const || a.n == 0 || a.meta->status) return;
   uint8_t* p = a.arena + m.payload_off;
@@ -94,6 +95,7 @@ struct EArgs {
   uint64_t* lb;           // [6][nchunks]
   uint32_t* tickets;      // [6]
   int inline_esc;         // 1: payload mode (escape values inline); 0: raw hook
+  int f0;                 // field of blockIdx.y (or .x) 0 (field groups)
   // parity-hook mode: raw bitstream output instead of a payload
   uint8_t* raw_out;
   uint32_t* raw_chunk_bits;
@@ -323,7 +325,7 @@ NBZG_DEV void encode_chunk(const EArgs& a, int field, int64_t c, const CodeTab& 
 __global__ void __launch_bounds__(kEThreads) encode_kernel(EArgs a) {
   __shared__ long long s_idx[kEWarps][64];
   __shared__ uint32_t s_bits[kEWarps][64];
-  const int field = blockIdx.y;
+  const int field = a.f0 + (int)blockIdx.y;
   const bool raw = a.raw_out != nullptr;
   if (!raw && (a.meta->f[field].is_const || a.n == 0 || a.meta->status)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -609,7 +611,7 @@ __global__ void __launch_bounds__(kEFWarps * 32, 2) encode_fast_kernel(EArgs a) 
   long long* s_idx = reinterpret_cast<long long*>(s_win + kEncWin);  // [warps][64]
   uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_idx + kEFWarps * 64);
   uint32_t* s_headw = s_bits + kEFWarps * 64;                         // [warps][32]
-  const int field = blockIdx.y;
+  const int field = a.f0 + (int)blockIdx.y;
   if (a.meta->f[field].is_const || a.n == 0 || a.meta->status) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   {
@@ -671,7 +673,7 @@ __global__ void __launch_bounds__(kE1Warps * 32, 2) chunk_bits_kernel(EArgs a, u
                                                                       int ctas_per_field) {
   extern __shared__ __align__(16) uint8_t e1sm[];
   uint8_t* s_len = e1sm;  // [nbins]
-  const int field = blockIdx.y;
+  const int field = a.f0 + (int)blockIdx.y;
   if (a.meta->f[field].is_const || a.n == 0 || a.meta->status) return;
   {
     const uint4* g = reinterpret_cast<const uint4*>(a.tlen8 + (size_t)field * a.nbins);
@@ -719,7 +721,7 @@ __global__ void __launch_bounds__(kE1Warps * 32, 2) chunk_bits_kernel(EArgs a, u
 // E2: per field exclusive scan of chunk bits -> chunk bit offsets; v2 index
 __global__ void __launch_bounds__(1024) chunk_scan_kernel(EArgs a, const uint32_t* ctot,
                                                           uint64_t* coff) {
-  const int field = blockIdx.x;
+  const int field = a.f0 + (int)blockIdx.x;
   const nbzg_field_meta& m = a.meta->f[field];
   if (m.is_const || a.n == 0 || a.meta->status) return;
   __shared__ unsigned long long scan_tmp[33];
@@ -770,7 +772,7 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
                                                                    int ctas_per_field) {
   extern __shared__ __align__(16) uint8_t e3sm[];
   uint32_t* s_win = reinterpret_cast<uint32_t*>(e3sm);  // [kEncWin]
-  const int field = blockIdx.y;
+  const int field = a.f0 + (int)blockIdx.y;
   const nbzg_field_meta* mp = &a.meta->f[field];
   if (mp->is_const || a.n == 0 || a.meta->status) return;
   {
@@ -916,11 +918,19 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
   }
 }
 
-int launch_encode(const Plan& p, cudaStream_t st) {
+bool encode_uses_tpc(const Plan& p) {
+  const char* ev = getenv("NBZG_ENCODE");
+  const bool tpc = ev ? ev[0] == 't' : p.nchunks >= kTpcEncMinChunks;
+  return p.nbins == 65536 && tpc;
+}
+
+// fields f0 .. f0+nf-1 (the TPC path may run in field groups; the other
+// encoders always take all six fields)
+int launch_encode(const Plan& p, cudaStream_t st, int f0, int nf) {
   if (p.n == 0) return NBZG_OK;
-  TArgs t{p.meta, p.arena, p.cb_sym, p.cb_len, p.nbins, p.nchunks, p.n};
+  TArgs t{p.meta, p.arena, p.cb_sym, p.cb_len, p.nbins, p.nchunks, p.n, f0};
   count_launch();
-  table_writer_kernel<<<6, 256, 0, st>>>(t);
+  table_writer_kernel<<<nf, 256, 0, st>>>(t);
   EArgs a{};
   a.meta = p.meta;
   a.arena = p.arena;
@@ -938,11 +948,13 @@ int launch_encode(const Plan& p, cudaStream_t st) {
   a.inline_esc = 1;
   a.twin = p.enc_win;
   a.tlen8 = p.enc_len8;
-  cudaMemsetAsync(p.lb, 0, sizeof(uint64_t) * 6 * p.nchunks, st);
-  cudaMemsetAsync(p.counters, 0, sizeof(uint32_t) * 8, st);
-  const char* ev = getenv("NBZG_ENCODE");
-  const bool tpc = ev ? ev[0] == 't' : p.nchunks >= kTpcEncMinChunks;
-  if (p.nbins == 65536 && tpc) {
+  a.f0 = f0;
+  const bool tpc = encode_uses_tpc(p);
+  if (!tpc) {  // look-back words and tickets of the warp encoders (all six fields)
+    cudaMemsetAsync(p.lb, 0, sizeof(uint64_t) * 6 * p.nchunks, st);
+    cudaMemsetAsync(p.counters, 0, sizeof(uint32_t) * 8, st);
+  }
+  if (tpc) {
     // E1 -> E2 -> E3: chunk offsets, then in-chunk block prefixes, chunk totals
     const int64_t nb = p.nchunks * kBlkPerChunk;
     uint64_t* coff = p.enc_boff;
@@ -955,16 +967,16 @@ int launch_encode(const Plan& p, cudaStream_t st) {
                            4 * kEncWin + 4 * kE3Ring * kE3Threads);
       attr3 = true;
     }
-    int g1 = max(1, 2 * sm_count() / 6);
+    int g1 = max(1, 2 * sm_count() / nf);
     if (g1 > (p.nchunks + kE1Warps - 1) / kE1Warps) g1 = (int)((p.nchunks + kE1Warps - 1) / kE1Warps);
     count_launch();
-    chunk_bits_kernel<<<dim3(g1, 6), kE1Warps * 32, (size_t)p.nbins, st>>>(a, bpre, ctot, g1);
+    chunk_bits_kernel<<<dim3(g1, nf), kE1Warps * 32, (size_t)p.nbins, st>>>(a, bpre, ctot, g1);
     count_launch();
-    chunk_scan_kernel<<<6, 1024, 0, st>>>(a, ctot, coff);
-    int g3 = max(1, 2 * sm_count() / 6);
+    chunk_scan_kernel<<<nf, 1024, 0, st>>>(a, ctot, coff);
+    int g3 = max(1, 2 * sm_count() / nf);
     if (g3 > (nb + kE3Threads - 1) / kE3Threads) g3 = (int)((nb + kE3Threads - 1) / kE3Threads);
     count_launch();
-    encode_tpc_kernel<<<dim3(g3, 6), kE3Threads, 4 * kEncWin + 4 * kE3Ring * kE3Threads, st>>>(
+    encode_tpc_kernel<<<dim3(g3, nf), kE3Threads, 4 * kEncWin + 4 * kE3Ring * kE3Threads, st>>>(
         a, coff, bpre, g3);
   } else if (p.nbins == 65536) {
     const size_t sm = 4 * kEncWin + kEFWarps * 64 * 12 + kEFWarps * 32 * 4;

@@ -68,10 +68,11 @@ int launch_minmax6(const float* const* f, int64_t n, uint32_t* minmax12, cudaStr
 int launch_minmax_seg(const Plan& p, cudaStream_t st);
 int launch_resolve(const Plan& p, cudaStream_t st);
 int launch_rindex_sort(const Plan& p, cudaStream_t st);
-int launch_quantize(const Plan& p, cudaStream_t st);
-int launch_codebook(const Plan& p, cudaStream_t st);
-int launch_layout(const Plan& p, cudaStream_t st);
-int launch_encode(const Plan& p, cudaStream_t st);
+int launch_quantize(const Plan& p, cudaStream_t st, int f0 = 0, int nf = 6);
+int launch_codebook(const Plan& p, cudaStream_t st, int f0 = 0, int nf = 6);
+int launch_layout(const Plan& p, cudaStream_t st, int f0 = 0, int nf = 6);
+int launch_encode(const Plan& p, cudaStream_t st, int f0 = 0, int nf = 6);
+bool encode_uses_tpc(const Plan& p);
 int launch_sz_skip(const Plan& p, cudaStream_t st);
 
 int sm_count();

@@ -37,6 +37,7 @@ struct QArgs {
   int64_t nbins;
   int groups;
   int use_tma;
+  int f0, nf;  // field group: fields f0 .. f0+nf-1
 };
 
 NBZG_DEV uint32_t smem_u32(const void* p) {
@@ -116,8 +117,8 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ int64_t s_carry2[2];
 
-  const int field = blockIdx.x % 6;
-  const int g = blockIdx.x / 6;
+  const int field = a.f0 + (int)(blockIdx.x % a.nf);
+  const int g = (int)(blockIdx.x / a.nf);
   const nbzg_field_meta& fm = a.meta->f[field];
   if (fm.is_const || a.n == 0 || a.meta->status) return;  // e.g. BOUND_TOO_SMALL in K2
   const int64_t tb = (a.ntiles * g) / a.groups, te = (a.ntiles * (g + 1)) / a.groups;
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(kQLThreads) quantize_lcf_kernel(QArgs a) {
   }
 }
 
-int launch_quantize(const Plan& p, cudaStream_t st) {
+int launch_quantize(const Plan& p, cudaStream_t st, int f0, int nf) {
   if (p.n == 0) return NBZG_OK;
   QArgs a;
   for (int f = 0; f < 6; f++) a.f[f] = p.f[f];
@@ -477,14 +478,16 @@ int launch_quantize(const Plan& p, cudaStream_t st) {
   a.code_stride = (p.n + 7) & ~int64_t(7);
   a.hist = p.hist;
   a.nbins = p.nbins;
-  int per_field = max(1, sm_count() / 6);
+  int per_field = max(1, sm_count() / nf);
   if (per_field > p.ntiles) per_field = (int)p.ntiles;
   a.groups = per_field;
+  a.f0 = f0;
+  a.nf = nf;
   bool aligned = true;
   for (int f = 0; f < 6; f++) aligned &= (reinterpret_cast<uintptr_t>(p.f[f]) & 15) == 0;
   a.use_tma = aligned && (p.tile % 8 == 0);
   size_t sm = 2 * kTileMax * 4 + 2 * kTileMax * 2 + (kQWin + 4) * 4;
-  cudaMemsetAsync(p.hist, 0, sizeof(uint32_t) * 6 * p.nbins, st);
+  cudaMemsetAsync(p.hist + (size_t)f0 * p.nbins, 0, sizeof(uint32_t) * nf * p.nbins, st);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(quantize_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -498,9 +501,9 @@ int launch_quantize(const Plan& p, cudaStream_t st) {
     int blocks = (int)min((p.n + per_cta - 1) / per_cta, (int64_t)(4 * sm_count() / 6 + 1));
     quantize_lcf_kernel<<<dim3(blocks, 6), kQLThreads, 0, st>>>(a);
   } else if (p.sorted) {
-    quantize_kernel<true><<<6 * per_field, kQThreads, sm, st>>>(a);
+    quantize_kernel<true><<<nf * per_field, kQThreads, sm, st>>>(a);
   } else {
-    quantize_kernel<false><<<6 * per_field, kQThreads, sm, st>>>(a);
+    quantize_kernel<false><<<nf * per_field, kQThreads, sm, st>>>(a);
   }
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
