@@ -691,6 +691,32 @@ __global__ void __launch_bounds__(kE1Warps * 32, 2) chunk_bits_kernel(EArgs a, u
     const int mc = (int)min((int64_t)kChunk, a.n - c0);
     const uint4* cp4 = reinterpret_cast<const uint4*>(codes + c0);
     uint32_t mine = 0;  // lane b keeps block b's count
+    if (mc == kChunk) {
+      // full chunk: four blocks per step, their eight 16-byte loads per lane
+      // issued before any is consumed
+#pragma unroll 1
+      for (int b = 0; b < kBlkPerChunk; b += 4) {
+        uint4 q[8];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          q[2 * u] = __ldg(cp4 + (b + u) * (kBlk / 8) + lane);
+          q[2 * u + 1] = __ldg(cp4 + (b + u) * (kBlk / 8) + 32 + lane);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          uint32_t bits = 0;
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            uint32_t cv[8];
+            unpack8(q[2 * u + h], cv);
+#pragma unroll
+            for (int qq = 0; qq < 8; qq++) bits += s_len[cv[qq]] + (cv[qq] == 0 ? 32u : 0u);
+          }
+          bits = warp_sum(bits);
+          mine = lane == b + u ? bits : mine;
+        }
+      }
+    } else
 #pragma unroll 2
     for (int b = 0; b < kBlkPerChunk; b++) {
       const int lo = b * kBlk;
