@@ -33,7 +33,7 @@ struct CBArgs {
   int64_t nchunks;
   int single_field;   // >= 0: only this field (parity hook), meta->f[0] receives
   uint32_t* twin;     // [6][kEncWin] encoder window table (may be null): code
-                      // half+1-kEncWin/2+i -> word << 6 | len (len <= 26, else 0)
+                      // half+1-kEncWin/2+i -> MSB-aligned word | len (len <= 26, else 0)
   uint8_t* tlen8;     // [6][nbins] code length by symbol (may be null)
   int f0;             // first field of this launch (CTA b -> field f0 + b)
 };
@@ -264,7 +264,9 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
         if (a.twin) {
           const uint32_t wi = sym[i] - (uint32_t)(a.nbins / 2 + 1 - kEncWin / 2);
           if (wi < (uint32_t)kEncWin)
-            a.twin[field * kEncWin + wi] = l <= 26 ? (uint32_t)((s_fc[l] + ex) << 6) | l : 0u;
+            // MSB-aligned code word | length (l <= 26 leaves the low 6 bits free)
+            a.twin[field * kEncWin + wi] =
+                l <= 26 ? ((uint32_t)(s_fc[l] + ex) << (32 - l)) | (uint32_t)l : 0u;
         }
         ex++;
       }

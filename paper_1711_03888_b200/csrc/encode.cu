@@ -356,8 +356,8 @@ NBZG_DEV bool win_word(const WinTab& T, uint32_t code, uint64_t& w, uint32_t& l)
   const uint32_t wi = code - T.wlo;
   const uint32_t e = wi < (uint32_t)kEncWin ? T.win[wi] : 0u;
   if (e) {
-    w = e >> 6;
     l = e & 63u;
+    w = (e & ~63u) >> (32 - l);  // entries hold the MSB-aligned word
     return true;
   }
   const uint64_t g = __ldg(&T.lut[code]);
@@ -544,7 +544,7 @@ NBZG_DEV void encode_chunk_fast(const EArgs& a, int field, int64_t c, const WinT
       }
       if (hit) {
 #pragma unroll
-        for (int q = 0; q < 8; q++) append(e[q] >> 6, e[q] & 63u);
+        for (int q = 0; q < 8; q++) append((e[q] & ~63u) >> (32 - (e[q] & 63u)), e[q] & 63u);
       } else {
 #pragma unroll
         for (int q = 0; q < 8; q++) put_code(cv[q], c0 + lo + j + q);
@@ -839,9 +839,8 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
     // ring slot of stream word u: (u + ow) & 15, so 32-byte aligned groups
     // occupy slots 0-7 or 8-15; `rs` = slot counter of the next word
     uint32_t rs = (uint32_t)(widx + ow);
-    // l in [1, 32]: append the low l bits of v
-    auto put32 = [&](uint32_t v, uint32_t l) {
-      const uint32_t wl = v << (32 - l);                 // MSB-aligned
+    // l in [1, 32]: append the l bits of the MSB-aligned word wl
+    auto put_msb = [&](uint32_t wl, uint32_t l) {
       cur |= wl >> nacc;
       const uint32_t spill = __funnelshift_lc(0u, wl, 32 - nacc);  // wl << (32 - nacc), 0 at 32
       const uint32_t t = nacc + l;
@@ -854,6 +853,7 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
       cur = full ? spill : cur;
       nacc = t & 31u;
     };
+    auto put32 = [&](uint32_t v, uint32_t l) { put_msb(v << (32 - l), l); };  // low l bits of v
     auto put64 = [&](uint64_t v, uint32_t l) {  // l <= 64
       if (l > 32) {
         put32((uint32_t)(v >> 32), l - 32);
@@ -914,7 +914,7 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
       if (hit) {
         // <= 8 x 26 bits: at most 7 new words; the ring (16) holds < 8 after a flush
 #pragma unroll
-        for (int q = 0; q < 8; q++) put32(e[q] >> 6, e[q] & 63u);
+        for (int q = 0; q < 8; q++) put_msb(e[q] & ~63u, e[q] & 63u);
       } else {
         // codes re-extracted from the packed group (no dynamically indexed array)
         const uint64_t lo = ((uint64_t)cu.y << 32) | cu.x, hi = ((uint64_t)cu.w << 32) | cu.z;
