@@ -355,24 +355,22 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
         }
         if (j == kQPer / 4 - 1 && last_lane) s_carry2[cur ^ 1] = k[3];
         // histogram
-        uint32_t wb[4], wf[4];  // window bin; far test value (escapes: 0)
+        // window bin code - wlo; escapes (code 0) and far codes fall outside
+        // the window and take the rare per-element path (escapes to bin kQWin)
+        uint32_t wv[4];
 #pragma unroll
-        for (int e = 0; e < 4; e++) {
-          const uint32_t wv = code[e] - (uint32_t)wlo;
-          wb[e] = code[e] == 0u ? (uint32_t)kQWin : wv;
-          wf[e] = code[e] == 0u ? 0u : wv;
-        }
-        const uint32_t wmax = max(max(wf[0], wf[1]), max(wf[2], wf[3]));
+        for (int e = 0; e < 4; e++) wv[e] = code[e] - (uint32_t)wlo;
+        const uint32_t wmax = max(max(wv[0], wv[1]), max(wv[2], wv[3]));
         if (__any_sync(0xffffffffu, wmax >= (uint32_t)kQWin)) {
 #pragma unroll
           for (int e = 0; e < 4; e++) {
-            if (wb[e] <= (uint32_t)kQWin && (code[e] == 0u || wb[e] < (uint32_t)kQWin))
-              red_shared_add1(hwin + 4u * wb[e]);
+            if (code[e] == 0u) red_shared_add1(hwin + 4u * (uint32_t)kQWin);
+            else if (wv[e] < (uint32_t)kQWin) red_shared_add1(hwin + 4u * wv[e]);
             else atomicAdd(&hist[code[e]], 1u);
           }
         } else {
 #pragma unroll
-          for (int e = 0; e < 4; e++) red_shared_add1(hwin + 4u * wb[e]);
+          for (int e = 0; e < 4; e++) red_shared_add1(hwin + 4u * wv[e]);
         }
         cd[32 * j] = make_uint2(code[0] | (code[1] << 16), code[2] | (code[3] << 16));
       }
