@@ -106,3 +106,27 @@ def test_c2_cpc_modes(snap_c2, mode):
     rec2 = nbz.decompress(nio.deserialize_archive(res.archive.serialized()), device=True)
     for fi in range(6):
         assert torch.equal(rec2.field(fi), rec.field(fi)), (mode, fi)
+
+
+@pytest.mark.parametrize("cfg", ["C0", "C1"])
+def test_baseline_configs_byte_identical(O, cfg):
+    """BASELINE configs 0 (HACC-like 100^3, the reference's CPU-runnable case)
+    and 1 (AMDF-like 2^22), at their full sizes: every mode's GPU archive is
+    byte-identical to the oracle's v2 archive and decodes to its values; the
+    ratio is within 0.5% of the reference algorithm's (oracle v1)."""
+    from paper_1711_03888_b200 import datagen
+    fields = datagen.generate(cfg)
+    snap = nbz.ParticleSnapshot(*fields)
+    for mode in ("sz-lv", "sz-lv-prx", "sz-cpc2000", "cpc2000"):
+        res = nbz.compress(snap, mode, nbz.ErrorBoundSpec.relative(1e-4))
+        wire = res.archive.serialized()
+        cpc = mode in ("sz-cpc2000", "cpc2000")
+        ref = (O.compress_cpc if cpc else O.compress)(fields, mode, "rel", 1e-4, fmt=2)
+        assert wire == ref["wire"], (cfg, mode)
+        v1 = (O.compress_cpc if cpc else O.compress)(fields, mode, "rel", 1e-4, fmt=1)
+        assert abs(nbz.ratio(res.archive) / v1["ratio"] - 1) < 0.005, (cfg, mode)
+        out = nbz.decompress(res.archive)
+        odec = (O.decompress_cpc if cpc else O.decompress)(ref["wire"])
+        for fi in range(6):
+            assert np.array_equal(np.asarray(out.field(fi)).view(np.uint32),
+                                  odec[fi].view(np.uint32)), (cfg, mode, fi)
