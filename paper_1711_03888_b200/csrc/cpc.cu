@@ -361,16 +361,19 @@ __global__ void __launch_bounds__(1024) cpc_scan_kernel(CArgs a) {
 // stored byte-swapped (MSB-first bytes); the first and last word of a
 // thread's run can be shared with its neighbours and go out with atomicOr
 struct BitSink {
+  // 32-bit MSB-aligned pending word `cur` holding `nacc` < 32 bits; words
+  // are stored byte-swapped (MSB-first bytes); the first word of a thread's
+  // run (and the last, in finish) can be shared with a neighbour: atomicOr
   uint32_t* words;
-  uint64_t acc;    // MSB-aligned pending bits
-  uint32_t nacc;   // pending bit count (< 32 between puts)
+  uint32_t cur;
+  uint32_t nacc;
   uint64_t wi;     // word index of the pending word
   bool first;
   NBZG_DEV void init(uint32_t* w, uint64_t bitpos) {
     words = w;
     wi = bitpos >> 5;
     nacc = (uint32_t)(bitpos & 31);
-    acc = 0;
+    cur = 0;
     first = true;
   }
   NBZG_DEV void emit(uint32_t v) {
@@ -380,35 +383,46 @@ struct BitSink {
     first = false;
     wi++;
   }
-  NBZG_DEV void put(uint64_t v, int nb) {  // nb <= 32
-    if (nb <= 0) return;
-    v &= (nb == 64) ? ~0ull : ((1ull << nb) - 1);
-    acc |= v << (64 - nacc - nb);
-    nacc += nb;
-    if (nacc >= 32) {
-      emit((uint32_t)(acc >> 32));
-      acc <<= 32;
-      nacc -= 32;
+  NBZG_DEV void put_msb(uint32_t wl, uint32_t l) {  // l in [1, 32], wl MSB-aligned
+    cur |= wl >> nacc;
+    const uint32_t spill = __funnelshift_lc(0u, wl, 32 - nacc);  // wl << (32 - nacc)
+    const uint32_t t = nacc + l;
+    if (t >= 32) {
+      emit(cur);
+      cur = spill;
     }
+    nacc = t & 31u;
+  }
+  NBZG_DEV void put(uint64_t v, int nb) {  // nb <= 32, v < 2^nb
+    if (nb > 0) put_msb((uint32_t)v << (32 - nb), (uint32_t)nb);
   }
   NBZG_DEV void put64(uint64_t v, int nb) {
     if (nb > 32) {
       put(v >> 32, nb - 32);
-      put(v, 32);
+      put(v & 0xffffffffull, 32);
     } else {
       put(v, nb);
     }
   }
   NBZG_DEV void finish() {
-    if (nacc > 0) atomicOr(words + wi, __byte_perm((uint32_t)(acc >> 32), 0, 0x0123));
+    if (nacc > 0) atomicOr(words + wi, __byte_perm(cur, 0, 0x0123));
   }
 };
 
+// one VLC code (_kernels.py:604-620): unary bucket prefix + payload; a code
+// of <= 32 bits goes in with one append
 NBZG_DEV void vlc_emit(BitSink& B, uint64_t m, int sid, const CTabs& T) {
   const int b = T.bkt[sid][bitlen_u64(m)];
-  if (b < 7) B.put((1u << (b + 1)) - 2, b + 1);
-  else B.put(127, 7);
-  B.put64(m, T.w[sid][b]);
+  const uint32_t plen = b < 7 ? (uint32_t)b + 1 : 7u;
+  const uint32_t pval = b < 7 ? (1u << (b + 1)) - 2 : 127u;
+  const uint32_t w = T.w[sid][b];
+  const uint32_t tot = plen + w;
+  if (tot <= 32) {
+    B.put_msb((pval << (32 - plen)) | (uint32_t)(m << (32 - tot)), tot);
+  } else {
+    B.put(pval, (int)plen);
+    B.put64(m, (int)w);
+  }
 }
 
 // grid (nseg, nstreams): the bitstream of every segment
