@@ -149,6 +149,93 @@ NBZG_DEV void block_sort_range(const KeyT* keys, uint16_t* perm, int lo, int m, 
   else block_sort_range_t<KeyT, false>(keys, perm, lo, m, sort_bits, whist, scan_tmp);
 }
 
+// Masked keys of one segment into keys[lo, lo + m) (rindex.py:164-198 +
+// _kernels.py:757-786): exact integerised coordinates minus the segment
+// minima, shifted by drop + ignored groups, bit-interleaved.  Split keys
+// (3w > 32 in a u32 array): part 0 = the low 32 key bits, 1 = the rest.
+template <typename KeyT>
+__device__ __noinline__ void gen_keys(const float* __restrict__ x0p, const float* __restrict__ x1p,
+                                      const float* __restrict__ x2p, const nbzg_field_meta* fm,
+                                      const SegParams* sp, KeyT* keys, int lo, int m, int64_t s0,
+                                      bool split, int part) {
+  const int shift = sp->shift;
+  const int64_t m0 = sp->mn[0], m1 = sp->mn[1], m2 = sp->mn[2];
+  // Segment-wide FP32 path (same margin argument as quantize_kernel):
+  // with tmax = max |x| * inv32 over the segment, |t - rint(t)| < c_c
+  // proves rint(fl(x * inv32)) == rint(f64(x) / 2b); otherwise the exact
+  // FP64 division.  Needs every |t| < 2^22 (32-bit indices).
+  float cm[3];
+  bool small = true;
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    const float tmax = sp->amax[c] * fm[c].inv32;
+    small &= tmax < 4194304.0f;
+    cm[c] = 0.5f - __fmaf_ru(tmax, 2.384185791015625e-07f, 9.5367431640625e-07f);
+  }
+  const float i0 = fm[0].inv32, i1 = fm[1].inv32, i2 = fm[2].inv32;
+  auto mk = [&](uint64_t u0, uint64_t u1, uint64_t u2) -> KeyT {
+    if (sizeof(KeyT) == 8) return (KeyT)make_key<uint64_t>(u0, u1, u2);
+    if (!split) return (KeyT)make_key<uint32_t>(u0, u1, u2);
+    const uint64_t k = make_key<uint64_t>(u0, u1, u2);
+    return (KeyT)(part ? (k >> 32) : k);
+  };
+  auto key_fast = [&](float x0, float x1, float x2) -> KeyT {
+    const float xv[3] = {x0, x1, x2};
+    const float iv[3] = {i0, i1, i2};
+    uint32_t u[3];
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      const float t = xv[c] * iv[c];
+      const float r = t + 12582912.0f;
+      const float d = t - (r - 12582912.0f);
+      int32_t k = __float_as_int(r) - 0x4B400000;
+      if (!(fabsf(d) < cm[c])) k = (int32_t)rint(__ddiv_rn((double)xv[c], fm[c].twob));
+      const int32_t mm = (int32_t)(c == 0 ? m0 : (c == 1 ? m1 : m2));
+      u[c] = (uint32_t)(k - mm) >> shift;
+    }
+    return mk(u[0], u[1], u[2]);
+  };
+  auto key_of = [&](float x0, float x1, float x2) -> KeyT {
+    const float xv[3] = {x0, x1, x2};
+    uint64_t u[3];
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      int64_t iv = fm[c].is_const ? 0 : integerize1(xv[c], fm[c]);
+      int64_t mm = c == 0 ? m0 : (c == 1 ? m1 : m2);
+      u[c] = (uint64_t)(iv - mm) >> shift;
+    }
+    return mk(u[0], u[1], u[2]);
+  };
+  const int m4 = (s0 & 3) ? 0 : m >> 2;  // float4 path needs 16-byte aligned segments
+  const float4* x4[3] = {reinterpret_cast<const float4*>(x0p + s0),
+                         reinterpret_cast<const float4*>(x1p + s0),
+                         reinterpret_cast<const float4*>(x2p + s0)};
+    if (small && sizeof(KeyT) == 4) {
+#pragma unroll 2
+      for (int v = threadIdx.x; v < m4; v += kSortThreads) {
+        const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
+        KeyT* kd = keys + lo + 4 * v;
+        kd[0] = key_fast(q0.x, q1.x, q2.x);
+        kd[1] = key_fast(q0.y, q1.y, q2.y);
+        kd[2] = key_fast(q0.z, q1.z, q2.z);
+        kd[3] = key_fast(q0.w, q1.w, q2.w);
+      }
+    } else {
+#pragma unroll 2
+      for (int v = threadIdx.x; v < m4; v += kSortThreads) {
+        const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
+        KeyT* kd = keys + lo + 4 * v;
+        kd[0] = key_of(q0.x, q1.x, q2.x);
+        kd[1] = key_of(q0.y, q1.y, q2.y);
+        kd[2] = key_of(q0.z, q1.z, q2.z);
+        kd[3] = key_of(q0.w, q1.w, q2.w);
+      }
+    }
+    for (int i = 4 * m4 + threadIdx.x; i < m; i += kSortThreads)
+      keys[lo + i] = key_of(x0p[s0 + i], x1p[s0 + i], x2p[s0 + i]);
+    __syncthreads();
+}
+
 template <typename KeyT>
 __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -271,90 +358,12 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
         for (int c = 0; c < 3; c++) a.minima[3 * (s0 / a.S) + c] = sp.mn[c];
     }
     if (w > 0) {
-      // ---- 2. masked keys
-      const int shift = sp.shift;
-      const int64_t m0 = sp.mn[0], m1 = sp.mn[1], m2 = sp.mn[2];
-      // Segment-wide FP32 path (same margin argument as quantize_kernel):
-      // with tmax = max |x| * inv32 over the segment, |t - rint(t)| < c_c
-      // proves rint(fl(x * inv32)) == rint(f64(x) / 2b); otherwise the exact
-      // FP64 division.  Needs every |t| < 2^22 (32-bit indices).
-      float cm[3];
-      bool small = true;
-#pragma unroll
-      for (int c = 0; c < 3; c++) {
-        const float tmax = sp.amax[c] * fm[c].inv32;
-        small &= tmax < 4194304.0f;
-        cm[c] = 0.5f - __fmaf_ru(tmax, 2.384185791015625e-07f, 9.5367431640625e-07f);
-      }
-      const float i0 = fm[0].inv32, i1 = fm[1].inv32, i2 = fm[2].inv32;
-      int part = 0;  // split keys: 0 = low 32 bits, 1 = high bits
-      auto mk = [&](uint64_t u0, uint64_t u1, uint64_t u2) -> KeyT {
-        if (sizeof(KeyT) == 8) return (KeyT)make_key<uint64_t>(u0, u1, u2);
-        if (!split) return (KeyT)make_key<uint32_t>(u0, u1, u2);
-        const uint64_t k = make_key<uint64_t>(u0, u1, u2);
-        return (KeyT)(part ? (k >> 32) : k);
-      };
-      auto key_fast = [&](float x0, float x1, float x2) -> KeyT {
-        const float xv[3] = {x0, x1, x2};
-        const float iv[3] = {i0, i1, i2};
-        uint32_t u[3];
-#pragma unroll
-        for (int c = 0; c < 3; c++) {
-          const float t = xv[c] * iv[c];
-          const float r = t + 12582912.0f;
-          const float d = t - (r - 12582912.0f);
-          int32_t k = __float_as_int(r) - 0x4B400000;
-          if (!(fabsf(d) < cm[c])) k = (int32_t)rint(__ddiv_rn((double)xv[c], fm[c].twob));
-          const int32_t mm = (int32_t)(c == 0 ? m0 : (c == 1 ? m1 : m2));
-          u[c] = (uint32_t)(k - mm) >> shift;
-        }
-        return mk(u[0], u[1], u[2]);
-      };
-      auto key_of = [&](float x0, float x1, float x2) -> KeyT {
-        const float xv[3] = {x0, x1, x2};
-        uint64_t u[3];
-#pragma unroll
-        for (int c = 0; c < 3; c++) {
-          int64_t iv = fm[c].is_const ? 0 : integerize1(xv[c], fm[c]);
-          int64_t mm = c == 0 ? m0 : (c == 1 ? m1 : m2);
-          u[c] = (uint64_t)(iv - mm) >> shift;
-        }
-        return mk(u[0], u[1], u[2]);
-      };
-      const int m4 = (s0 & 3) ? 0 : m >> 2;  // float4 path needs 16-byte aligned segments
-      const float4* x4[3] = {reinterpret_cast<const float4*>(a.x[0] + s0),
-                             reinterpret_cast<const float4*>(a.x[1] + s0),
-                             reinterpret_cast<const float4*>(a.x[2] + s0)};
-      auto fill = [&]() {
-        if (small && sizeof(KeyT) == 4) {
-#pragma unroll 2
-          for (int v = threadIdx.x; v < m4; v += kSortThreads) {
-            const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
-            KeyT* kd = keys + lo + 4 * v;
-            kd[0] = key_fast(q0.x, q1.x, q2.x);
-            kd[1] = key_fast(q0.y, q1.y, q2.y);
-            kd[2] = key_fast(q0.z, q1.z, q2.z);
-            kd[3] = key_fast(q0.w, q1.w, q2.w);
-          }
-        } else {
-#pragma unroll 2
-          for (int v = threadIdx.x; v < m4; v += kSortThreads) {
-            const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
-            KeyT* kd = keys + lo + 4 * v;
-            kd[0] = key_of(q0.x, q1.x, q2.x);
-            kd[1] = key_of(q0.y, q1.y, q2.y);
-            kd[2] = key_of(q0.z, q1.z, q2.z);
-            kd[3] = key_of(q0.w, q1.w, q2.w);
-          }
-        }
-        for (int i = 4 * m4 + threadIdx.x; i < m; i += kSortThreads)
-          keys[lo + i] = key_of(a.x[0][s0 + i], a.x[1][s0 + i], a.x[2][s0 + i]);
-        __syncthreads();
-      };
       // ---- 3. stable radix sort over 3w bits (one call site: one inlined copy)
       for (int ph = 0; ph < (split ? 2 : 1); ph++) {
-        part = ph;
-        fill();
+        // ---- 2. masked keys (not inlined: none of its state stays live
+        // across the sort, whose rank loop needs the registers)
+        gen_keys<KeyT>(a.x[0], a.x[1], a.x[2], a.meta->f + a.fbase, &sp, keys, lo, m, s0, split,
+                       ph);
         const int nbits = split ? (ph == 0 ? 32 : 3 * w - 32) : 3 * w;
         block_sort_range<KeyT>(keys, perm, lo, m, nbits, whist, scan_tmp);
       }
