@@ -340,6 +340,20 @@ def run_b200(args):
                  "unit": "GB/s", "bytes": "24n + S per direction (SURVEY.md 8d)",
                  "peak": hbm}
 
+    # ---- compress as the reference times it (metrics.py:178-180): including
+    # the payload CRC-64s of the serialised archive (on device), no D2H
+    from paper_1711_03888_b200 import io as _nio
+    tcc = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        r_ = shard.compress_shard(snap, args.mode, bounds, device="cuda").result
+        _nio._payload_crcs(r_.archive)
+        torch.cuda.synchronize()
+        tcc.append(1e3 * (time.perf_counter() - w0))
+    del r_
+    tc_crc = reduce_max(min(tcc), world)
+
     # ---- e2e: host buffers through the public API, H2D/D2H inside the region
     e2e = None
     if args.e2e_steps > 0:
@@ -348,11 +362,23 @@ def run_b200(args):
         # the globally resolved bounds of the device step (identical at N=1)
         e2e_bounds = dict(zip(nbz.FIELD_NAMES, shard_bounds[0]))
 
+        stage_ms = {"compress_h2d": [], "serialized_crc_d2h": [], "deserialize_h2d_crc": [],
+                    "decompress_d2h": []}
+
         def e2e_step():
+            c0 = time.perf_counter()
             res = nbz.compress(hsnap, args.mode, e2e_bounds)
+            torch.cuda.synchronize()
+            c1 = time.perf_counter()
             wire = res.archive.serialized()
+            c2 = time.perf_counter()
             ar = nio.deserialize_archive(wire)
+            torch.cuda.synchronize()
+            c3 = time.perf_counter()
             out = nbz.decompress(ar, device=False)
+            c4 = time.perf_counter()
+            for k, (a0, a1) in zip(stage_ms, ((c0, c1), (c1, c2), (c2, c3), (c3, c4))):
+                stage_ms[k].append(1e3 * (a1 - a0))
             return len(wire), out
 
         # W untimed warm-up calls, as for the device step (they also let the
@@ -362,6 +388,8 @@ def run_b200(args):
         for _ in range(max(3, args.warmup)):
             wl, _o = e2e_step()
         barrier(world)
+        for v in stage_ms.values():
+            v.clear()
         t0 = time.perf_counter()
         marks = [t0]
         for _ in range(args.e2e_steps):
@@ -373,6 +401,7 @@ def run_b200(args):
                "h2d_bytes_per_step": 24 * n + wl, "d2h_bytes_per_step": wl + 24 * n,
                "steps": args.e2e_steps,
                "step_ms": [round(1e3 * (b - a), 1) for a, b in zip(marks, marks[1:])],
+               "stages_ms": {k: round(sum(v) / len(v), 1) for k, v in stage_ms.items() if v},
                "path": "numpy (pinned) -> compress -> serialized() -> deserialize_archive -> "
                        "decompress -> numpy (pooled page-locked output); wall clock, "
                        "max over ranks"}
@@ -407,6 +436,10 @@ def run_b200(args):
             "compress_gbps": 24.0 * n_total / (tc * 1e-3) / 1e9,
             "decompress_gbps": 24.0 * n_total / (td * 1e-3) / 1e9,
             "compress_ms": tc, "decompress_ms": td,
+            "compress_with_crc": {"ms": tc_crc, "gbps": 24.0 * n_total / (tc_crc * 1e-3) / 1e9,
+                                  "note": "compress + payload CRC-64s on device (the reference's "
+                                          "timed compress includes CRC serialisation); wall "
+                                          "clock, best of 3"},
             "ratio": 24.0 * n_total / S_total,
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": hbm,
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
