@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
   }
   __syncthreads();  // ss (global) complete for the fused table
   // fused tables for the thread-per-chunk decoder.  Entry: bits 0-5 code
-  // length (0 = unresolved), bit 6 escape, bits 7-31 lattice delta
+  // length, bit 6 escape, bits 7-31 lattice delta; 64 = unresolved
   // sym - bias.  Primary: 15-bit prefix, codes <= 15 bits.  Secondary: the
   // canonical tail (32-bit window value >= R0, i.e. codes > 15 bits) at W-bit
   // resolution, W <= 24 chosen so the tail fits kTpc2Cap entries.
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
     };
     for (int e = tid; e < (1 << kTpcBits); e += blockDim.x) {
       const int l = lut[e << (kLutBits - kTpcBits)];
-      lut2[e] = (l >= 1 && l <= kTpcBits) ? entry(l, (uint64_t)e << (32 - kTpcBits)) : 0;
+      lut2[e] = (l >= 1 && l <= kTpcBits) ? entry(l, (uint64_t)e << (32 - kTpcBits)) : 64;
     }
     uint64_t R0 = 1ull << 32;
     int W = 0;
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
       int l = 0;
       for (int m = max_len; m > kTpcBits; m--)
         if (u < ((s_fc[m] + s_cbl[m]) << (32 - m))) l = m;
-      lut2[(1 << kTpcBits) + j] = (l > 0 && l <= W) ? entry(l, u) : 0;
+      lut2[(1 << kTpcBits) + j] = (l > 0 && l <= W) ? entry(l, u) : 64;
     }
     if (tid == 0) {
       P.t2_r0 = R0;
@@ -983,6 +983,291 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, 
   }
 }
 
+// ---------------------------------------------------------------- D2'': LV thread per chunk, 64-bit buffer
+// The sz-lv / sz-lv-prx decoder.  Same work split, tables and ring as
+// decode_tpc_kernel, but a shorter dependent chain per symbol: the next bits
+// sit left-aligned in a 64-bit register buffer (hi:lo), so a step is
+//   lookup(hi) -> l -> hi:lo <<= l
+// with the long-code table read speculatively beside the primary one (no
+// branch), one buffer refill from the ring per symbol PAIR (>= 32 valid bits
+// before an even symbol, an odd one checks l <= cnt), and the lattice index
+// accumulated in int64 as the oracle does (orc_dq_dequantize_p).  Anything
+// the fast step cannot take -- escape, unresolved code, too few buffered
+// bits, a ring word not yet loaded -- marks the lane and its 8-symbol group
+// is replayed with exact steps from the saved state.  Stream blocks are read
+// with a 256-byte L2 fill hint: one DRAM burst serves a lane's next 16
+// refills (the 96000 per-chunk streams otherwise miss L2 one sector at a
+// time; -7% kernel time at C2).
+struct BufReader {
+  uint32_t hi, lo;  // next stream bits, MSB first (bit 31 of hi is the next bit)
+  uint32_t cnt;     // valid bits in hi:lo (the bits after them are zero)
+  uint32_t wi;      // next stream word to enter the buffer
+  uint32_t wr;      // first stream word not in the ring (multiple of 4)
+  uint4 qs;         // block wr/4, loaded at the last group boundary
+};
+
+NBZG_DEV uint32_t shl_c(uint32_t x, uint32_t s) {  // s >= 32 -> 0
+  uint32_t r;
+  asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(s));
+  return r;
+}
+NBZG_DEV uint32_t shr_c(uint32_t x, uint32_t s) {  // s >= 32 -> 0
+  uint32_t r;
+  asm("shr.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(s));
+  return r;
+}
+NBZG_DEV void bb_take(BufReader& R, uint32_t l) {  // l <= 32
+  R.hi = __funnelshift_lc(R.lo, R.hi, l);
+  R.lo = shl_c(R.lo, l);
+  R.cnt -= l;
+}
+NBZG_DEV void bb_fill(BufReader& R, uint32_t nw) {  // cnt <= 32
+  R.hi |= shr_c(nw, R.cnt);
+  R.lo |= shl_c(nw, 32u - R.cnt);
+  R.cnt += 32;
+  R.wi += 1;
+}
+NBZG_DEV void bb_init(BufReader& R, const uint4* G, uint32_t* ring, uint64_t bitpos,
+                      uint32_t vmax) {
+  const uint32_t gw0 = (uint32_t)(bitpos >> 5);
+  const uint32_t blk = gw0 >> 2;
+  const uint4 A = __ldg(G + min(blk, vmax)), B = __ldg(G + min(blk + 1, vmax));
+  const uint32_t s0 = (4 * blk) & 7, s1 = s0 ^ 4;  // word w -> slot w & 7
+  ring[(s0 + 0) * kRingStride] = bswap32(A.x);
+  ring[(s0 + 1) * kRingStride] = bswap32(A.y);
+  ring[(s0 + 2) * kRingStride] = bswap32(A.z);
+  ring[(s0 + 3) * kRingStride] = bswap32(A.w);
+  ring[(s1 + 0) * kRingStride] = bswap32(B.x);
+  ring[(s1 + 1) * kRingStride] = bswap32(B.y);
+  ring[(s1 + 2) * kRingStride] = bswap32(B.z);
+  ring[(s1 + 3) * kRingStride] = bswap32(B.w);
+  const uint32_t off = (uint32_t)(bitpos & 31);
+  const uint32_t w0 = ring[(gw0 & 7) * kRingStride], w1 = ring[((gw0 + 1) & 7) * kRingStride];
+  R.hi = __funnelshift_l(w1, w0, off);
+  R.lo = shl_c(w1, off);
+  R.cnt = 64 - off;
+  R.wi = gw0 + 2;
+  R.wr = 4 * (blk + 2);
+  R.qs = make_uint4(0, 0, 0, 0);
+  ldg_v4_if(R.qs, G + min(blk + 2, vmax), true);
+}
+// group boundary: move the block loaded at the last boundary into the ring
+// when its slots are consumed, and issue the next block's load
+NBZG_DEV void ldg_v4_if_l2(uint4& q, const uint4* p, bool pred) {  // 256-byte L2 fill on a miss
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.u32 p, %4, 0;\n"
+      " @p ld.global.nc.L2::256B.v4.u32 {%0, %1, %2, %3}, [%5];\n}\n"
+      : "+r"(q.x), "+r"(q.y), "+r"(q.z), "+r"(q.w)
+      : "r"((uint32_t)pred), "l"(p));
+}
+NBZG_DEV void bb_refill(BufReader& R, uint32_t* ring, const uint4* G, uint32_t vmax) {
+  const bool room = (int32_t)(R.wr - R.wi) <= 4;
+  if (room) {
+    const uint32_t s = R.wr & 7;  // 0 or 4
+    ring[(s + 0) * kRingStride] = bswap32(R.qs.x);
+    ring[(s + 1) * kRingStride] = bswap32(R.qs.y);
+    ring[(s + 2) * kRingStride] = bswap32(R.qs.z);
+    ring[(s + 3) * kRingStride] = bswap32(R.qs.w);
+    R.wr += 4;
+  }
+  ldg_v4_if_l2(R.qs, G + min(R.wr >> 2, vmax), room);
+}
+
+__global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_lv_kernel(DArgs a, int ctas_per_field) {
+  extern __shared__ __align__(16) uint8_t dsm2[];
+  int32_t* LT = reinterpret_cast<int32_t*>(dsm2);  // [2^15 + t2_n]
+  __shared__ uint64_t s_limit[64];
+  __shared__ int32_t s_base[64];
+  const int fi = blockIdx.y;
+  const DField& F = a.f[fi];
+  const DParsed& P = a.parsed[fi];
+  if (F.kind != 3 || P.status || *a.status || P.max_len > 32) return;
+  const int64_t cb = (a.nchunks * blockIdx.x) / ctas_per_field;
+  const int64_t ce = (a.nchunks * (blockIdx.x + 1)) / ctas_per_field;
+  if (cb >= ce) return;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  uint32_t* ring = reinterpret_cast<uint32_t*>(dsm2 + 4 * kTpcTab) + tid;  // [8][kRingStride]
+  const uint32_t* ss = a.ssyms + fi * a.nbins;
+  const uint32_t n2 = P.t2_n;
+  int32_t* LT2 = LT + (1 << kTpcBits);
+  {
+    const int32_t* gl = a.lut2 + (size_t)fi * kTpcTab;
+    const uint32_t nv = ((1u << kTpcBits) + n2 + 3) / 4;
+    for (uint32_t i = tid; i < nv; i += nthr)
+      reinterpret_cast<uint4*>(LT)[i] = __ldg(reinterpret_cast<const uint4*>(gl) + i);
+  }
+  __syncthreads();
+  if (tid < 2 && n2 == 0) LT2[tid] = 64;  // the tail index of an empty long-code table
+  if (tid < 64) {
+    const int l = tid;
+    uint64_t lim = 0;
+    int32_t bs = 0;
+    if (l >= 1 && l <= 32 && l <= (int)P.max_len) {
+      lim = (P.first_code[l] + P.counts[l]) << (32 - l);
+      bs = (int32_t)P.first_idx[l] - (int32_t)P.first_code[l];
+    }
+    s_limit[l] = l > (int)P.max_len ? ~0ull : lim;
+    s_base[l] = bs;
+  }
+  __syncthreads();
+
+  const uintptr_t bits_addr = reinterpret_cast<uintptr_t>(F.payload + P.bits_off);
+  const uint4* G = reinterpret_cast<const uint4*>(bits_addr & ~uintptr_t(15));
+  const uint32_t* G32 = reinterpret_cast<const uint32_t*>(G);
+  const uint32_t a0 = (uint32_t)(bits_addr & 15) * 8;
+  const uint32_t vmax = (uint32_t)((a0 / 8 + 4 * ((P.total_bits + 31) / 32) + 16) / 16);
+  const uint32_t wmax = 4 * vmax + 3;
+  const uint64_t* choff = a.choff + fi * (a.nchunks + 1);
+  const int bias = a.half + 1;
+  const int max_len = (int)P.max_len;
+  const double twob = F.twob;
+  const bool vec = (reinterpret_cast<uintptr_t>(F.out) & 31) == 0;  // 32-byte stores
+  // table index of window v: codes <= 15 bits fill [0, r0) and resolve in
+  // the primary table; the rest index the long-code table, which covers
+  // [r0, 2^32) at 2^sh2 resolution (two unresolved entries when it is empty)
+  const uint32_t r0m1 = (uint32_t)(min(P.t2_r0, (uint64_t)1 << 32) - 1);
+  const uint32_t r0 = r0m1 + 1;
+  const uint32_t sh2 = n2 ? 32u - P.t2_w : 31u;
+  const int lmin = n2 ? (int)P.t2_w : kTpcBits;  // longer codes: canonical search
+  const uint32_t lt_s = (uint32_t)__cvta_generic_to_shared(LT);
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+
+  for (int64_t c = cb + tid; c < ce; c += nthr) {
+    const uint64_t b0 = choff[c];
+    const uint64_t Tb = choff[c + 1] - b0;
+    const int64_t i0 = c * kChunk;
+    const int mc = (int)min((int64_t)kChunk, a.n - i0);
+    const uint64_t B = a0 + b0;
+    BufReader R;
+    bb_init(R, G, ring, B, vmax);
+    long long k = 0;
+    int err = 0;
+    float* dst = F.out + i0;
+    auto consumed = [&]() -> uint64_t { return ((uint64_t)R.wi << 5) - R.cnt - B; };
+    // exact refill to > 32 valid bits (ring, or global words past it)
+    auto fill_safe = [&]() {
+#pragma unroll 1
+      while (R.cnt <= 32) {
+        uint32_t nw;
+        if ((int32_t)(R.wr - R.wi) > 0) {
+          nw = ring[(R.wi & 7) * kRingStride];
+        } else {
+          asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(nw) : "l"(G32 + min(R.wi, wmax)));
+          nw = bswap32(nw);
+        }
+        bb_fill(R, nw);
+      }
+    };
+    // canonical decode of the symbol at v (any length <= 32)
+    auto resolve = [&](uint32_t v) -> int32_t {
+      int32_t e = LT[v >> (32 - kTpcBits)];
+      if ((e & 63) == 0) {
+        e = v > r0m1 ? LT2[(v - r0) >> sh2] : 64;
+        if ((e & 63) == 0) {  // longer than the tables resolve, or invalid
+          int r = 0;
+#pragma unroll 1
+          for (int len = max_len; len > lmin; len--) r = ((uint64_t)v < s_limit[len]) ? len : r;
+          if (r == 0) {
+            err = NBZG_INVALID_CODE;
+            e = 1;
+          } else {
+            const uint32_t sym = __ldg(ss + (uint32_t)(s_base[r] + (int32_t)(v >> (32 - r))));
+            e = sym == 0 ? (r | 64) : (int32_t)(((uint32_t)((int)sym - bias) << 7) | (uint32_t)r);
+          }
+        }
+      }
+      return e;
+    };
+    auto safe_step = [&](float& o) {
+      fill_safe();
+      const int32_t e = resolve(R.hi);
+      bb_take(R, (uint32_t)e & 63u);
+      if (e & 64) {
+        fill_safe();
+        o = __uint_as_float(R.hi);
+        k = esc_k(o, F);
+        bb_take(R, 32);
+      } else {
+        k += (long long)(e >> 7);
+        o = (float)__dmul_rn((double)k, twob);
+      }
+    };
+    auto group = [&](float (&o)[8]) {
+      const uint32_t shi = R.hi, slo = R.lo, scnt = R.cnt, swi = R.wi;
+      const long long sk = k;
+      // int32 lattice index inside the group: 8 deltas move it < 2^19
+      int32_t k32 = (int32_t)k;
+      uint32_t flags = (unsigned long long)(k + (1ll << 30)) >> 31 ? 64u : 0u;  // |k| >= 2^30
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        if ((q & 1) == 0) {  // >= 32 valid bits before an even symbol (branch-free:
+          // both shifts are 0 when cnt > 32)
+          const uint32_t nw = lds_u32(ring_s + ((R.wi & 7) << 12));
+          R.hi |= shr_c(nw, R.cnt);
+          R.lo |= shl_c(nw, 32u - R.cnt);
+          const uint32_t t = R.cnt <= 32 ? 32u : 0u;
+          R.cnt += t;
+          R.wi += t >> 5;
+        }
+        const uint32_t v = R.hi;
+        const uint32_t ix = v > r0m1 ? (1u << kTpcBits) + ((v - r0) >> sh2) : v >> (32 - kTpcBits);
+        const int32_t e = (int32_t)lds_u32(lt_s + (ix << 2));
+        flags |= (uint32_t)e;  // bit 6: escape or unresolved
+        bb_take(R, (uint32_t)e & 63u);
+        k32 += e >> 7;
+        // f32(k * 2b) with k exact in double: 2^52 + 2^31 + k, minus the bias
+        const double kd = __hiloint2double(0x43300000, (int32_t)((uint32_t)k32 ^ 0x80000000u)) -
+                          4503601774854144.0;
+        o[q] = (float)__dmul_rn(kd, twob);
+      }
+      k = k32;
+      // replay when: a flagged entry; an odd symbol longer than the buffered
+      // bits (cnt wrapped: it then stays > 64); a ring word past the ring
+      if ((flags & 64u) || R.cnt > 64 || (int32_t)(R.wi - R.wr) > 0) {
+        R.hi = shi;
+        R.lo = slo;
+        R.cnt = scnt;
+        R.wi = swi;
+        k = sk;
+#pragma unroll 1
+        for (int q = 0; q < 8; q++) {
+          float t;
+          safe_step(t);
+#pragma unroll
+          for (int u = 0; u < 8; u++) o[u] = (u == q) ? t : o[u];
+        }
+      }
+      bb_refill(R, ring, G, vmax);
+    };
+    int i = 0;
+    if (vec) {
+      float oa[8], ob[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) ob[u] = 0.0f;
+      for (; i + 16 <= mc; i += 16) {
+        group(oa);
+        asm volatile("" ::"f"(ob[0]), "f"(ob[1]), "f"(ob[2]), "f"(ob[3]), "f"(ob[4]),
+                     "f"(ob[5]), "f"(ob[6]), "f"(ob[7]));
+        st_v8_cs(dst + i, oa);
+        group(ob);
+        asm volatile("" ::"f"(oa[0]), "f"(oa[1]), "f"(oa[2]), "f"(oa[3]), "f"(oa[4]),
+                     "f"(oa[5]), "f"(oa[6]), "f"(oa[7]));
+        st_v8_cs(dst + i + 8, ob);
+        if (consumed() > Tb) break;  // corrupt: stop early, reported below
+      }
+    }
+    for (; i < mc && consumed() <= Tb; i++) {
+      float o;
+      safe_step(o);
+      if ((i & 7) == 7) bb_refill(R, ring, G, vmax);
+      dst[i] = o;
+    }
+    const uint64_t pos = consumed();
+    if (!err && pos != Tb) err = pos > Tb ? NBZG_TRUNCATED : NBZG_BAD_STREAM;
+    if (err) fail(a.status, (uint32_t)err);
+  }
+}
+
 // v2 streams with codes longer than 32 bits (pathological alphabets):
 // serial decode per chunk (one thread per chunk), same semantics.
 template <bool LCF>
@@ -1227,6 +1512,7 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
                            smax);
       cudaFuncSetAttribute(decode_tpc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            smax);
+      cudaFuncSetAttribute(decode_lv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
       attr2 = true;
     }
     if (any_v2_lcf) {  // sz-lcf streams: thread-per-chunk decoder only
@@ -1235,7 +1521,7 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
     }
     if (use_tpc(a.nchunks)) {
       count_launch();
-      decode_tpc_kernel<false><<<dim3(groups, nf), thr, sm2, st>>>(a, groups);
+      decode_lv_kernel<<<dim3(groups, nf), thr, sm2, st>>>(a, groups);
     } else {
       count_launch();
       decode_kernel<true><<<groups * nf, kDThreads, sm, st>>>(a);
