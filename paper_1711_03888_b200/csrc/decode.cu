@@ -336,6 +336,13 @@ NBZG_DEV void ldg_v4_if(uint4& q, const uint4* p, bool pred) {
       : "+r"(q.x), "+r"(q.y), "+r"(q.z), "+r"(q.w)
       : "r"((uint32_t)pred), "l"(p));
 }
+NBZG_DEV void ldg_v4_if_l2(uint4& q, const uint4* p, bool pred) {  // 256-byte L2 fill on a miss
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.u32 p, %4, 0;\n"
+      " @p ld.global.nc.L2::256B.v4.u32 {%0, %1, %2, %3}, [%5];\n}\n"
+      : "+r"(q.x), "+r"(q.y), "+r"(q.z), "+r"(q.w)
+      : "r"((uint32_t)pred), "l"(p));
+}
 NBZG_DEV void br_skip(BitReader& R, uint32_t l) {  // l <= 32
   R.off += l;
   const bool adv = R.off >= 32;
@@ -723,7 +730,7 @@ NBZG_DEV void tpc_init(TpcReader& R, const uint4* G, uint32_t* ring, int nthr, u
                        uint32_t vmax) {
   const uint32_t gw0 = (uint32_t)(bitpos >> 5);
   const uint32_t blk = gw0 >> 2;
-  const uint4 A = __ldg(G + min(blk, vmax)), B = __ldg(G + min(blk + 1, vmax));
+  const uint4 A = ldg_l2fill(G + min(blk, vmax)), B = ldg_l2fill(G + min(blk + 1, vmax));
   const uint32_t s0 = (4 * blk) & 7, s1 = s0 ^ 4;  // word 4 blk + i -> slot (4 blk + i) & 7
   ring[(s0 + 0) * nthr] = bswap32(A.x);  // words stored byte-swapped
   ring[(s0 + 1) * nthr] = bswap32(A.y);
@@ -739,7 +746,7 @@ NBZG_DEV void tpc_init(TpcReader& R, const uint4* G, uint32_t* ring, int nthr, u
   R.wi = gw0 + 1;
   R.wr = 4 * (blk + 2);
   R.qs = make_uint4(0, 0, 0, 0);
-  ldg_v4_if(R.qs, G + min(blk + 2, vmax), true);
+  ldg_v4_if_l2(R.qs, G + min(blk + 2, vmax), true);
 }
 
 // consume l <= 32 bits.  The next ring word is read unconditionally (its
@@ -773,7 +780,7 @@ NBZG_DEV void tpc_refill(TpcReader& R, uint32_t* ring, int nthr, const uint4* G,
     ring[(s + 3) * nthr] = bswap32(R.qs.w);
     R.wr += 4;
   }
-  ldg_v4_if(R.qs, G + min(R.wr >> 2, vmax), room);
+  ldg_v4_if_l2(R.qs, G + min(R.wr >> 2, vmax), room);
 }
 
 // Lattice-index state of one chunk.  LV: k_i = k_{i-1} + q_i, kept in FP64
@@ -1031,7 +1038,7 @@ NBZG_DEV void bb_init(BufReader& R, const uint4* G, uint32_t* ring, uint64_t bit
                       uint32_t vmax) {
   const uint32_t gw0 = (uint32_t)(bitpos >> 5);
   const uint32_t blk = gw0 >> 2;
-  const uint4 A = __ldg(G + min(blk, vmax)), B = __ldg(G + min(blk + 1, vmax));
+  const uint4 A = ldg_l2fill(G + min(blk, vmax)), B = ldg_l2fill(G + min(blk + 1, vmax));
   const uint32_t s0 = (4 * blk) & 7, s1 = s0 ^ 4;  // word w -> slot w & 7
   ring[(s0 + 0) * kRingStride] = bswap32(A.x);
   ring[(s0 + 1) * kRingStride] = bswap32(A.y);
@@ -1049,17 +1056,10 @@ NBZG_DEV void bb_init(BufReader& R, const uint4* G, uint32_t* ring, uint64_t bit
   R.wi = gw0 + 2;
   R.wr = 4 * (blk + 2);
   R.qs = make_uint4(0, 0, 0, 0);
-  ldg_v4_if(R.qs, G + min(blk + 2, vmax), true);
+  ldg_v4_if_l2(R.qs, G + min(blk + 2, vmax), true);
 }
 // group boundary: move the block loaded at the last boundary into the ring
 // when its slots are consumed, and issue the next block's load
-NBZG_DEV void ldg_v4_if_l2(uint4& q, const uint4* p, bool pred) {  // 256-byte L2 fill on a miss
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.u32 p, %4, 0;\n"
-      " @p ld.global.nc.L2::256B.v4.u32 {%0, %1, %2, %3}, [%5];\n}\n"
-      : "+r"(q.x), "+r"(q.y), "+r"(q.z), "+r"(q.w)
-      : "r"((uint32_t)pred), "l"(p));
-}
 NBZG_DEV void bb_refill(BufReader& R, uint32_t* ring, const uint4* G, uint32_t vmax) {
   const bool room = (int32_t)(R.wr - R.wi) <= 4;
   if (room) {

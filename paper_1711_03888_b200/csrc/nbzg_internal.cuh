@@ -97,6 +97,16 @@ NBZG_DEV uint32_t lds_u16(uint32_t a) {
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
   return v;
 }
+// 16-byte read-only load whose L2 miss fills 256 bytes: for per-thread
+// sequential streams (a warp touching 32 separate streams would otherwise
+// fetch each stream from DRAM one 32-byte sector at a time)
+NBZG_DEV uint4 ldg_l2fill(const uint4* p) {
+  uint4 r;
+  asm("ld.global.nc.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
+  return r;
+}
 NBZG_DEV uint32_t lds_u32(uint32_t a) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
