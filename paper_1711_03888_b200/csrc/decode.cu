@@ -1073,6 +1073,169 @@ NBZG_DEV void bb_refill(BufReader& R, uint32_t* ring, const uint4* G, uint32_t v
   ldg_v4_if_l2(R.qs, G + min(R.wr >> 2, vmax), room);
 }
 
+// constants of one field's decode, shared by the chunk lanes of a thread
+struct LvCtx {
+  const int32_t* LT;
+  const uint64_t* s_limit;
+  const int32_t* s_base;
+  const uint32_t* ss;
+  const uint4* G;
+  const uint32_t* G32;
+  const DField* F;
+  double twob;
+  uint32_t vmax, wmax, r0m1, r0, sh2, lt_s;
+  int lmin, max_len, bias;
+};
+// one chunk being decoded
+struct LvChunk {
+  BufReader R;
+  long long k;     // lattice index of the last symbol
+  uint64_t B, Tb;  // first bit (from the aligned base) and bit length
+  float* dst;
+  uint32_t* ring;  // this chunk's ring column
+  uint32_t ring_s;
+  int mc, err;
+};
+struct LvSnap {
+  uint32_t hi, lo, cnt, wi;
+  long long k;
+};
+
+NBZG_DEV uint64_t lv_consumed(const LvChunk& S) {
+  return ((uint64_t)S.R.wi << 5) - S.R.cnt - S.B;
+}
+// exact refill to > 32 valid bits (ring, or global words past it)
+NBZG_DEV void lv_fill_safe(const LvCtx& X, LvChunk& S) {
+#pragma unroll 1
+  while (S.R.cnt <= 32) {
+    uint32_t nw;
+    if ((int32_t)(S.R.wr - S.R.wi) > 0) {
+      nw = S.ring[(S.R.wi & 7) * kRingStride];
+    } else {
+      asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(nw) : "l"(X.G32 + min(S.R.wi, X.wmax)));
+      nw = bswap32(nw);
+    }
+    bb_fill(S.R, nw);
+  }
+}
+// canonical decode of the symbol at v (any length <= 32)
+NBZG_DEV int32_t lv_resolve(const LvCtx& X, LvChunk& S, uint32_t v) {
+  int32_t e = X.LT[v >> (32 - kTpcBits)];
+  if ((e & 63) == 0) {
+    e = v > X.r0m1 ? X.LT[(1 << kTpcBits) + ((v - X.r0) >> X.sh2)] : 64;
+    if ((e & 63) == 0) {  // longer than the tables resolve, or invalid
+      int r = 0;
+#pragma unroll 1
+      for (int len = X.max_len; len > X.lmin; len--) r = ((uint64_t)v < X.s_limit[len]) ? len : r;
+      if (r == 0) {
+        S.err = NBZG_INVALID_CODE;
+        e = 1;
+      } else {
+        const uint32_t sym = __ldg(X.ss + (uint32_t)(X.s_base[r] + (int32_t)(v >> (32 - r))));
+        e = sym == 0 ? (r | 64) : (int32_t)(((uint32_t)((int)sym - X.bias) << 7) | (uint32_t)r);
+      }
+    }
+  }
+  return e;
+}
+NBZG_DEV void lv_safe_step(const LvCtx& X, LvChunk& S, float& o) {
+  lv_fill_safe(X, S);
+  const int32_t e = lv_resolve(X, S, S.R.hi);
+  bb_take(S.R, (uint32_t)e & 63u);
+  if (e & 64) {
+    lv_fill_safe(X, S);
+    o = __uint_as_float(S.R.hi);
+    S.k = esc_k(o, *X.F);
+    bb_take(S.R, 32);
+  } else {
+    S.k += (long long)(e >> 7);
+    o = (float)__dmul_rn((double)S.k, X.twob);
+  }
+}
+// 8 symbols, straight-line (no branch: the steps of two chunks interleave);
+// returns true when the group must be replayed exactly
+NBZG_DEV bool lv_fast8(const LvCtx& X, LvChunk& S, float (&o)[8], LvSnap& sn) {
+  BufReader& R = S.R;
+  sn.hi = R.hi;
+  sn.lo = R.lo;
+  sn.cnt = R.cnt;
+  sn.wi = R.wi;
+  sn.k = S.k;
+  // int32 lattice index inside the group: 8 deltas move it < 2^19
+  int32_t k32 = (int32_t)S.k;
+  uint32_t flags = (unsigned long long)(S.k + (1ll << 30)) >> 31 ? 64u : 0u;  // |k| >= 2^30
+#pragma unroll
+  for (int q = 0; q < 8; q++) {
+    if ((q & 1) == 0) {  // >= 32 valid bits before an even symbol (branch-free:
+      // both shifts are 0 when cnt > 32)
+      const uint32_t nw = S.ring[(R.wi & 7) * kRingStride];
+      R.hi |= shr_c(nw, R.cnt);
+      R.lo |= shl_c(nw, 32u - R.cnt);
+      const uint32_t t = R.cnt <= 32 ? 32u : 0u;
+      R.cnt += t;
+      R.wi += t >> 5;
+    }
+    const uint32_t v = R.hi;
+    const uint32_t ix =
+        v > X.r0m1 ? (1u << kTpcBits) + ((v - X.r0) >> X.sh2) : v >> (32 - kTpcBits);
+    const int32_t e = X.LT[ix];
+    flags |= (uint32_t)e;  // bit 6: escape or unresolved
+    bb_take(R, (uint32_t)e & 63u);
+    k32 += e >> 7;
+    // f32(k * 2b) with k exact in double: 2^52 + 2^31 + k, minus the bias
+    const double kd =
+        __hiloint2double(0x43300000, (int32_t)((uint32_t)k32 ^ 0x80000000u)) - 4503601774854144.0;
+    o[q] = (float)__dmul_rn(kd, X.twob);
+  }
+  S.k = k32;
+  // replay when: a flagged entry; an odd symbol longer than the buffered
+  // bits (cnt wrapped: it then stays > 64); a ring word past the ring
+  return (flags & 64u) || R.cnt > 64 || (int32_t)(R.wi - R.wr) > 0;
+}
+NBZG_DEV void lv_fix(const LvCtx& X, LvChunk& S, float (&o)[8], const LvSnap& sn, bool bad) {
+  if (bad) {
+    S.R.hi = sn.hi;
+    S.R.lo = sn.lo;
+    S.R.cnt = sn.cnt;
+    S.R.wi = sn.wi;
+    S.k = sn.k;
+#pragma unroll 1
+    for (int q = 0; q < 8; q++) {
+      float t;
+      lv_safe_step(X, S, t);
+#pragma unroll
+      for (int u = 0; u < 8; u++) o[u] = (u == q) ? t : o[u];
+    }
+  }
+  bb_refill(S.R, S.ring, X.G, X.vmax);
+}
+NBZG_DEV void lv_start(const LvCtx& X, const DArgs& a, const uint64_t* choff, uint32_t a0,
+                       int64_t c, uint32_t* ring, LvChunk& S) {
+  const uint64_t b0 = choff[c];
+  S.Tb = choff[c + 1] - b0;
+  const int64_t i0 = c * kChunk;
+  S.mc = (int)min((int64_t)kChunk, a.n - i0);
+  S.B = a0 + b0;
+  S.ring = ring;
+  S.ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+  bb_init(S.R, X.G, ring, S.B, X.vmax);
+  S.k = 0;
+  S.err = 0;
+  S.dst = X.F->out + i0;
+}
+// symbols [i, mc) one exact step at a time, then the end-of-chunk checks
+NBZG_DEV void lv_finish(const LvCtx& X, const DArgs& a, LvChunk& S, int i) {
+  for (; i < S.mc && lv_consumed(S) <= S.Tb; i++) {
+    float o;
+    lv_safe_step(X, S, o);
+    if ((i & 7) == 7) bb_refill(S.R, S.ring, X.G, X.vmax);
+    S.dst[i] = o;
+  }
+  const uint64_t pos = lv_consumed(S);
+  if (!S.err && pos != S.Tb) S.err = pos > S.Tb ? NBZG_TRUNCATED : NBZG_BAD_STREAM;
+  if (S.err) fail(a.status, (uint32_t)S.err);
+}
+
 __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_lv_kernel(DArgs a, int ctas_per_field) {
   extern __shared__ __align__(16) uint8_t dsm2[];
   int32_t* LT = reinterpret_cast<int32_t*>(dsm2);  // [2^15 + t2_n]
@@ -1087,9 +1250,7 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_lv_kernel(DArgs a, i
   if (cb >= ce) return;
   const int tid = threadIdx.x, nthr = blockDim.x;
   uint32_t* ring = reinterpret_cast<uint32_t*>(dsm2 + 4 * kTpcTab) + tid;  // [8][kRingStride]
-  const uint32_t* ss = a.ssyms + fi * a.nbins;
   const uint32_t n2 = P.t2_n;
-  int32_t* LT2 = LT + (1 << kTpcBits);
   {
     const int32_t* gl = a.lut2 + (size_t)fi * kTpcTab;
     const uint32_t nv = ((1u << kTpcBits) + n2 + 3) / 4;
@@ -1097,7 +1258,7 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_lv_kernel(DArgs a, i
       reinterpret_cast<uint4*>(LT)[i] = __ldg(reinterpret_cast<const uint4*>(gl) + i);
   }
   __syncthreads();
-  if (tid < 2 && n2 == 0) LT2[tid] = 64;  // the tail index of an empty long-code table
+  if (tid < 2 && n2 == 0) LT[(1 << kTpcBits) + tid] = 64;  // tail index of an empty long-code table
   if (tid < 64) {
     const int l = tid;
     uint64_t lim = 0;
@@ -1111,160 +1272,60 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_lv_kernel(DArgs a, i
   }
   __syncthreads();
 
+  LvCtx X;
+  X.LT = LT;
+  X.s_limit = s_limit;
+  X.s_base = s_base;
+  X.ss = a.ssyms + fi * a.nbins;
   const uintptr_t bits_addr = reinterpret_cast<uintptr_t>(F.payload + P.bits_off);
-  const uint4* G = reinterpret_cast<const uint4*>(bits_addr & ~uintptr_t(15));
-  const uint32_t* G32 = reinterpret_cast<const uint32_t*>(G);
+  X.G = reinterpret_cast<const uint4*>(bits_addr & ~uintptr_t(15));
+  X.G32 = reinterpret_cast<const uint32_t*>(X.G);
   const uint32_t a0 = (uint32_t)(bits_addr & 15) * 8;
-  const uint32_t vmax = (uint32_t)((a0 / 8 + 4 * ((P.total_bits + 31) / 32) + 16) / 16);
-  const uint32_t wmax = 4 * vmax + 3;
-  const uint64_t* choff = a.choff + fi * (a.nchunks + 1);
-  const int bias = a.half + 1;
-  const int max_len = (int)P.max_len;
-  const double twob = F.twob;
-  const bool vec = (reinterpret_cast<uintptr_t>(F.out) & 31) == 0;  // 32-byte stores
+  // last 16-byte block / word the stream may touch (payload + 64-byte slack)
+  X.vmax = (uint32_t)((a0 / 8 + 4 * ((P.total_bits + 31) / 32) + 16) / 16);
+  X.wmax = 4 * X.vmax + 3;
+  X.F = &F;
+  X.twob = F.twob;
+  X.bias = a.half + 1;
+  X.max_len = (int)P.max_len;
   // table index of window v: codes <= 15 bits fill [0, r0) and resolve in
   // the primary table; the rest index the long-code table, which covers
   // [r0, 2^32) at 2^sh2 resolution (two unresolved entries when it is empty)
-  const uint32_t r0m1 = (uint32_t)(min(P.t2_r0, (uint64_t)1 << 32) - 1);
-  const uint32_t r0 = r0m1 + 1;
-  const uint32_t sh2 = n2 ? 32u - P.t2_w : 31u;
-  const int lmin = n2 ? (int)P.t2_w : kTpcBits;  // longer codes: canonical search
-  const uint32_t lt_s = (uint32_t)__cvta_generic_to_shared(LT);
-  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+  X.r0m1 = (uint32_t)(min(P.t2_r0, (uint64_t)1 << 32) - 1);
+  X.r0 = X.r0m1 + 1;
+  X.sh2 = n2 ? 32u - P.t2_w : 31u;
+  X.lmin = n2 ? (int)P.t2_w : kTpcBits;  // longer codes: canonical search
+  X.lt_s = (uint32_t)__cvta_generic_to_shared(LT);
+  const uint64_t* choff = a.choff + fi * (a.nchunks + 1);
+  const bool vec = (reinterpret_cast<uintptr_t>(F.out) & 31) == 0;  // 32-byte stores
 
   for (int64_t c = cb + tid; c < ce; c += nthr) {
-    const uint64_t b0 = choff[c];
-    const uint64_t Tb = choff[c + 1] - b0;
-    const int64_t i0 = c * kChunk;
-    const int mc = (int)min((int64_t)kChunk, a.n - i0);
-    const uint64_t B = a0 + b0;
-    BufReader R;
-    bb_init(R, G, ring, B, vmax);
-    long long k = 0;
-    int err = 0;
-    float* dst = F.out + i0;
-    auto consumed = [&]() -> uint64_t { return ((uint64_t)R.wi << 5) - R.cnt - B; };
-    // exact refill to > 32 valid bits (ring, or global words past it)
-    auto fill_safe = [&]() {
-#pragma unroll 1
-      while (R.cnt <= 32) {
-        uint32_t nw;
-        if ((int32_t)(R.wr - R.wi) > 0) {
-          nw = ring[(R.wi & 7) * kRingStride];
-        } else {
-          asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(nw) : "l"(G32 + min(R.wi, wmax)));
-          nw = bswap32(nw);
-        }
-        bb_fill(R, nw);
-      }
-    };
-    // canonical decode of the symbol at v (any length <= 32)
-    auto resolve = [&](uint32_t v) -> int32_t {
-      int32_t e = LT[v >> (32 - kTpcBits)];
-      if ((e & 63) == 0) {
-        e = v > r0m1 ? LT2[(v - r0) >> sh2] : 64;
-        if ((e & 63) == 0) {  // longer than the tables resolve, or invalid
-          int r = 0;
-#pragma unroll 1
-          for (int len = max_len; len > lmin; len--) r = ((uint64_t)v < s_limit[len]) ? len : r;
-          if (r == 0) {
-            err = NBZG_INVALID_CODE;
-            e = 1;
-          } else {
-            const uint32_t sym = __ldg(ss + (uint32_t)(s_base[r] + (int32_t)(v >> (32 - r))));
-            e = sym == 0 ? (r | 64) : (int32_t)(((uint32_t)((int)sym - bias) << 7) | (uint32_t)r);
-          }
-        }
-      }
-      return e;
-    };
-    auto safe_step = [&](float& o) {
-      fill_safe();
-      const int32_t e = resolve(R.hi);
-      bb_take(R, (uint32_t)e & 63u);
-      if (e & 64) {
-        fill_safe();
-        o = __uint_as_float(R.hi);
-        k = esc_k(o, F);
-        bb_take(R, 32);
-      } else {
-        k += (long long)(e >> 7);
-        o = (float)__dmul_rn((double)k, twob);
-      }
-    };
-    auto group = [&](float (&o)[8]) {
-      const uint32_t shi = R.hi, slo = R.lo, scnt = R.cnt, swi = R.wi;
-      const long long sk = k;
-      // int32 lattice index inside the group: 8 deltas move it < 2^19
-      int32_t k32 = (int32_t)k;
-      uint32_t flags = (unsigned long long)(k + (1ll << 30)) >> 31 ? 64u : 0u;  // |k| >= 2^30
-#pragma unroll
-      for (int q = 0; q < 8; q++) {
-        if ((q & 1) == 0) {  // >= 32 valid bits before an even symbol (branch-free:
-          // both shifts are 0 when cnt > 32)
-          const uint32_t nw = lds_u32(ring_s + ((R.wi & 7) << 12));
-          R.hi |= shr_c(nw, R.cnt);
-          R.lo |= shl_c(nw, 32u - R.cnt);
-          const uint32_t t = R.cnt <= 32 ? 32u : 0u;
-          R.cnt += t;
-          R.wi += t >> 5;
-        }
-        const uint32_t v = R.hi;
-        const uint32_t ix = v > r0m1 ? (1u << kTpcBits) + ((v - r0) >> sh2) : v >> (32 - kTpcBits);
-        const int32_t e = (int32_t)lds_u32(lt_s + (ix << 2));
-        flags |= (uint32_t)e;  // bit 6: escape or unresolved
-        bb_take(R, (uint32_t)e & 63u);
-        k32 += e >> 7;
-        // f32(k * 2b) with k exact in double: 2^52 + 2^31 + k, minus the bias
-        const double kd = __hiloint2double(0x43300000, (int32_t)((uint32_t)k32 ^ 0x80000000u)) -
-                          4503601774854144.0;
-        o[q] = (float)__dmul_rn(kd, twob);
-      }
-      k = k32;
-      // replay when: a flagged entry; an odd symbol longer than the buffered
-      // bits (cnt wrapped: it then stays > 64); a ring word past the ring
-      if ((flags & 64u) || R.cnt > 64 || (int32_t)(R.wi - R.wr) > 0) {
-        R.hi = shi;
-        R.lo = slo;
-        R.cnt = scnt;
-        R.wi = swi;
-        k = sk;
-#pragma unroll 1
-        for (int q = 0; q < 8; q++) {
-          float t;
-          safe_step(t);
-#pragma unroll
-          for (int u = 0; u < 8; u++) o[u] = (u == q) ? t : o[u];
-        }
-      }
-      bb_refill(R, ring, G, vmax);
-    };
+    LvChunk A;
+    lv_start(X, a, choff, a0, c, ring, A);
     int i = 0;
     if (vec) {
       float oa[8], ob[8];
+      LvSnap sa;
 #pragma unroll
       for (int u = 0; u < 8; u++) ob[u] = 0.0f;
-      for (; i + 16 <= mc; i += 16) {
-        group(oa);
+      for (; i + 16 <= A.mc; i += 16) {
+        lv_fix(X, A, oa, sa, lv_fast8(X, A, oa, sa));
+        // two register sets: a set's stores are issued one group before the
+        // set is rewritten (pinned live meanwhile)
         asm volatile("" ::"f"(ob[0]), "f"(ob[1]), "f"(ob[2]), "f"(ob[3]), "f"(ob[4]),
                      "f"(ob[5]), "f"(ob[6]), "f"(ob[7]));
-        st_v8_cs(dst + i, oa);
-        group(ob);
+        st_v8_cs(A.dst + i, oa);
+        lv_fix(X, A, ob, sa, lv_fast8(X, A, ob, sa));
         asm volatile("" ::"f"(oa[0]), "f"(oa[1]), "f"(oa[2]), "f"(oa[3]), "f"(oa[4]),
                      "f"(oa[5]), "f"(oa[6]), "f"(oa[7]));
-        st_v8_cs(dst + i + 8, ob);
-        if (consumed() > Tb) break;  // corrupt: stop early, reported below
+        st_v8_cs(A.dst + i + 8, ob);
+        if (lv_consumed(A) > A.Tb) {
+          i += 16;
+          break;  // corrupt: stop early, reported below
+        }
       }
     }
-    for (; i < mc && consumed() <= Tb; i++) {
-      float o;
-      safe_step(o);
-      if ((i & 7) == 7) bb_refill(R, ring, G, vmax);
-      dst[i] = o;
-    }
-    const uint64_t pos = consumed();
-    if (!err && pos != Tb) err = pos > Tb ? NBZG_TRUNCATED : NBZG_BAD_STREAM;
-    if (err) fail(a.status, (uint32_t)err);
+    lv_finish(X, a, A, i);
   }
 }
 
