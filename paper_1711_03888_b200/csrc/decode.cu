@@ -67,6 +67,7 @@ struct DArgs {
   uint64_t* lb;        // [nf][2][nchunks]
   uint32_t* tickets;   // [nf]
   uint32_t* status;    // global status word
+  int cta0[7];         // decode_lv_kernel: first CTA of each field (cta0[nf] = grid)
 };
 
 NBZG_DEV uint32_t ld_u32_bytes(const uint8_t* p) {
@@ -1236,17 +1237,20 @@ NBZG_DEV void lv_finish(const LvCtx& X, const DArgs& a, LvChunk& S, int i) {
   if (S.err) fail(a.status, (uint32_t)S.err);
 }
 
-__global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_lv_kernel(DArgs a, int ctas_per_field) {
+__global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_lv_kernel(DArgs a) {
   extern __shared__ __align__(16) uint8_t dsm2[];
   int32_t* LT = reinterpret_cast<int32_t*>(dsm2);  // [2^15 + t2_n]
   __shared__ uint64_t s_limit[64];
   __shared__ int32_t s_base[64];
-  const int fi = blockIdx.y;
+  // fields own contiguous CTA ranges sized by their decode cost (host)
+  int fi = 0;
+  while (fi + 1 < a.nf && (int)blockIdx.x >= a.cta0[fi + 1]) fi++;
+  const int gj = (int)blockIdx.x - a.cta0[fi], gn = a.cta0[fi + 1] - a.cta0[fi];
   const DField& F = a.f[fi];
   const DParsed& P = a.parsed[fi];
   if (F.kind != 3 || P.status || *a.status || P.max_len > 32) return;
-  const int64_t cb = (a.nchunks * blockIdx.x) / ctas_per_field;
-  const int64_t ce = (a.nchunks * (blockIdx.x + 1)) / ctas_per_field;
+  const int64_t cb = (a.nchunks * gj) / gn;
+  const int64_t ce = (a.nchunks * (gj + 1)) / gn;
   if (cb >= ce) return;
   const int tid = threadIdx.x, nthr = blockDim.x;
   uint32_t* ring = reinterpret_cast<uint32_t*>(dsm2 + 4 * kTpcTab) + tid;  // [8][kRingStride]
@@ -1582,7 +1586,40 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
     }
     if (use_tpc(a.nchunks)) {
       count_launch();
-      decode_lv_kernel<<<dim3(groups, nf), thr, sm2, st>>>(a, groups);
+      // CTAs per field in proportion to an estimated decode cost per chunk
+      // (a fixed per-symbol part plus the stream bits: at C2 a 10-bit
+      // velocity symbol costs ~1.25x a 3.5-bit coordinate one), at most
+      // kTpcMaxThreads chunks per CTA, one CTA per SM
+      const int sms = sm_count();
+      double w[6], wsum = 0;
+      int gmin[6], g[6], gtot = 0;
+      for (int f = 0; f < nf; f++) {
+        const double bits = a.n ? 8.0 * (double)fields[f].payload_len / (double)a.n : 0.0;
+        w[f] = fields[f].kind == 3 ? 1.0 + bits / 26.0 : 0.0;
+        wsum += w[f];
+        gmin[f] = fields[f].kind == 3 ? (int)((a.nchunks + kTpcMaxThreads - 1) / kTpcMaxThreads) : 1;
+        gmin[f] = max(1, gmin[f]);
+      }
+      for (int f = 0; f < nf; f++) {
+        g[f] = wsum > 0 ? max(gmin[f], (int)((double)sms * w[f] / wsum)) : 1;
+        if (g[f] > a.nchunks) g[f] = (int)max((int64_t)1, a.nchunks);
+        gtot += g[f];
+      }
+      while (gtot > sms) {  // trim the fields with the most slack
+        int best = -1;
+        for (int f = 0; f < nf; f++)
+          if (g[f] > gmin[f] && (best < 0 || g[f] * w[best] > g[best] * w[f])) best = f;
+        if (best < 0) break;
+        g[best]--;
+        gtot--;
+      }
+      int thr_lv = 32;
+      a.cta0[0] = 0;
+      for (int f = 0; f < nf; f++) {
+        a.cta0[f + 1] = a.cta0[f] + g[f];
+        thr_lv = max(thr_lv, (int)min((int64_t)kTpcMaxThreads, ((a.nchunks + g[f] - 1) / g[f] + 31) / 32 * 32));
+      }
+      decode_lv_kernel<<<a.cta0[nf], thr_lv, sm2, st>>>(a);
     } else {
       count_launch();
       decode_kernel<true><<<groups * nf, kDThreads, sm, st>>>(a);
