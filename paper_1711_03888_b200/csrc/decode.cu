@@ -37,6 +37,7 @@ constexpr int kSmemSyms = 16384;   // sorted-symbol table staged in smem up to t
 constexpr int kTpcBits = 15;       // thread-per-chunk fused table index bits (i32, 128 KiB)
 constexpr int kTpc2Cap = 16384;    // secondary (long-code) table entries (64 KiB)
 constexpr int kTpcMaxThreads = 704;
+constexpr int kLvMaxThreads = 768;  // decode_lv_kernel: 80 registers x 768 fit the register file
 constexpr int kRingStride = 1024;  // words between ring slots (power of two, >= threads)
 constexpr int kTpcTab = (1 << kTpcBits) + kTpc2Cap;
 
@@ -1237,7 +1238,7 @@ NBZG_DEV void lv_finish(const LvCtx& X, const DArgs& a, LvChunk& S, int i) {
   if (S.err) fail(a.status, (uint32_t)S.err);
 }
 
-__global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_lv_kernel(DArgs a) {
+__global__ void __launch_bounds__(kLvMaxThreads, 1) decode_lv_kernel(DArgs a) {
   extern __shared__ __align__(16) uint8_t dsm2[];
   int32_t* LT = reinterpret_cast<int32_t*>(dsm2);  // [2^15 + t2_n]
   __shared__ uint64_t s_limit[64];
@@ -1589,7 +1590,7 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
       // CTAs per field in proportion to an estimated decode cost per chunk
       // (a fixed per-symbol part plus the stream bits: at C2 a 10-bit
       // velocity symbol costs ~1.25x a 3.5-bit coordinate one), at most
-      // kTpcMaxThreads chunks per CTA, one CTA per SM
+      // kLvMaxThreads chunks per CTA, one CTA per SM
       const int sms = sm_count();
       double w[6], wsum = 0;
       int gmin[6], g[6], gtot = 0;
@@ -1597,7 +1598,7 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
         const double bits = a.n ? 8.0 * (double)fields[f].payload_len / (double)a.n : 0.0;
         w[f] = fields[f].kind == 3 ? 1.0 + bits / 26.0 : 0.0;
         wsum += w[f];
-        gmin[f] = fields[f].kind == 3 ? (int)((a.nchunks + kTpcMaxThreads - 1) / kTpcMaxThreads) : 1;
+        gmin[f] = fields[f].kind == 3 ? (int)((a.nchunks + kLvMaxThreads - 1) / kLvMaxThreads) : 1;
         gmin[f] = max(1, gmin[f]);
       }
       for (int f = 0; f < nf; f++) {
@@ -1617,7 +1618,7 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
       a.cta0[0] = 0;
       for (int f = 0; f < nf; f++) {
         a.cta0[f + 1] = a.cta0[f] + g[f];
-        thr_lv = max(thr_lv, (int)min((int64_t)kTpcMaxThreads, ((a.nchunks + g[f] - 1) / g[f] + 31) / 32 * 32));
+        thr_lv = max(thr_lv, (int)min((int64_t)kLvMaxThreads, ((a.nchunks + g[f] - 1) / g[f] + 31) / 32 * 32));
       }
       decode_lv_kernel<<<a.cta0[nf], thr_lv, sm2, st>>>(a);
     } else {
