@@ -13,7 +13,10 @@
  *   - the caller owns and pre-allocates every buffer (workspace sizes come
  *     from the *_workspace_size queries);
  *   - `stream` is a cudaStream_t passed as void*; every call is async on it
- *     and keeps no mutable global state (reentrant across streams);
+ *     and reentrant across streams and host threads: all per-call state lives
+ *     in the caller's workspace; the only process-wide state is mutex-guarded
+ *     (per-device kernel attributes / SM counts, the opt-in launch counter and
+ *     event trace);
  *   - the return value is a status (NBZG_OK = 0); device-side failures
  *     (bound too small, invalid code, ...) are reported through the
  *     `status` word of the nbzg_meta block written by the call.
@@ -101,7 +104,13 @@ typedef struct nbzg_compress_args {
   int32_t cpc;            /* 0; 1 = sz-cpc2000, 2 = cpc2000 (full keys, no clamp, minima) */
   int64_t *seg_minima;    /* device, 3 x nseg (cpc) */
   uint32_t sz_skip;       /* bit f: no SZ stream for field f (cpc modes) */
-  uint32_t pad2;
+  int32_t phase;          /* 0: the whole compress.  Sharded compress in two
+                             calls with the same args and workspace: 1 = K1 only, this
+                             shard's exact f32 min/max -> meta->f[i].lo / .hi; 2 = resume
+                             with the GLOBAL min/max in h_minmax (all-gathered by the
+                             caller), so bounds resolve as on the whole snapshot
+                             (model.py:104-125) and K1 is not run twice */
+  float h_minmax[12];     /* phase 2: (lo, hi) of field 0..5, host values */
 } nbzg_compress_args;
 
 size_t nbzg_compress_workspace_size(int64_t n, int32_t sorted, int64_t interval_count,
@@ -117,7 +126,9 @@ int nbzg_compress(const nbzg_compress_args *args, void *stream);
  * (v1 reference streams, exact sequential chain); + NBZG_KIND_LCF (16) when the
  * archive's mode is sz-lcf (LCF predictor instead of last value).
  * payload: device bytes, any alignment, readable for payload_len + 64 bytes.
- * status: device u32, receives the first failure (NBZG_*). */
+ * status: device u32, receives the first failure (NBZG_*); the caller zeroes
+ * it (it is never cleared here, so one word can collect the failures of
+ * several decodes, e.g. a CPC coordinate stream and the SZ velocities). */
 typedef struct nbzg_decompress_args {
   const uint8_t *payload[6];
   int64_t payload_len[6];

@@ -77,7 +77,8 @@ class CompressArgs(ctypes.Structure):
                 ("ignored_groups", c_i32), ("rindex_variant", c_i32), ("workspace", c_p),
                 ("workspace_bytes", c_sz), ("arena", c_p), ("arena_bytes", c_sz),
                 ("meta", c_p), ("seg_bits", c_p), ("perm", c_p), ("predictor", c_i32),
-                ("cpc", c_i32), ("seg_minima", c_p), ("sz_skip", c_u32), ("pad2", c_u32)]
+                ("cpc", c_i32), ("seg_minima", c_p), ("sz_skip", c_u32), ("phase", c_i32),
+                ("h_minmax", c_f * 12)]
 
 
 class CpcMeta(ctypes.Structure):
@@ -204,37 +205,27 @@ def trace_read(max_entries: int = 65536):
             for i in range(cnt)]
 
 
-class _Pool:
-    """Grow-only device scratch buffers keyed by role (one set per device)."""
-
-    def __init__(self):
-        self._bufs: Dict[Tuple[int, str], object] = {}
-
-    def get(self, role: str, nbytes: int):
-        import torch
-        dev = torch.cuda.current_device()
-        key = (dev, role)
-        b = self._bufs.get(key)
-        if b is None or b.numel() < nbytes:
-            b = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device="cuda")
-            self._bufs[key] = b
-        return b
-
-    def clear(self):
-        self._bufs.clear()
+def workspace(nbytes: int):
+    """Per-call device scratch (uint8) from torch's caching allocator on the
+    current stream: repeated calls reuse the cached block, and concurrent
+    calls (host threads, each on its own stream) never share one -- the
+    C-ABI keeps all per-call state in this buffer."""
+    import torch
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device="cuda")
 
 
-POOL = _Pool()
-
-_SIDE: Dict[int, list] = {}
+_SIDE: Dict[Tuple[int, int], list] = {}
+_side_lock = threading.Lock()
 
 
 def side_streams(k: int):
-    """k persistent side CUDA streams of the current device (overlapping
-    independent per-stream decodes)."""
+    """k persistent side CUDA streams of the current device and host thread
+    (overlapping independent per-stream decodes; a host thread never shares
+    its side streams with another)."""
     import torch
-    dev = torch.cuda.current_device()
-    lst = _SIDE.setdefault(dev, [])
-    while len(lst) < k:
-        lst.append(torch.cuda.Stream())
-    return lst[:k]
+    key = (torch.cuda.current_device(), threading.get_ident())
+    with _side_lock:
+        lst = _SIDE.setdefault(key, [])
+        while len(lst) < k:
+            lst.append(torch.cuda.Stream())
+        return lst[:k]

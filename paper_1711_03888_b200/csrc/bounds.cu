@@ -196,6 +196,23 @@ int launch_minmax_seg(const Plan& p, cudaStream_t st) {
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
 
+// sharded compress, phase 2: the all-gathered global (lo, hi) per field
+struct MinMax12 {
+  float v[12];
+};
+__global__ void minmax_set_kernel(MinMax12 h, uint32_t* mm) {
+  const int i = threadIdx.x;
+  if (i < 12) mm[i] = f2ord(h.v[i]);
+}
+
+int launch_minmax_set(const float* h_minmax12, uint32_t* mm, cudaStream_t st) {
+  MinMax12 h;
+  for (int i = 0; i < 12; i++) h.v[i] = h_minmax12[i];
+  count_launch();
+  minmax_set_kernel<<<1, 32, 0, st>>>(h, mm);
+  return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
+}
+
 // resolve_field_bounds (pipeline.py:157-181): constant fields (zero range)
 // take the fast path regardless of bound kind; others get
 // b = value (absolute) or b = value * (float(hi) - float(lo)) in f64.

@@ -1,8 +1,9 @@
 #include <cstdio>
 #include <cstdlib>
 // capi.cu -- the extern "C" boundary (include/nbzg.h): argument validation,
-// workspace carving and kernel sequencing.  No mutable global state beyond
-// one-time cudaFuncSetAttribute calls.
+// workspace carving and kernel sequencing.  Process-wide state is limited to
+// mutex-guarded caches (per-device shared-memory attributes and SM counts)
+// and the opt-in diagnostics (launch counter, event trace).
 #include <atomic>
 #include <cstring>
 #include <mutex>
@@ -75,15 +76,41 @@ void trace_mark(const char* name, cudaStream_t st) {
   g_marks.push_back({name, e});
 }
 
+// SM count of the current device (cached per device)
 int sm_count() {
-  static int c = 0;
-  if (!c) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) dev = 0;
+  if (dev >= 64) {
+    int c = 0;
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    return c > 0 ? c : 148;
+  }
+  int c = cache[dev].load(std::memory_order_relaxed);
+  if (c <= 0) {
     cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
     if (c <= 0) c = 148;
+    cache[dev].store(c, std::memory_order_relaxed);
   }
   return c;
+}
+
+void smem_attr(const void* func, int bytes) {
+  struct Done {
+    int dev;
+    const void* func;
+    int bytes;
+  };
+  static std::mutex mu;
+  static std::vector<Done> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  for (const Done& d : done)
+    if (d.dev == dev && d.func == func && d.bytes >= bytes) return;
+  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
+      cudaSuccess)
+    done.push_back({dev, func, bytes});
 }
 
 static inline size_t al256(size_t v) { return (v + 255) & ~size_t(255); }
@@ -288,16 +315,26 @@ int nbzg_compress(const nbzg_compress_args* a, void* stream) {
   p.arena = a->arena;
   p.arena_bytes = a->arena_bytes;
   int rc;
+  if (a->phase < 0 || a->phase > 2) return NBZG_BAD_ARG;
   trace_mark(nullptr, st);
   // sorted mode with 3-field keys: K1 walks whole segments and also leaves
   // each segment's key-field min/max, so K2 reads the coordinates once
   const bool segmm = p.sorted && p.variant != 2 && p.n > 0 && p.S % 4 == 0;
-  if ((rc = segmm ? launch_minmax_seg(p, st) : launch_minmax6(p.f, p.n, p.minmax, st))) return rc;
+  if (a->phase == 2) {
+    // K1 ran in phase 1 (its segment min/max are still in the workspace);
+    // the global min/max replace the shard's
+    for (int i = 0; i < 12; i++)
+      if (a->h_minmax[i] != a->h_minmax[i]) return NBZG_BAD_ARG;  // NaN
+    if ((rc = launch_minmax_set(a->h_minmax, p.minmax, st))) return rc;
+  } else {
+    if ((rc = segmm ? launch_minmax_seg(p, st) : launch_minmax6(p.f, p.n, p.minmax, st)))
+      return rc;
+  }
   if (!segmm) p.seg_mm = nullptr;
   trace_mark("minmax6", st);
   if ((rc = launch_resolve(p, st))) return rc;
   trace_mark("resolve", st);
-  if (p.n == 0) return cuda_status();
+  if (p.n == 0 || a->phase == 1) return cuda_status();
   if (p.sorted) {
     if ((rc = launch_rindex_sort(p, st))) return rc;
     trace_mark("rindex_sort", st);
@@ -337,7 +374,8 @@ int nbzg_decompress(const nbzg_decompress_args* a, void* stream) {
     f[i].inv32 = (float)f[i].inv;
     f[i].out = a->out[i];
   }
-  cudaMemsetAsync(a->status, 0, sizeof(uint32_t), st);
+  // the status word is the caller's (zeroed by it): a preceding decode on
+  // the same word (the CPC coordinate stream) keeps its failure
   trace_mark(nullptr, st);
   return launch_decompress(f, a->nfields, a->n, a->interval_count,
                            a->workspace, a->workspace_bytes, a->status, st);
@@ -377,10 +415,11 @@ int nbzg_integerize(const float* x, int64_t n, double bound, int64_t* ints, uint
   if (!(bound > 0)) return NBZG_BAD_ARG;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   double twob = 2.0 * bound, inv = 1.0 / twob;
-  if (n > 0)
+  if (n > 0) {
     count_launch();
     integerize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, n, twob, inv, (float)inv,
                                                                    ints, status_dev);
+  }
   return cuda_status();
 }
 

@@ -294,11 +294,7 @@ int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uin
                          uint32_t* twin, uint8_t* tlen8, int f0, int nf) {
   CBArgs a{hist, nbins, sym, len, lut, scratch, meta, n, nchunks, single_field, twin, tlen8, f0};
   size_t sm = 14 * (size_t)kCBSmemK;  // keys u64 | L u32 | order u16
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(codebook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = true;
-  }
+  smem_attr((const void*)codebook_kernel, (int)sm);
   count_launch();
   codebook_kernel<<<single_field >= 0 ? 1 : nf, kCBThreads, sm, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
@@ -344,7 +340,7 @@ int launch_huffman_lengths(const uint32_t* counts, int64_t k, uint8_t* lengths, 
                            uint32_t* status, cudaStream_t st) {
   if (k <= 0 || k > 65536) return NBZG_BAD_ARG;
   size_t sm = 12 * (size_t)kCBSmemK;
-  cudaFuncSetAttribute(huffman_lengths_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  smem_attr((const void*)huffman_lengths_kernel, (int)sm);
   count_launch();
   huffman_lengths_kernel<<<1, kCBThreads, sm, st>>>(counts, (int)k, lengths, scr, status);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;

@@ -1552,13 +1552,8 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
   chunk_offsets_kernel<<<nf, 1024, 0, st>>>(a);
   trace_mark("dq_offsets", st);
   size_t sm = (1 << kLutBits) + kSmemSyms * 2;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm);
-    attr = true;
-  }
+  smem_attr((const void*)decode_kernel<true>, (int)sm);
+  smem_attr((const void*)decode_kernel<false>, (int)sm);
   bool any_v2 = false, any_v2_lcf = false, any_v1 = false;
   for (int i = 0; i < nf; i++) {
     any_v2 |= (fields[i].kind & 15) == 3;
@@ -1571,15 +1566,11 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
     const int per = (int)((a.nchunks + groups - 1) / groups);
     const int thr = min(kTpcMaxThreads, (per + 31) / 32 * 32);
     const size_t sm2 = 4 * kTpcTab + 32 * (size_t)kRingStride;
-    static bool attr2 = false;
-    if (!attr2) {  // sized for the largest launch
+    {  // sized for the largest launch
       const int smax = 4 * kTpcTab + 32 * kRingStride;
-      cudaFuncSetAttribute(decode_tpc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           smax);
-      cudaFuncSetAttribute(decode_tpc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           smax);
-      cudaFuncSetAttribute(decode_lv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-      attr2 = true;
+      smem_attr((const void*)decode_tpc_kernel<false>, smax);
+      smem_attr((const void*)decode_tpc_kernel<true>, smax);
+      smem_attr((const void*)decode_lv_kernel, smax);
     }
     if (any_v2_lcf) {  // sz-lcf streams: thread-per-chunk decoder only
       count_launch();

@@ -986,13 +986,8 @@ int launch_encode(const Plan& p, cudaStream_t st, int f0, int nf) {
     uint64_t* coff = p.enc_boff;
     uint32_t* bpre = reinterpret_cast<uint32_t*>(p.enc_boff + 6 * (p.nchunks + 1));
     uint32_t* ctot = bpre + 6 * nb;
-    static bool attr3 = false;
-    if (!attr3) {
-      cudaFuncSetAttribute(chunk_bits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-      cudaFuncSetAttribute(encode_tpc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           4 * kEncWin + 4 * kE3Ring * kE3Threads);
-      attr3 = true;
-    }
+    smem_attr((const void*)chunk_bits_kernel, 65536);
+    smem_attr((const void*)encode_tpc_kernel, 4 * kEncWin + 4 * kE3Ring * kE3Threads);
     int g1 = max(1, 2 * sm_count() / nf);
     if (g1 > (p.nchunks + kE1Warps - 1) / kE1Warps) g1 = (int)((p.nchunks + kE1Warps - 1) / kE1Warps);
     count_launch();
@@ -1006,12 +1001,7 @@ int launch_encode(const Plan& p, cudaStream_t st, int f0, int nf) {
         a, coff, bpre, g3);
   } else if (p.nbins == 65536) {
     const size_t sm = 4 * kEncWin + kEFWarps * 64 * 12 + kEFWarps * 32 * 4;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(encode_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sm);
-      attr = true;
-    }
+    smem_attr((const void*)encode_fast_kernel, (int)sm);
     int groups = max(1, 2 * sm_count() / 6);
     const int64_t need = (p.nchunks + kEFWarps - 1) / kEFWarps;
     if (groups > need) groups = (int)need;

@@ -66,6 +66,7 @@ void plan_shape(Plan& p, int64_t n, int sorted, int64_t interval_count, int64_t 
 // kernel launchers (each enqueues on `st`)
 int launch_minmax6(const float* const* f, int64_t n, uint32_t* minmax12, cudaStream_t st);
 int launch_minmax_seg(const Plan& p, cudaStream_t st);
+int launch_minmax_set(const float* h_minmax12, uint32_t* minmax12, cudaStream_t st);
 int launch_resolve(const Plan& p, cudaStream_t st);
 int launch_rindex_sort(const Plan& p, cudaStream_t st);
 int launch_quantize(const Plan& p, cudaStream_t st, int f0 = 0, int nf = 6);
@@ -76,5 +77,9 @@ bool encode_uses_tpc(const Plan& p);
 int launch_sz_skip(const Plan& p, cudaStream_t st);
 
 int sm_count();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel,
+// size): the attribute is per device, so a process-wide flag would leave a
+// second GPU at the 48 KB default.  Thread-safe.
+void smem_attr(const void* func, int bytes);
 
 }  // namespace nbzg

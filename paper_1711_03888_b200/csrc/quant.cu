@@ -486,13 +486,8 @@ int launch_quantize(const Plan& p, cudaStream_t st, int f0, int nf) {
   a.use_tma = aligned && (p.tile % 8 == 0);
   size_t sm = 2 * kTileMax * 4 + 2 * kTileMax * 2 + (kQWin + 4) * 4;
   cudaMemsetAsync(p.hist + (size_t)f0 * p.nbins, 0, sizeof(uint32_t) * nf * p.nbins, st);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(quantize_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(quantize_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm);
-    attr = true;
-  }
+  smem_attr((const void*)quantize_kernel<true>, (int)sm);
+  smem_attr((const void*)quantize_kernel<false>, (int)sm);
   count_launch();
   if (p.predictor == 1) {
     const int64_t per_cta = (int64_t)kQLThreads * 16;

@@ -504,18 +504,10 @@ int launch_rindex_sort(const Plan& p, cudaStream_t st) {
   a.seg_mm = p.seg_mm;
   size_t sm32 = kTileMax * (4 + 2) + kSortWarps * kRadix * 2;
   size_t sm64 = kTileMax * (8 + 2) + kSortWarps * kRadix * 2;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(rindex_sort_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm32);
-    cudaFuncSetAttribute(rindex_sort_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm64);
-    cudaFuncSetAttribute(rindex_sort6_kernel<uint32_t>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm32);
-    cudaFuncSetAttribute(rindex_sort6_kernel<uint64_t>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm64);
-    attr = true;
-  }
+  smem_attr((const void*)rindex_sort_kernel<uint32_t>, (int)sm32);
+  smem_attr((const void*)rindex_sort_kernel<uint64_t>, (int)sm64);
+  smem_attr((const void*)rindex_sort6_kernel<uint32_t>, (int)sm32);
+  smem_attr((const void*)rindex_sort6_kernel<uint64_t>, (int)sm64);
   cudaMemsetAsync(p.tile_flags, 0, sizeof(uint32_t) * p.ntiles, st);
   a.pass = 0;
   count_launch();
@@ -675,7 +667,7 @@ int launch_prx_order(const uint64_t* keys, int64_t n, int64_t S, const uint8_t* 
   if (S > kTileMax) return NBZG_UNSUPPORTED;
   OArgs a{keys, n, S, seg_bits, ig, order};
   size_t sm = kTileMax * (8 + 2) + kSortWarps * kRadix * 2;
-  cudaFuncSetAttribute(prx_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  smem_attr((const void*)prx_order_kernel, (int)sm);
   int64_t nseg = (n + S - 1) / S;
   if (nseg > 0) {
     count_launch();

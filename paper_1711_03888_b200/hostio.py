@@ -6,10 +6,15 @@ transfer therefore goes through two grow-only pinned staging buffers: the
 DMA of chunk k+1 overlaps the (multi-threaded) CPU copy of chunk k between
 the staging buffer and the caller's pageable memory.  Already-pinned host
 tensors are copied directly.
+
+The staging buffers are process-wide, so staged copies hold a lock and
+return only once the DMA that reads / writes the staging memory is done:
+concurrent callers (host threads) never share a buffer in flight.
 """
 
 from __future__ import annotations
 
+import threading
 from typing import Dict, Tuple
 
 import numpy as np
@@ -17,17 +22,19 @@ import numpy as np
 CHUNK = 64 << 20  # bytes per staging chunk
 
 _pinned: Dict[Tuple[str, int], object] = {}
+_stage_lock = threading.RLock()  # the staging buffers, the pinned cache, the pool
 
 
 def pinned(role: str, nbytes: int):
     """Grow-only pinned uint8 host buffer keyed by role."""
     import torch
     key = (role, 0)
-    b = _pinned.get(key)
-    if b is None or b.numel() < nbytes:
-        b = torch.empty(max(int(nbytes), 4096), dtype=torch.uint8, pin_memory=True)
-        _pinned[key] = b
-    return b
+    with _stage_lock:
+        b = _pinned.get(key)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(max(int(nbytes), 4096), dtype=torch.uint8, pin_memory=True)
+            _pinned[key] = b
+        return b
 
 
 def _host_u8(buf):
@@ -57,18 +64,22 @@ def to_device(src, dst) -> None:
     if h.is_pinned():
         dst[:n].copy_(h, non_blocking=True)
         return
-    stage = [pinned("h2d0", CHUNK), pinned("h2d1", CHUNK)]
-    ev = [None, None]
-    stream = torch.cuda.current_stream()
-    for k, off in enumerate(range(0, n, CHUNK)):
-        m = min(CHUNK, n - off)
-        s = k & 1
-        if ev[s] is not None:
-            ev[s].synchronize()  # the DMA that last read this buffer is done
-        stage[s][:m].copy_(h[off:off + m])
-        dst[off:off + m].copy_(stage[s][:m], non_blocking=True)
-        ev[s] = torch.cuda.Event()
-        ev[s].record(stream)
+    with _stage_lock:
+        stage = [pinned("h2d0", CHUNK), pinned("h2d1", CHUNK)]
+        ev = [None, None]
+        stream = torch.cuda.current_stream()
+        for k, off in enumerate(range(0, n, CHUNK)):
+            m = min(CHUNK, n - off)
+            s = k & 1
+            if ev[s] is not None:
+                ev[s].synchronize()  # the DMA that last read this buffer is done
+            stage[s][:m].copy_(h[off:off + m])
+            dst[off:off + m].copy_(stage[s][:m], non_blocking=True)
+            ev[s] = torch.cuda.Event()
+            ev[s].record(stream)
+        for e in ev:  # the staging buffers are free before another caller writes them
+            if e is not None:
+                e.synchronize()
 
 
 def to_host(src, dst) -> None:
@@ -82,26 +93,27 @@ def to_host(src, dst) -> None:
     if h.is_pinned():
         h.copy_(src[:n], non_blocking=False)
         return
-    stage = [pinned("d2h0", CHUNK), pinned("d2h1", CHUNK)]
-    stream = torch.cuda.current_stream()
-    chunks = list(range(0, n, CHUNK))
-    ev = [None, None]
+    with _stage_lock:
+        stage = [pinned("d2h0", CHUNK), pinned("d2h1", CHUNK)]
+        stream = torch.cuda.current_stream()
+        chunks = list(range(0, n, CHUNK))
+        ev = [None, None]
 
-    def issue(k):
-        off = chunks[k]
-        m = min(CHUNK, n - off)
-        stage[k & 1][:m].copy_(src[off:off + m], non_blocking=True)
-        e = torch.cuda.Event()
-        e.record(stream)
-        ev[k & 1] = e
+        def issue(k):
+            off = chunks[k]
+            m = min(CHUNK, n - off)
+            stage[k & 1][:m].copy_(src[off:off + m], non_blocking=True)
+            e = torch.cuda.Event()
+            e.record(stream)
+            ev[k & 1] = e
 
-    issue(0)
-    for k, off in enumerate(chunks):
-        if k + 1 < len(chunks):
-            issue(k + 1)
-        ev[k & 1].synchronize()
-        m = min(CHUNK, n - off)
-        h[off:off + m].copy_(stage[k & 1][:m])
+        issue(0)
+        for k, off in enumerate(chunks):
+            if k + 1 < len(chunks):
+                issue(k + 1)
+            ev[k & 1].synchronize()
+            m = min(CHUNK, n - off)
+            h[off:off + m].copy_(stage[k & 1][:m])
 
 
 def _advise_huge(addr: int, nbytes: int) -> None:
@@ -183,6 +195,10 @@ class PinnedPool:
         self.misses = {}  # nbytes -> count
 
     def take(self, nbytes: int):
+        with _stage_lock:
+            return self._take(nbytes)
+
+    def _take(self, nbytes: int):
         import sys
         lst = self.blocks.setdefault(nbytes, [])
         for i in range(len(lst)):

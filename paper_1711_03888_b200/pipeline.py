@@ -155,16 +155,34 @@ def slot_field(slot: int) -> int:
 class Archive:
     """Self-describing compressed container (in-memory form, pipeline.py:116-143).
 
-    Same attributes as the reference.  ``streams`` and ``serialized()`` pull
-    payload bytes off the device on first use.
+    Same constructor and attributes as the reference's dataclass:
+    ``Archive(mode, n, interval_count, segment_size, ignored_groups,
+    rindex_variant, bounds, constant_mask, constants, segments, streams,
+    _wire=None)``.  The B200 path builds archives whose payloads stay in HBM
+    (keyword-only ``device``; ``seg_bits`` / ``seg_minima`` arrays instead of
+    Segment objects); ``streams``, ``segments`` and ``serialized()`` pull
+    bytes off the device on first use.  ``version`` is the container
+    version: 2 when a stream is SZ_DQ or the payloads are device-resident,
+    else 1 (reference streams).
     """
 
     def __init__(self, mode: Mode, n: int, interval_count: int, segment_size: int,
                  ignored_groups: int, rindex_variant: Optional[RIndexVariant],
                  bounds: Tuple[float, ...], constant_mask: int, constants: Tuple[float, ...],
-                 seg_bits=None, streams: Optional[Tuple[Stream, ...]] = None,
-                 device: Optional[_Device] = None, version: int = 2,
-                 device_output: bool = False, seg_minima=None):
+                 segments: Optional[Tuple[Segment, ...]] = None,
+                 streams: Optional[Tuple[Stream, ...]] = None, _wire: Optional[bytes] = None,
+                 *, seg_bits=None, device: Optional[_Device] = None,
+                 version: Optional[int] = None, device_output: bool = False, seg_minima=None):
+        if segments is not None and seg_bits is None and len(segments):
+            segments = tuple(segments)
+            seg_bits = np.array([s.bits for s in segments], np.uint8)
+            if mode.stores_minima:
+                seg_minima = np.array([tuple(s.minima) for s in segments],
+                                      np.int64).reshape(-1, 3)
+        if version is None:
+            v2 = device is not None or any(
+                int(s.kind) == int(StreamKind.SZ_DQ) for s in (streams or ()))
+            version = 2 if v2 else 1
         self.mode = mode
         self.n = int(n)
         self.interval_count = int(interval_count)
@@ -176,12 +194,13 @@ class Archive:
         self.constants = tuple(float(c) for c in constants)
         self._seg_bits = seg_bits          # numpy u8 or CUDA tensor or None
         self._seg_minima = seg_minima      # (nseg, 3) int64 numpy or CUDA tensor (CPC modes)
-        self._segments: Optional[Tuple[Segment, ...]] = None
-        self._streams = streams
+        self._segments: Optional[Tuple[Segment, ...]] = (
+            tuple(segments) if segments is not None and len(segments) else None)
+        self._streams = tuple(streams) if streams is not None else None
         self._dev = device
         self.version = version
         self.device_output = device_output
-        self._wire: Optional[bytes] = None
+        self._wire: Optional[bytes] = _wire
         self._host_dir = None  # deserialized: [(kind, field, wire offset, length)]
 
     # -- reference attributes -------------------------------------------------
@@ -265,16 +284,22 @@ class Archive:
 
 class CompressResult:
     """pipeline.py:146-149: the archive plus the sorted-mode permutation
-    sidecar (``order[i]`` = original index of sorted position i)."""
+    sidecar (``order[i]`` = original index of sorted position i).  Same
+    constructor as the reference (``CompressResult(archive, order)``); the
+    B200 path passes the device permutation (keyword-only ``perm``, u16
+    tile-local) and the int64 ``order`` is expanded from it on first use."""
 
-    def __init__(self, archive: Archive, perm=None, tile: int = 16384):
+    def __init__(self, archive: Archive, order: Optional[np.ndarray] = None, *, perm=None,
+                 tile: int = 16384):
         self.archive = archive
         self._perm = perm
         self._tile = tile
-        self._order = None
+        self._order = None if order is None else np.asarray(order, np.int64)
 
     @property
     def order(self) -> Optional[np.ndarray]:
+        if self._order is not None:
+            return self._order
         if self._perm is None:
             return None
         if self._order is None:
@@ -284,7 +309,7 @@ class CompressResult:
     def order_device(self):
         import torch
         if self._perm is None:
-            return None
+            return None if self._order is None else torch.from_numpy(self._order).cuda()
         n = self.archive.n
         out = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
         L = N.lib()
@@ -385,85 +410,144 @@ def compress(snapshot: ParticleSnapshot, mode, bounds: Bounds,
         best.archive.device_output = bool(snapshot.on_device)
         del hold
         return best
-    mode = _as_mode(mode)
-    if mode not in GPU_MODES:
-        raise ValidationError(f"mode {mode.value} is not implemented by the B200 path")
-    specs = _specs(bounds)
-    n = snapshot.n
-    L = N.lib()
-    fields, _hold = device_fields(snapshot)
-    sorted_mode = 1 if (mode.is_sorted and n > 0) else 0
-    ic = settings.interval_count
-    if ic > 65536:
-        raise ValidationError("the B200 path supports interval_count <= 65536")
-    S = settings.segment_size
-    if sorted_mode and S > 16384:
-        raise ValidationError("the B200 path supports segment_size <= 16384")
-    ws_bytes = L.nbzg_compress_workspace_size(n, sorted_mode, ic, S)
-    ws = N.POOL.get("compress_ws", ws_bytes)
-    arena_bytes = L.nbzg_compress_arena_bound(n, ic)
-    arena = torch.empty(arena_bytes, dtype=torch.uint8, device="cuda")
-    meta_t = torch.empty(ctypes.sizeof(N.Meta), dtype=torch.uint8, device="cuda")
-    nseg = (n + S - 1) // S if sorted_mode else 0
-    seg_bits = torch.empty(max(nseg, 1), dtype=torch.uint8, device="cuda")
-    perm = torch.empty(max(n, 1), dtype=torch.int16, device="cuda") if sorted_mode else None
-    cpc = (1 if mode is Mode.SZ_CPC2000 else 2 if mode is Mode.CPC2000 else 0) if sorted_mode else 0
-    minima = torch.empty(3 * max(nseg, 1), dtype=torch.int64, device="cuda") if cpc else None
-    a = N.CompressArgs()
-    for i in range(6):
-        a.fields[i] = N.ptr(fields[i]) if n else None
-        a.bound_kind[i] = 0 if specs[i].kind is BoundKind.ABSOLUTE else 1
-        a.bound_value[i] = float(specs[i].value)
-    a.n = n
-    a.sorted = sorted_mode
-    a.interval_count = ic
-    a.segment_size = S
-    a.ignored_groups = settings.ignored_groups
-    a.rindex_variant = 0 if mode.stores_minima else _VARIANT_CODE[settings.rindex_variant]
-    a.cpc = cpc
-    if cpc:
-        a.seg_minima = N.ptr(minima)
-        a.sz_skip = 0b000111 if cpc == 1 else 0b111111
-    a.predictor = 1 if mode is Mode.SZ_LCF else 0
-    a.workspace = N.ptr(ws)
-    a.workspace_bytes = ws.numel()
-    a.arena = N.ptr(arena)
-    a.arena_bytes = arena.numel()
-    a.meta = N.ptr(meta_t)
-    a.seg_bits = N.ptr(seg_bits)
-    a.perm = N.ptr(perm) if perm is not None else None
-    N.check(L.nbzg_compress(ctypes.byref(a), N.stream_handle()), "compress")
-    meta = N.Meta.from_buffer_copy(meta_t.cpu().numpy().tobytes())
-    _raise_status(meta.status, "compress")
-    offsets, lengths, kinds = [], [], []
-    for fi in range(6):
-        fm = meta.f[fi]
-        if n == 0 or fm.is_const:
-            offsets.append(None)
-            lengths.append(0)
+    return _CompressCall(snapshot, mode, bounds, settings).finish()
+
+
+class _CompressCall:
+    """One nbzg_compress call: argument block, per-call workspace and
+    outputs.  ``finish()`` runs the whole compress (phase 0).  The sharded
+    compress (shard.py) splits it: ``local_minmax()`` runs K1 only (phase
+    1), the caller all-gathers the shards' min/max, and ``finish(global)``
+    resumes with them (phase 2) on the same workspace, so K1 runs once."""
+
+    def __init__(self, snapshot: ParticleSnapshot, mode, bounds: Bounds,
+                 settings: Settings = DEFAULT_SETTINGS):
+        import torch
+        mode = _as_mode(mode)
+        if mode not in GPU_MODES:
+            raise ValidationError(f"mode {mode.value} is not implemented by the B200 path")
+        specs = _specs(bounds)
+        n = snapshot.n
+        self.L = L = N.lib()
+        fields, self._hold = device_fields(snapshot)
+        sorted_mode = 1 if (mode.is_sorted and n > 0) else 0
+        ic = settings.interval_count
+        if ic > 65536:
+            raise ValidationError("the B200 path supports interval_count <= 65536")
+        S = settings.segment_size
+        if sorted_mode and S > 16384:
+            raise ValidationError("the B200 path supports segment_size <= 16384")
+        ws_bytes = L.nbzg_compress_workspace_size(n, sorted_mode, ic, S)
+        self.ws = N.workspace(ws_bytes)
+        arena_bytes = L.nbzg_compress_arena_bound(n, ic)
+        self.arena = torch.empty(arena_bytes, dtype=torch.uint8, device="cuda")
+        self.meta_t = torch.empty(ctypes.sizeof(N.Meta), dtype=torch.uint8, device="cuda")
+        nseg = (n + S - 1) // S if sorted_mode else 0
+        self.seg_bits = torch.empty(max(nseg, 1), dtype=torch.uint8, device="cuda")
+        self.perm = (torch.empty(max(n, 1), dtype=torch.int16, device="cuda")
+                     if sorted_mode else None)
+        cpc = ((1 if mode is Mode.SZ_CPC2000 else 2 if mode is Mode.CPC2000 else 0)
+               if sorted_mode else 0)
+        self.minima = (torch.empty(3 * max(nseg, 1), dtype=torch.int64, device="cuda")
+                       if cpc else None)
+        a = self.args = N.CompressArgs()
+        for i in range(6):
+            a.fields[i] = N.ptr(fields[i]) if n else None
+            a.bound_kind[i] = 0 if specs[i].kind is BoundKind.ABSOLUTE else 1
+            a.bound_value[i] = float(specs[i].value)
+        a.n = n
+        a.sorted = sorted_mode
+        a.interval_count = ic
+        a.segment_size = S
+        a.ignored_groups = settings.ignored_groups
+        a.rindex_variant = 0 if mode.stores_minima else _VARIANT_CODE[settings.rindex_variant]
+        a.cpc = cpc
+        if cpc:
+            a.seg_minima = N.ptr(self.minima)
+            a.sz_skip = 0b000111 if cpc == 1 else 0b111111
+        a.predictor = 1 if mode is Mode.SZ_LCF else 0
+        a.workspace = N.ptr(self.ws)
+        a.workspace_bytes = self.ws.numel()
+        a.arena = N.ptr(self.arena)
+        a.arena_bytes = self.arena.numel()
+        a.meta = N.ptr(self.meta_t)
+        a.seg_bits = N.ptr(self.seg_bits)
+        a.perm = N.ptr(self.perm) if self.perm is not None else None
+        self.fields, self.mode, self.settings = fields, mode, settings
+        self.n, self.S, self.nseg, self.ic, self.cpc = n, S, nseg, ic, cpc
+        self.sorted_mode = sorted_mode
+        self.on_device = snapshot.on_device
+        self._phase1 = False
+
+    def _meta(self):
+        return N.Meta.from_buffer_copy(self.meta_t.cpu().numpy().tobytes())
+
+    def local_minmax(self) -> np.ndarray:
+        """Phase 1: this snapshot's exact f32 (min, max) per field, (6, 2)
+        float64; (+inf, -inf) rows for an empty snapshot."""
+        out = np.empty((6, 2), np.float64)
+        if self.n == 0:
+            out[:, 0], out[:, 1] = np.inf, -np.inf
+            return out
+        self.args.phase = 1
+        N.check(self.L.nbzg_compress(ctypes.byref(self.args), N.stream_handle()), "compress")
+        meta = self._meta()
+        for i in range(6):
+            out[i] = (meta.f[i].lo, meta.f[i].hi)
+        self._phase1 = True
+        return out
+
+    def finish(self, global_minmax=None) -> CompressResult:
+        """The rest of the compress: phase 0 (whole call) or, after
+        ``local_minmax()``, phase 2 with the global (6, 2) min/max."""
+        a = self.args
+        n = self.n
+        if global_minmax is not None and n > 0:
+            if not self._phase1:
+                raise ValidationError("finish(global_minmax) needs local_minmax() first")
+            mm = np.asarray(global_minmax, np.float64).reshape(6, 2)
+            a.phase = 2
+            for i in range(6):
+                a.h_minmax[2 * i] = float(mm[i, 0])
+                a.h_minmax[2 * i + 1] = float(mm[i, 1])
         else:
-            offsets.append(int(fm.payload_off))
-            lengths.append(int(fm.payload_len))
-        kinds.append(int(StreamKind.SZ_DQ))
-    dev = _Device(arena[:max(int(meta.arena_used), 1)], offsets, lengths, kinds,
-                  keep=(meta_t,))
-    if cpc:
-        _cpc_streams(dev, cpc, fields, n, S, perm, seg_bits, minima, meta, meta_t)
-    variant = None
-    if sorted_mode:
-        variant = RIndexVariant.COORDINATE if mode.stores_minima else settings.rindex_variant
-    archive = Archive(
-        mode=mode, n=n, interval_count=ic, segment_size=S,
-        ignored_groups=settings.ignored_groups,
-        rindex_variant=variant,
-        bounds=tuple(meta.f[i].bound for i in range(6)),
-        constant_mask=meta.mask,
-        constants=tuple(meta.f[i].constant for i in range(6)),
-        seg_bits=seg_bits[:nseg] if sorted_mode else None,
-        device=dev, version=2, device_output=snapshot.on_device,
-        seg_minima=minima[:3 * nseg].view(nseg, 3) if cpc else None)
-    tile = (max(1, 16384 // S) * S) if S < 16384 else S
-    return CompressResult(archive, perm=perm[:n] if perm is not None else None, tile=tile)
+            a.phase = 0
+        N.check(self.L.nbzg_compress(ctypes.byref(a), N.stream_handle()), "compress")
+        meta = self._meta()
+        _raise_status(meta.status, "compress")
+        mode, settings, S, nseg, cpc = self.mode, self.settings, self.S, self.nseg, self.cpc
+        offsets, lengths, kinds = [], [], []
+        for fi in range(6):
+            fm = meta.f[fi]
+            if n == 0 or fm.is_const:
+                offsets.append(None)
+                lengths.append(0)
+            else:
+                offsets.append(int(fm.payload_off))
+                lengths.append(int(fm.payload_len))
+            kinds.append(int(StreamKind.SZ_DQ))
+        dev = _Device(self.arena[:max(int(meta.arena_used), 1)], offsets, lengths, kinds,
+                      keep=(self.meta_t,))
+        if cpc:
+            _cpc_streams(dev, cpc, self.fields, n, S, self.perm, self.seg_bits, self.minima,
+                         meta, self.meta_t)
+        variant = None
+        if self.sorted_mode:
+            variant = RIndexVariant.COORDINATE if mode.stores_minima else settings.rindex_variant
+        archive = Archive(
+            mode=mode, n=n, interval_count=self.ic, segment_size=S,
+            ignored_groups=settings.ignored_groups,
+            rindex_variant=variant,
+            bounds=tuple(meta.f[i].bound for i in range(6)),
+            constant_mask=meta.mask,
+            constants=tuple(meta.f[i].constant for i in range(6)),
+            seg_bits=self.seg_bits[:nseg] if self.sorted_mode else None,
+            device=dev, version=2, device_output=self.on_device,
+            seg_minima=self.minima[:3 * nseg].view(nseg, 3) if cpc else None)
+        tile = (max(1, 16384 // S) * S) if S < 16384 else S
+        perm = self.perm[:n] if self.perm is not None else None
+        self.ws = None  # the workspace goes back to the caching allocator
+        return CompressResult(archive, perm=perm, tile=tile)
 
 
 def _cpc_streams(dev: _Device, cpc: int, fields, n: int, S: int, perm, seg_bits, minima, meta,
@@ -474,7 +558,7 @@ def _cpc_streams(dev: _Device, cpc: int, fields, n: int, S: int, perm, seg_bits,
     import torch
     L = N.lib()
     nseg = (n + S - 1) // S
-    ws = N.POOL.get("cpc_ws", L.nbzg_cpc_workspace_size(n, S))
+    ws = N.workspace(L.nbzg_cpc_workspace_size(n, S))
     cm_t = torch.zeros(ctypes.sizeof(N.CpcMeta), dtype=torch.uint8, device="cuda")
     ca = N.CpcArgs()
     for i in range(6):
@@ -554,44 +638,56 @@ def _cpc_decode(archive: "Archive", views, status) -> None:
                 if d.offsets[fi] is None or d.kinds[fi] != int(StreamKind.VLC_FIELD):
                     raise DecodeError(f"missing stream for field {FIELD_NAMES[fi]}")
                 jobs.append((fi, 1, [fi]))
+    # everything a job needs is validated before the first launch, so an
+    # error never leaves side-stream work running on freed buffers
+    totals = [_cpc_total_bits(archive, slot, nseg) for slot, _k, _f in jobs]
+    for slot, _k, fis in jobs:
+        for fi in fis:
+            if not archive.is_constant(fi) and not (archive.bounds[fi] > 0):
+                raise DecodeError(f"field {FIELD_NAMES[fi]}: invalid bound")
     # one side stream per job: a decode launch holds one thread per segment,
     # so independent streams overlap (e.g. the coordinate and three velocity
-    # streams of cpc2000)
-    totals = [_cpc_total_bits(archive, slot, nseg) for slot, _k, _f in jobs]  # before any launch
+    # streams of cpc2000).  Workspaces are per call (reentrant across host
+    # threads); the caching allocator keeps them stream-ordered.
     main = torch.cuda.current_stream()
     ready = torch.cuda.Event()
     ready.record(main)
     side = N.side_streams(len(jobs))
-    for j, (slot, kind, fis) in enumerate(jobs):
-        sj = side[j]
-        sj.wait_event(ready)
-        a = N.CpcDecodeArgs()
-        a.payload = N.ptr(d.buf(slot)) + d.offsets[slot]
-        a.payload_len = d.lengths[slot]
-        a.kind = kind
-        a.indexed = 1 if archive.version >= 2 else 0
-        a.n = n
-        a.segment_size = S
-        a.total_bits = totals[j]
-        a.seg_bits = N.ptr(sb)
-        a.seg_minima = N.ptr(mn)
-        for c, fi in enumerate(fis):
-            a.bound[c] = archive.bounds[fi]
-            if not archive.is_constant(fi):
-                if not (archive.bounds[fi] > 0):
-                    raise DecodeError(f"field {FIELD_NAMES[fi]}: invalid bound")
-                a.out[c] = N.ptr(views[fi])
-        wsj = N.POOL.get(f"cpc_dec_ws{j}", L.nbzg_cpc_decode_workspace_size(n, S))
-        a.workspace = N.ptr(wsj)
-        a.workspace_bytes = wsj.numel()
-        a.status = N.ptr(status)
-        rc = L.nbzg_cpc_decode(ctypes.byref(a), ctypes.c_void_p(sj.cuda_stream))
-        if rc in (N.NBZG_BAD_ARG, N.NBZG_UNSUPPORTED, N.NBZG_TRUNCATED):
-            raise DecodeError(f"decompress: {N.STATUS_NAMES.get(rc, rc)}")
-        N.check(rc, "decompress")
-        done = torch.cuda.Event()
-        done.record(sj)
-        main.wait_event(done)
+    launched = []
+    try:
+        for j, (slot, kind, fis) in enumerate(jobs):
+            sj = side[j]
+            sj.wait_event(ready)
+            a = N.CpcDecodeArgs()
+            a.payload = N.ptr(d.buf(slot)) + d.offsets[slot]
+            a.payload_len = d.lengths[slot]
+            a.kind = kind
+            a.indexed = 1 if archive.version >= 2 else 0
+            a.n = n
+            a.segment_size = S
+            a.total_bits = totals[j]
+            a.seg_bits = N.ptr(sb)
+            a.seg_minima = N.ptr(mn)
+            for c, fi in enumerate(fis):
+                a.bound[c] = archive.bounds[fi]
+                if not archive.is_constant(fi):
+                    a.out[c] = N.ptr(views[fi])
+            with torch.cuda.stream(sj):
+                wsj = N.workspace(L.nbzg_cpc_decode_workspace_size(n, S))
+            a.workspace = N.ptr(wsj)
+            a.workspace_bytes = wsj.numel()
+            a.status = N.ptr(status)
+            rc = L.nbzg_cpc_decode(ctypes.byref(a), ctypes.c_void_p(sj.cuda_stream))
+            launched.append((sj, wsj))
+            if rc in (N.NBZG_BAD_ARG, N.NBZG_UNSUPPORTED, N.NBZG_TRUNCATED):
+                raise DecodeError(f"decompress: {N.STATUS_NAMES.get(rc, rc)}")
+            N.check(rc, "decompress")
+    finally:
+        for sj, wsj in launched:  # the main stream waits for every launched job
+            done = torch.cuda.Event()
+            done.record(sj)
+            main.wait_event(done)
+            wsj.record_stream(main)
 
 
 _KIND_CODE = {StreamKind.SZ_DQ: 3, StreamKind.SZ_FIELD: 0}
@@ -656,7 +752,7 @@ def decompress(archive: Archive, device: Optional[bool] = None) -> ParticleSnaps
         nf += 1
     if nf:
         ws_bytes = L.nbzg_decompress_workspace_size(n, archive.interval_count, nf)
-        ws = N.POOL.get("decompress_ws", ws_bytes)
+        ws = N.workspace(ws_bytes)
         a.nfields = nf
         a.n = n
         a.interval_count = archive.interval_count

@@ -69,10 +69,23 @@ def global_bounds(mm: np.ndarray, specs: Sequence[ErrorBoundSpec]) -> List[Error
     return out
 
 
+def _collective_device(group=None, device=None):
+    """Where the collectives' tensors live: the caller's choice, else the
+    current CUDA device under NCCL (which rejects CPU tensors), else CPU."""
+    import torch
+    import torch.distributed as dist
+    if device is not None:
+        return device
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return None
+
+
 def _all_gather_f64(vals: np.ndarray, group=None, device=None) -> np.ndarray:
     import torch
     import torch.distributed as dist
     t = torch.as_tensor(np.asarray(vals, np.float64).ravel(), dtype=torch.float64)
+    device = _collective_device(group, device)
     if device is not None:
         t = t.to(device)
     world = dist.get_world_size(group)
@@ -95,7 +108,8 @@ def exclusive_offsets(sizes: Sequence[int]) -> np.ndarray:
 def local_minmax(fields) -> np.ndarray:
     """Exact f32 (min, max) per field of this shard, (6, 2) f64; an empty
     shard gives (+inf, -inf).  CUDA fields: one fused pass (nbzg_minmax6,
-    the K1 kernel); host arrays: numpy."""
+    the K1 kernel; fields re-allocated 16-byte aligned if a view is not);
+    host arrays: numpy."""
     import torch
     out = np.empty((6, 2), np.float64)
     fields = list(fields)
@@ -108,6 +122,7 @@ def local_minmax(fields) -> np.ndarray:
 
         from . import _native as N
         ts = [f.contiguous() for f in fields]
+        ts = [t if t.data_ptr() % 16 == 0 else t.clone() for t in ts]
         arr = (ctypes.c_void_p * 6)(*[t.data_ptr() for t in ts])
         mm = torch.empty(12, dtype=torch.float32, device=ts[0].device)
         N.check(N.lib().nbzg_minmax6(arr, n, N.ptr(mm), N.stream_handle()), "minmax6")
@@ -130,23 +145,30 @@ class ShardResult:
 
 def compress_shard(snapshot, mode, bounds, settings=None, group=None,
                    device=None) -> ShardResult:
-    """Compress this rank's shard with globally resolved bounds (collective
-    1), then all-gather the archive sizes (collective 2)."""
+    """Compress this rank's shard with bounds resolved on the GLOBAL range
+    (collective 1), then all-gather the archive sizes (collective 2).
+
+    The compress runs in two C-ABI phases on one workspace: K1 gives the
+    shard's exact min/max, the ranks all-gather them, and the rest of the
+    compress resumes with the global min/max -- K1 runs once per rank."""
     import torch.distributed as dist
 
-    from .pipeline import DEFAULT_SETTINGS, _specs, compress
+    from .pipeline import DEFAULT_SETTINGS, _CompressCall, _specs
 
     specs = _specs(bounds)
+    settings = settings or DEFAULT_SETTINGS
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
+    call = _CompressCall(snapshot, mode, bounds, settings)
     if world == 1:  # the shard is the snapshot: resolve locally, as compress does
-        res = compress(snapshot, mode, bounds, settings or DEFAULT_SETTINGS)
+        res = call.finish()
         size = res.archive.total_bytes()
-        return ShardResult(res, 0, 1, specs, 0, int(size))
-    mm = local_minmax(snapshot.fields())
-    resolved = global_bounds(merge_minmax(allgather_minmax(mm, group, device)), specs)
-    res = compress(snapshot, mode, dict(zip(FIELD_NAMES, resolved)),
-                   settings or DEFAULT_SETTINGS)
+        resolved = [ErrorBoundSpec.absolute(b) if b > 0 else s
+                    for b, s in zip(res.archive.bounds, specs)]
+        return ShardResult(res, 0, 1, resolved, 0, int(size))
+    mm = merge_minmax(allgather_minmax(call.local_minmax(), group, device))
+    resolved = global_bounds(mm, specs)
+    res = call.finish(mm)
     size = res.archive.total_bytes()
     sizes = _all_gather_f64(np.array([float(size)]), group, device).ravel().astype(np.int64)
     offs = exclusive_offsets(sizes)
