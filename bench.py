@@ -6,9 +6,12 @@ Metric: compress/decompress GB/s per 6-field fp32 snapshot at eb_rel = 1e-4
 pkg/src/nbz/metrics.py:100-110), plus ratio and %HBM roofline.
 
 One STEP = compress + decompress of the resident snapshot through the public
-API (nbz.compress -> nbz.decompress, device-resident input and output).
-``value`` is the round-trip rate 24*n_total / step time; the compress and
-decompress rates are reported beside it.
+API (nbz.compress -> payload CRC-64s -> nbz.decompress, device-resident input
+and output).  The compress leg includes the archive's payload CRC-64s, as the
+reference's compress rate includes its CRC serialisation
+(pkg/src/nbz/metrics.py:178-180).  ``value`` is the round-trip rate
+24*n_total / step time; the compress and decompress rates are reported
+beside it.
 
 Workload at N=1: BASELINE config 2, the 640^3 HACC-like snapshot
 (262,144,000 particles, 6.29 GB), mode sz-lv-prx (R-index on).  At N>1 each
@@ -18,6 +21,10 @@ NCCL all-gather of per-shard min/max and the per-shard archive sizes are
 all-gathered after compress -- the only collectives.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+With --gpus N > 1 and no torchrun environment, bench.py launches its N ranks
+itself (torch.distributed.run, one process per GPU, rendezvous on
+127.0.0.1) and checks that the world size is N.
 """
 
 from __future__ import annotations
@@ -169,9 +176,57 @@ def cpu_sample(spec, m):
     return datagen.generate(spec, 0, m)
 
 
+def reference_package_1core(m: int = 1 << 22, mode: str = "sz-lv-prx", eb: float = 1e-4,
+                            timeout: int = 240):
+    """The reference package itself (baseline/_ref, pure Python + numba, one
+    core: its kernels hold the GIL and have no prange) on a bounded C2
+    sample: compress + serialise, best of 3 after a 4096-particle warm-up,
+    then decompress of the in-memory archive (SURVEY.md 8d CPU baseline (i);
+    test_acceptance.py:375-402, metrics.py:173-188).  Run in a subprocess so
+    numba's JIT and threads stay out of the bench process."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "nbz")):
+        return {"value": None, "error": "baseline/_ref not installed"}
+    code = f"""
+import json, os, sys, time
+sys.path.insert(0, {ROOT!r})
+import numpy as np
+from nbz import ErrorBoundSpec, Mode, ParticleSnapshot, compress, decompress
+from paper_1711_03888_b200 import datagen
+f = datagen.generate(datagen.CONFIGS["C2"], 0, {m})
+snap = ParticleSnapshot(*f)
+spec = ErrorBoundSpec.relative({eb})
+mode = Mode({mode!r})
+small = ParticleSnapshot(*(x[:4096] for x in f))
+decompress(compress(small, mode, spec).archive)
+tc = []
+for _ in range(3):
+    t0 = time.perf_counter(); r = compress(snap, mode, spec); r.archive.serialized()
+    tc.append(time.perf_counter() - t0)
+t0 = time.perf_counter(); decompress(r.archive); td = time.perf_counter() - t0
+print(json.dumps({{"tc": min(tc), "td": td}}))
+"""
+    env = dict(os.environ, PYTHONPATH=ref, NUMBA_CACHE_DIR="/tmp/nbz_numba_cache",
+               OMP_NUM_THREADS="1", NUMBA_NUM_THREADS="1")
+    try:
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                             timeout=timeout, env=env)
+        r = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as exc:  # reported, never fatal
+        return {"value": None, "error": str(exc)[:200]}
+    b = 24.0 * m
+    return {"value": b / (r["tc"] + r["td"]) / 1e9, "unit": "GB/s", "cores": 1,
+            "kind": "reference", "compress_gbps": b / r["tc"] / 1e9,
+            "decompress_gbps": b / r["td"] / 1e9, "nproc": os.cpu_count(),
+            "sample": f"first {m} particles of C2, {mode} eb_rel {eb}: the reference package "
+                      f"(baseline/_ref nbz, numba, 1 core) compress+serialized() best of 3, then "
+                      f"decompress"}
+
+
 def cpu_baseline(spec, mode, eb, budget_s=12.0):
     """Reference algorithm (oracle C port, exact chain = the reference's
-    SZ_FIELD path) on the host's cores over a bounded prefix sample."""
+    SZ_FIELD path) on the host's cores over a bounded prefix sample, plus the
+    reference package itself on one core."""
     import oracle
     oracle.build()
     threads = os.cpu_count() or 1
@@ -190,44 +245,43 @@ def cpu_baseline(spec, mode, eb, budget_s=12.0):
             "sample": f"first {m} particles of the {spec.lattice[0]}x{spec.lattice[1]}x"
                       f"{spec.lattice[2]} HACC-like workload, {mode} eb_rel {eb}, compress+"
                       f"decompress round trip, {threads} threads x contiguous shards "
-                      f"(oracle/nbz_oracle.c, the reference's exact SZ-LV chain), best of 2"}
+                      f"(oracle/nbz_oracle.c, the reference's algorithm), best of 2",
+            "reference_1core": reference_package_1core(mode=mode, eb=eb)}
 
 
 def run_reference(args):
     """--impl reference: the reference's algorithm on the host CPU cores
-    (oracle/ C port; the reference itself is a Python+numba package that
-    cannot travel to the GPU box)."""
+    (the oracle C port, one contiguous 16384-aligned shard per core -- the
+    paper's per-process model).  At N=1 every step is the WHOLE config-2
+    snapshot (the B200 arm's workload); at N>1 (rank 0 alone) a step is one
+    640^3 slab, a bounded sample of the N-slab workload."""
     import oracle
     from paper_1711_03888_b200 import datagen
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     oracle.build()
     spec = datagen.HaccSpec((SIDE * max(1, args.gpus), SIDE, SIDE), 2.5)
     threads = os.cpu_count() or 1
-    m = 1 << 22
+    m = SIDE ** 3 if args.n is None else args.n
     fields = cpu_sample(spec, m)
-    t = cpu_round_trip(fields, args.mode, args.eb, threads)
-    # size each step to ~3 s of CPU work so K+W steps finish in minutes
-    m2 = int(min(max(m, m * 3.0 / max(t, 1e-3)), 1 << 26))
-    m2 = (m2 // 16384) * 16384
-    if m2 > m:
-        fields = cpu_sample(spec, m2)
-        m = m2
     for _ in range(args.warmup):
         cpu_round_trip(fields, args.mode, args.eb, threads)
     ts = [cpu_round_trip(fields, args.mode, args.eb, threads) for _ in range(args.steps)]
     tot = sum(ts)
     value = 24.0 * m * args.steps / tot / 1e9
-    sample = (f"first {m} particles of the C2 HACC-like workload per step, {args.mode} eb_rel "
-              f"{args.eb}, compress+decompress, {threads} threads")
+    whole = args.gpus == 1 and m == SIDE ** 3
+    sample = (f"{'the whole' if whole else 'a ' + str(m) + '-particle'} C2 HACC-like "
+              f"{SIDE}^3 snapshot per step, {args.mode} eb_rel {args.eb}, compress+decompress, "
+              f"{threads} threads x contiguous shards (oracle/nbz_oracle.c)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded HACC-like generator)",
-            "config": {"workload": "C2 HACC-like 640^3 per GPU (bounded CPU sample per step)",
-                       "mode": args.mode, "eb_rel": args.eb},
+            "config": {"workload": f"C2: HACC-like {SIDE}^3 = {SIDE ** 3} particles per GPU "
+                                   f"(6.29 GB), box 1600, {args.mode}"
+                                   + ("" if whole else " (bounded CPU sample per step)"),
+                       "n_per_gpu": SIDE ** 3, "mode": args.mode, "eb_rel": args.eb},
             "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
                              "sample": sample},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
@@ -253,19 +307,22 @@ def run_b200(args):
     import paper_1711_03888_b200 as nbz
     from paper_1711_03888_b200 import _native as N
     from paper_1711_03888_b200 import datagen, shard
+    from paper_1711_03888_b200 import io as nio
 
     rank, world, local = dist_init(args.gpus)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus}: the process group has {world} ranks")
     N.lib()
     n = SIDE ** 3 if args.n is None else args.n
     spec = datagen.HaccSpec((SIDE * world, SIDE, SIDE), 2.5)
     p0, p1 = rank * n, (rank + 1) * n
-    # pinned host snapshot (the e2e leg reads it from here)
-    host_t = [torch.empty(n, dtype=torch.float32, pin_memory=True) for _ in range(6)]
-    host = [t.numpy() for t in host_t]
+    # pageable host snapshot, as an ordinary caller holds it (the e2e leg
+    # reads it from here; the device copy below is the in-situ input)
+    host = [np.empty(n, np.float32) for _ in range(6)]
     tg = time.perf_counter()
     datagen.generate(spec, p0, p1, out=host)
     gen_s = time.perf_counter() - tg
-    dev = [t.cuda(non_blocking=True) for t in host_t]
+    dev = [torch.from_numpy(h).cuda() for h in host]
     torch.cuda.synchronize()
     snap = nbz.ParticleSnapshot(*dev)
 
@@ -277,8 +334,11 @@ def run_b200(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e2 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        # global bounds (collective 1), shard compress, archive sizes (collective 2)
-        sr = shard.compress_shard(snap, args.mode, bounds, device="cuda")
+        # global bounds (collective 1), shard compress, archive sizes (collective 2),
+        # then the payload CRC-64s (on device; the reference's compress rate
+        # includes its CRC serialisation, metrics.py:178-180)
+        sr = shard.compress_shard(snap, args.mode, bounds)
+        nio._payload_crcs(sr.result.archive)
         e1.record()
         out = nbz.decompress(sr.result.archive, device=True)
         e2.record()
@@ -340,24 +400,9 @@ def run_b200(args):
                  "unit": "GB/s", "bytes": "24n + S per direction (SURVEY.md 8d)",
                  "peak": hbm}
 
-    # ---- compress as the reference times it (metrics.py:178-180): including
-    # the payload CRC-64s of the serialised archive (on device), no D2H
-    from paper_1711_03888_b200 import io as _nio
-    tcc = []
-    for _ in range(3):
-        torch.cuda.synchronize()
-        w0 = time.perf_counter()
-        r_ = shard.compress_shard(snap, args.mode, bounds, device="cuda").result
-        _nio._payload_crcs(r_.archive)
-        torch.cuda.synchronize()
-        tcc.append(1e3 * (time.perf_counter() - w0))
-    del r_
-    tc_crc = reduce_max(min(tcc), world)
-
     # ---- e2e: host buffers through the public API, H2D/D2H inside the region
     e2e = None
     if args.e2e_steps > 0:
-        from paper_1711_03888_b200 import io as nio
         hsnap = nbz.ParticleSnapshot(*host)
         # the globally resolved bounds of the device step (identical at N=1)
         e2e_bounds = dict(zip(nbz.FIELD_NAMES, shard_bounds[0]))
@@ -402,8 +447,9 @@ def run_b200(args):
                "steps": args.e2e_steps,
                "step_ms": [round(1e3 * (b - a), 1) for a, b in zip(marks, marks[1:])],
                "stages_ms": {k: round(sum(v) / len(v), 1) for k, v in stage_ms.items() if v},
-               "path": "numpy (pinned) -> compress -> serialized() -> deserialize_archive -> "
-                       "decompress -> numpy (pooled page-locked output); wall clock, "
+               "path": "numpy (pageable, H2D staged through pinned chunks) -> compress -> "
+                       "serialized() -> deserialize_archive -> decompress -> numpy (the "
+                       "library's page-locked output pool after the first call); wall clock, "
                        "max over ranks"}
 
     cpu = None
@@ -430,16 +476,13 @@ def run_b200(args):
             "config": {"workload": f"C2: HACC-like {SIDE}^3 = {n} particles per GPU "
                                    f"(6.29 GB), box 1600, {args.mode}",
                        "n_per_gpu": n, "mode": args.mode, "eb_rel": args.eb,
-                       "step": "compress + decompress, device-resident in/out",
+                       "step": "compress (incl. payload CRC-64s) + decompress, device-resident "
+                               "in/out",
                        "l2": "inputs (6.3 GB/GPU) exceed the 126 MB L2; no flush needed",
                        "parallelism": f"{world} contiguous shard(s), weak scaling"},
             "compress_gbps": 24.0 * n_total / (tc * 1e-3) / 1e9,
             "decompress_gbps": 24.0 * n_total / (td * 1e-3) / 1e9,
             "compress_ms": tc, "decompress_ms": td,
-            "compress_with_crc": {"ms": tc_crc, "gbps": 24.0 * n_total / (tc_crc * 1e-3) / 1e9,
-                                  "note": "compress + payload CRC-64s on device (the reference's "
-                                          "timed compress includes CRC serialisation); wall "
-                                          "clock, best of 3"},
             "ratio": 24.0 * n_total / S_total,
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": hbm,
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
@@ -459,6 +502,24 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def launch_ranks(n: int) -> int:
+    """Re-run this command as n ranks (one process per GPU) under
+    torch.distributed.run on 127.0.0.1; returns its exit code."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # NCCL init lines on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench.py: launching {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -474,6 +535,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args.gpus))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -296,6 +296,12 @@ int nbzg_huff_encode(const uint16_t *syms, int64_t n, const uint64_t *lut, uint8
 int nbzg_crc64(const uint8_t *data, int64_t n, uint64_t *crc_dev, void *workspace,
                size_t workspace_bytes, void *stream);
 size_t nbzg_crc64_workspace_size(int64_t n);
+/* CRC-64/XZ of `count` device buffers (an archive's payloads: io.py:123-124
+ * computes one per stream) in one grid; h_data / h_n are host arrays of the
+ * device pointers and lengths, crc_dev[count] (device) receives the CRCs. */
+int nbzg_crc64_many(const uint8_t *const *h_data, const int64_t *h_n, int32_t count,
+                    uint64_t *crc_dev, void *workspace, size_t workspace_bytes, void *stream);
+size_t nbzg_crc64_many_workspace_size(const int64_t *h_n, int32_t count);
 
 /* library / device info and diagnostics */
 const char *nbzg_version(void);

@@ -666,11 +666,33 @@ def decompress_cpc(wire: bytes) -> List[np.ndarray]:
 def compress_shards(fields, mode: str, eb_rel: float, nshards: int, nthreads: int,
                     interval_count: int = 65536, segment_size: int = 16384,
                     ignored_groups: int = 6, fmt: int = 1, decompress_too: bool = False) -> int:
-    """CPU baseline: global bounds, then one segment-aligned shard per thread."""
+    """CPU baseline: global bounds, then one segment-aligned shard per thread.
+    SZ modes run in one C call (OpenMP over shards); the CPC modes run the
+    CPC restatement per shard on a thread pool (the C stages release the
+    GIL).  Returns the total payload / wire bytes."""
     f32 = [_c(a, np.float32) for a in fields]
     n = int(f32[0].size)
     resolved, _c2, mask = resolve_field_bounds(f32, ["rel"] * 6, [eb_rel] * 6)
     bounds = np.array([b if b is not None else 0.0 for b in resolved], np.float64)
+    if mode in ("sz-cpc2000", "cpc2000"):
+        import concurrent.futures as cf
+        per = -(-n // max(nshards, 1))
+        per = -(-per // segment_size) * segment_size
+        kinds = ["abs" if b is not None else "rel" for b in resolved]
+        vals = [b if b is not None else eb_rel for b in resolved]
+
+        def one(s):
+            lo, hi = s * per, min(n, (s + 1) * per)
+            if hi <= lo:
+                return 0
+            r = compress_cpc([a[lo:hi] for a in f32], mode, kinds, vals,
+                             interval_count=interval_count, segment_size=segment_size, fmt=fmt)
+            if decompress_too:
+                decompress_cpc(r["wire"])
+            return len(r["wire"])
+
+        with cf.ThreadPoolExecutor(max_workers=max(1, nthreads)) as ex:
+            return int(sum(ex.map(one, range(max(nshards, 1)))))
     ptrs = (ctypes.c_void_p * 6)(*[a.ctypes.data for a in f32])
     bad = np.zeros(1, np.int64)
     tot = lib().orc_compress_shards(ptrs, n, int(mode == "sz-lv-prx"), _p(bounds), mask,

@@ -16,7 +16,9 @@ import threading
 from typing import Dict, Tuple
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnbzg.so")
+# NBZG_LIB selects another in-tree build of the same library (kernel
+# experiments: scripts/dec_variants.py); it is never a different implementation
+LIB_PATH = os.environ.get("NBZG_LIB") or os.path.join(_HERE, "libnbzg.so")
 
 NBZG_OK = 0
 NBZG_BOUND_TOO_SMALL = 1
@@ -40,7 +42,7 @@ EXPORTED = (
     "nbzg_version", "nbzg_device_sm_count", "nbzg_launch_count", "nbzg_trace_enable",
     "nbzg_trace_read", "nbzg_cpc_workspace_size", "nbzg_cpc_plan", "nbzg_cpc_pack",
     "nbzg_cpc_decode", "nbzg_cpc_decode_workspace_size", "nbzg_huff_decode",
-    "nbzg_deinterleave3",
+    "nbzg_deinterleave3", "nbzg_crc64_many", "nbzg_crc64_many_workspace_size",
 )
 
 
@@ -136,6 +138,8 @@ _SIGS = {
     "nbzg_huff_decode": (ctypes.c_int, [c_p, c_u64, c_i64, c_i32, c_i32, c_p, c_p, c_p, c_p, c_p,
                                         c_p, c_p]),
     "nbzg_deinterleave3": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_p]),
+    "nbzg_crc64_many": (ctypes.c_int, [c_p, c_p, c_i32, c_p, c_p, c_sz, c_p]),
+    "nbzg_crc64_many_workspace_size": (c_sz, [c_p, c_i32]),
 }
 
 _lib = None

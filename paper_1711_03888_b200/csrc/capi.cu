@@ -32,6 +32,9 @@ int launch_huff_encode_raw(const uint16_t* syms, int64_t n, const uint64_t* lut,
                            uint32_t* chunk_bits, uint64_t* lb, uint32_t* tickets,
                            cudaStream_t st);
 size_t crc_ws(int64_t n);
+size_t crc_ws_many(const int64_t* n, int count);
+int launch_crc64_many(const uint8_t* const* data, const int64_t* n, int count, uint64_t* crc_out,
+                      void* ws, size_t ws_bytes, cudaStream_t st);
 int launch_crc64(const uint8_t* data, int64_t n, uint64_t* crc_out, void* ws, size_t ws_bytes,
                  cudaStream_t st);
 
@@ -270,6 +273,7 @@ size_t nbzg_compress_arena_bound(int64_t n, int64_t interval_count) {
 }
 
 int nbzg_compress(const nbzg_compress_args* a, void* stream) {
+  NvtxScope range_call("nbzg_compress");
   if (!a) return NBZG_BAD_ARG;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (a->n < 0 || a->n >= (int64_t(1) << 32) - 1) return NBZG_UNSUPPORTED;
@@ -320,25 +324,30 @@ int nbzg_compress(const nbzg_compress_args* a, void* stream) {
   // sorted mode with 3-field keys: K1 walks whole segments and also leaves
   // each segment's key-field min/max, so K2 reads the coordinates once
   const bool segmm = p.sorted && p.variant != 2 && p.n > 0 && p.S % 4 == 0;
-  if (a->phase == 2) {
-    // K1 ran in phase 1 (its segment min/max are still in the workspace);
-    // the global min/max replace the shard's
-    for (int i = 0; i < 12; i++)
-      if (a->h_minmax[i] != a->h_minmax[i]) return NBZG_BAD_ARG;  // NaN
-    if ((rc = launch_minmax_set(a->h_minmax, p.minmax, st))) return rc;
-  } else {
-    if ((rc = segmm ? launch_minmax_seg(p, st) : launch_minmax6(p.f, p.n, p.minmax, st)))
-      return rc;
+  {
+    NvtxScope range("K1 minmax + resolve");
+    if (a->phase == 2) {
+      // K1 ran in phase 1 (its segment min/max are still in the workspace);
+      // the global min/max replace the shard's
+      for (int i = 0; i < 12; i++)
+        if (a->h_minmax[i] != a->h_minmax[i]) return NBZG_BAD_ARG;  // NaN
+      if ((rc = launch_minmax_set(a->h_minmax, p.minmax, st))) return rc;
+    } else {
+      if ((rc = segmm ? launch_minmax_seg(p, st) : launch_minmax6(p.f, p.n, p.minmax, st)))
+        return rc;
+    }
+    if (!segmm) p.seg_mm = nullptr;
+    trace_mark("minmax6", st);
+    if ((rc = launch_resolve(p, st))) return rc;
   }
-  if (!segmm) p.seg_mm = nullptr;
-  trace_mark("minmax6", st);
-  if ((rc = launch_resolve(p, st))) return rc;
   trace_mark("resolve", st);
   if (p.n == 0 || a->phase == 1) return cuda_status();
   if (p.sorted) {
+    NvtxScope r("K2 rindex_sort");
     if ((rc = launch_rindex_sort(p, st))) return rc;
     trace_mark("rindex_sort", st);
   }
+  NvtxScope range_sz("K3-K5 quantize / codebook / encode");
   if (p.sz_skip && (rc = launch_sz_skip(p, st))) return rc;
   if (p.predictor == 0 && encode_uses_tpc(p)) return sz_stages_split(p, st);
   if ((rc = launch_quantize(p, st))) return rc;
@@ -357,6 +366,7 @@ size_t nbzg_decompress_workspace_size(int64_t n, int64_t interval_count, int32_t
 }
 
 int nbzg_decompress(const nbzg_decompress_args* a, void* stream) {
+  NvtxScope range_call("nbzg_decompress");
   if (!a || a->nfields < 0 || a->nfields > 6 || a->n < 0) return NBZG_BAD_ARG;
   if (a->nfields == 0 || a->n == 0) return NBZG_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -494,6 +504,22 @@ int nbzg_deinterleave3(const uint64_t* keys, int64_t n, int64_t* x, int64_t* y, 
 }
 
 size_t nbzg_crc64_workspace_size(int64_t n) { return crc_ws(n); }
+
+size_t nbzg_crc64_many_workspace_size(const int64_t* h_n, int32_t count) {
+  size_t best = 0;
+  for (int c0 = 0; c0 < count; c0 += 8) {
+    const size_t s = crc_ws_many(h_n + c0, count - c0 < 8 ? count - c0 : 8);
+    best = s > best ? s : best;
+  }
+  return best ? best : 64;
+}
+
+int nbzg_crc64_many(const uint8_t* const* h_data, const int64_t* h_n, int32_t count,
+                    uint64_t* crc_dev, void* workspace, size_t workspace_bytes, void* stream) {
+  if (count < 0 || (count > 0 && (!h_data || !h_n))) return NBZG_BAD_ARG;
+  return launch_crc64_many(h_data, h_n, count, crc_dev, workspace, workspace_bytes,
+                           reinterpret_cast<cudaStream_t>(stream));
+}
 
 int nbzg_crc64(const uint8_t* data, int64_t n, uint64_t* crc_dev, void* workspace,
                size_t workspace_bytes, void* stream) {

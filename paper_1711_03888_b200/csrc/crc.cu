@@ -93,15 +93,31 @@ int upload_tables() {
 }
 }  // namespace
 
-// crc0 of each 512 KiB span of the front-padded stream (pad zero bytes,
+// Up to kCrcMax buffers per launch (an archive's payloads): one grid over
+// all their spans, so small payloads still fill the GPU.
+constexpr int kCrcMax = 8;
+struct CrcJobs {
+  const uint8_t* data[kCrcMax];
+  int64_t n[kCrcMax];
+  int64_t pad[kCrcMax];
+  int64_t span0[kCrcMax + 1];  // first span (CTA) of each buffer; span0[count] = total
+  uint64_t* out[kCrcMax];
+  int run_log[kCrcMax];
+  int count;
+};
+
+// crc0 of each 512 KiB span of each front-padded stream (pad zero bytes,
 // then data[0, n)).
-__global__ void __launch_bounds__(kCrcThreads) crc_span_kernel(const uint8_t* data, int64_t n,
-                                                              int64_t pad, uint64_t* span_out) {
+__global__ void __launch_bounds__(kCrcThreads) crc_span_kernel(CrcJobs J, uint64_t* span_out) {
   __shared__ uint64_t T[16 * 256];
   __shared__ uint64_t wsum[kCrcThreads / 32];
   for (int i = threadIdx.x; i < 16 * 256; i += kCrcThreads) T[i] = g_crc_slice[i];
+  int b = 0;
+  while (b + 1 < J.count && (int64_t)blockIdx.x >= J.span0[b + 1]) b++;
+  const uint8_t* data = J.data[b];
+  const int64_t n = J.n[b], pad = J.pad[b];
   __syncthreads();
-  const int64_t g = (int64_t)blockIdx.x * kCrcThreads + threadIdx.x;
+  const int64_t g = ((int64_t)blockIdx.x - J.span0[b]) * kCrcThreads + threadIdx.x;
   int64_t s = (g << kCrcBlockLog) - pad, e = s + (1 << kCrcBlockLog);
   if (s < 0) s = 0;  // leading virtual zeros leave crc0 at 0
   if (e > n) e = n;
@@ -159,10 +175,15 @@ __global__ void __launch_bounds__(kCrcThreads) crc_span_kernel(const uint8_t* da
 }
 
 // fold C span values (front-padded with zero spans to kFoldThreads runs of
-// 2^run_log) and finish
-__global__ void __launch_bounds__(kFoldThreads) crc_fold_kernel(const uint64_t* span, int64_t C,
-                                                               int run_log, int64_t n,
-                                                               uint64_t* crc_out) {
+// 2^run_log) and finish; one CTA per buffer
+__global__ void __launch_bounds__(kFoldThreads) crc_fold_kernel(CrcJobs J,
+                                                               const uint64_t* span_all) {
+  const int b = blockIdx.x;
+  const uint64_t* span = span_all + J.span0[b];
+  const int64_t C = J.span0[b + 1] - J.span0[b];
+  const int run_log = J.run_log[b];
+  const int64_t n = J.n[b];
+  uint64_t* crc_out = J.out[b];
   __shared__ uint64_t v[kFoldThreads];
   const int t = threadIdx.x;
   const int64_t run = int64_t(1) << run_log;
@@ -199,23 +220,52 @@ static int64_t crc_spans(int64_t n) {
 
 size_t crc_ws(int64_t n) { return sizeof(uint64_t) * (size_t)(crc_spans(n) + 8); }
 
-int launch_crc64(const uint8_t* data, int64_t n, uint64_t* crc_out, void* ws, size_t ws_bytes,
-                 cudaStream_t st) {
-  if (n < 0 || (n >> kCrcLevels)) return NBZG_BAD_ARG;
-  if (ws_bytes < crc_ws(n)) return NBZG_BAD_ARG;
+size_t crc_ws_many(const int64_t* n, int count) {
+  size_t s = 8;
+  for (int i = 0; i < count; i++) s += (size_t)crc_spans(n[i]);
+  return sizeof(uint64_t) * s;
+}
+
+// CRC-64/XZ of `count` device buffers in two launches; crc_out[i] (device)
+int launch_crc64_many(const uint8_t* const* data, const int64_t* n, int count, uint64_t* crc_out,
+                      void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (count < 0) return NBZG_BAD_ARG;
+  if (count == 0) return NBZG_OK;
   if (int rc = upload_tables()) return rc;
   uint64_t* span = reinterpret_cast<uint64_t*>(ws);
-  const int64_t C = crc_spans(n);
-  const int64_t pad = (C << kCrcSpanLog) - n;
-  int run_log = 0;
-  while ((int64_t(kFoldThreads) << run_log) < C) run_log++;
-  // the fold tree's top level is Z_{2^(span_log + run_log + 9)}
-  if (kCrcSpanLog + run_log + 9 >= kCrcLevels) return NBZG_BAD_ARG;
-  count_launch();
-  crc_span_kernel<<<(unsigned)C, kCrcThreads, 0, st>>>(data, n, pad, span);
-  count_launch();
-  crc_fold_kernel<<<1, kFoldThreads, 0, st>>>(span, C, run_log, n, crc_out);
+  for (int c0 = 0; c0 < count; c0 += kCrcMax) {
+    const int cnt = count - c0 < kCrcMax ? count - c0 : kCrcMax;
+    if (ws_bytes < crc_ws_many(n + c0, cnt)) return NBZG_BAD_ARG;
+    CrcJobs J;
+    J.count = cnt;
+    J.span0[0] = 0;
+    for (int i = 0; i < cnt; i++) {
+      const int64_t ni = n[c0 + i];
+      if (ni < 0 || (ni >> kCrcLevels)) return NBZG_BAD_ARG;
+      const int64_t C = crc_spans(ni);
+      int run_log = 0;
+      while ((int64_t(kFoldThreads) << run_log) < C) run_log++;
+      // the fold tree's top level is Z_{2^(span_log + run_log + 9)}
+      if (kCrcSpanLog + run_log + 9 >= kCrcLevels) return NBZG_BAD_ARG;
+      J.data[i] = data[c0 + i];
+      J.n[i] = ni;
+      J.pad[i] = (C << kCrcSpanLog) - ni;
+      J.span0[i + 1] = J.span0[i] + C;
+      J.out[i] = crc_out + c0 + i;
+      J.run_log[i] = run_log;
+    }
+    count_launch();
+    crc_span_kernel<<<(unsigned)J.span0[cnt], kCrcThreads, 0, st>>>(J, span);
+    count_launch();
+    crc_fold_kernel<<<cnt, kFoldThreads, 0, st>>>(J, span);  // (next batch: stream-ordered)
+  }
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
+}
+
+int launch_crc64(const uint8_t* data, int64_t n, uint64_t* crc_out, void* ws, size_t ws_bytes,
+                 cudaStream_t st) {
+  if (ws_bytes < crc_ws(n)) return NBZG_BAD_ARG;
+  return launch_crc64_many(&data, &n, 1, crc_out, ws, ws_bytes, st);
 }
 
 }  // namespace nbzg

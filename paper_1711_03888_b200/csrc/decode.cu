@@ -35,10 +35,20 @@ constexpr int kDThreads = kDWarps * 32;
 constexpr int kLutBits = 16;       // code-length table index bits (u8 entries, 64 KiB)
 constexpr int kSmemSyms = 16384;   // sorted-symbol table staged in smem up to this k
 constexpr int kTpcBits = 15;       // thread-per-chunk fused table index bits (i32, 128 KiB)
-constexpr int kTpc2Cap = 16384;    // secondary (long-code) table entries (64 KiB)
+#ifndef NBZG_LV_RING
+#define NBZG_LV_RING 16
+#endif
+// decode_lv_kernel's per-thread word ring (8 or 16 words; 16 leaves room for
+// two 16-byte stream blocks in flight per lane, at the cost of half the
+// long-code table)
+constexpr int kLvRing = NBZG_LV_RING;
+constexpr int kLvRingMask = kLvRing - 1;
+constexpr int kTpc2Cap = kLvRing == 16 ? 12288 : 16384;  // secondary (long-code) table entries
 constexpr int kTpcMaxThreads = 704;
 constexpr int kLvMaxThreads = 768;  // decode_lv_kernel: 80 registers x 768 fit the register file
 constexpr int kRingStride = 1024;  // words between ring slots (power of two, >= threads)
+// decode_lv_kernel's ring: slot stride = its thread cap
+constexpr int kLvStride = NBZG_LV_RING == 16 ? 768 : kRingStride;
 constexpr int kTpcTab = (1 << kTpcBits) + kTpc2Cap;
 
 struct DParsed {
@@ -336,6 +346,13 @@ NBZG_DEV void ldg_v4_if(uint4& q, const uint4* p, bool pred) {
       "{\n .reg .pred p;\n setp.ne.u32 p, %4, 0;\n"
       " @p ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%5];\n}\n"
       : "+r"(q.x), "+r"(q.y), "+r"(q.z), "+r"(q.w)
+      : "r"((uint32_t)pred), "l"(p));
+}
+NBZG_DEV void ldg_v8_if_l2(uint4& q, uint4& r, const uint4* p, bool pred) {  // 32 bytes per lane
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.u32 p, %8, 0;\n"
+      " @p ld.global.nc.L2::256B.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%9];\n}\n"
+      : "+r"(q.x), "+r"(q.y), "+r"(q.z), "+r"(q.w), "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w)
       : "r"((uint32_t)pred), "l"(p));
 }
 NBZG_DEV void ldg_v4_if_l2(uint4& q, const uint4* p, bool pred) {  // 256-byte L2 fill on a miss
@@ -723,9 +740,14 @@ struct TpcReader {
 
 // one 32-byte streaming store (sm_100 256-bit STG): a whole sector per lane
 NBZG_DEV void st_v8_cs(float* p, const float (&o)[8]) {
+#ifdef NBZG_DEC_NOSTORE  // timing experiment only: values consumed, nothing stored
+  float s = ((o[0] + o[1]) + (o[2] + o[3])) + ((o[4] + o[5]) + (o[6] + o[7]));
+  if (s == 1234.5678f) *p = s;
+#else
   asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(o[0]),
                "f"(o[1]), "f"(o[2]), "f"(o[3]), "f"(o[4]), "f"(o[5]), "f"(o[6]), "f"(o[7])
                : "memory");
+#endif
 }
 
 NBZG_DEV void tpc_init(TpcReader& R, const uint4* G, uint32_t* ring, int nthr, uint64_t bitpos,
@@ -1012,7 +1034,10 @@ struct BufReader {
   uint32_t cnt;     // valid bits in hi:lo (the bits after them are zero)
   uint32_t wi;      // next stream word to enter the buffer
   uint32_t wr;      // first stream word not in the ring (multiple of 4)
-  uint4 qs;         // block wr/4, loaded at the last group boundary
+  uint4 qs;         // block wr/4, loaded at the last refill
+#if NBZG_LV_RING == 16
+  uint4 qs2;        // block wr/4 + 1
+#endif
 };
 
 NBZG_DEV uint32_t shl_c(uint32_t x, uint32_t s) {  // s >= 32 -> 0
@@ -1036,6 +1061,53 @@ NBZG_DEV void bb_fill(BufReader& R, uint32_t nw) {  // cnt <= 32
   R.cnt += 32;
   R.wi += 1;
 }
+NBZG_DEV void ring_put(uint32_t* ring, uint32_t s, const uint4& q) {
+  ring[(s + 0) * kLvStride] = bswap32(q.x);
+  ring[(s + 1) * kLvStride] = bswap32(q.y);
+  ring[(s + 2) * kLvStride] = bswap32(q.z);
+  ring[(s + 3) * kLvStride] = bswap32(q.w);
+}
+#if NBZG_LV_RING == 16
+// 16-word ring refilled 8 words at a time: one 32-byte load per lane (half
+// the L1 wavefronts of 16-byte loads) that has several groups to land.
+// Stream blocks are 32-byte aligned here: G8 = the 32-byte block index.
+NBZG_DEV void bb_init(BufReader& R, const uint4* G, uint32_t* ring, uint64_t bitpos,
+                      uint32_t vmax) {
+  const uint32_t gw0 = (uint32_t)(bitpos >> 5);
+  const uint32_t blk = gw0 >> 3;  // 8-word block
+  const uint32_t v8 = vmax >> 1;
+  uint4 A0 = make_uint4(0, 0, 0, 0), A1 = A0, B0 = A0, B1 = A0;
+  ldg_v8_if_l2(A0, A1, G + 2 * min(blk, v8), true);
+  ldg_v8_if_l2(B0, B1, G + 2 * min(blk + 1, v8), true);
+  const uint32_t s0 = (8 * blk) & 15, s1 = s0 ^ 8;
+  ring_put(ring, s0, A0);
+  ring_put(ring, s0 + 4, A1);
+  ring_put(ring, s1, B0);
+  ring_put(ring, s1 + 4, B1);
+  const uint32_t off = (uint32_t)(bitpos & 31);
+  const uint32_t w0 = ring[(gw0 & 15) * kLvStride], w1 = ring[((gw0 + 1) & 15) * kLvStride];
+  R.hi = __funnelshift_l(w1, w0, off);
+  R.lo = shl_c(w1, off);
+  R.cnt = 64 - off;
+  R.wi = gw0 + 2;
+  R.wr = 8 * (blk + 2);
+  R.qs = make_uint4(0, 0, 0, 0);
+  R.qs2 = make_uint4(0, 0, 0, 0);
+  ldg_v8_if_l2(R.qs, R.qs2, G + 2 * min(blk + 2, v8), true);
+}
+// group boundary: when 8 ring slots are consumed, move the 32-byte block
+// loaded at the last such refill into the ring and issue the next load
+NBZG_DEV void bb_refill(BufReader& R, uint32_t* ring, const uint4* G, uint32_t vmax) {
+  const bool room = (int32_t)(R.wr - R.wi) <= 8;
+  if (room) {
+    const uint32_t s = R.wr & 15;  // 0 or 8
+    ring_put(ring, s, R.qs);
+    ring_put(ring, s + 4, R.qs2);
+    R.wr += 8;
+  }
+  ldg_v8_if_l2(R.qs, R.qs2, G + 2 * min(R.wr >> 3, vmax >> 1), room);
+}
+#else
 NBZG_DEV void bb_init(BufReader& R, const uint4* G, uint32_t* ring, uint64_t bitpos,
                       uint32_t vmax) {
   const uint32_t gw0 = (uint32_t)(bitpos >> 5);
@@ -1074,6 +1146,7 @@ NBZG_DEV void bb_refill(BufReader& R, uint32_t* ring, const uint4* G, uint32_t v
   }
   ldg_v4_if_l2(R.qs, G + min(R.wr >> 2, vmax), room);
 }
+#endif
 
 // constants of one field's decode, shared by the chunk lanes of a thread
 struct LvCtx {
@@ -1086,6 +1159,7 @@ struct LvCtx {
   const DField* F;
   double twob;
   uint32_t vmax, wmax, r0m1, r0, sh2, lt_s;
+  uint32_t rlim, m2;  // table index of window v: hi(min(v, rlim) * 2^15) + hi((v - min) * m2)
   int lmin, max_len, bias;
 };
 // one chunk being decoded
@@ -1112,7 +1186,7 @@ NBZG_DEV void lv_fill_safe(const LvCtx& X, LvChunk& S) {
   while (S.R.cnt <= 32) {
     uint32_t nw;
     if ((int32_t)(S.R.wr - S.R.wi) > 0) {
-      nw = S.ring[(S.R.wi & 7) * kRingStride];
+      nw = S.ring[(S.R.wi & kLvRingMask) * kLvStride];
     } else {
       asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(nw) : "l"(X.G32 + min(S.R.wi, X.wmax)));
       nw = bswap32(nw);
@@ -1120,11 +1194,20 @@ NBZG_DEV void lv_fill_safe(const LvCtx& X, LvChunk& S) {
     bb_fill(S.R, nw);
   }
 }
+// Index of window v in the shared table: codes <= 15 bits resolve in the
+// primary entries [0, P) (P = r0 >> 17: the 15-bit prefixes below the first
+// long code), longer codes in the long-code entries [P, P + n2) at 2^sh2
+// resolution.  Branch- and select-free, mostly on the FMA pipe (two
+// IMAD.HI): min(v, r0) >> 17 is the prefix of a short code and P for a long
+// one; (v - min(v, r0)) >> sh2 is 0 for a short code.
+NBZG_DEV uint32_t lv_index(const LvCtx& X, uint32_t v) {
+  const uint32_t m = min(v, X.rlim);
+  return __umulhi(m, 1u << kTpcBits) + __umulhi(v - m, X.m2);
+}
 // canonical decode of the symbol at v (any length <= 32)
 NBZG_DEV int32_t lv_resolve(const LvCtx& X, LvChunk& S, uint32_t v) {
-  int32_t e = X.LT[v >> (32 - kTpcBits)];
-  if ((e & 63) == 0) {
-    e = v > X.r0m1 ? X.LT[(1 << kTpcBits) + ((v - X.r0) >> X.sh2)] : 64;
+  int32_t e = X.LT[lv_index(X, v)];
+  {
     if ((e & 63) == 0) {  // longer than the tables resolve, or invalid
       int r = 0;
 #pragma unroll 1
@@ -1170,7 +1253,7 @@ NBZG_DEV bool lv_fast8(const LvCtx& X, LvChunk& S, float (&o)[8], LvSnap& sn) {
   for (int q = 0; q < 8; q++) {
     if ((q & 1) == 0) {  // >= 32 valid bits before an even symbol (branch-free:
       // both shifts are 0 when cnt > 32)
-      const uint32_t nw = S.ring[(R.wi & 7) * kRingStride];
+      const uint32_t nw = S.ring[(R.wi & kLvRingMask) * kLvStride];
       R.hi |= shr_c(nw, R.cnt);
       R.lo |= shl_c(nw, 32u - R.cnt);
       const uint32_t t = R.cnt <= 32 ? 32u : 0u;
@@ -1178,15 +1261,17 @@ NBZG_DEV bool lv_fast8(const LvCtx& X, LvChunk& S, float (&o)[8], LvSnap& sn) {
       R.wi += t >> 5;
     }
     const uint32_t v = R.hi;
-    const uint32_t ix =
-        v > X.r0m1 ? (1u << kTpcBits) + ((v - X.r0) >> X.sh2) : v >> (32 - kTpcBits);
-    const int32_t e = X.LT[ix];
+    const int32_t e = X.LT[lv_index(X, v)];
     flags |= (uint32_t)e;  // bit 6: escape or unresolved
     bb_take(R, (uint32_t)e & 63u);
     k32 += e >> 7;
+#ifdef NBZG_DEC_MAGIC
     // f32(k * 2b) with k exact in double: 2^52 + 2^31 + k, minus the bias
     const double kd =
         __hiloint2double(0x43300000, (int32_t)((uint32_t)k32 ^ 0x80000000u)) - 4503601774854144.0;
+#else
+    const double kd = (double)k32;  // I2F.F64 (exact): one conversion-pipe op
+#endif
     o[q] = (float)__dmul_rn(kd, X.twob);
   }
   S.k = k32;
@@ -1254,16 +1339,20 @@ __global__ void __launch_bounds__(kLvMaxThreads, 1) decode_lv_kernel(DArgs a) {
   const int64_t ce = (a.nchunks * (gj + 1)) / gn;
   if (cb >= ce) return;
   const int tid = threadIdx.x, nthr = blockDim.x;
-  uint32_t* ring = reinterpret_cast<uint32_t*>(dsm2 + 4 * kTpcTab) + tid;  // [8][kRingStride]
+  uint32_t* ring = reinterpret_cast<uint32_t*>(dsm2 + 4 * kTpcTab) + tid;  // [kLvRing][kRingStride]
   const uint32_t n2 = P.t2_n;
+  // shared table: the primary entries of the 15-bit prefixes below r0, then
+  // the long-code entries (lv_index); one unresolved entry when long codes
+  // exist but their table is empty
+  const bool has_long = P.t2_r0 < ((uint64_t)1 << 32);
+  const uint32_t P15 = has_long ? (uint32_t)(P.t2_r0 >> (32 - kTpcBits)) : (1u << kTpcBits);
   {
     const int32_t* gl = a.lut2 + (size_t)fi * kTpcTab;
-    const uint32_t nv = ((1u << kTpcBits) + n2 + 3) / 4;
-    for (uint32_t i = tid; i < nv; i += nthr)
-      reinterpret_cast<uint4*>(LT)[i] = __ldg(reinterpret_cast<const uint4*>(gl) + i);
+    for (uint32_t i = tid; i < P15; i += nthr) LT[i] = __ldg(gl + i);
+    for (uint32_t i = tid; i < n2; i += nthr) LT[P15 + i] = __ldg(gl + (1 << kTpcBits) + i);
+    if (tid == 0 && has_long && n2 == 0) LT[P15] = 64;
   }
   __syncthreads();
-  if (tid < 2 && n2 == 0) LT[(1 << kTpcBits) + tid] = 64;  // tail index of an empty long-code table
   if (tid < 64) {
     const int l = tid;
     uint64_t lim = 0;
@@ -1283,9 +1372,13 @@ __global__ void __launch_bounds__(kLvMaxThreads, 1) decode_lv_kernel(DArgs a) {
   X.s_base = s_base;
   X.ss = a.ssyms + fi * a.nbins;
   const uintptr_t bits_addr = reinterpret_cast<uintptr_t>(F.payload + P.bits_off);
-  X.G = reinterpret_cast<const uint4*>(bits_addr & ~uintptr_t(15));
+  // stream base aligned to the refill load size (the bit offset a0 absorbs
+  // the rest; the payload's table precedes its bitstream, so the aligned
+  // base stays inside the payload)
+  constexpr uintptr_t kAl = NBZG_LV_RING == 16 ? 31 : 15;
+  X.G = reinterpret_cast<const uint4*>(bits_addr & ~kAl);
   X.G32 = reinterpret_cast<const uint32_t*>(X.G);
-  const uint32_t a0 = (uint32_t)(bits_addr & 15) * 8;
+  const uint32_t a0 = (uint32_t)(bits_addr & kAl) * 8;
   // last 16-byte block / word the stream may touch (payload + 64-byte slack)
   X.vmax = (uint32_t)((a0 / 8 + 4 * ((P.total_bits + 31) / 32) + 16) / 16);
   X.wmax = 4 * X.vmax + 3;
@@ -1299,6 +1392,8 @@ __global__ void __launch_bounds__(kLvMaxThreads, 1) decode_lv_kernel(DArgs a) {
   X.r0m1 = (uint32_t)(min(P.t2_r0, (uint64_t)1 << 32) - 1);
   X.r0 = X.r0m1 + 1;
   X.sh2 = n2 ? 32u - P.t2_w : 31u;
+  X.rlim = has_long ? (uint32_t)P.t2_r0 : 0xffffffffu;
+  X.m2 = n2 ? (1u << P.t2_w) : 0u;
   X.lmin = n2 ? (int)P.t2_w : kTpcBits;  // longer codes: canonical search
   X.lt_s = (uint32_t)__cvta_generic_to_shared(LT);
   const uint64_t* choff = a.choff + fi * (a.nchunks + 1);
@@ -1323,7 +1418,11 @@ __global__ void __launch_bounds__(kLvMaxThreads, 1) decode_lv_kernel(DArgs a) {
         lv_fix(X, A, ob, sa, lv_fast8(X, A, ob, sa));
         asm volatile("" ::"f"(oa[0]), "f"(oa[1]), "f"(oa[2]), "f"(oa[3]), "f"(oa[4]),
                      "f"(oa[5]), "f"(oa[6]), "f"(oa[7]));
+#ifndef NBZG_DEC_STHALF  // timing experiment: half the stores
         st_v8_cs(A.dst + i + 8, ob);
+#else
+        if (ob[0] == 1234.5f) A.dst[i] = ob[1];
+#endif
         if (lv_consumed(A) > A.Tb) {
           i += 16;
           break;  // corrupt: stop early, reported below
@@ -1567,7 +1666,7 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
     const int thr = min(kTpcMaxThreads, (per + 31) / 32 * 32);
     const size_t sm2 = 4 * kTpcTab + 32 * (size_t)kRingStride;
     {  // sized for the largest launch
-      const int smax = 4 * kTpcTab + 32 * kRingStride;
+      const int smax = 4 * kTpcTab + 4 * max(kLvRing * kLvStride, 8 * kRingStride);
       smem_attr((const void*)decode_tpc_kernel<false>, smax);
       smem_attr((const void*)decode_tpc_kernel<true>, smax);
       smem_attr((const void*)decode_lv_kernel, smax);
@@ -1611,7 +1710,7 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
         a.cta0[f + 1] = a.cta0[f] + g[f];
         thr_lv = max(thr_lv, (int)min((int64_t)kLvMaxThreads, ((a.nchunks + g[f] - 1) / g[f] + 31) / 32 * 32));
       }
-      decode_lv_kernel<<<a.cta0[nf], thr_lv, sm2, st>>>(a);
+      decode_lv_kernel<<<a.cta0[nf], thr_lv, 4 * kTpcTab + 4 * kLvRing * (size_t)kLvStride, st>>>(a);
     } else {
       count_launch();
       decode_kernel<true><<<groups * nf, kDThreads, sm, st>>>(a);

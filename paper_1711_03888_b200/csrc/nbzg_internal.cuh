@@ -10,6 +10,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/nbzg.h"
 
@@ -20,6 +21,15 @@ namespace nbzg {
 // launch accounting + optional per-kernel CUDA-event tracing (capi.cu)
 void count_launch();
 void trace_mark(const char* name, cudaStream_t st);
+
+// NVTX range for the host-side span of one stage (header-only NVTX3: a no-op
+// unless a profiler injects its library, e.g. nsys / ncu --nvtx)
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+  NvtxScope(const NvtxScope&) = delete;
+  NvtxScope& operator=(const NvtxScope&) = delete;
+};
 
 constexpr int kTileMax = 16384;        // particles per tile / codes per chunk
 constexpr int kChunk = 16384;          // v2 chunk index granularity (symbols)

@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort_kernel(RArgs a) {
   __shared__ SegParams sp;
 
   const int64_t t = blockIdx.x;
-  if (a.pass == 1 && a.tile_flags[t] == 0) return;
+  if (a.pass >= 1 && a.tile_flags[t] != (uint32_t)a.pass) return;
   const int64_t t0 = t * a.tile;
   const int64_t t1 = min(a.n, t0 + a.tile);
   const int mt = (int)(t1 - t0);
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort6_kernel(RArgs a) 
   __shared__ int s_shift, s_w, s_bits, s_bad;
 
   const int64_t t = blockIdx.x;
-  if (a.pass == 1 && a.tile_flags[t] == 0) return;
+  if (a.pass >= 1 && a.tile_flags[t] != (uint32_t)a.pass) return;
   const int64_t t0 = t * a.tile;
   const int64_t t1 = min(a.n, t0 + a.tile);
   const int mt = (int)(t1 - t0);
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort6_kernel(RArgs a) 
     }
     const int w = s_w;
     if (sizeof(KeyT) == 4 && 6 * w > 32) {
-      if (threadIdx.x == 0) a.tile_flags[t] = 1;
+      if (threadIdx.x == 0) a.tile_flags[t] = 2;
       return;  // redone by the u64 pass
     }
     if (threadIdx.x == 0) a.seg_bits[s0 / a.S] = (uint8_t)s_bits;
@@ -480,6 +480,316 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort6_kernel(RArgs a) 
     }
     __syncthreads();
   }
+  for (int i = threadIdx.x; i < mt; i += kSortThreads) a.perm[t0 + i] = perm[i];
+}
+
+// ---------------------------------------------------------------- compact-key sort
+// The stable order by the masked key K is unchanged when K is replaced by
+// any strictly increasing function of the keys present in the segment.  Bits
+// that are zero in every key of the segment are such a function's free
+// choice: field t's masked value u_t = (k_t - mn_t) >> shift lies in
+// [0, umax_t] with umax_t = (hi_t - lo_t) >> shift known from the segment's
+// integerised min / max, so only its low w_t = bitlen(umax_t) bits can be
+// set.  The compacted key keeps exactly those bits, in the interleaved
+// order (group j high to low, x before y before z within a group): bit j of
+// field t goes to position P_t(j) = sum_t' min(j, w_t') + #{t' > t : j < w_t'}.
+// Per segment, byte-wise tables T[t][b][v] give each field's contribution,
+// so a key costs three table reads instead of three bit-spreads.  At config
+// 2 (eb 1e-4) the masked keys carry 21 bits but only ~9 vary: one radix pass
+// with 2^cw bins sorts the segment.  Segments whose compacted key exceeds 16
+// bits are flagged for the general kernel (rindex_sort_kernel, pass 1).
+constexpr int kCsMaxBits = 16;  // compacted key bits handled here (u16 keys)
+constexpr int kCsOneBits = 10;  // <= this: a single pass with 2^cw bins
+constexpr int kCsJ = kTileMax / kSortThreads;  // elements per thread (32)
+
+struct CsSeg {
+  int64_t mn[3];
+  float amax[3];
+  int shift, w, bits, bad, cw, wmax;
+  int wt[3];
+};
+
+// one stable counting pass over m <= 16384 elements: digit of element
+// (warp-major position pos) = (key >> sh) & (2^D - 1), key = keys[src(pos)],
+// src = pos (FIRST) or perm[pos]; output perm[dst] = src, in place.
+// Values in perm are tile-local (segment start lo + segment index).
+template <bool FIRST>
+__device__ __noinline__ void cs_pass(const uint16_t* keys, uint16_t* perm, int lo, int m, int sh, int D,
+                      uint16_t* whist, uint32_t* scan_tmp) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nb = 1 << D;
+  const uint32_t msk = (uint32_t)nb - 1;
+  const uint32_t keys_s = sh_addr(keys), perm_s = sh_addr(perm);
+  const uint32_t wh_s = sh_addr(whist) + 2u * (uint32_t)(w * nb);
+  for (int i = threadIdx.x; i < kSortWarps * nb / 2; i += kSortThreads)
+    sts_u32(sh_addr(whist) + 4u * (uint32_t)i, 0u);
+  __syncthreads();
+  const int base = w * (kTileMax / kSortWarps);
+  // per element: FIRST -> rank (16 bits, two per register); else idx | rank << 14 | d << 24
+  uint32_t packed[FIRST ? kCsJ / 2 : kCsJ];
+#pragma unroll
+  for (int j = 0; j < kCsJ; j++) {
+    const int pos = base + j * 32 + lane;
+    const bool valid = pos < m;
+    const uint32_t src =
+        FIRST ? (uint32_t)pos : (valid ? lds_u16(perm_s + 2u * (uint32_t)pos) - (uint32_t)lo : 0u);
+    const uint32_t d = valid ? ((lds_u16(keys_s + 2u * src) >> sh) & msk) : 0x10000u;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t lt = __popc(peers & lanemask_lt());
+    const uint32_t cnt = valid ? lds_u16(wh_s + 2u * d) : 0u;
+    __syncwarp();
+    if (valid && lt == 0) sts_u16(wh_s + 2u * d, cnt + __popc(peers));
+    __syncwarp();
+    const uint32_t r = cnt + lt;
+    if (FIRST) {
+      if (j & 1) packed[j >> 1] |= r << 16;
+      else packed[j >> 1] = r;
+    } else {
+      packed[j] = src | (r << 14) | (d << 24);
+    }
+  }
+  __syncthreads();
+  // digit-major / warp-minor exclusive scan of the per-warp counts: counter
+  // q = d * 16 + w; thread t owns counters [t*ipt, (t+1)*ipt)
+  {
+    const int C = kSortWarps * nb;
+    const int ipt = (C + kSortThreads - 1) / kSortThreads;  // 1 .. 32
+    const int q0 = threadIdx.x * ipt;
+    uint32_t s = 0;
+    for (int q = q0; q < min(C, q0 + ipt); q++) s += whist[(q & 15) * nb + (q >> 4)];
+    uint32_t tot;
+    uint32_t ex = block_excl_scan<uint32_t>(s, scan_tmp, &tot);
+    for (int q = q0; q < min(C, q0 + ipt); q++) {
+      const int a = (q & 15) * nb + (q >> 4);
+      const uint32_t c = whist[a];
+      whist[a] = (uint16_t)ex;
+      ex += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kCsJ; j++) {
+    const int pos = base + j * 32 + lane;
+    if (pos < m) {
+      uint32_t src, r, d;
+      if (FIRST) {
+        src = (uint32_t)pos;
+        r = (packed[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+        d = (lds_u16(keys_s + 2u * src) >> sh) & msk;
+      } else {
+        src = packed[j] & 0x3fffu;
+        r = (packed[j] >> 14) & 0x3ffu;
+        d = packed[j] >> 24;
+      }
+      sts_u16(perm_s + 2u * (lds_u16(wh_s + 2u * d) + r), src + (uint32_t)lo);
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) {
+  extern __shared__ __align__(16) uint8_t csm[];
+  uint16_t* keys = reinterpret_cast<uint16_t*>(csm);          // [kTileMax] segment-local
+  uint16_t* perm = keys + kTileMax;                           // [kTileMax] tile-local values
+  uint16_t* whist = perm + kTileMax;                          // [16][2^10]
+  uint32_t(*lut)[3][256] = reinterpret_cast<uint32_t(*)[3][256]>(whist + (kSortWarps << kCsOneBits));
+  __shared__ uint32_t scan_tmp[33];
+  __shared__ float red[2][3][kSortWarps];
+  __shared__ CsSeg sp;
+
+  const int64_t t = blockIdx.x;
+  const int64_t t0 = t * a.tile;
+  const int64_t t1 = min(a.n, t0 + a.tile);
+  const int mt = (int)(t1 - t0);
+  const nbzg_field_meta* fm = a.meta->f + a.fbase;
+  bool flagged = false;
+
+  for (int64_t s0 = t0; s0 < t1; s0 += a.S) {
+    const int lo = (int)(s0 - t0);
+    const int m = (int)(min(t1, s0 + a.S) - s0);
+    // ---- 1. segment min / max (K1's per-segment values, else reduced here)
+    float mn[3], mx[3];
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      mn[c] = __int_as_float(0x7f800000);
+      mx[c] = -__int_as_float(0x7f800000);
+    }
+    if (a.seg_mm) {
+      const float* sm = a.seg_mm + 6 * (s0 / a.S);
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        mn[c] = sm[2 * c];
+        mx[c] = sm[2 * c + 1];
+      }
+    } else {
+      for (int i = threadIdx.x; i < m; i += kSortThreads) {
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+          const float v = a.x[c][s0 + i];
+          mn[c] = fminf(mn[c], v);
+          mx[c] = fmaxf(mx[c], v);
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        mn[c] = fminf(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
+        mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+      }
+      if ((threadIdx.x & 31) == 0) {
+        red[0][c][threadIdx.x >> 5] = mn[c];
+        red[1][c][threadIdx.x >> 5] = mx[c];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // rindex.py:164-198: per-segment minima, need, bits, clamp drop
+      int need = 0, bad = 0;
+      int64_t rng[3];
+      for (int c = 0; c < 3; c++) {
+        float a0 = red[0][c][0], b0 = red[1][c][0];
+        for (int q = 1; q < kSortWarps; q++) {
+          a0 = fminf(a0, red[0][c][q]);
+          b0 = fmaxf(b0, red[1][c][q]);
+        }
+        sp.amax[c] = fmaxf(fabsf(a0), fabsf(b0));
+        rng[c] = 0;
+        if (fm[c].is_const) {
+          sp.mn[c] = 0;
+          continue;
+        }
+        const double qa = __ddiv_rn((double)a0, fm[c].twob), qb = __ddiv_rn((double)b0, fm[c].twob);
+        if (fabs(qa) > kIntLimit || fabs(qb) > kIntLimit) bad = 1;
+        const int64_t ia = (int64_t)rint(qa), ib = (int64_t)rint(qb);
+        sp.mn[c] = ia;
+        rng[c] = ib - ia;
+        need = max(need, bitlen64((uint64_t)rng[c]));
+      }
+      const int bits = min(need, 21);
+      const int drop = need > 21 ? need - 21 : 0;  // allow_key_clamp (pipeline.py:463)
+      if (a.no_clamp && need > 21) bad = 1;       // CPC: BoundTooSmallError (rindex.py:185-190)
+      const int eff = min(a.ig, bits);
+      sp.bits = bits;
+      sp.shift = drop + eff;
+      sp.w = bits - eff;
+      sp.bad = bad;
+      int cw = 0, wmax = 0;
+      for (int c = 0; c < 3; c++) {
+        const int wt = sp.w > 0 ? bitlen64((uint64_t)rng[c] >> sp.shift) : 0;
+        sp.wt[c] = wt;
+        cw += wt;
+        wmax = max(wmax, wt);
+      }
+      sp.cw = cw;
+      sp.wmax = wmax;
+    }
+    __syncthreads();
+    if (sp.bad) {
+      if (threadIdx.x == 0) set_status(a.status, NBZG_BOUND_TOO_SMALL);
+      return;
+    }
+    if (threadIdx.x == 0) {
+      a.seg_bits[s0 / a.S] = (uint8_t)sp.bits;
+      if (a.minima)
+        for (int c = 0; c < 3; c++) a.minima[3 * (s0 / a.S) + c] = sp.mn[c];
+    }
+    const int cw = sp.cw;
+    if (cw > kCsMaxBits) {  // the general kernel redoes this tile
+      flagged = true;
+      continue;
+    }
+    if (flagged) continue;  // (seg_bits / minima still written for every segment)
+    if (cw == 0) {
+      for (int i = threadIdx.x; i < m; i += kSortThreads) perm[lo + i] = (uint16_t)(lo + i);
+      __syncthreads();
+      continue;
+    }
+    // ---- 2. compaction tables: T[t][b][v] = sum_i bit_i(v) << P_t(8b + i)
+    const int nbyte = (sp.wmax + 7) >> 3;
+    for (int e = threadIdx.x; e < 3 * nbyte * 256; e += kSortThreads) {
+      const int tt = e / (nbyte * 256), b = (e >> 8) % nbyte, v = e & 255;
+      uint32_t out = 0;
+      for (int i = 0; i < 8; i++) {
+        const int j = 8 * b + i;
+        if (!((v >> i) & 1) || j >= sp.wt[tt]) continue;
+        int pos = 0;
+#pragma unroll
+        for (int c = 0; c < 3; c++) pos += min(j, sp.wt[c]) + ((c > tt && j < sp.wt[c]) ? 1 : 0);
+        out |= 1u << pos;
+      }
+      lut[tt][b][v] = out;
+    }
+    __syncthreads();
+    // ---- 3. compacted keys (exact integerisation: FP32 under a segment-wide
+    // margin, FP64 division otherwise -- same argument as gen_keys)
+    {
+      const int shift = sp.shift;
+      const int32_t m0 = (int32_t)sp.mn[0], m1 = (int32_t)sp.mn[1], m2 = (int32_t)sp.mn[2];
+      float cm[3];
+      bool small = true;
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        const float tmax = sp.amax[c] * fm[c].inv32;
+        small &= tmax < 4194304.0f;
+        cm[c] = 0.5f - __fmaf_ru(tmax, 2.384185791015625e-07f, 9.5367431640625e-07f);
+      }
+      const uint32_t lut_s = sh_addr(&lut[0][0][0]);
+      auto key_of = [&](float x0, float x1, float x2) -> uint32_t {
+        const float xv[3] = {x0, x1, x2};
+        const int32_t mv[3] = {m0, m1, m2};
+        uint32_t key = 0;
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+          uint32_t u;
+          if (small) {
+            const float tt = xv[c] * fm[c].inv32;
+            const float r = tt + 12582912.0f;
+            const float d = tt - (r - 12582912.0f);
+            int32_t k = __float_as_int(r) - 0x4B400000;
+            if (!(fabsf(d) < cm[c])) k = (int32_t)rint(__ddiv_rn((double)xv[c], fm[c].twob));
+            u = (uint32_t)(k - mv[c]) >> shift;
+          } else {
+            const int64_t iv = fm[c].is_const ? 0 : integerize1(xv[c], fm[c]);
+            u = (uint32_t)((uint64_t)(iv - sp.mn[c]) >> shift);
+          }
+          const uint32_t tb = lut_s + 4u * (uint32_t)(c * 3 * 256);
+          key |= lds_u32(tb + 4u * (u & 255u));
+          if (nbyte > 1) key |= lds_u32(tb + 4u * (256u + ((u >> 8) & 255u)));
+          if (nbyte > 2) key |= lds_u32(tb + 4u * (512u + ((u >> 16) & 255u)));
+        }
+        return key;
+      };
+      const int m4 = (s0 & 3) ? 0 : m >> 2;
+      const float4* x4[3] = {reinterpret_cast<const float4*>(a.x[0] + s0),
+                             reinterpret_cast<const float4*>(a.x[1] + s0),
+                             reinterpret_cast<const float4*>(a.x[2] + s0)};
+#pragma unroll 2
+      for (int v = threadIdx.x; v < m4; v += kSortThreads) {
+        const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
+        const uint32_t k0 = key_of(q0.x, q1.x, q2.x), k1 = key_of(q0.y, q1.y, q2.y);
+        const uint32_t k2 = key_of(q0.z, q1.z, q2.z), k3 = key_of(q0.w, q1.w, q2.w);
+        *reinterpret_cast<uint2*>(keys + 4 * v) = make_uint2(k0 | (k1 << 16), k2 | (k3 << 16));
+      }
+      for (int i = 4 * m4 + threadIdx.x; i < m; i += kSortThreads)
+        keys[i] = (uint16_t)key_of(a.x[0][s0 + i], a.x[1][s0 + i], a.x[2][s0 + i]);
+    }
+    __syncthreads();
+    // ---- 4. stable LSD over cw bits, output into this segment's perm range
+    if (cw <= kCsOneBits) {
+      cs_pass<true>(keys, perm + lo, lo, m, 0, cw, whist, scan_tmp);
+    } else {
+      const int d1 = cw >> 1;
+      cs_pass<true>(keys, perm + lo, lo, m, 0, d1, whist, scan_tmp);
+      cs_pass<false>(keys, perm + lo, lo, m, d1, cw - d1, whist, scan_tmp);
+    }
+  }
+  if (flagged) {
+    if (threadIdx.x == 0) a.tile_flags[t] = 1;
+    return;
+  }
+  // ---- write the tile's permutation (coalesced)
   for (int i = threadIdx.x; i < mt; i += kSortThreads) a.perm[t0 + i] = perm[i];
 }
 
@@ -504,19 +814,30 @@ int launch_rindex_sort(const Plan& p, cudaStream_t st) {
   a.seg_mm = p.seg_mm;
   size_t sm32 = kTileMax * (4 + 2) + kSortWarps * kRadix * 2;
   size_t sm64 = kTileMax * (8 + 2) + kSortWarps * kRadix * 2;
+  size_t smc = kTileMax * (2 + 2) + (kSortWarps << kCsOneBits) * 2 + 3 * 3 * 256 * 4;
+  smem_attr((const void*)rindex_csort_kernel, (int)smc);
   smem_attr((const void*)rindex_sort_kernel<uint32_t>, (int)sm32);
   smem_attr((const void*)rindex_sort_kernel<uint64_t>, (int)sm64);
   smem_attr((const void*)rindex_sort6_kernel<uint32_t>, (int)sm32);
   smem_attr((const void*)rindex_sort6_kernel<uint64_t>, (int)sm64);
   cudaMemsetAsync(p.tile_flags, 0, sizeof(uint32_t) * p.ntiles, st);
-  a.pass = 0;
-  count_launch();
-  if (nk == 6) rindex_sort6_kernel<uint32_t><<<(unsigned)p.ntiles, kSortThreads, sm32, st>>>(a);
-  else rindex_sort_kernel<uint32_t><<<(unsigned)p.ntiles, kSortThreads, sm32, st>>>(a);
-  a.pass = 1;
-  count_launch();
-  if (nk == 6) rindex_sort6_kernel<uint64_t><<<(unsigned)p.ntiles, kSortThreads, sm64, st>>>(a);
-  else rindex_sort_kernel<uint64_t><<<(unsigned)p.ntiles, kSortThreads, sm64, st>>>(a);
+  if (nk == 6) {
+    a.pass = 0;
+    count_launch();
+    rindex_sort6_kernel<uint32_t><<<(unsigned)p.ntiles, kSortThreads, sm32, st>>>(a);
+    a.pass = 2;  // tiles whose 6-field keys exceed 32 bits
+    count_launch();
+    rindex_sort6_kernel<uint64_t><<<(unsigned)p.ntiles, kSortThreads, sm64, st>>>(a);
+  } else {
+    // compact-key sort; tiles with a segment of more than 16 varying key
+    // bits (flag 1) are redone by the general kernel
+    a.pass = 0;
+    count_launch();
+    rindex_csort_kernel<<<(unsigned)p.ntiles, kSortThreads, smc, st>>>(a);
+    a.pass = 1;
+    count_launch();
+    rindex_sort_kernel<uint32_t><<<(unsigned)p.ntiles, kSortThreads, sm32, st>>>(a);
+  }
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
 

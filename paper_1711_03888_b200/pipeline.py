@@ -371,14 +371,21 @@ def device_fields(snapshot: ParticleSnapshot):
                 f = f.clone()
             out.append(f)
         return out, None
+    from . import hostio
     stride = _align_n(n)
     buf = torch.empty(6 * max(stride, 1), dtype=torch.float32, device="cuda")
     out = []
     for i, f in enumerate(fs):
         dst = buf[i * stride:i * stride + n]
         if n:
-            src = f if _is_tensor(f) else torch.from_numpy(f)
-            dst.copy_(src, non_blocking=True)
+            if _is_tensor(f) and f.is_cuda:
+                dst.copy_(f)
+            else:
+                # pinned sources DMA directly; pageable ones are staged through
+                # the pinned chunks (the CPU copy of one chunk overlaps the DMA
+                # of the previous) instead of a synchronous pageable copy
+                src = f if _is_tensor(f) else np.ascontiguousarray(f, np.float32)
+                hostio.to_device(src, dst.view(torch.uint8))
         out.append(dst)
     return out, buf
 
