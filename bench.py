@@ -334,11 +334,11 @@ def run_b200(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e2 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        # global bounds (collective 1), shard compress, archive sizes (collective 2),
-        # then the payload CRC-64s (on device; the reference's compress rate
-        # includes its CRC serialisation, metrics.py:178-180)
+        # global bounds (collective 1), shard compress (which queues the
+        # payload CRC-64s on device: the reference's compress rate includes
+        # its CRC serialisation, metrics.py:178-180), archive sizes
+        # (collective 2)
         sr = shard.compress_shard(snap, args.mode, bounds)
-        nio._payload_crcs(sr.result.archive)
         e1.record()
         out = nbz.decompress(sr.result.archive, device=True)
         e2.record()

@@ -111,10 +111,18 @@ typedef struct nbzg_compress_args {
                              caller), so bounds resolve as on the whole snapshot
                              (model.py:104-125) and K1 is not run twice */
   float h_minmax[12];     /* phase 2: (lo, hi) of field 0..5, host values */
+  int32_t fmt;            /* 0 or 2: v2 SZ_DQ streams (chunk-parallel, container 2);
+                             1: reference-readable SZ_FIELD streams (container 1) -- the
+                             reference's exact chain restarted by a forced escape every
+                             16384 values; sz-lv / sz-lv-prx only.
+                             Workspace: nbzg_compress_workspace_size_fmt(..., 1) */
+  int32_t pad3;
 } nbzg_compress_args;
 
 size_t nbzg_compress_workspace_size(int64_t n, int32_t sorted, int64_t interval_count,
                                     int64_t segment_size);
+size_t nbzg_compress_workspace_size_fmt(int64_t n, int32_t sorted, int64_t interval_count,
+                                        int64_t segment_size, int32_t fmt);
 size_t nbzg_compress_arena_bound(int64_t n, int64_t interval_count);
 int nbzg_compress(const nbzg_compress_args *args, void *stream);
 

@@ -348,11 +348,13 @@ _FIXED = struct.Struct("<4sHBBQIIBBH")
 def serialize(mode: str, n: int, interval_count: int, segment_size: int, ignored_groups: int,
               bounds, mask: int, constants, seg_bits, payloads, fmt: int,
               variant: int = 0) -> bytes:
-    """Container restatement of io.py:105-125; fmt 2 writes version 2 and kind 3."""
+    """Container restatement of io.py:105-125; fmt 2 writes version 2 and kind 3
+    (fmt 3, the chunk-restart chain, is a version-1 container of SZ_FIELD streams)."""
     sorted_mode = mode == "sz-lv-prx"
     variant_uid = variant if (sorted_mode and n > 0) else 255
     head = bytearray()
-    head += _FIXED.pack(b"NBZ1", fmt, MODE_UIDS[mode], variant_uid, n, interval_count,
+    head += _FIXED.pack(b"NBZ1", 1 if fmt == 3 else fmt, MODE_UIDS[mode], variant_uid, n,
+                        interval_count,
                         segment_size, ignored_groups, mask, 0)
     head += struct.pack("<6d", *bounds)
     head += struct.pack("<6f", *constants)
@@ -360,7 +362,7 @@ def serialize(mode: str, n: int, interval_count: int, segment_size: int, ignored
     segs = bytes(np.asarray(seg_bits, np.uint8)) if (sorted_mode and n > 0) else b""
     head += struct.pack("<II", len(segs), len(streams))
     head += segs
-    kind = KIND_SZ_FIELD if fmt == 1 else KIND_SZ_DQ
+    kind = KIND_SZ_DQ if fmt == 2 else KIND_SZ_FIELD
     for f, p in streams:
         head += struct.pack("<BBHQQ", kind, f, 0, len(p), crc64(p))
     head += struct.pack("<Q", crc64(bytes(head)))
@@ -390,7 +392,9 @@ def compress(fields: Sequence[np.ndarray], mode: str, kinds, values, interval_co
              segment_size: int = 16384, ignored_groups: int = 6, fmt: int = 1,
              variant: str = "coord") -> dict:
     """Whole-snapshot oracle compress.  fmt 1 reproduces the reference's v1
-    archive byte-for-byte; fmt 2 is the dual-quant v2 archive the GPU emits."""
+    archive byte-for-byte; fmt 2 is the dual-quant v2 archive the GPU emits;
+    fmt 3 is the reference-readable v1 archive the GPU emits on request
+    (the reference's chain restarted by a forced escape every 16384 values)."""
     f32 = [_c(a, np.float32) for a in fields]
     n = int(f32[0].size)
     if isinstance(kinds, str):

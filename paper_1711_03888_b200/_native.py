@@ -43,6 +43,7 @@ EXPORTED = (
     "nbzg_trace_read", "nbzg_cpc_workspace_size", "nbzg_cpc_plan", "nbzg_cpc_pack",
     "nbzg_cpc_decode", "nbzg_cpc_decode_workspace_size", "nbzg_huff_decode",
     "nbzg_deinterleave3", "nbzg_crc64_many", "nbzg_crc64_many_workspace_size",
+    "nbzg_compress_workspace_size_fmt",
 )
 
 
@@ -80,7 +81,7 @@ class CompressArgs(ctypes.Structure):
                 ("workspace_bytes", c_sz), ("arena", c_p), ("arena_bytes", c_sz),
                 ("meta", c_p), ("seg_bits", c_p), ("perm", c_p), ("predictor", c_i32),
                 ("cpc", c_i32), ("seg_minima", c_p), ("sz_skip", c_u32), ("phase", c_i32),
-                ("h_minmax", c_f * 12)]
+                ("h_minmax", c_f * 12), ("fmt", c_i32), ("pad3", c_i32)]
 
 
 class CpcMeta(ctypes.Structure):
@@ -112,6 +113,7 @@ class DecompressArgs(ctypes.Structure):
 _SIGS = {
     "nbzg_compress": (ctypes.c_int, [c_p, c_p]),
     "nbzg_compress_workspace_size": (c_sz, [c_i64, c_i32, c_i64, c_i64]),
+    "nbzg_compress_workspace_size_fmt": (c_sz, [c_i64, c_i32, c_i64, c_i64, c_i32]),
     "nbzg_compress_arena_bound": (c_sz, [c_i64, c_i64]),
     "nbzg_decompress": (ctypes.c_int, [c_p, c_p]),
     "nbzg_decompress_workspace_size": (c_sz, [c_i64, c_i64, c_i32]),

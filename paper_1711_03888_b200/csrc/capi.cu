@@ -25,7 +25,7 @@ int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uin
                          uint64_t* lut, uint32_t* scratch, nbzg_meta* meta, int64_t n,
                          int64_t nchunks, int single_field, cudaStream_t st,
                          uint32_t* twin = nullptr, uint8_t* tlen8 = nullptr, int f0 = 0,
-                         int nf = 6);
+                         int nf = 6, int v1 = 0);
 int launch_huffman_lengths(const uint32_t* counts, int64_t k, uint8_t* lengths, uint32_t* scr,
                            uint32_t* status, cudaStream_t st);
 int launch_huff_encode_raw(const uint16_t* syms, int64_t n, const uint64_t* lut, uint8_t* out,
@@ -118,8 +118,9 @@ void smem_attr(const void* func, int bytes) {
 
 static inline size_t al256(size_t v) { return (v + 255) & ~size_t(255); }
 
-void plan_shape(Plan& p, int64_t n, int sorted, int64_t ic, int64_t S) {
+void plan_shape(Plan& p, int64_t n, int sorted, int64_t ic, int64_t S, int fmt) {
   p.n = n;
+  p.fmt = fmt;
   p.sorted = sorted;
   p.S = S;
   if (sorted) {
@@ -131,8 +132,11 @@ void plan_shape(Plan& p, int64_t n, int sorted, int64_t ic, int64_t S) {
   p.ntiles = (n + p.tile - 1) / p.tile;
   p.nseg = sorted ? (n + S - 1) / S : 0;
   p.nchunks = (n + kChunk - 1) / kChunk;
-  p.nbins = ic;
+  p.nbins = fmt == 1 ? ic + 1 : ic;  // v1 codes span [0, 2 half]; v2 [0, 2 half - 1]
   p.half = (int)(ic / 2);
+  p.v1_stride = (n + 3) & ~int64_t(3);
+  // Huffman's mean length is below log2(k) + 1 <= 18 bits for k <= 2^16 + 1
+  p.v1_wstride = fmt == 1 ? (int64_t)((n * 18 + 31) / 32 + 16) : 0;
 }
 
 size_t plan_workspace(Plan& p, void* base) {
@@ -160,6 +164,17 @@ size_t plan_workspace(Plan& p, void* base) {
   p.counters = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 64));
   p.tile_flags = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * (p.ntiles + 1)));
   p.seg_mm = reinterpret_cast<float*>(take(sizeof(float) * 6 * ((size_t)p.nseg + 1)));
+  if (p.fmt == 1) {
+    const size_t xs = (size_t)p.v1_stride, nc = (size_t)p.nchunks;
+    p.v1_xsort = p.sorted ? reinterpret_cast<float*>(take(sizeof(float) * 6 * xs)) : nullptr;
+    p.v1_codes = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 6 * xs));
+    p.v1_esc = reinterpret_cast<float*>(take(sizeof(float) * 6 * xs));
+    p.v1_esc_cnt = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 6 * nc));
+    p.v1_cbits = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 6 * nc));
+    p.v1_boff = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 6 * (nc + 1)));
+    p.v1_eoff = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 6 * (nc + 1)));
+    p.v1_words = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 6 * (size_t)p.v1_wstride));
+  }
   return off;
 }
 
@@ -180,45 +195,56 @@ __global__ void ord_decode_kernel(uint32_t* m) {
 
 static int cuda_status() { return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR; }
 
-// The SZ stages in two field groups (coordinates, velocities) so the
-// codebook -- six single-CTA Huffman builds that leave the rest of the GPU
-// idle -- overlaps real work: group A's codebook runs beside group B's
-// quantisation, group B's codebook beside group A's encoding.
-//   st: Q(A) -> Q(B) -> CB(B) -> [wait layout A] layout(B) -> E(B) -> [wait E(A)]
-//   sd:   [wait Q(A)] CB(A) -> layout(A) -> E(A)
-// A side stream and three events per call (no shared mutable state).
+#ifndef NBZG_SZ_GROUPS
+#define NBZG_SZ_GROUPS 2
+#endif
+// The SZ stages in G field groups so the codebook -- single-CTA Huffman
+// builds that leave the rest of the GPU idle -- and the encoding of one
+// group overlap the quantisation of the next.  All quantise launches go on
+// the caller's stream; group g's codebook, layout and encode follow on its
+// own side stream as soon as Q(g) is done (layouts in group order: each
+// appends to the arena after the previous group's payloads); the caller's
+// stream then waits for every group.  Side streams and events are per call
+// (no shared mutable state).
 static int sz_stages_split(Plan& p, cudaStream_t st) {
-  cudaStream_t sd;
-  cudaEvent_t eqa, ela, eea;
-  if (cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking) != cudaSuccess) return NBZG_CUDA_ERROR;
-  cudaEventCreateWithFlags(&eqa, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&ela, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&eea, cudaEventDisableTiming);
+  constexpr int G = NBZG_SZ_GROUPS;
+  static_assert(G == 2 || G == 3 || G == 6, "field groups: 2, 3 or 6");
+  constexpr int per = 6 / G;
+  cudaStream_t sd[G];
+  cudaEvent_t eq[G], el[G], ee[G];
+  int made = 0;
   int rc = NBZG_OK;
-  do {
-    if ((rc = launch_quantize(p, st, 0, 3))) break;
-    cudaEventRecord(eqa, st);
-    if ((rc = launch_quantize(p, st, 3, 3))) break;
-    trace_mark("quantize", st);
-    cudaStreamWaitEvent(sd, eqa, 0);
-    if ((rc = launch_codebook(p, sd, 0, 3))) break;
-    if ((rc = launch_layout(p, sd, 0, 3))) break;
-    cudaEventRecord(ela, sd);
-    if ((rc = launch_encode(p, sd, 0, 3))) break;
-    cudaEventRecord(eea, sd);
-    if ((rc = launch_codebook(p, st, 3, 3))) break;
-    trace_mark("codebook", st);
-    cudaStreamWaitEvent(st, ela, 0);
-    if ((rc = launch_layout(p, st, 3, 3))) break;
-    trace_mark("layout", st);
-    if ((rc = launch_encode(p, st, 3, 3))) break;
-    cudaStreamWaitEvent(st, eea, 0);
-    trace_mark("encode", st);
-  } while (0);
-  cudaEventDestroy(eqa);
-  cudaEventDestroy(ela);
-  cudaEventDestroy(eea);
-  cudaStreamDestroy(sd);
+  for (; made < G; made++) {
+    if (cudaStreamCreateWithFlags(&sd[made], cudaStreamNonBlocking) != cudaSuccess) break;
+    cudaEventCreateWithFlags(&eq[made], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&el[made], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ee[made], cudaEventDisableTiming);
+  }
+  if (made < G) rc = NBZG_CUDA_ERROR;
+  for (int g = 0; g < G && !rc; g++) {
+    if ((rc = launch_quantize(p, st, g * per, per))) break;
+    cudaEventRecord(eq[g], st);
+  }
+  if (!rc) trace_mark("quantize", st);
+  for (int g = 0; g < G && !rc; g++) {
+    cudaStreamWaitEvent(sd[g], eq[g], 0);
+    if ((rc = launch_codebook(p, sd[g], g * per, per))) break;
+    if (g > 0) cudaStreamWaitEvent(sd[g], el[g - 1], 0);
+    if ((rc = launch_layout(p, sd[g], g * per, per))) break;
+    cudaEventRecord(el[g], sd[g]);
+    if ((rc = launch_encode(p, sd[g], g * per, per))) break;
+    cudaEventRecord(ee[g], sd[g]);
+  }
+  for (int g = 0; g < made; g++) {
+    if (!rc) cudaStreamWaitEvent(st, ee[g], 0);
+  }
+  if (!rc) trace_mark("encode", st);
+  for (int g = 0; g < made; g++) {
+    cudaEventDestroy(eq[g]);
+    cudaEventDestroy(el[g]);
+    cudaEventDestroy(ee[g]);
+    cudaStreamDestroy(sd[g]);
+  }
   return rc ? rc : cuda_status();
 }
 
@@ -256,8 +282,14 @@ int nbzg_device_sm_count(void) { return sm_count(); }
 
 size_t nbzg_compress_workspace_size(int64_t n, int32_t sorted, int64_t interval_count,
                                     int64_t segment_size) {
+  return nbzg_compress_workspace_size_fmt(n, sorted, interval_count, segment_size, 2);
+}
+
+size_t nbzg_compress_workspace_size_fmt(int64_t n, int32_t sorted, int64_t interval_count,
+                                        int64_t segment_size, int32_t fmt) {
   Plan p;
-  plan_shape(p, n, sorted, interval_count, segment_size < 1 ? 1 : segment_size);
+  plan_shape(p, n, sorted, interval_count, segment_size < 1 ? 1 : segment_size,
+             fmt == 1 ? 1 : 2);
   return plan_workspace(p, nullptr);
 }
 
@@ -287,8 +319,11 @@ int nbzg_compress(const nbzg_compress_args* a, void* stream) {
     if (a->bound_kind[f] != 0 && a->bound_kind[f] != 1) return NBZG_BAD_ARG;
     if (!(a->bound_value[f] > 0)) return NBZG_BAD_ARG;
   }
+  const int fmt = a->fmt == 0 ? 2 : a->fmt;
+  if (fmt != 1 && fmt != 2) return NBZG_BAD_ARG;
+  if (fmt == 1 && (a->predictor != 0 || a->cpc != 0)) return NBZG_UNSUPPORTED;
   Plan p;
-  plan_shape(p, a->n, a->sorted, a->interval_count, a->segment_size);
+  plan_shape(p, a->n, a->sorted, a->interval_count, a->segment_size, fmt);
   p.ig = a->ignored_groups;
   if (a->rindex_variant < 0 || a->rindex_variant > 2) return NBZG_BAD_ARG;
   p.variant = a->rindex_variant;
@@ -349,6 +384,7 @@ int nbzg_compress(const nbzg_compress_args* a, void* stream) {
   }
   NvtxScope range_sz("K3-K5 quantize / codebook / encode");
   if (p.sz_skip && (rc = launch_sz_skip(p, st))) return rc;
+  if (p.fmt == 1) return launch_v1(p, st);
   if (p.predictor == 0 && encode_uses_tpc(p)) return sz_stages_split(p, st);
   if ((rc = launch_quantize(p, st))) return rc;
   trace_mark("quantize", st);

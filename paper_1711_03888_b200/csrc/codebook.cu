@@ -36,6 +36,7 @@ struct CBArgs {
                       // half+1-kEncWin/2+i -> MSB-aligned word | len (len <= 26, else 0)
   uint8_t* tlen8;     // [6][nbins] code length by symbol (may be null)
   int f0;             // first field of this launch (CTA b -> field f0 + b)
+  int v1;             // payload sizes of a v1 SZ_FIELD stream (escapes after the bits)
 };
 
 NBZG_DEV void bitonic_sort_u64(uint64_t* a, int N) {
@@ -175,6 +176,10 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
   }
   __syncthreads();
   if (k == 0) return;
+  if (k > 65536) {  // ranks are 16-bit (only a v1 alphabet of 2^16 + 1 symbols can get here)
+    if (tid == 0) atomicCAS(&a.meta->status, 0u, (uint32_t)NBZG_UNSUPPORTED);
+    return;
+  }
 
   // memory for the merge: shared for k <= 16384, else global scratch.
   // layout (N = pow2 >= k): keys u64[N] | L u32[N] | order u16[N]; after the
@@ -278,21 +283,30 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
   unsigned long long tbits;
   block_excl_scan<unsigned long long>(tb, scan_u64, &tbits);
   if (tid == 0) {
-    tbits += 32ull * fm.n_esc;  // v2: escape values ride inline in the bitstream
-    fm.total_bits = tbits;
-    uint64_t table_end = 8 + 5 * (uint64_t)k;
-    fm.index_off = table_end + 8;
-    fm.bits_off = (fm.index_off + 4 * (uint64_t)a.nchunks + 3) & ~3ull;
-    fm.esc_off = fm.bits_off + 4 * ((tbits + 31) / 32);  // == payload end (no escape area)
-    fm.payload_len = fm.esc_off;
+    const uint64_t table_end = 8 + 5 * (uint64_t)k;
+    if (a.v1) {  // pipeline.py:188-200: table | u64 bits | bytes | f32 escapes
+      fm.total_bits = tbits;
+      fm.index_off = 0;
+      fm.bits_off = table_end + 8;
+      fm.esc_off = fm.bits_off + (tbits + 7) / 8;
+      fm.payload_len = fm.esc_off + 4 * fm.n_esc;
+    } else {
+      tbits += 32ull * fm.n_esc;  // v2: escape values ride inline in the bitstream
+      fm.total_bits = tbits;
+      fm.index_off = table_end + 8;
+      fm.bits_off = (fm.index_off + 4 * (uint64_t)a.nchunks + 3) & ~3ull;
+      fm.esc_off = fm.bits_off + 4 * ((tbits + 31) / 32);  // == payload end (no escape area)
+      fm.payload_len = fm.esc_off;
+    }
   }
 }
 
 int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uint8_t* len,
                          uint64_t* lut, uint32_t* scratch, nbzg_meta* meta, int64_t n,
                          int64_t nchunks, int single_field, cudaStream_t st,
-                         uint32_t* twin, uint8_t* tlen8, int f0, int nf) {
-  CBArgs a{hist, nbins, sym, len, lut, scratch, meta, n, nchunks, single_field, twin, tlen8, f0};
+                         uint32_t* twin, uint8_t* tlen8, int f0, int nf, int v1) {
+  CBArgs a{hist, nbins, sym, len, lut, scratch, meta, n, nchunks, single_field, twin, tlen8, f0,
+           v1};
   size_t sm = 14 * (size_t)kCBSmemK;  // keys u64 | L u32 | order u16
   smem_attr((const void*)codebook_kernel, (int)sm);
   count_launch();
@@ -303,7 +317,8 @@ int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uin
 int launch_codebook(const Plan& p, cudaStream_t st, int f0, int nf) {
   if (p.n == 0) return NBZG_OK;
   return launch_codebook_impl(p.hist, p.nbins, p.cb_sym, p.cb_len, p.lut, p.cb_scratch, p.meta,
-                              p.n, p.nchunks, -1, st, p.enc_win, p.enc_len8, f0, nf);
+                              p.n, p.nchunks, -1, st, p.fmt == 1 ? nullptr : p.enc_win,
+                              p.enc_len8, f0, nf, p.fmt == 1 ? 1 : 0);
 }
 
 // ---- parity hook: K.huffman_lengths on sorted counts (one CTA)

@@ -1160,6 +1160,7 @@ struct LvCtx {
   double twob;
   uint32_t vmax, wmax, r0m1, r0, sh2, lt_s;
   uint32_t rlim, m2;  // table index of window v: hi(min(v, rlim) * 2^15) + hi((v - min) * m2)
+  uint32_t p15;       // first long-code entry (= r0 >> 17 when long codes exist)
   int lmin, max_len, bias;
 };
 // one chunk being decoded
@@ -1201,8 +1202,12 @@ NBZG_DEV void lv_fill_safe(const LvCtx& X, LvChunk& S) {
 // IMAD.HI): min(v, r0) >> 17 is the prefix of a short code and P for a long
 // one; (v - min(v, r0)) >> sh2 is 0 for a short code.
 NBZG_DEV uint32_t lv_index(const LvCtx& X, uint32_t v) {
+#ifdef NBZG_DEC_LVINDEX  // (measured slower: the IMAD.HI chain lengthens the critical path)
   const uint32_t m = min(v, X.rlim);
   return __umulhi(m, 1u << kTpcBits) + __umulhi(v - m, X.m2);
+#else
+  return v > X.r0m1 ? X.p15 + ((v - X.r0) >> X.sh2) : v >> (32 - kTpcBits);
+#endif
 }
 // canonical decode of the symbol at v (any length <= 32)
 NBZG_DEV int32_t lv_resolve(const LvCtx& X, LvChunk& S, uint32_t v) {
@@ -1350,7 +1355,7 @@ __global__ void __launch_bounds__(kLvMaxThreads, 1) decode_lv_kernel(DArgs a) {
     const int32_t* gl = a.lut2 + (size_t)fi * kTpcTab;
     for (uint32_t i = tid; i < P15; i += nthr) LT[i] = __ldg(gl + i);
     for (uint32_t i = tid; i < n2; i += nthr) LT[P15 + i] = __ldg(gl + (1 << kTpcBits) + i);
-    if (tid == 0 && has_long && n2 == 0) LT[P15] = 64;
+    if (tid < 2 && has_long && n2 == 0) LT[P15 + tid] = 64;  // (v - r0) >> 31 is 0 or 1
   }
   __syncthreads();
   if (tid < 64) {
@@ -1393,6 +1398,7 @@ __global__ void __launch_bounds__(kLvMaxThreads, 1) decode_lv_kernel(DArgs a) {
   X.r0 = X.r0m1 + 1;
   X.sh2 = n2 ? 32u - P.t2_w : 31u;
   X.rlim = has_long ? (uint32_t)P.t2_r0 : 0xffffffffu;
+  X.p15 = P15;
   X.m2 = n2 ? (1u << P.t2_w) : 0u;
   X.lmin = n2 ? (int)P.t2_w : kTpcBits;  // longer codes: canonical search
   X.lt_s = (uint32_t)__cvta_generic_to_shared(LT);

@@ -24,6 +24,7 @@ struct Plan {
   int predictor = 0;    // 0 last value, 1 LCF (sz-lcf)
   int cpc = 0;          // 0; 1 sz-cpc2000; 2 cpc2000 (full keys, no clamp, minima)
   uint32_t sz_skip = 0; // fields without an SZ stream (CPC modes)
+  int fmt = 2;          // 2: v2 SZ_DQ streams; 1: reference-readable SZ_FIELD streams (v1.cu)
   int64_t* minima = nullptr;  // 3 per segment (CPC)
   const float* f[6] = {};
   int bound_kind[6] = {};
@@ -48,6 +49,17 @@ struct Plan {
   uint32_t* tile_flags = nullptr;  // ntiles (u64-key fallback tiles)
   uint8_t* arena = nullptr;
   size_t arena_bytes = 0;
+  // fmt 1 (v1.cu) buffers
+  int64_t v1_stride = 0;        // per-field stride of the arrays below
+  float* v1_xsort = nullptr;    // [6][stride] fields in sorted order (sorted modes)
+  uint32_t* v1_codes = nullptr; // [6][stride]
+  float* v1_esc = nullptr;      // [6][stride] chunk c's escapes from c * 16384
+  uint32_t* v1_esc_cnt = nullptr;  // [6][nchunks]
+  uint32_t* v1_cbits = nullptr;    // [6][nchunks]
+  uint64_t* v1_boff = nullptr;     // [6][nchunks + 1]
+  uint64_t* v1_eoff = nullptr;     // [6][nchunks + 1]
+  uint32_t* v1_words = nullptr;    // [6][v1_wstride]
+  int64_t v1_wstride = 0;
 };
 
 // one field of a decompress call (decode.cu)
@@ -61,7 +73,8 @@ struct DField {
 };
 
 size_t plan_workspace(Plan& p, void* base);  // carve (base may be null: size only)
-void plan_shape(Plan& p, int64_t n, int sorted, int64_t interval_count, int64_t segment_size);
+void plan_shape(Plan& p, int64_t n, int sorted, int64_t interval_count, int64_t segment_size,
+                int fmt = 2);
 
 // kernel launchers (each enqueues on `st`)
 int launch_minmax6(const float* const* f, int64_t n, uint32_t* minmax12, cudaStream_t st);
@@ -75,6 +88,7 @@ int launch_layout(const Plan& p, cudaStream_t st, int f0 = 0, int nf = 6);
 int launch_encode(const Plan& p, cudaStream_t st, int f0 = 0, int nf = 6);
 bool encode_uses_tpc(const Plan& p);
 int launch_sz_skip(const Plan& p, cudaStream_t st);
+int launch_v1(const Plan& p, cudaStream_t st);  // fmt 1: all SZ stages (v1.cu)
 
 int sm_count();
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel,

@@ -498,6 +498,13 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_sort6_kernel(RArgs a) 
 // 2 (eb 1e-4) the masked keys carry 21 bits but only ~9 vary: one radix pass
 // with 2^cw bins sorts the segment.  Segments whose compacted key exceeds 16
 // bits are flagged for the general kernel (rindex_sort_kernel, pass 1).
+// rint(f64(x) / 2b) by the exact division (quantize.py:122): the near-tie
+// fallback of the compact-key sort, kept out of line (one copy of the
+// division code, executed only by the lanes that need it)
+__device__ __noinline__ int32_t exact_index(float x, const nbzg_field_meta* m) {
+  return m->is_const ? 0 : (int32_t)rint(__ddiv_rn((double)x, m->twob));
+}
+
 constexpr int kCsMaxBits = 16;  // compacted key bits handled here (u16 keys)
 constexpr int kCsOneBits = 10;  // <= this: a single pass with 2^cw bins
 constexpr int kCsJ = kTileMax / kSortThreads;  // elements per thread (32)
@@ -514,7 +521,7 @@ struct CsSeg {
 // src = pos (FIRST) or perm[pos]; output perm[dst] = src, in place.
 // Values in perm are tile-local (segment start lo + segment index).
 template <bool FIRST>
-__device__ __noinline__ void cs_pass(const uint16_t* keys, uint16_t* perm, int lo, int m, int sh, int D,
+NBZG_DEV void cs_pass(const uint16_t* keys, uint16_t* perm, int lo, int m, int sh, int D,
                       uint16_t* whist, uint32_t* scan_tmp) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nb = 1 << D;
@@ -587,6 +594,13 @@ __device__ __noinline__ void cs_pass(const uint16_t* keys, uint16_t* perm, int l
   __syncthreads();
 }
 
+// the second pass of a two-pass segment (rare: ~5% of config-2 segments),
+// out of line so its 32-register packed state does not weigh on the kernel
+__device__ __noinline__ void cs_pass_next(const uint16_t* keys, uint16_t* perm, int lo, int m,
+                                          int sh, int D, uint16_t* whist, uint32_t* scan_tmp) {
+  cs_pass<false>(keys, perm, lo, m, sh, D, whist, scan_tmp);
+}
+
 __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) {
   extern __shared__ __align__(16) uint8_t csm[];
   uint16_t* keys = reinterpret_cast<uint16_t*>(csm);          // [kTileMax] segment-local
@@ -597,11 +611,28 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
   __shared__ float red[2][3][kSortWarps];
   __shared__ CsSeg sp;
 
-  const int64_t t = blockIdx.x;
+  const nbzg_field_meta* fm = a.meta->f + a.fbase;
+  // persistent CTAs (2 per SM): while a tile is sorted, the next tile's
+  // coordinates are already streaming into L2 (one bulk prefetch per
+  // coordinate), so the key generation's loads hit L2 instead of waiting on
+  // DRAM with no other work to overlap
+  auto prefetch = [&](int64_t tt) {
+    if (threadIdx.x != 0 || tt >= a.ntiles) return;
+    const int64_t p0 = tt * a.tile;
+    const uint32_t bytes = (uint32_t)(min(a.tile, a.n - p0) * 4) & ~15u;
+    if (!bytes) return;
+    for (int c = 0; c < 3; c++) {
+      const float* src = a.x[c] + p0;
+      if (reinterpret_cast<uintptr_t>(src) & 15) continue;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+    }
+  };
+  prefetch(blockIdx.x);
+  for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+  prefetch(t + gridDim.x);
   const int64_t t0 = t * a.tile;
   const int64_t t1 = min(a.n, t0 + a.tile);
   const int mt = (int)(t1 - t0);
-  const nbzg_field_meta* fm = a.meta->f + a.fbase;
   bool flagged = false;
 
   for (int64_t s0 = t0; s0 < t1; s0 += a.S) {
@@ -722,75 +753,118 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
       lut[tt][b][v] = out;
     }
     __syncthreads();
-    // ---- 3. compacted keys (exact integerisation: FP32 under a segment-wide
-    // margin, FP64 division otherwise -- same argument as gen_keys)
+    // ---- 3. compacted keys.  Exact integerisation rint(f64(x) / 2b)
+    // (quantize.py:117-128) from the FP64 product t = x * (1/2b): |t - x/2b|
+    // <= |t| 2^-51, so unless t is within tmax 2^-50 of a half-integer,
+    // rint(t) equals the reference's rint of the rounded quotient; those
+    // near-ties (probability ~2^-40) take the exact division out of line.
+    // rint(t) = low word of t + 1.5 * 2^52 (|t| < 2^31).
     {
       const int shift = sp.shift;
       const int32_t m0 = (int32_t)sp.mn[0], m1 = (int32_t)sp.mn[1], m2 = (int32_t)sp.mn[2];
-      float cm[3];
+      const uint32_t lut_s = sh_addr(&lut[0][0][0]);
+      const double iv0 = fm[0].inv, iv1 = fm[1].inv, iv2 = fm[2].inv;
       bool small = true;
+      double tie = 0.0;
 #pragma unroll
       for (int c = 0; c < 3; c++) {
-        const float tmax = sp.amax[c] * fm[c].inv32;
-        small &= tmax < 4194304.0f;
-        cm[c] = 0.5f - __fmaf_ru(tmax, 2.384185791015625e-07f, 9.5367431640625e-07f);
+        const double tmax = (double)sp.amax[c] * fm[c].inv;
+        small &= tmax < 1073741824.0 || fm[c].is_const;  // |k| < 2^30
+        tie = fmax(tie, tmax * 8.881784197001252e-16);  // 2^-50
       }
-      const uint32_t lut_s = sh_addr(&lut[0][0][0]);
-      auto key_of = [&](float x0, float x1, float x2) -> uint32_t {
-        const float xv[3] = {x0, x1, x2};
-        const int32_t mv[3] = {m0, m1, m2};
-        uint32_t key = 0;
-#pragma unroll
-        for (int c = 0; c < 3; c++) {
-          uint32_t u;
-          if (small) {
-            const float tt = xv[c] * fm[c].inv32;
-            const float r = tt + 12582912.0f;
-            const float d = tt - (r - 12582912.0f);
-            int32_t k = __float_as_int(r) - 0x4B400000;
-            if (!(fabsf(d) < cm[c])) k = (int32_t)rint(__ddiv_rn((double)xv[c], fm[c].twob));
-            u = (uint32_t)(k - mv[c]) >> shift;
-          } else {
-            const int64_t iv = fm[c].is_const ? 0 : integerize1(xv[c], fm[c]);
-            u = (uint32_t)((uint64_t)(iv - sp.mn[c]) >> shift);
-          }
-          const uint32_t tb = lut_s + 4u * (uint32_t)(c * 3 * 256);
-          key |= lds_u32(tb + 4u * (u & 255u));
-          if (nbyte > 1) key |= lds_u32(tb + 4u * (256u + ((u >> 8) & 255u)));
-          if (nbyte > 2) key |= lds_u32(tb + 4u * (512u + ((u >> 16) & 255u)));
-        }
+      const double cut = 0.5 - tie;
+      // one component: lattice index minus the segment minimum (near-ties
+      // flagged in `slow`, fixed after a warp vote)
+      auto comp = [&](float x, double inv, int32_t mn, uint32_t& slow, int bit) -> int32_t {
+        const double t = __dmul_rn((double)x, inv);
+        const double r = __dadd_rn(t, 6755399441055744.0);
+        if (!(fabs(__dsub_rn(t, __dsub_rn(r, 6755399441055744.0))) < cut)) slow |= 1u << bit;
+        return __double2loint(r) - mn;
+      };
+      auto lut3 = [&](uint32_t u0, uint32_t u1, uint32_t u2) -> uint32_t {
+        uint32_t key = lds_u32(lut_s + 4u * (u0 & 255u)) | lds_u32(lut_s + 4u * (768u + (u1 & 255u))) |
+                       lds_u32(lut_s + 4u * (1536u + (u2 & 255u)));
+        if (nbyte > 1)
+          key |= lds_u32(lut_s + 4u * (256u + ((u0 >> 8) & 255u))) |
+                 lds_u32(lut_s + 4u * (1024u + ((u1 >> 8) & 255u))) |
+                 lds_u32(lut_s + 4u * (1792u + ((u2 >> 8) & 255u)));
+        if (nbyte > 2)
+          key |= lds_u32(lut_s + 4u * (512u + ((u0 >> 16) & 255u))) |
+                 lds_u32(lut_s + 4u * (1280u + ((u1 >> 16) & 255u))) |
+                 lds_u32(lut_s + 4u * (2048u + ((u2 >> 16) & 255u)));
         return key;
       };
+      auto key_of = [&](float x0, float x1, float x2) -> uint32_t {
+        uint32_t slow = 0;
+        int32_t d[3] = {comp(x0, iv0, m0, slow, 0), comp(x1, iv1, m1, slow, 1),
+                        comp(x2, iv2, m2, slow, 2)};
+        if (slow) {
+          const float xv[3] = {x0, x1, x2};
+          const int32_t mv[3] = {m0, m1, m2};
+#pragma unroll
+          for (int c = 0; c < 3; c++)
+            if (slow & (1u << c)) d[c] = exact_index(xv[c], fm + c) - mv[c];
+        }
+        return lut3((uint32_t)d[0] >> shift, (uint32_t)d[1] >> shift, (uint32_t)d[2] >> shift);
+      };
+      if (!small) {  // indices beyond 2^30: the general kernel redoes the tile
+        flagged = true;
+        continue;
+      }
       const int m4 = (s0 & 3) ? 0 : m >> 2;
       const float4* x4[3] = {reinterpret_cast<const float4*>(a.x[0] + s0),
                              reinterpret_cast<const float4*>(a.x[1] + s0),
                              reinterpret_cast<const float4*>(a.x[2] + s0)};
-#pragma unroll 2
       for (int v = threadIdx.x; v < m4; v += kSortThreads) {
         const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
-        const uint32_t k0 = key_of(q0.x, q1.x, q2.x), k1 = key_of(q0.y, q1.y, q2.y);
-        const uint32_t k2 = key_of(q0.z, q1.z, q2.z), k3 = key_of(q0.w, q1.w, q2.w);
-        *reinterpret_cast<uint2*>(keys + 4 * v) = make_uint2(k0 | (k1 << 16), k2 | (k3 << 16));
+        const float xv[12] = {q0.x, q1.x, q2.x, q0.y, q1.y, q2.y, q0.z, q1.z, q2.z, q0.w, q1.w, q2.w};
+        const double ivs[3] = {iv0, iv1, iv2};
+        const int32_t mvs[3] = {m0, m1, m2};
+        uint32_t slow = 0;
+        int32_t d[12];
+#pragma unroll
+        for (int e = 0; e < 12; e++) d[e] = comp(xv[e], ivs[e % 3], mvs[e % 3], slow, e);
+        if (__any_sync(0xffffffffu, slow != 0)) {  // near-ties: ~2^-40 per value
+#pragma unroll 1
+          for (uint32_t sl = slow; sl; sl &= sl - 1) {
+            const int e = __ffs(sl) - 1;
+            float x = xv[0];
+            int32_t mm = m0;
+#pragma unroll
+            for (int q = 0; q < 12; q++)
+              if (q == e) x = xv[q], mm = mvs[q % 3];
+            const int32_t de = exact_index(x, fm + e % 3) - mm;
+#pragma unroll
+            for (int q = 0; q < 12; q++)
+              if (q == e) d[q] = de;
+          }
+        }
+        uint32_t kk[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+          kk[j] = lut3((uint32_t)d[3 * j] >> shift, (uint32_t)d[3 * j + 1] >> shift,
+                       (uint32_t)d[3 * j + 2] >> shift);
+        *reinterpret_cast<uint2*>(keys + 4 * v) = make_uint2(kk[0] | (kk[1] << 16), kk[2] | (kk[3] << 16));
       }
       for (int i = 4 * m4 + threadIdx.x; i < m; i += kSortThreads)
         keys[i] = (uint16_t)key_of(a.x[0][s0 + i], a.x[1][s0 + i], a.x[2][s0 + i]);
     }
     __syncthreads();
     // ---- 4. stable LSD over cw bits, output into this segment's perm range
-    if (cw <= kCsOneBits) {
-      cs_pass<true>(keys, perm + lo, lo, m, 0, cw, whist, scan_tmp);
-    } else {
-      const int d1 = cw >> 1;
+    {
+      const int d1 = cw <= kCsOneBits ? cw : cw >> 1;  // one pass, or two balanced digits
       cs_pass<true>(keys, perm + lo, lo, m, 0, d1, whist, scan_tmp);
-      cs_pass<false>(keys, perm + lo, lo, m, d1, cw - d1, whist, scan_tmp);
+      if (cw > d1) cs_pass_next(keys, perm + lo, lo, m, d1, cw - d1, whist, scan_tmp);
     }
   }
   if (flagged) {
     if (threadIdx.x == 0) a.tile_flags[t] = 1;
-    return;
+  } else {
+    // ---- write the tile's permutation (coalesced)
+    for (int i = threadIdx.x; i < mt; i += kSortThreads) a.perm[t0 + i] = perm[i];
   }
-  // ---- write the tile's permutation (coalesced)
-  for (int i = threadIdx.x; i < mt; i += kSortThreads) a.perm[t0 + i] = perm[i];
+  __syncthreads();  // perm is reused by the next tile
+  }
 }
 
 int launch_rindex_sort(const Plan& p, cudaStream_t st) {
@@ -833,7 +907,8 @@ int launch_rindex_sort(const Plan& p, cudaStream_t st) {
     // bits (flag 1) are redone by the general kernel
     a.pass = 0;
     count_launch();
-    rindex_csort_kernel<<<(unsigned)p.ntiles, kSortThreads, smc, st>>>(a);
+    const unsigned gcs = (unsigned)min(p.ntiles, (int64_t)2 * sm_count());
+    rindex_csort_kernel<<<gcs, kSortThreads, smc, st>>>(a);
     a.pass = 1;
     count_launch();
     rindex_sort_kernel<uint32_t><<<(unsigned)p.ntiles, kSortThreads, sm32, st>>>(a);

@@ -133,6 +133,7 @@ class _Device:
         self.kinds = list(kinds) + [int(StreamKind.RINDEX)] * (7 - len(kinds))
         self.keep = keep            # tensors that must outlive the archive
         self.bufs = bufs or {}
+        self.crc = None             # (slots, CUDA int64 CRC-64s) once queued
 
     def buf(self, slot: int):
         return self.bufs.get(slot, self.arena)
@@ -396,7 +397,7 @@ _VARIANT_CODE = {RIndexVariant.COORDINATE: 0, RIndexVariant.VELOCITY: 1,
 
 
 def compress(snapshot: ParticleSnapshot, mode, bounds: Bounds,
-             settings: Settings = DEFAULT_SETTINGS) -> CompressResult:
+             settings: Settings = DEFAULT_SETTINGS, *, version: int = 2) -> CompressResult:
     """pipeline.py:447-526 on the B200: SZ-LV (R-index off) and SZ-LV-PRX
     (R-index on).
 
@@ -404,20 +405,28 @@ def compress(snapshot: ParticleSnapshot, mode, bounds: Bounds,
     selector): compress with both modes and keep the smaller archive.  The
     result is an ordinary mode-1 or mode-2 archive, decodable by any reader;
     the choice is snapshot-level because all six fields share one
-    permutation (a per-field choice would need the permutation stored)."""
+    permutation (a per-field choice would need the permutation stored).
+
+    ``version=1`` (sz-lv / sz-lv-prx; an extension, not in the reference)
+    writes a reference-readable archive: container version 1 with SZ_FIELD
+    streams that the unmodified reference deserialises and decodes.  Its
+    chain is the reference's, restarted by a forced escape every 16384
+    values so the GPU runs it chunk-parallel; the
+    size cost is ~0.01%.  Decoding it needs the reference's sequential
+    chain (the compat decoder here), so the default stays version 2."""
     import torch
     if isinstance(mode, str) and mode == AUTO:
         fields, hold = device_fields(snapshot)  # one H2D for both attempts
         dsnap = ParticleSnapshot.__new__(ParticleSnapshot)
         for name, f in zip(FIELD_NAMES, fields):
             object.__setattr__(dsnap, name, f)
-        a = compress(dsnap, Mode.SZ_LV, bounds, settings)
-        b = compress(dsnap, Mode.SZ_LV_PRX, bounds, settings)
+        a = compress(dsnap, Mode.SZ_LV, bounds, settings, version=version)
+        b = compress(dsnap, Mode.SZ_LV_PRX, bounds, settings, version=version)
         best = b if b.archive.total_bytes() < a.archive.total_bytes() else a
         best.archive.device_output = bool(snapshot.on_device)
         del hold
         return best
-    return _CompressCall(snapshot, mode, bounds, settings).finish()
+    return _CompressCall(snapshot, mode, bounds, settings, version=version).finish()
 
 
 class _CompressCall:
@@ -428,11 +437,16 @@ class _CompressCall:
     resumes with them (phase 2) on the same workspace, so K1 runs once."""
 
     def __init__(self, snapshot: ParticleSnapshot, mode, bounds: Bounds,
-                 settings: Settings = DEFAULT_SETTINGS):
+                 settings: Settings = DEFAULT_SETTINGS, version: int = 2):
         import torch
         mode = _as_mode(mode)
         if mode not in GPU_MODES:
             raise ValidationError(f"mode {mode.value} is not implemented by the B200 path")
+        if version not in (1, 2):
+            raise ValidationError(f"archive version must be 1 or 2, got {version}")
+        if version == 1 and mode not in (Mode.SZ_LV, Mode.SZ_LV_PRX):
+            raise ValidationError("version=1 (reference-readable) archives: sz-lv / sz-lv-prx")
+        self.version = version
         specs = _specs(bounds)
         n = snapshot.n
         self.L = L = N.lib()
@@ -444,7 +458,7 @@ class _CompressCall:
         S = settings.segment_size
         if sorted_mode and S > 16384:
             raise ValidationError("the B200 path supports segment_size <= 16384")
-        ws_bytes = L.nbzg_compress_workspace_size(n, sorted_mode, ic, S)
+        ws_bytes = L.nbzg_compress_workspace_size_fmt(n, sorted_mode, ic, S, version)
         self.ws = N.workspace(ws_bytes)
         arena_bytes = L.nbzg_compress_arena_bound(n, ic)
         self.arena = torch.empty(arena_bytes, dtype=torch.uint8, device="cuda")
@@ -480,6 +494,7 @@ class _CompressCall:
         a.meta = N.ptr(self.meta_t)
         a.seg_bits = N.ptr(self.seg_bits)
         a.perm = N.ptr(self.perm) if self.perm is not None else None
+        a.fmt = version
         self.fields, self.mode, self.settings = fields, mode, settings
         self.n, self.S, self.nseg, self.ic, self.cpc = n, S, nseg, ic, cpc
         self.sorted_mode = sorted_mode
@@ -532,7 +547,7 @@ class _CompressCall:
             else:
                 offsets.append(int(fm.payload_off))
                 lengths.append(int(fm.payload_len))
-            kinds.append(int(StreamKind.SZ_DQ))
+            kinds.append(int(StreamKind.SZ_DQ if self.version == 2 else StreamKind.SZ_FIELD))
         dev = _Device(self.arena[:max(int(meta.arena_used), 1)], offsets, lengths, kinds,
                       keep=(self.meta_t,))
         if cpc:
@@ -549,8 +564,12 @@ class _CompressCall:
             constant_mask=meta.mask,
             constants=tuple(meta.f[i].constant for i in range(6)),
             seg_bits=self.seg_bits[:nseg] if self.sorted_mode else None,
-            device=dev, version=2, device_output=self.on_device,
+            device=dev, version=self.version, device_output=self.on_device,
             seg_minima=self.minima[:3 * nseg].view(nseg, 3) if cpc else None)
+        # the payload CRC-64s, queued now (no synchronisation): the
+        # reference's compress serialises with them (metrics.py:178-180)
+        from . import io as nbz_io
+        nbz_io.payload_crcs_async(archive)
         tile = (max(1, 16384 // S) * S) if S < 16384 else S
         perm = self.perm[:n] if self.perm is not None else None
         self.ws = None  # the workspace goes back to the caching allocator

@@ -21,15 +21,22 @@ def main():
     ap.add_argument("--mode", default="sz-lv-prx")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--compress-only", action="store_true")
+    ap.add_argument("--trace", action="store_true", help="print per-stage ms of the last rep")
     args = ap.parse_args()
+    from paper_1711_03888_b200 import _native as N
     spec = datagen.HaccSpec((640, 640, 640), 2.5)
     fields = datagen.generate(spec, 0, args.n)
     snap = nbz.ParticleSnapshot(*[torch.from_numpy(f).cuda() for f in fields])
-    for _ in range(args.reps):
+    for r in range(args.reps):
+        if args.trace and r == args.reps - 1:
+            N.trace_enable(True)
         res = nbz.compress(snap, args.mode, nbz.ErrorBoundSpec.relative(1e-4))
         if not args.compress_only:
             out = nbz.decompress(res.archive, device=True)
     torch.cuda.synchronize()
+    if args.trace:
+        print(" ".join(f"{k}={v:.3f}" for k, v in N.trace_read()))
+        N.trace_enable(False)
     print("ratio", nbz.ratio(res.archive), "n", snap.n)
 
 
