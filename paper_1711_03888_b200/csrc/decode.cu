@@ -1243,7 +1243,11 @@ NBZG_DEV void lv_safe_step(const LvCtx& X, LvChunk& S, float& o) {
   }
 }
 // 8 symbols, straight-line (no branch: the steps of two chunks interleave);
-// returns true when the group must be replayed exactly
+// returns true when the group must be replayed exactly.  The 64-bit buffer
+// is topped up to > 32 bits every RF symbols: every 2 for long codes, every
+// 4 for short ones (a field's mean code length below 6 bits) -- a window
+// that outruns the buffer wraps `cnt` and the group is replayed.
+template <int RF>
 NBZG_DEV bool lv_fast8(const LvCtx& X, LvChunk& S, float (&o)[8], LvSnap& sn) {
   BufReader& R = S.R;
   sn.hi = R.hi;
@@ -1256,7 +1260,7 @@ NBZG_DEV bool lv_fast8(const LvCtx& X, LvChunk& S, float (&o)[8], LvSnap& sn) {
   uint32_t flags = (unsigned long long)(S.k + (1ll << 30)) >> 31 ? 64u : 0u;  // |k| >= 2^30
 #pragma unroll
   for (int q = 0; q < 8; q++) {
-    if ((q & 1) == 0) {  // >= 32 valid bits before an even symbol (branch-free:
+    if ((q & (RF - 1)) == 0) {  // > 32 valid bits before every RF-th symbol (branch-free:
       // both shifts are 0 when cnt > 32)
       const uint32_t nw = S.ring[(R.wi & kLvRingMask) * kLvStride];
       R.hi |= shr_c(nw, R.cnt);
@@ -1327,6 +1331,46 @@ NBZG_DEV void lv_finish(const LvCtx& X, const DArgs& a, LvChunk& S, int i) {
   if (!S.err && pos != S.Tb) S.err = pos > S.Tb ? NBZG_TRUNCATED : NBZG_BAD_STREAM;
   if (S.err) fail(a.status, (uint32_t)S.err);
 }
+
+// the chunks [cb, ce) of one field, a chunk per thread
+template <int RF>
+NBZG_DEV void lv_chunks(const LvCtx& X, const DArgs& a, const uint64_t* choff, uint32_t a0,
+                        int64_t cb, int64_t ce, uint32_t* ring, bool vec) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  for (int64_t c = cb + tid; c < ce; c += nthr) {
+    LvChunk A;
+    lv_start(X, a, choff, a0, c, ring, A);
+    int i = 0;
+    if (vec) {
+      float oa[8], ob[8];
+      LvSnap sa;
+#pragma unroll
+      for (int u = 0; u < 8; u++) ob[u] = 0.0f;
+      for (; i + 16 <= A.mc; i += 16) {
+        lv_fix(X, A, oa, sa, lv_fast8<RF>(X, A, oa, sa));
+        // two register sets: a set's stores are issued one group before the
+        // set is rewritten (pinned live meanwhile)
+        asm volatile("" ::"f"(ob[0]), "f"(ob[1]), "f"(ob[2]), "f"(ob[3]), "f"(ob[4]),
+                     "f"(ob[5]), "f"(ob[6]), "f"(ob[7]));
+        st_v8_cs(A.dst + i, oa);
+        lv_fix(X, A, ob, sa, lv_fast8<RF>(X, A, ob, sa));
+        asm volatile("" ::"f"(oa[0]), "f"(oa[1]), "f"(oa[2]), "f"(oa[3]), "f"(oa[4]),
+                     "f"(oa[5]), "f"(oa[6]), "f"(oa[7]));
+#ifndef NBZG_DEC_STHALF  // timing experiment: half the stores
+        st_v8_cs(A.dst + i + 8, ob);
+#else
+        if (ob[0] == 1234.5f) A.dst[i] = ob[1];
+#endif
+        if (lv_consumed(A) > A.Tb) {
+          i += 16;
+          break;  // corrupt: stop early, reported below
+        }
+      }
+    }
+    lv_finish(X, a, A, i);
+  }
+}
+
 
 __global__ void __launch_bounds__(kLvMaxThreads, 1) decode_lv_kernel(DArgs a) {
   extern __shared__ __align__(16) uint8_t dsm2[];
@@ -1405,38 +1449,13 @@ __global__ void __launch_bounds__(kLvMaxThreads, 1) decode_lv_kernel(DArgs a) {
   const uint64_t* choff = a.choff + fi * (a.nchunks + 1);
   const bool vec = (reinterpret_cast<uintptr_t>(F.out) & 31) == 0;  // 32-byte stores
 
-  for (int64_t c = cb + tid; c < ce; c += nthr) {
-    LvChunk A;
-    lv_start(X, a, choff, a0, c, ring, A);
-    int i = 0;
-    if (vec) {
-      float oa[8], ob[8];
-      LvSnap sa;
-#pragma unroll
-      for (int u = 0; u < 8; u++) ob[u] = 0.0f;
-      for (; i + 16 <= A.mc; i += 16) {
-        lv_fix(X, A, oa, sa, lv_fast8(X, A, oa, sa));
-        // two register sets: a set's stores are issued one group before the
-        // set is rewritten (pinned live meanwhile)
-        asm volatile("" ::"f"(ob[0]), "f"(ob[1]), "f"(ob[2]), "f"(ob[3]), "f"(ob[4]),
-                     "f"(ob[5]), "f"(ob[6]), "f"(ob[7]));
-        st_v8_cs(A.dst + i, oa);
-        lv_fix(X, A, ob, sa, lv_fast8(X, A, ob, sa));
-        asm volatile("" ::"f"(oa[0]), "f"(oa[1]), "f"(oa[2]), "f"(oa[3]), "f"(oa[4]),
-                     "f"(oa[5]), "f"(oa[6]), "f"(oa[7]));
-#ifndef NBZG_DEC_STHALF  // timing experiment: half the stores
-        st_v8_cs(A.dst + i + 8, ob);
-#else
-        if (ob[0] == 1234.5f) A.dst[i] = ob[1];
+#ifndef NBZG_DEC_RF4
+#define NBZG_DEC_RF4 1
 #endif
-        if (lv_consumed(A) > A.Tb) {
-          i += 16;
-          break;  // corrupt: stop early, reported below
-        }
-      }
-    }
-    lv_finish(X, a, A, i);
-  }
+  // refill cadence by the field's mean code length (bits per symbol)
+  const bool rf4 = NBZG_DEC_RF4 && 8 * F.payload_len < 6 * a.n;
+  if (rf4) lv_chunks<4>(X, a, choff, a0, cb, ce, ring, vec);
+  else lv_chunks<2>(X, a, choff, a0, cb, ce, ring, vec);
 }
 
 // v2 streams with codes longer than 32 bits (pathological alphabets):

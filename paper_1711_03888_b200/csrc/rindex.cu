@@ -824,7 +824,8 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
         int32_t d[12];
 #pragma unroll
         for (int e = 0; e < 12; e++) d[e] = comp(xv[e], ivs[e % 3], mvs[e % 3], slow, e);
-        if (__any_sync(0xffffffffu, slow != 0)) {  // near-ties: ~2^-40 per value
+        // (a ragged segment leaves some lanes of a warp outside this loop)
+        if (__any_sync(__activemask(), slow != 0)) {  // near-ties: ~2^-40 per value
 #pragma unroll 1
           for (uint32_t sl = slow; sl; sl &= sl - 1) {
             const int e = __ffs(sl) - 1;
