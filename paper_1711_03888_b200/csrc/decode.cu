@@ -1450,7 +1450,7 @@ __global__ void __launch_bounds__(kLvMaxThreads, 1) decode_lv_kernel(DArgs a) {
   const bool vec = (reinterpret_cast<uintptr_t>(F.out) & 31) == 0;  // 32-byte stores
 
 #ifndef NBZG_DEC_RF4
-#define NBZG_DEC_RF4 1
+#define NBZG_DEC_RF4 0
 #endif
   // refill cadence by the field's mean code length (bits per symbol)
   const bool rf4 = NBZG_DEC_RF4 && 8 * F.payload_len < 6 * a.n;

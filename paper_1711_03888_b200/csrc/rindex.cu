@@ -505,6 +505,11 @@ __device__ __noinline__ int32_t exact_index(float x, const nbzg_field_meta* m) {
   return m->is_const ? 0 : (int32_t)rint(__ddiv_rn((double)x, m->twob));
 }
 
+#ifdef NBZG_CS_PROF  // timing experiment: per-phase clock totals of CTA 0, printed at exit
+#define CS_T(i) do { if (threadIdx.x == 0) { long long _c = clock64(); cs_t[i] += _c - cs_last; cs_last = _c; } } while (0)
+#else
+#define CS_T(i) do { } while (0)
+#endif
 constexpr int kCsMaxBits = 16;  // compacted key bits handled here (u16 keys)
 constexpr int kCsOneBits = 10;  // <= this: a single pass with 2^cw bins
 constexpr int kCsJ = kTileMax / kSortThreads;  // elements per thread (32)
@@ -610,8 +615,14 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
   __shared__ uint32_t scan_tmp[33];
   __shared__ float red[2][3][kSortWarps];
   __shared__ CsSeg sp;
+  __shared__ float cs_v[6];     // segment (min, max) per key field
+  __shared__ int64_t cs_q[6];   // their lattice indices
+  __shared__ int cs_big[6];
 
   const nbzg_field_meta* fm = a.meta->f + a.fbase;
+#ifdef NBZG_CS_PROF
+  long long cs_t[8] = {0, 0, 0, 0, 0, 0, 0, 0}, cs_last = clock64();
+#endif
   // persistent CTAs (2 per SM): while a tile is sorted, the next tile's
   // coordinates are already streaming into L2 (one bulk prefetch per
   // coordinate), so the key generation's loads hit L2 instead of waiting on
@@ -619,6 +630,8 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
   auto prefetch = [&](int64_t tt) {
     if (threadIdx.x != 0 || tt >= a.ntiles) return;
     const int64_t p0 = tt * a.tile;
+    if (a.seg_mm)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.seg_mm + 6 * (p0 / a.S)) : "memory");
     const uint32_t bytes = (uint32_t)(min(a.tile, a.n - p0) * 4) & ~15u;
     if (!bytes) return;
     for (int c = 0; c < 3; c++) {
@@ -638,21 +651,27 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
   for (int64_t s0 = t0; s0 < t1; s0 += a.S) {
     const int lo = (int)(s0 - t0);
     const int m = (int)(min(t1, s0 + a.S) - s0);
-    // ---- 1. segment min / max (K1's per-segment values, else reduced here)
-    float mn[3], mx[3];
-#pragma unroll
-    for (int c = 0; c < 3; c++) {
-      mn[c] = __int_as_float(0x7f800000);
-      mx[c] = -__int_as_float(0x7f800000);
-    }
+    // ---- 1. segment parameters (rindex.py:164-198): with K1's per-segment
+    // min / max, six threads integerise them in parallel; else the CTA
+    // reduces the segment first
     if (a.seg_mm) {
-      const float* sm = a.seg_mm + 6 * (s0 / a.S);
-#pragma unroll
-      for (int c = 0; c < 3; c++) {
-        mn[c] = sm[2 * c];
-        mx[c] = sm[2 * c + 1];
+      if (threadIdx.x < 6) {
+        const int c = threadIdx.x >> 1;
+        const float v = a.seg_mm[6 * (s0 / a.S) + threadIdx.x];
+        cs_v[threadIdx.x] = v;
+        if (!fm[c].is_const) {
+          const double q = __ddiv_rn((double)v, fm[c].twob);
+          cs_q[threadIdx.x] = (int64_t)rint(q);
+          cs_big[threadIdx.x] = fabs(q) > kIntLimit;
+        }
       }
     } else {
+      float mn[3], mx[3];
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        mn[c] = __int_as_float(0x7f800000);
+        mx[c] = -__int_as_float(0x7f800000);
+      }
       for (int i = threadIdx.x; i < m; i += kSortThreads) {
 #pragma unroll
         for (int c = 0; c < 3; c++) {
@@ -661,41 +680,46 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
           mx[c] = fmaxf(mx[c], v);
         }
       }
-    }
 #pragma unroll
-    for (int c = 0; c < 3; c++) {
+      for (int c = 0; c < 3; c++) {
 #pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        mn[c] = fminf(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
-        mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+        for (int o = 16; o; o >>= 1) {
+          mn[c] = fminf(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
+          mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+          red[0][c][threadIdx.x >> 5] = mn[c];
+          red[1][c][threadIdx.x >> 5] = mx[c];
+        }
       }
-      if ((threadIdx.x & 31) == 0) {
-        red[0][c][threadIdx.x >> 5] = mn[c];
-        red[1][c][threadIdx.x >> 5] = mx[c];
+      __syncthreads();
+      if (threadIdx.x < 6) {
+        const int c = threadIdx.x >> 1, hiw = threadIdx.x & 1;
+        float v = red[hiw][c][0];
+        for (int q = 1; q < kSortWarps; q++)
+          v = hiw ? fmaxf(v, red[1][c][q]) : fminf(v, red[0][c][q]);
+        cs_v[threadIdx.x] = v;
+        if (!fm[c].is_const) {
+          const double q = __ddiv_rn((double)v, fm[c].twob);
+          cs_q[threadIdx.x] = (int64_t)rint(q);
+          cs_big[threadIdx.x] = fabs(q) > kIntLimit;
+        }
       }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      // rindex.py:164-198: per-segment minima, need, bits, clamp drop
       int need = 0, bad = 0;
       int64_t rng[3];
       for (int c = 0; c < 3; c++) {
-        float a0 = red[0][c][0], b0 = red[1][c][0];
-        for (int q = 1; q < kSortWarps; q++) {
-          a0 = fminf(a0, red[0][c][q]);
-          b0 = fmaxf(b0, red[1][c][q]);
-        }
-        sp.amax[c] = fmaxf(fabsf(a0), fabsf(b0));
+        sp.amax[c] = fmaxf(fabsf(cs_v[2 * c]), fabsf(cs_v[2 * c + 1]));
         rng[c] = 0;
         if (fm[c].is_const) {
           sp.mn[c] = 0;
           continue;
         }
-        const double qa = __ddiv_rn((double)a0, fm[c].twob), qb = __ddiv_rn((double)b0, fm[c].twob);
-        if (fabs(qa) > kIntLimit || fabs(qb) > kIntLimit) bad = 1;
-        const int64_t ia = (int64_t)rint(qa), ib = (int64_t)rint(qb);
-        sp.mn[c] = ia;
-        rng[c] = ib - ia;
+        bad |= cs_big[2 * c] | cs_big[2 * c + 1];
+        sp.mn[c] = cs_q[2 * c];
+        rng[c] = cs_q[2 * c + 1] - cs_q[2 * c];
         need = max(need, bitlen64((uint64_t)rng[c]));
       }
       const int bits = min(need, 21);
@@ -737,6 +761,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
       __syncthreads();
       continue;
     }
+    CS_T(0);  // segment parameters
     // ---- 2. compaction tables: T[t][b][v] = sum_i bit_i(v) << P_t(8b + i)
     const int nbyte = (sp.wmax + 7) >> 3;
     for (int e = threadIdx.x; e < 3 * nbyte * 256; e += kSortThreads) {
@@ -753,6 +778,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
       lut[tt][b][v] = out;
     }
     __syncthreads();
+    CS_T(1);  // tables
     // ---- 3. compacted keys.  Exact integerisation rint(f64(x) / 2b)
     // (quantize.py:117-128) from the FP64 product t = x * (1/2b): |t - x/2b|
     // <= |t| 2^-51, so unless t is within tmax 2^-50 of a half-integer,
@@ -815,6 +841,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
       const float4* x4[3] = {reinterpret_cast<const float4*>(a.x[0] + s0),
                              reinterpret_cast<const float4*>(a.x[1] + s0),
                              reinterpret_cast<const float4*>(a.x[2] + s0)};
+#pragma unroll 2  // two iterations' loads in flight
       for (int v = threadIdx.x; v < m4; v += kSortThreads) {
         const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
         const float xv[12] = {q0.x, q1.x, q2.x, q0.y, q1.y, q2.y, q0.z, q1.z, q2.z, q0.w, q1.w, q2.w};
@@ -851,12 +878,14 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
         keys[i] = (uint16_t)key_of(a.x[0][s0 + i], a.x[1][s0 + i], a.x[2][s0 + i]);
     }
     __syncthreads();
+    CS_T(2);  // keys
     // ---- 4. stable LSD over cw bits, output into this segment's perm range
     {
       const int d1 = cw <= kCsOneBits ? cw : cw >> 1;  // one pass, or two balanced digits
       cs_pass<true>(keys, perm + lo, lo, m, 0, d1, whist, scan_tmp);
       if (cw > d1) cs_pass_next(keys, perm + lo, lo, m, d1, cw - d1, whist, scan_tmp);
     }
+    CS_T(3);  // sort
   }
   if (flagged) {
     if (threadIdx.x == 0) a.tile_flags[t] = 1;
@@ -865,7 +894,13 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
     for (int i = threadIdx.x; i < mt; i += kSortThreads) a.perm[t0 + i] = perm[i];
   }
   __syncthreads();  // perm is reused by the next tile
+  CS_T(4);  // write-out
   }
+#ifdef NBZG_CS_PROF
+  if (threadIdx.x == 0 && blockIdx.x < 2)
+    printf("csort CTA %d cycles: params %lld tables %lld keys %lld sort %lld out %lld\n", blockIdx.x,
+           cs_t[0], cs_t[1], cs_t[2], cs_t[3], cs_t[4]);
+#endif
 }
 
 int launch_rindex_sort(const Plan& p, cudaStream_t st) {

@@ -17,8 +17,11 @@ signatures, defaults and exception types.  What changes underneath:
   (``Archive.streams`` / ``serialized()``), and ``CompressResult.order``
   is materialised from the device permutation on first access.
 
-Modes outside the north-star path (sz-lcf, sz-cpc2000, cpc2000) are not
-implemented by the B200 path and raise ``ValidationError``.
+Every mode of the reference runs on the B200 path: sz-lv and sz-lv-prx (the
+north-star path), sz-lcf, and the CPC2000 modes sz-cpc2000 / cpc2000
+(SURVEY.md §8 f2-f4).  ``compress(..., version=1)`` writes
+reference-readable archives (v1 container, SZ_FIELD streams) for sz-lv /
+sz-lv-prx.
 """
 
 from __future__ import annotations

@@ -1,6 +1,7 @@
 """R-index vocabulary (pkg/src/nbz/rindex.py:24-56, 155-161).
 
-Only the coordinate variant is on the B200 path; the key
+All three variants run on the B200 path: coordinate keys,
+velocity keys and the six-field coord+velocity keys (§8 f4); the key
 construction and the segmented sort themselves run on device
 (csrc/rindex.cu).  ``segment_bounds`` and ``Segment`` keep the reference's
 meaning: segment boundaries are derived from (n, segment_size), never stored.
