@@ -221,18 +221,24 @@ static int sz_stages_split(Plan& p, cudaStream_t st) {
     cudaEventCreateWithFlags(&ee[made], cudaEventDisableTiming);
   }
   if (made < G) rc = NBZG_CUDA_ERROR;
+#ifndef NBZG_SZ_REVERSE
+#define NBZG_SZ_REVERSE 0
+#endif
+  // group order: REVERSE puts the velocities (large alphabets: the slow
+  // codebooks) first, so the last -- exposed -- codebook is a coordinate one
+  auto f0_of = [&](int g) { return (NBZG_SZ_REVERSE ? G - 1 - g : g) * per; };
   for (int g = 0; g < G && !rc; g++) {
-    if ((rc = launch_quantize(p, st, g * per, per))) break;
+    if ((rc = launch_quantize(p, st, f0_of(g), per))) break;
     cudaEventRecord(eq[g], st);
   }
   if (!rc) trace_mark("quantize", st);
   for (int g = 0; g < G && !rc; g++) {
     cudaStreamWaitEvent(sd[g], eq[g], 0);
-    if ((rc = launch_codebook(p, sd[g], g * per, per))) break;
+    if ((rc = launch_codebook(p, sd[g], f0_of(g), per))) break;
     if (g > 0) cudaStreamWaitEvent(sd[g], el[g - 1], 0);
-    if ((rc = launch_layout(p, sd[g], g * per, per))) break;
+    if ((rc = launch_layout(p, sd[g], f0_of(g), per, g == 0))) break;
     cudaEventRecord(el[g], sd[g]);
-    if ((rc = launch_encode(p, sd[g], g * per, per))) break;
+    if ((rc = launch_encode(p, sd[g], f0_of(g), per))) break;
     cudaEventRecord(ee[g], sd[g]);
   }
   for (int g = 0; g < made; g++) {

@@ -363,9 +363,9 @@ int launch_huffman_lengths(const uint32_t* counts, int64_t k, uint8_t* lengths, 
 
 // ---- K5: payload layout (offsets of the non-constant fields, field order)
 // fields f0 .. f1-1, placed after the fields before f0 (whose layout ran first)
-__global__ void layout_kernel(nbzg_meta* meta, int64_t n, int f0, int f1) {
+__global__ void layout_kernel(nbzg_meta* meta, int64_t n, int f0, int f1, int first) {
   if (threadIdx.x != 0) return;
-  uint64_t off = f0 == 0 ? 0 : meta->arena_used;
+  uint64_t off = first ? 0 : meta->arena_used;
   for (int f = f0; f < f1; f++) {
     nbzg_field_meta& m = meta->f[f];
     m.payload_off = off;
@@ -378,9 +378,9 @@ __global__ void layout_kernel(nbzg_meta* meta, int64_t n, int f0, int f1) {
   meta->arena_used = off;
 }
 
-int launch_layout(const Plan& p, cudaStream_t st, int f0, int nf) {
+int launch_layout(const Plan& p, cudaStream_t st, int f0, int nf, bool first) {
   count_launch();
-  layout_kernel<<<1, 32, 0, st>>>(p.meta, p.n, f0, f0 + nf);
+  layout_kernel<<<1, 32, 0, st>>>(p.meta, p.n, f0, f0 + nf, first ? 1 : 0);
   return cudaGetLastError() == cudaSuccess ? NBZG_OK : NBZG_CUDA_ERROR;
 }
 

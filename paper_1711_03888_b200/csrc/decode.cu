@@ -1161,6 +1161,7 @@ struct LvCtx {
   uint32_t vmax, wmax, r0m1, r0, sh2, lt_s;
   uint32_t rlim, m2;  // table index of window v: hi(min(v, rlim) * 2^15) + hi((v - min) * m2)
   uint32_t p15;       // first long-code entry (= r0 >> 17 when long codes exist)
+  uint32_t lt_n;      // entries in the shared table (checked build)
   int lmin, max_len, bias;
 };
 // one chunk being decoded
@@ -1270,6 +1271,7 @@ NBZG_DEV bool lv_fast8(const LvCtx& X, LvChunk& S, float (&o)[8], LvSnap& sn) {
       R.wi += t >> 5;
     }
     const uint32_t v = R.hi;
+    NBZG_CHECK(lv_index(X, v) < X.lt_n);
     const int32_t e = X.LT[lv_index(X, v)];
     flags |= (uint32_t)e;  // bit 6: escape or unresolved
     bb_take(R, (uint32_t)e & 63u);
@@ -1347,6 +1349,7 @@ NBZG_DEV void lv_chunks(const LvCtx& X, const DArgs& a, const uint64_t* choff, u
 #pragma unroll
       for (int u = 0; u < 8; u++) ob[u] = 0.0f;
       for (; i + 16 <= A.mc; i += 16) {
+        NBZG_CHECK(A.dst + i + 16 <= X.F->out + a.n);
         lv_fix(X, A, oa, sa, lv_fast8<RF>(X, A, oa, sa));
         // two register sets: a set's stores are issued one group before the
         // set is rewritten (pinned live meanwhile)
@@ -1443,6 +1446,7 @@ __global__ void __launch_bounds__(kLvMaxThreads, 1) decode_lv_kernel(DArgs a) {
   X.sh2 = n2 ? 32u - P.t2_w : 31u;
   X.rlim = has_long ? (uint32_t)P.t2_r0 : 0xffffffffu;
   X.p15 = P15;
+  X.lt_n = P15 + max(n2, 2u);
   X.m2 = n2 ? (1u << P.t2_w) : 0u;
   X.lmin = n2 ? (int)P.t2_w : kTpcBits;  // longer codes: canonical search
   X.lt_s = (uint32_t)__cvta_generic_to_shared(LT);

@@ -869,6 +869,7 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
       widx = (B >> 5) + (uint32_t)(rs - (uint32_t)((B >> 5) + ow));
       while (fl < widx) {
         if (fl < va) {
+          NBZG_CHECK(fl < (mp->payload_len - mp->bits_off) / 4);
           if (fl >= fo) outw[fl] = ring_at(fl);
           fl++;
         } else if (fl + 8 <= widx) {
@@ -876,6 +877,7 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
           uint32_t v[8];
 #pragma unroll
           for (int u = 0; u < 8; u++) v[u] = lds_u32(base + rstride * u);
+          NBZG_CHECK(fl + 8 <= (mp->payload_len - mp->bits_off + 3) / 4 + 8);
           st_v8_u32(outw + fl, v);
           fl += 8;
         } else {
@@ -933,8 +935,10 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
     }
     // ring words of the last (incomplete) aligned group
     widx = (B >> 5) + (uint32_t)(rs - (uint32_t)((B >> 5) + ow));
-    for (uint64_t u = fl; u < widx; u++)
+    for (uint64_t u = fl; u < widx; u++) {
+      NBZG_CHECK(u < (mp->payload_len - mp->bits_off) / 4);
       if (u >= fo) outw[u] = ring_at(u);
+    }
     // final partial word: completed with the leading bits that follow
     if (nacc > 0 && (Bend >> 5) >= fo) {
       uint32_t w = cur;

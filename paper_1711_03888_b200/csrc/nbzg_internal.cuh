@@ -9,6 +9,7 @@
 //   * a "chunk" is 16384 consecutive codes: the v2 stream's index granularity
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 
@@ -21,6 +22,25 @@ namespace nbzg {
 // launch accounting + optional per-kernel CUDA-event tracing (capi.cu)
 void count_launch();
 void trace_mark(const char* name, cudaStream_t st);
+
+// Bounds checks of the checked build (make variant V=checks
+// EXTRA=-DNBZG_CHECKS): a violated index traps the kernel with its location.
+// The GPU pool has compute-sanitizer closed, so the test suite runs against
+// this build instead (scripts/gpu/checks.sh, profiles/r02_checks.txt).
+#ifdef NBZG_CHECKS
+#define NBZG_CHECK(cond)                                                                   \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("nbzg check failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__,          \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                                  \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define NBZG_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 // NVTX range for the host-side span of one stage (header-only NVTX3: a no-op
 // unless a profiler injects its library, e.g. nsys / ncu --nvtx)

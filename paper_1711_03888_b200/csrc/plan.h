@@ -84,7 +84,7 @@ int launch_resolve(const Plan& p, cudaStream_t st);
 int launch_rindex_sort(const Plan& p, cudaStream_t st);
 int launch_quantize(const Plan& p, cudaStream_t st, int f0 = 0, int nf = 6);
 int launch_codebook(const Plan& p, cudaStream_t st, int f0 = 0, int nf = 6);
-int launch_layout(const Plan& p, cudaStream_t st, int f0 = 0, int nf = 6);
+int launch_layout(const Plan& p, cudaStream_t st, int f0 = 0, int nf = 6, bool first = true);
 int launch_encode(const Plan& p, cudaStream_t st, int f0 = 0, int nf = 6);
 bool encode_uses_tpc(const Plan& p);
 int launch_sz_skip(const Plan& p, cudaStream_t st);

@@ -593,6 +593,7 @@ NBZG_DEV void cs_pass(const uint16_t* keys, uint16_t* perm, int lo, int m, int s
         r = (packed[j] >> 14) & 0x3ffu;
         d = packed[j] >> 24;
       }
+      NBZG_CHECK(lds_u16(wh_s + 2u * d) + r < (uint32_t)m && src < (uint32_t)m);
       sts_u16(perm_s + 2u * (lds_u16(wh_s + 2u * d) + r), src + (uint32_t)lo);
     }
   }

@@ -202,6 +202,7 @@ __global__ void __launch_bounds__(kV1Threads) v1_pack_kernel(V1Args a) {
   uint32_t nb = (uint32_t)(b0 & 31);  // bits of the first word owned by earlier chunks (zeros)
   uint64_t wi = w_first;
   auto emit = [&](uint32_t word) {
+    NBZG_CHECK(wi <= w_last && wi < (uint64_t)a.wstride);
     if (wi == w_first || wi == w_last) atomicOr(&words[wi], word);
     else words[wi] = word;
     wi++;
@@ -273,6 +274,7 @@ __global__ void __launch_bounds__(kV1Threads) v1_esc_kernel(V1Args a) {
   const uint64_t e0 = a.eoff[field * (a.nchunks + 1) + c];
   const float* esc = a.esc + field * a.xs + c * kChunk;
   uint8_t* dst = a.arena + m.payload_off + m.esc_off + 4 * e0;
+  NBZG_CHECK(m.esc_off + 4 * (e0 + ne) <= m.payload_len);
   for (uint32_t j = 0; j < ne; j++) put_u32(dst + 4 * j, __float_as_uint(esc[j]));
 }
 
