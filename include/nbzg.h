@@ -109,7 +109,11 @@ typedef struct nbzg_compress_args {
                              shard's exact f32 min/max -> meta->f[i].lo / .hi; 2 = resume
                              with the GLOBAL min/max in h_minmax (all-gathered by the
                              caller), so bounds resolve as on the whole snapshot
-                             (model.py:104-125) and K1 is not run twice */
+                             (model.py:104-125) and K1 is not run twice.
+                             3 = everything but the encoding: meta holds the exact
+                             payload sizes (the `auto` mode compares two modes' sizes);
+                             4 = resume a phase-3 call: encode only (same args,
+                             workspace and arena).  Phases 3/4: fmt 2, SZ modes */
   float h_minmax[12];     /* phase 2: (lo, hi) of field 0..5, host values */
   int32_t fmt;            /* 0 or 2: v2 SZ_DQ streams (chunk-parallel, container 2);
                              1: reference-readable SZ_FIELD streams (container 1) -- the

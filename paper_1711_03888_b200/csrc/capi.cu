@@ -360,8 +360,16 @@ int nbzg_compress(const nbzg_compress_args* a, void* stream) {
   p.arena = a->arena;
   p.arena_bytes = a->arena_bytes;
   int rc;
-  if (a->phase < 0 || a->phase > 2) return NBZG_BAD_ARG;
+  if (a->phase < 0 || a->phase > 4) return NBZG_BAD_ARG;
+  if (a->phase >= 3 && (p.fmt != 2 || p.cpc || p.predictor)) return NBZG_UNSUPPORTED;
   trace_mark(nullptr, st);
+  if (a->phase == 4) {  // resume a phase-3 call: encode only (payload sizes are final)
+    NvtxScope r("K5 encode");
+    if (p.n == 0) return cuda_status();
+    if ((rc = launch_encode(p, st))) return rc;
+    trace_mark("encode", st);
+    return cuda_status();
+  }
   // sorted mode with 3-field keys: K1 walks whole segments and also leaves
   // each segment's key-field min/max, so K2 reads the coordinates once
   const bool segmm = p.sorted && p.variant != 2 && p.n > 0 && p.S % 4 == 0;
@@ -391,13 +399,14 @@ int nbzg_compress(const nbzg_compress_args* a, void* stream) {
   NvtxScope range_sz("K3-K5 quantize / codebook / encode");
   if (p.sz_skip && (rc = launch_sz_skip(p, st))) return rc;
   if (p.fmt == 1) return launch_v1(p, st);
-  if (p.predictor == 0 && encode_uses_tpc(p)) return sz_stages_split(p, st);
+  if (a->phase != 3 && p.predictor == 0 && encode_uses_tpc(p)) return sz_stages_split(p, st);
   if ((rc = launch_quantize(p, st))) return rc;
   trace_mark("quantize", st);
   if ((rc = launch_codebook(p, st))) return rc;
   trace_mark("codebook", st);
   if ((rc = launch_layout(p, st))) return rc;
   trace_mark("layout", st);
+  if (a->phase == 3) return cuda_status();  // sizes only: meta holds every payload length
   if ((rc = launch_encode(p, st))) return rc;
   trace_mark("encode", st);
   return cuda_status();

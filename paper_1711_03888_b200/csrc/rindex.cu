@@ -624,26 +624,10 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
 #ifdef NBZG_CS_PROF
   long long cs_t[8] = {0, 0, 0, 0, 0, 0, 0, 0}, cs_last = clock64();
 #endif
-  // persistent CTAs (2 per SM): while a tile is sorted, the next tile's
-  // coordinates are already streaming into L2 (one bulk prefetch per
-  // coordinate), so the key generation's loads hit L2 instead of waiting on
-  // DRAM with no other work to overlap
-  auto prefetch = [&](int64_t tt) {
-    if (threadIdx.x != 0 || tt >= a.ntiles) return;
-    const int64_t p0 = tt * a.tile;
-    if (a.seg_mm)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.seg_mm + 6 * (p0 / a.S)) : "memory");
-    const uint32_t bytes = (uint32_t)(min(a.tile, a.n - p0) * 4) & ~15u;
-    if (!bytes) return;
-    for (int c = 0; c < 3; c++) {
-      const float* src = a.x[c] + p0;
-      if (reinterpret_cast<uintptr_t>(src) & 15) continue;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-    }
-  };
-  prefetch(blockIdx.x);
+  // persistent CTAs (2 per SM), tiles strided by the grid.  (An L2 bulk
+  // prefetch of the next tile's coordinates was measured: the lines were
+  // evicted before use -- twice the DRAM reads -- and the tile got slower.)
   for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
-  prefetch(t + gridDim.x);
   const int64_t t0 = t * a.tile;
   const int64_t t1 = min(a.n, t0 + a.tile);
   const int mt = (int)(t1 - t0);

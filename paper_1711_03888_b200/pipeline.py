@@ -423,9 +423,19 @@ def compress(snapshot: ParticleSnapshot, mode, bounds: Bounds,
         dsnap = ParticleSnapshot.__new__(ParticleSnapshot)
         for name, f in zip(FIELD_NAMES, fields):
             object.__setattr__(dsnap, name, f)
-        a = compress(dsnap, Mode.SZ_LV, bounds, settings, version=version)
-        b = compress(dsnap, Mode.SZ_LV_PRX, bounds, settings, version=version)
-        best = b if b.archive.total_bytes() < a.archive.total_bytes() else a
+        if version == 1 or snapshot.n == 0:  # reference-readable: two full compresses
+            a = compress(dsnap, Mode.SZ_LV, bounds, settings, version=version)
+            b = compress(dsnap, Mode.SZ_LV_PRX, bounds, settings, version=version)
+            best = b if b.archive.total_bytes() < a.archive.total_bytes() else a
+        else:
+            # both modes up to their exact payload sizes (histograms and
+            # codebooks fix them), then only the smaller one is encoded
+            ca = _CompressCall(dsnap, Mode.SZ_LV, bounds, settings)
+            sa = ca.sized()
+            cb = _CompressCall(dsnap, Mode.SZ_LV_PRX, bounds, settings)
+            sb = cb.sized()
+            best = cb.finish_encoding() if sb < sa else ca.finish_encoding()
+            del ca, cb
         best.archive.device_output = bool(snapshot.on_device)
         del hold
         return best
@@ -522,6 +532,26 @@ class _CompressCall:
         self._phase1 = True
         return out
 
+    def sized(self) -> int:
+        """Phase 3: everything but the encoding; returns the archive's exact
+        serialized size (mode="auto" compares two modes with it, then
+        ``finish_encoding()`` completes only the smaller)."""
+        self.args.phase = 3
+        N.check(self.L.nbzg_compress(ctypes.byref(self.args), N.stream_handle()), "compress")
+        meta = self._meta()
+        _raise_status(meta.status, "compress")
+        from . import io as nbz_io
+        pls = [int(meta.f[i].payload_len) for i in range(6)
+               if self.n > 0 and not meta.f[i].is_const]
+        nseg = self.nseg if self.sorted_mode else 0
+        return nbz_io.serialized_size_of(nseg, self.mode.stores_minima, pls)
+
+    def finish_encoding(self) -> CompressResult:
+        """Phase 4: resume a ``sized()`` call (encode only)."""
+        self.args.phase = 4
+        N.check(self.L.nbzg_compress(ctypes.byref(self.args), N.stream_handle()), "compress")
+        return self._result()
+
     def finish(self, global_minmax=None) -> CompressResult:
         """The rest of the compress: phase 0 (whole call) or, after
         ``local_minmax()``, phase 2 with the global (6, 2) min/max."""
@@ -538,6 +568,10 @@ class _CompressCall:
         else:
             a.phase = 0
         N.check(self.L.nbzg_compress(ctypes.byref(a), N.stream_handle()), "compress")
+        return self._result()
+
+    def _result(self) -> CompressResult:
+        n = self.n
         meta = self._meta()
         _raise_status(meta.status, "compress")
         mode, settings, S, nseg, cpc = self.mode, self.settings, self.S, self.nseg, self.cpc

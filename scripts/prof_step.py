@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--compress-only", action="store_true")
     ap.add_argument("--trace", action="store_true", help="print per-stage ms of the last rep")
+    ap.add_argument("--crc", action="store_true", help="also serialise (payload CRC-64s)")
     args = ap.parse_args()
     from paper_1711_03888_b200 import _native as N
     spec = datagen.HaccSpec((640, 640, 640), 2.5)
@@ -31,6 +32,9 @@ def main():
         if args.trace and r == args.reps - 1:
             N.trace_enable(True)
         res = nbz.compress(snap, args.mode, nbz.ErrorBoundSpec.relative(1e-4))
+        if args.crc:
+            from paper_1711_03888_b200 import io as nio
+            nio._payload_crcs(res.archive)
         if not args.compress_only:
             out = nbz.decompress(res.archive, device=True)
     torch.cuda.synchronize()

@@ -562,10 +562,13 @@ def test_settings_variants_byte_identical(O, seg, ig, ic, decoder, encoder):
             assert float(err.max()) <= res.archive.bounds[fi]
 
 
-@pytest.mark.parametrize("gen", ["hacc", "amdf"])
+@pytest.mark.parametrize("gen", ["hacc", "amdf", "C1"])
 def test_auto_mode_keeps_smaller_archive(O, gen):
-    """a13: snapshot-level auto policy = the smaller of sz-lv / sz-lv-prx."""
-    fields = datagen.small_hacc(32) if gen == "hacc" else datagen.small_amdf(40000)
+    """a13: snapshot-level auto policy = the smaller of sz-lv / sz-lv-prx,
+    chosen from both modes' exact sizes before encoding (C1: the
+    chunk-parallel encoder resumed after the sizing phase)."""
+    fields = {"hacc": lambda: datagen.small_hacc(32), "amdf": lambda: datagen.small_amdf(40000),
+              "C1": lambda: datagen.generate("C1")}[gen]()
     snap = nbz.ParticleSnapshot(*fields)
     a = nbz.compress(snap, "sz-lv", REL4).archive.serialized()
     b = nbz.compress(snap, "sz-lv-prx", REL4).archive.serialized()
