@@ -826,6 +826,66 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
       const float4* x4[3] = {reinterpret_cast<const float4*>(a.x[0] + s0),
                              reinterpret_cast<const float4*>(a.x[1] + s0),
                              reinterpret_cast<const float4*>(a.x[2] + s0)};
+      // FP32 bucket path.  u = (rint(Q) - mn) >> s = floor(g) with
+      // g = (Q - mn + 0.5) / 2^s, Q = f64(x) / 2b -- exactly, unless Q sits on
+      // a bucket boundary (g an integer; a rint tie there is where rint's
+      // half-even rule matters).  g32 = fma(x, fl32(inv/2^s), -(mn - 0.5)/2^s)
+      // is within (gmax + tmax/2^s + 1) 2^-22 of g, so a fractional part of
+      // g32 farther than that from 0 and 1 decides floor(g); the others (a
+      // bucket edge per 2^s lattice units: ~2^-14 of the values here) take
+      // the exact division.  Needs s >= 4, |mn| < 2^22 (mn - 0.5 exact in
+      // FP32) and g < 2^21 (g + 1.5 2^23 rounded down is 1.5 2^23 + floor(g)).
+      bool f32 = shift >= 4;
+      float invs[3], cs[3];
+      float lim = 0.5f;
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        const double sc = ldexp(1.0, -shift);
+        invs[c] = (float)(fm[c].inv * sc);
+        cs[c] = (float)(((double)sp.mn[c] - 0.5) * sc);
+        f32 &= fm[c].is_const || (sp.mn[c] > -4194304 && sp.mn[c] < 4194304);
+        const double tmax = (double)sp.amax[c] * fm[c].inv;
+        const double eps = (ldexp(1.0, sp.w) + tmax * sc + 1.0) * 2.384185791015625e-07;  // 2^-22
+        lim = fminf(lim, (float)(0.5 - 2.0 * eps));
+      }
+      f32 &= lim > 0.25f;
+      if (f32) {
+#pragma unroll 2  // two iterations' loads in flight
+        for (int v = threadIdx.x; v < m4; v += kSortThreads) {
+          const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
+          const float xv[12] = {q0.x, q1.x, q2.x, q0.y, q1.y, q2.y, q0.z, q1.z, q2.z, q0.w, q1.w, q2.w};
+          uint32_t slow = 0;
+          uint32_t u[12];
+#pragma unroll
+          for (int e = 0; e < 12; e++) {
+            const float g = __fmaf_rn(xv[e], invs[e % 3], -cs[e % 3]);
+            const float r = __fadd_rd(g, 12582912.0f);
+            const float fr = __fsub_rn(g, __fsub_rn(r, 12582912.0f));
+            if (!(fabsf(__fsub_rn(fr, 0.5f)) < lim)) slow |= 1u << e;
+            u[e] = (uint32_t)(__float_as_int(r) - 0x4B400000);
+          }
+          if (__any_sync(__activemask(), slow != 0)) {  // bucket edges
+#pragma unroll 1
+            for (uint32_t sl = slow; sl; sl &= sl - 1) {
+              const int e = __ffs(sl) - 1;
+              float x = xv[0];
+              int32_t mm = m0;
+#pragma unroll
+              for (int q = 0; q < 12; q++)
+                if (q == e) x = xv[q], mm = (q % 3 == 0 ? m0 : (q % 3 == 1 ? m1 : m2));
+              const uint32_t ue = (uint32_t)(exact_index(x, fm + e % 3) - mm) >> shift;
+#pragma unroll
+              for (int q = 0; q < 12; q++)
+                if (q == e) u[q] = ue;
+            }
+          }
+          uint32_t kk[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) kk[j] = lut3(u[3 * j], u[3 * j + 1], u[3 * j + 2]);
+          *reinterpret_cast<uint2*>(keys + 4 * v) =
+              make_uint2(kk[0] | (kk[1] << 16), kk[2] | (kk[3] << 16));
+        }
+      } else
 #pragma unroll 2  // two iterations' loads in flight
       for (int v = threadIdx.x; v < m4; v += kSortThreads) {
         const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
