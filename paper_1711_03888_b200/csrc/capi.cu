@@ -164,6 +164,12 @@ size_t plan_workspace(Plan& p, void* base) {
   p.counters = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 64));
   p.tile_flags = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * (p.ntiles + 1)));
   p.seg_mm = reinterpret_cast<float*>(take(sizeof(float) * 6 * ((size_t)p.nseg + 1)));
+#ifdef NBZG_CS_SPLIT
+  if (p.sorted) {
+    p.keys16 = reinterpret_cast<uint16_t*>(take(sizeof(uint16_t) * ((size_t)p.n + 8)));
+    p.seg_cw = reinterpret_cast<uint8_t*>(take((size_t)p.nseg + 16));
+  }
+#endif
   if (p.fmt == 1) {
     const size_t xs = (size_t)p.v1_stride, nc = (size_t)p.nchunks;
     p.v1_xsort = p.sorted ? reinterpret_cast<float*>(take(sizeof(float) * 6 * xs)) : nullptr;

@@ -32,6 +32,8 @@ struct Plan {
   // workspace
   uint32_t* minmax = nullptr;   // 12 ordered u32
   float* seg_mm = nullptr;      // [nseg][3][2] per-segment min/max of the key fields (from K1)
+  uint16_t* keys16 = nullptr;   // [n] compacted R-index keys (split compact sort)
+  uint8_t* seg_cw = nullptr;    // [nseg] their width per segment
   nbzg_meta* meta = nullptr;
   uint16_t* perm = nullptr;
   uint8_t* seg_bits = nullptr;

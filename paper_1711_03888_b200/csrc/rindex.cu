@@ -42,6 +42,8 @@ struct RArgs {
   int no_clamp;     // CPC modes: allow_key_clamp=False (rindex.py:185-190)
   int64_t* minima;  // CPC modes: 3 segment minima per segment (io.py:115-117), else null
   const float* seg_mm;  // [nseg][3][2] key-field min/max per segment from K1, or null
+  uint16_t* keys16;     // [n] compacted keys (split compact sort)
+  uint8_t* seg_cw;      // [nseg] compacted key width, 255 = general kernel
 };
 
 NBZG_DEV void set_status(uint32_t* status, uint32_t code) { atomicCAS(status, 0u, code); }
@@ -510,6 +512,7 @@ __device__ __noinline__ int32_t exact_index(float x, const nbzg_field_meta* m) {
 #else
 #define CS_T(i) do { } while (0)
 #endif
+constexpr int kCsKeyThreads = 256;  // K2a block
 constexpr int kCsMaxBits = 16;  // compacted key bits handled here (u16 keys)
 constexpr int kCsOneBits = 10;  // <= this: a single pass with 2^cw bins
 constexpr int kCsJ = kTileMax / kSortThreads;  // elements per thread (32)
@@ -607,12 +610,20 @@ __device__ __noinline__ void cs_pass_next(const uint16_t* keys, uint16_t* perm, 
   cs_pass<false>(keys, perm, lo, m, sh, D, whist, scan_tmp);
 }
 
-__global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) {
+// MODE 0: keys and sort in one kernel (keys in shared memory); MODE 1:
+// segment parameters + compacted keys to HBM (u16, 2 B/particle) and the
+// per-segment key width; MODE 2: the sort, keys loaded from HBM.  The split
+// (1 + 2) streams the coordinates at high occupancy instead of holding a
+// 105 KB sort CTA idle on them.
+template <int MODE>
+NBZG_DEV void csort_body(const RArgs& a) {
   extern __shared__ __align__(16) uint8_t csm[];
   uint16_t* keys = reinterpret_cast<uint16_t*>(csm);          // [kTileMax] segment-local
   uint16_t* perm = keys + kTileMax;                           // [kTileMax] tile-local values
   uint16_t* whist = perm + kTileMax;                          // [16][2^10]
-  uint32_t(*lut)[3][256] = reinterpret_cast<uint32_t(*)[3][256]>(whist + (kSortWarps << kCsOneBits));
+  uint32_t(*lut)[3][256] = reinterpret_cast<uint32_t(*)[3][256]>(
+      MODE == 1 ? csm : reinterpret_cast<uint8_t*>(whist + (kSortWarps << kCsOneBits)));
+  constexpr int NT = MODE == 1 ? kCsKeyThreads : kSortThreads;
   __shared__ uint32_t scan_tmp[33];
   __shared__ float red[2][3][kSortWarps];
   __shared__ CsSeg sp;
@@ -632,10 +643,30 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
   const int64_t t1 = min(a.n, t0 + a.tile);
   const int mt = (int)(t1 - t0);
   bool flagged = false;
+  if (MODE == 2 && a.tile_flags[t]) continue;  // the general kernel sorts this tile
 
   for (int64_t s0 = t0; s0 < t1; s0 += a.S) {
     const int lo = (int)(s0 - t0);
     const int m = (int)(min(t1, s0 + a.S) - s0);
+    if (MODE == 2) {
+      const int cw = a.seg_cw[s0 / a.S];
+      if (cw == 0) {
+        for (int i = threadIdx.x; i < m; i += NT) perm[lo + i] = (uint16_t)(lo + i);
+        __syncthreads();
+        continue;
+      }
+      // the segment's compacted keys (K2a), coalesced 16-byte loads
+      const uint16_t* src = a.keys16 + s0;
+      const int m8 = (s0 & 7) ? 0 : m >> 3;
+      for (int i = threadIdx.x; i < m8; i += NT)
+        reinterpret_cast<uint4*>(keys)[i] = __ldg(reinterpret_cast<const uint4*>(src) + i);
+      for (int i = 8 * m8 + threadIdx.x; i < m; i += NT) keys[i] = src[i];
+      __syncthreads();
+      const int d1 = cw <= kCsOneBits ? cw : cw >> 1;
+      cs_pass<true>(keys, perm + lo, lo, m, 0, d1, whist, scan_tmp);
+      if (cw > d1) cs_pass_next(keys, perm + lo, lo, m, d1, cw - d1, whist, scan_tmp);
+      continue;
+    }
     // ---- 1. segment parameters (rindex.py:164-198): with K1's per-segment
     // min / max, six threads integerise them in parallel; else the CTA
     // reduces the segment first
@@ -657,7 +688,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
         mn[c] = __int_as_float(0x7f800000);
         mx[c] = -__int_as_float(0x7f800000);
       }
-      for (int i = threadIdx.x; i < m; i += kSortThreads) {
+      for (int i = threadIdx.x; i < m; i += NT) {
 #pragma unroll
         for (int c = 0; c < 3; c++) {
           const float v = a.x[c][s0 + i];
@@ -681,7 +712,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
       if (threadIdx.x < 6) {
         const int c = threadIdx.x >> 1, hiw = threadIdx.x & 1;
         float v = red[hiw][c][0];
-        for (int q = 1; q < kSortWarps; q++)
+        for (int q = 1; q < NT / 32; q++)
           v = hiw ? fmaxf(v, red[1][c][q]) : fminf(v, red[0][c][q]);
         cs_v[threadIdx.x] = v;
         if (!fm[c].is_const) {
@@ -736,20 +767,23 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
         for (int c = 0; c < 3; c++) a.minima[3 * (s0 / a.S) + c] = sp.mn[c];
     }
     const int cw = sp.cw;
+    if (MODE == 1 && threadIdx.x == 0) a.seg_cw[s0 / a.S] = (uint8_t)(cw > kCsMaxBits ? 255 : cw);
     if (cw > kCsMaxBits) {  // the general kernel redoes this tile
       flagged = true;
       continue;
     }
     if (flagged) continue;  // (seg_bits / minima still written for every segment)
     if (cw == 0) {
-      for (int i = threadIdx.x; i < m; i += kSortThreads) perm[lo + i] = (uint16_t)(lo + i);
-      __syncthreads();
+      if (MODE == 0) {
+        for (int i = threadIdx.x; i < m; i += NT) perm[lo + i] = (uint16_t)(lo + i);
+        __syncthreads();
+      }
       continue;
     }
     CS_T(0);  // segment parameters
     // ---- 2. compaction tables: T[t][b][v] = sum_i bit_i(v) << P_t(8b + i)
     const int nbyte = (sp.wmax + 7) >> 3;
-    for (int e = threadIdx.x; e < 3 * nbyte * 256; e += kSortThreads) {
+    for (int e = threadIdx.x; e < 3 * nbyte * 256; e += NT) {
       const int tt = e / (nbyte * 256), b = (e >> 8) % nbyte, v = e & 255;
       uint32_t out = 0;
       for (int i = 0; i < 8; i++) {
@@ -774,6 +808,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
       const int shift = sp.shift;
       const int32_t m0 = (int32_t)sp.mn[0], m1 = (int32_t)sp.mn[1], m2 = (int32_t)sp.mn[2];
       const uint32_t lut_s = sh_addr(&lut[0][0][0]);
+      uint16_t* kdst = MODE == 1 ? a.keys16 + s0 : keys;  // K2a: to HBM (s0 % 4 == 0)
       const double iv0 = fm[0].inv, iv1 = fm[1].inv, iv2 = fm[2].inv;
       bool small = true;
       double tie = 0.0;
@@ -851,7 +886,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
       f32 &= lim > 0.25f;
       if (f32) {
 #pragma unroll 2  // two iterations' loads in flight
-        for (int v = threadIdx.x; v < m4; v += kSortThreads) {
+        for (int v = threadIdx.x; v < m4; v += NT) {
           const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
           const float xv[12] = {q0.x, q1.x, q2.x, q0.y, q1.y, q2.y, q0.z, q1.z, q2.z, q0.w, q1.w, q2.w};
           uint32_t slow = 0;
@@ -882,12 +917,12 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
           uint32_t kk[4];
 #pragma unroll
           for (int j = 0; j < 4; j++) kk[j] = lut3(u[3 * j], u[3 * j + 1], u[3 * j + 2]);
-          *reinterpret_cast<uint2*>(keys + 4 * v) =
+          *reinterpret_cast<uint2*>(kdst + 4 * v) =
               make_uint2(kk[0] | (kk[1] << 16), kk[2] | (kk[3] << 16));
         }
       } else
 #pragma unroll 2  // two iterations' loads in flight
-      for (int v = threadIdx.x; v < m4; v += kSortThreads) {
+      for (int v = threadIdx.x; v < m4; v += NT) {
         const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
         const float xv[12] = {q0.x, q1.x, q2.x, q0.y, q1.y, q2.y, q0.z, q1.z, q2.z, q0.w, q1.w, q2.w};
         const double ivs[3] = {iv0, iv1, iv2};
@@ -917,15 +952,15 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
         for (int j = 0; j < 4; j++)
           kk[j] = lut3((uint32_t)d[3 * j] >> shift, (uint32_t)d[3 * j + 1] >> shift,
                        (uint32_t)d[3 * j + 2] >> shift);
-        *reinterpret_cast<uint2*>(keys + 4 * v) = make_uint2(kk[0] | (kk[1] << 16), kk[2] | (kk[3] << 16));
+        *reinterpret_cast<uint2*>(kdst + 4 * v) = make_uint2(kk[0] | (kk[1] << 16), kk[2] | (kk[3] << 16));
       }
-      for (int i = 4 * m4 + threadIdx.x; i < m; i += kSortThreads)
-        keys[i] = (uint16_t)key_of(a.x[0][s0 + i], a.x[1][s0 + i], a.x[2][s0 + i]);
+      for (int i = 4 * m4 + threadIdx.x; i < m; i += NT)
+        kdst[i] = (uint16_t)key_of(a.x[0][s0 + i], a.x[1][s0 + i], a.x[2][s0 + i]);
     }
     __syncthreads();
     CS_T(2);  // keys
     // ---- 4. stable LSD over cw bits, output into this segment's perm range
-    {
+    if (MODE == 0) {
       const int d1 = cw <= kCsOneBits ? cw : cw >> 1;  // one pass, or two balanced digits
       cs_pass<true>(keys, perm + lo, lo, m, 0, d1, whist, scan_tmp);
       if (cw > d1) cs_pass_next(keys, perm + lo, lo, m, d1, cw - d1, whist, scan_tmp);
@@ -933,10 +968,10 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
     CS_T(3);  // sort
   }
   if (flagged) {
-    if (threadIdx.x == 0) a.tile_flags[t] = 1;
-  } else {
+    if (MODE != 2 && threadIdx.x == 0) a.tile_flags[t] = 1;
+  } else if (MODE != 1) {
     // ---- write the tile's permutation (coalesced)
-    for (int i = threadIdx.x; i < mt; i += kSortThreads) a.perm[t0 + i] = perm[i];
+    for (int i = threadIdx.x; i < mt; i += NT) a.perm[t0 + i] = perm[i];
   }
   __syncthreads();  // perm is reused by the next tile
   CS_T(4);  // write-out
@@ -947,6 +982,10 @@ __global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) 
            cs_t[0], cs_t[1], cs_t[2], cs_t[3], cs_t[4]);
 #endif
 }
+
+__global__ void __launch_bounds__(kSortThreads, 2) rindex_csort_kernel(RArgs a) { csort_body<0>(a); }
+__global__ void __launch_bounds__(kCsKeyThreads, 4) rindex_ckeys_kernel(RArgs a) { csort_body<1>(a); }
+__global__ void __launch_bounds__(kSortThreads, 2) rindex_crank_kernel(RArgs a) { csort_body<2>(a); }
 
 int launch_rindex_sort(const Plan& p, cudaStream_t st) {
   if (p.n == 0) return NBZG_OK;
@@ -967,10 +1006,14 @@ int launch_rindex_sort(const Plan& p, cudaStream_t st) {
   a.no_clamp = p.cpc ? 1 : 0;
   a.minima = p.cpc ? p.minima : nullptr;
   a.seg_mm = p.seg_mm;
+  a.keys16 = p.keys16;
+  a.seg_cw = p.seg_cw;
   size_t sm32 = kTileMax * (4 + 2) + kSortWarps * kRadix * 2;
   size_t sm64 = kTileMax * (8 + 2) + kSortWarps * kRadix * 2;
   size_t smc = kTileMax * (2 + 2) + (kSortWarps << kCsOneBits) * 2 + 3 * 3 * 256 * 4;
   smem_attr((const void*)rindex_csort_kernel, (int)smc);
+  smem_attr((const void*)rindex_crank_kernel, (int)smc);
+  const size_t smk = 3 * 3 * 256 * 4;  // K2a: the compaction tables only
   smem_attr((const void*)rindex_sort_kernel<uint32_t>, (int)sm32);
   smem_attr((const void*)rindex_sort_kernel<uint64_t>, (int)sm64);
   smem_attr((const void*)rindex_sort6_kernel<uint32_t>, (int)sm32);
@@ -987,9 +1030,21 @@ int launch_rindex_sort(const Plan& p, cudaStream_t st) {
     // compact-key sort; tiles with a segment of more than 16 varying key
     // bits (flag 1) are redone by the general kernel
     a.pass = 0;
-    count_launch();
     const unsigned gcs = (unsigned)min(p.ntiles, (int64_t)2 * sm_count());
+#ifdef NBZG_CS_SPLIT
+    // K2a: segment parameters + compacted keys, streamed at 4 CTAs/SM;
+    // K2b: the counting sort from the u16 keys.  Measured at config 2:
+    // 0.82 + 1.01 ms, the same as the fused kernel (1.82 ms): the sort
+    // itself is the limiter, so the fused kernel (no key round trip) is the
+    // default
+    count_launch();
+    rindex_ckeys_kernel<<<(unsigned)min(p.ntiles, (int64_t)4 * sm_count()), kCsKeyThreads, smk, st>>>(a);
+    count_launch();
+    rindex_crank_kernel<<<gcs, kSortThreads, smc, st>>>(a);
+#else
+    count_launch();
     rindex_csort_kernel<<<gcs, kSortThreads, smc, st>>>(a);
+#endif
     a.pass = 1;
     count_launch();
     rindex_sort_kernel<uint32_t><<<(unsigned)p.ntiles, kSortThreads, sm32, st>>>(a);
