@@ -98,7 +98,7 @@ typedef struct nbzg_compress_args {
   size_t arena_bytes;
   nbzg_meta *meta;        /* device */
   uint8_t *seg_bits;      /* device, ceil(n/segment_size) bytes (sorted) */
-  uint16_t *perm;         /* device, n entries (sorted) */
+  uint16_t *perm;         /* device, n entries (sorted, segment_size <= 16384) */
   int32_t predictor;      /* 0 = last value (sz-lv, sz-lv-prx), 1 = LCF 2*prev - prev2
                              (Mode.SZ_LCF, _kernels.py:162-165; unsorted only) */
   int32_t cpc;            /* 0; 1 = sz-cpc2000, 2 = cpc2000 (full keys, no clamp, minima) */
@@ -121,6 +121,11 @@ typedef struct nbzg_compress_args {
                              16384 values; sz-lv / sz-lv-prx only.
                              Workspace: nbzg_compress_workspace_size_fmt(..., 1) */
   int32_t pad3;
+  uint32_t *order32;      /* device, n entries: sorted mode with segment_size > 16384 (one
+                             segment no longer fits a tile; rindex.py:155-229 has no size
+                             cap) -- the global source index of every sorted position,
+                             replacing perm.  Rindex variants 0/1, no cpc; one host
+                             synchronisation (the radix pass count is data-dependent) */
 } nbzg_compress_args;
 
 size_t nbzg_compress_workspace_size(int64_t n, int32_t sorted, int64_t interval_count,

@@ -81,7 +81,8 @@ class CompressArgs(ctypes.Structure):
                 ("workspace_bytes", c_sz), ("arena", c_p), ("arena_bytes", c_sz),
                 ("meta", c_p), ("seg_bits", c_p), ("perm", c_p), ("predictor", c_i32),
                 ("cpc", c_i32), ("seg_minima", c_p), ("sz_skip", c_u32), ("phase", c_i32),
-                ("h_minmax", c_f * 12), ("fmt", c_i32), ("pad3", c_i32)]
+                ("h_minmax", c_f * 12), ("fmt", c_i32), ("pad3", c_i32),
+                ("order32", c_p)]
 
 
 class CpcMeta(ctypes.Structure):

@@ -123,7 +123,8 @@ void plan_shape(Plan& p, int64_t n, int sorted, int64_t ic, int64_t S, int fmt) 
   p.fmt = fmt;
   p.sorted = sorted;
   p.S = S;
-  if (sorted) {
+  p.large = sorted && S > kTileMax;
+  if (sorted && !p.large) {
     int64_t spt = S >= kTileMax ? 1 : kTileMax / S;
     p.tile = spt * S;
   } else {
@@ -170,9 +171,10 @@ size_t plan_workspace(Plan& p, void* base) {
     p.seg_cw = reinterpret_cast<uint8_t*>(take((size_t)p.nseg + 16));
   }
 #endif
+  if (p.large) p.large_ws = take(large_ws(p.n, p.nseg));
   if (p.fmt == 1) {
     const size_t xs = (size_t)p.v1_stride, nc = (size_t)p.nchunks;
-    p.v1_xsort = p.sorted ? reinterpret_cast<float*>(take(sizeof(float) * 6 * xs)) : nullptr;
+    p.v1_xsort = p.sorted && !p.large ? reinterpret_cast<float*>(take(sizeof(float) * 6 * xs)) : nullptr;
     p.v1_codes = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 6 * xs));
     p.v1_esc = reinterpret_cast<float*>(take(sizeof(float) * 6 * xs));
     p.v1_esc_cnt = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 6 * nc));
@@ -324,7 +326,8 @@ int nbzg_compress(const nbzg_compress_args* a, void* stream) {
   if (a->interval_count < 2 || (a->interval_count & 1) || a->interval_count > 65536)
     return NBZG_UNSUPPORTED;
   if (a->segment_size < 1 || a->ignored_groups < 0) return NBZG_BAD_ARG;
-  if (a->sorted && a->segment_size > kTileMax) return NBZG_UNSUPPORTED;
+  const bool large = a->sorted && a->segment_size > kTileMax;
+  if (large && (a->cpc || a->rindex_variant == 2)) return NBZG_UNSUPPORTED;
   for (int f = 0; f < 6; f++) {
     if (a->n > 0 && (!a->fields[f] || (reinterpret_cast<uintptr_t>(a->fields[f]) & 15)))
       return NBZG_BAD_ARG;
@@ -358,10 +361,12 @@ int nbzg_compress(const nbzg_compress_args* a, void* stream) {
   }
   if (a->workspace_bytes < plan_workspace(p, nullptr)) return NBZG_BAD_ARG;
   if (a->arena_bytes < nbzg_compress_arena_bound(a->n, a->interval_count)) return NBZG_BAD_ARG;
-  if (!a->meta || (a->sorted && a->n > 0 && (!a->perm || !a->seg_bits))) return NBZG_BAD_ARG;
+  if (!a->meta || (a->sorted && a->n > 0 && ((large ? !a->order32 : !a->perm) || !a->seg_bits)))
+    return NBZG_BAD_ARG;
   plan_workspace(p, a->workspace);
   p.meta = a->meta;
   p.perm = a->perm;
+  p.order32 = a->order32;
   p.seg_bits = a->seg_bits;
   p.arena = a->arena;
   p.arena_bytes = a->arena_bytes;
@@ -372,13 +377,17 @@ int nbzg_compress(const nbzg_compress_args* a, void* stream) {
   if (a->phase == 4) {  // resume a phase-3 call: encode only (payload sizes are final)
     NvtxScope r("K5 encode");
     if (p.n == 0) return cuda_status();
+    if (p.large) {  // the SZ stages read the sorted copies, as in phase 3
+      large_fields(p);
+      p.sorted = 0;
+    }
     if ((rc = launch_encode(p, st))) return rc;
     trace_mark("encode", st);
     return cuda_status();
   }
   // sorted mode with 3-field keys: K1 walks whole segments and also leaves
   // each segment's key-field min/max, so K2 reads the coordinates once
-  const bool segmm = p.sorted && p.variant != 2 && p.n > 0 && p.S % 4 == 0;
+  const bool segmm = p.sorted && !p.large && p.variant != 2 && p.n > 0 && p.S % 4 == 0;
   {
     NvtxScope range("K1 minmax + resolve");
     if (a->phase == 2) {
@@ -397,7 +406,16 @@ int nbzg_compress(const nbzg_compress_args* a, void* stream) {
   }
   trace_mark("resolve", st);
   if (p.n == 0 || a->phase == 1) return cuda_status();
-  if (p.sorted) {
+  if (p.large) {
+    // one device-wide radix sort, then the SZ stages on sorted copies as on
+    // an unsorted snapshot (rlarge.cu)
+    NvtxScope r("K2 rindex_sort (long segments)");
+    bool stop = false;
+    if ((rc = launch_rindex_large(p, st, stop))) return rc;
+    trace_mark("rindex_sort", st);
+    if (stop) return cuda_status();
+    p.sorted = 0;
+  } else if (p.sorted) {
     NvtxScope r("K2 rindex_sort");
     if ((rc = launch_rindex_sort(p, st))) return rc;
     trace_mark("rindex_sort", st);

@@ -62,6 +62,10 @@ struct Plan {
   uint64_t* v1_eoff = nullptr;     // [6][nchunks + 1]
   uint32_t* v1_words = nullptr;    // [6][v1_wstride]
   int64_t v1_wstride = 0;
+  // long segments (sorted, S > 16384: rlarge.cu)
+  int large = 0;
+  uint8_t* large_ws = nullptr;
+  uint32_t* order32 = nullptr;  // [n] source index per sorted position
 };
 
 // one field of a decompress call (decode.cu)
@@ -84,6 +88,9 @@ int launch_minmax_seg(const Plan& p, cudaStream_t st);
 int launch_minmax_set(const float* h_minmax12, uint32_t* minmax12, cudaStream_t st);
 int launch_resolve(const Plan& p, cudaStream_t st);
 int launch_rindex_sort(const Plan& p, cudaStream_t st);
+int launch_rindex_large(Plan& p, cudaStream_t st, bool& stop);
+void large_fields(Plan& p);
+size_t large_ws(int64_t n, int64_t nseg);
 int launch_quantize(const Plan& p, cudaStream_t st, int f0 = 0, int nf = 6);
 int launch_codebook(const Plan& p, cudaStream_t st, int f0 = 0, int nf = 6);
 int launch_layout(const Plan& p, cudaStream_t st, int f0 = 0, int nf = 6, bool first = true);

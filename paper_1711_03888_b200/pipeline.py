@@ -291,12 +291,14 @@ class CompressResult:
     sidecar (``order[i]`` = original index of sorted position i).  Same
     constructor as the reference (``CompressResult(archive, order)``); the
     B200 path passes the device permutation (keyword-only ``perm``, u16
-    tile-local) and the int64 ``order`` is expanded from it on first use."""
+    tile-local; or ``order32``, u32 global, for segments longer than a tile)
+    and the int64 ``order`` is expanded from it on first use."""
 
     def __init__(self, archive: Archive, order: Optional[np.ndarray] = None, *, perm=None,
-                 tile: int = 16384):
+                 tile: int = 16384, order32=None):
         self.archive = archive
         self._perm = perm
+        self._order32 = order32
         self._tile = tile
         self._order = None if order is None else np.asarray(order, np.int64)
 
@@ -304,14 +306,15 @@ class CompressResult:
     def order(self) -> Optional[np.ndarray]:
         if self._order is not None:
             return self._order
-        if self._perm is None:
+        if self._perm is None and self._order32 is None:
             return None
-        if self._order is None:
-            self._order = self.order_device().cpu().numpy()
+        self._order = self.order_device().cpu().numpy()
         return self._order
 
     def order_device(self):
         import torch
+        if self._order32 is not None:
+            return self._order32.to(torch.int64)
         if self._perm is None:
             return None if self._order is None else torch.from_numpy(self._order).cuda()
         n = self.archive.n
@@ -469,8 +472,12 @@ class _CompressCall:
         if ic > 65536:
             raise ValidationError("the B200 path supports interval_count <= 65536")
         S = settings.segment_size
-        if sorted_mode and S > 16384:
-            raise ValidationError("the B200 path supports segment_size <= 16384")
+        # a segment longer than one 16384-particle tile: one device-wide radix
+        # sort instead of the tile-local one (csrc/rlarge.cu)
+        large = bool(sorted_mode and S > 16384)
+        if large and (mode.stores_minima or settings.rindex_variant is RIndexVariant.COORD_VELOCITY):
+            raise ValidationError("segment_size > 16384: sz-lv-prx with coordinate or velocity "
+                                  "keys only on the B200 path")
         ws_bytes = L.nbzg_compress_workspace_size_fmt(n, sorted_mode, ic, S, version)
         self.ws = N.workspace(ws_bytes)
         arena_bytes = L.nbzg_compress_arena_bound(n, ic)
@@ -479,7 +486,9 @@ class _CompressCall:
         nseg = (n + S - 1) // S if sorted_mode else 0
         self.seg_bits = torch.empty(max(nseg, 1), dtype=torch.uint8, device="cuda")
         self.perm = (torch.empty(max(n, 1), dtype=torch.int16, device="cuda")
-                     if sorted_mode else None)
+                     if sorted_mode and not large else None)
+        self.order32 = (torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+                        if large else None)
         cpc = ((1 if mode is Mode.SZ_CPC2000 else 2 if mode is Mode.CPC2000 else 0)
                if sorted_mode else 0)
         self.minima = (torch.empty(3 * max(nseg, 1), dtype=torch.int64, device="cuda")
@@ -507,6 +516,7 @@ class _CompressCall:
         a.meta = N.ptr(self.meta_t)
         a.seg_bits = N.ptr(self.seg_bits)
         a.perm = N.ptr(self.perm) if self.perm is not None else None
+        a.order32 = N.ptr(self.order32) if self.order32 is not None else None
         a.fmt = version
         self.fields, self.mode, self.settings = fields, mode, settings
         self.n, self.S, self.nseg, self.ic, self.cpc = n, S, nseg, ic, cpc
@@ -609,8 +619,9 @@ class _CompressCall:
         nbz_io.payload_crcs_async(archive)
         tile = (max(1, 16384 // S) * S) if S < 16384 else S
         perm = self.perm[:n] if self.perm is not None else None
+        order32 = self.order32[:n] if self.order32 is not None else None
         self.ws = None  # the workspace goes back to the caching allocator
-        return CompressResult(archive, perm=perm, tile=tile)
+        return CompressResult(archive, perm=perm, tile=tile, order32=order32)
 
 
 def _cpc_streams(dev: _Device, cpc: int, fields, n: int, S: int, perm, seg_bits, minima, meta,
