@@ -68,9 +68,12 @@ NBZG_DEV void tq_st(uint32_t* base, uint32_t sbase, int i, uint32_t v) {
   if (SH) sts_u32(sbase + 4u * (uint32_t)i, v);
   else base[i] = v;
 }
-// The merge is sequential; both queue heads and the element behind each
-// head are kept in registers, so the load of the next element overlaps the
-// following picks instead of sitting on the compare chain.
+// The merge is sequential, so its cost is the latency of one pick.  Both
+// queues keep a three-deep register window (head, next, next-next); a pick is
+// compare -> selects, branch-free, with ONE refill load (from whichever queue
+// advanced) two elements ahead of the head, so no load sits on the
+// compare chain.  A freshly produced internal node is patched into the node
+// window when it lands within it (the queue was shorter than the window).
 template <bool SH>
 NBZG_DEV void two_queue_impl(uint32_t* L, uint32_t* I, int k) {
   const uint32_t INF = 0xffffffffu;
@@ -78,33 +81,42 @@ NBZG_DEV void two_queue_impl(uint32_t* L, uint32_t* I, int k) {
   int leaf = 0, node = 0;
   uint32_t wl = tq_ld<SH>(L, Ls, 0);
   uint32_t wl_n = k > 1 ? tq_ld<SH>(L, Ls, 1) : INF;
-  uint32_t wi = INF, wi_n = INF;  // node queue I[node .. nI) empty
+  uint32_t wl_nn = k > 2 ? tq_ld<SH>(L, Ls, 2) : INF;
+  uint32_t wi = INF, wi_n = INF, wi_nn = INF;  // node queue I[node .. nI) empty
   for (int nI = 0; nI < k - 1; nI++) {
     uint32_t w2[2];
 #pragma unroll
     for (int r = 0; r < 2; r++) {
-      if (wl <= wi) {  // leaf wins ties (weight[leaf] <= weight[node])
-        w2[r] = wl;
-        tq_st<SH>(L, Ls, leaf, (uint32_t)nI);
-        leaf++;
-        wl = wl_n;
-        wl_n = leaf + 1 < k ? tq_ld<SH>(L, Ls, leaf + 1) : INF;
-      } else {
-        w2[r] = wi;
-        tq_st<SH>(I, Is, node, (uint32_t)nI);
-        node++;
-        wi = wi_n;
-        wi_n = node + 1 < nI ? tq_ld<SH>(I, Is, node + 1) : INF;
-      }
+      const bool p = wl <= wi;  // leaf wins ties (weight[leaf] <= weight[node])
+      w2[r] = p ? wl : wi;
+      // the parent of the picked element, in place of its weight
+      if (SH) sts_u32(p ? Ls + 4u * (uint32_t)leaf : Is + 4u * (uint32_t)node, (uint32_t)nI);
+      else (p ? L + leaf : I + node)[0] = (uint32_t)nI;
+      leaf += p ? 1 : 0;
+      node += p ? 0 : 1;
+      // refill two ahead of the new head of the queue that advanced
+      const int ri = p ? leaf + 2 : node + 2;
+      const bool ok = p ? ri < k : ri < nI;
+      const int rc = ok ? ri : 0;
+      const uint32_t x0 = SH ? lds_u32((p ? Ls : Is) + 4u * (uint32_t)rc) : (p ? L : I)[rc];
+      const uint32_t x = ok ? x0 : INF;
+      wl = p ? wl_n : wl;
+      wl_n = p ? wl_nn : wl_n;
+      wl_nn = p ? x : wl_nn;
+      wi = p ? wi : wi_n;
+      wi_n = p ? wi_n : wi_nn;
+      wi_nn = p ? wi_nn : x;
     }
     const uint32_t s = w2[0] + w2[1];
     tq_st<SH>(I, Is, nI, s);
-    if (node == nI) wi = s;            // the queue was empty
-    else if (node + 1 == nI) wi_n = s;  // s sits right behind the head
+    const int d = nI - node;  // position of the new node in the queue
+    wi = d == 0 ? s : wi;
+    wi_n = d == 1 ? s : wi_n;
+    wi_nn = d == 2 ? s : wi_nn;
   }
   tq_st<SH>(I, Is, k - 2, INF);
 }
-NBZG_DEV void two_queue(uint32_t* L, uint32_t* I, int k, bool in_smem) {
+__device__ __noinline__ void two_queue(uint32_t* L, uint32_t* I, int k, bool in_smem) {
   if (in_smem) two_queue_impl<true>(L, I, k);
   else two_queue_impl<false>(L, I, k);
 }
@@ -129,8 +141,17 @@ NBZG_DEV void node_depths(const uint32_t* I, uint8_t* D, int ni) {
   }
 }
 
+#ifdef NBZG_CB_PROF  // timing experiment: per-phase clocks of every CTA, printed at exit
+#define CB_T(i) do { __syncthreads(); if (threadIdx.x == 0) { long long _c = clock64(); cb_t[i] = _c - cb_last; cb_last = _c; } } while (0)
+#else
+#define CB_T(i) do { } while (0)
+#endif
+
 __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
+#ifdef NBZG_CB_PROF
+  long long cb_t[8] = {0, 0, 0, 0, 0, 0, 0, 0}, cb_last = clock64();
+#endif
   __shared__ uint32_t scan_u32[33];
   __shared__ unsigned long long scan_u64[33];
   __shared__ uint32_t s_cbl[64];
@@ -148,28 +169,37 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
   const int tid = threadIdx.x;
   const int64_t nb = a.nbins;
 
-  // ---- A. compact non-zero bins, ascending symbol
-  const int R = (int)((nb + kCBThreads - 1) / kCBThreads);
+  // ---- A. compact non-zero bins, ascending symbol: warp w owns the bins
+  // [w * per, (w + 1) * per), read 32 at a time (coalesced) and ranked by
+  // ballot; a block scan of the warp totals gives each warp's output base
   uint32_t* cnt = scr;  // compact counts (global scratch, k entries)
+  const int lane = tid & 31, warp = tid >> 5;
+  const int64_t per = ((nb + kCBThreads - 1) / kCBThreads) * 32;  // bins per warp (multiple of 32)
+  const int64_t b0 = (int64_t)warp * per, b1 = min(nb, b0 + per);
   uint32_t mine = 0;
-  for (int r = 0; r < R; r++) {
-    int64_t bin = (int64_t)tid * R + r;
-    if (bin < nb && hist[bin]) mine++;
+#pragma unroll 4
+  for (int64_t bb = b0; bb < b1; bb += 32) {
+    const int64_t bin = bb + lane;
+    const uint32_t c = bin < b1 ? hist[bin] : 0u;
+    mine += __popc(__ballot_sync(0xffffffffu, c != 0));
   }
   uint32_t ktot;
-  uint32_t off = block_excl_scan<uint32_t>(mine, scan_u32, &ktot);
-  for (int r = 0; r < R; r++) {
-    int64_t bin = (int64_t)tid * R + r;
-    if (bin < nb) {
-      uint32_t c = hist[bin];
-      if (c) {
-        sym[off] = (uint32_t)bin;
-        cnt[off] = c;
-        off++;
-      }
+  uint32_t off = block_excl_scan<uint32_t>(lane == 0 ? mine : 0u, scan_u32, &ktot);
+  off = __shfl_sync(0xffffffffu, off, 0);
+#pragma unroll 4
+  for (int64_t bb = b0; bb < b1; bb += 32) {
+    const int64_t bin = bb + lane;
+    const uint32_t c = bin < b1 ? hist[bin] : 0u;
+    const uint32_t m = __ballot_sync(0xffffffffu, c != 0);
+    if (c) {
+      const uint32_t o = off + __popc(m & ((1u << lane) - 1u));
+      sym[o] = (uint32_t)bin;
+      cnt[o] = c;
     }
+    off += __popc(m);
   }
   const int k = (int)ktot;
+  CB_T(0);  // compaction
   if (tid == 0) {
     fm.k = (uint32_t)k;
     fm.n_esc = hist[0];
@@ -208,9 +238,11 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
       order[i] = (uint16_t)(kv & 0xffff);
     }
     __syncthreads();
+    CB_T(1);  // sort
     // ---- C. two-queue merge (sequential, exact)
     if (tid == 0) two_queue(L, I, k, small);
     __syncthreads();
+    CB_T(2);  // merge
     // ---- D. depths
     node_depths(I, D, k - 1);
     // leaf depth = depth(parent) + 1, scattered to ascending-symbol rank
@@ -220,6 +252,7 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
     }
   }
   __syncthreads();
+  CB_T(3);  // depths
 
   // ---- E. canonical codes (encode.py:123-152)
   if (tid < 64) s_cbl[tid] = 0;
@@ -277,6 +310,7 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
       }
     }
   }
+  CB_T(4);  // canonical codes + tables
   // ---- sizes: total bits = sum count * len
   unsigned long long tb = 0;
   for (int i = tid; i < k; i += kCBThreads) tb += (unsigned long long)cnt[i] * lenr[i];
@@ -299,6 +333,12 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
       fm.payload_len = fm.esc_off;
     }
   }
+#ifdef NBZG_CB_PROF
+  CB_T(5);
+  if (tid == 0)
+    printf("codebook field %d k %d cycles: compact %lld sort %lld merge %lld depths %lld codes %lld sizes %lld\n",
+           field, k, cb_t[0], cb_t[1], cb_t[2], cb_t[3], cb_t[4], cb_t[5]);
+#endif
 }
 
 int launch_codebook_impl(const uint32_t* hist, int64_t nbins, uint32_t* sym, uint8_t* len,

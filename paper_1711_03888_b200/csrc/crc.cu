@@ -4,15 +4,27 @@
 // CRC is linear over GF(2):  crc0(A||B) = Z_|B|(crc0(A)) ^ crc0(B), where
 // crc0 is the zero-init, no-xorout CRC and Z_L ("feed L zero bytes") is a
 // 64x64 bit matrix, applied as 8 byte-sliced lookup tables.  Leading zero
-// bytes do not change crc0, so the stream is front-padded (virtually) to a
-// whole number of 512 KiB CTA spans:
-//   K1 crc_span_kernel: each thread CRCs a 2 KiB block (slicing-by-16 from a
-//      32 KiB shared table, 16-byte loads), the CTA folds its 256 blocks in a
-//      shuffle / shared-memory tree -> crc0 of its span;
+// bytes do not change crc0, so the stream -- minus the < 16 tail bytes past
+// the last 16-byte-aligned address, which the fold kernel appends bytewise --
+// is front-padded (virtually) to a whole number of 512 KiB CTA spans; every
+// 16-byte piece of the padded stream is then aligned in memory:
+//   K1 crc_span_kernel: a warp CRCs a 64 KiB block in 128 coalesced 512-byte
+//      steps, lane j taking the 16-byte piece j of every step.  A lane's pieces
+//      lie 496 bytes apart; "absorb 16 bytes, then 496 zero bytes" is one
+//      linear map of (state ^ piece), so its slicing-by-16 tables are
+//      Z_496 o T_k -- the same 16 lookups per 16 bytes as contiguous slicing.
+//      The tables sit in shared memory entry-major ([byte value][k], 8-byte
+//      entries: table k lives in bank pair k) and lane j visits its bytes in
+//      the rotated order (s + j) mod 16, so the 16 lanes of a half-warp read
+//      16 different tables = 16 different bank pairs: every lookup is
+//      conflict-free (2 wavefronts instead of ~6 for random 8-byte reads).
+//      The last step uses the plain tables; a shuffle tree folds the lanes
+//      (Z_16 ... Z_256), then the CTA's 8 warps -> crc0 of its 512 KiB span;
 //   K2 crc_fold_kernel: one CTA folds the span values (sequential runs, then
 //      a tree) and applies  crc = Z_n(~0) ^ crc0 ^ ~0.
 // The tables (slicing and Z_{2^j}, j = 0..40) are built once on the host and
 // uploaded once per device.  HBM-bound: one read of the data.
+#include <algorithm>
 #include <mutex>
 
 #include "nbzg_internal.cuh"
@@ -28,6 +40,7 @@ constexpr int kFoldThreads = 1024;
 constexpr uint64_t kPoly = 0xC96C5795D7870F42ull;
 
 __device__ uint64_t g_crc_slice[16 * 256];          // T_k[b]: byte b then k zero bytes
+__device__ uint64_t g_crc_skip[256 * 16];           // [b][k]: Z_496(T_k[b]) (interleaved pieces)
 __device__ uint64_t g_crc_z[kCrcLevels * 8 * 256];  // Z_{2^j} byte-sliced
 
 NBZG_DEV uint64_t zshift(const uint64_t* T, uint64_t v) {  // T: [8][256]
@@ -41,6 +54,7 @@ NBZG_DEV uint64_t zshift(const uint64_t* T, uint64_t v) {  // T: [8][256]
 namespace {
 struct CrcTables {
   uint64_t slice[16 * 256];
+  uint64_t skip[256 * 16];
   uint64_t z[kCrcLevels * 8 * 256];
 };
 const CrcTables& host_tables() {
@@ -72,6 +86,12 @@ const CrcTables& host_tables() {
         for (int b = 0; b < 256; b++)
           T->z[(size_t)L * 2048 + j * 256 + b] = apply(P, apply(P, (uint64_t)b << (8 * j)));
     }
+    for (int k = 0; k < 16; k++)  // Z_496 = Z_256 o Z_128 o Z_64 o Z_32 o Z_16
+      for (int b = 0; b < 256; b++) {
+        uint64_t v = T->slice[k * 256 + b];
+        for (int L = 4; L <= 8; L++) v = apply(T->z + (size_t)L * 2048, v);
+        T->skip[b * 16 + k] = v;
+      }
     return T;
   }();
   return *t;
@@ -86,6 +106,7 @@ int upload_tables() {
   if (done[dev]) return NBZG_OK;
   const CrcTables& T = host_tables();
   if (cudaMemcpyToSymbol(g_crc_slice, T.slice, sizeof(T.slice)) != cudaSuccess ||
+      cudaMemcpyToSymbol(g_crc_skip, T.skip, sizeof(T.skip)) != cudaSuccess ||
       cudaMemcpyToSymbol(g_crc_z, T.z, sizeof(T.z)) != cudaSuccess)
     return NBZG_CUDA_ERROR;
   done[dev] = true;
@@ -98,79 +119,127 @@ int upload_tables() {
 constexpr int kCrcMax = 8;
 struct CrcJobs {
   const uint8_t* data[kCrcMax];
-  int64_t n[kCrcMax];
-  int64_t pad[kCrcMax];
-  int64_t span0[kCrcMax + 1];  // first span (CTA) of each buffer; span0[count] = total
+  int64_t n[kCrcMax];       // whole length (the init / xorout term)
+  int64_t n_main[kCrcMax];  // bytes the span kernel covers: ends 16-byte aligned
+  int64_t pad[kCrcMax];     // virtual leading zero bytes of the main part
+  int64_t span0[kCrcMax + 1];  // first span of each buffer; span0[count] = total
   uint64_t* out[kCrcMax];
   int run_log[kCrcMax];
   int count;
 };
 
-// crc0 of each 512 KiB span of each front-padded stream (pad zero bytes,
-// then data[0, n)).
-__global__ void __launch_bounds__(kCrcThreads) crc_span_kernel(CrcJobs J, uint64_t* span_out) {
-  __shared__ uint64_t T[16 * 256];
-  __shared__ uint64_t wsum[kCrcThreads / 32];
-  for (int i = threadIdx.x; i < 16 * 256; i += kCrcThreads) T[i] = g_crc_slice[i];
-  int b = 0;
-  while (b + 1 < J.count && (int64_t)blockIdx.x >= J.span0[b + 1]) b++;
-  const uint8_t* data = J.data[b];
-  const int64_t n = J.n[b], pad = J.pad[b];
-  __syncthreads();
-  const int64_t g = ((int64_t)blockIdx.x - J.span0[b]) * kCrcThreads + threadIdx.x;
-  int64_t s = (g << kCrcBlockLog) - pad, e = s + (1 << kCrcBlockLog);
-  if (s < 0) s = 0;  // leading virtual zeros leave crc0 at 0
-  if (e > n) e = n;
-  if (e < s) e = s;  // block entirely inside the padding
-  uint64_t crc = 0;
-  // unaligned head, 16-byte body, tail
-  while (s < e && ((reinterpret_cast<uintptr_t>(data) + s) & 15)) {
-    crc = T[(crc ^ data[s]) & 0xff] ^ (crc >> 8);
-    s++;
-  }
-  const uint4* q = reinterpret_cast<const uint4*>(data + s);
-  const int64_t nq = (e - s) >> 4;
-  auto step = [&](const uint4 d) {
-    const uint64_t lo = (((uint64_t)d.y << 32) | d.x) ^ crc;
-    const uint64_t hi = ((uint64_t)d.w << 32) | d.z;
-    uint64_t r = 0;
-#pragma unroll
-    for (int k = 0; k < 8; k++) r ^= T[(15 - k) * 256 + ((lo >> (8 * k)) & 0xff)];
-#pragma unroll
-    for (int k = 0; k < 8; k++) r ^= T[(7 - k) * 256 + ((hi >> (8 * k)) & 0xff)];
-    crc = r;
-  };
-  int64_t i = 0;
-  for (; i + 4 <= nq; i += 4) {
-    const uint4 d0 = __ldg(q + i), d1 = __ldg(q + i + 1), d2 = __ldg(q + i + 2),
-                d3 = __ldg(q + i + 3);
-    step(d0);
-    step(d1);
-    step(d2);
-    step(d3);
-  }
-  for (; i < nq; i++) step(__ldg(q + i));
-  for (s += nq << 4; s < e; s++) crc = T[(crc ^ data[s]) & 0xff] ^ (crc >> 8);
+constexpr int kCrcWarpLog = 16;  // 64 KiB per warp: 128 steps of 32 x 16 bytes
+constexpr int kCrcSteps = 1 << (kCrcWarpLog - 9);
 
-  // fold the CTA's 256 blocks: warp tree, then the 8 warp values
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int l = 0; l < 5; l++) {
-    const uint64_t right = __shfl_down_sync(0xffffffffu, crc, 1 << l);
-    const uint64_t shifted = zshift(g_crc_z + (size_t)(kCrcBlockLog + l) * 2048, crc);
-    if ((lane & ((2 << l) - 1)) == 0) crc = shifted ^ right;
-  }
-  if (lane == 0) wsum[warp] = crc;
+// crc0 of each 512 KiB span of each front-padded stream (pad zero bytes,
+// then data[0, n_main)); persistent CTAs, spans strided by the grid.
+__global__ void __launch_bounds__(kCrcThreads) crc_span_kernel(CrcJobs J, uint64_t* span_out) {
+  __shared__ __align__(128) uint64_t TS[256 * 16];  // [byte][k]
+  __shared__ uint64_t wsum[kCrcThreads / 32];
+  for (int i = threadIdx.x; i < 256 * 16; i += kCrcThreads) TS[i] = g_crc_skip[i];
   __syncthreads();
-  if (warp == 0) {
-    crc = lane < kCrcThreads / 32 ? wsum[lane] : 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t jl = (uint32_t)lane & 15u;
+  // step s of a piece reads byte (s + jl) & 15 -> table k = 15 - that byte
+  uint32_t koff[16];
 #pragma unroll
-    for (int l = 0; l < 3; l++) {
+  for (int s = 0; s < 16; s++) koff[s] = ((15u - (uint32_t)s - jl) & 15u) << 3;
+  const uint32_t ts_s = (uint32_t)__cvta_generic_to_shared(TS);
+  const uint32_t rot8 = 8u * (jl & 3u);
+  const bool rw1 = (jl >> 2) & 1u, rw2 = (jl >> 3) & 1u;
+
+  for (int64_t sp = blockIdx.x; sp < J.span0[J.count]; sp += gridDim.x) {
+    int b = 0;
+    while (b + 1 < J.count && sp >= J.span0[b + 1]) b++;
+    const int64_t pad = J.pad[b];
+    // padded offset of this warp's block; piece `lane` of step m at p0 + 512 m
+    const int64_t p0 = ((sp - J.span0[b]) << kCrcSpanLog) + ((int64_t)warp << kCrcWarpLog) + 16 * lane;
+    const uint8_t* base = J.data[b] - pad;  // padded offset 0 (never dereferenced below data)
+    auto load = [&](int m) -> uint4 {
+      const int64_t p = p0 + 512 * (int64_t)m;
+      uint4 d = make_uint4(0, 0, 0, 0);
+      if (p + 16 > pad) {
+        d = __ldg(reinterpret_cast<const uint4*>(base + p));
+        if (p < pad) {  // the piece straddling the start of the data: zero its lead
+          const int lead = (int)(pad - p);  // 1 .. 15
+          uint32_t w[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const int z = lead - 4 * q;  // leading bytes of word q to clear
+            w[q] = z >= 4 ? 0u : (z > 0 ? w[q] & (0xffffffffu << (8 * z)) : w[q]);
+          }
+          d = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      return d;
+    };
+    uint64_t crc = 0;
+    // absorb one piece, then 496 zero bytes (the skip tables)
+    auto step = [&](const uint4 d) {
+      uint32_t w0 = d.x ^ (uint32_t)crc, w1 = d.y ^ (uint32_t)(crc >> 32), w2 = d.z, w3 = d.w;
+      // rotate the 16 bytes right by jl: words, then bytes
+      uint32_t t0 = rw1 ? w1 : w0, t1 = rw1 ? w2 : w1, t2 = rw1 ? w3 : w2, t3 = rw1 ? w0 : w3;
+      w0 = rw2 ? t2 : t0, w1 = rw2 ? t3 : t1, w2 = rw2 ? t0 : t2, w3 = rw2 ? t1 : t3;
+      const uint32_t r[4] = {__funnelshift_r(w0, w1, rot8), __funnelshift_r(w1, w2, rot8),
+                             __funnelshift_r(w2, w3, rot8), __funnelshift_r(w3, w0, rot8)};
+      uint32_t lo = 0, hi = 0;
+#pragma unroll
+      for (int s = 0; s < 16; s++) {
+        const uint32_t x = r[s >> 2];
+        const uint32_t v7 = (s & 3) == 0 ? (x << 7) : ((s & 3) == 1 ? (x >> 1) : ((s & 3) == 2 ? (x >> 9) : (x >> 17)));
+        uint32_t e0, e1;
+        asm("ld.shared.v2.u32 {%0, %1}, [%2];"
+                     : "=r"(e0), "=r"(e1)
+                     : "r"(ts_s + ((v7 & 0x7f80u) | koff[s])));
+        lo ^= e0;
+        hi ^= e1;
+      }
+      crc = ((uint64_t)hi << 32) | lo;
+    };
+    int m = 0;
+    for (; m + 4 < kCrcSteps; m += 4) {
+      const uint4 d0 = load(m), d1 = load(m + 1), d2 = load(m + 2), d3 = load(m + 3);
+      step(d0);
+      step(d1);
+      step(d2);
+      step(d3);
+    }
+    {
+      const uint4 d0 = load(m), d1 = load(m + 1), d2 = load(m + 2), d3 = load(m + 3);
+      step(d0);
+      step(d1);
+      step(d2);
+      // the last piece: plain slicing-by-16 (no trailing zeros)
+      const uint64_t lo = (((uint64_t)d3.y << 32) | d3.x) ^ crc;
+      const uint64_t hi = ((uint64_t)d3.w << 32) | d3.z;
+      uint64_t r = 0;
+#pragma unroll
+      for (int k = 0; k < 8; k++) r ^= __ldg(g_crc_slice + (15 - k) * 256 + ((lo >> (8 * k)) & 0xff));
+#pragma unroll
+      for (int k = 0; k < 8; k++) r ^= __ldg(g_crc_slice + (7 - k) * 256 + ((hi >> (8 * k)) & 0xff));
+      crc = r;
+    }
+    // fold the warp's 32 lanes (lane j ends 16 (31 - j) bytes before the block
+    // end), then the CTA's 8 warps
+#pragma unroll
+    for (int l = 0; l < 5; l++) {
       const uint64_t right = __shfl_down_sync(0xffffffffu, crc, 1 << l);
-      const uint64_t shifted = zshift(g_crc_z + (size_t)(kCrcBlockLog + 5 + l) * 2048, crc);
+      const uint64_t shifted = zshift(g_crc_z + (size_t)(4 + l) * 2048, crc);
       if ((lane & ((2 << l) - 1)) == 0) crc = shifted ^ right;
     }
-    if (lane == 0) span_out[blockIdx.x] = crc;
+    if (lane == 0) wsum[warp] = crc;
+    __syncthreads();
+    if (warp == 0) {
+      crc = lane < kCrcThreads / 32 ? wsum[lane] : 0;
+#pragma unroll
+      for (int l = 0; l < 3; l++) {
+        const uint64_t right = __shfl_down_sync(0xffffffffu, crc, 1 << l);
+        const uint64_t shifted = zshift(g_crc_z + (size_t)(kCrcWarpLog + l) * 2048, crc);
+        if ((lane & ((2 << l) - 1)) == 0) crc = shifted ^ right;
+      }
+      if (lane == 0) span_out[sp] = crc;
+    }
+    __syncthreads();  // wsum is reused by the next span
   }
 }
 
@@ -206,10 +275,13 @@ __global__ void __launch_bounds__(kFoldThreads) crc_fold_kernel(CrcJobs J,
     __syncthreads();
   }
   if (t == 0) {
+    uint64_t c0 = v[0];  // crc0 of the main part; the < 16 tail bytes follow bytewise
+    for (int64_t i = J.n_main[b]; i < n; i++)
+      c0 = __ldg(g_crc_slice + ((c0 ^ J.data[b][i]) & 0xff)) ^ (c0 >> 8);
     uint64_t r = ~0ull;
     for (int j = 0; j < kCrcLevels; j++)
       if ((n >> j) & 1) r = zshift(g_crc_z + (size_t)j * 2048, r);
-    *crc_out = r ^ v[0] ^ ~0ull;
+    *crc_out = r ^ c0 ^ ~0ull;
   }
 }
 
@@ -242,20 +314,26 @@ int launch_crc64_many(const uint8_t* const* data, const int64_t* n, int count, u
     for (int i = 0; i < cnt; i++) {
       const int64_t ni = n[c0 + i];
       if (ni < 0 || (ni >> kCrcLevels)) return NBZG_BAD_ARG;
-      const int64_t C = crc_spans(ni);
+      // the main part ends at the last 16-byte-aligned address of the buffer
+      int64_t tail = (int64_t)((reinterpret_cast<uintptr_t>(data[c0 + i]) + (uint64_t)ni) & 15);
+      if (tail > ni) tail = ni;
+      const int64_t nm = ni - tail;
+      const int64_t C = crc_spans(nm);
       int run_log = 0;
       while ((int64_t(kFoldThreads) << run_log) < C) run_log++;
       // the fold tree's top level is Z_{2^(span_log + run_log + 9)}
       if (kCrcSpanLog + run_log + 9 >= kCrcLevels) return NBZG_BAD_ARG;
       J.data[i] = data[c0 + i];
       J.n[i] = ni;
-      J.pad[i] = (C << kCrcSpanLog) - ni;
+      J.n_main[i] = nm;
+      J.pad[i] = (C << kCrcSpanLog) - nm;
       J.span0[i + 1] = J.span0[i] + C;
       J.out[i] = crc_out + c0 + i;
       J.run_log[i] = run_log;
     }
     count_launch();
-    crc_span_kernel<<<(unsigned)J.span0[cnt], kCrcThreads, 0, st>>>(J, span);
+    const int64_t grid = std::min<int64_t>(J.span0[cnt], 4 * (int64_t)sm_count());
+    crc_span_kernel<<<(unsigned)grid, kCrcThreads, 0, st>>>(J, span);
     count_launch();
     crc_fold_kernel<<<cnt, kFoldThreads, 0, st>>>(J, span);  // (next batch: stream-ordered)
   }
