@@ -92,8 +92,15 @@ NBZG_DEV void fail(uint32_t* status, uint32_t code) { atomicCAS(status, 0u, code
 // ---------------------------------------------------------------- D0: parse
 // Validates the table (HuffmanTable.__post_init__, encode.py:105-121 and
 // deserialize 182-196) and builds the canonical decode tables.
+__device__ void chunk_offsets_body(const DArgs& a, int fi);
+NBZG_DEV void parse_body(const DArgs& a, int fi);
+// grid (nf, 2): row 0 parses the tables, row 1 scans the chunk index (it
+// re-derives the few header fields it needs, so the two run side by side)
 __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
-  const int fi = blockIdx.x;
+  if (blockIdx.y == 0) parse_body(a, (int)blockIdx.x);
+  else chunk_offsets_body(a, (int)blockIdx.x);
+}
+NBZG_DEV void parse_body(const DArgs& a, int fi) {
   const DField& F = a.f[fi];
   DParsed& P = a.parsed[fi];
   uint8_t* lut = reinterpret_cast<uint8_t*>(a.lut) + fi * (1 << kLutBits);
@@ -102,6 +109,7 @@ __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
   __shared__ uint32_t scan_tmp[33];
   __shared__ uint64_t s_fc[64];
   __shared__ uint32_t s_fi[64];
+  __shared__ uint32_t s_lim16[kLutBits + 1];
   const int tid = threadIdx.x;
   const uint8_t* p = F.payload;
   const int64_t L = F.payload_len;
@@ -111,7 +119,8 @@ __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
     s_min = 255;
   }
   if (tid < 64) s_cbl[tid] = 0;
-  for (int i = tid; i < (1 << kLutBits); i += blockDim.x) lut[i] = 0;
+  for (int i = tid; i < (1 << kLutBits) / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(lut)[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   if (L < 8) {
     if (tid == 0) P.status = NBZG_TRUNCATED, fail(a.status, NBZG_TRUNCATED);
@@ -183,22 +192,32 @@ __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
     }
   }
   // length table: entry e (16-bit prefix) -> smallest l with e.. < limit[l]
-  // (canonical order), 0xFE when the code is longer than 16 bits, 0 = invalid
-  for (int e = tid; e < (1 << kLutBits); e += blockDim.x) {
-    uint8_t len = 0;
-    for (int l = 1; l <= max_len; l++) {
-      if (l <= kLutBits) {
-        uint64_t lim = (s_fc[l] + s_cbl[l]) << (kLutBits - l);  // limit in 16-bit units
-        if ((uint64_t)e < lim) {
-          len = (uint8_t)l;
-          break;
-        }
-      } else {
-        len = 0xFE;
-        break;
+  // (canonical order), 0xFE when the code is longer than 16 bits, 0 = invalid.
+  // The limits rise with l, so a thread walks its run of consecutive entries
+  // with one monotone length cursor and stores 16 entries per instruction.
+  if (tid <= kLutBits) {
+    const int l = tid;  // s_lim16[l]: first 16-bit prefix past the codes of length <= l
+    s_lim16[l] = (l >= 1 && l <= max_len) ? (uint32_t)((s_fc[l] + s_cbl[l]) << (kLutBits - l)) : 0u;
+  }
+  __syncthreads();
+  {
+    constexpr int kPer = (1 << kLutBits) / 1024;  // entries per thread (block of 1024)
+    static_assert(kPer % 16 == 0, "16 entries per store");
+    const int e0 = tid * kPer;
+    int l = 1;
+    uint4* dst = reinterpret_cast<uint4*>(lut + e0);
+#pragma unroll 1
+    for (int g = 0; g < kPer / 16; g++) {
+      uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        const uint32_t e = (uint32_t)(e0 + 16 * g + j);
+        while (l <= max_len && l <= kLutBits && e >= s_lim16[l]) l++;
+        const uint32_t len = l > max_len ? 0u : (l > kLutBits ? 0xFEu : (uint32_t)l);
+        w[j >> 2] |= len << (8 * (j & 3));
       }
+      dst[g] = make_uint4(w[0], w[1], w[2], w[3]);
     }
-    lut[e] = len;
   }
   __syncthreads();  // ss (global) complete for the fused table
   // fused tables for the thread-per-chunk decoder.  Entry: bits 0-5 code
@@ -276,31 +295,61 @@ __global__ void __launch_bounds__(1024) parse_kernel(DArgs a) {
 }
 
 // ---------------------------------------------------------------- D1: chunk offsets
-__global__ void __launch_bounds__(1024) chunk_offsets_kernel(DArgs a) {
-  const int fi = blockIdx.x;
-  const DParsed& P = a.parsed[fi];
-  if (P.status || (a.f[fi].kind & 15) != 3) return;
+// Exclusive scan of the v2 chunk index (u32 bit counts, unaligned in the
+// payload).  Independent of parse_body: the index position follows from the
+// header's symbol count; a malformed header is parse_body's to report.
+__device__ void chunk_offsets_body(const DArgs& a, int fi) {
+  const DField& F = a.f[fi];
+  if ((F.kind & 15) != 3) return;
+  const uint8_t* p = F.payload;
+  const uint64_t L = (uint64_t)F.payload_len;
+  if (L < 8) return;
+  const uint64_t k = ld_u32_bytes(p + 4);
+  const uint64_t table_end = 8 + 5 * k;
+  if (k == 0 || k > (uint64_t)a.nbins || table_end + 8 + 4 * (uint64_t)a.nchunks > L) return;
+  const uint64_t total_bits = ld_u64_bytes(p + table_end);
   __shared__ unsigned long long scan_tmp[33];
-  const uint8_t* idx = a.f[fi].payload + P.index_off;
+  const uint8_t* idx = p + table_end + 8;
   uint64_t* off = a.choff + fi * (a.nchunks + 1);
   const int R = (int)((a.nchunks + blockDim.x - 1) / blockDim.x);
+  constexpr int kReg = 16;  // index entries per thread held in registers
+  uint32_t v[kReg];
   unsigned long long s = 0;
-  for (int r = 0; r < R; r++) {
-    int64_t c = (int64_t)threadIdx.x * R + r;
-    if (c < a.nchunks) s += ld_u32_bytes(idx + 4 * c);
+  if (R <= kReg) {
+#pragma unroll
+    for (int r = 0; r < kReg; r++) {
+      const int64_t c = (int64_t)threadIdx.x * R + r;
+      v[r] = (r < R && c < a.nchunks) ? ld_u32_bytes(idx + 4 * c) : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < kReg; r++) s += v[r];
+  } else {
+    for (int r = 0; r < R; r++) {
+      const int64_t c = (int64_t)threadIdx.x * R + r;
+      if (c < a.nchunks) s += ld_u32_bytes(idx + 4 * c);
+    }
   }
   unsigned long long tot;
   unsigned long long ex = block_excl_scan<unsigned long long>(s, scan_tmp, &tot);
-  for (int r = 0; r < R; r++) {
-    int64_t c = (int64_t)threadIdx.x * R + r;
-    if (c < a.nchunks) {
-      off[c] = ex;
-      ex += ld_u32_bytes(idx + 4 * c);
+  if (R <= kReg) {
+#pragma unroll
+    for (int r = 0; r < kReg; r++) {
+      const int64_t c = (int64_t)threadIdx.x * R + r;
+      if (r < R && c < a.nchunks) off[c] = ex;
+      ex += v[r];
+    }
+  } else {
+    for (int r = 0; r < R; r++) {
+      const int64_t c = (int64_t)threadIdx.x * R + r;
+      if (c < a.nchunks) {
+        off[c] = ex;
+        ex += ld_u32_bytes(idx + 4 * c);
+      }
     }
   }
   if (threadIdx.x == 0) {
     off[a.nchunks] = tot;
-    if (tot != P.total_bits) fail(a.status, NBZG_BAD_STREAM);
+    if (tot != total_bits) fail(a.status, NBZG_BAD_STREAM);
   }
 }
 
@@ -1674,11 +1723,8 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
   cudaMemsetAsync(a.lb, 0, sizeof(uint64_t) * nf * 2 * a.nchunks, st);
   cudaMemsetAsync(a.tickets, 0, sizeof(uint32_t) * 16, st);
   count_launch();
-  parse_kernel<<<nf, 1024, 0, st>>>(a);
+  parse_kernel<<<dim3(nf, 2), 1024, 0, st>>>(a);
   trace_mark("dq_parse", st);
-  count_launch();
-  chunk_offsets_kernel<<<nf, 1024, 0, st>>>(a);
-  trace_mark("dq_offsets", st);
   size_t sm = (1 << kLutBits) + kSmemSyms * 2;
   smem_attr((const void*)decode_kernel<true>, (int)sm);
   smem_attr((const void*)decode_kernel<false>, (int)sm);

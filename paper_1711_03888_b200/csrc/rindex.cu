@@ -889,17 +889,25 @@ NBZG_DEV void csort_body(const RArgs& a) {
         for (int v = threadIdx.x; v < m4; v += NT) {
           const float4 q0 = __ldg(x4[0] + v), q1 = __ldg(x4[1] + v), q2 = __ldg(x4[2] + v);
           const float xv[12] = {q0.x, q1.x, q2.x, q0.y, q1.y, q2.y, q0.z, q1.z, q2.z, q0.w, q1.w, q2.w};
-          uint32_t slow = 0;
           uint32_t u[12];
+          bool fine = true;  // one predicate accumulates; the edge set is rebuilt on the rare path
 #pragma unroll
           for (int e = 0; e < 12; e++) {
             const float g = __fmaf_rn(xv[e], invs[e % 3], -cs[e % 3]);
             const float r = __fadd_rd(g, 12582912.0f);
             const float fr = __fsub_rn(g, __fsub_rn(r, 12582912.0f));
-            if (!(fabsf(__fsub_rn(fr, 0.5f)) < lim)) slow |= 1u << e;
+            fine = fine && (fabsf(__fsub_rn(fr, 0.5f)) < lim);
             u[e] = (uint32_t)(__float_as_int(r) - 0x4B400000);
           }
-          if (__any_sync(__activemask(), slow != 0)) {  // bucket edges
+          if (__any_sync(__activemask(), !fine)) {  // bucket edges
+            uint32_t slow = 0;
+#pragma unroll
+            for (int e = 0; e < 12; e++) {
+              const float g = __fmaf_rn(xv[e], invs[e % 3], -cs[e % 3]);
+              const float r = __fadd_rd(g, 12582912.0f);
+              const float fr = __fsub_rn(g, __fsub_rn(r, 12582912.0f));
+              if (!(fabsf(__fsub_rn(fr, 0.5f)) < lim)) slow |= 1u << e;
+            }
 #pragma unroll 1
             for (uint32_t sl = slow; sl; sl &= sl - 1) {
               const int e = __ffs(sl) - 1;
@@ -970,8 +978,12 @@ NBZG_DEV void csort_body(const RArgs& a) {
   if (flagged) {
     if (MODE != 2 && threadIdx.x == 0) a.tile_flags[t] = 1;
   } else if (MODE != 1) {
-    // ---- write the tile's permutation (coalesced)
-    for (int i = threadIdx.x; i < mt; i += NT) a.perm[t0 + i] = perm[i];
+    // ---- write the tile's permutation (coalesced, 16 bytes per lane: tiles
+    // start at multiples of 8 elements whenever the tile size is one)
+    const int m8 = (t0 & 7) ? 0 : mt >> 3;
+    for (int i = threadIdx.x; i < m8; i += NT)
+      reinterpret_cast<uint4*>(a.perm + t0)[i] = reinterpret_cast<const uint4*>(perm)[i];
+    for (int i = 8 * m8 + threadIdx.x; i < mt; i += NT) a.perm[t0 + i] = perm[i];
   }
   __syncthreads();  // perm is reused by the next tile
   CS_T(4);  // write-out
