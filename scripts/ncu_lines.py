@@ -60,5 +60,5 @@ for (loc, txt), r in zip(ins, data):
 S = sum(v[0] for v in agg.values()) or 1
 I = sum(v[1] for v in agg.values()) or 1
 print(f"{cands[0]}: {S} stall samples, {I} warp instructions")
-for loc, (st, ie, ti) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+for loc, (st, ie, ti) in sorted(agg.items(), key=lambda kv: -kv[1][1 if os.environ.get("BY_INST") else 0])[:top]:
     print(f"{100*st/S:5.1f}% stall {100*ie/I:5.1f}% inst  {ti/max(ie,1):4.1f} thr  {loc}")
