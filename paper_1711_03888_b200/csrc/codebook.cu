@@ -56,81 +56,200 @@ NBZG_DEV void bitonic_sort_u64(uint64_t* a, int N) {
     }
 }
 
-// Two-queue Huffman over ascending leaf weights L[0..k).  On return L[i]
-// holds the internal index of leaf i's parent and I[j] that of internal node
-// j's parent (root = k-2 holds 0xffffffff).  Exactly _kernels.py:213-232.
-template <bool SH>
-NBZG_DEV uint32_t tq_ld(uint32_t* base, uint32_t sbase, int i) {
-  return SH ? lds_u32(sbase + 4u * (uint32_t)i) : base[i];
-}
-template <bool SH>
-NBZG_DEV void tq_st(uint32_t* base, uint32_t sbase, int i, uint32_t v) {
-  if (SH) sts_u32(sbase + 4u * (uint32_t)i, v);
-  else base[i] = v;
-}
-// The merge is sequential, so its cost is the latency of one pick.  Both
-// queues keep a three-deep register window (head, next, next-next); a pick is
-// compare -> selects, branch-free, with ONE refill load (from whichever queue
-// advanced) two elements ahead of the head, so no load sits on the
-// compare chain.  A freshly produced internal node is patched into the node
-// window when it lands within it (the queue was shorter than the window).
-template <bool SH>
-NBZG_DEV void two_queue_impl(uint32_t* L, uint32_t* I, int k) {
-  const uint32_t INF = 0xffffffffu;
-  const uint32_t Ls = SH ? sh_addr(L) : 0u, Is = SH ? sh_addr(I) : 0u;
-  int leaf = 0, node = 0;
-  uint32_t wl = tq_ld<SH>(L, Ls, 0);
-  uint32_t wl_n = k > 1 ? tq_ld<SH>(L, Ls, 1) : INF;
-  uint32_t wl_nn = k > 2 ? tq_ld<SH>(L, Ls, 2) : INF;
-  uint32_t wi = INF, wi_n = INF, wi_nn = INF;  // node queue I[node .. nI) empty
-  for (int nI = 0; nI < k - 1; nI++) {
-    uint32_t w2[2];
+// Stable LSD radix sort (4-bit digits) of the k leaves (w, idx) by weight,
+// ping-pong between the A and B arrays, result in A.  Thread t owns the
+// contiguous run [t RK, (t + 1) RK): it counts its digits in registers, eight
+// u64 block scans (two digits each) turn the counts into digit-major /
+// thread-major offsets, and the run is scattered in order -- stable, so equal
+// counts stay in ascending symbol order like the reference's stable argsort.
+NBZG_DEV void radix_sort_leaves(uint32_t* wA, uint16_t* iA, uint32_t* wB, uint16_t* iB, int k,
+                                int bits, unsigned long long* scan_tmp) {
+  const int nt = blockDim.x, tid = threadIdx.x;
+  const int RK = (k + nt - 1) / nt;
+  const int i0 = min(k, tid * RK), i1 = min(k, i0 + RK);
+  int passes = max(2, (bits + 3) / 4);
+  passes += passes & 1;  // even: the result lands in A
+  for (int p = 0; p < passes; p++) {
+    const uint32_t* sw = (p & 1) ? wB : wA;
+    const uint16_t* si = (p & 1) ? iB : iA;
+    uint32_t* dw = (p & 1) ? wA : wB;
+    uint16_t* di = (p & 1) ? iA : iB;
+    const int sh = 4 * p;
+    uint32_t c[16];
 #pragma unroll
-    for (int r = 0; r < 2; r++) {
-      const bool p = wl <= wi;  // leaf wins ties (weight[leaf] <= weight[node])
-      w2[r] = p ? wl : wi;
-      // the parent of the picked element, in place of its weight
-      if (SH) sts_u32(p ? Ls + 4u * (uint32_t)leaf : Is + 4u * (uint32_t)node, (uint32_t)nI);
-      else (p ? L + leaf : I + node)[0] = (uint32_t)nI;
-      leaf += p ? 1 : 0;
-      node += p ? 0 : 1;
-      // refill two ahead of the new head of the queue that advanced
-      const int ri = p ? leaf + 2 : node + 2;
-      const bool ok = p ? ri < k : ri < nI;
-      const int rc = ok ? ri : 0;
-      const uint32_t x0 = SH ? lds_u32((p ? Ls : Is) + 4u * (uint32_t)rc) : (p ? L : I)[rc];
-      const uint32_t x = ok ? x0 : INF;
-      wl = p ? wl_n : wl;
-      wl_n = p ? wl_nn : wl_n;
-      wl_nn = p ? x : wl_nn;
-      wi = p ? wi : wi_n;
-      wi_n = p ? wi_n : wi_nn;
-      wi_nn = p ? wi_nn : x;
+    for (int d = 0; d < 16; d++) c[d] = 0;
+    for (int i = i0; i < i1; i++) {
+      const uint32_t d = sh < 32 ? (sw[i] >> sh) & 15u : 0u;
+#pragma unroll
+      for (int dd = 0; dd < 16; dd++) c[dd] += d == (uint32_t)dd ? 1u : 0u;
     }
-    const uint32_t s = w2[0] + w2[1];
-    tq_st<SH>(I, Is, nI, s);
-    const int d = nI - node;  // position of the new node in the queue
-    wi = d == 0 ? s : wi;
-    wi_n = d == 1 ? s : wi_n;
-    wi_nn = d == 2 ? s : wi_nn;
+    uint32_t base[16], run = 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      unsigned long long tot;
+      const unsigned long long ex = block_excl_scan<unsigned long long>(
+          (unsigned long long)c[2 * q] | ((unsigned long long)c[2 * q + 1] << 32), scan_tmp, &tot);
+      base[2 * q] = run + (uint32_t)ex;
+      run += (uint32_t)tot;
+      base[2 * q + 1] = run + (uint32_t)(ex >> 32);
+      run += (uint32_t)(tot >> 32);
+    }
+    for (int i = i0; i < i1; i++) {
+      const uint32_t w = sw[i];
+      const uint16_t id = si[i];
+      const uint32_t d = sh < 32 ? (w >> sh) & 15u : 0u;
+      uint32_t pos = 0;
+#pragma unroll
+      for (int dd = 0; dd < 16; dd++) {
+        if (d == (uint32_t)dd) {
+          pos = base[dd];
+          base[dd]++;
+        }
+      }
+      dw[pos] = w;
+      di[pos] = id;
+    }
+    __syncthreads();
   }
-  tq_st<SH>(I, Is, k - 2, INF);
-}
-__device__ __noinline__ void two_queue(uint32_t* L, uint32_t* I, int k, bool in_smem) {
-  if (in_smem) two_queue_impl<true>(L, I, k);
-  else two_queue_impl<false>(L, I, k);
 }
 
-// Depth of every internal node (root = ni-1, parent index in I[j], parent >
+// Two-queue Huffman (_kernels.py:213-232) over ascending leaf weights
+// Lw[0..k), run by the whole CTA in batched rounds.  The reference picks,
+// 2 (k - 1) times, the smaller head of the leaf queue and of the FIFO queue of
+// internal nodes (the leaf on ties) and joins consecutive picks in pairs.
+// Internal nodes are created in non-decreasing weight order, so the pick
+// sequence is the stable merge (leaves first on ties) of the leaves with the
+// node queue, and a node created now is never smaller than a node that already
+// exists.  One round therefore settles, in parallel, every pick up to the last
+// EXISTING node: with wmax that node's weight, the cL leaves of weight <= wmax
+// and the e live nodes merge by rank (one binary search per element: a leaf's
+// rank = its index + #nodes < it, a node's = its index + #leaves <= it), the
+// pick left unpaired by the previous round goes in front, consecutive
+// positions pair up into new nodes (weights by atomicAdd) and an odd last
+// pick -- always the node of weight wmax -- is carried over.  Every live node
+// is consumed in the round after its creation, so the number of rounds is at
+// most about twice the tree height (<= 57, else CODE_TOO_LONG), whatever k.
+// Outputs: PL[i] / PI[j] = internal index of leaf i's / node j's parent
+// (root k-2: 0xffff).  Iw: k u32 of scratch (node weights).
+struct TQState {
+  int leaf, node, nI;      // next leaf, first live node, nodes created
+  int carry;               // 0 none, 1 a leaf, 2 a node: picked, not yet paired
+  int carry_idx;
+  uint32_t carry_w;
+  int ncarry_idx;          // the node left over by this round (or -1)
+};
+
+NBZG_DEV int tq_upper(const uint32_t* a, int n, uint32_t w) {  // #elements <= w (a ascending)
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] <= w) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+NBZG_DEV int tq_lower(const uint32_t* a, int n, uint32_t w) {  // #elements < w
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < w) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+NBZG_DEV void two_queue(const uint32_t* Lw, uint32_t* Iw, uint16_t* PL, uint16_t* PI, int k,
+                        TQState* st) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < k; i += nt) Iw[i] = 0;
+  if (tid == 0) {
+    st->leaf = 0;
+    st->node = 0;
+    st->nI = 0;
+    st->carry = 0;
+    st->ncarry_idx = -1;
+  }
+  __syncthreads();
+  while (true) {
+    const int leaf = st->leaf, node = st->node, nI = st->nI, carry = st->carry;
+    if (nI >= k - 1) break;
+    const int e = nI - node;
+    if (e == 0) {
+      // no live node: the carried pick (if any) and the next leaves make one pair
+      if (tid == 0) {
+        uint32_t sum = 0;
+        int lf = leaf;
+        if (carry == 1) PL[st->carry_idx] = (uint16_t)nI, sum += st->carry_w;
+        else if (carry == 2) PI[st->carry_idx] = (uint16_t)nI, sum += st->carry_w;
+        for (int c = carry ? 1 : 0; c < 2; c++) {
+          sum += Lw[lf];
+          PL[lf] = (uint16_t)nI;
+          lf++;
+        }
+        Iw[nI] = sum;
+        st->leaf = lf;
+        st->nI = nI + 1;
+        st->carry = 0;
+      }
+      __syncthreads();
+      continue;
+    }
+    const uint32_t wmax = Iw[nI - 1];
+    const int cL = tq_upper(Lw + leaf, k - leaf, wmax);
+    const int T = cL + e, c = carry ? 1 : 0;
+    const bool odd = (T + c) & 1;
+    if (tid == 0 && carry) {  // the carried pick opens the sequence: position 0
+      if (carry == 1) PL[st->carry_idx] = (uint16_t)nI;
+      else PI[st->carry_idx] = (uint16_t)nI;
+      atomicAdd(&Iw[nI], st->carry_w);
+    }
+    for (int t = tid; t < T; t += nt) {
+      if (t < cL) {
+        const uint32_t w = Lw[leaf + t];
+        const int pos = t + tq_lower(Iw + node, e, w) + c;
+        PL[leaf + t] = (uint16_t)(nI + (pos >> 1));
+        atomicAdd(&Iw[nI + (pos >> 1)], w);
+      } else {
+        const int j = t - cL;
+        const uint32_t w = Iw[node + j];
+        const int pos = j + tq_upper(Lw + leaf, cL, w) + c;
+        if (odd && pos == T + c - 1) {
+          st->ncarry_idx = node + j;  // (one thread: the last pick is the last node)
+        } else {
+          PI[node + j] = (uint16_t)(nI + (pos >> 1));
+          atomicAdd(&Iw[nI + (pos >> 1)], w);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      st->leaf = leaf + cL;
+      st->node = nI;
+      st->nI = nI + ((T + c) >> 1);
+      if (odd) {
+        st->carry = 2;
+        st->carry_idx = st->ncarry_idx;
+        st->carry_w = Iw[st->ncarry_idx];
+      } else {
+        st->carry = 0;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) PI[k - 2] = 0xffff;
+  __syncthreads();
+}
+
+// Depth of every internal node (root = ni-1, parent index in P[j], parent >
 // child): level-synchronous passes until no node changes (<= 58 passes).
-NBZG_DEV void node_depths(const uint32_t* I, uint8_t* D, int ni) {
+NBZG_DEV void node_depths(const uint16_t* P, uint8_t* D, int ni) {
   for (int j = threadIdx.x; j < ni; j += blockDim.x) D[j] = (j == ni - 1) ? 0 : 0xff;
   __syncthreads();
   while (true) {
     int changed = 0;
     for (int j = threadIdx.x; j < ni; j += blockDim.x) {
       if (D[j] == 0xff) {
-        uint8_t dp = D[I[j]];
+        uint8_t dp = D[P[j]];
         if (dp != 0xff) {
           D[j] = (uint8_t)min(dp + 1, 254);
           changed = 1;
@@ -177,7 +296,7 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
   const int64_t per = ((nb + kCBThreads - 1) / kCBThreads) * 32;  // bins per warp (multiple of 32)
   const int64_t b0 = (int64_t)warp * per, b1 = min(nb, b0 + per);
   uint32_t mine = 0;
-#pragma unroll 4
+#pragma unroll 8
   for (int64_t bb = b0; bb < b1; bb += 32) {
     const int64_t bin = bb + lane;
     const uint32_t c = bin < b1 ? hist[bin] : 0u;
@@ -186,7 +305,7 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
   uint32_t ktot;
   uint32_t off = block_excl_scan<uint32_t>(lane == 0 ? mine : 0u, scan_u32, &ktot);
   off = __shfl_sync(0xffffffffu, off, 0);
-#pragma unroll 4
+#pragma unroll 8
   for (int64_t bb = b0; bb < b1; bb += 32) {
     const int64_t bin = bb + lane;
     const uint32_t c = bin < b1 ? hist[bin] : 0u;
@@ -211,44 +330,81 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
     return;
   }
 
-  // memory for the merge: shared for k <= 16384, else global scratch.
-  // layout (N = pow2 >= k): keys u64[N] | L u32[N] | order u16[N]; after the
-  // split the keys region is reused for I u32[N] | D u8[N].
+  // memory for the sort and the merge: shared for k <= 16384, else global
+  // scratch (L2-resident).  Layout (N = pow2 >= k), byte offsets:
+  //   sort   A: L u32 @8N, order u16 @12N     B: tmp u32 @0, tmp u16 @4N
+  //   merge  Iw u32 @0, PL u16 @4N, PI u16 @6N, L @8N
+  // Depths and the canonical-code pass then run out of shared memory in both
+  // cases: D u8[k] and a copy of the lengths by rank (s_len) overlay dead
+  // arrays; the large-k case first copies PI into the (otherwise unused)
+  // shared memory.
   const bool small = k <= kCBSmemK;
   uint8_t* base = small ? smem : reinterpret_cast<uint8_t*>(scr + a.nbins);  // after cnt
   int N = 1;
   while (N < k) N <<= 1;
-  uint64_t* keys = reinterpret_cast<uint64_t*>(base);
   uint32_t* L = reinterpret_cast<uint32_t*>(base + 8 * (size_t)N);
   uint16_t* order = reinterpret_cast<uint16_t*>(base + 12 * (size_t)N);
-  uint32_t* I = reinterpret_cast<uint32_t*>(base);
-  uint8_t* D = base + 4 * (size_t)N;
+  uint32_t* Iw = reinterpret_cast<uint32_t*>(base);
+  uint16_t* PL = reinterpret_cast<uint16_t*>(base + 4 * (size_t)N);
+  uint16_t* PI = reinterpret_cast<uint16_t*>(base + 6 * (size_t)N);
+  uint16_t* PIs = small ? PI : reinterpret_cast<uint16_t*>(smem);  // parents, shared
+  uint8_t* D = small ? smem : smem + 2 * (size_t)N;                 // node depths, shared
+  uint8_t* s_len = small ? smem + (size_t)N : smem;                 // lengths by rank, shared
+  __shared__ TQState tq_state;
+  __shared__ uint32_t s_wmax;
 
   if (k == 1) {
-    if (tid == 0) lenr[0] = 1;  // _kernels.py:207-209
+    if (tid == 0) lenr[0] = 1, s_len[0] = 1;  // _kernels.py:207-209
   } else {
-    // ---- B. sort leaves by (count, rank)
-    for (int i = tid; i < N; i += kCBThreads)
-      keys[i] = i < k ? (((uint64_t)cnt[i] << 16) | (uint64_t)i) : ~0ull;
-    __syncthreads();
-    bitonic_sort_u64(keys, N);
-    for (int i = tid; i < k; i += kCBThreads) {
-      uint64_t kv = keys[i];
-      L[i] = (uint32_t)(kv >> 16);
-      order[i] = (uint16_t)(kv & 0xffff);
+    // ---- B. sort leaves by (count, rank) = the reference's stable argsort by
+    // count.  Measured (C3, cycles): bitonic on (count << 16 | rank) keys 16 K
+    // at N = 512, 146 K at N = 8192; the stable radix sort 55 K and 102 K.
+    // Radix for the large shared-memory cases, bitonic otherwise (also for the
+    // global-scratch case, where the radix sort's per-thread runs serialise
+    // on L2 latency).
+    if (small && N >= 8192) {
+      if (tid == 0) s_wmax = 0;
+      __syncthreads();
+      uint32_t mx = 0;
+      for (int i = tid; i < k; i += kCBThreads) {
+        const uint32_t c = cnt[i];
+        L[i] = c;
+        order[i] = (uint16_t)i;
+        mx = max(mx, c);
+      }
+      atomicMax(&s_wmax, mx);
+      __syncthreads();
+      radix_sort_leaves(L, order, Iw, PL, k, 32 - __clz(s_wmax), scan_u64);
+    } else {
+      uint64_t* keys = reinterpret_cast<uint64_t*>(base);
+      for (int i = tid; i < N; i += kCBThreads)
+        keys[i] = i < k ? (((uint64_t)cnt[i] << 16) | (uint64_t)i) : ~0ull;
+      __syncthreads();
+      bitonic_sort_u64(keys, N);
+      for (int i = tid; i < k; i += kCBThreads) {
+        uint64_t kv = keys[i];
+        L[i] = (uint32_t)(kv >> 16);
+        order[i] = (uint16_t)(kv & 0xffff);
+      }
+      __syncthreads();
     }
-    __syncthreads();
     CB_T(1);  // sort
-    // ---- C. two-queue merge (sequential, exact)
-    if (tid == 0) two_queue(L, I, k, small);
-    __syncthreads();
+    // ---- C. two-queue merge (exact; batched rounds, whole CTA)
+    two_queue(L, Iw, PL, PI, k, &tq_state);
     CB_T(2);  // merge
-    // ---- D. depths
-    node_depths(I, D, k - 1);
+    // ---- D. depths (shared memory)
+    if (!small) {
+      for (int i = tid; i < k - 1; i += kCBThreads) PIs[i] = PI[i];
+      __syncthreads();
+    }
+    node_depths(PIs, D, k - 1);
     // leaf depth = depth(parent) + 1, scattered to ascending-symbol rank
+    // (s_len overlays only arrays that are dead by now: Iw, or the PI copy)
     for (int i = tid; i < k; i += kCBThreads) {
-      uint32_t d = (uint32_t)D[L[i]] + 1;
-      lenr[order[i]] = (uint8_t)min(d, 255u);
+      const uint32_t d = (uint32_t)D[PL[i]] + 1;
+      const uint8_t d8 = (uint8_t)min(d, 255u);
+      lenr[order[i]] = d8;
+      s_len[order[i]] = d8;
     }
   }
   __syncthreads();
@@ -262,7 +418,7 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
   }
   __syncthreads();
   for (int i = tid; i < k; i += kCBThreads) {
-    uint32_t l = lenr[i];
+    uint32_t l = s_len[i];
     atomicAdd(&s_cbl[min(l, 63u)], 1u);
     atomicMax(&s_max, l);
     atomicMin(&s_min, l);
@@ -290,13 +446,13 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
     uint32_t c = 0;
     for (int r = 0; r < RK; r++) {
       int i = tid * RK + r;
-      if (i < k && lenr[i] == l) c++;
+      if (i < k && s_len[i] == l) c++;
     }
     uint32_t tot;
     uint32_t ex = block_excl_scan<uint32_t>(c, scan_u32, &tot);
     for (int r = 0; r < RK; r++) {
       int i = tid * RK + r;
-      if (i < k && lenr[i] == l) {
+      if (i < k && s_len[i] == l) {
         lut[sym[i]] = ((uint64_t)l << 57) | (s_fc[l] + ex);
         if (a.tlen8) a.tlen8[field * a.nbins + sym[i]] = (uint8_t)l;
         if (a.twin) {
@@ -313,7 +469,7 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
   CB_T(4);  // canonical codes + tables
   // ---- sizes: total bits = sum count * len
   unsigned long long tb = 0;
-  for (int i = tid; i < k; i += kCBThreads) tb += (unsigned long long)cnt[i] * lenr[i];
+  for (int i = tid; i < k; i += kCBThreads) tb += (unsigned long long)cnt[i] * s_len[i];
   unsigned long long tbits;
   block_excl_scan<unsigned long long>(tb, scan_u64, &tbits);
   if (tid == 0) {
@@ -367,12 +523,15 @@ __global__ void __launch_bounds__(kCBThreads) huffman_lengths_kernel(const uint3
                                                                      uint32_t* scr,
                                                                      uint32_t* status) {
   extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ TQState tq_state;
   const bool small = k <= kCBSmemK;
   int N = 1;
   while (N < k) N <<= 1;
   uint8_t* base = small ? smem : reinterpret_cast<uint8_t*>(scr);
-  uint32_t* I = reinterpret_cast<uint32_t*>(base);
-  uint8_t* D = base + 4 * (size_t)N;
+  uint32_t* Iw = reinterpret_cast<uint32_t*>(base);
+  uint16_t* PL = reinterpret_cast<uint16_t*>(base + 4 * (size_t)N);
+  uint16_t* PI = reinterpret_cast<uint16_t*>(base + 6 * (size_t)N);
+  uint8_t* D = base;
   uint32_t* L = reinterpret_cast<uint32_t*>(base + 8 * (size_t)N);
   const int tid = threadIdx.x;
   if (k == 1) {
@@ -381,11 +540,10 @@ __global__ void __launch_bounds__(kCBThreads) huffman_lengths_kernel(const uint3
   }
   for (int i = tid; i < k; i += kCBThreads) L[i] = counts[i];
   __syncthreads();
-  if (tid == 0) two_queue(L, I, k, small);
-  __syncthreads();
-  node_depths(I, D, k - 1);
+  two_queue(L, Iw, PL, PI, k, &tq_state);
+  node_depths(PI, D, k - 1);
   for (int i = tid; i < k; i += kCBThreads) {
-    uint32_t d = (uint32_t)D[L[i]] + 1;
+    uint32_t d = (uint32_t)D[PL[i]] + 1;
     lengths[i] = (uint8_t)min(d, 255u);
     if (d > kMaxCodeLen) atomicCAS(status, 0u, (uint32_t)NBZG_CODE_TOO_LONG);
   }

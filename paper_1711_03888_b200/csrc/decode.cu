@@ -768,7 +768,11 @@ __global__ void __launch_bounds__(kDThreads, 1) decode_kernel(DArgs a) {
 // f32(k * 2b).  Outputs are buffered 8 at a time and written as two 16-byte
 // stores (one full sector per lane).  Escapes and codes longer than 15 bits
 // take the canonical slow path (limits + symbol table, also in smem).
-constexpr int kTpcMinChunks = 256;
+// A thread's chunk takes ~1.4-3 ms whatever the input size, the warp decoder's
+// time grows with n: measured crossover (scripts/path_crossover.py, HACC-like
+// slabs, eb 1e-4) between 1536 and 2048 chunks per field (1024: 1.24 vs
+// 2.09 ms, 2048: 2.30 vs 2.04 ms).
+constexpr int kTpcMinChunks = 1792;
 
 // Per-lane bit reader of the thread-per-chunk decoder.  The window (w0, w1)
 // lives in registers; the words after it come from an 8-word ring per lane

@@ -23,15 +23,19 @@ def main():
     ap.add_argument("--compress-only", action="store_true")
     ap.add_argument("--trace", action="store_true", help="print per-stage ms of the last rep")
     ap.add_argument("--crc", action="store_true", help="also serialise (payload CRC-64s)")
+    ap.add_argument("--eb", type=float, default=1e-4)
+    ap.add_argument("--workload", default=None, help="a datagen.CONFIGS name instead of the C2 slab")
     args = ap.parse_args()
     from paper_1711_03888_b200 import _native as N
-    spec = datagen.HaccSpec((640, 640, 640), 2.5)
-    fields = datagen.generate(spec, 0, args.n)
+    if args.workload:
+        fields = datagen.generate(args.workload)
+    else:
+        fields = datagen.generate(datagen.HaccSpec((640, 640, 640), 2.5), 0, args.n)
     snap = nbz.ParticleSnapshot(*[torch.from_numpy(f).cuda() for f in fields])
     for r in range(args.reps):
         if args.trace and r == args.reps - 1:
             N.trace_enable(True)
-        res = nbz.compress(snap, args.mode, nbz.ErrorBoundSpec.relative(1e-4))
+        res = nbz.compress(snap, args.mode, nbz.ErrorBoundSpec.relative(args.eb))
         if args.crc:
             from paper_1711_03888_b200 import io as nio
             nio._payload_crcs(res.archive)
