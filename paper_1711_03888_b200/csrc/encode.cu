@@ -637,11 +637,11 @@ __global__ void __launch_bounds__(kEFWarps * 32, 2) encode_fast_kernel(EArgs a) 
 // index); E3 packs each block with ONE thread at its known offset: no
 // look-back, no merges.  A block writes the words whose first bit it holds;
 // its last, partial word is completed with the leading bits of the stream
-// after it (a few codes of lookahead).  Below ~5000 chunks per field the
-// one-launch warp encoder (and quantising all six fields at once) is faster:
-// quantise + encode 1.81 vs 1.96 ms at 4096 chunks, 2.63 vs 2.24 ms at 6144
-// (scripts/path_crossover.py); at 256 chunks 0.20 vs 0.69 ms.
-constexpr int kTpcEncMinChunks = 5120;
+// after it (a few codes of lookahead).  With the field-group overlap this
+// path wins from 128 chunks per field up (whole compress 0.44 vs 0.47 ms at
+// 128, 0.91 vs 1.06 ms at 1024, 2.47 vs 2.83 ms at 4096 chunks; equal at 64:
+// scripts/path_crossover.py).
+constexpr int kTpcEncMinChunks = 128;
 constexpr int kBlk = 512;                  // codes per block (= warp encoder's lane share)
 constexpr int kBlkPerChunk = kChunk / kBlk;
 constexpr int kE1Warps = 16;

@@ -30,6 +30,7 @@ for n in sizes:
             for k, v in N.trace_read():
                 best[k] = min(best.get(k, 1e9), v)
             N.trace_enable(False)
+        comp = sum(v for k, v in best.items() if not k.startswith("dq_"))
+        sz = sum(best.get(k, 0) for k in ("quantize", "codebook", "layout", "encode"))
         print(f"n={n} (~2^{lg}) chunks/field={n // 16384} enc={enc} dec={dec} "
-              f"encode={best.get('encode', 0):.3f} dq_decode={best.get('dq_decode', 0):.3f} "
-              f"quantize={best.get('quantize', 0):.3f}", flush=True)
+              f"compress={comp:.3f} sz_stages={sz:.3f} dq_decode={best.get('dq_decode', 0):.3f}", flush=True)
