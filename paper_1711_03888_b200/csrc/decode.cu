@@ -50,6 +50,9 @@ constexpr int kRingStride = 1024;  // words between ring slots (power of two, >=
 // decode_lv_kernel's ring: slot stride = its thread cap
 constexpr int kLvStride = NBZG_LV_RING == 16 ? 768 : kRingStride;
 constexpr int kTpcTab = (1 << kTpcBits) + kTpc2Cap;
+constexpr double kCanonMass = 0.99;   // fused-table coverage below which the canonical mode decodes
+constexpr int kCanonMaxK = 65536;     // its symbol table: u16 by canonical rank, <= 128 KiB
+constexpr int kCanonBits = 11;        // first-length table index bits
 
 struct DParsed {
   uint64_t n_esc, k, total_bits;
@@ -60,6 +63,7 @@ struct DParsed {
   uint64_t esc_code;  // its canonical code word: first_code[esc_len] (rank 0)
   uint64_t t2_r0;     // thread-per-chunk secondary table: window start,
   uint32_t t2_w, t2_n;  // resolution bits and entry count (0 = none)
+  uint32_t use_canon;   // thread-per-chunk decoder: canonical mode (large alphabets)
   uint64_t first_code[64];
   uint32_t first_idx[64];
   uint32_t counts[64];
@@ -262,7 +266,19 @@ NBZG_DEV void parse_body(const DArgs& a, int fi) {
       P.t2_r0 = R0;
       P.t2_w = (uint32_t)W;
       P.t2_n = n2;
+      // Share of the symbols the fused tables resolve, estimated from the
+      // code lengths (a Huffman code of length l has probability ~2^-l): the
+      // codes of <= max(15, W) bits.  One unresolved symbol replays its whole
+      // 8-symbol group on the exact path for every lane of the warp, so below
+      // ~99% the canonical mode (symbols by rank in shared memory, two or
+      // three dependent lookups per symbol, no replays) is faster.
+      const int lres = n2 ? max(W, kTpcBits) : kTpcBits;
+      double mass = 0.0;
+      for (int l = 1; l <= min(max_len, lres); l++) mass += ldexp((double)s_cbl[l], -l);
+      P.use_canon = (mass < kCanonMass && k <= (uint64_t)kCanonMaxK && max_len <= 32) ? 1u : 0u;
     }
+  } else if (tid == 0) {
+    P.use_canon = 0;
   }
   if (tid == 0) {
     const uint64_t table_end = 8 + 5 * k;
@@ -1428,6 +1444,79 @@ NBZG_DEV void lv_chunks(const LvCtx& X, const DArgs& a, const uint64_t* choff, u
 }
 
 
+// ---- canonical mode of the thread-per-chunk decoder (large alphabets) ----
+// When most codes are longer than the fused tables resolve (k ~ 2^15-2^16
+// symbols at tight error bounds: code lengths 14-18), every group would be
+// replayed on the exact path, whose symbol lookup is a global load.  This
+// mode keeps the canonical decode (encode.py:242-261) entirely in shared
+// memory instead: the symbols by canonical rank (u16, <= 128 KiB), the
+// left-aligned limits and rank bases per length, and a 2^11-entry table with
+// the first length possible for an 11-bit prefix.  A symbol is
+//   l = first[v >> 21];  while (v >= limit[l]) l++;          (0-2 steps)
+//   sym = syms[base[l] + (v >> (32 - l))]
+// i.e. three or four dependent shared-memory reads and no speculation.
+struct CanonCtx {
+  const uint16_t* syms;
+  const uint8_t* first;
+  const uint64_t* limit;  // [l]: first window value past the codes of length <= l (<= 2^32)
+  const int32_t* base;    // [l]: rank of the first code of length l minus its code value
+  int max_len, bias;
+};
+
+NBZG_DEV void canon_step(const LvCtx& X, const CanonCtx& C, LvChunk& S, float& o) {
+  lv_fill_safe(X, S);
+  const uint32_t v = S.R.hi;
+  int l = C.first[v >> (32 - kCanonBits)];
+  while (l <= C.max_len && (uint64_t)v >= C.limit[l]) l++;
+  if (l > C.max_len) {  // outside the code (incomplete table)
+    S.err = NBZG_INVALID_CODE;
+    l = 1;
+    bb_take(S.R, 1);
+    o = 0.0f;
+    return;
+  }
+  const uint32_t sym = C.syms[C.base[l] + (int32_t)(v >> (32 - l))];
+  bb_take(S.R, (uint32_t)l);
+  if (sym == 0) {  // escape: the raw f32 follows
+    lv_fill_safe(X, S);
+    o = __uint_as_float(S.R.hi);
+    S.k = esc_k(o, *X.F);
+    bb_take(S.R, 32);
+  } else {
+    S.k += (long long)((int)sym - C.bias);
+    o = (float)__dmul_rn((double)S.k, X.twob);
+  }
+}
+
+NBZG_DEV void canon_chunks(const LvCtx& X, const CanonCtx& C, const DArgs& a, const uint64_t* choff,
+                           uint32_t a0, int64_t cb, int64_t ce, uint32_t* ring, bool vec) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  for (int64_t c = cb + tid; c < ce; c += nthr) {
+    LvChunk A;
+    lv_start(X, a, choff, a0, c, ring, A);
+    int i = 0;
+    if (vec) {
+      for (; i + 8 <= A.mc && lv_consumed(A) <= A.Tb; i += 8) {
+        float o[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) canon_step(X, C, A, o[q]);
+        bb_refill(A.R, A.ring, X.G, X.vmax);
+        st_v8_cs(A.dst + i, o);
+      }
+    }
+    for (; i < A.mc && lv_consumed(A) <= A.Tb; i++) {
+      float o;
+      canon_step(X, C, A, o);
+      if ((i & 7) == 7) bb_refill(A.R, A.ring, X.G, X.vmax);
+      A.dst[i] = o;
+    }
+    const uint64_t pos = lv_consumed(A);
+    if (!A.err && pos != A.Tb) A.err = pos > A.Tb ? NBZG_TRUNCATED : NBZG_BAD_STREAM;
+    if (A.err) fail(a.status, (uint32_t)A.err);
+  }
+}
+
+
 __global__ void __launch_bounds__(kLvMaxThreads, 1) decode_lv_kernel(DArgs a) {
   extern __shared__ __align__(16) uint8_t dsm2[];
   int32_t* LT = reinterpret_cast<int32_t*>(dsm2);  // [2^15 + t2_n]
@@ -1445,6 +1534,47 @@ __global__ void __launch_bounds__(kLvMaxThreads, 1) decode_lv_kernel(DArgs a) {
   if (cb >= ce) return;
   const int tid = threadIdx.x, nthr = blockDim.x;
   uint32_t* ring = reinterpret_cast<uint32_t*>(dsm2 + 4 * kTpcTab) + tid;  // [kLvRing][kRingStride]
+  if (P.use_canon) {
+    // shared layout: syms u16[k] | first u8[2^11] (both inside the fused
+    // table's 180 KiB), then the ring as in the fused mode
+    uint16_t* c_syms = reinterpret_cast<uint16_t*>(dsm2);
+    uint8_t* c_first = dsm2 + 2 * (size_t)kCanonMaxK;
+    const uint32_t* gs = a.ssyms + fi * a.nbins;
+    for (uint32_t i = tid; i < (uint32_t)P.k; i += nthr) c_syms[i] = (uint16_t)__ldg(gs + i);
+    if (tid < 64) {
+      const int l = tid;
+      uint64_t lim = 0;
+      int32_t bs = 0;
+      if (l >= 1 && l <= 32 && l <= (int)P.max_len) {
+        lim = (P.first_code[l] + P.counts[l]) << (32 - l);
+        bs = (int32_t)P.first_idx[l] - (int32_t)P.first_code[l];
+      }
+      s_limit[l] = lim;
+      s_base[l] = bs;
+    }
+    __syncthreads();
+    for (uint32_t pfx = tid; pfx < (1u << kCanonBits); pfx += nthr) {
+      const uint64_t v = (uint64_t)pfx << (32 - kCanonBits);
+      int l = 1;
+      while (l <= (int)P.max_len && v >= s_limit[l]) l++;
+      c_first[pfx] = (uint8_t)min(l, 33);
+    }
+    __syncthreads();
+    LvCtx X{};
+    const uintptr_t bits_addr = reinterpret_cast<uintptr_t>(F.payload + P.bits_off);
+    constexpr uintptr_t kAl = NBZG_LV_RING == 16 ? 31 : 15;
+    X.G = reinterpret_cast<const uint4*>(bits_addr & ~kAl);
+    X.G32 = reinterpret_cast<const uint32_t*>(X.G);
+    const uint32_t a0 = (uint32_t)(bits_addr & kAl) * 8;
+    X.vmax = (uint32_t)((a0 / 8 + 4 * ((P.total_bits + 31) / 32) + 16) / 16);
+    X.wmax = 4 * X.vmax + 3;
+    X.F = &F;
+    X.twob = F.twob;
+    CanonCtx C{c_syms, c_first, s_limit, s_base, (int)P.max_len, a.half + 1};
+    const bool vec = (reinterpret_cast<uintptr_t>(F.out) & 31) == 0;
+    canon_chunks(X, C, a, a.choff + fi * (a.nchunks + 1), a0, cb, ce, ring, vec);
+    return;
+  }
   const uint32_t n2 = P.t2_n;
   // shared table: the primary entries of the 15-bit prefixes below r0, then
   // the long-code entries (lv_index); one unresolved entry when long codes
