@@ -113,6 +113,87 @@ NBZG_DEV void radix_sort_leaves(uint32_t* wA, uint16_t* iA, uint32_t* wB, uint16
   }
 }
 
+// The same sort for leaves in global scratch (k > 16384): elements are read
+// in order, 1024 per round and coalesced; MATCH.ANY ranks equal digits inside
+// a warp, u16 counters per (round, warp, digit) in shared memory are scanned
+// digit-major, and the second sweep scatters.  cnt: R * 32 * 16 u16.
+NBZG_DEV void radix_sort_leaves_striped(uint32_t* wA, uint16_t* iA, uint32_t* wB, uint16_t* iB, int k,
+                                        int bits, uint16_t* cnt, uint32_t* scan_tmp) {
+  const int nt = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int R = (k + nt - 1) / nt;
+  const int RW = R * 32;       // (round, warp) slots; counters digit-major: cnt[d * RW + r * 32 + warp]
+  const int C = RW * 16;
+  int passes = max(2, (bits + 3) / 4);
+  passes += passes & 1;
+  for (int p = 0; p < passes; p++) {
+    const uint32_t* sw = (p & 1) ? wB : wA;
+    const uint16_t* si = (p & 1) ? iB : iA;
+    uint32_t* dw = (p & 1) ? wA : wB;
+    uint16_t* di = (p & 1) ? iA : iB;
+    const int sh = 4 * p;
+    for (int r0 = 0; r0 < R; r0 += 4) {  // four rounds' loads in flight
+      uint32_t wv[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int i = (r0 + u) * nt + tid;
+        wv[u] = (r0 + u < R && i < k) ? sw[i] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int r = r0 + u;
+        if (r >= R) break;  // uniform
+        const bool valid = r * nt + tid < k;
+        const uint32_t d = valid ? (sh < 32 ? (wv[u] >> sh) & 15u : 0u) : 16u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        uint16_t* c = cnt + r * 32 + warp;
+        if (lane < 16) c[lane * RW] = 0;
+        __syncwarp();
+        if (valid && (peers & lanemask_lt()) == 0) c[d * RW] = (uint16_t)__popc(peers);
+      }
+    }
+    __syncthreads();
+    {  // exclusive scan of the digit-major counters
+      const int per = (C + nt - 1) / nt;
+      const int q0 = min(C, tid * per), q1 = min(C, q0 + per);
+      uint32_t sum = 0;
+      for (int q = q0; q < q1; q++) sum += cnt[q];
+      uint32_t tot;
+      uint32_t ex = block_excl_scan<uint32_t>(sum, scan_tmp, &tot);
+      for (int q = q0; q < q1; q++) {
+        const uint32_t v = cnt[q];
+        cnt[q] = (uint16_t)ex;
+        ex += v;
+      }
+    }
+    __syncthreads();
+    for (int r0 = 0; r0 < R; r0 += 4) {
+      uint32_t wv[4];
+      uint16_t iv[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int i = (r0 + u) * nt + tid;
+        const bool ok = r0 + u < R && i < k;
+        wv[u] = ok ? sw[i] : 0u;
+        iv[u] = ok ? si[i] : (uint16_t)0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int r = r0 + u;
+        if (r >= R) break;  // uniform
+        const bool valid = r * nt + tid < k;
+        const uint32_t d = valid ? (sh < 32 ? (wv[u] >> sh) & 15u : 0u) : 16u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        if (valid) {
+          const uint32_t pos = (uint32_t)cnt[d * RW + r * 32 + warp] + __popc(peers & lanemask_lt());
+          dw[pos] = wv[u];
+          di[pos] = iv[u];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Two-queue Huffman (_kernels.py:213-232) over ascending leaf weights
 // Lw[0..k), run by the whole CTA in batched rounds.  The reference picks,
 // 2 (k - 1) times, the smaller head of the leaf queue and of the FIFO queue of
@@ -359,10 +440,9 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
     // ---- B. sort leaves by (count, rank) = the reference's stable argsort by
     // count.  Measured (C3, cycles): bitonic on (count << 16 | rank) keys 16 K
     // at N = 512, 146 K at N = 8192; the stable radix sort 55 K and 102 K.
-    // Radix for the large shared-memory cases, bitonic otherwise (also for the
-    // global-scratch case, where the radix sort's per-thread runs serialise
-    // on L2 latency).
-    if (small && N >= 8192) {
+    // Radix for N >= 8192 (per-thread runs in shared memory; the striped
+    // variant for the global-scratch case), bitonic below.
+    if (N >= 8192) {
       if (tid == 0) s_wmax = 0;
       __syncthreads();
       uint32_t mx = 0;
@@ -374,6 +454,10 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
       }
       atomicMax(&s_wmax, mx);
       __syncthreads();
+      if (!small)
+        radix_sort_leaves_striped(L, order, Iw, PL, k, 32 - __clz(s_wmax),
+                                  reinterpret_cast<uint16_t*>(smem), scan_u32);
+      else
       radix_sort_leaves(L, order, Iw, PL, k, 32 - __clz(s_wmax), scan_u64);
     } else {
       uint64_t* keys = reinterpret_cast<uint64_t*>(base);
@@ -410,18 +494,48 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
   __syncthreads();
   CB_T(3);  // depths
 
-  // ---- E. canonical codes (encode.py:123-152)
-  if (tid < 64) s_cbl[tid] = 0;
+  // ---- E. canonical codes (encode.py:123-152): a symbol's code is
+  // first_code[len] + its rank among the symbols of that length, ascending
+  // symbol.  Warp w owns the symbols [w B, (w + 1) B), 32 consecutive ones per
+  // round; MATCH.ANY groups the lanes of equal length, so a round costs one
+  // counter update per distinct length.  Pass 1 counts per (warp, length), 64
+  // threads scan the warps, pass 2 replays the rounds with the running
+  // counters as ranks.
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(smem + 131072);  // [32 warps][64 lengths]
   if (tid == 0) {
     s_max = 0;
     s_min = 255;
   }
+  for (int i = tid; i < 32 * 64; i += kCBThreads) wcnt[i] = 0;
   __syncthreads();
-  for (int i = tid; i < k; i += kCBThreads) {
-    uint32_t l = s_len[i];
-    atomicAdd(&s_cbl[min(l, 63u)], 1u);
-    atomicMax(&s_max, l);
-    atomicMin(&s_min, l);
+  const int RB = (k + kCBThreads - 1) / kCBThreads;  // rounds per warp
+  const int wbase = warp * RB * 32;
+  {
+    uint32_t lmax = 0, lmin = 255;
+    for (int r = 0; r < RB; r++) {
+      const int i = wbase + r * 32 + lane;
+      const bool valid = i < k;
+      const uint32_t l = valid ? (uint32_t)s_len[i] : 0x100u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, l);
+      if (valid) {
+        lmax = max(lmax, l);
+        lmin = min(lmin, l);
+        if ((peers & lanemask_lt()) == 0) wcnt[warp * 64 + min(l, 63u)] += __popc(peers);
+      }
+      __syncwarp();
+    }
+    atomicMax(&s_max, lmax);
+    atomicMin(&s_min, lmin);
+  }
+  __syncthreads();
+  if (tid < 64) {  // exclusive prefix over the warps, per length
+    uint32_t run = 0;
+    for (int w = 0; w < 32; w++) {
+      const uint32_t c = wcnt[w * 64 + tid];
+      wcnt[w * 64 + tid] = run;
+      run += c;
+    }
+    s_cbl[tid] = run;
   }
   __syncthreads();
   const int max_len = (int)s_max;
@@ -439,30 +553,27 @@ __global__ void __launch_bounds__(kCBThreads) codebook_kernel(CBArgs a) {
     fm.max_len = s_max;
   }
   __syncthreads();
-  // rank within length class, ascending symbol: per present length, a block scan
-  const int RK = (k + kCBThreads - 1) / kCBThreads;
-  for (int l = 1; l <= max_len; l++) {
-    if (s_cbl[l] == 0) continue;  // uniform
-    uint32_t c = 0;
-    for (int r = 0; r < RK; r++) {
-      int i = tid * RK + r;
-      if (i < k && s_len[i] == l) c++;
-    }
-    uint32_t tot;
-    uint32_t ex = block_excl_scan<uint32_t>(c, scan_u32, &tot);
-    for (int r = 0; r < RK; r++) {
-      int i = tid * RK + r;
-      if (i < k && s_len[i] == l) {
-        lut[sym[i]] = ((uint64_t)l << 57) | (s_fc[l] + ex);
-        if (a.tlen8) a.tlen8[field * a.nbins + sym[i]] = (uint8_t)l;
-        if (a.twin) {
-          const uint32_t wi = sym[i] - (uint32_t)(a.nbins / 2 + 1 - kEncWin / 2);
-          if (wi < (uint32_t)kEncWin)
-            // MSB-aligned code word | length (l <= 26 leaves the low 6 bits free)
-            a.twin[field * kEncWin + wi] =
-                l <= 26 ? ((uint32_t)(s_fc[l] + ex) << (32 - l)) | (uint32_t)l : 0u;
-        }
-        ex++;
+  for (int r = 0; r < RB; r++) {
+    const int i = wbase + r * 32 + lane;
+    const bool valid = i < k;
+    const uint32_t l = valid ? (uint32_t)s_len[i] : 0x100u;
+    const uint32_t peers = __match_any_sync(0xffffffffu, l);
+    const uint32_t lt = peers & lanemask_lt();
+    uint32_t rank = 0;
+    if (valid) rank = wcnt[warp * 64 + l] + __popc(lt);
+    __syncwarp();
+    if (valid && lt == 0) wcnt[warp * 64 + l] += __popc(peers);
+    __syncwarp();
+    if (valid) {
+      const uint32_t sy = sym[i];
+      const uint64_t word = s_fc[l] + rank;
+      lut[sy] = ((uint64_t)l << 57) | word;
+      if (a.tlen8) a.tlen8[field * a.nbins + sy] = (uint8_t)l;
+      if (a.twin) {
+        const uint32_t wi = sy - (uint32_t)(a.nbins / 2 + 1 - kEncWin / 2);
+        if (wi < (uint32_t)kEncWin)
+          // MSB-aligned code word | length (l <= 26 leaves the low 6 bits free)
+          a.twin[field * kEncWin + wi] = l <= 26 ? ((uint32_t)word << (32 - l)) | (uint32_t)l : 0u;
       }
     }
   }

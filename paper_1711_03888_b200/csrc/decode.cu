@@ -53,6 +53,10 @@ constexpr int kTpcTab = (1 << kTpcBits) + kTpc2Cap;
 constexpr double kCanonMass = 0.99;   // fused-table coverage below which the canonical mode decodes
 constexpr int kCanonMaxK = 65536;     // its symbol table: u16 by canonical rank, <= 128 KiB
 constexpr int kCanonBits = 11;        // first-length table index bits
+#ifndef NBZG_CANON_COST
+#define NBZG_CANON_COST 1.5
+#endif
+constexpr double kCanonCost = NBZG_CANON_COST, kCanonCostBits = 12.5;  // host-side CTA split
 
 struct DParsed {
   uint64_t n_esc, k, total_bits;
@@ -1896,6 +1900,9 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
       for (int f = 0; f < nf; f++) {
         const double bits = a.n ? 8.0 * (double)fields[f].payload_len / (double)a.n : 0.0;
         w[f] = fields[f].kind == 3 ? 1.0 + bits / 26.0 : 0.0;
+        // (streams this dense usually decode in the canonical mode: two or
+        // three dependent lookups per symbol instead of one)
+        if (bits >= kCanonCostBits) w[f] *= kCanonCost;
         wsum += w[f];
         gmin[f] = fields[f].kind == 3 ? (int)((a.nchunks + kLvMaxThreads - 1) / kLvMaxThreads) : 1;
         gmin[f] = max(1, gmin[f]);

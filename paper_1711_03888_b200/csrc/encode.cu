@@ -921,6 +921,20 @@ __global__ void __launch_bounds__(kE3Threads, 2) encode_tpc_kernel(EArgs a, cons
 #pragma unroll
         for (int q = 0; q < 8; q++) put_msb(e[q] & ~63u, e[q] & 63u);
       } else {
+        // Long codes, codes outside the window, escapes.  The serial loop
+        // below reads one global LUT entry (and, for an escape, perm and the
+        // value) per miss; touch them all first so those dependent reads hit
+        // L1 instead of paying an L2 round trip each (large alphabets: most
+        // groups come here).
+        {
+          uint32_t sink = 0;
+#pragma unroll
+          for (int q = 0; q < 8; q++) {
+            if (e[q] == 0) sink ^= (uint32_t)__ldg(&T.lut[cv[q]]);
+            if (cv[q] == 0) sink ^= esc_value_bits(a, field, s0 + 8 * g + q);
+          }
+          asm volatile("" ::"r"(sink));
+        }
         // codes re-extracted from the packed group (no dynamically indexed array)
         const uint64_t lo = ((uint64_t)cu.y << 32) | cu.x, hi = ((uint64_t)cu.w << 32) | cu.z;
 #pragma unroll 1

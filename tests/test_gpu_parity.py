@@ -602,10 +602,14 @@ def test_config3_eb_sweep(O, eb, gen, decoder):
         assert abs(nbz.ratio(res.archive) / v1["ratio"] - 1) < 0.005, (mode, eb)
         rec = nbz.decompress(res.archive, device=True)
         work = fields if res.order is None else [f[res.order] for f in fields]
+        # (eb <= 1e-5: alphabets of 2^15-2^16 symbols -- the thread decoder's
+        # canonical mode and the codebook's large-alphabet path)
+        odec = O.decompress(ref["wire"])
         for fi in range(6):
             err = (torch.from_numpy(work[fi]).cuda().double() - rec.field(fi).double()).abs().max()
             lim = res.archive.bounds[fi] if not res.archive.is_constant(fi) else 0.0
             assert float(err) <= lim, (mode, eb, fi)
+            assert np.array_equal(rec.field(fi).cpu().numpy(), odec[fi]), (mode, eb, fi)
 
 
 @pytest.mark.parametrize("case", ["variants_hacc24", "variants_amdf20k"])
