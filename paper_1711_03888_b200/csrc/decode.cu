@@ -118,6 +118,7 @@ NBZG_DEV void parse_body(const DArgs& a, int fi) {
   __shared__ uint64_t s_fc[64];
   __shared__ uint32_t s_fi[64];
   __shared__ uint32_t s_lim16[kLutBits + 1];
+  __shared__ uint32_t s_wcnt[32 * 64];  // [warp][length] counters of the canonical ranking
   const int tid = threadIdx.x;
   const uint8_t* p = F.payload;
   const int64_t L = F.payload_len;
@@ -178,25 +179,47 @@ NBZG_DEV void parse_body(const DArgs& a, int fi) {
     if (tid == 0) P.status = NBZG_BAD_STREAM, fail(a.status, NBZG_BAD_STREAM);
     return;
   }
-  // canonical order: rank within length class, ascending symbol
-  const int RK = (int)((k + blockDim.x - 1) / blockDim.x);
-  for (int l = 1; l <= max_len; l++) {
-    if (s_cbl[l] == 0) continue;
-    uint32_t c = 0;
-    for (int r = 0; r < RK; r++) {
-      uint64_t i = (uint64_t)tid * RK + r;
-      if (i < k && p[8 + 5 * i + 4] == l) c++;
+  // canonical order: rank within length class, ascending symbol.  Warp w owns
+  // the table entries [w B, (w + 1) B), 32 consecutive ones per round;
+  // MATCH.ANY groups the lanes of equal length.  Pass 1 counts per (warp,
+  // length), 64 threads scan the warps, pass 2 replays the rounds with the
+  // running counters as ranks (same scheme as the encoder's codebook).
+  {
+    const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    for (int i = tid; i < 32 * 64; i += blockDim.x) s_wcnt[i] = 0;
+    __syncthreads();
+    const uint64_t RB = (k + blockDim.x - 1) / blockDim.x;  // rounds per warp
+    const uint64_t wbase = (uint64_t)warp * RB * 32;
+    for (uint64_t r = 0; r < RB; r++) {
+      const uint64_t i = wbase + r * 32 + lane;
+      const bool valid = i < k;
+      const uint32_t l = valid ? (uint32_t)p[8 + 5 * i + 4] : 0x100u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, l);
+      if (valid && (peers & lanemask_lt()) == 0) s_wcnt[warp * 64 + l] += __popc(peers);
+      __syncwarp();
     }
-    uint32_t tot;
-    uint32_t ex = block_excl_scan<uint32_t>(c, scan_tmp, &tot);
-    for (int r = 0; r < RK; r++) {
-      uint64_t i = (uint64_t)tid * RK + r;
-      if (i < k && p[8 + 5 * i + 4] == l) {
-        uint32_t sym = ld_u32_bytes(p + 8 + 5 * i);
-        uint32_t pos = s_fi[l] + ex;
-        ss[pos] = sym;
-        ex++;
+    __syncthreads();
+    if (tid < 64) {
+      uint32_t run = 0;
+      for (int w = 0; w < nw; w++) {
+        const uint32_t c = s_wcnt[w * 64 + tid];
+        s_wcnt[w * 64 + tid] = run;
+        run += c;
       }
+    }
+    __syncthreads();
+    for (uint64_t r = 0; r < RB; r++) {
+      const uint64_t i = wbase + r * 32 + lane;
+      const bool valid = i < k;
+      const uint32_t l = valid ? (uint32_t)p[8 + 5 * i + 4] : 0x100u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, l);
+      const uint32_t lt = peers & lanemask_lt();
+      uint32_t rank = 0;
+      if (valid) rank = s_wcnt[warp * 64 + l] + __popc(lt);
+      __syncwarp();
+      if (valid && lt == 0) s_wcnt[warp * 64 + l] += __popc(peers);
+      __syncwarp();
+      if (valid) ss[s_fi[l] + rank] = ld_u32_bytes(p + 8 + 5 * i);
     }
   }
   // length table: entry e (16-bit prefix) -> smallest l with e.. < limit[l]
