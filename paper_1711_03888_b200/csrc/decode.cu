@@ -50,7 +50,10 @@ constexpr int kRingStride = 1024;  // words between ring slots (power of two, >=
 // decode_lv_kernel's ring: slot stride = its thread cap
 constexpr int kLvStride = NBZG_LV_RING == 16 ? 768 : kRingStride;
 constexpr int kTpcTab = (1 << kTpcBits) + kTpc2Cap;
-constexpr double kCanonMass = 0.99;   // fused-table coverage below which the canonical mode decodes
+#ifndef NBZG_CANON_MASS
+#define NBZG_CANON_MASS 0.996
+#endif
+constexpr double kCanonMass = NBZG_CANON_MASS;  // fused-table coverage below which the canonical mode decodes
 constexpr int kCanonMaxK = 65536;     // its symbol table: u16 by canonical rank, <= 128 KiB
 constexpr int kCanonBits = 11;        // first-length table index bits
 #ifndef NBZG_CANON_COST
@@ -296,13 +299,20 @@ NBZG_DEV void parse_body(const DArgs& a, int fi) {
       // Share of the symbols the fused tables resolve, estimated from the
       // code lengths (a Huffman code of length l has probability ~2^-l): the
       // codes of <= max(15, W) bits.  One unresolved symbol replays its whole
-      // 8-symbol group on the exact path for every lane of the warp, so below
-      // ~99% the canonical mode (symbols by rank in shared memory, two or
-      // three dependent lookups per symbol, no replays) is faster.
+      // 8-symbol group on the exact path for every lane of the warp.  The
+      // canonical mode (symbols by rank in shared memory, three or four
+      // dependent lookups per symbol, no replays) costs ~2.5x a clean fused
+      // decode; measured at 2^26 particles: coverage 0.9985 -> fused 2.5 ms,
+      // canonical 4.5 ms; 0.9971 -> equal (6.9 ms); 0.94 -> fused 13.1 ms,
+      // canonical 4.6 ms.
       const int lres = n2 ? max(W, kTpcBits) : kTpcBits;
       double mass = 0.0;
       for (int l = 1; l <= min(max_len, lres); l++) mass += ldexp((double)s_cbl[l], -l);
       P.use_canon = (mass < kCanonMass && k <= (uint64_t)kCanonMaxK && max_len <= 32) ? 1u : 0u;
+#ifdef NBZG_CANON_DEBUG
+      printf("parse field %d k %llu max_len %d W %d n2 %u resolved mass %.6f canon %u\n", fi,
+             (unsigned long long)k, max_len, W, n2, mass, P.use_canon);
+#endif
     }
   } else if (tid == 0) {
     P.use_canon = 0;

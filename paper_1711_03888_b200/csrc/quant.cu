@@ -23,6 +23,10 @@ namespace nbzg {
 
 constexpr int kQThreads = 1024;
 constexpr int kQPer = kTileMax / kQThreads;  // 16 positions per thread
+#ifndef NBZG_Q_FAR_BUDGET
+#define NBZG_Q_FAR_BUDGET 65536u
+#endif
+constexpr uint32_t kQFarBudget = NBZG_Q_FAR_BUDGET;  // far codes a CTA counts with global atomics
 constexpr int kQWin = 4096;                  // histogram window (bins)
 
 struct QArgs {
@@ -116,6 +120,8 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
   uint32_t* hw = reinterpret_cast<uint32_t*>(pbuf + 2 * kTileMax);    // [kQWin + 1]: window + escapes
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ int64_t s_carry2[2];
+  __shared__ uint32_t s_far;      // far codes this CTA sent to global atomics so far
+  __shared__ long long s_dstart;  // first deferred tile (te: none)
 
   const int field = a.f0 + (int)(blockIdx.x % a.nf);
   const int g = (int)(blockIdx.x / a.nf);
@@ -144,6 +150,15 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
   const double inv = fm.inv;
 
   for (int i = tid; i <= kQWin; i += kQThreads) hw[i] = 0;
+  // Codes outside the shared window go to global atomics -- fine while they
+  // are rare.  Once a CTA has sent kQFarBudget of them (large alphabets at
+  // tight bounds: L2 atomic throughput then bounds the kernel), the far codes
+  // of its remaining tiles are deferred: after its last tile the CTA counts
+  // them from the stored u16 codes in a 32768-bin shared histogram (the tile
+  // buffers are free by then), one half of the code range at a time.  The
+  // switch costs nothing per tile: the warp whose count crosses the budget
+  // publishes the next tile as the first deferred one.
+  if (tid == 0) s_far = 0, s_dstart = te;
   if (tid == 0) {
     // k carried into the range: k of the last sorted element of tile tb-1
     int64_t kc = 0;
@@ -278,7 +293,13 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
         // far codes go straight to global memory
         const uint32_t wb = code - (uint32_t)wlo;
         if (wb < (uint32_t)kQWin) red_shared_add1(hw_s + 4u * wb);
-        else atomicAdd(&hist[code], 1u);
+        else if (code == 0u) atomicAdd(&hist[0], 1u);
+        else if (t >= *(volatile long long*)&s_dstart) {
+          // deferred
+        } else {
+          atomicAdd(&hist[code], 1u);
+          if (atomicAdd(&s_far, 1u) + 1u == kQFarBudget) s_dstart = t + 1;
+        }
         cdst[32 * j] = (uint16_t)code;
       }
     };
@@ -362,11 +383,24 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
         for (int e = 0; e < 4; e++) wv[e] = code[e] - (uint32_t)wlo;
         const uint32_t wmax = max(max(wv[0], wv[1]), max(wv[2], wv[3]));
         if (__any_sync(0xffffffffu, wmax >= (uint32_t)kQWin)) {
+          // (s_dstart only ever moves to t + 1 during tile t: uniform for the tile)
+          const bool defer = t >= *(volatile long long*)&s_dstart;
+          uint32_t far = 0;
 #pragma unroll
           for (int e = 0; e < 4; e++) {
             if (code[e] == 0u) red_shared_add1(hwin + 4u * (uint32_t)kQWin);
             else if (wv[e] < (uint32_t)kQWin) red_shared_add1(hwin + 4u * wv[e]);
-            else atomicAdd(&hist[code[e]], 1u);
+            else {
+              far++;
+              if (!defer) atomicAdd(&hist[code[e]], 1u);
+            }
+          }
+          if (!defer) {
+            far = __reduce_add_sync(0xffffffffu, far);
+            if (lane == 0 && far) {
+              const uint32_t old = atomicAdd(&s_far, far);
+              if (old < kQFarBudget && old + far >= kQFarBudget) s_dstart = t + 1;
+            }
           }
         } else {
 #pragma unroll
@@ -390,6 +424,32 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
     uint32_t c = hw[i];
     int code = i == kQWin ? 0 : wlo + i;
     if (c && code >= 0 && code < (int)a.nbins) atomicAdd(&hist[code], c);
+  }
+  // ---- far codes of the deferred tiles [s_dstart, te)
+  __syncthreads();
+  const int64_t td = s_dstart;
+  if (td < te) {
+    uint32_t* h = reinterpret_cast<uint32_t*>(xbuf);  // [32768]
+    for (uint32_t hsel = 0; hsel < 2; hsel++) {
+      for (int i = tid; i < 32768; i += kQThreads) h[i] = 0;
+      __syncthreads();
+      for (int64_t t = td; t < te; t++) {
+        const int64_t t0 = t * a.tile;
+        const int m = (int)min(a.tile, a.n - t0);
+        for (int i = tid; i < m; i += kQThreads) {
+          const uint32_t c = codes[t0 + i];
+          if (c != 0u && c - (uint32_t)wlo >= (uint32_t)kQWin && (c >> 15) == hsel)
+            atomicAdd(&h[c & 32767u], 1u);
+        }
+      }
+      __syncthreads();
+      for (int i = tid; i < 32768; i += kQThreads) {
+        const uint32_t v = h[i];
+        const uint32_t code = (hsel << 15) | (uint32_t)i;
+        if (v && (int64_t)code < a.nbins) atomicAdd(&hist[code], v);
+      }
+      __syncthreads();
+    }
   }
 }
 
