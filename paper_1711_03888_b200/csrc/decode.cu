@@ -55,7 +55,7 @@ constexpr int kTpcTab = (1 << kTpcBits) + kTpc2Cap;
 #endif
 constexpr double kCanonMass = NBZG_CANON_MASS;  // fused-table coverage below which the canonical mode decodes
 constexpr int kCanonMaxK = 65536;     // its symbol table: u16 by canonical rank, <= 128 KiB
-constexpr int kCanonBits = 11;        // first-length table index bits
+constexpr int kCanonBits = 12;        // first-length table index bits (8-byte entries: 32 KiB)
 #ifndef NBZG_CANON_COST
 #define NBZG_CANON_COST 1.5
 #endif
@@ -1487,14 +1487,16 @@ NBZG_DEV void lv_chunks(const LvCtx& X, const DArgs& a, const uint64_t* choff, u
 // replayed on the exact path, whose symbol lookup is a global load.  This
 // mode keeps the canonical decode (encode.py:242-261) entirely in shared
 // memory instead: the symbols by canonical rank (u16, <= 128 KiB), the
-// left-aligned limits and rank bases per length, and a 2^11-entry table with
-// the first length possible for an 11-bit prefix.  A symbol is
-//   l = first[v >> 21];  while (v >= limit[l]) l++;          (0-2 steps)
-//   sym = syms[base[l] + (v >> (32 - l))]
-// i.e. three or four dependent shared-memory reads and no speculation.
+// left-aligned limits and rank bases per length, and a 2^12-entry table with
+// the first length possible for a 12-bit prefix (and its rank base).  A symbol is
+//   (l, base) = first[v >> 20];  unless the prefix holds one length only:
+//   while (v >= limit[l]) l++;  base = base_of[l];
+//   sym = syms[base + (v >> (32 - l))]
+// i.e. two dependent shared-memory reads for most symbols (a 12-bit prefix of
+// 14-18-bit codes rarely straddles two lengths) and no speculation.
 struct CanonCtx {
   const uint16_t* syms;
-  const uint8_t* first;
+  const uint2* first;     // [2^kCanonBits]: .x = rank base of length l, .y = l | unique << 8
   const uint64_t* limit;  // [l]: first window value past the codes of length <= l (<= 2^32)
   const int32_t* base;    // [l]: rank of the first code of length l minus its code value
   int max_len, bias;
@@ -1503,16 +1505,20 @@ struct CanonCtx {
 NBZG_DEV void canon_step(const LvCtx& X, const CanonCtx& C, LvChunk& S, float& o) {
   lv_fill_safe(X, S);
   const uint32_t v = S.R.hi;
-  int l = C.first[v >> (32 - kCanonBits)];
-  while (l <= C.max_len && (uint64_t)v >= C.limit[l]) l++;
-  if (l > C.max_len) {  // outside the code (incomplete table)
-    S.err = NBZG_INVALID_CODE;
-    l = 1;
-    bb_take(S.R, 1);
-    o = 0.0f;
-    return;
+  const uint2 e = C.first[v >> (32 - kCanonBits)];
+  int l = (int)(e.y & 0xffu);
+  int32_t bs = (int32_t)e.x;
+  if (!(e.y & 0x100u)) {  // the prefix spans several lengths: walk the limits
+    while (l <= C.max_len && (uint64_t)v >= C.limit[l]) l++;
+    if (l > C.max_len) {  // outside the code (incomplete table)
+      S.err = NBZG_INVALID_CODE;
+      bb_take(S.R, 1);
+      o = 0.0f;
+      return;
+    }
+    bs = C.base[l];
   }
-  const uint32_t sym = C.syms[C.base[l] + (int32_t)(v >> (32 - l))];
+  const uint32_t sym = C.syms[bs + (int32_t)(v >> (32 - l))];
   bb_take(S.R, (uint32_t)l);
   if (sym == 0) {  // escape: the raw f32 follows
     lv_fill_safe(X, S);
@@ -1570,12 +1576,25 @@ __global__ void __launch_bounds__(kLvMaxThreads, 1) decode_lv_kernel(DArgs a) {
   const int64_t ce = (a.nchunks * (gj + 1)) / gn;
   if (cb >= ce) return;
   const int tid = threadIdx.x, nthr = blockDim.x;
+#ifdef NBZG_LV_PROF  // timing experiment: cycles of the first CTA of every field
+  const long long lv_t0 = clock64();
+  struct LvProf {
+    long long t0;
+    int fi, gn, canon;
+    int64_t nch;
+    __device__ ~LvProf() {
+      __syncthreads();
+      if (threadIdx.x == 0 && t0) printf("decode_lv field %d canon %d ctas %d chunks/cta %lld cycles %lld\n", fi, canon, gn, (long long)nch, clock64() - t0);
+    }
+  } lv_prof{lv_t0, fi, gn, (int)P.use_canon, ce - cb};
+  if (gj != 0) lv_prof.t0 = 0;
+#endif
   uint32_t* ring = reinterpret_cast<uint32_t*>(dsm2 + 4 * kTpcTab) + tid;  // [kLvRing][kRingStride]
   if (P.use_canon) {
-    // shared layout: syms u16[k] | first u8[2^11] (both inside the fused
+    // shared layout: syms u16[k] | first uint2[2^12] (both inside the fused
     // table's 180 KiB), then the ring as in the fused mode
     uint16_t* c_syms = reinterpret_cast<uint16_t*>(dsm2);
-    uint8_t* c_first = dsm2 + 2 * (size_t)kCanonMaxK;
+    uint2* c_first = reinterpret_cast<uint2*>(dsm2 + 2 * (size_t)kCanonMaxK);
     const uint32_t* gs = a.ssyms + fi * a.nbins;
     for (uint32_t i = tid; i < (uint32_t)P.k; i += nthr) c_syms[i] = (uint16_t)__ldg(gs + i);
     if (tid < 64) {
@@ -1591,10 +1610,15 @@ __global__ void __launch_bounds__(kLvMaxThreads, 1) decode_lv_kernel(DArgs a) {
     }
     __syncthreads();
     for (uint32_t pfx = tid; pfx < (1u << kCanonBits); pfx += nthr) {
-      const uint64_t v = (uint64_t)pfx << (32 - kCanonBits);
-      int l = 1;
-      while (l <= (int)P.max_len && v >= s_limit[l]) l++;
-      c_first[pfx] = (uint8_t)min(l, 33);
+      // length of the first and of the last window value of the prefix
+      const uint64_t v0 = (uint64_t)pfx << (32 - kCanonBits);
+      const uint64_t v1 = v0 + ((1ull << (32 - kCanonBits)) - 1);
+      int l0 = 1;
+      while (l0 <= (int)P.max_len && v0 >= s_limit[l0]) l0++;
+      int l1 = l0;
+      while (l1 <= (int)P.max_len && v1 >= s_limit[l1]) l1++;
+      const bool unique = l0 == l1 && l0 <= (int)P.max_len;
+      c_first[pfx] = make_uint2((uint32_t)s_base[min(l0, 63)], (uint32_t)min(l0, 33) | (unique ? 0x100u : 0u));
     }
     __syncthreads();
     LvCtx X{};

@@ -16,6 +16,8 @@
 // Tiles (field values + the tile-local permutation) are staged into shared
 // memory with TMA bulk copies (cp.async.bulk + mbarrier), double buffered,
 // so the next tile streams in while the current one is gathered.
+#include <cstdlib>
+
 #include "nbzg_internal.cuh"
 #include "plan.h"
 
@@ -23,10 +25,7 @@ namespace nbzg {
 
 constexpr int kQThreads = 1024;
 constexpr int kQPer = kTileMax / kQThreads;  // 16 positions per thread
-#ifndef NBZG_Q_FAR_BUDGET
-#define NBZG_Q_FAR_BUDGET 65536u
-#endif
-constexpr uint32_t kQFarBudget = NBZG_Q_FAR_BUDGET;  // far codes a CTA counts with global atomics
+constexpr uint32_t kQFarBudget = 65536u;  // far codes a CTA counts with global atomics (NBZG_Q_FAR_BUDGET overrides: tests)
 constexpr int kQWin = 4096;                  // histogram window (bins)
 
 struct QArgs {
@@ -42,6 +41,7 @@ struct QArgs {
   int groups;
   int use_tma;
   int f0, nf;  // field group: fields f0 .. f0+nf-1
+  uint32_t far_budget;  // far codes a CTA counts with global atomics before deferring
 };
 
 NBZG_DEV uint32_t smem_u32(const void* p) {
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
 
   for (int i = tid; i <= kQWin; i += kQThreads) hw[i] = 0;
   // Codes outside the shared window go to global atomics -- fine while they
-  // are rare.  Once a CTA has sent kQFarBudget of them (large alphabets at
+  // are rare.  Once a CTA has sent far_budget (kQFarBudget) of them (large alphabets at
   // tight bounds: L2 atomic throughput then bounds the kernel), the far codes
   // of its remaining tiles are deferred: after its last tile the CTA counts
   // them from the stored u16 codes in a 32768-bin shared histogram (the tile
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
           // deferred
         } else {
           atomicAdd(&hist[code], 1u);
-          if (atomicAdd(&s_far, 1u) + 1u == kQFarBudget) s_dstart = t + 1;
+          if (atomicAdd(&s_far, 1u) + 1u == a.far_budget) s_dstart = t + 1;
         }
         cdst[32 * j] = (uint16_t)code;
       }
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
             far = __reduce_add_sync(0xffffffffu, far);
             if (lane == 0 && far) {
               const uint32_t old = atomicAdd(&s_far, far);
-              if (old < kQFarBudget && old + far >= kQFarBudget) s_dstart = t + 1;
+              if (old < a.far_budget && old + far >= a.far_budget) s_dstart = t + 1;
             }
           }
         } else {
@@ -541,6 +541,8 @@ int launch_quantize(const Plan& p, cudaStream_t st, int f0, int nf) {
   a.groups = per_field;
   a.f0 = f0;
   a.nf = nf;
+  a.far_budget = kQFarBudget;
+  if (const char* e = getenv("NBZG_Q_FAR_BUDGET")) a.far_budget = (uint32_t)max(1L, atol(e));
   bool aligned = true;
   for (int f = 0; f < 6; f++) aligned &= (reinterpret_cast<uintptr_t>(p.f[f]) & 15) == 0;
   a.use_tma = aligned && (p.tile % 8 == 0);

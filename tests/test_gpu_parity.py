@@ -372,6 +372,21 @@ def test_escape_heavy_and_tight_bounds(O, rng, decoder, encoder):
                 assert float(err.max()) <= res.archive.bounds[fi]
 
 
+def test_deferred_far_code_histogram(O, rng, monkeypatch):
+    """Large alphabets: once a quantise CTA has spent its budget of global
+    histogram atomics, the far codes of its remaining tiles are counted from
+    the stored codes in shared memory (quant.cu).  A budget of 64 makes every
+    CTA with more than one tile switch: archives still byte-identical."""
+    monkeypatch.setenv("NBZG_Q_FAR_BUDGET", "64")
+    n = 6_000_000  # 367 tiles per field over <= 49 CTAs: several tiles per CTA
+    fields = [(rng.standard_normal(n) * (10.0 ** (f % 3))).astype(np.float32) for f in range(6)]
+    snap = nbz.ParticleSnapshot(*fields)
+    for mode in ("sz-lv", "sz-lv-prx"):
+        res = nbz.compress(snap, mode, nbz.ErrorBoundSpec.relative(2e-6))
+        ref = O.compress(fields, mode, "rel", 2e-6, fmt=2)
+        assert res.archive.serialized() == ref["wire"], mode
+
+
 def test_bound_too_small_raises():
     x = np.array([1e30, -1e30, 5.0, 7.0], np.float32)
     snap = nbz.ParticleSnapshot(x, x, x, x, x, x)
