@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ int64_t s_carry2[2];
   __shared__ uint32_t s_far;      // far codes this CTA sent to global atomics so far
+  __shared__ uint32_t s_budget;   // next count at which the far-code rate is examined
   __shared__ long long s_dstart;  // first deferred tile (te: none)
 
   const int field = a.f0 + (int)(blockIdx.x % a.nf);
@@ -151,14 +152,15 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
 
   for (int i = tid; i <= kQWin; i += kQThreads) hw[i] = 0;
   // Codes outside the shared window go to global atomics -- fine while they
-  // are rare.  Once a CTA has sent far_budget (kQFarBudget) of them (large alphabets at
-  // tight bounds: L2 atomic throughput then bounds the kernel), the far codes
-  // of its remaining tiles are deferred: after its last tile the CTA counts
+  // are rare.  Once a CTA has sent far_budget (kQFarBudget) of them at a rate of
+  // at least one code in 16 (large alphabets at tight bounds: L2 atomic
+  // throughput then bounds the kernel), the far codes of its remaining tiles
+  // are deferred: after its last tile the CTA counts
   // them from the stored u16 codes in a 32768-bin shared histogram (the tile
   // buffers are free by then), one half of the code range at a time.  The
   // switch costs nothing per tile: the warp whose count crosses the budget
   // publishes the next tile as the first deferred one.
-  if (tid == 0) s_far = 0, s_dstart = te;
+  if (tid == 0) s_far = 0, s_budget = a.far_budget, s_dstart = te;
   if (tid == 0) {
     // k carried into the range: k of the last sorted element of tile tb-1
     int64_t kc = 0;
@@ -298,7 +300,11 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
           // deferred
         } else {
           atomicAdd(&hist[code], 1u);
-          if (atomicAdd(&s_far, 1u) + 1u == a.far_budget) s_dstart = t + 1;
+          const uint32_t bud = *(volatile uint32_t*)&s_budget;
+          if (atomicAdd(&s_far, 1u) + 1u == bud) {
+            if ((uint64_t)(t - tb + 1) * (uint64_t)(a.tile >> 4) <= (uint64_t)bud) s_dstart = t + 1;
+            else s_budget = bud < 0x80000000u ? 2u * bud : 0xffffffffu;
+          }
         }
         cdst[32 * j] = (uint16_t)code;
       }
@@ -383,23 +389,30 @@ __global__ void __launch_bounds__(kQThreads, 1) quantize_kernel(QArgs a) {
         for (int e = 0; e < 4; e++) wv[e] = code[e] - (uint32_t)wlo;
         const uint32_t wmax = max(max(wv[0], wv[1]), max(wv[2], wv[3]));
         if (__any_sync(0xffffffffu, wmax >= (uint32_t)kQWin)) {
-          // (s_dstart only ever moves to t + 1 during tile t: uniform for the tile)
-          const bool defer = t >= *(volatile long long*)&s_dstart;
           uint32_t far = 0;
 #pragma unroll
           for (int e = 0; e < 4; e++) {
             if (code[e] == 0u) red_shared_add1(hwin + 4u * (uint32_t)kQWin);
             else if (wv[e] < (uint32_t)kQWin) red_shared_add1(hwin + 4u * wv[e]);
-            else {
-              far++;
-              if (!defer) atomicAdd(&hist[code[e]], 1u);
-            }
+            else far |= 1u << e;
           }
-          if (!defer) {
-            far = __reduce_add_sync(0xffffffffu, far);
-            if (lane == 0 && far) {
-              const uint32_t old = atomicAdd(&s_far, far);
-              if (old < a.far_budget && old + far >= a.far_budget) s_dstart = t + 1;
+          if (far) {  // only the lanes that hold far codes pay for the bookkeeping
+            // (s_dstart only ever moves to t + 1 during tile t: uniform for the tile)
+            if (t < *(volatile long long*)&s_dstart) {
+#pragma unroll
+              for (int e = 0; e < 4; e++)
+                if (far & (1u << e)) atomicAdd(&hist[code[e]], 1u);
+              const uint32_t nf = (uint32_t)__popc(far);
+              const uint32_t old = atomicAdd(&s_far, nf);
+              const uint32_t bud = *(volatile uint32_t*)&s_budget;
+              if (old < bud && old + nf >= bud) {
+                // the budget is spent: defer from the next tile on if at least
+                // 1/16 of the codes so far were far, else examine again at
+                // twice the count (a few percent of far codes are cheaper as
+                // global atomics than as a second pass over the codes)
+                if ((uint64_t)(t - tb + 1) * (uint64_t)(a.tile >> 4) <= (uint64_t)bud) s_dstart = t + 1;
+                else s_budget = bud < 0x80000000u ? 2u * bud : 0xffffffffu;
+              }
             }
           }
         } else {
