@@ -309,7 +309,11 @@ int nbzg_huff_encode(const uint16_t *syms, int64_t n, const uint64_t *lut, uint8
                      uint32_t *chunk_bits, void *workspace, size_t workspace_bytes,
                      void *stream);
 
-/* CRC-64/XZ (_kernels.py:954-994) of a device buffer; result to *crc_dev. */
+/* CRC-64/XZ (_kernels.py:954-994) of a device buffer; result to *crc_dev.
+ * `data` may have any alignment; the kernel reads whole 16-byte aligned
+ * granules, so when `data` is not 16-byte aligned it also touches the (up to
+ * 15) bytes before it inside the same granule -- always inside the same device
+ * allocation (cudaMalloc aligns to 256 bytes), and masked out of the CRC. */
 int nbzg_crc64(const uint8_t *data, int64_t n, uint64_t *crc_dev, void *workspace,
                size_t workspace_bytes, void *stream);
 size_t nbzg_crc64_workspace_size(int64_t n);
