@@ -43,13 +43,17 @@ constexpr int kTpcBits = 15;       // thread-per-chunk fused table index bits (i
 // long-code table)
 constexpr int kLvRing = NBZG_LV_RING;
 constexpr int kLvRingMask = kLvRing - 1;
-constexpr int kTpc2Cap = kLvRing == 16 ? 12288 : 16384;  // secondary (long-code) table entries
+// secondary (long-code) table entries that always fit beside a full primary
+// table (12800: with the 48 KiB ring and 768 B of static shared memory the
+// CTA sits 256 bytes under the 227 KiB limit)
+constexpr int kTpc2Cap = kLvRing == 16 ? 12800 : 16384;
 constexpr int kTpcMaxThreads = 704;
 constexpr int kLvMaxThreads = 768;  // decode_lv_kernel: 80 registers x 768 fit the register file
 constexpr int kRingStride = 1024;  // words between ring slots (power of two, >= threads)
 // decode_lv_kernel's ring: slot stride = its thread cap
 constexpr int kLvStride = NBZG_LV_RING == 16 ? 768 : kRingStride;
 constexpr int kTpcTab = (1 << kTpcBits) + kTpc2Cap;
+constexpr int kLut2Stride = 2 << kTpcBits;  // global fused table per field: primary | long entries
 #ifndef NBZG_CANON_MASS
 #define NBZG_CANON_MASS 0.996
 #endif
@@ -260,7 +264,7 @@ NBZG_DEV void parse_body(const DArgs& a, int fi) {
   // canonical tail (32-bit window value >= R0, i.e. codes > 15 bits) at W-bit
   // resolution, W <= 24 chosen so the tail fits kTpc2Cap entries.
   if ((F.kind & 15) == 3) {
-    int32_t* lut2 = a.lut2 + (size_t)fi * kTpcTab;
+    int32_t* lut2 = a.lut2 + (size_t)fi * kLut2Stride;
     const int bias = a.half + 1;
     auto entry = [&](int l, uint64_t u) -> int32_t {  // u: 32-bit window value
       const uint32_t idx = s_fi[l] + (uint32_t)((u >> (32 - l)) - s_fc[l]);
@@ -278,7 +282,13 @@ NBZG_DEV void parse_body(const DArgs& a, int fi) {
       R0 = (s_fc[kTpcBits] + s_cbl[kTpcBits]) << (32 - kTpcBits);
       for (int w = min(max_len, 24); w > kTpcBits; w--) {
         const uint64_t cnt = ((1ull << 32) - R0 + (1ull << (32 - w)) - 1) >> (32 - w);
-        if (cnt <= (uint64_t)kTpc2Cap) {
+        // decode_lv_kernel stores only the primary entries below R0, so what
+        // the long codes take from the primary table is theirs again
+        // (decode_tpc_kernel, sz-lcf, keeps the full primary table)
+        const uint64_t room = F.kind == 3
+                                  ? min((uint64_t)kTpcTab - (R0 >> (32 - kTpcBits)), (uint64_t)1 << kTpcBits)
+                                  : (uint64_t)kTpc2Cap;
+        if (cnt <= room) {
           W = w;
           n2 = (uint32_t)cnt;
           break;
@@ -962,7 +972,7 @@ __global__ void __launch_bounds__(kTpcMaxThreads, 1) decode_tpc_kernel(DArgs a, 
   const uint32_t* ss = a.ssyms + fi * a.nbins;
   const uint32_t n2 = P.t2_n;
   {
-    const int32_t* gl = a.lut2 + (size_t)fi * kTpcTab;
+    const int32_t* gl = a.lut2 + (size_t)fi * kLut2Stride;
     const uint32_t nv = ((1u << kTpcBits) + n2 + 3) / 4;
     for (uint32_t i = tid; i < nv; i += nthr)
       reinterpret_cast<uint4*>(LT)[i] = __ldg(reinterpret_cast<const uint4*>(gl) + i);
@@ -1643,7 +1653,7 @@ __global__ void __launch_bounds__(kLvMaxThreads, 1) decode_lv_kernel(DArgs a) {
   const bool has_long = P.t2_r0 < ((uint64_t)1 << 32);
   const uint32_t P15 = has_long ? (uint32_t)(P.t2_r0 >> (32 - kTpcBits)) : (1u << kTpcBits);
   {
-    const int32_t* gl = a.lut2 + (size_t)fi * kTpcTab;
+    const int32_t* gl = a.lut2 + (size_t)fi * kLut2Stride;
     for (uint32_t i = tid; i < P15; i += nthr) LT[i] = __ldg(gl + i);
     for (uint32_t i = tid; i < n2; i += nthr) LT[P15 + i] = __ldg(gl + (1 << kTpcBits) + i);
     if (tid < 2 && has_long && n2 == 0) LT[P15 + tid] = 64;  // (v - r0) >> 31 is 0 or 1
@@ -1877,7 +1887,7 @@ size_t decompress_ws(int nf, int64_t n, int64_t nbins) {
   auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
   s += al(sizeof(DParsed) * nf);
   s += al((size_t)nf * (1 << kLutBits));
-  s += al((size_t)nf * 4 * kTpcTab);
+  s += al((size_t)nf * 4 * kLut2Stride);
   s += al(sizeof(uint32_t) * nf * nbins);
   s += al(sizeof(uint64_t) * nf * (nchunks + 1));
   s += al(sizeof(uint64_t) * nf * 2 * (nchunks + 1));
@@ -1905,7 +1915,7 @@ int launch_decompress(const DField* fields, int nf, int64_t n, int64_t interval_
   a.lut = reinterpret_cast<uint32_t*>(p);
   p += al((size_t)nf * (1 << kLutBits));
   a.lut2 = reinterpret_cast<int32_t*>(p);
-  p += al((size_t)nf * 4 * kTpcTab);
+  p += al((size_t)nf * 4 * kLut2Stride);
   a.ssyms = reinterpret_cast<uint32_t*>(p);
   p += al(sizeof(uint32_t) * nf * nbins);
   a.choff = reinterpret_cast<uint64_t*>(p);
