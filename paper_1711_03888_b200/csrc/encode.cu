@@ -758,19 +758,43 @@ __global__ void __launch_bounds__(1024) chunk_scan_kernel(EArgs a, const uint32_
   uint64_t* off = coff + (size_t)field * (a.nchunks + 1);
   uint8_t* idx = a.arena + m.payload_off + m.index_off;
   const int64_t R = (a.nchunks + blockDim.x - 1) / blockDim.x;
+  constexpr int kReg = 16;  // chunk totals per thread held in registers (one pass over ctot)
+  uint32_t v[kReg];
   unsigned long long s = 0;
-  for (int64_t r = 0; r < R; r++) {
-    const int64_t c = (int64_t)threadIdx.x * R + r;
-    if (c < a.nchunks) s += ct[c];
+  if (R <= kReg) {
+#pragma unroll
+    for (int r = 0; r < kReg; r++) {
+      const int64_t c = (int64_t)threadIdx.x * R + r;
+      v[r] = (r < R && c < a.nchunks) ? ct[c] : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < kReg; r++) s += v[r];
+  } else {
+    for (int64_t r = 0; r < R; r++) {
+      const int64_t c = (int64_t)threadIdx.x * R + r;
+      if (c < a.nchunks) s += ct[c];
+    }
   }
   unsigned long long tot;
   unsigned long long ex = block_excl_scan<unsigned long long>(s, scan_tmp, &tot);
-  for (int64_t r = 0; r < R; r++) {
-    const int64_t c = (int64_t)threadIdx.x * R + r;
-    if (c < a.nchunks) {
-      off[c] = ex;
-      put_u32_bytes(idx + 4 * c, ct[c]);
-      ex += ct[c];
+  if (R <= kReg) {
+#pragma unroll
+    for (int r = 0; r < kReg; r++) {
+      const int64_t c = (int64_t)threadIdx.x * R + r;
+      if (r < R && c < a.nchunks) {
+        off[c] = ex;
+        put_u32_bytes(idx + 4 * c, v[r]);
+      }
+      ex += v[r];
+    }
+  } else {
+    for (int64_t r = 0; r < R; r++) {
+      const int64_t c = (int64_t)threadIdx.x * R + r;
+      if (c < a.nchunks) {
+        off[c] = ex;
+        put_u32_bytes(idx + 4 * c, ct[c]);
+        ex += ct[c];
+      }
     }
   }
   if (threadIdx.x == 0) {
