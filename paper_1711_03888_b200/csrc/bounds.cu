@@ -91,7 +91,19 @@ int launch_minmax6(const float* const* f, int64_t n, uint32_t* mm, cudaStream_t 
 // Sorted mode: the same exact min/max of all six fields, one CTA per
 // R-index segment at a time, also writing the segment's min/max of the
 // three key fields (fields kf0..kf0+2) for K2's per-segment bits/minima.
-__global__ void __launch_bounds__(512) minmax_seg_kernel(Fields6 F, int64_t n, int64_t S,
+// One CTA per SM with the whole register file (125 registers: 24 float4 loads
+// = 384 bytes in flight per thread) streams at 7.2 TB/s; with the default
+// register allocation (97: 12 loads in flight) the kernel ran at 5.7 TB/s, and
+// two CTAs of 64 registers per SM are no faster (measured 0.875 / 0.875 /
+// 0.92 ms for 1 CTA, 2 CTAs, 2 CTAs without unrolling; 1.10 ms before).
+#ifndef NBZG_MM_CTAS
+#define NBZG_MM_CTAS 1
+#endif
+#ifndef NBZG_MM_UNROLL
+#define NBZG_MM_UNROLL 2
+#endif
+constexpr int kMmUnroll = NBZG_MM_UNROLL;
+__global__ void __launch_bounds__(512, NBZG_MM_CTAS) minmax_seg_kernel(Fields6 F, int64_t n, int64_t S,
                                                          int64_t nseg, int kf0, uint32_t* mm,
                                                          float* seg_mm) {
   float lo[6], hi[6];
@@ -112,7 +124,7 @@ __global__ void __launch_bounds__(512) minmax_seg_kernel(Fields6 F, int64_t n, i
       sl[f] = __int_as_float(0x7f800000);
       sh[f] = -__int_as_float(0x7f800000);
     }
-#pragma unroll 2
+#pragma unroll kMmUnroll
     for (int v = threadIdx.x; v < m4; v += blockDim.x) {
 #pragma unroll
       for (int f = 0; f < 6; f++) {
